@@ -1,0 +1,245 @@
+/*
+ * tps.h — C ABI of the B200-native TiMePReSt pipeline-parallel training step
+ *          (V-TiMePReSt and I-TiMePReSt, arXiv 2509.23241).
+ *
+ * One handle = one pipeline stage = one consecutive set of layers on one GPU
+ * ("the layers of a DNN are divided into sets of consecutive
+ * layers without overlapping, and these sets are distributed over the
+ * accelerators").  Each mini-batch is split into m micro-batches whose forwards
+ * run first, followed by ONE collective backward for the whole mini-batch
+ * and a weight update.  V-TiMePReSt runs every pass on the
+ * stage's latest weights; I-TiMePReSt runs the backward on the
+ * intermediate weight W_i(x,y) = (2 - 1/f(δ))·W_i(x|y), f(δ) = e^{-λδ}
+ * (Eq. 1, Eq. 2), generalised here to
+ * W_res = α·W_stash + β·W_latest (reading Z1).
+ *
+ * Conventions (every entry point):
+ *   - returns tps_status; TPS_OK = 0.  On error, tps_last_error() returns a
+ *     thread-local message; no C++ exception crosses this boundary.
+ *   - "device" pointers are CUDA device addresses on the handle's device;
+ *     "host" pointers are CPU memory (pinned memory is faster but optional).
+ *   - all tensors are row-major.  Feature dimensions are stored padded to a
+ *     multiple of 16 elements ("ld" = pad16(d)); padding columns are zero.
+ *   - enqueue calls are asynchronous w.r.t. the host (stream-ordered on the
+ *     handle's compute stream).  Caller-owned inputs must stay valid until the
+ *     next tps_synchronize().  Device-side failures are latched and reported by
+ *     tps_synchronize() (TPS_E_CUDA / TPS_E_NCCL).
+ *   - one host thread drives a handle; handles are not re-entrant.
+ *   - the handle owns every device allocation it makes (cudaMalloc) and frees
+ *     them in tps_pipeline_destroy().
+ *   - there is no CPU fallback: without an sm_100 device every compute call
+ *     returns TPS_E_ARCH.
+ */
+#ifndef TPS_H
+#define TPS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TPS_ABI_VERSION 1
+
+typedef enum {
+  TPS_OK = 0,
+  TPS_E_INVALID_ARG = 1,  /* null pointer, negative size, out-of-range index       */
+  TPS_E_CONFIG = 2,       /* S<1, m<1, b<1, λ<=0 for I, bad partition, bad dims      */
+  TPS_E_ORDER = 3,        /* call is not the next event of the stage's static order */
+  TPS_E_STALENESS = 4,    /* explicit δ has no live stashed version                 */
+  TPS_E_CUDA = 5,         /* CUDA runtime/driver error (message has the CUDA text)  */
+  TPS_E_NCCL = 6,         /* NCCL error                                             */
+  TPS_E_OOM = 7,          /* device allocation failed                               */
+  TPS_E_ARCH = 8,         /* no sm_100 device                                       */
+  TPS_E_STATE = 9,        /* handle poisoned by an earlier device error             */
+  TPS_E_UNSUPPORTED = 10  /* valid request this build does not implement            */
+} tps_status;
+
+typedef enum { TPS_V = 0, TPS_I = 1 } tps_variant;
+
+/* Z1: EQ1 = the paper's closed form α = 2 - e^{λδ}, β = 0 (Eq. 1, Eq. 12);
+ *     CONVEX = the prose reading α = e^{-λδ}, β = 1 - α.               */
+typedef enum { TPS_BLEND_EQ1 = 0, TPS_BLEND_CONVEX = 1 } tps_blend;
+
+/* How a stage exchanges activations / activation-gradients with its neighbours
+ * (one-to-one transfers).  NONE: S = 1.  LOCAL: all stages are handles
+ * in one process on one GPU (device copies; used by tests and replicas).
+ * NCCL: one process per stage, ncclSend/ncclRecv over NVLink.                    */
+typedef enum { TPS_TRANSPORT_NONE = 0, TPS_TRANSPORT_LOCAL = 1, TPS_TRANSPORT_NCCL = 2 } tps_transport;
+
+typedef enum { TPS_EV_F = 0, TPS_EV_B = 1, TPS_EV_U = 2 } tps_event_kind;
+
+/* One schedule / trace record.  F: micro-batches [micro, micro+micro_count) of
+ * mini-batch mb, forward on version v_used (= the stage's latest).
+ * B: backward of mb; v_used = version whose weights are read (I: the stash the
+ * forward used; V: the latest), v_latest = latest version, delta = v_latest -
+ * v_forward for I (reading Z5) and 0 for V; alpha/beta =
+ * the fp32 blend coefficients applied.  U: update producing version v_latest.   */
+typedef struct {
+  int32_t stage, kind, micro, micro_count;
+  int64_t mb, v_used, v_latest;
+  int32_t delta;
+  float alpha, beta;
+} tps_event;
+
+/* Pipeline configuration (read once by tps_pipeline_init; arrays are copied).
+ * Network: num_layers Linear layers; layer l maps dims[l] -> dims[l+1]; every
+ * layer but the last is followed by ReLU; the last produces dims[L] logits for a
+ * softmax cross-entropy loss (mean over the B = m·b rows of a mini-batch, Z11).
+ * stage_bounds has num_stages+1 entries; stage s owns layers
+ * [stage_bounds[s], stage_bounds[s+1]) (consecutive, non-empty).        */
+typedef struct {
+  int32_t num_layers;
+  const int32_t* dims;          /* host, num_layers+1 entries, each >= 1            */
+  int32_t num_stages;           /* S >= 1                                            */
+  const int32_t* stage_bounds;  /* host, S+1 entries                                 */
+  int32_t stage_id;             /* 0 <= s < S                                        */
+  int32_t micro_batches;        /* m >= 1                                    */
+  int32_t micro_batch_size;     /* b >= 1                                            */
+  int32_t fwd_group;            /* micro-batches per forward launch/transfer; divides m;
+                                   0 => m (all micro-batch forwards "in parallel") */
+  int32_t variant;              /* tps_variant                                       */
+  int32_t blend;                /* tps_blend (I only)                                */
+  double lambda;                /* λ > 0, I only                             */
+  float lr, momentum, weight_decay;  /* SGD, PyTorch momentum convention (Z10)       */
+  int32_t transport;            /* tps_transport                                     */
+  const void* nccl_ids;         /* NCCL only: 2(S-1) ncclUniqueId (128 B each); id[2e] =
+                                   forward comm of edge e (stage e -> e+1), id[2e+1] =
+                                   backward comm of edge e (e+1 -> e)                 */
+  int32_t device;               /* CUDA device ordinal                               */
+  uint64_t seed;                /* synthetic-init seed (tps_init_weights_synthetic)  */
+  uint64_t compute_stream;      /* cudaStream_t to enqueue on; 0 => handle-owned     */
+  int32_t extra_recv_slot;      /* 1 => one extra input slot so the next forward's
+                                   receive overlaps the backward (costs B·d_in·2 B)   */
+  int32_t reserved[7];
+} tps_config;
+
+typedef struct tps_pipeline tps_pipeline;  /* opaque; one per stage */
+
+/* ---- lifecycle ------------------------------------------------------------ */
+int32_t tps_abi_version(void);
+const char* tps_last_error(void);
+/* 128-byte ncclUniqueId into out128 (host).  TPS_E_NCCL on failure. */
+tps_status tps_nccl_unique_id(void* out128);
+/* Validates cfg (TPS_E_CONFIG), checks the device is sm_100 (TPS_E_ARCH),
+ * allocates weights (fp32 master + momentum), the bf16 version ring (K_s = S - s
+ * slots for I, 1 for V), activation stash and exchange buffers,
+ * and (NCCL) joins the edge communicators.  Weights start at zero: call
+ * tps_init_weights_synthetic or tps_set_weights before training.            */
+tps_status tps_pipeline_init(const tps_config* cfg, tps_pipeline** out);
+tps_status tps_pipeline_destroy(tps_pipeline* p);
+/* LOCAL transport: connect the S handles of one process (stage order). */
+tps_status tps_local_link(tps_pipeline* const* stages, int32_t num_stages);
+
+/* ---- the training step (one mini-batch = B(j) U(j) + m forwards) ----------- */
+/* Declare a run of mini-batches [first_mb, first_mb+n_mb): builds the stage's
+ * static order (fill, steady state, drain; reading Z7) against which the
+ * following stage_forward/backward/update calls are checked.  A run must end
+ * (all its events issued) before the next begins; versions carry over.        */
+tps_status tps_begin_run(tps_pipeline* p, int64_t first_mb, int64_t n_mb);
+/* Forward of micro-batches [micro, micro+count) of mini-batch mb on the latest
+ * weights.  x: stage 0 only — [count·b, dims[0]] bf16, dense rows
+ * (ld = dims[0]); device or host pointer.  labels: last stage only —
+ * [count·b] int32, device or host.  Must be the stage's next static event
+ * (TPS_E_ORDER otherwise).                                                     */
+tps_status tps_stage_forward(tps_pipeline* p, int64_t mb, int32_t micro, int32_t count,
+                             const void* x, const int32_t* labels);
+/* Collective backward of mini-batch mb on the resolved weight:
+ * V: latest; I: α·W_stash(v_fwd) + β·W_latest with δ = v_latest - v_fwd.
+ * staleness = -1 => δ from the version log; >= 0 => must equal the logged δ in
+ * a scheduled run (TPS_E_STALENESS otherwise).                                */
+tps_status tps_stage_backward(tps_pipeline* p, int64_t mb, int32_t staleness);
+/* SGD/momentum update of every layer of the stage from the gradients of mb;
+ * writes the new bf16 version into a free ring slot (I) or in place (V); the
+ * stash of a version is released once its last consumer's backward ran. */
+tps_status tps_stage_update(tps_pipeline* p, int64_t mb);
+/* Walk the stage's static order for mini-batches [first_mb, first_mb+n_mb)
+ * (fill, steady state, drain).  x_pool: stage 0, [pool, B, dims[0]] bf16;
+ * y_pool: last stage, [pool, B] int32; mini-batch j uses slot j % pool.
+ * Pools may be device or host memory (host: copied per mini-batch inside).   */
+tps_status tps_run_schedule(tps_pipeline* p, int64_t first_mb, int64_t n_mb,
+                            const void* x_pool, const int32_t* y_pool, int32_t pool);
+/* LOCAL transport: drive all S linked handles of this process through the same
+ * range, interleaving stages in a dependency-respecting host order.            */
+tps_status tps_run_schedule_local(tps_pipeline* const* stages, int32_t num_stages,
+                                  int64_t first_mb, int64_t n_mb,
+                                  const void* x_pool, const int32_t* y_pool, int32_t pool);
+tps_status tps_synchronize(tps_pipeline* p);
+
+/* ---- stash / intermediate-weight management -------------------------------- */
+tps_status tps_blend_coeffs(int32_t variant, int32_t blend, int32_t staleness, double lambda,
+                            float* alpha, float* beta);
+/* live_versions: bf16 weight versions currently held; stash_bytes: bytes of live
+ * versions other than the latest; peak_stash_bytes: max over the run.          */
+tps_status tps_stash_info(tps_pipeline* p, int32_t* live_versions, int64_t* stash_bytes,
+                          int64_t* peak_stash_bytes);
+/* Debug materialiser (K8): out_bf16 (device, [out, ld_in]) =
+ * bf16_rne(fp32(α·W_stash) + fp32(β·W_latest)) for stage-local layer index
+ * `layer`, with W_stash = latest - staleness.  Never used by the training path. */
+tps_status tps_intermediate_weight(tps_pipeline* p, int32_t layer, int32_t staleness,
+                                   void* out_bf16);
+
+/* Debug read of a live bf16 weight version (device out, [pad16(out), pad16(in)]):
+ * version latest - staleness of stage-local layer `layer`.                    */
+tps_status tps_get_version(tps_pipeline* p, int32_t layer, int32_t staleness, void* out_bf16);
+
+/* ---- static schedule (host only) ------------------------------------------- */
+/* Stage s's static order for M mini-batches (reading Z6/Z7): F of mini-batches
+ * 0..K-1 (K = min(S-s, M)), then per j: B(j), U(j), F(j+K).  One F record per
+ * forward group.  Writes up to cap records; *n = total.                       */
+tps_status tps_schedule_events(int32_t S, int32_t s, int32_t m, int32_t fwd_group, int64_t M,
+                               tps_event* out, int64_t cap, int64_t* n);
+
+/* ---- state access ------------------------------------------------------------ */
+/* Stage-local layer `layer`: host fp32 buffers of logical size [out, in] / [out]
+ * (any may be NULL).  Synchronizes the handle.                                */
+tps_status tps_get_weights(tps_pipeline* p, int32_t layer, float* w, float* b,
+                           float* mom_w, float* mom_b);
+/* Sets the fp32 master (and the latest bf16 version) of a layer; zeroes momentum. */
+tps_status tps_set_weights(tps_pipeline* p, int32_t layer, const float* w, const float* b);
+/* Device-side synthetic init, bit-identical to synthgen.weights(seed, global layer). */
+tps_status tps_init_weights_synthetic(tps_pipeline* p);
+/* Per-mini-batch mean losses of the last stage, in mini-batch order since init. */
+tps_status tps_get_losses(tps_pipeline* p, float* out, int64_t cap, int64_t* n);
+tps_status tps_get_trace(tps_pipeline* p, tps_event* out, int64_t cap, int64_t* n);
+tps_status tps_clear_trace(tps_pipeline* p);
+/* Bytes held by category; peak = max over the handle's life of their sum. */
+tps_status tps_memory_stats(tps_pipeline* p, int64_t* weights, int64_t* stash, int64_t* acts,
+                            int64_t* optim, int64_t* comm, int64_t* peak);
+/* Kernel timing: when enabled, CUDA events bracket every GEMM launch on the
+ * compute stream; tps_kernel_stats returns launch count, summed device ms and
+ * summed algorithmic FLOPs of GEMM kind `which` (0 fwd, 1 dgrad, 2 wgrad,
+ * 3 all GEMMs, 4 update kernel [bytes instead of FLOPs]).  Synchronizes.       */
+tps_status tps_set_profiling(tps_pipeline* p, int32_t enable);
+tps_status tps_kernel_stats(tps_pipeline* p, int32_t which, int64_t* launches, double* ms,
+                            double* work);
+/* Number of kernels this handle has launched since init (product kernels only). */
+tps_status tps_launch_count(tps_pipeline* p, int64_t* n);
+
+/* ---- synthetic inputs (device counter-based generator = synthgen) ------------ */
+/* kind 0: x = ((h & 0xFF) - 128)/128; kind 1: x = (h & 0xFF)/256 (bf16 out, rows×cols
+ * dense); kind 2: labels (h >> 8) % classes (int32 out, `rows` entries).  tid as in
+ * synthgen (TID_X + mb, TID_Y + mb).  dst is a device pointer.                  */
+tps_status tps_fill_synthetic(int32_t kind, uint64_t seed, uint64_t tid, int64_t rows,
+                              int64_t cols, int32_t classes, void* dst, uint64_t stream);
+
+/* ---- raw stage GEMM (kernel unit tests / microbenchmarks) -------------------- */
+/* D[M,N] = alpha · A·Bᵀ (fp32 accumulate on tcgen05), A and B bf16, device.
+ * mode 0 (forward):  A [M,K] ld=lda (K-major), B [N,K] ld=ldb (K-major);
+ *        epilogue: + bias[N] (fp32, may be NULL), ReLU if relu, out bf16 or fp32.
+ * mode 1 (dgrad):    A [M,K] (K-major), B stored [K,N] ld=ldb (MN-major);
+ *        epilogue: ·alpha, then zero where mask[M,N] (bf16, ld=ldm) is <= 0 (mask may be NULL).
+ * mode 2 (wgrad):    A stored [K,M] ld=lda (MN-major), B stored [K,N] (MN-major); fp32 out.
+ * mode 3 (dgrad, blended operand, CONVEX/I): B = alpha·B + beta·B2 formed in shared memory
+ *        before the MMA (B2 same layout/ld as B); mask as mode 1; no extra alpha scale.
+ * out_f32: 1 => fp32 output, else bf16.  Requires N % 8 == 0 and 16-byte aligned rows. */
+tps_status tps_gemm(int32_t mode, int32_t M, int32_t N, int32_t K,
+                    const void* A, int32_t lda, const void* B, int32_t ldb, const void* B2,
+                    void* out, int32_t ldo, int32_t out_f32, const float* bias, int32_t relu,
+                    float alpha, float beta, const void* mask, int32_t ldm, uint64_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TPS_H */

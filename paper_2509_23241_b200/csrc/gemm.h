@@ -1,0 +1,30 @@
+// gemm.h — host interface of the sm_100a stage GEMM (gemm_sm100.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace tps {
+
+enum GemmMode { GEMM_FWD = 0, GEMM_DGRAD = 1, GEMM_WGRAD = 2, GEMM_DGRAD_BLEND = 3 };
+
+struct GemmOperands {
+  const void* A;  int lda;    // bf16
+  const void* B;  int ldb;    // bf16
+  const void* B2;             // bf16, BLEND only (the latest weight; same ld as B)
+};
+
+// Passed by value to the kernel.
+struct GemmArgs {
+  int M, N, K;
+  void* out; int ldo; int out_f32;
+  const float* bias; int relu;
+  float alpha;                // epilogue scale (EQ1 α), 1 = none
+  float xa, xb;               // BLEND operand coefficients
+  const uint16_t* mask; int ldm;  // bf16 ReLU mask source (zero where <= 0), may be null
+};
+
+cudaError_t gemm_run(int mode, const GemmOperands& op, const GemmArgs& args, cudaStream_t st, int* bn_out = nullptr);
+const char* gemm_mode_name(int mode);
+
+}  // namespace tps

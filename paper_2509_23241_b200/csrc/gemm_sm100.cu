@@ -1,0 +1,448 @@
+// gemm_sm100.cu — the stage GEMMs of the TiMePReSt hot path on 5th-gen tensor cores.
+//
+// One persistent, warp-specialised kernel template serves the three contractions of
+// a Linear layer (PAPER P:134 forward / backward):
+//   forward  Y  = act(X·Wᵀ + b)             A = X  [M,K] K-major,  B = W  [N,K] K-major
+//   dgrad    dX = (G·W_res) ⊙ 1[X_in > 0]    A = G  [M,K] K-major,  B = W  stored [K,N] (MN-major)
+//   wgrad    dW = Gᵀ·X                       A = G  stored [K,M],   B = X  stored [K,N] (both MN-major)
+// so no transpose is ever materialised.  For I-TiMePReSt the dgrad weight is the
+// intermediate weight (Eq. 1, reading Z1): either α applied in the epilogue
+// (EQ1: α·(G·W_stash), exact in real arithmetic) or, with BLEND, W_res = α·W_stash +
+// β·W_latest formed by transform warps from two TMA-staged tiles straight into the MMA
+// operand buffer — the blended weight never exists in HBM.
+//
+// Roles (one CTA per SM, persistent over output tiles 128 x BN):
+//   warp 0      TMA producer (one elected lane): A/B tiles -> 128B-swizzled smem ring
+//   warp 1      MMA issuer (one lane): tcgen05.mma kind::f16, fp32 accumulators in TMEM
+//   warps 2..5  epilogue: tcgen05.ld TMEM -> registers -> bias/ReLU/α/mask -> global
+//   warps 6..9  (BLEND only) operand transform warps
+// TMEM holds two accumulators (2·BN columns) so the epilogue of tile i overlaps the
+// MMAs of tile i+1.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdio>
+
+#include "gemm.h"
+#include "ptx.cuh"
+
+namespace tps {
+
+namespace {
+
+constexpr int BM = 128;
+constexpr int BK = 64;                     // 64 bf16 = 128 B = one swizzle atom row
+constexpr int A_BYTES = BM * BK * 2;       // 16 KiB
+constexpr int SMEM_BUDGET = 227 * 1024;
+
+template <int BN, int BLEND>
+struct Cfg {
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES * (BLEND ? 3 : 1);
+  static constexpr int STAGES_RAW = (SMEM_BUDGET - 2048) / STAGE_BYTES;
+  static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
+  static constexpr int THREADS = BLEND ? 320 : 192;
+  static constexpr int TMEM_COLS = 2 * BN;
+  static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + 256;
+  static constexpr uint32_t TX = A_BYTES + B_BYTES * (BLEND ? 2 : 1);
+};
+
+__device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int& mb, int& nb) {
+  constexpr int G = 8;                      // group m-blocks so B tiles are reused from L2
+  const int group = G * num_n;
+  const int g = t / group;
+  const int first_m = g * G;
+  const int gm = min(G, num_m - first_m);
+  const int r = t - g * group;
+  mb = first_m + r % gm;
+  nb = r / gm;
+}
+
+__device__ __forceinline__ float bf16_bits_to_f32(uint32_t h) { return __uint_as_float(h << 16); }
+
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+template <int BN, int A_MN, int B_MN, int BLEND>
+__global__ void __launch_bounds__(Cfg<BN, BLEND>::THREADS, 1)
+    gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                const __grid_constant__ CUtensorMap tmB2, const GemmArgs args) {
+  using C = Cfg<BN, BLEND>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* stages = smem;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* xform = empty + C::STAGES;
+  uint64_t* tmem_full = xform + C::STAGES;
+  uint64_t* tmem_empty = tmem_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int num_m = (args.M + BM - 1) / BM;
+  const int num_n = (args.N + BN - 1) / BN;
+  const int num_k = (args.K + BK - 1) / BK;
+  const int num_tiles = num_m * num_n;
+
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&tmA);
+    ptx::prefetch_tmap(&tmB);
+    if (BLEND) ptx::prefetch_tmap(&tmB2);
+    for (int s = 0; s < C::STAGES; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+      ptx::mbar_init(&xform[s], 128);
+    }
+    for (int a = 0; a < 2; ++a) {
+      ptx::mbar_init(&tmem_full[a], 1);
+      ptx::mbar_init(&tmem_empty[a], 4);
+    }
+    ptx::fence_barrier_init();
+  }
+  if (warp == 1) ptx::tmem_alloc(tmem_slot, C::TMEM_COLS);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ===================== TMA producer =====================
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        int mb, nb;
+        tile_coords(t, num_m, num_n, mb, nb);
+        for (int kb = 0; kb < num_k; ++kb) {
+          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sA = stages + stage * C::STAGE_BYTES;
+          uint8_t* sB = sA + A_BYTES;
+          ptx::mbar_expect_tx(&full[stage], C::TX);
+          if (!A_MN) {
+            ptx::tma_load_2d(sA, &tmA, &full[stage], kb * BK, mb * BM);
+          } else {
+#pragma unroll
+            for (int i = 0; i < BM / 64; ++i)
+              ptx::tma_load_2d(sA + i * 8192, &tmA, &full[stage], mb * BM + 64 * i, kb * BK);
+          }
+          // BLEND: stash -> staging 1, latest -> staging 2; transform warps fill sB
+          uint8_t* dB = BLEND ? sB + C::B_BYTES : sB;
+          if (!B_MN) {
+            ptx::tma_load_2d(dB, &tmB, &full[stage], kb * BK, nb * BN);
+            if (BLEND) ptx::tma_load_2d(dB + C::B_BYTES, &tmB2, &full[stage], kb * BK, nb * BN);
+          } else {
+#pragma unroll
+            for (int i = 0; i < BN / 64; ++i) {
+              ptx::tma_load_2d(dB + i * 8192, &tmB, &full[stage], nb * BN + 64 * i, kb * BK);
+              if (BLEND) ptx::tma_load_2d(dB + C::B_BYTES + i * 8192, &tmB2, &full[stage], nb * BN + 64 * i, kb * BK);
+            }
+          }
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer =====================
+    if (lane == 0) {
+      constexpr uint32_t idesc = ptx::make_idesc_bf16(BM, BN, A_MN, B_MN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+        const int acc = it & 1;
+        const uint32_t acc_phase = (it >> 1) & 1;
+        ptx::mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_k; ++kb) {
+          ptx::mbar_wait(&full[stage], phase);
+          if (BLEND) ptx::mbar_wait(&xform[stage], phase);
+          ptx::tc_fence_after();
+          const uint32_t a_addr = ptx::smem_u32(stages + stage * C::STAGE_BYTES);
+          const uint32_t b_addr = a_addr + A_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            // K-major SW128: +32 B per 16-element K step, SBO = 8 rows x 128 B
+            // MN-major SW128: +16 K-rows x 128 B per step, LBO = 64-element MN chunk (8 KiB), SBO = 1 KiB
+            const uint64_t ad = A_MN ? ptx::make_sdesc_sw128(a_addr + kk * 2048, 8192, 1024)
+                                     : ptx::make_sdesc_sw128(a_addr + kk * 32, 16, 1024);
+            const uint64_t bd = B_MN ? ptx::make_sdesc_sw128(b_addr + kk * 2048, 8192, 1024)
+                                     : ptx::make_sdesc_sw128(b_addr + kk * 32, 16, 1024);
+            ptx::umma_f16(d_tmem, ad, bd, idesc, (kb | kk) != 0);
+          }
+          ptx::umma_commit(&empty[stage]);
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+        ptx::umma_commit(&tmem_full[acc]);
+      }
+    }
+  } else if (warp < 6) {
+    // ===================== epilogue =====================
+    const int q = warp & 3;                 // TMEM lane quarter this warp may access
+    const int row = q * 32 + lane;
+    int it = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+      int mb, nb;
+      tile_coords(t, num_m, num_n, mb, nb);
+      const int acc = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
+      ptx::mbar_wait(&tmem_full[acc], acc_phase);
+      ptx::tc_fence_after();
+      const int grow = mb * BM + row;
+      const bool row_ok = grow < args.M;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t r[32];
+        ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c * 32, r);
+        ptx::tmem_ld_wait();
+        const int gcol = nb * BN + c * 32;
+        if (!row_ok || gcol >= args.N) continue;
+        float v[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+        const int nchunk = min(4, (args.N - gcol) >> 3);   // 8-column chunks inside N
+        if (args.alpha != 1.0f) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = __fmul_rn(v[i], args.alpha);
+        }
+        if (args.bias) {
+          const float* bp = args.bias + gcol;
+#pragma unroll
+          for (int ch = 0; ch < 4; ++ch) {
+            if (ch < nchunk) {
+              const float4 b0 = __ldg(reinterpret_cast<const float4*>(bp + ch * 8));
+              const float4 b1 = __ldg(reinterpret_cast<const float4*>(bp + ch * 8 + 4));
+              v[ch * 8 + 0] = __fadd_rn(v[ch * 8 + 0], b0.x);
+              v[ch * 8 + 1] = __fadd_rn(v[ch * 8 + 1], b0.y);
+              v[ch * 8 + 2] = __fadd_rn(v[ch * 8 + 2], b0.z);
+              v[ch * 8 + 3] = __fadd_rn(v[ch * 8 + 3], b0.w);
+              v[ch * 8 + 4] = __fadd_rn(v[ch * 8 + 4], b1.x);
+              v[ch * 8 + 5] = __fadd_rn(v[ch * 8 + 5], b1.y);
+              v[ch * 8 + 6] = __fadd_rn(v[ch * 8 + 6], b1.z);
+              v[ch * 8 + 7] = __fadd_rn(v[ch * 8 + 7], b1.w);
+            }
+          }
+        }
+        if (args.relu) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.0f);
+        }
+        if (args.mask) {
+          const uint4* mp = reinterpret_cast<const uint4*>(args.mask + static_cast<size_t>(grow) * args.ldm + gcol);
+#pragma unroll
+          for (int ch = 0; ch < 4; ++ch) {
+            if (ch < nchunk) {
+              const uint4 mv = __ldg(mp + ch);
+              const uint32_t w[4] = {mv.x, mv.y, mv.z, mv.w};
+#pragma unroll
+              for (int e = 0; e < 8; ++e) {
+                const uint32_t h = (w[e >> 1] >> ((e & 1) * 16)) & 0xFFFFu;
+                const bool pos = ((h & 0x8000u) == 0u) && ((h & 0x7FFFu) != 0u);
+                if (!pos) v[ch * 8 + e] = 0.0f;
+              }
+            }
+          }
+        }
+        if (args.out_f32) {
+          float* op = reinterpret_cast<float*>(args.out) + static_cast<size_t>(grow) * args.ldo + gcol;
+#pragma unroll
+          for (int ch = 0; ch < 4; ++ch) {
+            if (ch < nchunk) {
+              reinterpret_cast<float4*>(op + ch * 8)[0] = make_float4(v[ch * 8], v[ch * 8 + 1], v[ch * 8 + 2], v[ch * 8 + 3]);
+              reinterpret_cast<float4*>(op + ch * 8)[1] =
+                  make_float4(v[ch * 8 + 4], v[ch * 8 + 5], v[ch * 8 + 6], v[ch * 8 + 7]);
+            }
+          }
+        } else {
+          __nv_bfloat16* op = reinterpret_cast<__nv_bfloat16*>(args.out) + static_cast<size_t>(grow) * args.ldo + gcol;
+#pragma unroll
+          for (int ch = 0; ch < 4; ++ch) {
+            if (ch < nchunk) {
+              uint4 o;
+              o.x = pack_bf16(v[ch * 8 + 0], v[ch * 8 + 1]);
+              o.y = pack_bf16(v[ch * 8 + 2], v[ch * 8 + 3]);
+              o.z = pack_bf16(v[ch * 8 + 4], v[ch * 8 + 5]);
+              o.w = pack_bf16(v[ch * 8 + 6], v[ch * 8 + 7]);
+              reinterpret_cast<uint4*>(op)[ch] = o;
+            }
+          }
+        }
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&tmem_empty[acc]);
+    }
+  } else if (BLEND) {
+    // ===================== operand transform: W_res = α·W_stash + β·W_latest =====================
+    const int tt = threadIdx.x - 6 * 32;    // 0..127
+    const float xa = args.xa, xb = args.xb;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      for (int kb = 0; kb < num_k; ++kb) {
+        ptx::mbar_wait(&full[stage], phase);
+        uint8_t* sB = stages + stage * C::STAGE_BYTES + A_BYTES;
+        const uint4* s = reinterpret_cast<const uint4*>(sB + C::B_BYTES);
+        const uint4* l = reinterpret_cast<const uint4*>(sB + 2 * C::B_BYTES);
+        uint4* o = reinterpret_cast<uint4*>(sB);
+        // identical swizzled layouts: the blend is elementwise on raw 16-byte chunks
+#pragma unroll 4
+        for (int i = tt; i < C::B_BYTES / 16; i += 128) {
+          const uint4 a = s[i];
+          const uint4 b = l[i];
+          const uint32_t aw[4] = {a.x, a.y, a.z, a.w};
+          const uint32_t bw[4] = {b.x, b.y, b.z, b.w};
+          uint32_t ow[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float a0 = bf16_bits_to_f32(aw[e] & 0xFFFFu), a1 = bf16_bits_to_f32(aw[e] >> 16);
+            const float b0 = bf16_bits_to_f32(bw[e] & 0xFFFFu), b1 = bf16_bits_to_f32(bw[e] >> 16);
+            const float r0 = __fadd_rn(__fmul_rn(xa, a0), __fmul_rn(xb, b0));
+            const float r1 = __fadd_rn(__fmul_rn(xa, a1), __fmul_rn(xb, b1));
+            ow[e] = pack_bf16(r0, r1);
+          }
+          o[i] = make_uint4(ow[0], ow[1], ow[2], ow[3]);
+        }
+        ptx::fence_proxy_async_smem();
+        ptx::mbar_arrive(&xform[stage]);
+        if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem_base, C::TMEM_COLS);
+  }
+}
+
+// ---------------------------------------------------------------- host side
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// 2-D bf16 tensor [rows, cols] (cols contiguous, ld elements), box {64, box_rows}, 128B swizzle.
+bool make_tmap(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint64_t ld, uint32_t box_rows) {
+  EncodeTiledFn enc = get_encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {ld * 2};
+  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <int BN, int A_MN, int B_MN, int BLEND>
+cudaError_t launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& b2, const GemmArgs& args,
+                   cudaStream_t st) {
+  using C = Cfg<BN, BLEND>;
+  auto kern = gemm_kernel<BN, A_MN, B_MN, BLEND>;
+  static bool attr_set = false;   // per instantiation
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const int tiles = ((args.M + BM - 1) / BM) * ((args.N + BN - 1) / BN);
+  const int grid = std::max(1, std::min(tiles, num_sms()));
+  kern<<<grid, C::THREADS, C::SMEM, st>>>(a, b, b2, args);
+  return cudaGetLastError();
+}
+
+int pick_bn(int M, int N, int mode) {
+  if (mode == GEMM_DGRAD_BLEND) return 128;
+  const int tm = (M + BM - 1) / BM;
+  const int sms = num_sms();
+  const int cand[3] = {256, 128, 64};
+  for (int i = 0; i < 3; ++i) {
+    const int bn = cand[i];
+    if (bn > 64 && N <= bn / 2) continue;          // mostly padding
+    const int tiles = tm * ((N + bn - 1) / bn);
+    if (tiles >= (sms * 3) / 4 || bn == 64) return bn;
+  }
+  return 64;
+}
+
+}  // namespace
+
+const char* gemm_mode_name(int mode) {
+  switch (mode) {
+    case GEMM_FWD: return "fwd";
+    case GEMM_DGRAD: return "dgrad";
+    case GEMM_WGRAD: return "wgrad";
+    case GEMM_DGRAD_BLEND: return "dgrad_blend";
+  }
+  return "?";
+}
+
+cudaError_t gemm_run(int mode, const GemmOperands& op, const GemmArgs& args_in, cudaStream_t st, int* bn_out) {
+  GemmArgs args = args_in;
+  if (args.M <= 0 || args.N <= 0 || args.K <= 0) return cudaSuccess;
+  const int bn = pick_bn(args.M, args.N, mode);
+  if (bn_out) *bn_out = bn;
+  CUtensorMap ta, tb, tb2;
+  const bool a_mn = (mode == GEMM_WGRAD);
+  const bool b_mn = (mode != GEMM_FWD);
+  bool ok = true;
+  // A: K-major [M,K] -> box {64 K, 128 rows}; MN-major stored [K,M] -> box {64 M, 64 K}
+  if (!a_mn) ok &= make_tmap(&ta, op.A, args.M, args.K, op.lda, BM);
+  else ok &= make_tmap(&ta, op.A, args.K, args.M, op.lda, 64);
+  if (!b_mn) ok &= make_tmap(&tb, op.B, args.N, args.K, op.ldb, bn);
+  else ok &= make_tmap(&tb, op.B, args.K, args.N, op.ldb, 64);
+  if (mode == GEMM_DGRAD_BLEND) ok &= make_tmap(&tb2, op.B2, args.K, args.N, op.ldb, 64);
+  else tb2 = tb;
+  if (!ok) return cudaErrorInvalidValue;
+  switch (mode) {
+    case GEMM_FWD:
+      if (bn == 256) return launch<256, 0, 0, 0>(ta, tb, tb2, args, st);
+      if (bn == 128) return launch<128, 0, 0, 0>(ta, tb, tb2, args, st);
+      return launch<64, 0, 0, 0>(ta, tb, tb2, args, st);
+    case GEMM_DGRAD:
+      if (bn == 256) return launch<256, 0, 1, 0>(ta, tb, tb2, args, st);
+      if (bn == 128) return launch<128, 0, 1, 0>(ta, tb, tb2, args, st);
+      return launch<64, 0, 1, 0>(ta, tb, tb2, args, st);
+    case GEMM_WGRAD:
+      if (bn == 256) return launch<256, 1, 1, 0>(ta, tb, tb2, args, st);
+      if (bn == 128) return launch<128, 1, 1, 0>(ta, tb, tb2, args, st);
+      return launch<64, 1, 1, 0>(ta, tb, tb2, args, st);
+    case GEMM_DGRAD_BLEND:
+      return launch<128, 0, 1, 1>(ta, tb, tb2, args, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace tps

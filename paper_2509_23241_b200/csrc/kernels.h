@@ -1,0 +1,43 @@
+// kernels.h — launchers of the non-GEMM kernels of the hot path (elementwise.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace tps {
+
+// Fused SGD/momentum update + new bf16 version (row a10):
+//   g' = g + wd·w ; v = μ·v + g' ; w = w - lr·v   (fp32, one rounding per op, PyTorch order)
+//   ver = bf16_rne(w)  (skipped if ver == nullptr).  μ == 0 => v untouched (14 B/param).
+cudaError_t launch_sgd_update(float* w, float* v, const float* g, uint16_t* ver, int64_t n, float lr, float mu,
+                              float wd, cudaStream_t st);
+
+// db[c] = Σ_{r<rows} G[r, c] for c < cols (G bf16 [rows, ldg]); deterministic two-phase
+// reduction using `scratch` (>= bias_grad_scratch_floats(rows, cols) floats).
+int64_t bias_grad_scratch_floats(int rows, int cols);
+cudaError_t launch_bias_grad(const uint16_t* G, int rows, int cols, int ldg, float* db, float* scratch,
+                             cudaStream_t st);
+
+// Softmax cross-entropy forward+backward for `rows` rows of fp32 logits [rows, ldl] with
+// `classes` valid columns: loss_rows[r] = logsumexp(z) - z_y ;
+// G[r, c] = bf16((softmax(z)_c - [c == y]) / batch) for c < classes, 0 for classes <= c < ldg.
+cudaError_t launch_softmax_xent(const float* logits, int ldl, const int32_t* labels, int rows, int classes,
+                                int batch, float* loss_rows, uint16_t* G, int ldg, cudaStream_t st);
+
+// losses[idx] = (Σ_{r<rows} loss_rows[r]) / rows   (fixed-order fp64 reduction, one block)
+cudaError_t launch_loss_mean(const float* loss_rows, int rows, float* losses, int64_t idx, cudaStream_t st);
+
+// fp32 -> bf16 RNE, n elements
+cudaError_t launch_f32_to_bf16(const float* in, uint16_t* out, int64_t n, cudaStream_t st);
+
+// K8 debug materialiser: out = bf16(fp32(α·s) + fp32(β·l))
+cudaError_t launch_blend_materialize(const uint16_t* s, const uint16_t* l, uint16_t* out, int64_t n, float a,
+                                     float b, cudaStream_t st);
+
+// synthgen-identical counter-based generator (see synthgen/__init__.py)
+//   kind 0/1: bf16 inputs into dst[rows, ld] (cols valid); kind 2: int32 labels[rows];
+//   kind 3: fp32 weights [rows=out, ld] (cols=in valid), scale 2^-(23 + shift).
+cudaError_t launch_fill_synthetic(int kind, uint64_t seed, uint64_t tid, int64_t rows, int64_t cols, int64_t ld,
+                                  int classes, int shift, void* dst, cudaStream_t st);
+
+}  // namespace tps

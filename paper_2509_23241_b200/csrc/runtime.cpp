@@ -1,0 +1,1134 @@
+// runtime.cpp — host runtime behind include/tps.h: one handle per pipeline stage.
+//
+// What it does per mini-batch j at stage s:
+//   F(j, group)  forward of a group of micro-batches on the stage's LATEST bf16 weights
+//                (V: P:182/P:188; I: P:213, reading Z8), activations kept for the backward
+//   B(j)         one collective backward over the B = m·b rows: wgrad + bias grad and
+//                dgrad on the resolved weight (V: latest; I: α·W_stash + β·W_latest,
+//                Eq. 1 P:220 / reading Z1) with δ = latest - version the forward used
+//   U(j)         fused SGD/momentum update; the new bf16 version goes into ring slot
+//                (version mod R): R = S - s for I (stash kept until its last consumer,
+//                P:408), R = 1 for V (old version overwritten at once)
+// in the static per-stage order of reading Z7 (K_s = S - s mini-batches in flight).
+// The host only enqueues: kernels on the compute stream, transfers on four comm
+// streams ordered by CUDA events; nothing blocks until tps_synchronize.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/tps.h"
+#include "gemm.h"
+#include "kernels.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+tps_status fail(tps_status st, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+
+#define CUDA_OK(expr)                                                                                   \
+  do {                                                                                                  \
+    cudaError_t _e = (expr);                                                                            \
+    if (_e != cudaSuccess) return fail(TPS_E_CUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(_e), __FILE__, __LINE__); \
+  } while (0)
+
+#define NCCL_OK(expr)                                                                                   \
+  do {                                                                                                  \
+    ncclResult_t _r = (expr);                                                                           \
+    if (_r != ncclSuccess) return fail(TPS_E_NCCL, "%s: %s", #expr, ncclGetErrorString(_r));           \
+  } while (0)
+
+#define TPS_TRY(expr)                  \
+  do {                                 \
+    tps_status _s = (expr);            \
+    if (_s != TPS_OK) return _s;       \
+  } while (0)
+
+inline int pad16(int d) { return (d + 15) / 16 * 16; }
+
+bool is_host_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeUnregistered;
+}
+
+tps_status check_arch(int device) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n <= device) {
+    cudaGetLastError();
+    return fail(TPS_E_ARCH, "no CUDA device %d (this build has no CPU fallback)", device);
+  }
+  cudaDeviceProp pr;
+  CUDA_OK(cudaGetDeviceProperties(&pr, device));
+  if (pr.major != 10) return fail(TPS_E_ARCH, "device %d is sm_%d%d; this library targets sm_100a", device, pr.major, pr.minor);
+  return TPS_OK;
+}
+
+struct Layer {
+  int gidx = 0, in = 0, out = 0, Kp = 0, Np = 0;
+  float *W = nullptr, *b = nullptr, *mW = nullptr, *mb = nullptr, *dW = nullptr, *db = nullptr;
+  std::vector<uint16_t*> ver;  // R bf16 [Np, Kp] slots
+};
+
+struct Msg {  // LOCAL transport mailbox entry
+  const void* src;
+  size_t bytes;
+  cudaEvent_t ready;
+  cudaEvent_t consumed;  // owned by the sender; recorded by the receiver after its copy
+};
+
+struct TimedLaunch {
+  int kind;
+  double work;
+  cudaEvent_t a, b;
+};
+
+}  // namespace
+
+struct tps_pipeline {
+  // ---- configuration
+  int S = 1, s = 0, m = 1, bsz = 1, B = 1, g = 1, ng = 1, Kmax = 1, R = 1, A0 = 1;
+  int variant = TPS_V, blend = TPS_BLEND_EQ1, transport = TPS_TRANSPORT_NONE, device = 0;
+  double lambda = 0.05;
+  float lr = 0.01f, mu = 0.f, wd = 0.f;
+  uint64_t seed = 0;
+  bool first = true, last = true, eq1_on_load = false;
+  std::vector<int> dims;  // global
+  std::vector<Layer> layers;
+  int classes = 0;
+
+  // ---- device buffers
+  std::vector<std::vector<uint16_t*>> act;  // act[slot][k]  bf16 [B, Kp_k]   (slot count A0 for k=0, Kmax else)
+  uint16_t* send_fwd[2] = {nullptr, nullptr};
+  uint16_t* gin[2] = {nullptr, nullptr};
+  uint16_t* gout[2] = {nullptr, nullptr};
+  uint16_t* gwork[2] = {nullptr, nullptr};
+  float* logits = nullptr;
+  uint16_t* gce = nullptr;
+  float* loss_rows = nullptr;
+  float* losses = nullptr;
+  int64_t loss_cap = 0, loss_count = 0;
+  int32_t* labels_dev = nullptr;
+  float* scratch = nullptr;
+  std::vector<void*> allocs;
+
+  // ---- memory accounting
+  int64_t mem_weights = 0, mem_stash = 0, mem_acts = 0, mem_optim = 0, mem_comm = 0, mem_peak = 0;
+  int64_t ver_bytes = 0, peak_stash_live = 0;
+
+  // ---- versions and run state
+  int64_t latest = 0;
+  std::map<int64_t, int64_t> fwd_version;  // mb -> version its forward used (until its backward)
+  std::map<int64_t, int> fwd_groups_done;
+  std::vector<tps_event> order;
+  size_t pos = 0;
+  int64_t run_first = 0, run_n = 0;
+  bool in_run = false;
+  int64_t pending_update = -1;
+  std::vector<tps_event> trace;
+
+  // ---- streams, events, transport
+  cudaStream_t cs = nullptr;
+  bool own_cs = false;
+  cudaStream_t s_fin = nullptr, s_fout = nullptr, s_bin = nullptr, s_bout = nullptr;
+  std::vector<cudaEvent_t> ev_fwd_ready, ev_fwd_sent;  // [2 * ng]
+  std::vector<cudaEvent_t> ev_act_free;                // [A0]
+  cudaEvent_t ev_recv = nullptr, ev_gin_free[2] = {nullptr, nullptr}, ev_gout_ready = nullptr,
+              ev_bwd_sent[2] = {nullptr, nullptr}, ev_gin_ready = nullptr;
+  ncclComm_t c_fin = nullptr, c_fout = nullptr, c_bin = nullptr, c_bout = nullptr;
+  tps_pipeline* prev_local = nullptr;
+  tps_pipeline* next_local = nullptr;
+  std::map<std::pair<int64_t, int>, Msg> mbox_fwd;  // keyed (mb, group), filled by prev stage
+  std::map<int64_t, Msg> mbox_bwd;                  // keyed mb, filled by next stage
+
+  // ---- profiling / counters
+  bool profiling = false;
+  std::vector<TimedLaunch> timed;
+  std::vector<cudaEvent_t> ev_pool;
+  double stat_ms[5] = {0, 0, 0, 0, 0}, stat_work[5] = {0, 0, 0, 0, 0};
+  int64_t stat_n[5] = {0, 0, 0, 0, 0};
+  int64_t launches = 0;
+  bool poisoned = false;
+
+  int nlayers() const { return static_cast<int>(layers.size()); }
+};
+
+namespace {
+
+// ------------------------------------------------------------------ helpers
+tps_status dev_alloc(tps_pipeline* p, void** out, size_t bytes, int64_t* category) {
+  *out = nullptr;
+  if (bytes == 0) return TPS_OK;
+  cudaError_t e = cudaMalloc(out, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(TPS_E_OOM, "cudaMalloc(%zu) failed: %s", bytes, cudaGetErrorString(e));
+  }
+  CUDA_OK(cudaMemset(*out, 0, bytes));
+  p->allocs.push_back(*out);
+  if (category) *category += static_cast<int64_t>(bytes);
+  p->mem_peak = std::max(p->mem_peak, p->mem_weights + p->mem_stash + p->mem_acts + p->mem_optim + p->mem_comm);
+  return TPS_OK;
+}
+
+template <class T>
+tps_status alloc_t(tps_pipeline* p, T** out, size_t count, int64_t* category) {
+  void* v = nullptr;
+  TPS_TRY(dev_alloc(p, &v, count * sizeof(T), category));
+  *out = static_cast<T*>(v);
+  return TPS_OK;
+}
+
+cudaEvent_t new_event() {
+  cudaEvent_t e = nullptr;
+  cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  return e;
+}
+
+void compute_coeffs(int variant, int blend, int delta, double lambda, float* a, float* b) {
+  if (variant == TPS_V) {
+    *a = 1.0f;
+    *b = 0.0f;
+    return;
+  }
+  const double f = std::exp(-lambda * static_cast<double>(delta));  // Eq. 2
+  if (blend == TPS_BLEND_EQ1) {
+    *a = static_cast<float>(2.0 - 1.0 / f);                         // Eq. 1
+    *b = 0.0f;
+  } else {
+    *a = static_cast<float>(f);                                     // reading Z1 (CONVEX)
+    *b = static_cast<float>(1.0 - f);
+  }
+}
+
+void build_order(int S, int s, int m, int g, int64_t first, int64_t n, std::vector<tps_event>* out) {
+  out->clear();
+  const int64_t K = std::min<int64_t>(S - s, n);
+  auto push_f = [&](int64_t j) {
+    for (int a = 0; a < m; a += g) {
+      tps_event e{};
+      e.stage = s; e.kind = TPS_EV_F; e.micro = a; e.micro_count = g; e.mb = j;
+      e.v_used = e.v_latest = -1; e.alpha = 1.f;
+      out->push_back(e);
+    }
+  };
+  for (int64_t j = first; j < first + K; ++j) push_f(j);
+  for (int64_t j = first; j < first + n; ++j) {
+    tps_event e{};
+    e.stage = s; e.kind = TPS_EV_B; e.mb = j; e.v_used = e.v_latest = -1; e.alpha = 1.f;
+    out->push_back(e);
+    e.kind = TPS_EV_U;
+    out->push_back(e);
+    if (j + K < first + n) push_f(j + K);
+  }
+}
+
+double gemm_flops(int M, int N, int K) { return 2.0 * M * static_cast<double>(N) * K; }
+
+tps_status run_gemm(tps_pipeline* p, int mode, const tps::GemmOperands& op, const tps::GemmArgs& args, int kind) {
+  TimedLaunch tl{};
+  if (p->profiling) {
+    if (p->ev_pool.size() < 2) {
+      for (int i = 0; i < 64; ++i) {
+        cudaEvent_t e;
+        CUDA_OK(cudaEventCreate(&e));
+        p->ev_pool.push_back(e);
+      }
+    }
+    tl.kind = kind;
+    tl.work = gemm_flops(args.M, args.N, args.K);
+    tl.a = p->ev_pool.back(); p->ev_pool.pop_back();
+    tl.b = p->ev_pool.back(); p->ev_pool.pop_back();
+    CUDA_OK(cudaEventRecord(tl.a, p->cs));
+  }
+  CUDA_OK(tps::gemm_run(mode, op, args, p->cs));
+  p->launches += 1;
+  if (p->profiling) {
+    CUDA_OK(cudaEventRecord(tl.b, p->cs));
+    p->timed.push_back(tl);
+  }
+  return TPS_OK;
+}
+
+tps_status time_begin(tps_pipeline* p, TimedLaunch* tl, int kind, double work) {
+  if (!p->profiling) return TPS_OK;
+  if (p->ev_pool.size() < 2) {
+    for (int i = 0; i < 64; ++i) {
+      cudaEvent_t e;
+      CUDA_OK(cudaEventCreate(&e));
+      p->ev_pool.push_back(e);
+    }
+  }
+  tl->kind = kind;
+  tl->work = work;
+  tl->a = p->ev_pool.back(); p->ev_pool.pop_back();
+  tl->b = p->ev_pool.back(); p->ev_pool.pop_back();
+  CUDA_OK(cudaEventRecord(tl->a, p->cs));
+  return TPS_OK;
+}
+
+tps_status time_end(tps_pipeline* p, TimedLaunch* tl) {
+  if (!p->profiling) return TPS_OK;
+  CUDA_OK(cudaEventRecord(tl->b, p->cs));
+  p->timed.push_back(*tl);
+  return TPS_OK;
+}
+
+tps_status drain_timing(tps_pipeline* p) {
+  for (auto& t : p->timed) {
+    float ms = 0.f;
+    CUDA_OK(cudaEventElapsedTime(&ms, t.a, t.b));
+    const int k = t.kind;
+    p->stat_ms[k] += ms; p->stat_work[k] += t.work; p->stat_n[k] += 1;
+    if (k <= 2) { p->stat_ms[3] += ms; p->stat_work[3] += t.work; p->stat_n[3] += 1; }
+    p->ev_pool.push_back(t.a);
+    p->ev_pool.push_back(t.b);
+  }
+  p->timed.clear();
+  return TPS_OK;
+}
+
+tps_status check_usable(tps_pipeline* p) {
+  if (!p) return fail(TPS_E_INVALID_ARG, "null handle");
+  if (p->poisoned) return fail(TPS_E_STATE, "handle poisoned by an earlier device error");
+  CUDA_OK(cudaSetDevice(p->device));
+  return TPS_OK;
+}
+
+// ------------------------------------------------------------------ transport
+tps_status send_fwd(tps_pipeline* p, int64_t j, int grp, const void* src, size_t bytes) {
+  const int e = static_cast<int>(j & 1) * p->ng + grp;
+  CUDA_OK(cudaEventRecord(p->ev_fwd_ready[e], p->cs));
+  if (p->transport == TPS_TRANSPORT_NCCL) {
+    CUDA_OK(cudaStreamWaitEvent(p->s_fout, p->ev_fwd_ready[e], 0));
+    NCCL_OK(ncclSend(src, bytes / 2, ncclBfloat16, 1, p->c_fout, p->s_fout));
+    CUDA_OK(cudaEventRecord(p->ev_fwd_sent[e], p->s_fout));
+  } else {
+    tps_pipeline* q = p->next_local;
+    if (!q) return fail(TPS_E_STATE, "LOCAL transport not linked");
+    q->mbox_fwd[{j, grp}] = Msg{src, bytes, p->ev_fwd_ready[e], p->ev_fwd_sent[e]};
+  }
+  return TPS_OK;
+}
+
+tps_status recv_fwd(tps_pipeline* p, int64_t j, int grp, void* dst, size_t bytes) {
+  const int slot = static_cast<int>(j % p->A0);
+  CUDA_OK(cudaStreamWaitEvent(p->s_fin, p->ev_act_free[slot], 0));
+  if (p->transport == TPS_TRANSPORT_NCCL) {
+    NCCL_OK(ncclRecv(dst, bytes / 2, ncclBfloat16, 0, p->c_fin, p->s_fin));
+  } else {
+    auto it = p->mbox_fwd.find({j, grp});
+    if (it == p->mbox_fwd.end()) return fail(TPS_E_ORDER, "stage %d: forward input of mb %lld group %d not sent yet", p->s, (long long)j, grp);
+    Msg msg = it->second;
+    p->mbox_fwd.erase(it);
+    if (msg.bytes != bytes) return fail(TPS_E_STATE, "forward message size mismatch");
+    CUDA_OK(cudaStreamWaitEvent(p->s_fin, msg.ready, 0));
+    CUDA_OK(cudaMemcpyAsync(dst, msg.src, bytes, cudaMemcpyDeviceToDevice, p->s_fin));
+    CUDA_OK(cudaEventRecord(msg.consumed, p->s_fin));
+  }
+  CUDA_OK(cudaEventRecord(p->ev_recv, p->s_fin));
+  CUDA_OK(cudaStreamWaitEvent(p->cs, p->ev_recv, 0));
+  return TPS_OK;
+}
+
+tps_status send_bwd(tps_pipeline* p, int64_t j, const void* src, size_t bytes) {
+  const int e = static_cast<int>(j & 1);
+  CUDA_OK(cudaEventRecord(p->ev_gout_ready, p->cs));
+  if (p->transport == TPS_TRANSPORT_NCCL) {
+    CUDA_OK(cudaStreamWaitEvent(p->s_bout, p->ev_gout_ready, 0));
+    NCCL_OK(ncclSend(src, bytes / 2, ncclBfloat16, 0, p->c_bout, p->s_bout));
+    CUDA_OK(cudaEventRecord(p->ev_bwd_sent[e], p->s_bout));
+  } else {
+    tps_pipeline* q = p->prev_local;
+    if (!q) return fail(TPS_E_STATE, "LOCAL transport not linked");
+    // the ready event must stay distinct per message: use the sent-event slot's twin
+    cudaEvent_t ready = new_event();
+    CUDA_OK(cudaEventRecord(ready, p->cs));
+    q->mbox_bwd[j] = Msg{src, bytes, ready, p->ev_bwd_sent[e]};
+  }
+  return TPS_OK;
+}
+
+tps_status recv_bwd(tps_pipeline* p, int64_t j, void* dst, size_t bytes) {
+  const int e = static_cast<int>(j & 1);
+  CUDA_OK(cudaStreamWaitEvent(p->s_bin, p->ev_gin_free[e], 0));
+  if (p->transport == TPS_TRANSPORT_NCCL) {
+    NCCL_OK(ncclRecv(dst, bytes / 2, ncclBfloat16, 1, p->c_bin, p->s_bin));
+  } else {
+    auto it = p->mbox_bwd.find(j);
+    if (it == p->mbox_bwd.end()) return fail(TPS_E_ORDER, "stage %d: gradient of mb %lld not sent yet", p->s, (long long)j);
+    Msg msg = it->second;
+    p->mbox_bwd.erase(it);
+    if (msg.bytes != bytes) return fail(TPS_E_STATE, "backward message size mismatch");
+    CUDA_OK(cudaStreamWaitEvent(p->s_bin, msg.ready, 0));
+    CUDA_OK(cudaMemcpyAsync(dst, msg.src, bytes, cudaMemcpyDeviceToDevice, p->s_bin));
+    CUDA_OK(cudaEventRecord(msg.consumed, p->s_bin));
+    cudaEventDestroy(msg.ready);  // destruction is deferred by the runtime until the event completes
+  }
+  CUDA_OK(cudaEventRecord(p->ev_gin_ready, p->s_bin));
+  CUDA_OK(cudaStreamWaitEvent(p->cs, p->ev_gin_ready, 0));
+  return TPS_OK;
+}
+
+// ------------------------------------------------------------------ order checking
+tps_status expect(tps_pipeline* p, int kind, int64_t mb, int micro, int count) {
+  if (!p->in_run) return fail(TPS_E_ORDER, "stage %d: no run declared (tps_begin_run)", p->s);
+  if (p->pos >= p->order.size()) return fail(TPS_E_ORDER, "stage %d: run already complete", p->s);
+  const tps_event& e = p->order[p->pos];
+  static const char* kn[3] = {"F", "B", "U"};
+  if (e.kind != kind || e.mb != mb || (kind == TPS_EV_F && (e.micro != micro || e.micro_count != count)))
+    return fail(TPS_E_ORDER, "stage %d: got %s(mb=%lld, micro=%d, count=%d), next static event is %s(mb=%lld, micro=%d, count=%d)",
+                p->s, kn[kind], (long long)mb, micro, count, kn[e.kind], (long long)e.mb, e.micro, e.micro_count);
+  return TPS_OK;
+}
+
+void advance(tps_pipeline* p) {
+  p->pos += 1;
+  if (p->pos == p->order.size()) p->in_run = false;
+}
+
+void update_stash_peak(tps_pipeline* p) {
+  // live versions = latest + distinct versions referenced by forwarded-but-not-backwarded mbs
+  std::vector<int64_t> live{p->latest};
+  for (auto& kv : p->fwd_version)
+    if (std::find(live.begin(), live.end(), kv.second) == live.end()) live.push_back(kv.second);
+  const int64_t stash = static_cast<int64_t>(live.size() - 1) * p->ver_bytes;
+  p->peak_stash_live = std::max(p->peak_stash_live, stash);
+}
+
+// ------------------------------------------------------------------ the three events
+tps_status do_forward(tps_pipeline* p, int64_t j, int a0, int cnt, const void* x, const int32_t* labels) {
+  TPS_TRY(expect(p, TPS_EV_F, j, a0, cnt));
+  if (p->first && !x) return fail(TPS_E_INVALID_ARG, "stage 0 forward needs x");
+  if (p->last && !labels) return fail(TPS_E_INVALID_ARG, "last stage forward needs labels");
+  const int grp = a0 / p->g;
+  const int r0 = a0 * p->bsz, nr = cnt * p->bsz;
+  const int64_t v = p->latest;
+  if (a0 == 0) p->fwd_version[j] = v;
+  const int slot0 = static_cast<int>(j % p->A0);
+  const int slot = static_cast<int>(j % p->Kmax);
+  Layer& L0 = p->layers[0];
+  uint16_t* X = p->act[slot0][0] + static_cast<size_t>(r0) * L0.Kp;
+  if (p->first) {
+    const size_t w = static_cast<size_t>(L0.in) * 2;
+    CUDA_OK(cudaMemcpy2DAsync(X, static_cast<size_t>(L0.Kp) * 2, x, w, w, nr, cudaMemcpyDefault, p->cs));
+  } else {
+    TPS_TRY(recv_fwd(p, j, grp, X, static_cast<size_t>(nr) * L0.Kp * 2));
+  }
+  if (!p->last) {  // the send buffer of mb j-2 must have left
+    CUDA_OK(cudaStreamWaitEvent(p->cs, p->ev_fwd_sent[static_cast<int>(j & 1) * p->ng + grp], 0));
+  }
+  const int nl = p->nlayers();
+  const uint16_t* Xin = X;
+  for (int k = 0; k < nl; ++k) {
+    Layer& Lk = p->layers[k];
+    tps::GemmOperands op{Xin, Lk.Kp, Lk.ver[v % p->R], Lk.Kp, nullptr};
+    tps::GemmArgs ga{};
+    ga.M = nr; ga.N = Lk.Np; ga.K = Lk.Kp; ga.alpha = 1.f; ga.bias = Lk.b; ga.xa = 1.f; ga.xb = 0.f;
+    void* out;
+    if (k < nl - 1) {
+      out = p->act[slot][k + 1] + static_cast<size_t>(r0) * Lk.Np;
+      ga.relu = 1;
+    } else if (!p->last) {
+      out = p->send_fwd[j & 1] + static_cast<size_t>(r0) * Lk.Np;
+      ga.relu = 1;
+    } else {
+      out = p->logits + static_cast<size_t>(r0) * Lk.Np;
+      ga.relu = 0;
+      ga.out_f32 = 1;
+    }
+    ga.out = out; ga.ldo = Lk.Np;
+    TPS_TRY(run_gemm(p, tps::GEMM_FWD, op, ga, 0));
+    Xin = static_cast<const uint16_t*>(out);
+  }
+  if (p->last) {
+    Layer& Ll = p->layers[nl - 1];
+    const int32_t* lab = labels;
+    if (is_host_ptr(labels)) {
+      CUDA_OK(cudaMemcpyAsync(p->labels_dev + r0, labels, static_cast<size_t>(nr) * 4, cudaMemcpyHostToDevice, p->cs));
+      lab = p->labels_dev + r0;
+    }
+    CUDA_OK(tps::launch_softmax_xent(p->logits + static_cast<size_t>(r0) * Ll.Np, Ll.Np, lab, nr, p->classes, p->B,
+                                     p->loss_rows + r0, p->gce + static_cast<size_t>(r0) * Ll.Np, Ll.Np, p->cs));
+    p->launches += 1;
+    if (a0 + cnt == p->m) {
+      if (p->loss_count >= p->loss_cap) return fail(TPS_E_STATE, "loss buffer full (%lld mini-batches)", (long long)p->loss_cap);
+      CUDA_OK(tps::launch_loss_mean(p->loss_rows, p->B, p->losses, p->loss_count, p->cs));
+      p->loss_count += 1;
+      p->launches += 1;
+    }
+  } else {
+    Layer& Ll = p->layers[nl - 1];
+    TPS_TRY(send_fwd(p, j, grp, p->send_fwd[j & 1] + static_cast<size_t>(r0) * Ll.Np,
+                     static_cast<size_t>(nr) * Ll.Np * 2));
+  }
+  tps_event e{};
+  e.stage = p->s; e.kind = TPS_EV_F; e.micro = a0; e.micro_count = cnt; e.mb = j;
+  e.v_used = v; e.v_latest = v; e.delta = 0; e.alpha = 1.f; e.beta = 0.f;
+  p->trace.push_back(e);
+  p->fwd_groups_done[j] += 1;
+  update_stash_peak(p);
+  advance(p);
+  return TPS_OK;
+}
+
+tps_status do_backward(tps_pipeline* p, int64_t j, int staleness) {
+  TPS_TRY(expect(p, TPS_EV_B, j, -1, 0));
+  auto fv = p->fwd_version.find(j);
+  if (fv == p->fwd_version.end()) return fail(TPS_E_ORDER, "backward of mb %lld without its forward", (long long)j);
+  const int64_t vf = fv->second, vl = p->latest;
+  const int64_t dlog = vl - vf;
+  int64_t delta, v_used;
+  if (p->variant == TPS_V) {
+    delta = 0;          // V reads the latest weights: zero staleness
+    v_used = vl;
+    if (staleness > 0) return fail(TPS_E_STALENESS, "V-TiMePReSt has no stash (requested staleness %d)", staleness);
+  } else {
+    delta = staleness >= 0 ? staleness : dlog;
+    if (staleness >= 0 && staleness != dlog)
+      return fail(TPS_E_STALENESS, "explicit staleness %d != logged %lld for mb %lld", staleness, (long long)dlog, (long long)j);
+    v_used = vl - delta;
+    if (v_used < 0 || v_used < vl - p->R + 1) return fail(TPS_E_STALENESS, "no live stash for staleness %lld", (long long)delta);
+  }
+  float alpha, beta;
+  compute_coeffs(p->variant, p->blend, static_cast<int>(delta), p->lambda, &alpha, &beta);
+  const int nl = p->nlayers();
+  Layer& Ll = p->layers[nl - 1];
+  const uint16_t* G;
+  if (p->last) {
+    G = p->gce;
+  } else {
+    TPS_TRY(recv_bwd(p, j, p->gin[j & 1], static_cast<size_t>(p->B) * Ll.Np * 2));
+    G = p->gin[j & 1];
+  }
+  const int slot0 = static_cast<int>(j % p->A0);
+  const int slot = static_cast<int>(j % p->Kmax);
+  int wbuf = 0;
+  for (int k = nl - 1; k >= 0; --k) {
+    Layer& Lk = p->layers[k];
+    const uint16_t* X = (k == 0) ? p->act[slot0][0] : p->act[slot][k];
+    // wgrad: dW[Np, Kp] = Gᵀ·X   (A = G stored [B, Np], B = X stored [B, Kp])
+    {
+      tps::GemmOperands op{G, Lk.Np, X, Lk.Kp, nullptr};
+      tps::GemmArgs ga{};
+      ga.M = Lk.Np; ga.N = Lk.Kp; ga.K = p->B; ga.out = Lk.dW; ga.ldo = Lk.Kp; ga.out_f32 = 1;
+      ga.alpha = 1.f; ga.xa = 1.f;
+      TPS_TRY(run_gemm(p, tps::GEMM_WGRAD, op, ga, 2));
+    }
+    CUDA_OK(tps::launch_bias_grad(G, p->B, Lk.Np, Lk.Np, Lk.db, p->scratch, p->cs));
+    p->launches += 2;
+    if (Lk.gidx == 0) break;  // the network's first layer has no dgrad
+    uint16_t* dst;
+    if (k > 0) {
+      dst = p->gwork[wbuf];
+      wbuf ^= 1;
+    } else {
+      CUDA_OK(cudaStreamWaitEvent(p->cs, p->ev_bwd_sent[j & 1], 0));  // gout of mb j-2 has left
+      dst = p->gout[j & 1];
+    }
+    const uint16_t* Ws = Lk.ver[v_used % p->R];
+    const uint16_t* Wl = Lk.ver[vl % p->R];
+    tps::GemmArgs ga{};
+    ga.M = p->B; ga.N = Lk.Kp; ga.K = Lk.Np; ga.out = dst; ga.ldo = Lk.Kp; ga.out_f32 = 0;
+    ga.mask = X; ga.ldm = Lk.Kp; ga.alpha = 1.f; ga.xa = 1.f; ga.xb = 0.f;
+    const bool blend_on_load = p->variant == TPS_I && delta > 0 && (p->blend == TPS_BLEND_CONVEX || p->eq1_on_load);
+    if (blend_on_load) {
+      tps::GemmOperands op{G, Lk.Np, Ws, Lk.Kp, Wl};
+      ga.xa = alpha; ga.xb = beta;
+      TPS_TRY(run_gemm(p, tps::GEMM_DGRAD_BLEND, op, ga, 1));
+    } else {
+      tps::GemmOperands op{G, Lk.Np, Ws, Lk.Kp, nullptr};
+      ga.alpha = (p->variant == TPS_I) ? alpha : 1.f;   // EQ1: α·(G·W_stash) = G·(α·W_stash)
+      TPS_TRY(run_gemm(p, tps::GEMM_DGRAD, op, ga, 1));
+    }
+    G = dst;
+  }
+  // the input slot and the received gradient buffer may now be refilled
+  CUDA_OK(cudaEventRecord(p->ev_act_free[slot0], p->cs));
+  if (!p->last) CUDA_OK(cudaEventRecord(p->ev_gin_free[j & 1], p->cs));
+  if (!p->first) {
+    TPS_TRY(send_bwd(p, j, p->gout[j & 1], static_cast<size_t>(p->B) * p->layers[0].Kp * 2));
+  }
+  tps_event e{};
+  e.stage = p->s; e.kind = TPS_EV_B; e.micro = -1; e.mb = j;
+  e.v_used = v_used; e.v_latest = vl; e.delta = static_cast<int32_t>(delta); e.alpha = alpha; e.beta = beta;
+  p->trace.push_back(e);
+  p->fwd_version.erase(j);
+  p->fwd_groups_done.erase(j);
+  p->pending_update = j;
+  advance(p);
+  return TPS_OK;
+}
+
+tps_status do_update(tps_pipeline* p, int64_t j) {
+  TPS_TRY(expect(p, TPS_EV_U, j, -1, 0));
+  if (p->pending_update != j) return fail(TPS_E_ORDER, "update of mb %lld without its backward", (long long)j);
+  const int64_t vn = p->latest + 1;
+  for (auto& Lk : p->layers) {
+    const int64_t n = static_cast<int64_t>(Lk.Np) * Lk.Kp;
+    TimedLaunch tl{};
+    TPS_TRY(time_begin(p, &tl, 4, (p->mu != 0.f ? 22.0 : 14.0) * n));
+    CUDA_OK(tps::launch_sgd_update(Lk.W, Lk.mW, Lk.dW, Lk.ver[vn % p->R], n, p->lr, p->mu, p->wd, p->cs));
+    TPS_TRY(time_end(p, &tl));
+    CUDA_OK(tps::launch_sgd_update(Lk.b, Lk.mb, Lk.db, nullptr, Lk.Np, p->lr, p->mu, p->wd, p->cs));
+    p->launches += 2;
+  }
+  tps_event e{};
+  e.stage = p->s; e.kind = TPS_EV_U; e.micro = -1; e.mb = j;
+  e.v_used = p->latest; e.v_latest = vn; e.alpha = 1.f;
+  p->trace.push_back(e);
+  p->latest = vn;
+  p->pending_update = -1;
+  update_stash_peak(p);
+  advance(p);
+  return TPS_OK;
+}
+
+tps_status begin_run(tps_pipeline* p, int64_t first, int64_t n) {
+  if (n <= 0 || first < 0) return fail(TPS_E_INVALID_ARG, "bad run [%lld, +%lld)", (long long)first, (long long)n);
+  if (p->in_run) return fail(TPS_E_ORDER, "stage %d: previous run not finished", p->s);
+  build_order(p->S, p->s, p->m, p->g, first, n, &p->order);
+  p->pos = 0;
+  p->run_first = first;
+  p->run_n = n;
+  p->in_run = true;
+  return TPS_OK;
+}
+
+tps_status fire(tps_pipeline* p, const tps_event& e, const void* x_pool, const int32_t* y_pool, int pool) {
+  if (e.kind == TPS_EV_F) {
+    const int64_t slot = e.mb % pool;
+    const void* x = nullptr;
+    const int32_t* y = nullptr;
+    if (p->first)
+      x = static_cast<const uint16_t*>(x_pool) + (slot * p->B + static_cast<int64_t>(e.micro) * p->bsz) * p->dims[0];
+    if (p->last) y = y_pool + slot * p->B + static_cast<int64_t>(e.micro) * p->bsz;
+    return do_forward(p, e.mb, e.micro, e.micro_count, x, y);
+  }
+  if (e.kind == TPS_EV_B) return do_backward(p, e.mb, -1);
+  return do_update(p, e.mb);
+}
+
+}  // namespace
+
+// ======================================================================== C ABI
+extern "C" {
+
+int32_t tps_abi_version(void) { return TPS_ABI_VERSION; }
+const char* tps_last_error(void) { return g_err.c_str(); }
+
+tps_status tps_nccl_unique_id(void* out128) {
+  if (!out128) return fail(TPS_E_INVALID_ARG, "null out");
+  ncclUniqueId id;
+  NCCL_OK(ncclGetUniqueId(&id));
+  std::memcpy(out128, &id, sizeof(id));
+  return TPS_OK;
+}
+
+tps_status tps_blend_coeffs(int32_t variant, int32_t blend, int32_t staleness, double lambda, float* alpha, float* beta) {
+  if (!alpha || !beta) return fail(TPS_E_INVALID_ARG, "null out");
+  if (staleness < 0) return fail(TPS_E_INVALID_ARG, "staleness must be >= 0 (P:211)");
+  if (variant != TPS_V && variant != TPS_I) return fail(TPS_E_INVALID_ARG, "bad variant");
+  if (variant == TPS_I && !(lambda > 0)) return fail(TPS_E_CONFIG, "lambda must be > 0 (P:227)");
+  if (blend != TPS_BLEND_EQ1 && blend != TPS_BLEND_CONVEX) return fail(TPS_E_INVALID_ARG, "bad blend");
+  compute_coeffs(variant, blend, staleness, lambda, alpha, beta);
+  return TPS_OK;
+}
+
+tps_status tps_schedule_events(int32_t S, int32_t s, int32_t m, int32_t fwd_group, int64_t M, tps_event* out,
+                               int64_t cap, int64_t* n) {
+  if (S < 1 || s < 0 || s >= S || m < 1 || M < 0 || !n) return fail(TPS_E_INVALID_ARG, "bad schedule arguments");
+  const int g = fwd_group <= 0 ? m : fwd_group;
+  if (m % g) return fail(TPS_E_CONFIG, "fwd_group must divide m");
+  std::vector<tps_event> ev;
+  if (M > 0) build_order(S, s, m, g, 0, M, &ev);
+  *n = static_cast<int64_t>(ev.size());
+  if (out) std::memcpy(out, ev.data(), sizeof(tps_event) * static_cast<size_t>(std::min<int64_t>(cap, *n)));
+  return TPS_OK;
+}
+
+tps_status tps_pipeline_init(const tps_config* c, tps_pipeline** out) {
+  if (!c || !out) return fail(TPS_E_INVALID_ARG, "null argument");
+  *out = nullptr;
+  if (c->num_layers < 1 || !c->dims || !c->stage_bounds) return fail(TPS_E_CONFIG, "need >= 1 layer, dims and stage_bounds");
+  if (c->num_stages < 1) return fail(TPS_E_CONFIG, "num_stages must be >= 1");
+  if (c->stage_id < 0 || c->stage_id >= c->num_stages) return fail(TPS_E_CONFIG, "stage_id out of range");
+  if (c->micro_batches < 1 || c->micro_batch_size < 1) return fail(TPS_E_CONFIG, "m and b must be >= 1");
+  if (c->variant != TPS_V && c->variant != TPS_I) return fail(TPS_E_CONFIG, "bad variant");
+  if (c->blend != TPS_BLEND_EQ1 && c->blend != TPS_BLEND_CONVEX) return fail(TPS_E_CONFIG, "bad blend");
+  if (c->variant == TPS_I && !(c->lambda > 0)) return fail(TPS_E_CONFIG, "lambda must be > 0 (P:227)");
+  for (int l = 0; l <= c->num_layers; ++l)
+    if (c->dims[l] < 1) return fail(TPS_E_CONFIG, "dims[%d] < 1", l);
+  if (c->stage_bounds[0] != 0 || c->stage_bounds[c->num_stages] != c->num_layers)
+    return fail(TPS_E_CONFIG, "stage_bounds must start at 0 and end at num_layers");
+  for (int s = 0; s < c->num_stages; ++s)
+    if (c->stage_bounds[s + 1] <= c->stage_bounds[s]) return fail(TPS_E_CONFIG, "stage %d owns no layer", s);
+  const int g = c->fwd_group <= 0 ? c->micro_batches : c->fwd_group;
+  if (c->micro_batches % g) return fail(TPS_E_CONFIG, "fwd_group must divide micro_batches");
+  if (c->num_stages > 1 && c->transport == TPS_TRANSPORT_NONE) return fail(TPS_E_CONFIG, "S > 1 needs a transport");
+  if (c->transport == TPS_TRANSPORT_NCCL && c->num_stages > 1 && !c->nccl_ids) return fail(TPS_E_CONFIG, "NCCL transport needs ids");
+  TPS_TRY(check_arch(c->device));
+  CUDA_OK(cudaSetDevice(c->device));
+
+  tps_pipeline* p = new tps_pipeline();
+  p->S = c->num_stages; p->s = c->stage_id; p->m = c->micro_batches; p->bsz = c->micro_batch_size;
+  p->B = p->m * p->bsz; p->g = g; p->ng = p->m / g;
+  p->variant = c->variant; p->blend = c->blend; p->lambda = c->lambda;
+  p->lr = c->lr; p->mu = c->momentum; p->wd = c->weight_decay;
+  p->transport = c->num_stages == 1 ? TPS_TRANSPORT_NONE : c->transport;
+  p->device = c->device; p->seed = c->seed;
+  p->first = p->s == 0; p->last = p->s == p->S - 1;
+  p->dims.assign(c->dims, c->dims + c->num_layers + 1);
+  p->classes = c->dims[c->num_layers];
+  p->Kmax = p->S - p->s;                         // in-flight mini-batches (reading Z6)
+  p->R = (p->variant == TPS_I) ? p->Kmax : 1;    // weight version ring
+  p->A0 = p->Kmax + ((c->extra_recv_slot && !p->first) ? 1 : 0);
+  const char* env = std::getenv("TPS_EQ1_ON_LOAD");
+  p->eq1_on_load = env && env[0] == '1';
+
+  auto cleanup = [&](tps_status st) {
+    tps_pipeline_destroy(p);
+    return st;
+  };
+  const int lb = c->stage_bounds[p->s], le = c->stage_bounds[p->s + 1];
+  int maxd = 0;
+  for (int l = lb; l < le; ++l) {
+    Layer L;
+    L.gidx = l; L.in = c->dims[l]; L.out = c->dims[l + 1]; L.Kp = pad16(L.in); L.Np = pad16(L.out);
+    maxd = std::max({maxd, L.Kp, L.Np});
+    const size_t n = static_cast<size_t>(L.Np) * L.Kp;
+    tps_status st;
+    if ((st = alloc_t(p, &L.W, n, &p->mem_weights)) != TPS_OK) return cleanup(st);
+    if ((st = alloc_t(p, &L.b, L.Np, &p->mem_weights)) != TPS_OK) return cleanup(st);
+    if (p->mu != 0.f) {
+      if ((st = alloc_t(p, &L.mW, n, &p->mem_optim)) != TPS_OK) return cleanup(st);
+      if ((st = alloc_t(p, &L.mb, L.Np, &p->mem_optim)) != TPS_OK) return cleanup(st);
+    }
+    if ((st = alloc_t(p, &L.dW, n, &p->mem_optim)) != TPS_OK) return cleanup(st);
+    if ((st = alloc_t(p, &L.db, L.Np, &p->mem_optim)) != TPS_OK) return cleanup(st);
+    L.ver.resize(p->R);
+    for (int r = 0; r < p->R; ++r)
+      if ((st = alloc_t(p, &L.ver[r], n, r == 0 ? &p->mem_weights : &p->mem_stash)) != TPS_OK) return cleanup(st);
+    p->ver_bytes += static_cast<int64_t>(n) * 2;
+    p->layers.push_back(L);
+  }
+  const int nl = p->nlayers();
+  tps_status st;
+  p->act.assign(std::max(p->A0, p->Kmax), std::vector<uint16_t*>(nl, nullptr));
+  for (int slot = 0; slot < static_cast<int>(p->act.size()); ++slot)
+    for (int k = 0; k < nl; ++k) {
+      const bool need = (k == 0) ? slot < p->A0 : slot < p->Kmax;
+      if (need && (st = alloc_t(p, &p->act[slot][k], static_cast<size_t>(p->B) * p->layers[k].Kp, &p->mem_acts)) != TPS_OK)
+        return cleanup(st);
+    }
+  const int NpL = p->layers[nl - 1].Np, Kp0 = p->layers[0].Kp;
+  for (int i = 0; i < 2; ++i) {
+    if (!p->last) {
+      if ((st = alloc_t(p, &p->send_fwd[i], static_cast<size_t>(p->B) * NpL, &p->mem_comm)) != TPS_OK) return cleanup(st);
+      if ((st = alloc_t(p, &p->gin[i], static_cast<size_t>(p->B) * NpL, &p->mem_comm)) != TPS_OK) return cleanup(st);
+    }
+    if (!p->first && (st = alloc_t(p, &p->gout[i], static_cast<size_t>(p->B) * Kp0, &p->mem_comm)) != TPS_OK) return cleanup(st);
+    if (nl > 1 && (st = alloc_t(p, &p->gwork[i], static_cast<size_t>(p->B) * maxd, &p->mem_acts)) != TPS_OK) return cleanup(st);
+  }
+  if (p->last) {
+    if ((st = alloc_t(p, &p->logits, static_cast<size_t>(p->B) * NpL, &p->mem_acts)) != TPS_OK) return cleanup(st);
+    if ((st = alloc_t(p, &p->gce, static_cast<size_t>(p->B) * NpL, &p->mem_acts)) != TPS_OK) return cleanup(st);
+    if ((st = alloc_t(p, &p->loss_rows, p->B, &p->mem_acts)) != TPS_OK) return cleanup(st);
+    if ((st = alloc_t(p, &p->labels_dev, p->B, &p->mem_acts)) != TPS_OK) return cleanup(st);
+    p->loss_cap = 1 << 20;
+    if ((st = alloc_t(p, &p->losses, p->loss_cap, &p->mem_acts)) != TPS_OK) return cleanup(st);
+  }
+  int64_t scr = 0;
+  for (auto& L : p->layers) scr = std::max(scr, tps::bias_grad_scratch_floats(p->B, L.Np));
+  if ((st = alloc_t(p, &p->scratch, scr, &p->mem_optim)) != TPS_OK) return cleanup(st);
+
+  // streams and events
+  if (c->compute_stream) {
+    p->cs = reinterpret_cast<cudaStream_t>(c->compute_stream);
+  } else {
+    if (cudaStreamCreateWithFlags(&p->cs, cudaStreamNonBlocking) != cudaSuccess) return cleanup(fail(TPS_E_CUDA, "stream create"));
+    p->own_cs = true;
+  }
+  for (cudaStream_t* sp : {&p->s_fin, &p->s_fout, &p->s_bin, &p->s_bout})
+    if (cudaStreamCreateWithFlags(sp, cudaStreamNonBlocking) != cudaSuccess) return cleanup(fail(TPS_E_CUDA, "stream create"));
+  p->ev_fwd_ready.resize(2 * p->ng);
+  p->ev_fwd_sent.resize(2 * p->ng);
+  for (int i = 0; i < 2 * p->ng; ++i) {
+    p->ev_fwd_ready[i] = new_event();
+    p->ev_fwd_sent[i] = new_event();
+  }
+  p->ev_act_free.resize(p->A0);
+  for (auto& e : p->ev_act_free) e = new_event();
+  p->ev_recv = new_event();
+  p->ev_gout_ready = new_event();
+  p->ev_gin_ready = new_event();
+  for (int i = 0; i < 2; ++i) {
+    p->ev_gin_free[i] = new_event();
+    p->ev_bwd_sent[i] = new_event();
+  }
+
+  // NCCL edge communicators: edge e has a forward comm (ids[2e]) and a backward comm
+  // (ids[2e+1]); in both, stage e is rank 0 and stage e+1 is rank 1.  Edges are joined
+  // in increasing order so the blocking inits of neighbours pair up without deadlock.
+  if (p->transport == TPS_TRANSPORT_NCCL) {
+    const ncclUniqueId* ids = static_cast<const ncclUniqueId*>(c->nccl_ids);
+    ncclResult_t r;
+    if (!p->first) {
+      const int e = p->s - 1;
+      if ((r = ncclCommInitRank(&p->c_fin, 2, ids[2 * e], 1)) != ncclSuccess) return cleanup(fail(TPS_E_NCCL, "init fin: %s", ncclGetErrorString(r)));
+      if ((r = ncclCommInitRank(&p->c_bout, 2, ids[2 * e + 1], 1)) != ncclSuccess) return cleanup(fail(TPS_E_NCCL, "init bout: %s", ncclGetErrorString(r)));
+    }
+    if (!p->last) {
+      const int e = p->s;
+      if ((r = ncclCommInitRank(&p->c_fout, 2, ids[2 * e], 0)) != ncclSuccess) return cleanup(fail(TPS_E_NCCL, "init fout: %s", ncclGetErrorString(r)));
+      if ((r = ncclCommInitRank(&p->c_bin, 2, ids[2 * e + 1], 0)) != ncclSuccess) return cleanup(fail(TPS_E_NCCL, "init bin: %s", ncclGetErrorString(r)));
+    }
+  }
+  if (cudaDeviceSynchronize() != cudaSuccess) return cleanup(fail(TPS_E_CUDA, "init sync: %s", cudaGetErrorString(cudaGetLastError())));
+  *out = p;
+  return TPS_OK;
+}
+
+tps_status tps_pipeline_destroy(tps_pipeline* p) {
+  if (!p) return TPS_OK;
+  cudaSetDevice(p->device);
+  cudaDeviceSynchronize();
+  for (ncclComm_t c : {p->c_fin, p->c_fout, p->c_bin, p->c_bout})
+    if (c) ncclCommDestroy(c);
+  for (void* a : p->allocs) cudaFree(a);
+  auto kill_ev = [](cudaEvent_t e) { if (e) cudaEventDestroy(e); };
+  for (auto e : p->ev_fwd_ready) kill_ev(e);
+  for (auto e : p->ev_fwd_sent) kill_ev(e);
+  for (auto e : p->ev_act_free) kill_ev(e);
+  for (auto e : p->ev_pool) kill_ev(e);
+  for (auto& t : p->timed) { kill_ev(t.a); kill_ev(t.b); }
+  for (cudaEvent_t e : {p->ev_recv, p->ev_gout_ready, p->ev_gin_ready, p->ev_gin_free[0], p->ev_gin_free[1],
+                        p->ev_bwd_sent[0], p->ev_bwd_sent[1]})
+    kill_ev(e);
+  for (cudaStream_t s : {p->s_fin, p->s_fout, p->s_bin, p->s_bout})
+    if (s) cudaStreamDestroy(s);
+  if (p->own_cs && p->cs) cudaStreamDestroy(p->cs);
+  if (p->prev_local) p->prev_local->next_local = nullptr;
+  if (p->next_local) p->next_local->prev_local = nullptr;
+  delete p;
+  return TPS_OK;
+}
+
+tps_status tps_local_link(tps_pipeline* const* st, int32_t n) {
+  if (!st || n < 1) return fail(TPS_E_INVALID_ARG, "bad stage list");
+  for (int i = 0; i < n; ++i) {
+    if (!st[i]) return fail(TPS_E_INVALID_ARG, "null stage %d", i);
+    if (st[i]->s != i || st[i]->S != n) return fail(TPS_E_CONFIG, "handle %d is stage %d of %d", i, st[i]->s, st[i]->S);
+    if (n > 1 && st[i]->transport != TPS_TRANSPORT_LOCAL) return fail(TPS_E_CONFIG, "stage %d is not LOCAL transport", i);
+  }
+  for (int i = 0; i < n; ++i) {
+    st[i]->prev_local = i > 0 ? st[i - 1] : nullptr;
+    st[i]->next_local = i + 1 < n ? st[i + 1] : nullptr;
+  }
+  return TPS_OK;
+}
+
+tps_status tps_begin_run(tps_pipeline* p, int64_t first_mb, int64_t n_mb) {
+  TPS_TRY(check_usable(p));
+  return begin_run(p, first_mb, n_mb);
+}
+
+tps_status tps_stage_forward(tps_pipeline* p, int64_t mb, int32_t micro, int32_t count, const void* x,
+                             const int32_t* labels) {
+  TPS_TRY(check_usable(p));
+  return do_forward(p, mb, micro, count, x, labels);
+}
+
+tps_status tps_stage_backward(tps_pipeline* p, int64_t mb, int32_t staleness) {
+  TPS_TRY(check_usable(p));
+  return do_backward(p, mb, staleness);
+}
+
+tps_status tps_stage_update(tps_pipeline* p, int64_t mb) {
+  TPS_TRY(check_usable(p));
+  return do_update(p, mb);
+}
+
+tps_status tps_run_schedule(tps_pipeline* p, int64_t first_mb, int64_t n_mb, const void* x_pool, const int32_t* y_pool,
+                            int32_t pool) {
+  TPS_TRY(check_usable(p));
+  if (p->transport == TPS_TRANSPORT_LOCAL) return fail(TPS_E_CONFIG, "LOCAL transport: use tps_run_schedule_local");
+  if (pool < 1) return fail(TPS_E_INVALID_ARG, "pool must be >= 1");
+  if ((p->first && !x_pool) || (p->last && !y_pool)) return fail(TPS_E_INVALID_ARG, "missing input pool");
+  TPS_TRY(begin_run(p, first_mb, n_mb));
+  while (p->in_run) {
+    const tps_event e = p->order[p->pos];
+    TPS_TRY(fire(p, e, x_pool, y_pool, pool));
+  }
+  return TPS_OK;
+}
+
+tps_status tps_run_schedule_local(tps_pipeline* const* st, int32_t S, int64_t first_mb, int64_t n_mb,
+                                  const void* x_pool, const int32_t* y_pool, int32_t pool) {
+  if (!st || S < 1 || pool < 1) return fail(TPS_E_INVALID_ARG, "bad arguments");
+  for (int s = 0; s < S; ++s) {
+    TPS_TRY(check_usable(st[s]));
+    TPS_TRY(begin_run(st[s], first_mb, n_mb));
+  }
+  // Round-robin over stages; fire a stage's next static event once its cross-stage
+  // input has been enqueued and the buffer it overwrites has been consumed downstream.
+  std::vector<int64_t> fcount(S, 0), bcount(S, 0);
+  const int ng = st[0]->ng;
+  for (;;) {
+    bool all_done = true, progress = false;
+    for (int s = 0; s < S; ++s) {
+      tps_pipeline* p = st[s];
+      if (!p->in_run) continue;
+      all_done = false;
+      const tps_event e = p->order[p->pos];
+      const int64_t jr = e.mb - first_mb;
+      if (e.kind == TPS_EV_F) {
+        const int grp = e.micro / p->g;
+        const int64_t idx = jr * ng + grp;
+        if (s > 0 && fcount[s - 1] <= idx) continue;                          // input not produced
+        if (s < S - 1 && jr >= 2 && fcount[s + 1] <= (jr - 2) * ng + grp) continue;  // send buffer busy
+      } else if (e.kind == TPS_EV_B) {
+        if (s < S - 1 && bcount[s + 1] <= jr) continue;                      // gradient not produced
+        if (s > 0 && jr >= 2 && bcount[s - 1] <= jr - 2) continue;           // gout buffer busy
+      }
+      TPS_TRY(fire(p, e, x_pool, y_pool, pool));
+      if (e.kind == TPS_EV_F) fcount[s] += 1;
+      if (e.kind == TPS_EV_B) bcount[s] += 1;
+      progress = true;
+    }
+    if (all_done) break;
+    if (!progress) return fail(TPS_E_STATE, "local schedule deadlock");
+  }
+  return TPS_OK;
+}
+
+tps_status tps_synchronize(tps_pipeline* p) {
+  if (!p) return fail(TPS_E_INVALID_ARG, "null handle");
+  if (p->poisoned) return fail(TPS_E_STATE, "handle poisoned");
+  cudaSetDevice(p->device);
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    p->poisoned = true;
+    return fail(TPS_E_CUDA, "device error: %s", cudaGetErrorString(e));
+  }
+  for (ncclComm_t c : {p->c_fin, p->c_fout, p->c_bin, p->c_bout}) {
+    if (!c) continue;
+    ncclResult_t ar = ncclSuccess;
+    ncclCommGetAsyncError(c, &ar);
+    if (ar != ncclSuccess) {
+      p->poisoned = true;
+      return fail(TPS_E_NCCL, "async NCCL error: %s", ncclGetErrorString(ar));
+    }
+  }
+  return drain_timing(p);
+}
+
+tps_status tps_stash_info(tps_pipeline* p, int32_t* live, int64_t* stash, int64_t* peak) {
+  if (!p) return fail(TPS_E_INVALID_ARG, "null handle");
+  std::vector<int64_t> lv{p->latest};
+  for (auto& kv : p->fwd_version)
+    if (std::find(lv.begin(), lv.end(), kv.second) == lv.end()) lv.push_back(kv.second);
+  if (live) *live = static_cast<int32_t>(lv.size());
+  if (stash) *stash = static_cast<int64_t>(lv.size() - 1) * p->ver_bytes;
+  if (peak) *peak = p->peak_stash_live;
+  return TPS_OK;
+}
+
+tps_status tps_intermediate_weight(tps_pipeline* p, int32_t layer, int32_t staleness, void* out_bf16) {
+  TPS_TRY(check_usable(p));
+  if (layer < 0 || layer >= p->nlayers() || !out_bf16) return fail(TPS_E_INVALID_ARG, "bad layer/out");
+  if (staleness < 0 || staleness > p->latest || staleness >= p->R) return fail(TPS_E_STALENESS, "no live stash for staleness %d", staleness);
+  float a, b;
+  compute_coeffs(p->variant, p->blend, staleness, p->lambda, &a, &b);
+  Layer& L = p->layers[layer];
+  const int64_t vs = p->latest - staleness;
+  CUDA_OK(tps::launch_blend_materialize(L.ver[vs % p->R], L.ver[p->latest % p->R], static_cast<uint16_t*>(out_bf16),
+                                        static_cast<int64_t>(L.Np) * L.Kp, a, b, p->cs));
+  p->launches += 1;
+  return TPS_OK;
+}
+
+tps_status tps_get_version(tps_pipeline* p, int32_t layer, int32_t staleness, void* out_bf16) {
+  TPS_TRY(check_usable(p));
+  if (layer < 0 || layer >= p->nlayers() || !out_bf16) return fail(TPS_E_INVALID_ARG, "bad layer/out");
+  if (staleness < 0 || staleness > p->latest || staleness >= p->R) return fail(TPS_E_STALENESS, "no live version at staleness %d", staleness);
+  Layer& L = p->layers[layer];
+  CUDA_OK(cudaMemcpyAsync(out_bf16, L.ver[(p->latest - staleness) % p->R], static_cast<size_t>(L.Np) * L.Kp * 2,
+                          cudaMemcpyDeviceToDevice, p->cs));
+  CUDA_OK(cudaStreamSynchronize(p->cs));
+  return TPS_OK;
+}
+
+tps_status tps_get_weights(tps_pipeline* p, int32_t layer, float* w, float* b, float* mw, float* mb) {
+  TPS_TRY(check_usable(p));
+  if (layer < 0 || layer >= p->nlayers()) return fail(TPS_E_INVALID_ARG, "bad layer %d", layer);
+  CUDA_OK(cudaStreamSynchronize(p->cs));
+  Layer& L = p->layers[layer];
+  const size_t rowb = static_cast<size_t>(L.in) * 4, ldb = static_cast<size_t>(L.Kp) * 4;
+  if (w) CUDA_OK(cudaMemcpy2D(w, rowb, L.W, ldb, rowb, L.out, cudaMemcpyDeviceToHost));
+  if (b) CUDA_OK(cudaMemcpy(b, L.b, static_cast<size_t>(L.out) * 4, cudaMemcpyDeviceToHost));
+  if (mw) {
+    if (L.mW) CUDA_OK(cudaMemcpy2D(mw, rowb, L.mW, ldb, rowb, L.out, cudaMemcpyDeviceToHost));
+    else std::memset(mw, 0, rowb * L.out);
+  }
+  if (mb) {
+    if (L.mb) CUDA_OK(cudaMemcpy(mb, L.mb, static_cast<size_t>(L.out) * 4, cudaMemcpyDeviceToHost));
+    else std::memset(mb, 0, static_cast<size_t>(L.out) * 4);
+  }
+  return TPS_OK;
+}
+
+tps_status tps_set_weights(tps_pipeline* p, int32_t layer, const float* w, const float* b) {
+  TPS_TRY(check_usable(p));
+  if (layer < 0 || layer >= p->nlayers()) return fail(TPS_E_INVALID_ARG, "bad layer %d", layer);
+  CUDA_OK(cudaStreamSynchronize(p->cs));
+  Layer& L = p->layers[layer];
+  const size_t rowb = static_cast<size_t>(L.in) * 4, ldb = static_cast<size_t>(L.Kp) * 4;
+  const size_t n = static_cast<size_t>(L.Np) * L.Kp;
+  if (w) {
+    CUDA_OK(cudaMemset(L.W, 0, n * 4));
+    CUDA_OK(cudaMemcpy2D(L.W, ldb, w, rowb, rowb, L.out, cudaMemcpyHostToDevice));
+  }
+  if (b) {
+    CUDA_OK(cudaMemset(L.b, 0, static_cast<size_t>(L.Np) * 4));
+    CUDA_OK(cudaMemcpy(L.b, b, static_cast<size_t>(L.out) * 4, cudaMemcpyHostToDevice));
+  }
+  if (L.mW) CUDA_OK(cudaMemset(L.mW, 0, n * 4));
+  if (L.mb) CUDA_OK(cudaMemset(L.mb, 0, static_cast<size_t>(L.Np) * 4));
+  CUDA_OK(tps::launch_f32_to_bf16(L.W, L.ver[p->latest % p->R], static_cast<int64_t>(n), p->cs));
+  p->launches += 1;
+  CUDA_OK(cudaStreamSynchronize(p->cs));
+  return TPS_OK;
+}
+
+tps_status tps_init_weights_synthetic(tps_pipeline* p) {
+  TPS_TRY(check_usable(p));
+  for (auto& L : p->layers) {
+    const int shift = static_cast<int>(std::lround(std::log2(std::sqrt(static_cast<double>(L.in)))));
+    CUDA_OK(cudaMemsetAsync(L.W, 0, static_cast<size_t>(L.Np) * L.Kp * 4, p->cs));
+    CUDA_OK(tps::launch_fill_synthetic(3, p->seed, 0x0100 + static_cast<uint64_t>(L.gidx), L.out, L.in, L.Kp, 0, shift,
+                                       L.W, p->cs));
+    CUDA_OK(cudaMemsetAsync(L.b, 0, static_cast<size_t>(L.Np) * 4, p->cs));
+    if (L.mW) CUDA_OK(cudaMemsetAsync(L.mW, 0, static_cast<size_t>(L.Np) * L.Kp * 4, p->cs));
+    if (L.mb) CUDA_OK(cudaMemsetAsync(L.mb, 0, static_cast<size_t>(L.Np) * 4, p->cs));
+    CUDA_OK(tps::launch_f32_to_bf16(L.W, L.ver[p->latest % p->R], static_cast<int64_t>(L.Np) * L.Kp, p->cs));
+    p->launches += 2;
+  }
+  CUDA_OK(cudaStreamSynchronize(p->cs));
+  return TPS_OK;
+}
+
+tps_status tps_get_losses(tps_pipeline* p, float* out, int64_t cap, int64_t* n) {
+  TPS_TRY(check_usable(p));
+  if (!n) return fail(TPS_E_INVALID_ARG, "null n");
+  *n = p->last ? p->loss_count : 0;
+  if (p->last && out && *n > 0) {
+    CUDA_OK(cudaStreamSynchronize(p->cs));
+    CUDA_OK(cudaMemcpy(out, p->losses, sizeof(float) * static_cast<size_t>(std::min(cap, *n)), cudaMemcpyDeviceToHost));
+  }
+  return TPS_OK;
+}
+
+tps_status tps_get_trace(tps_pipeline* p, tps_event* out, int64_t cap, int64_t* n) {
+  if (!p || !n) return fail(TPS_E_INVALID_ARG, "null argument");
+  *n = static_cast<int64_t>(p->trace.size());
+  if (out) std::memcpy(out, p->trace.data(), sizeof(tps_event) * static_cast<size_t>(std::min(cap, *n)));
+  return TPS_OK;
+}
+
+tps_status tps_clear_trace(tps_pipeline* p) {
+  if (!p) return fail(TPS_E_INVALID_ARG, "null handle");
+  p->trace.clear();
+  return TPS_OK;
+}
+
+tps_status tps_memory_stats(tps_pipeline* p, int64_t* weights, int64_t* stash, int64_t* acts, int64_t* optim,
+                            int64_t* comm, int64_t* peak) {
+  if (!p) return fail(TPS_E_INVALID_ARG, "null handle");
+  if (weights) *weights = p->mem_weights;
+  if (stash) *stash = p->mem_stash;
+  if (acts) *acts = p->mem_acts;
+  if (optim) *optim = p->mem_optim;
+  if (comm) *comm = p->mem_comm;
+  if (peak) *peak = p->mem_peak;
+  return TPS_OK;
+}
+
+tps_status tps_set_profiling(tps_pipeline* p, int32_t enable) {
+  TPS_TRY(check_usable(p));
+  CUDA_OK(cudaStreamSynchronize(p->cs));
+  TPS_TRY(drain_timing(p));
+  p->profiling = enable != 0;
+  for (int k = 0; k < 5; ++k) { p->stat_ms[k] = 0; p->stat_work[k] = 0; p->stat_n[k] = 0; }
+  return TPS_OK;
+}
+
+tps_status tps_kernel_stats(tps_pipeline* p, int32_t which, int64_t* launches, double* ms, double* work) {
+  TPS_TRY(check_usable(p));
+  if (which < 0 || which > 4) return fail(TPS_E_INVALID_ARG, "bad kernel class");
+  CUDA_OK(cudaStreamSynchronize(p->cs));
+  TPS_TRY(drain_timing(p));
+  if (launches) *launches = p->stat_n[which];
+  if (ms) *ms = p->stat_ms[which];
+  if (work) *work = p->stat_work[which];
+  return TPS_OK;
+}
+
+tps_status tps_launch_count(tps_pipeline* p, int64_t* n) {
+  if (!p || !n) return fail(TPS_E_INVALID_ARG, "null argument");
+  *n = p->launches;
+  return TPS_OK;
+}
+
+tps_status tps_fill_synthetic(int32_t kind, uint64_t seed, uint64_t tid, int64_t rows, int64_t cols, int32_t classes,
+                              void* dst, uint64_t stream) {
+  if (!dst || rows < 0 || cols < 0 || kind < 0 || kind > 2) return fail(TPS_E_INVALID_ARG, "bad fill arguments");
+  if (kind == 2 && classes < 1) return fail(TPS_E_INVALID_ARG, "classes must be >= 1");
+  int dev = 0;
+  CUDA_OK(cudaGetDevice(&dev));
+  TPS_TRY(check_arch(dev));
+  CUDA_OK(tps::launch_fill_synthetic(kind, seed, tid, rows, cols, cols, classes, 0, dst,
+                                     reinterpret_cast<cudaStream_t>(stream)));
+  return TPS_OK;
+}
+
+tps_status tps_gemm(int32_t mode, int32_t M, int32_t N, int32_t K, const void* A, int32_t lda, const void* B,
+                    int32_t ldb, const void* B2, void* out, int32_t ldo, int32_t out_f32, const float* bias,
+                    int32_t relu, float alpha, float beta, const void* mask, int32_t ldm, uint64_t stream) {
+  if (mode < 0 || mode > 3) return fail(TPS_E_INVALID_ARG, "bad mode");
+  if (M < 0 || N < 0 || K < 0 || !A || !B || !out) return fail(TPS_E_INVALID_ARG, "bad operands");
+  if (N % 8 || ldo % 8 || lda % 8 || ldb % 8 || (mask && ldm % 8)) return fail(TPS_E_INVALID_ARG, "N and leading dims must be multiples of 8");
+  if (mode == 3 && !B2) return fail(TPS_E_INVALID_ARG, "blend mode needs B2");
+  int dev = 0;
+  CUDA_OK(cudaGetDevice(&dev));
+  TPS_TRY(check_arch(dev));
+  tps::GemmOperands op{A, lda, B, ldb, B2};
+  tps::GemmArgs ga{};
+  ga.M = M; ga.N = N; ga.K = K; ga.out = out; ga.ldo = ldo; ga.out_f32 = out_f32; ga.bias = bias; ga.relu = relu;
+  ga.alpha = mode == 3 ? 1.f : alpha; ga.xa = alpha; ga.xb = beta;
+  ga.mask = static_cast<const uint16_t*>(mask); ga.ldm = ldm;
+  CUDA_OK(tps::gemm_run(mode, op, ga, reinterpret_cast<cudaStream_t>(stream)));
+  return TPS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,308 @@
+"""Thin ctypes binding of include/tps.h — argument marshalling only.
+
+Every step of the training path runs inside libtps.so (the sm_100a kernels and the C++
+runtime).  Nothing here computes: if the library is missing the import of `lib()`
+raises, and the library itself refuses to run without an sm_100 device (TPS_E_ARCH) —
+there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "lib", "libtps.so")
+
+TPS_V, TPS_I = 0, 1
+TPS_BLEND_EQ1, TPS_BLEND_CONVEX = 0, 1
+TPS_TRANSPORT_NONE, TPS_TRANSPORT_LOCAL, TPS_TRANSPORT_NCCL = 0, 1, 2
+TPS_EV_F, TPS_EV_B, TPS_EV_U = 0, 1, 2
+GEMM_FWD, GEMM_DGRAD, GEMM_WGRAD, GEMM_DGRAD_BLEND = 0, 1, 2, 3
+STATUS = {0: "TPS_OK", 1: "TPS_E_INVALID_ARG", 2: "TPS_E_CONFIG", 3: "TPS_E_ORDER", 4: "TPS_E_STALENESS",
+          5: "TPS_E_CUDA", 6: "TPS_E_NCCL", 7: "TPS_E_OOM", 8: "TPS_E_ARCH", 9: "TPS_E_STATE",
+          10: "TPS_E_UNSUPPORTED"}
+
+# every symbol include/tps.h declares (tests check the .so exports all of them)
+EXPORTS = [
+    "tps_abi_version", "tps_last_error", "tps_nccl_unique_id", "tps_pipeline_init", "tps_pipeline_destroy",
+    "tps_local_link", "tps_begin_run", "tps_stage_forward", "tps_stage_backward", "tps_stage_update",
+    "tps_run_schedule", "tps_run_schedule_local", "tps_synchronize", "tps_blend_coeffs", "tps_stash_info",
+    "tps_intermediate_weight", "tps_get_version", "tps_schedule_events", "tps_get_weights", "tps_set_weights",
+    "tps_init_weights_synthetic", "tps_get_losses", "tps_get_trace", "tps_clear_trace", "tps_memory_stats",
+    "tps_set_profiling", "tps_kernel_stats", "tps_launch_count", "tps_fill_synthetic", "tps_gemm",
+]
+
+
+class TpsError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class Event(C.Structure):
+    _fields_ = [("stage", C.c_int32), ("kind", C.c_int32), ("micro", C.c_int32), ("micro_count", C.c_int32),
+                ("mb", C.c_int64), ("v_used", C.c_int64), ("v_latest", C.c_int64), ("delta", C.c_int32),
+                ("alpha", C.c_float), ("beta", C.c_float)]
+
+
+class Config(C.Structure):
+    _fields_ = [("num_layers", C.c_int32), ("dims", C.POINTER(C.c_int32)), ("num_stages", C.c_int32),
+                ("stage_bounds", C.POINTER(C.c_int32)), ("stage_id", C.c_int32), ("micro_batches", C.c_int32),
+                ("micro_batch_size", C.c_int32), ("fwd_group", C.c_int32), ("variant", C.c_int32),
+                ("blend", C.c_int32), ("lambda_", C.c_double), ("lr", C.c_float), ("momentum", C.c_float),
+                ("weight_decay", C.c_float), ("transport", C.c_int32), ("nccl_ids", C.c_void_p),
+                ("device", C.c_int32), ("seed", C.c_uint64), ("compute_stream", C.c_uint64),
+                ("extra_recv_slot", C.c_int32), ("reserved", C.c_int32 * 7)]
+
+
+_LIB = None
+
+
+def lib() -> C.CDLL:
+    """Load libtps.so (built by __graft_entry__.build()); raises if it is missing."""
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = C.CDLL(LIB_PATH)
+        P, I32, I64, U64, F, D = C.c_void_p, C.c_int32, C.c_int64, C.c_uint64, C.c_float, C.c_double
+        sig = {
+            "tps_abi_version": (I32, []),
+            "tps_last_error": (C.c_char_p, []),
+            "tps_nccl_unique_id": (I32, [P]),
+            "tps_pipeline_init": (I32, [C.POINTER(Config), C.POINTER(P)]),
+            "tps_pipeline_destroy": (I32, [P]),
+            "tps_local_link": (I32, [C.POINTER(P), I32]),
+            "tps_begin_run": (I32, [P, I64, I64]),
+            "tps_stage_forward": (I32, [P, I64, I32, I32, P, P]),
+            "tps_stage_backward": (I32, [P, I64, I32]),
+            "tps_stage_update": (I32, [P, I64]),
+            "tps_run_schedule": (I32, [P, I64, I64, P, P, I32]),
+            "tps_run_schedule_local": (I32, [C.POINTER(P), I32, I64, I64, P, P, I32]),
+            "tps_synchronize": (I32, [P]),
+            "tps_blend_coeffs": (I32, [I32, I32, I32, D, C.POINTER(F), C.POINTER(F)]),
+            "tps_stash_info": (I32, [P, C.POINTER(I32), C.POINTER(I64), C.POINTER(I64)]),
+            "tps_intermediate_weight": (I32, [P, I32, I32, P]),
+            "tps_get_version": (I32, [P, I32, I32, P]),
+            "tps_schedule_events": (I32, [I32, I32, I32, I32, I64, C.POINTER(Event), I64, C.POINTER(I64)]),
+            "tps_get_weights": (I32, [P, I32, P, P, P, P]),
+            "tps_set_weights": (I32, [P, I32, P, P]),
+            "tps_init_weights_synthetic": (I32, [P]),
+            "tps_get_losses": (I32, [P, P, I64, C.POINTER(I64)]),
+            "tps_get_trace": (I32, [P, C.POINTER(Event), I64, C.POINTER(I64)]),
+            "tps_clear_trace": (I32, [P]),
+            "tps_memory_stats": (I32, [P] + [C.POINTER(I64)] * 6),
+            "tps_set_profiling": (I32, [P, I32]),
+            "tps_kernel_stats": (I32, [P, I32, C.POINTER(I64), C.POINTER(D), C.POINTER(D)]),
+            "tps_launch_count": (I32, [P, C.POINTER(I64)]),
+            "tps_fill_synthetic": (I32, [I32, U64, U64, I64, I64, I32, P, U64]),
+            "tps_gemm": (I32, [I32, I32, I32, I32, P, I32, P, I32, P, P, I32, I32, P, I32, F, F, P, I32, U64]),
+        }
+        for name, (res, args) in sig.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _LIB = L
+    return _LIB
+
+
+def check(status: int) -> None:
+    if status != 0:
+        raise TpsError(status, lib().tps_last_error().decode())
+
+
+def ptr(t) -> int | None:
+    """Address of a torch tensor / numpy array / None."""
+    if t is None:
+        return None
+    if hasattr(t, "data_ptr"):
+        return t.data_ptr()
+    return t.ctypes.data
+
+
+# ------------------------------------------------------------------ free functions
+def blend_coeffs(variant: int, blend: int, staleness: int, lam: float) -> tuple[float, float]:
+    a, b = C.c_float(), C.c_float()
+    check(lib().tps_blend_coeffs(variant, blend, staleness, lam, C.byref(a), C.byref(b)))
+    return a.value, b.value
+
+
+def schedule_events(S: int, s: int, m: int, fwd_group: int, M: int) -> list[Event]:
+    n = C.c_int64()
+    check(lib().tps_schedule_events(S, s, m, fwd_group, M, None, 0, C.byref(n)))
+    buf = (Event * n.value)()
+    check(lib().tps_schedule_events(S, s, m, fwd_group, M, buf, n.value, C.byref(n)))
+    return list(buf)
+
+
+def nccl_unique_id() -> bytes:
+    b = C.create_string_buffer(128)
+    check(lib().tps_nccl_unique_id(b))
+    return b.raw
+
+
+def fill_synthetic(kind: int, seed: int, tid: int, rows: int, cols: int, classes: int, dst, stream: int = 0) -> None:
+    check(lib().tps_fill_synthetic(kind, seed, tid, rows, cols, classes, ptr(dst), stream))
+
+
+def gemm(mode, M, N, K, A, lda, B, ldb, out, ldo, out_f32=0, bias=None, relu=0, alpha=1.0, beta=0.0,
+         mask=None, ldm=0, B2=None, stream: int = 0) -> None:
+    check(lib().tps_gemm(mode, M, N, K, ptr(A), lda, ptr(B), ldb, ptr(B2), ptr(out), ldo, out_f32, ptr(bias), relu,
+                         alpha, beta, ptr(mask), ldm, stream))
+
+
+# ------------------------------------------------------------------ handle wrapper
+@dataclass
+class StageSpec:
+    dims: list[int]
+    stage_bounds: list[int]
+    stage_id: int
+    micro_batches: int
+    micro_batch_size: int
+    fwd_group: int = 0
+    variant: int = TPS_I
+    blend: int = TPS_BLEND_EQ1
+    lam: float = 0.05
+    lr: float = 0.01
+    momentum: float = 0.0
+    weight_decay: float = 0.0
+    transport: int = TPS_TRANSPORT_NONE
+    nccl_ids: bytes | None = None
+    device: int = 0
+    seed: int = 0
+    compute_stream: int = 0
+    extra_recv_slot: int = 1
+    _keep: list = field(default_factory=list)
+
+
+class Pipeline:
+    """One pipeline stage (tps_pipeline*)."""
+
+    def __init__(self, spec: StageSpec):
+        self.spec = spec
+        L = len(spec.dims) - 1
+        dims = (C.c_int32 * (L + 1))(*spec.dims)
+        bounds = (C.c_int32 * len(spec.stage_bounds))(*spec.stage_bounds)
+        ids = C.create_string_buffer(spec.nccl_ids, len(spec.nccl_ids)) if spec.nccl_ids else None
+        cfg = Config(num_layers=L, dims=dims, num_stages=len(spec.stage_bounds) - 1, stage_bounds=bounds,
+                     stage_id=spec.stage_id, micro_batches=spec.micro_batches,
+                     micro_batch_size=spec.micro_batch_size, fwd_group=spec.fwd_group, variant=spec.variant,
+                     blend=spec.blend, lambda_=spec.lam, lr=spec.lr, momentum=spec.momentum,
+                     weight_decay=spec.weight_decay, transport=spec.transport,
+                     nccl_ids=C.cast(ids, C.c_void_p) if ids is not None else None, device=spec.device,
+                     seed=spec.seed, compute_stream=spec.compute_stream, extra_recv_slot=spec.extra_recv_slot)
+        h = C.c_void_p()
+        check(lib().tps_pipeline_init(C.byref(cfg), C.byref(h)))
+        self.h = h
+        self.S = len(spec.stage_bounds) - 1
+        self.layers = list(range(spec.stage_bounds[spec.stage_id], spec.stage_bounds[spec.stage_id + 1]))
+
+    def close(self):
+        if self.h:
+            check(lib().tps_pipeline_destroy(self.h))
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # the step
+    def begin_run(self, first_mb: int, n_mb: int):
+        check(lib().tps_begin_run(self.h, first_mb, n_mb))
+
+    def stage_forward(self, mb: int, micro: int, count: int, x=None, labels=None):
+        check(lib().tps_stage_forward(self.h, mb, micro, count, ptr(x), ptr(labels)))
+
+    def stage_backward(self, mb: int, staleness: int = -1):
+        check(lib().tps_stage_backward(self.h, mb, staleness))
+
+    def stage_update(self, mb: int):
+        check(lib().tps_stage_update(self.h, mb))
+
+    def run_schedule(self, first_mb: int, n_mb: int, x_pool=None, y_pool=None, pool: int = 1):
+        check(lib().tps_run_schedule(self.h, first_mb, n_mb, ptr(x_pool), ptr(y_pool), pool))
+
+    def synchronize(self):
+        check(lib().tps_synchronize(self.h))
+
+    # state
+    def init_weights_synthetic(self):
+        check(lib().tps_init_weights_synthetic(self.h))
+
+    def set_weights(self, layer: int, w, b):
+        import numpy as np
+        w = np.ascontiguousarray(w, dtype=np.float32)
+        b = np.ascontiguousarray(b, dtype=np.float32)
+        check(lib().tps_set_weights(self.h, layer, w.ctypes.data, b.ctypes.data))
+
+    def get_weights(self, layer: int):
+        import numpy as np
+        g = self.layers[layer]
+        out_f, in_f = self.spec.dims[g + 1], self.spec.dims[g]
+        w = np.zeros((out_f, in_f), np.float32)
+        b = np.zeros(out_f, np.float32)
+        mw = np.zeros_like(w)
+        mb = np.zeros_like(b)
+        check(lib().tps_get_weights(self.h, layer, w.ctypes.data, b.ctypes.data, mw.ctypes.data, mb.ctypes.data))
+        return w, b, mw, mb
+
+    def losses(self):
+        import numpy as np
+        n = C.c_int64()
+        check(lib().tps_get_losses(self.h, None, 0, C.byref(n)))
+        out = np.zeros(n.value, np.float32)
+        if n.value:
+            check(lib().tps_get_losses(self.h, out.ctypes.data, n.value, C.byref(n)))
+        return out
+
+    def trace(self) -> list[Event]:
+        n = C.c_int64()
+        check(lib().tps_get_trace(self.h, None, 0, C.byref(n)))
+        buf = (Event * max(1, n.value))()
+        check(lib().tps_get_trace(self.h, buf, n.value, C.byref(n)))
+        return list(buf)[: n.value]
+
+    def clear_trace(self):
+        check(lib().tps_clear_trace(self.h))
+
+    def stash_info(self):
+        lv, st, pk = C.c_int32(), C.c_int64(), C.c_int64()
+        check(lib().tps_stash_info(self.h, C.byref(lv), C.byref(st), C.byref(pk)))
+        return lv.value, st.value, pk.value
+
+    def intermediate_weight(self, layer: int, staleness: int, out):
+        check(lib().tps_intermediate_weight(self.h, layer, staleness, ptr(out)))
+
+    def get_version(self, layer: int, staleness: int, out):
+        check(lib().tps_get_version(self.h, layer, staleness, ptr(out)))
+
+    def memory_stats(self) -> dict:
+        v = [C.c_int64() for _ in range(6)]
+        check(lib().tps_memory_stats(self.h, *[C.byref(x) for x in v]))
+        return dict(zip(["weights", "stash", "acts", "optim", "comm", "peak"], [x.value for x in v]))
+
+    def set_profiling(self, on: bool):
+        check(lib().tps_set_profiling(self.h, 1 if on else 0))
+
+    def kernel_stats(self, which: int):
+        n, ms, work = C.c_int64(), C.c_double(), C.c_double()
+        check(lib().tps_kernel_stats(self.h, which, C.byref(n), C.byref(ms), C.byref(work)))
+        return n.value, ms.value, work.value
+
+    def launch_count(self) -> int:
+        n = C.c_int64()
+        check(lib().tps_launch_count(self.h, C.byref(n)))
+        return n.value
+
+
+def local_link(stages: list[Pipeline]):
+    arr = (C.c_void_p * len(stages))(*[s.h.value for s in stages])
+    check(lib().tps_local_link(arr, len(stages)))
+
+
+def run_schedule_local(stages: list[Pipeline], first_mb: int, n_mb: int, x_pool=None, y_pool=None, pool: int = 1):
+    arr = (C.c_void_p * len(stages))(*[s.h.value for s in stages])
+    check(lib().tps_run_schedule_local(arr, len(stages), first_mb, n_mb, ptr(x_pool), ptr(y_pool), pool))

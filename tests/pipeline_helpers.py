@@ -1,0 +1,82 @@
+"""Shared helpers for parity tests: run the same seeded workload through the oracle
+(CPU) and through the C ABI (GPU), and compare."""
+from __future__ import annotations
+
+import numpy as np
+
+import synthgen
+from oracle import pipeline as opipe
+from oracle import staleness as ost
+
+
+def workload(dims, m, b, M, seed=0, kind=synthgen.X_SIGNED):
+    B = m * b
+    xs = [synthgen.inputs(seed, j, B, dims[0], kind) for j in range(M)]
+    ys = [synthgen.labels(seed, j, B, dims[-1]) for j in range(M)]
+    w0 = [synthgen.weights(seed, l, dims[l + 1], dims[l]) for l in range(len(dims) - 1)]
+    b0 = [np.zeros(dims[l + 1], np.float32) for l in range(len(dims) - 1)]
+    return xs, ys, w0, b0
+
+
+def run_oracle(dims, bounds, m, b, M, variant, blend, lam, lr, mu, wd=0.0, seed=0, kind=synthgen.X_SIGNED):
+    xs, ys, w0, b0 = workload(dims, m, b, M, seed, kind)
+    cfg = opipe.Config(dims, bounds, m, b, M, variant=variant, blend=blend, lam=lam, lr=lr, momentum=mu, wd=wd)
+    return opipe.run(cfg, xs, ys, w0, b0)
+
+
+def run_gpu(dims, bounds, m, b, M, variant, blend, lam, lr, mu, wd=0.0, seed=0, kind=synthgen.X_SIGNED,
+            fwd_group=0, init="set", extra_recv_slot=1, stepwise=False):
+    """All S stages as LOCAL-transport handles on cuda:0; returns (stages, losses)."""
+    import torch
+
+    from paper_2509_23241_b200 import tps
+
+    S = len(bounds) - 1
+    xs, ys, w0, b0 = workload(dims, m, b, M, seed, kind)
+    x_pool = torch.from_numpy(np.stack(xs)).to(torch.bfloat16).cuda().contiguous()
+    y_pool = torch.from_numpy(np.stack(ys)).cuda().contiguous()
+    V = tps.TPS_V if variant == ost.V_VARIANT else tps.TPS_I
+    BL = tps.TPS_BLEND_EQ1 if blend == ost.EQ1 else tps.TPS_BLEND_CONVEX
+    stages = []
+    for s in range(S):
+        spec = tps.StageSpec(dims=dims, stage_bounds=bounds, stage_id=s, micro_batches=m, micro_batch_size=b,
+                             fwd_group=fwd_group, variant=V, blend=BL, lam=lam, lr=lr, momentum=mu, weight_decay=wd,
+                             transport=tps.TPS_TRANSPORT_LOCAL if S > 1 else tps.TPS_TRANSPORT_NONE, seed=seed,
+                             extra_recv_slot=extra_recv_slot)
+        st = tps.Pipeline(spec)
+        if init == "set":
+            for k, l in enumerate(st.layers):
+                st.set_weights(k, w0[l], b0[l])
+        else:
+            st.init_weights_synthetic()
+        stages.append(st)
+    if S > 1:
+        tps.local_link(stages)
+    tps.run_schedule_local(stages, 0, M, x_pool, y_pool, M)
+    for st in stages:
+        st.synchronize()
+    return stages, stages[-1].losses()
+
+
+def expand_gpu_trace(stages):
+    rows = []
+    for st in stages:
+        for e in st.trace():
+            if e.kind == 0:
+                for a in range(e.micro, e.micro + e.micro_count):
+                    rows.append((e.stage, "F", e.mb, a, e.v_used, e.v_latest, e.delta, 1.0, 0.0))
+            elif e.kind == 1:
+                rows.append((e.stage, "B", e.mb, -1, e.v_used, e.v_latest, e.delta, e.alpha, e.beta))
+            else:
+                rows.append((e.stage, "U", e.mb, -1, e.v_used, e.v_latest, 0, 1.0, 0.0))
+    return sorted(rows)
+
+
+def oracle_trace(res):
+    return sorted((r.stage, r.kind, r.mb, r.micro, r.v_used, r.v_latest, r.delta,
+                   float(r.alpha), float(r.beta)) for r in res.trace)
+
+
+def weight_rel_err(got, ref):
+    """max|Δ| / max|w_ref| per tensor (reading Z19)."""
+    return float(np.abs(got.astype(np.float64) - ref).max() / max(np.abs(ref).max(), 1e-30))

@@ -1,0 +1,145 @@
+"""End-to-end parity of the CUDA path (through the C ABI) with the CPU oracle.
+
+Bar (north_star): schedule and staleness degrees bit-exact; losses within 1e-3
+relative and weights within 5e-3 max-relative (max|Δ|/max|w|, reading Z19) after
+10 mini-batches, bf16 inputs with fp32 accumulation.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import synthgen
+from oracle import mlp as omlp
+from oracle import staleness as ost
+from paper_2509_23241_b200 import tps
+from pipeline_helpers import expand_gpu_trace, oracle_trace, run_gpu, run_oracle, weight_rel_err, workload
+
+pytestmark = pytest.mark.gpu
+
+CASES = {
+    # name: dims, bounds, m, b, M, variant, blend, lam, lr, mu, kind
+    "C1-V": ([784, 256, 10], [0, 1, 2], 4, 8, 10, ost.V_VARIANT, ost.EQ1, 0.05, 0.05, 0.0, synthgen.X_UNIT),
+    "C1-I-EQ1": ([784, 256, 10], [0, 1, 2], 4, 8, 10, ost.I_VARIANT, ost.EQ1, 0.05, 0.05, 0.0, synthgen.X_UNIT),
+    "C1-I-CONVEX": ([784, 256, 10], [0, 1, 2], 4, 8, 10, ost.I_VARIANT, ost.CONVEX, 0.5, 0.05, 0.0, synthgen.X_UNIT),
+    "S1-deep": ([512, 384, 256, 16], [0, 3], 4, 32, 10, ost.I_VARIANT, ost.EQ1, 0.05, 0.05, 0.9, synthgen.X_SIGNED),
+    "S4-I-EQ1": ([256, 256, 256, 256, 256, 256, 10], [0, 2, 3, 5, 6], 2, 64, 10, ost.I_VARIANT, ost.EQ1, 0.3, 0.05, 0.9,
+                 synthgen.X_SIGNED),
+    "S4-I-CONVEX": ([256, 256, 256, 256, 256, 256, 10], [0, 2, 3, 5, 6], 2, 64, 10, ost.I_VARIANT, ost.CONVEX, 0.3, 0.05,
+                    0.0, synthgen.X_SIGNED),
+    "S4-V": ([256, 256, 256, 256, 256, 256, 10], [0, 2, 3, 5, 6], 2, 64, 10, ost.V_VARIANT, ost.EQ1, 0.3, 0.05, 0.9,
+             synthgen.X_SIGNED),
+    "S3-ragged": ([200, 136, 72, 40, 10], [0, 2, 3, 4], 3, 24, 10, ost.I_VARIANT, ost.CONVEX, 0.2, 0.05, 0.5,
+                  synthgen.X_SIGNED),
+    "S8-I": ([128] * 9 + [10], [0, 2, 3, 4, 5, 6, 7, 8, 9], 2, 16, 12, ost.I_VARIANT, ost.EQ1, 0.05, 0.05, 0.9,
+             synthgen.X_SIGNED),
+}
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_parity_with_oracle(gpu_lib, name):
+    dims, bounds, m, b, M, var, blend, lam, lr, mu, kind = CASES[name]
+    ref = run_oracle(dims, bounds, m, b, M, var, blend, lam, lr, mu, kind=kind)
+    stages, losses = run_gpu(dims, bounds, m, b, M, var, blend, lam, lr, mu, kind=kind)
+    # schedule, versions, δ, α, β: bit-exact
+    assert expand_gpu_trace(stages) == oracle_trace(ref)
+    # losses: 1e-3 relative
+    np.testing.assert_allclose(losses, ref.losses, rtol=1e-3, atol=0)
+    # weights: 5e-3 max-relative per tensor
+    for st in stages:
+        for k, l in enumerate(st.layers):
+            w, bb, _, _ = st.get_weights(k)
+            assert weight_rel_err(w, ref.weights[l]) <= 5e-3, (name, l)
+            if np.abs(ref.biases[l]).max() > 0:
+                assert weight_rel_err(bb, ref.biases[l]) <= 5e-3, (name, l)
+
+
+def test_fwd_groups_and_stepwise_api_agree(gpu_lib):
+    dims, bounds = [256, 256, 256, 16], [0, 1, 2, 3]
+    r1 = run_gpu(dims, bounds, 4, 16, 6, ost.I_VARIANT, ost.EQ1, 0.3, 0.05, 0.0, fwd_group=1)[1]
+    r2 = run_gpu(dims, bounds, 4, 16, 6, ost.I_VARIANT, ost.EQ1, 0.3, 0.05, 0.0, fwd_group=4)[1]
+    r3 = run_gpu(dims, bounds, 4, 16, 6, ost.I_VARIANT, ost.EQ1, 0.3, 0.05, 0.0, fwd_group=2, extra_recv_slot=0)[1]
+    # a row's forward does not depend on how rows are grouped into launches
+    np.testing.assert_array_equal(r1, r2)
+    np.testing.assert_array_equal(r1, r3)
+
+
+def test_v_equals_i_bitwise_on_config1(gpu_lib):
+    # reading Z12: single-layer stage 0 + δ = 0 on the last stage => V ≡ I
+    args = ([784, 256, 10], [0, 1, 2], 4, 8, 10)
+    out = [run_gpu(*args, v, bl, 0.5, 0.05, 0.0, kind=synthgen.X_UNIT)
+           for v, bl in [(ost.V_VARIANT, ost.EQ1), (ost.I_VARIANT, ost.EQ1), (ost.I_VARIANT, ost.CONVEX)]]
+    for st, l in out[1:]:
+        np.testing.assert_array_equal(l, out[0][1])
+        for k in range(2):
+            np.testing.assert_array_equal(st[k].get_weights(0)[0], out[0][0][k].get_weights(0)[0])
+
+
+def test_i_eq1_freeze_at_ln2_on_gpu(gpu_lib):
+    # EQ1, λ = ln 2, μ = 0: stage S-2 has α = 0 for j >= 1, so everything below its
+    # last layer stays bitwise constant after the first update (exact on any GPU order).
+    dims, bounds = [128, 128, 128, 128, 128, 10], [0, 2, 4, 5]
+    st1, _ = run_gpu(dims, bounds, 2, 16, 1, ost.I_VARIANT, ost.EQ1, math.log(2), 0.1, 0.0)
+    stM, _ = run_gpu(dims, bounds, 2, 16, 6, ost.I_VARIANT, ost.EQ1, math.log(2), 0.1, 0.0)
+    for s, k in [(0, 0), (0, 1), (1, 0)]:
+        np.testing.assert_array_equal(st1[s].get_weights(k)[0], stM[s].get_weights(k)[0])
+        np.testing.assert_array_equal(st1[s].get_weights(k)[1], stM[s].get_weights(k)[1])
+    assert not np.array_equal(st1[1].get_weights(1)[0], stM[1].get_weights(1)[0])
+    alphas = [e.alpha for e in stM[1].trace() if e.kind == 1]
+    assert alphas == [1.0] + [0.0] * 5
+
+
+def test_device_init_matches_synthgen(gpu_lib):
+    dims, bounds = [200, 136, 10], [0, 2]
+    st, _ = run_gpu(dims, bounds, 2, 8, 0 + 1, ost.V_VARIANT, ost.EQ1, 0.05, 0.0, 0.0, init="synthetic", seed=3)
+    for k in range(2):
+        w = st[0].get_weights(k)[0]
+        np.testing.assert_array_equal(w, synthgen.weights(3, k, dims[k + 1], dims[k]))
+
+
+def test_fill_synthetic_matches_synthgen(gpu_lib):
+    x = torch.empty(64, 200, dtype=torch.bfloat16, device="cuda")
+    y = torch.empty(64, dtype=torch.int32, device="cuda")
+    for kind in (synthgen.X_SIGNED, synthgen.X_UNIT):
+        tps.fill_synthetic(kind, 5, synthgen.TID_X + 7, 64, 200, 0, x)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(x.float().cpu().numpy(), synthgen.inputs(5, 7, 64, 200, kind))
+    tps.fill_synthetic(2, 5, synthgen.TID_Y + 7, 64, 1, 10, y)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(y.cpu().numpy(), synthgen.labels(5, 7, 64, 10))
+
+
+def test_intermediate_weight_materialiser_matches_oracle(gpu_lib):
+    # K8 debug materialiser == oracle.mlp.materialize_blend (reading Z14), bit-exact, on the
+    # GPU's own stashed versions; the latest version == bf16_rne(fp32 master).
+    dims, bounds = [64, 64, 64, 64, 10], [0, 1, 2, 3, 4]
+    stages, _ = run_gpu(dims, bounds, 2, 8, 3, ost.I_VARIANT, ost.CONVEX, 0.4, 0.1, 0.0)
+    st = stages[0]                      # K_0 = 4 ring slots; latest = version 3
+    from oracle import bf16 as obf
+    lat = torch.empty(64, 64, dtype=torch.bfloat16, device="cuda")
+    st.get_version(0, 0, lat)
+    latn = lat.float().cpu().numpy().astype(np.float64)
+    np.testing.assert_array_equal(latn, obf.rne(st.get_weights(0)[0]))
+    out = torch.empty_like(lat)
+    sv = torch.empty_like(lat)
+    for d in (1, 2, 3):
+        st.get_version(0, d, sv)
+        st.intermediate_weight(0, d, out)
+        torch.cuda.synchronize()
+        a, b = tps.blend_coeffs(tps.TPS_I, tps.TPS_BLEND_CONVEX, d, 0.4)
+        ref = omlp.materialize_blend(sv.float().cpu().numpy(), latn, a, b)
+        np.testing.assert_array_equal(out.float().cpu().numpy().astype(np.float64), ref)
+        assert not np.array_equal(sv.float().cpu().numpy(), lat.float().cpu().numpy())
+
+
+def test_memory_v_vs_i(gpu_lib):
+    dims, bounds = [512] * 5 + [10], [0, 2, 3, 4, 5]
+    mem = {}
+    for var in (tps.TPS_V, tps.TPS_I):
+        st = tps.Pipeline(tps.StageSpec(dims, bounds, 0, 2, 16, variant=var, transport=tps.TPS_TRANSPORT_LOCAL))
+        mem[var] = st.memory_stats()
+        st.close()
+    # I keeps K_0 - 1 = 3 extra bf16 versions of stage 0's two 512x512 layers
+    assert mem[tps.TPS_I]["stash"] - mem[tps.TPS_V]["stash"] == 3 * 2 * 512 * 512 * 2
+    assert mem[tps.TPS_V]["stash"] == 0
