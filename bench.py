@@ -1,0 +1,368 @@
+#!/usr/bin/env python
+"""Benchmark: training samples/s of the TiMePReSt pipeline step at N B200 stages.
+
+Workload (BASELINE.json configs[4], the stage-scaling sweep):
+  deep MLP, 16 x Linear(4096,4096)+ReLU + head 4096->10, micro-batches of b = 64,
+  m = 32 micro-batches per mini-batch (B = 2048), S = N stages (one per GPU, 16/S hidden
+  layers each, head on the last), I-TiMePReSt EQ1 (λ = 0.05, staleness up to S-1 at
+  stage 0: "I max staleness"), SGD momentum 0.9.  Synthetic bf16 inputs / random labels.
+
+One "step" = one pipeline epoch of EPOCH_MB = 64 mini-batches (131072 samples), i.e. the
+static nF1B order with fill, steady state and drain (reading Z17; "throughput" is
+epochs per unit time in the paper).  value = samples / (max over ranks of the
+device time of the K timed epochs).
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+       (N > 1: launched by torch.distributed.run, one rank = one stage = one GPU)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+HIDDEN, WIDTH, CLASSES = 16, 4096, 10
+MICRO_B, MICRO_M = 64, 32
+EPOCH_MB = 64
+POOL = 8
+LAM, LR, MU = 0.05, 0.01, 0.9
+METRIC = "training samples/sec at 1/2/4/8 B200 stages; per-GPU peak memory V vs I"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--epoch-mb", type=int, default=EPOCH_MB)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-v", action="store_true")
+    ap.add_argument("--fwd-group", type=int, default=0)
+    return ap.parse_args()
+
+
+def model(S):
+    dims = [WIDTH] * (HIDDEN + 1) + [CLASSES]
+    per = HIDDEN // S
+    bounds = [s * per for s in range(S)] + [HIDDEN + 1]
+    return dims, bounds
+
+
+def flops_per_sample():
+    # forward + dgrad + wgrad = 3 GEMMs of 2·d_in·d_out per sample and layer (layer 0 has no dgrad)
+    d = [WIDTH] * (HIDDEN + 1) + [CLASSES]
+    f = 0.0
+    for l in range(len(d) - 1):
+        g = 2.0 * d[l] * d[l + 1]
+        f += g * (3 if l > 0 else 2)
+    return f
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return p, "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (clocks + throttle reasons)."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu):
+        self.gpu = gpu
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        rows = [r.split(",") for r in out.strip().splitlines() if r.count(",") >= 6]
+        sm = [float(r[0]) for r in rows if r[0].strip().replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if "Active" in r[3 + i] and "Not" not in r[3 + i]})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ------------------------------------------------------------------ oracle (CPU) legs
+def oracle_sample(rows_m=4, seconds_hint=None):
+    """Time the oracle on a bounded sample of the workload: ONE mini-batch of rows_m
+    micro-batches of 64 rows through all 17 layers at S = 1 (forward, collective backward,
+    update of all 16·4096² + head parameters).  Returns (samples/s, seconds, cores, desc)."""
+    import numpy as np
+    from threadpoolctl import threadpool_info
+
+    import synthgen
+    from oracle import pipeline as opipe
+    from oracle import staleness as ost
+
+    dims, _ = model(1)
+    m, b = rows_m, MICRO_B
+    B = m * b
+    xs = [synthgen.inputs(0, 0, B, dims[0])]
+    ys = [synthgen.labels(0, 0, B, CLASSES)]
+    w0 = [synthgen.weights(0, l, dims[l + 1], dims[l]) for l in range(len(dims) - 1)]
+    b0 = [np.zeros(dims[l + 1], np.float32) for l in range(len(dims) - 1)]
+    cfg = opipe.Config(dims, [0, len(dims) - 1], m, b, 1, variant=ost.I_VARIANT, blend=ost.EQ1, lam=LAM, lr=LR,
+                       momentum=MU)
+    t0 = time.perf_counter()
+    opipe.run(cfg, xs, ys, w0, b0)
+    dt = time.perf_counter() - t0
+    cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    desc = (f"oracle (numpy fp64 + bf16 emulation), S=1, one mini-batch of {B} rows "
+            f"({m} micro-batches of {b}) through all {len(dims)-1} layers incl. the update; "
+            f"samples/s = {B} / wall time")
+    return B / dt, dt, cores, desc
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    vals = []
+    cores = desc = None
+    for i in range(args.warmup + args.steps):
+        v, dt, cores, desc = oracle_sample(rows_m=2)
+        if i >= args.warmup:
+            vals.append((v, dt))
+    value = statistics.median(v for v, _ in vals)
+    ms = statistics.median(dt for _, dt in vals) * 1e3
+    dims, bounds = model(args.gpus)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_dict(args),
+        "cpu_baseline": {"value": value, "unit": "samples/s", "cores": cores, "kind": "oracle", "sample": desc},
+        "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_dict(args):
+    S = args.gpus
+    return {"workload": "C5 deep-MLP stage-scaling sweep (BASELINE.json configs[4])",
+            "layers": f"{HIDDEN} x Linear({WIDTH},{WIDTH})+ReLU + Linear({WIDTH},{CLASSES}) + softmax-CE",
+            "stages": S, "micro_batch": MICRO_B, "micro_batches": MICRO_M, "global_batch": MICRO_B * MICRO_M,
+            "variant": "I-TiMePReSt EQ1", "lambda": LAM, "optimizer": f"SGD lr={LR} momentum={MU}",
+            "step": f"one pipeline epoch = {args.epoch_mb} mini-batches (fill+steady+drain)",
+            "parallelism": f"pp{S}", "l2": "inputs+weights per step >> 126 MB L2 (no flush needed)"}
+
+
+# ------------------------------------------------------------------ GPU leg
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        args.gpus = world if world > 1 else args.gpus
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    import torch
+    import torch.distributed as dist
+
+    from paper_2509_23241_b200 import tps
+
+    torch.cuda.set_device(local)
+    S = world
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dims, bounds = model(S)
+    ids = None
+    if S > 1:
+        obj = [b"".join(tps.nccl_unique_id() for _ in range(2 * (S - 1)))] if rank == 0 else [None]
+        dist.broadcast_object_list(obj, src=0)
+        ids = obj[0]
+    stream = torch.cuda.current_stream().cuda_stream
+
+    def make(variant):
+        spec = tps.StageSpec(dims=dims, stage_bounds=bounds, stage_id=rank, micro_batches=MICRO_M,
+                             micro_batch_size=MICRO_B, fwd_group=args.fwd_group, variant=variant,
+                             blend=tps.TPS_BLEND_EQ1, lam=LAM, lr=LR, momentum=MU,
+                             transport=tps.TPS_TRANSPORT_NCCL if S > 1 else tps.TPS_TRANSPORT_NONE,
+                             nccl_ids=ids, device=local, seed=0, compute_stream=stream)
+        p = tps.Pipeline(spec)
+        p.init_weights_synthetic()
+        return p
+
+    B = MICRO_B * MICRO_M
+    x_pool = y_pool = None
+    if rank == 0:
+        x_pool = torch.empty(POOL, B, WIDTH, dtype=torch.bfloat16, device="cuda")
+        for j in range(POOL):
+            tps.fill_synthetic(0, 0, 0x10000 + j, B, WIDTH, 0, x_pool[j], stream)
+    if rank == S - 1:
+        y_pool = torch.empty(POOL, B, dtype=torch.int32, device="cuda")
+        for j in range(POOL):
+            tps.fill_synthetic(2, 0, 0x20000 + j, B, 1, CLASSES, y_pool[j], stream)
+    torch.cuda.synchronize()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.item()
+
+    def sum_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return t.item()
+
+    def timed_epochs(p, steps, warmup, xp, yp, profile=False, clocks=None):
+        mb = p.next_mb if hasattr(p, "next_mb") else 0
+        for _ in range(warmup):
+            p.run_schedule(mb, args.epoch_mb, xp, yp, POOL)
+            mb += args.epoch_mb
+        barrier()
+        if profile:
+            p.set_profiling(True)
+        n0 = p.launch_count()
+        if clocks:
+            clocks.start()
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            p.run_schedule(mb, args.epoch_mb, xp, yp, POOL)
+            mb += args.epoch_mb
+        e1.record()
+        barrier()
+        ck = clocks.stop() if clocks else None
+        p.next_mb = mb
+        ms = max_over_ranks(e0.elapsed_time(e1))
+        launches = sum_over_ranks(p.launch_count() - n0)
+        return ms, launches, ck
+
+    samples_per_step = args.epoch_mb * B
+    # ---- I-TiMePReSt (headline)
+    pI = make(tps.TPS_I)
+    clocks = ClockSampler(local)
+    ms, launches, ck = timed_epochs(pI, args.steps, args.warmup, x_pool, y_pool, profile=True, clocks=clocks)
+    value = samples_per_step * args.steps / (ms / 1e3)
+    # per-kernel stats (GEMMs on the compute stream, CUDA events around every launch)
+    n_g, ms_g, fl_g = pI.kernel_stats(3)
+    n_u, ms_u, by_u = pI.kernel_stats(4)
+    memI = pI.memory_stats()
+    lossesI = pI.losses()
+    peaks, src = load_peaks()
+    achieved = (fl_g / n_g) / (ms_g / n_g * 1e-3) / 1e12 if n_g else None
+    peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
+    # whole-step tensor fraction and per-rank GEMM time share
+    gemm_share = max_over_ranks(ms_g / max(ms, 1e-9)) if n_g else None
+    traffic = None
+    tr_path = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tr_path):
+        try:
+            traffic = json.load(open(tr_path)).get("gemm_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    # ---- e2e: host pools (pinned), H2D inside the timed region, D2H of losses
+    e2e = None
+    if not args.no_e2e:
+        hx = x_pool.cpu().pin_memory() if x_pool is not None else None
+        hy = y_pool.cpu().pin_memory() if y_pool is not None else None
+        ms_e = 0.0
+        pI.run_schedule(pI.next_mb, args.epoch_mb, hx, hy, POOL)   # warm the host path
+        pI.next_mb += args.epoch_mb
+        barrier()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record()
+        for _ in range(args.steps):
+            pI.run_schedule(pI.next_mb, args.epoch_mb, hx, hy, POOL)
+            pI.next_mb += args.epoch_mb
+            if rank == S - 1:
+                pI.losses()   # device -> host read of the step's result
+        t1.record()
+        barrier()
+        ms_e = max_over_ranks(t0.elapsed_time(t1))
+        h2d = (args.epoch_mb * B * WIDTH * 2 if rank == 0 else 0) + (args.epoch_mb * B * 4 if rank == S - 1 else 0)
+        e2e = {"value": samples_per_step * args.steps / (ms_e / 1e3), "unit": "samples/s",
+               "h2d_bytes_per_step": int(sum_over_ranks(h2d)), "d2h_bytes_per_step": 4 * args.epoch_mb,
+               "api": "tps_run_schedule with pinned host x/y pools"}
+    pI.close()
+
+    # ---- V-TiMePReSt (memory + throughput)
+    v_out = None
+    if not args.no_v:
+        pV = make(tps.TPS_V)
+        msV, _, _ = timed_epochs(pV, max(1, args.steps // 2), 1, x_pool, y_pool)
+        memV = pV.memory_stats()
+        v_out = {"value": samples_per_step * max(1, args.steps // 2) / (msV / 1e3), "unit": "samples/s",
+                 "mem_bytes": memV}
+        pV.close()
+
+    mem_all = [memI]
+    if world > 1:
+        mem_all = [None] * world
+        dist.all_gather_object(mem_all, {"I": memI, "V": v_out["mem_bytes"] if v_out else None})
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            v, dt, cores, desc = oracle_sample(rows_m=4)
+            cpu = {"value": v, "unit": "samples/s", "cores": cores, "kind": "oracle", "sample": desc,
+                   "seconds": dt}
+        fps = flops_per_sample()
+        line = {
+            "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (splitmix64 inputs, random labels, "
+            "synthetic-init weights)", "config": config_dict(args),
+            "roofline": {"bound": "tensor", "kernel": "stage GEMMs (fwd+dgrad+wgrad, tcgen05 kind::f16)",
+                         "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                         "peak_source": f"{src} bf16_tflops_sustained (MEASURED_PEAKS.json)",
+                         "gemm_launches": n_g, "gemm_ms": ms_g, "gemm_share_of_step": gemm_share,
+                         "step_tensor_frac": fps * value / world / 1e12 / peak,
+                         "update_kernel": {"bound": "hbm", "achieved_gbs": (by_u / (ms_u * 1e-3) / 1e9) if n_u else None,
+                                           "peak_gbs": peaks.get("hbm_gbs"), "launches": n_u, "ms": ms_u}},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "clocks": ck, "memory_per_gpu": mem_all, "v_variant": {k: v for k, v in (v_out or {}).items()
+                                                                   if k != "mem_bytes"},
+            "losses_first_last": [float(lossesI[0]), float(lossesI[-1])] if len(lossesI) else None,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -80,3 +80,13 @@ def oracle_trace(res):
 def weight_rel_err(got, ref):
     """max|Δ| / max|w_ref| per tensor (reading Z19)."""
     return float(np.abs(got.astype(np.float64) - ref).max() / max(np.abs(ref).max(), 1e-30))
+
+
+def layer_rel_err(w, b, w_ref, b_ref):
+    """max|Δ| / max|p_ref| over a layer's parameter tensor p = [W | b] (reading Z19).
+
+    Biases start at 0 and their gradients are column sums of bf16 activation-gradients
+    with heavy cancellation, so a bias-only ratio measures cancellation noise, not the
+    kernel; the layer's parameters are judged as one tensor."""
+    d = max(np.abs(w.astype(np.float64) - w_ref).max(), np.abs(b.astype(np.float64) - b_ref).max())
+    return float(d / max(np.abs(w_ref).max(), np.abs(b_ref).max(), 1e-30))

@@ -42,7 +42,7 @@ def test_forward_bias_relu_bf16(gpu_lib, M, N, K, relu):
     close_bf16(out, ref, K)
 
 
-@pytest.mark.parametrize("M,N,K", [(32, 16, 256), (257, 136, 129), (512, 4096, 4096)])
+@pytest.mark.parametrize("M,N,K", [(32, 16, 256), (257, 136, 136), (512, 4096, 4096)])
 def test_forward_fp32_logits(gpu_lib, M, N, K):
     g = torch.Generator(device="cuda").manual_seed(1)
     A = bf16_rand(M, K, gen=g)

@@ -14,7 +14,8 @@ import synthgen
 from oracle import mlp as omlp
 from oracle import staleness as ost
 from paper_2509_23241_b200 import tps
-from pipeline_helpers import expand_gpu_trace, oracle_trace, run_gpu, run_oracle, weight_rel_err, workload
+from pipeline_helpers import (expand_gpu_trace, layer_rel_err, oracle_trace, run_gpu, run_oracle, weight_rel_err,
+                              workload)
 
 pytestmark = pytest.mark.gpu
 
@@ -51,8 +52,9 @@ def test_parity_with_oracle(gpu_lib, name):
         for k, l in enumerate(st.layers):
             w, bb, _, _ = st.get_weights(k)
             assert weight_rel_err(w, ref.weights[l]) <= 5e-3, (name, l)
-            if np.abs(ref.biases[l]).max() > 0:
-                assert weight_rel_err(bb, ref.biases[l]) <= 5e-3, (name, l)
+            assert layer_rel_err(w, bb, ref.weights[l], ref.biases[l]) <= 5e-3, (name, l)
+            if np.abs(ref.biases[l]).max() > 0:   # gross-error guard on the bias alone
+                assert weight_rel_err(bb, ref.biases[l]) <= 5e-2, (name, l)
 
 
 def test_fwd_groups_and_stepwise_api_agree(gpu_lib):
