@@ -273,8 +273,11 @@ def main():
     # ---- I-TiMePReSt (headline)
     pI = make(tps.TPS_I)
     clocks = ClockSampler(local)
-    ms, launches, ck = timed_epochs(pI, args.steps, args.warmup, x_pool, y_pool, profile=True, clocks=clocks)
+    ms, launches, ck = timed_epochs(pI, args.steps, args.warmup, x_pool, y_pool, clocks=clocks)
     value = samples_per_step * args.steps / (ms / 1e3)
+    # second timed region with CUDA events around every GEMM / update launch on the compute
+    # stream (the events add small gaps, so the headline value above is taken without them)
+    ms_prof, _, _ = timed_epochs(pI, max(1, args.steps // 2), 0, x_pool, y_pool, profile=True)
     # per-kernel stats (GEMMs on the compute stream, CUDA events around every launch)
     n_g, ms_g, fl_g = pI.kernel_stats(3)
     n_u, ms_u, by_u = pI.kernel_stats(4)
@@ -284,7 +287,7 @@ def main():
     achieved = (fl_g / n_g) / (ms_g / n_g * 1e-3) / 1e12 if n_g else None
     peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
     # whole-step tensor fraction and per-rank GEMM time share
-    gemm_share = max_over_ranks(ms_g / max(ms, 1e-9)) if n_g else None
+    gemm_share = max_over_ranks(ms_g / max(ms_prof, 1e-9)) if n_g else None
     traffic = None
     tr_path = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tr_path):
@@ -348,6 +351,7 @@ def main():
             "roofline": {"bound": "tensor", "kernel": "stage GEMMs (fwd+dgrad+wgrad, tcgen05 kind::f16)",
                          "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                         "frac_of_burst_peak": (achieved / peaks["bf16_tflops"]) if achieved else None,
                          "peak_source": f"{src} bf16_tflops_sustained (MEASURED_PEAKS.json)",
                          "gemm_launches": n_g, "gemm_ms": ms_g, "gemm_share_of_step": gemm_share,
                          "step_tensor_frac": fps * value / world / 1e12 / peak,
