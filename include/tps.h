@@ -112,7 +112,13 @@ typedef struct {
   uint64_t compute_stream;      /* cudaStream_t to enqueue on; 0 => handle-owned     */
   int32_t extra_recv_slot;      /* 1 => one extra input slot so the next forward's
                                    receive overlaps the backward (costs B·d_in·2 B)   */
-  int32_t reserved[7];
+  int32_t fuse_update;          /* 1 => the SGD/momentum update of each layer runs in the
+                                   epilogue of its wgrad GEMM during tps_stage_backward (the
+                                   dgrad of that layer is issued first, so it still reads the
+                                   pre-update weights); tps_stage_update then only commits the
+                                   new version.  Legal because U(j) always directly follows
+                                   B(j) in the static order (reading Z7).  0 => separate kernel. */
+  int32_t reserved[6];
 } tps_config;
 
 typedef struct tps_pipeline tps_pipeline;  /* opaque; one per stage */

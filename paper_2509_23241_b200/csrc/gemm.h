@@ -22,7 +22,14 @@ struct GemmArgs {
   float alpha;                // epilogue scale (EQ1 α), 1 = none
   float xa, xb;               // BLEND operand coefficients
   const uint16_t* mask; int ldm;  // bf16 ReLU mask source (zero where <= 0), may be null
+  // EPI_SGD (wgrad only): instead of storing dW, apply the PyTorch-order SGD/momentum update
+  // to the fp32 master w / momentum v ([M, N], ld = ldo) and write bf16(w) to ver.
+  int epi;
+  float* w; float* v; uint16_t* ver;
+  float lr, mu, wd;
 };
+
+enum GemmEpilogue { EPI_STORE = 0, EPI_SGD = 1 };
 
 cudaError_t gemm_run(int mode, const GemmOperands& op, const GemmArgs& args, cudaStream_t st, int* bn_out = nullptr);
 const char* gemm_mode_name(int mode);

@@ -249,7 +249,50 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND>::THREADS, 1)
             }
           }
         }
-        if (args.out_f32) {
+        if (args.epi == EPI_SGD) {
+          // fused update (row a10): g' = g + wd·w ; v = μ·v + g' ; w = w - lr·v ; ver = bf16(w)
+          const size_t off = static_cast<size_t>(grow) * args.ldo + gcol;
+          float* wp = args.w + off;
+          float* vp = args.v + off;
+          uint16_t* qp = args.ver + off;
+#pragma unroll
+          for (int ch = 0; ch < 4; ++ch) {
+            if (ch < nchunk) {
+              float4 w0 = reinterpret_cast<float4*>(wp + ch * 8)[0];
+              float4 w1 = reinterpret_cast<float4*>(wp + ch * 8)[1];
+              float ww[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+              float vv[8];
+              if (args.mu != 0.0f) {
+                const float4 v0 = reinterpret_cast<float4*>(vp + ch * 8)[0];
+                const float4 v1 = reinterpret_cast<float4*>(vp + ch * 8)[1];
+                vv[0] = v0.x; vv[1] = v0.y; vv[2] = v0.z; vv[3] = v0.w;
+                vv[4] = v1.x; vv[5] = v1.y; vv[6] = v1.z; vv[7] = v1.w;
+              }
+#pragma unroll
+              for (int e = 0; e < 8; ++e) {
+                const float gp = __fadd_rn(v[ch * 8 + e], __fmul_rn(args.wd, ww[e]));
+                float upd = gp;
+                if (args.mu != 0.0f) {
+                  vv[e] = __fadd_rn(__fmul_rn(args.mu, vv[e]), gp);
+                  upd = vv[e];
+                }
+                ww[e] = __fsub_rn(ww[e], __fmul_rn(args.lr, upd));
+              }
+              reinterpret_cast<float4*>(wp + ch * 8)[0] = make_float4(ww[0], ww[1], ww[2], ww[3]);
+              reinterpret_cast<float4*>(wp + ch * 8)[1] = make_float4(ww[4], ww[5], ww[6], ww[7]);
+              if (args.mu != 0.0f) {
+                reinterpret_cast<float4*>(vp + ch * 8)[0] = make_float4(vv[0], vv[1], vv[2], vv[3]);
+                reinterpret_cast<float4*>(vp + ch * 8)[1] = make_float4(vv[4], vv[5], vv[6], vv[7]);
+              }
+              uint4 o;
+              o.x = pack_bf16(ww[0], ww[1]);
+              o.y = pack_bf16(ww[2], ww[3]);
+              o.z = pack_bf16(ww[4], ww[5]);
+              o.w = pack_bf16(ww[6], ww[7]);
+              reinterpret_cast<uint4*>(qp)[ch] = o;
+            }
+          }
+        } else if (args.out_f32) {
           float* op = reinterpret_cast<float*>(args.out) + static_cast<size_t>(grow) * args.ldo + gcol;
 #pragma unroll
           for (int ch = 0; ch < 4; ++ch) {

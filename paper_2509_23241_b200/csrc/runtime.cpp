@@ -73,6 +73,8 @@ bool is_host_ptr(const void* p) {
 }
 
 tps_status check_arch(int device) {
+  static thread_local int ok_device = -1;   // cache a positive answer (cudaGetDeviceProperties is slow)
+  if (device == ok_device) return TPS_OK;
   int n = 0;
   if (cudaGetDeviceCount(&n) != cudaSuccess || n <= device) {
     cudaGetLastError();
@@ -81,6 +83,7 @@ tps_status check_arch(int device) {
   cudaDeviceProp pr;
   CUDA_OK(cudaGetDeviceProperties(&pr, device));
   if (pr.major != 10) return fail(TPS_E_ARCH, "device %d is sm_%d%d; this library targets sm_100a", device, pr.major, pr.minor);
+  ok_device = device;
   return TPS_OK;
 }
 
@@ -112,7 +115,7 @@ struct tps_pipeline {
   double lambda = 0.05;
   float lr = 0.01f, mu = 0.f, wd = 0.f;
   uint64_t seed = 0;
-  bool first = true, last = true, eq1_on_load = false;
+  bool first = true, last = true, eq1_on_load = false, fuse_update = false;
   std::vector<int> dims;  // global
   std::vector<Layer> layers;
   int classes = 0;
@@ -430,8 +433,13 @@ tps_status do_forward(tps_pipeline* p, int64_t j, int a0, int cnt, const void* x
   Layer& L0 = p->layers[0];
   uint16_t* X = p->act[slot0][0] + static_cast<size_t>(r0) * L0.Kp;
   if (p->first) {
+    // input copy (device pool or pinned host) on the input stream: with the extra input
+    // slot it overlaps the backward/update still running on the compute stream
     const size_t w = static_cast<size_t>(L0.in) * 2;
-    CUDA_OK(cudaMemcpy2DAsync(X, static_cast<size_t>(L0.Kp) * 2, x, w, w, nr, cudaMemcpyDefault, p->cs));
+    CUDA_OK(cudaStreamWaitEvent(p->s_fin, p->ev_act_free[slot0], 0));
+    CUDA_OK(cudaMemcpy2DAsync(X, static_cast<size_t>(L0.Kp) * 2, x, w, w, nr, cudaMemcpyDefault, p->s_fin));
+    CUDA_OK(cudaEventRecord(p->ev_recv, p->s_fin));
+    CUDA_OK(cudaStreamWaitEvent(p->cs, p->ev_recv, 0));
   } else {
     TPS_TRY(recv_fwd(p, j, grp, X, static_cast<size_t>(nr) * L0.Kp * 2));
   }
@@ -524,44 +532,58 @@ tps_status do_backward(tps_pipeline* p, int64_t j, int staleness) {
   const int slot0 = static_cast<int>(j % p->A0);
   const int slot = static_cast<int>(j % p->Kmax);
   int wbuf = 0;
+  const int64_t vn = vl + 1;   // version the update of this mini-batch produces
   for (int k = nl - 1; k >= 0; --k) {
     Layer& Lk = p->layers[k];
     const uint16_t* X = (k == 0) ? p->act[slot0][0] : p->act[slot][k];
-    // wgrad: dW[Np, Kp] = Gᵀ·X   (A = G stored [B, Np], B = X stored [B, Kp])
+    // dgrad first: it must read this layer's weights before a fused update rewrites them
+    uint16_t* dst = nullptr;
+    if (Lk.gidx > 0) {  // the network's first layer has no dgrad
+      if (k > 0) {
+        dst = p->gwork[wbuf];
+        wbuf ^= 1;
+      } else {
+        CUDA_OK(cudaStreamWaitEvent(p->cs, p->ev_bwd_sent[j & 1], 0));  // gout of mb j-2 has left
+        dst = p->gout[j & 1];
+      }
+      const uint16_t* Ws = Lk.ver[v_used % p->R];
+      const uint16_t* Wl = Lk.ver[vl % p->R];
+      tps::GemmArgs ga{};
+      ga.M = p->B; ga.N = Lk.Kp; ga.K = Lk.Np; ga.out = dst; ga.ldo = Lk.Kp; ga.out_f32 = 0;
+      ga.mask = X; ga.ldm = Lk.Kp; ga.alpha = 1.f; ga.xa = 1.f; ga.xb = 0.f;
+      const bool blend_on_load =
+          p->variant == TPS_I && delta > 0 && (p->blend == TPS_BLEND_CONVEX || p->eq1_on_load);
+      if (blend_on_load) {
+        tps::GemmOperands op{G, Lk.Np, Ws, Lk.Kp, Wl};
+        ga.xa = alpha; ga.xb = beta;
+        TPS_TRY(run_gemm(p, tps::GEMM_DGRAD_BLEND, op, ga, 1));
+      } else {
+        tps::GemmOperands op{G, Lk.Np, Ws, Lk.Kp, nullptr};
+        ga.alpha = (p->variant == TPS_I) ? alpha : 1.f;   // EQ1: α·(G·W_stash) = G·(α·W_stash)
+        TPS_TRY(run_gemm(p, tps::GEMM_DGRAD, op, ga, 1));
+      }
+    }
+    // wgrad: dW[Np, Kp] = Gᵀ·X   (A = G stored [B, Np], B = X stored [B, Kp]); with fuse_update
+    // the epilogue applies the SGD/momentum step and writes version vn instead of storing dW
     {
       tps::GemmOperands op{G, Lk.Np, X, Lk.Kp, nullptr};
       tps::GemmArgs ga{};
       ga.M = Lk.Np; ga.N = Lk.Kp; ga.K = p->B; ga.out = Lk.dW; ga.ldo = Lk.Kp; ga.out_f32 = 1;
       ga.alpha = 1.f; ga.xa = 1.f;
+      if (p->fuse_update) {
+        ga.epi = tps::EPI_SGD;
+        ga.w = Lk.W; ga.v = Lk.mW; ga.ver = Lk.ver[vn % p->R];
+        ga.lr = p->lr; ga.mu = p->mu; ga.wd = p->wd;
+      }
       TPS_TRY(run_gemm(p, tps::GEMM_WGRAD, op, ga, 2));
     }
     CUDA_OK(tps::launch_bias_grad(G, p->B, Lk.Np, Lk.Np, Lk.db, p->scratch, p->cs));
     p->launches += 2;
-    if (Lk.gidx == 0) break;  // the network's first layer has no dgrad
-    uint16_t* dst;
-    if (k > 0) {
-      dst = p->gwork[wbuf];
-      wbuf ^= 1;
-    } else {
-      CUDA_OK(cudaStreamWaitEvent(p->cs, p->ev_bwd_sent[j & 1], 0));  // gout of mb j-2 has left
-      dst = p->gout[j & 1];
+    if (p->fuse_update) {
+      CUDA_OK(tps::launch_sgd_update(Lk.b, Lk.mb, Lk.db, nullptr, Lk.Np, p->lr, p->mu, p->wd, p->cs));
+      p->launches += 1;
     }
-    const uint16_t* Ws = Lk.ver[v_used % p->R];
-    const uint16_t* Wl = Lk.ver[vl % p->R];
-    tps::GemmArgs ga{};
-    ga.M = p->B; ga.N = Lk.Kp; ga.K = Lk.Np; ga.out = dst; ga.ldo = Lk.Kp; ga.out_f32 = 0;
-    ga.mask = X; ga.ldm = Lk.Kp; ga.alpha = 1.f; ga.xa = 1.f; ga.xb = 0.f;
-    const bool blend_on_load = p->variant == TPS_I && delta > 0 && (p->blend == TPS_BLEND_CONVEX || p->eq1_on_load);
-    if (blend_on_load) {
-      tps::GemmOperands op{G, Lk.Np, Ws, Lk.Kp, Wl};
-      ga.xa = alpha; ga.xb = beta;
-      TPS_TRY(run_gemm(p, tps::GEMM_DGRAD_BLEND, op, ga, 1));
-    } else {
-      tps::GemmOperands op{G, Lk.Np, Ws, Lk.Kp, nullptr};
-      ga.alpha = (p->variant == TPS_I) ? alpha : 1.f;   // EQ1: α·(G·W_stash) = G·(α·W_stash)
-      TPS_TRY(run_gemm(p, tps::GEMM_DGRAD, op, ga, 1));
-    }
-    G = dst;
+    if (dst) G = dst;
   }
   // the input slot and the received gradient buffer may now be refilled
   CUDA_OK(cudaEventRecord(p->ev_act_free[slot0], p->cs));
@@ -585,6 +607,7 @@ tps_status do_update(tps_pipeline* p, int64_t j) {
   if (p->pending_update != j) return fail(TPS_E_ORDER, "update of mb %lld without its backward", (long long)j);
   const int64_t vn = p->latest + 1;
   for (auto& Lk : p->layers) {
+    if (p->fuse_update) break;   // already applied by the wgrad epilogues of B(j)
     const int64_t n = static_cast<int64_t>(Lk.Np) * Lk.Kp;
     TimedLaunch tl{};
     TPS_TRY(time_begin(p, &tl, 4, (p->mu != 0.f ? 22.0 : 14.0) * n));
@@ -702,9 +725,10 @@ tps_status tps_pipeline_init(const tps_config* c, tps_pipeline** out) {
   p->classes = c->dims[c->num_layers];
   p->Kmax = p->S - p->s;                         // in-flight mini-batches (reading Z6)
   p->R = (p->variant == TPS_I) ? p->Kmax : 1;    // weight version ring
-  p->A0 = p->Kmax + ((c->extra_recv_slot && !p->first) ? 1 : 0);
+  p->A0 = p->Kmax + (c->extra_recv_slot ? 1 : 0);
   const char* env = std::getenv("TPS_EQ1_ON_LOAD");
   p->eq1_on_load = env && env[0] == '1';
+  p->fuse_update = c->fuse_update != 0;
 
   auto cleanup = [&](tps_status st) {
     tps_pipeline_destroy(p);
@@ -724,7 +748,7 @@ tps_status tps_pipeline_init(const tps_config* c, tps_pipeline** out) {
       if ((st = alloc_t(p, &L.mW, n, &p->mem_optim)) != TPS_OK) return cleanup(st);
       if ((st = alloc_t(p, &L.mb, L.Np, &p->mem_optim)) != TPS_OK) return cleanup(st);
     }
-    if ((st = alloc_t(p, &L.dW, n, &p->mem_optim)) != TPS_OK) return cleanup(st);
+    if (!p->fuse_update && (st = alloc_t(p, &L.dW, n, &p->mem_optim)) != TPS_OK) return cleanup(st);
     if ((st = alloc_t(p, &L.db, L.Np, &p->mem_optim)) != TPS_OK) return cleanup(st);
     L.ver.resize(p->R);
     for (int r = 0; r < p->R; ++r)

@@ -53,7 +53,8 @@ class Config(C.Structure):
                 ("blend", C.c_int32), ("lambda_", C.c_double), ("lr", C.c_float), ("momentum", C.c_float),
                 ("weight_decay", C.c_float), ("transport", C.c_int32), ("nccl_ids", C.c_void_p),
                 ("device", C.c_int32), ("seed", C.c_uint64), ("compute_stream", C.c_uint64),
-                ("extra_recv_slot", C.c_int32), ("reserved", C.c_int32 * 7)]
+                ("extra_recv_slot", C.c_int32), ("fuse_update", C.c_int32),
+                ("reserved", C.c_int32 * 6)]
 
 
 _LIB = None
@@ -173,6 +174,7 @@ class StageSpec:
     seed: int = 0
     compute_stream: int = 0
     extra_recv_slot: int = 1
+    fuse_update: int = 1
     _keep: list = field(default_factory=list)
 
 
@@ -191,7 +193,8 @@ class Pipeline:
                      blend=spec.blend, lambda_=spec.lam, lr=spec.lr, momentum=spec.momentum,
                      weight_decay=spec.weight_decay, transport=spec.transport,
                      nccl_ids=C.cast(ids, C.c_void_p) if ids is not None else None, device=spec.device,
-                     seed=spec.seed, compute_stream=spec.compute_stream, extra_recv_slot=spec.extra_recv_slot)
+                     seed=spec.seed, compute_stream=spec.compute_stream, extra_recv_slot=spec.extra_recv_slot,
+                     fuse_update=spec.fuse_update)
         h = C.c_void_p()
         check(lib().tps_pipeline_init(C.byref(cfg), C.byref(h)))
         self.h = h

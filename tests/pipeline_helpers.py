@@ -25,7 +25,7 @@ def run_oracle(dims, bounds, m, b, M, variant, blend, lam, lr, mu, wd=0.0, seed=
 
 
 def run_gpu(dims, bounds, m, b, M, variant, blend, lam, lr, mu, wd=0.0, seed=0, kind=synthgen.X_SIGNED,
-            fwd_group=0, init="set", extra_recv_slot=1, stepwise=False):
+            fwd_group=0, init="set", extra_recv_slot=1, fuse_update=1):
     """All S stages as LOCAL-transport handles on cuda:0; returns (stages, losses)."""
     import torch
 
@@ -42,7 +42,7 @@ def run_gpu(dims, bounds, m, b, M, variant, blend, lam, lr, mu, wd=0.0, seed=0, 
         spec = tps.StageSpec(dims=dims, stage_bounds=bounds, stage_id=s, micro_batches=m, micro_batch_size=b,
                              fwd_group=fwd_group, variant=V, blend=BL, lam=lam, lr=lr, momentum=mu, weight_decay=wd,
                              transport=tps.TPS_TRANSPORT_LOCAL if S > 1 else tps.TPS_TRANSPORT_NONE, seed=seed,
-                             extra_recv_slot=extra_recv_slot)
+                             extra_recv_slot=extra_recv_slot, fuse_update=fuse_update)
         st = tps.Pipeline(spec)
         if init == "set":
             for k, l in enumerate(st.layers):

@@ -39,10 +39,11 @@ CASES = {
 
 
 @pytest.mark.parametrize("name", list(CASES))
-def test_parity_with_oracle(gpu_lib, name):
+@pytest.mark.parametrize("fuse", [1, 0])
+def test_parity_with_oracle(gpu_lib, name, fuse):
     dims, bounds, m, b, M, var, blend, lam, lr, mu, kind = CASES[name]
     ref = run_oracle(dims, bounds, m, b, M, var, blend, lam, lr, mu, kind=kind)
-    stages, losses = run_gpu(dims, bounds, m, b, M, var, blend, lam, lr, mu, kind=kind)
+    stages, losses = run_gpu(dims, bounds, m, b, M, var, blend, lam, lr, mu, kind=kind, fuse_update=fuse)
     # schedule, versions, δ, α, β: bit-exact
     assert expand_gpu_trace(stages) == oracle_trace(ref)
     # losses: 1e-3 relative

@@ -1,0 +1,61 @@
+"""Microbenchmark of the stage GEMM modes at the bench shapes (C5: B=2048, d=4096),
+CUDA-event timed, with cuBLAS (torch.matmul) beside it for context."""
+import argparse
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2509_23241_b200 import tps  # noqa: E402
+
+
+def timeit(fn, iters=20, warm=5):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(iters):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / iters
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--M", type=int, default=2048)
+    ap.add_argument("--N", type=int, default=4096)
+    ap.add_argument("--K", type=int, default=4096)
+    ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--modes", default="0,1,2,3")
+    a = ap.parse_args()
+    M, N, K = a.M, a.N, a.K
+    X = torch.randn(M, K, device="cuda").to(torch.bfloat16)          # fwd A / dgrad A (G)
+    W = (torch.randn(N, K, device="cuda") * K ** -0.5).to(torch.bfloat16)
+    Wt = (torch.randn(K, N, device="cuda") * K ** -0.5).to(torch.bfloat16)  # dgrad B stored [K, N]
+    W2 = Wt.clone()
+    Gk = torch.randn(K, M, device="cuda").to(torch.bfloat16)          # wgrad A stored [K, M]
+    Xk = torch.randn(K, N, device="cuda").to(torch.bfloat16)          # wgrad B stored [K, N]
+    mask = torch.randn(M, N, device="cuda").to(torch.bfloat16)
+    bias = torch.zeros(N, device="cuda")
+    ob = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    of = torch.empty(M, N, device="cuda", dtype=torch.float32)
+    fl = 2.0 * M * N * K
+    runs = {
+        0: ("fwd  (K-major A,B; bias+ReLU)", lambda: tps.gemm(0, M, N, K, X, K, W, K, ob, N, 0, bias, 1)),
+        1: ("dgrad(MN-major B; α, mask)", lambda: tps.gemm(1, M, N, K, X, K, Wt, N, ob, N, 0, None, 0, 0.9, 0.0, mask, N)),
+        2: ("wgrad(MN-major A,B; fp32)", lambda: tps.gemm(2, M, N, K, Gk, M, Xk, N, of, N, 1)),
+        3: ("dgrad blend-on-load", lambda: tps.gemm(3, M, N, K, X, K, Wt, N, ob, N, 0, None, 0, 0.7, 0.3, mask, N, B2=W2)),
+    }
+    for m in [int(x) for x in a.modes.split(",")]:
+        name, fn = runs[m]
+        ms = timeit(fn, a.iters)
+        print(f"mode {m} {name:34s} {M}x{N}x{K}: {ms*1e3:8.1f} us  {fl/ms/1e9:7.1f} TFLOP/s", flush=True)
+    ms = timeit(lambda: torch.matmul(X, W.T), a.iters)
+    print(f"cuBLAS torch.matmul bf16 {M}x{N}x{K}: {ms*1e3:8.1f} us  {fl/ms/1e9:7.1f} TFLOP/s")
+
+
+if __name__ == "__main__":
+    main()
