@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-v", action="store_true")
     ap.add_argument("--fwd-group", type=int, default=0)
+    ap.add_argument("--fuse-update", type=int, default=0, help="1: SGD update in the wgrad epilogue")
     return ap.parse_args()
 
 
@@ -170,7 +171,7 @@ def config_dict(args):
             "stages": S, "micro_batch": MICRO_B, "micro_batches": MICRO_M, "global_batch": MICRO_B * MICRO_M,
             "variant": "I-TiMePReSt EQ1", "lambda": LAM, "optimizer": f"SGD lr={LR} momentum={MU}",
             "step": f"one pipeline epoch = {args.epoch_mb} mini-batches (fill+steady+drain)",
-            "parallelism": f"pp{S}", "l2": "inputs+weights per step >> 126 MB L2 (no flush needed)"}
+            "fused_update": bool(args.fuse_update), "parallelism": f"pp{S}", "l2": "inputs+weights per step >> 126 MB L2 (no flush needed)"}
 
 
 # ------------------------------------------------------------------ GPU leg
@@ -206,7 +207,8 @@ def main():
                              micro_batch_size=MICRO_B, fwd_group=args.fwd_group, variant=variant,
                              blend=tps.TPS_BLEND_EQ1, lam=LAM, lr=LR, momentum=MU,
                              transport=tps.TPS_TRANSPORT_NCCL if S > 1 else tps.TPS_TRANSPORT_NONE,
-                             nccl_ids=ids, device=local, seed=0, compute_stream=stream)
+                             nccl_ids=ids, device=local, seed=0, compute_stream=stream,
+                             fuse_update=args.fuse_update)
         p = tps.Pipeline(spec)
         p.init_weights_synthetic()
         return p
