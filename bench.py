@@ -282,6 +282,11 @@ def main():
     ms_prof, _, _ = timed_epochs(pI, max(1, args.steps // 2), 0, x_pool, y_pool, profile=True)
     # per-kernel stats (GEMMs on the compute stream, CUDA events around every launch)
     n_g, ms_g, fl_g = pI.kernel_stats(3)
+    per_kind = {}
+    for kind, nm in ((0, "fwd"), (1, "dgrad"), (2, "wgrad" + ("+update" if args.fuse_update else ""))):
+        n_k, ms_k, fl_k = pI.kernel_stats(kind)
+        if n_k:
+            per_kind[nm] = {"launches": n_k, "ms": round(ms_k, 3), "tflops": round(fl_k / (ms_k * 1e-3) / 1e12, 1)}
     n_u, ms_u, by_u = pI.kernel_stats(4)
     memI = pI.memory_stats()
     lossesI = pI.losses()
@@ -356,6 +361,7 @@ def main():
                          "frac_of_burst_peak": (achieved / peaks["bf16_tflops"]) if achieved else None,
                          "peak_source": f"{src} bf16_tflops_sustained (MEASURED_PEAKS.json)",
                          "gemm_launches": n_g, "gemm_ms": ms_g, "gemm_share_of_step": gemm_share,
+                         "per_kind": per_kind,
                          "step_tensor_frac": fps * value / world / 1e12 / peak,
                          "update_kernel": {"bound": "hbm", "achieved_gbs": (by_u / (ms_u * 1e-3) / 1e9) if n_u else None,
                                            "peak_gbs": peaks.get("hbm_gbs"), "launches": n_u, "ms": ms_u}},

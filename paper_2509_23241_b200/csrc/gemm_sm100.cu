@@ -14,8 +14,9 @@
 // Roles (one CTA per SM, persistent over output tiles 128 x BN):
 //   warp 0      TMA producer (one elected lane): A/B tiles -> 128B-swizzled smem ring
 //   warp 1      MMA issuer (one lane): tcgen05.mma kind::f16, fp32 accumulators in TMEM
-//   warps 2..5  epilogue: tcgen05.ld TMEM -> registers -> bias/ReLU/α/mask -> global
-//   warps 6..9  (BLEND only) operand transform warps
+//   warps 2..9  epilogue: tcgen05.ld TMEM -> registers -> smem transpose -> bias/ReLU/α/mask
+//               (or the fused SGD update) -> coalesced global row segments
+//   warps 10..13 (BLEND only) operand transform warps
 // TMEM holds two accumulators (2·BN columns) so the epilogue of tile i overlaps the
 // MMAs of tile i+1.
 #include <cuda.h>
@@ -37,16 +38,19 @@ constexpr int BM = 128;
 constexpr int BK = 64;                     // 64 bf16 = 128 B = one swizzle atom row
 constexpr int A_BYTES = BM * BK * 2;       // 16 KiB
 constexpr int SMEM_BUDGET = 227 * 1024;
+constexpr int EPI_WARPS = 8;
+constexpr int EPI_SMEM = EPI_WARPS * 32 * 33 * 4;   // per-warp 32x33 fp32 transpose buffer
 
-template <int BN, int BLEND>
+template <int BN, int BLEND, int SGD = 0>
 struct Cfg {
+  static constexpr int EPI = SGD ? EPI_SMEM : 0;   // transpose buffer only for the fused update
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES * (BLEND ? 3 : 1);
-  static constexpr int STAGES_RAW = (SMEM_BUDGET - 2048) / STAGE_BYTES;
+  static constexpr int STAGES_RAW = (SMEM_BUDGET - 2048 - EPI) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
-  static constexpr int THREADS = BLEND ? 320 : 192;
+  static constexpr int THREADS = 32 * (2 + EPI_WARPS + (BLEND ? 4 : 0));
   static constexpr int TMEM_COLS = 2 * BN;
-  static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + 256;
+  static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + EPI + 256;
   static constexpr uint32_t TX = A_BYTES + B_BYTES * (BLEND ? 2 : 1);
 };
 
@@ -68,11 +72,11 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
-template <int BN, int A_MN, int B_MN, int BLEND>
-__global__ void __launch_bounds__(Cfg<BN, BLEND>::THREADS, 1)
+template <int BN, int A_MN, int B_MN, int BLEND, int SGD>
+__global__ void __launch_bounds__(Cfg<BN, BLEND, SGD>::THREADS, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmB2, const GemmArgs args) {
-  using C = Cfg<BN, BLEND>;
+  using C = Cfg<BN, BLEND, SGD>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* stages = smem;
@@ -82,6 +86,7 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND>::THREADS, 1)
   uint64_t* tmem_full = xform + C::STAGES;
   uint64_t* tmem_empty = tmem_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+  float* epi_stage = reinterpret_cast<float*>(smem + C::STAGES * C::STAGE_BYTES + 256);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -101,7 +106,7 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND>::THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tmem_full[a], 1);
-      ptx::mbar_init(&tmem_empty[a], 4);
+      ptx::mbar_init(&tmem_empty[a], EPI_WARPS);
     }
     ptx::fence_barrier_init();
   }
@@ -182,10 +187,13 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND>::THREADS, 1)
         ptx::umma_commit(&tmem_full[acc]);
       }
     }
-  } else if (warp < 6) {
+  } else if (warp < 2 + EPI_WARPS) {
     // ===================== epilogue =====================
+    // 8 warps: warp w reads TMEM lane quarter (w % 4) and handles every other 32-column chunk.
+    const int e = warp - 2;
     const int q = warp & 3;                 // TMEM lane quarter this warp may access
-    const int row = q * 32 + lane;
+    const int half = e >> 2;
+    float* stg = epi_stage + e * (32 * 33);
     int it = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
       int mb, nb;
@@ -194,15 +202,59 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND>::THREADS, 1)
       const uint32_t acc_phase = (it >> 1) & 1;
       ptx::mbar_wait(&tmem_full[acc], acc_phase);
       ptx::tc_fence_after();
-      const int grow = mb * BM + row;
-      const bool row_ok = grow < args.M;
+      const int row0 = mb * BM + q * 32;
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = half; c < BN / 32; c += 2) {
         uint32_t r[32];
         ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c * 32, r);
         ptx::tmem_ld_wait();
+        if (c + 2 >= BN / 32) {             // last TMEM read of this warp for this tile
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(&tmem_empty[acc]);
+        }
+        if (SGD) {
+          // fused update (row a10), staged through smem so lane = column and every access is a
+          // coalesced 128-byte row segment:  g' = g + wd·w ; v = μ·v + g' ; w = w - lr·v ; bf16(w)
+#pragma unroll
+          for (int i = 0; i < 32; ++i) stg[lane * 33 + i] = __uint_as_float(r[i]);
+          __syncwarp();
+          const int gcol = nb * BN + c * 32 + lane;
+          const bool col_ok = gcol < args.N;
+          const int rows = min(32, args.M - row0);
+#pragma unroll 1
+          for (int r0 = 0; r0 < rows; r0 += 16) {
+            float wv[16], vv[16];
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+              const size_t off = static_cast<size_t>(row0 + r0 + k) * args.ldo + gcol;
+              const bool ok = col_ok && (r0 + k) < rows;
+              wv[k] = ok ? args.w[off] : 0.0f;
+              vv[k] = (ok && args.mu != 0.0f) ? args.v[off] : 0.0f;
+            }
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+              if (!col_ok || (r0 + k) >= rows) continue;
+              const size_t off = static_cast<size_t>(row0 + r0 + k) * args.ldo + gcol;
+              const float g = stg[(r0 + k) * 33 + lane];
+              const float gp = __fadd_rn(g, __fmul_rn(args.wd, wv[k]));
+              float upd = gp;
+              if (args.mu != 0.0f) {
+                upd = __fadd_rn(__fmul_rn(args.mu, vv[k]), gp);
+                args.v[off] = upd;
+              }
+              const float wn = __fsub_rn(wv[k], __fmul_rn(args.lr, upd));
+              args.w[off] = wn;
+              reinterpret_cast<__nv_bfloat16*>(args.ver)[off] = __float2bfloat16_rn(wn);
+            }
+          }
+          __syncwarp();
+          continue;
+        }
+        // plain epilogue: thread = row, 16-byte vector loads/stores along the row
+        const int grow = row0 + lane;
         const int gcol = nb * BN + c * 32;
-        if (!row_ok || gcol >= args.N) continue;
+        if (grow >= args.M || gcol >= args.N) continue;
         float v[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
@@ -241,58 +293,15 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND>::THREADS, 1)
               const uint4 mv = __ldg(mp + ch);
               const uint32_t w[4] = {mv.x, mv.y, mv.z, mv.w};
 #pragma unroll
-              for (int e = 0; e < 8; ++e) {
-                const uint32_t h = (w[e >> 1] >> ((e & 1) * 16)) & 0xFFFFu;
+              for (int e2 = 0; e2 < 8; ++e2) {
+                const uint32_t h = (w[e2 >> 1] >> ((e2 & 1) * 16)) & 0xFFFFu;
                 const bool pos = ((h & 0x8000u) == 0u) && ((h & 0x7FFFu) != 0u);
-                if (!pos) v[ch * 8 + e] = 0.0f;
+                if (!pos) v[ch * 8 + e2] = 0.0f;
               }
             }
           }
         }
-        if (args.epi == EPI_SGD) {
-          // fused update (row a10): g' = g + wd·w ; v = μ·v + g' ; w = w - lr·v ; ver = bf16(w)
-          const size_t off = static_cast<size_t>(grow) * args.ldo + gcol;
-          float* wp = args.w + off;
-          float* vp = args.v + off;
-          uint16_t* qp = args.ver + off;
-#pragma unroll
-          for (int ch = 0; ch < 4; ++ch) {
-            if (ch < nchunk) {
-              float4 w0 = reinterpret_cast<float4*>(wp + ch * 8)[0];
-              float4 w1 = reinterpret_cast<float4*>(wp + ch * 8)[1];
-              float ww[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
-              float vv[8];
-              if (args.mu != 0.0f) {
-                const float4 v0 = reinterpret_cast<float4*>(vp + ch * 8)[0];
-                const float4 v1 = reinterpret_cast<float4*>(vp + ch * 8)[1];
-                vv[0] = v0.x; vv[1] = v0.y; vv[2] = v0.z; vv[3] = v0.w;
-                vv[4] = v1.x; vv[5] = v1.y; vv[6] = v1.z; vv[7] = v1.w;
-              }
-#pragma unroll
-              for (int e = 0; e < 8; ++e) {
-                const float gp = __fadd_rn(v[ch * 8 + e], __fmul_rn(args.wd, ww[e]));
-                float upd = gp;
-                if (args.mu != 0.0f) {
-                  vv[e] = __fadd_rn(__fmul_rn(args.mu, vv[e]), gp);
-                  upd = vv[e];
-                }
-                ww[e] = __fsub_rn(ww[e], __fmul_rn(args.lr, upd));
-              }
-              reinterpret_cast<float4*>(wp + ch * 8)[0] = make_float4(ww[0], ww[1], ww[2], ww[3]);
-              reinterpret_cast<float4*>(wp + ch * 8)[1] = make_float4(ww[4], ww[5], ww[6], ww[7]);
-              if (args.mu != 0.0f) {
-                reinterpret_cast<float4*>(vp + ch * 8)[0] = make_float4(vv[0], vv[1], vv[2], vv[3]);
-                reinterpret_cast<float4*>(vp + ch * 8)[1] = make_float4(vv[4], vv[5], vv[6], vv[7]);
-              }
-              uint4 o;
-              o.x = pack_bf16(ww[0], ww[1]);
-              o.y = pack_bf16(ww[2], ww[3]);
-              o.z = pack_bf16(ww[4], ww[5]);
-              o.w = pack_bf16(ww[6], ww[7]);
-              reinterpret_cast<uint4*>(qp)[ch] = o;
-            }
-          }
-        } else if (args.out_f32) {
+        if (args.out_f32) {
           float* op = reinterpret_cast<float*>(args.out) + static_cast<size_t>(grow) * args.ldo + gcol;
 #pragma unroll
           for (int ch = 0; ch < 4; ++ch) {
@@ -317,13 +326,10 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND>::THREADS, 1)
           }
         }
       }
-      ptx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&tmem_empty[acc]);
     }
   } else if (BLEND) {
     // ===================== operand transform: W_res = α·W_stash + β·W_latest =====================
-    const int tt = threadIdx.x - 6 * 32;    // 0..127
+    const int tt = threadIdx.x - (2 + EPI_WARPS) * 32;    // 0..127
     const float xa = args.xa, xb = args.xb;
     int stage = 0;
     uint32_t phase = 0;
@@ -409,11 +415,11 @@ int num_sms() {
   return n;
 }
 
-template <int BN, int A_MN, int B_MN, int BLEND>
+template <int BN, int A_MN, int B_MN, int BLEND, int SGD = 0>
 cudaError_t launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& b2, const GemmArgs& args,
                    cudaStream_t st) {
-  using C = Cfg<BN, BLEND>;
-  auto kern = gemm_kernel<BN, A_MN, B_MN, BLEND>;
+  using C = Cfg<BN, BLEND, SGD>;
+  auto kern = gemm_kernel<BN, A_MN, B_MN, BLEND, SGD>;
   static bool attr_set = false;   // per instantiation
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
@@ -479,6 +485,11 @@ cudaError_t gemm_run(int mode, const GemmOperands& op, const GemmArgs& args_in, 
       if (bn == 128) return launch<128, 0, 1, 0>(ta, tb, tb2, args, st);
       return launch<64, 0, 1, 0>(ta, tb, tb2, args, st);
     case GEMM_WGRAD:
+      if (args.epi == EPI_SGD) {
+        if (bn == 256) return launch<256, 1, 1, 0, 1>(ta, tb, tb2, args, st);
+        if (bn == 128) return launch<128, 1, 1, 0, 1>(ta, tb, tb2, args, st);
+        return launch<64, 1, 1, 0, 1>(ta, tb, tb2, args, st);
+      }
       if (bn == 256) return launch<256, 1, 1, 0>(ta, tb, tb2, args, st);
       if (bn == 128) return launch<128, 1, 1, 0>(ta, tb, tb2, args, st);
       return launch<64, 1, 1, 0>(ta, tb, tb2, args, st);

@@ -154,6 +154,8 @@ struct tps_pipeline {
   cudaStream_t cs = nullptr;
   bool own_cs = false;
   cudaStream_t s_fin = nullptr, s_fout = nullptr, s_bin = nullptr, s_bout = nullptr;
+  cudaStream_t s_upd = nullptr;                        // optimizer stream (overlaps the next GEMMs)
+  std::vector<cudaEvent_t> ev_grad_ready, ev_upd_done;  // per layer
   std::vector<cudaEvent_t> ev_fwd_ready, ev_fwd_sent;  // [2 * ng]
   std::vector<cudaEvent_t> ev_act_free;                // [A0]
   cudaEvent_t ev_recv = nullptr, ev_gin_free[2] = {nullptr, nullptr}, ev_gout_ready = nullptr,
@@ -273,7 +275,7 @@ tps_status run_gemm(tps_pipeline* p, int mode, const tps::GemmOperands& op, cons
   return TPS_OK;
 }
 
-tps_status time_begin(tps_pipeline* p, TimedLaunch* tl, int kind, double work) {
+tps_status time_begin(tps_pipeline* p, TimedLaunch* tl, int kind, double work, cudaStream_t st = nullptr) {
   if (!p->profiling) return TPS_OK;
   if (p->ev_pool.size() < 2) {
     for (int i = 0; i < 64; ++i) {
@@ -286,13 +288,13 @@ tps_status time_begin(tps_pipeline* p, TimedLaunch* tl, int kind, double work) {
   tl->work = work;
   tl->a = p->ev_pool.back(); p->ev_pool.pop_back();
   tl->b = p->ev_pool.back(); p->ev_pool.pop_back();
-  CUDA_OK(cudaEventRecord(tl->a, p->cs));
+  CUDA_OK(cudaEventRecord(tl->a, st ? st : p->cs));
   return TPS_OK;
 }
 
-tps_status time_end(tps_pipeline* p, TimedLaunch* tl) {
+tps_status time_end(tps_pipeline* p, TimedLaunch* tl, cudaStream_t st = nullptr) {
   if (!p->profiling) return TPS_OK;
-  CUDA_OK(cudaEventRecord(tl->b, p->cs));
+  CUDA_OK(cudaEventRecord(tl->b, st ? st : p->cs));
   p->timed.push_back(*tl);
   return TPS_OK;
 }
@@ -308,6 +310,19 @@ tps_status drain_timing(tps_pipeline* p) {
     p->ev_pool.push_back(t.b);
   }
   p->timed.clear();
+  return TPS_OK;
+}
+
+// make the compute stream wait for the optimizer stream (end of a run: the caller's
+// stream-ordered view then includes every update of the run)
+tps_status join_update_stream(tps_pipeline* p) {
+  for (auto e : p->ev_upd_done) CUDA_OK(cudaStreamWaitEvent(p->cs, e, 0));
+  return TPS_OK;
+}
+
+tps_status sync_streams(tps_pipeline* p) {
+  CUDA_OK(cudaStreamSynchronize(p->cs));
+  if (p->s_upd) CUDA_OK(cudaStreamSynchronize(p->s_upd));
   return TPS_OK;
 }
 
@@ -450,6 +465,7 @@ tps_status do_forward(tps_pipeline* p, int64_t j, int a0, int cnt, const void* x
   const uint16_t* Xin = X;
   for (int k = 0; k < nl; ++k) {
     Layer& Lk = p->layers[k];
+    CUDA_OK(cudaStreamWaitEvent(p->cs, p->ev_upd_done[k], 0));   // latest version of layer k written
     tps::GemmOperands op{Xin, Lk.Kp, Lk.ver[v % p->R], Lk.Kp, nullptr};
     tps::GemmArgs ga{};
     ga.M = nr; ga.N = Lk.Np; ga.K = Lk.Kp; ga.alpha = 1.f; ga.bias = Lk.b; ga.xa = 1.f; ga.xb = 0.f;
@@ -579,10 +595,24 @@ tps_status do_backward(tps_pipeline* p, int64_t j, int staleness) {
     }
     CUDA_OK(tps::launch_bias_grad(G, p->B, Lk.Np, Lk.Np, Lk.db, p->scratch, p->cs));
     p->launches += 2;
-    if (p->fuse_update) {
-      CUDA_OK(tps::launch_sgd_update(Lk.b, Lk.mb, Lk.db, nullptr, Lk.Np, p->lr, p->mu, p->wd, p->cs));
+    // U(j) always directly follows B(j) in the static order (reading Z7), so the update of
+    // this layer is issued now: either it already ran in the wgrad epilogue (fuse_update), or
+    // it runs on the optimizer stream, HBM-bound, underneath the remaining tensor-bound GEMMs
+    // of this backward.  The next forward of layer k waits for ev_upd_done[k].
+    cudaStream_t us = p->fuse_update ? p->cs : p->s_upd;
+    if (!p->fuse_update) {
+      CUDA_OK(cudaEventRecord(p->ev_grad_ready[k], p->cs));
+      CUDA_OK(cudaStreamWaitEvent(us, p->ev_grad_ready[k], 0));
+      const int64_t n = static_cast<int64_t>(Lk.Np) * Lk.Kp;
+      TimedLaunch tl{};
+      TPS_TRY(time_begin(p, &tl, 4, (p->mu != 0.f ? 22.0 : 14.0) * n, us));
+      CUDA_OK(tps::launch_sgd_update(Lk.W, Lk.mW, Lk.dW, Lk.ver[vn % p->R], n, p->lr, p->mu, p->wd, us));
+      TPS_TRY(time_end(p, &tl, us));
       p->launches += 1;
     }
+    CUDA_OK(tps::launch_sgd_update(Lk.b, Lk.mb, Lk.db, nullptr, Lk.Np, p->lr, p->mu, p->wd, us));
+    p->launches += 1;
+    CUDA_OK(cudaEventRecord(p->ev_upd_done[k], us));
     if (dst) G = dst;
   }
   // the input slot and the received gradient buffer may now be refilled
@@ -606,16 +636,8 @@ tps_status do_update(tps_pipeline* p, int64_t j) {
   TPS_TRY(expect(p, TPS_EV_U, j, -1, 0));
   if (p->pending_update != j) return fail(TPS_E_ORDER, "update of mb %lld without its backward", (long long)j);
   const int64_t vn = p->latest + 1;
-  for (auto& Lk : p->layers) {
-    if (p->fuse_update) break;   // already applied by the wgrad epilogues of B(j)
-    const int64_t n = static_cast<int64_t>(Lk.Np) * Lk.Kp;
-    TimedLaunch tl{};
-    TPS_TRY(time_begin(p, &tl, 4, (p->mu != 0.f ? 22.0 : 14.0) * n));
-    CUDA_OK(tps::launch_sgd_update(Lk.W, Lk.mW, Lk.dW, Lk.ver[vn % p->R], n, p->lr, p->mu, p->wd, p->cs));
-    TPS_TRY(time_end(p, &tl));
-    CUDA_OK(tps::launch_sgd_update(Lk.b, Lk.mb, Lk.db, nullptr, Lk.Np, p->lr, p->mu, p->wd, p->cs));
-    p->launches += 2;
-  }
+  // the parameter update of mb j was issued by its backward (see do_backward); this event
+  // commits the new version vn (ring slot vn mod R) as the stage's latest
   tps_event e{};
   e.stage = p->s; e.kind = TPS_EV_U; e.micro = -1; e.mb = j;
   e.v_used = p->latest; e.v_latest = vn; e.alpha = 1.f;
@@ -793,13 +815,19 @@ tps_status tps_pipeline_init(const tps_config* c, tps_pipeline** out) {
     if (cudaStreamCreateWithFlags(&p->cs, cudaStreamNonBlocking) != cudaSuccess) return cleanup(fail(TPS_E_CUDA, "stream create"));
     p->own_cs = true;
   }
-  for (cudaStream_t* sp : {&p->s_fin, &p->s_fout, &p->s_bin, &p->s_bout})
+  for (cudaStream_t* sp : {&p->s_fin, &p->s_fout, &p->s_bin, &p->s_bout, &p->s_upd})
     if (cudaStreamCreateWithFlags(sp, cudaStreamNonBlocking) != cudaSuccess) return cleanup(fail(TPS_E_CUDA, "stream create"));
   p->ev_fwd_ready.resize(2 * p->ng);
   p->ev_fwd_sent.resize(2 * p->ng);
   for (int i = 0; i < 2 * p->ng; ++i) {
     p->ev_fwd_ready[i] = new_event();
     p->ev_fwd_sent[i] = new_event();
+  }
+  p->ev_grad_ready.resize(nl);
+  p->ev_upd_done.resize(nl);
+  for (int k = 0; k < nl; ++k) {
+    p->ev_grad_ready[k] = new_event();
+    p->ev_upd_done[k] = new_event();
   }
   p->ev_act_free.resize(p->A0);
   for (auto& e : p->ev_act_free) e = new_event();
@@ -844,12 +872,14 @@ tps_status tps_pipeline_destroy(tps_pipeline* p) {
   for (auto e : p->ev_fwd_ready) kill_ev(e);
   for (auto e : p->ev_fwd_sent) kill_ev(e);
   for (auto e : p->ev_act_free) kill_ev(e);
+  for (auto e : p->ev_grad_ready) kill_ev(e);
+  for (auto e : p->ev_upd_done) kill_ev(e);
   for (auto e : p->ev_pool) kill_ev(e);
   for (auto& t : p->timed) { kill_ev(t.a); kill_ev(t.b); }
   for (cudaEvent_t e : {p->ev_recv, p->ev_gout_ready, p->ev_gin_ready, p->ev_gin_free[0], p->ev_gin_free[1],
                         p->ev_bwd_sent[0], p->ev_bwd_sent[1]})
     kill_ev(e);
-  for (cudaStream_t s : {p->s_fin, p->s_fout, p->s_bin, p->s_bout})
+  for (cudaStream_t s : {p->s_fin, p->s_fout, p->s_bin, p->s_bout, p->s_upd})
     if (s) cudaStreamDestroy(s);
   if (p->own_cs && p->cs) cudaStreamDestroy(p->cs);
   if (p->prev_local) p->prev_local->next_local = nullptr;
@@ -904,7 +934,7 @@ tps_status tps_run_schedule(tps_pipeline* p, int64_t first_mb, int64_t n_mb, con
     const tps_event e = p->order[p->pos];
     TPS_TRY(fire(p, e, x_pool, y_pool, pool));
   }
-  return TPS_OK;
+  return join_update_stream(p);
 }
 
 tps_status tps_run_schedule_local(tps_pipeline* const* st, int32_t S, int64_t first_mb, int64_t n_mb,
@@ -943,6 +973,7 @@ tps_status tps_run_schedule_local(tps_pipeline* const* st, int32_t S, int64_t fi
     if (all_done) break;
     if (!progress) return fail(TPS_E_STATE, "local schedule deadlock");
   }
+  for (int s = 0; s < S; ++s) TPS_TRY(join_update_stream(st[s]));
   return TPS_OK;
 }
 
@@ -985,6 +1016,7 @@ tps_status tps_intermediate_weight(tps_pipeline* p, int32_t layer, int32_t stale
   float a, b;
   compute_coeffs(p->variant, p->blend, staleness, p->lambda, &a, &b);
   Layer& L = p->layers[layer];
+  CUDA_OK(cudaStreamWaitEvent(p->cs, p->ev_upd_done[layer], 0));
   const int64_t vs = p->latest - staleness;
   CUDA_OK(tps::launch_blend_materialize(L.ver[vs % p->R], L.ver[p->latest % p->R], static_cast<uint16_t*>(out_bf16),
                                         static_cast<int64_t>(L.Np) * L.Kp, a, b, p->cs));
@@ -997,16 +1029,17 @@ tps_status tps_get_version(tps_pipeline* p, int32_t layer, int32_t staleness, vo
   if (layer < 0 || layer >= p->nlayers() || !out_bf16) return fail(TPS_E_INVALID_ARG, "bad layer/out");
   if (staleness < 0 || staleness > p->latest || staleness >= p->R) return fail(TPS_E_STALENESS, "no live version at staleness %d", staleness);
   Layer& L = p->layers[layer];
+  CUDA_OK(cudaStreamWaitEvent(p->cs, p->ev_upd_done[layer], 0));
   CUDA_OK(cudaMemcpyAsync(out_bf16, L.ver[(p->latest - staleness) % p->R], static_cast<size_t>(L.Np) * L.Kp * 2,
                           cudaMemcpyDeviceToDevice, p->cs));
-  CUDA_OK(cudaStreamSynchronize(p->cs));
+  TPS_TRY(sync_streams(p));
   return TPS_OK;
 }
 
 tps_status tps_get_weights(tps_pipeline* p, int32_t layer, float* w, float* b, float* mw, float* mb) {
   TPS_TRY(check_usable(p));
   if (layer < 0 || layer >= p->nlayers()) return fail(TPS_E_INVALID_ARG, "bad layer %d", layer);
-  CUDA_OK(cudaStreamSynchronize(p->cs));
+  TPS_TRY(sync_streams(p));
   Layer& L = p->layers[layer];
   const size_t rowb = static_cast<size_t>(L.in) * 4, ldb = static_cast<size_t>(L.Kp) * 4;
   if (w) CUDA_OK(cudaMemcpy2D(w, rowb, L.W, ldb, rowb, L.out, cudaMemcpyDeviceToHost));
@@ -1025,7 +1058,7 @@ tps_status tps_get_weights(tps_pipeline* p, int32_t layer, float* w, float* b, f
 tps_status tps_set_weights(tps_pipeline* p, int32_t layer, const float* w, const float* b) {
   TPS_TRY(check_usable(p));
   if (layer < 0 || layer >= p->nlayers()) return fail(TPS_E_INVALID_ARG, "bad layer %d", layer);
-  CUDA_OK(cudaStreamSynchronize(p->cs));
+  TPS_TRY(sync_streams(p));
   Layer& L = p->layers[layer];
   const size_t rowb = static_cast<size_t>(L.in) * 4, ldb = static_cast<size_t>(L.Kp) * 4;
   const size_t n = static_cast<size_t>(L.Np) * L.Kp;
@@ -1041,7 +1074,7 @@ tps_status tps_set_weights(tps_pipeline* p, int32_t layer, const float* w, const
   if (L.mb) CUDA_OK(cudaMemset(L.mb, 0, static_cast<size_t>(L.Np) * 4));
   CUDA_OK(tps::launch_f32_to_bf16(L.W, L.ver[p->latest % p->R], static_cast<int64_t>(n), p->cs));
   p->launches += 1;
-  CUDA_OK(cudaStreamSynchronize(p->cs));
+  TPS_TRY(sync_streams(p));
   return TPS_OK;
 }
 
@@ -1058,7 +1091,7 @@ tps_status tps_init_weights_synthetic(tps_pipeline* p) {
     CUDA_OK(tps::launch_f32_to_bf16(L.W, L.ver[p->latest % p->R], static_cast<int64_t>(L.Np) * L.Kp, p->cs));
     p->launches += 2;
   }
-  CUDA_OK(cudaStreamSynchronize(p->cs));
+  TPS_TRY(sync_streams(p));
   return TPS_OK;
 }
 
@@ -1067,7 +1100,7 @@ tps_status tps_get_losses(tps_pipeline* p, float* out, int64_t cap, int64_t* n) 
   if (!n) return fail(TPS_E_INVALID_ARG, "null n");
   *n = p->last ? p->loss_count : 0;
   if (p->last && out && *n > 0) {
-    CUDA_OK(cudaStreamSynchronize(p->cs));
+    TPS_TRY(sync_streams(p));
     CUDA_OK(cudaMemcpy(out, p->losses, sizeof(float) * static_cast<size_t>(std::min(cap, *n)), cudaMemcpyDeviceToHost));
   }
   return TPS_OK;
@@ -1100,7 +1133,7 @@ tps_status tps_memory_stats(tps_pipeline* p, int64_t* weights, int64_t* stash, i
 
 tps_status tps_set_profiling(tps_pipeline* p, int32_t enable) {
   TPS_TRY(check_usable(p));
-  CUDA_OK(cudaStreamSynchronize(p->cs));
+  TPS_TRY(sync_streams(p));
   TPS_TRY(drain_timing(p));
   p->profiling = enable != 0;
   for (int k = 0; k < 5; ++k) { p->stat_ms[k] = 0; p->stat_work[k] = 0; p->stat_n[k] = 0; }
@@ -1110,7 +1143,7 @@ tps_status tps_set_profiling(tps_pipeline* p, int32_t enable) {
 tps_status tps_kernel_stats(tps_pipeline* p, int32_t which, int64_t* launches, double* ms, double* work) {
   TPS_TRY(check_usable(p));
   if (which < 0 || which > 4) return fail(TPS_E_INVALID_ARG, "bad kernel class");
-  CUDA_OK(cudaStreamSynchronize(p->cs));
+  TPS_TRY(sync_streams(p));
   TPS_TRY(drain_timing(p));
   if (launches) *launches = p->stat_n[which];
   if (ms) *ms = p->stat_ms[which];
