@@ -233,11 +233,11 @@ uint64_t host_mix64(uint64_t x) {
 }  // namespace
 
 cudaError_t launch_sgd_update(float* w, float* v, const float* g, uint16_t* ver, int64_t n, float lr, float mu,
-                              float wd, cudaStream_t st) {
+                              float wd, cudaStream_t st, int blocks_per_sm) {
   if (n <= 0) return cudaSuccess;
   if (n % 4) return cudaErrorInvalidValue;
   const int64_t n4 = n / 4;
-  const int grid = grid_for(n4, 256);
+  const int grid = grid_for(n4, 256, blocks_per_sm);
   const bool mom = mu != 0.0f;
   if (mom && ver) sgd_update_kernel<true, true><<<grid, 256, 0, st>>>(w, v, g, ver, n4, lr, mu, wd);
   else if (mom) sgd_update_kernel<true, false><<<grid, 256, 0, st>>>(w, v, g, ver, n4, lr, mu, wd);

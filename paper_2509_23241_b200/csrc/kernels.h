@@ -9,8 +9,9 @@ namespace tps {
 // Fused SGD/momentum update + new bf16 version (row a10):
 //   g' = g + wd·w ; v = μ·v + g' ; w = w - lr·v   (fp32, one rounding per op, PyTorch order)
 //   ver = bf16_rne(w)  (skipped if ver == nullptr).  μ == 0 => v untouched (14 B/param).
+// blocks_per_sm bounds the grid (a small grid lets the update run underneath a persistent GEMM).
 cudaError_t launch_sgd_update(float* w, float* v, const float* g, uint16_t* ver, int64_t n, float lr, float mu,
-                              float wd, cudaStream_t st);
+                              float wd, cudaStream_t st, int blocks_per_sm = 8);
 
 // db[c] = Σ_{r<rows} G[r, c] for c < cols (G bf16 [rows, ldg]); deterministic two-phase
 // reduction using `scratch` (>= bias_grad_scratch_floats(rows, cols) floats).

@@ -19,6 +19,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -116,6 +117,7 @@ struct tps_pipeline {
   float lr = 0.01f, mu = 0.f, wd = 0.f;
   uint64_t seed = 0;
   bool first = true, last = true, eq1_on_load = false, fuse_update = false;
+  int upd_blocks_per_sm = 2;
   std::vector<int> dims;  // global
   std::vector<Layer> layers;
   int classes = 0;
@@ -606,7 +608,8 @@ tps_status do_backward(tps_pipeline* p, int64_t j, int staleness) {
       const int64_t n = static_cast<int64_t>(Lk.Np) * Lk.Kp;
       TimedLaunch tl{};
       TPS_TRY(time_begin(p, &tl, 4, (p->mu != 0.f ? 22.0 : 14.0) * n, us));
-      CUDA_OK(tps::launch_sgd_update(Lk.W, Lk.mW, Lk.dW, Lk.ver[vn % p->R], n, p->lr, p->mu, p->wd, us));
+      CUDA_OK(tps::launch_sgd_update(Lk.W, Lk.mW, Lk.dW, Lk.ver[vn % p->R], n, p->lr, p->mu, p->wd, us,
+                                     p->upd_blocks_per_sm));
       TPS_TRY(time_end(p, &tl, us));
       p->launches += 1;
     }
@@ -751,6 +754,7 @@ tps_status tps_pipeline_init(const tps_config* c, tps_pipeline** out) {
   const char* env = std::getenv("TPS_EQ1_ON_LOAD");
   p->eq1_on_load = env && env[0] == '1';
   p->fuse_update = c->fuse_update != 0;
+  if (const char* e2 = std::getenv("TPS_UPD_BPS")) p->upd_blocks_per_sm = std::max(1, std::atoi(e2));
 
   auto cleanup = [&](tps_status st) {
     tps_pipeline_destroy(p);
@@ -815,8 +819,14 @@ tps_status tps_pipeline_init(const tps_config* c, tps_pipeline** out) {
     if (cudaStreamCreateWithFlags(&p->cs, cudaStreamNonBlocking) != cudaSuccess) return cleanup(fail(TPS_E_CUDA, "stream create"));
     p->own_cs = true;
   }
-  for (cudaStream_t* sp : {&p->s_fin, &p->s_fout, &p->s_bin, &p->s_bout, &p->s_upd})
+  for (cudaStream_t* sp : {&p->s_fin, &p->s_fout, &p->s_bin, &p->s_bout})
     if (cudaStreamCreateWithFlags(sp, cudaStreamNonBlocking) != cudaSuccess) return cleanup(fail(TPS_E_CUDA, "stream create"));
+  {
+    int lo = 0, hi = 0;   // optimizer stream at the lowest priority: GEMM CTAs are placed first
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    if (cudaStreamCreateWithPriority(&p->s_upd, cudaStreamNonBlocking, lo) != cudaSuccess)
+      return cleanup(fail(TPS_E_CUDA, "stream create"));
+  }
   p->ev_fwd_ready.resize(2 * p->ng);
   p->ev_fwd_sent.resize(2 * p->ng);
   for (int i = 0; i < 2 * p->ng; ++i) {
