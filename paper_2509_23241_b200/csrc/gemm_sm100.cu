@@ -26,6 +26,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 
 #include "gemm.h"
 #include "ptx.cuh"
@@ -41,17 +42,18 @@ constexpr int SMEM_BUDGET = 227 * 1024;
 constexpr int EPI_WARPS = 8;
 constexpr int EPI_SMEM = EPI_WARPS * 32 * 33 * 4;   // per-warp 32x33 fp32 transpose buffer
 
-template <int BN, int BLEND, int SGD = 0>
+template <int BN, int BLEND, int SGD = 0, int CG = 1>
 struct Cfg {
   static constexpr int EPI = SGD ? EPI_SMEM : 0;   // transpose buffer only for the fused update
-  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int B_BYTES = (BN / CG) * BK * 2;   // this CTA's share of the B tile
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES * (BLEND ? 3 : 1);
   static constexpr int STAGES_RAW = (SMEM_BUDGET - 2048 - EPI) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr int THREADS = 32 * (2 + EPI_WARPS + (BLEND ? 4 : 0));
   static constexpr int TMEM_COLS = 2 * BN;
   static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + EPI + 256;
-  static constexpr uint32_t TX = A_BYTES + B_BYTES * (BLEND ? 2 : 1);
+  // bytes the leader's full barrier waits for per stage (both CTAs of a pair land on it)
+  static constexpr uint32_t TX = (A_BYTES + B_BYTES * (BLEND ? 2 : 1)) * CG;
 };
 
 __device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int& mb, int& nb) {
@@ -72,11 +74,15 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
-template <int BN, int A_MN, int B_MN, int BLEND, int SGD>
-__global__ void __launch_bounds__(Cfg<BN, BLEND, SGD>::THREADS, 1)
+template <int BN, int A_MN, int B_MN, int BLEND, int SGD, int CG>
+__global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmB2, const GemmArgs args) {
-  using C = Cfg<BN, BLEND, SGD>;
+  // CG = 2: a cluster of two CTAs on one TPC computes a 256 x BN tile with one
+  // tcgen05.mma.cta_group::2 stream issued by the leader; each CTA stages its own 128 rows
+  // of A and half of the B tile, so per-SM operand traffic drops by a third.
+  using C = Cfg<BN, BLEND, SGD, CG>;
+  static_assert(CG == 1 || (!BLEND && BN / CG >= 64), "pair mode: no blend, >= 64 B columns per CTA");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* stages = smem;
@@ -90,7 +96,9 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD>::THREADS, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int num_m = (args.M + BM - 1) / BM;
+  const uint32_t rank = CG == 2 ? ptx::cluster_rank() : 0;
+  const int cid = blockIdx.x / CG, ncl = gridDim.x / CG;
+  const int num_m = (args.M + BM * CG - 1) / (BM * CG);
   const int num_n = (args.N + BN - 1) / BN;
   const int num_k = (args.K + BK - 1) / BK;
   const int num_tiles = num_m * num_n;
@@ -106,13 +114,17 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD>::THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tmem_full[a], 1);
-      ptx::mbar_init(&tmem_empty[a], EPI_WARPS);
+      ptx::mbar_init(&tmem_empty[a], EPI_WARPS * CG);
     }
     ptx::fence_barrier_init();
   }
-  if (warp == 1) ptx::tmem_alloc(tmem_slot, C::TMEM_COLS);
+  if (warp == 1) {
+    if (CG == 2) ptx::tmem_alloc_cg2(tmem_slot, C::TMEM_COLS);
+    else ptx::tmem_alloc(tmem_slot, C::TMEM_COLS);
+  }
   ptx::tc_fence_before();
-  __syncthreads();
+  if (CG == 2) ptx::cluster_sync();
+  else __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -121,31 +133,49 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD>::THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      for (int t = cid; t < num_tiles; t += ncl) {
         int mb, nb;
         tile_coords(t, num_m, num_n, mb, nb);
+        const int m0 = mb * BM * CG + static_cast<int>(rank) * BM;          // this CTA's 128 rows
+        const int n0 = nb * BN + static_cast<int>(rank) * (BN / CG);       // this CTA's B share
         for (int kb = 0; kb < num_k; ++kb) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sA = stages + stage * C::STAGE_BYTES;
           uint8_t* sB = sA + A_BYTES;
-          ptx::mbar_expect_tx(&full[stage], C::TX);
-          if (!A_MN) {
-            ptx::tma_load_2d(sA, &tmA, &full[stage], kb * BK, mb * BM);
-          } else {
+          if (rank == 0) ptx::mbar_expect_tx(&full[stage], C::TX);
+          if (CG == 2) {
+            const uint32_t fb = ptx::mapa(ptx::smem_u32(&full[stage]), 0);   // leader's barrier
+            if (!A_MN) {
+              ptx::tma_load_2d_cg2(sA, &tmA, fb, kb * BK, m0);
+            } else {
 #pragma unroll
-            for (int i = 0; i < BM / 64; ++i)
-              ptx::tma_load_2d(sA + i * 8192, &tmA, &full[stage], mb * BM + 64 * i, kb * BK);
-          }
-          // BLEND: stash -> staging 1, latest -> staging 2; transform warps fill sB
-          uint8_t* dB = BLEND ? sB + C::B_BYTES : sB;
-          if (!B_MN) {
-            ptx::tma_load_2d(dB, &tmB, &full[stage], kb * BK, nb * BN);
-            if (BLEND) ptx::tma_load_2d(dB + C::B_BYTES, &tmB2, &full[stage], kb * BK, nb * BN);
-          } else {
+              for (int i = 0; i < BM / 64; ++i) ptx::tma_load_2d_cg2(sA + i * 8192, &tmA, fb, m0 + 64 * i, kb * BK);
+            }
+            if (!B_MN) {
+              ptx::tma_load_2d_cg2(sB, &tmB, fb, kb * BK, n0);
+            } else {
 #pragma unroll
-            for (int i = 0; i < BN / 64; ++i) {
-              ptx::tma_load_2d(dB + i * 8192, &tmB, &full[stage], nb * BN + 64 * i, kb * BK);
-              if (BLEND) ptx::tma_load_2d(dB + C::B_BYTES + i * 8192, &tmB2, &full[stage], nb * BN + 64 * i, kb * BK);
+              for (int i = 0; i < BN / CG / 64; ++i) ptx::tma_load_2d_cg2(sB + i * 8192, &tmB, fb, n0 + 64 * i, kb * BK);
+            }
+          } else {
+            if (!A_MN) {
+              ptx::tma_load_2d(sA, &tmA, &full[stage], kb * BK, m0);
+            } else {
+#pragma unroll
+              for (int i = 0; i < BM / 64; ++i)
+                ptx::tma_load_2d(sA + i * 8192, &tmA, &full[stage], m0 + 64 * i, kb * BK);
+            }
+            // BLEND: stash -> staging 1, latest -> staging 2; transform warps fill sB
+            uint8_t* dB = BLEND ? sB + C::B_BYTES : sB;
+            if (!B_MN) {
+              ptx::tma_load_2d(dB, &tmB, &full[stage], kb * BK, n0);
+              if (BLEND) ptx::tma_load_2d(dB + C::B_BYTES, &tmB2, &full[stage], kb * BK, n0);
+            } else {
+#pragma unroll
+              for (int i = 0; i < BN / 64; ++i) {
+                ptx::tma_load_2d(dB + i * 8192, &tmB, &full[stage], n0 + 64 * i, kb * BK);
+                if (BLEND) ptx::tma_load_2d(dB + C::B_BYTES + i * 8192, &tmB2, &full[stage], n0 + 64 * i, kb * BK);
+              }
             }
           }
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
@@ -154,12 +184,12 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD>::THREADS, 1)
     }
   } else if (warp == 1) {
     // ===================== MMA issuer =====================
-    if (lane == 0) {
-      constexpr uint32_t idesc = ptx::make_idesc_bf16(BM, BN, A_MN, B_MN);
+    if (lane == 0 && rank == 0) {
+      constexpr uint32_t idesc = ptx::make_idesc_bf16(BM * CG, BN, A_MN, B_MN);
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+      for (int t = cid; t < num_tiles; t += ncl, ++it) {
         const int acc = it & 1;
         const uint32_t acc_phase = (it >> 1) & 1;
         ptx::mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
@@ -179,12 +209,15 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD>::THREADS, 1)
                                      : ptx::make_sdesc_sw128(a_addr + kk * 32, 16, 1024);
             const uint64_t bd = B_MN ? ptx::make_sdesc_sw128(b_addr + kk * 2048, 8192, 1024)
                                      : ptx::make_sdesc_sw128(b_addr + kk * 32, 16, 1024);
-            ptx::umma_f16(d_tmem, ad, bd, idesc, (kb | kk) != 0);
+            if (CG == 2) ptx::umma_f16_cg2(d_tmem, ad, bd, idesc, (kb | kk) != 0);
+            else ptx::umma_f16(d_tmem, ad, bd, idesc, (kb | kk) != 0);
           }
-          ptx::umma_commit(&empty[stage]);
+          if (CG == 2) ptx::umma_commit_cg2_mc(&empty[stage], 0x3);
+          else ptx::umma_commit(&empty[stage]);
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
-        ptx::umma_commit(&tmem_full[acc]);
+        if (CG == 2) ptx::umma_commit_cg2_mc(&tmem_full[acc], 0x3);
+        else ptx::umma_commit(&tmem_full[acc]);
       }
     }
   } else if (warp < 2 + EPI_WARPS) {
@@ -195,14 +228,14 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD>::THREADS, 1)
     const int half = e >> 2;
     float* stg = epi_stage + e * (32 * 33);
     int it = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+    for (int t = cid; t < num_tiles; t += ncl, ++it) {
       int mb, nb;
       tile_coords(t, num_m, num_n, mb, nb);
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       ptx::mbar_wait(&tmem_full[acc], acc_phase);
       ptx::tc_fence_after();
-      const int row0 = mb * BM + q * 32;
+      const int row0 = mb * BM * CG + static_cast<int>(rank) * BM + q * 32;
 #pragma unroll 1
       for (int c = half; c < BN / 32; c += 2) {
         uint32_t r[32];
@@ -211,7 +244,10 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD>::THREADS, 1)
         if (c + 2 >= BN / 32) {             // last TMEM read of this warp for this tile
           ptx::tc_fence_before();
           __syncwarp();
-          if (lane == 0) ptx::mbar_arrive(&tmem_empty[acc]);
+          if (lane == 0) {
+            if (CG == 2) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&tmem_empty[acc]), 0));
+            else ptx::mbar_arrive(&tmem_empty[acc]);
+          }
         }
         if (SGD) {
           // fused update (row a10), staged through smem so lane = column and every access is a
@@ -333,7 +369,7 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD>::THREADS, 1)
     const float xa = args.xa, xb = args.xb;
     int stage = 0;
     uint32_t phase = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+    for (int t = cid; t < num_tiles; t += ncl) {
       for (int kb = 0; kb < num_k; ++kb) {
         ptx::mbar_wait(&full[stage], phase);
         uint8_t* sB = stages + stage * C::STAGE_BYTES + A_BYTES;
@@ -366,10 +402,12 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD>::THREADS, 1)
   }
 
   ptx::tc_fence_before();
-  __syncthreads();
+  if (CG == 2) ptx::cluster_sync();
+  else __syncthreads();
   if (warp == 1) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc(tmem_base, C::TMEM_COLS);
+    if (CG == 2) ptx::tmem_dealloc_cg2(tmem_base, C::TMEM_COLS);
+    else ptx::tmem_dealloc(tmem_base, C::TMEM_COLS);
   }
 }
 
@@ -415,35 +453,81 @@ int num_sms() {
   return n;
 }
 
-template <int BN, int A_MN, int B_MN, int BLEND, int SGD = 0>
+template <int BN, int A_MN, int B_MN, int BLEND, int SGD = 0, int CG = 1>
 cudaError_t launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& b2, const GemmArgs& args,
                    cudaStream_t st) {
-  using C = Cfg<BN, BLEND, SGD>;
-  auto kern = gemm_kernel<BN, A_MN, B_MN, BLEND, SGD>;
+  using C = Cfg<BN, BLEND, SGD, CG>;
+  auto kern = gemm_kernel<BN, A_MN, B_MN, BLEND, SGD, CG>;
   static bool attr_set = false;   // per instantiation
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  const int tiles = ((args.M + BM - 1) / BM) * ((args.N + BN - 1) / BN);
-  const int grid = std::max(1, std::min(tiles, num_sms()));
-  kern<<<grid, C::THREADS, C::SMEM, st>>>(a, b, b2, args);
+  const int tiles = ((args.M + BM * CG - 1) / (BM * CG)) * ((args.N + BN - 1) / BN);
+  const int clusters = std::max(1, std::min(tiles, num_sms() / CG));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(clusters * CG);
+  cfg.blockDim = dim3(C::THREADS);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a, b, b2, args);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
-int pick_bn(int M, int N, int mode) {
-  if (mode == GEMM_DGRAD_BLEND) return 128;
-  const int tm = (M + BM - 1) / BM;
+struct Tiling {
+  int cg, bn;
+};
+
+// Pick the CTA-pair mode and tile width.  Pairs (256 x BN tiles, cta_group::2) cut operand
+// traffic per SM by a third; they are used when M fills at least two 128-row blocks and the
+// pair grid still covers the chip.  Env TPS_GEMM_CG=1 forces single-CTA tiles.
+Tiling pick_tiling(int M, int N, int mode, bool sgd) {
+  if (mode == GEMM_DGRAD_BLEND) return {1, 128};
   const int sms = num_sms();
+  static int force_cg = -1;
+  if (force_cg < 0) {
+    const char* e = std::getenv("TPS_GEMM_CG");
+    force_cg = e ? std::atoi(e) : 0;
+  }
+  if (force_cg != 1 && M >= 256) {
+    const int tm = (M + 255) / 256;
+    for (int bn : {256, 128}) {
+      if (N <= bn / 2) continue;
+      const int tiles = tm * ((N + bn - 1) / bn);
+      if (tiles >= (sms / 2) * 3 / 4) return {2, bn};
+    }
+  }
+  const int tm = (M + BM - 1) / BM;
   const int cand[3] = {256, 128, 64};
   for (int i = 0; i < 3; ++i) {
     const int bn = cand[i];
     if (bn > 64 && N <= bn / 2) continue;          // mostly padding
     const int tiles = tm * ((N + bn - 1) / bn);
-    if (tiles >= (sms * 3) / 4 || bn == 64) return bn;
+    if (tiles >= (sms * 3) / 4 || bn == 64) return {1, bn};
   }
-  return 64;
+  (void)sgd;
+  return {1, 64};
+}
+
+template <int A_MN, int B_MN, int SGD>
+cudaError_t dispatch(const Tiling& tl, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tb2,
+                     const GemmArgs& args, cudaStream_t st) {
+  if (tl.cg == 2) {
+    if (tl.bn == 256) return launch<256, A_MN, B_MN, 0, SGD, 2>(ta, tb, tb2, args, st);
+    return launch<128, A_MN, B_MN, 0, SGD, 2>(ta, tb, tb2, args, st);
+  }
+  if (tl.bn == 256) return launch<256, A_MN, B_MN, 0, SGD, 1>(ta, tb, tb2, args, st);
+  if (tl.bn == 128) return launch<128, A_MN, B_MN, 0, SGD, 1>(ta, tb, tb2, args, st);
+  return launch<64, A_MN, B_MN, 0, SGD, 1>(ta, tb, tb2, args, st);
 }
 
 }  // namespace
@@ -461,40 +545,29 @@ const char* gemm_mode_name(int mode) {
 cudaError_t gemm_run(int mode, const GemmOperands& op, const GemmArgs& args_in, cudaStream_t st, int* bn_out) {
   GemmArgs args = args_in;
   if (args.M <= 0 || args.N <= 0 || args.K <= 0) return cudaSuccess;
-  const int bn = pick_bn(args.M, args.N, mode);
-  if (bn_out) *bn_out = bn;
+  const bool sgd = (mode == GEMM_WGRAD && args.epi == EPI_SGD);
+  const Tiling tl = pick_tiling(args.M, args.N, mode, sgd);
+  if (bn_out) *bn_out = tl.bn * 10 + tl.cg;
   CUtensorMap ta, tb, tb2;
   const bool a_mn = (mode == GEMM_WGRAD);
   const bool b_mn = (mode != GEMM_FWD);
   bool ok = true;
   // A: K-major [M,K] -> box {64 K, 128 rows}; MN-major stored [K,M] -> box {64 M, 64 K}
+  // B: K-major [N,K] -> box {64 K, BN/CG rows} (each CTA of a pair loads its share)
   if (!a_mn) ok &= make_tmap(&ta, op.A, args.M, args.K, op.lda, BM);
   else ok &= make_tmap(&ta, op.A, args.K, args.M, op.lda, 64);
-  if (!b_mn) ok &= make_tmap(&tb, op.B, args.N, args.K, op.ldb, bn);
+  if (!b_mn) ok &= make_tmap(&tb, op.B, args.N, args.K, op.ldb, tl.bn / tl.cg);
   else ok &= make_tmap(&tb, op.B, args.K, args.N, op.ldb, 64);
   if (mode == GEMM_DGRAD_BLEND) ok &= make_tmap(&tb2, op.B2, args.K, args.N, op.ldb, 64);
   else tb2 = tb;
   if (!ok) return cudaErrorInvalidValue;
   switch (mode) {
-    case GEMM_FWD:
-      if (bn == 256) return launch<256, 0, 0, 0>(ta, tb, tb2, args, st);
-      if (bn == 128) return launch<128, 0, 0, 0>(ta, tb, tb2, args, st);
-      return launch<64, 0, 0, 0>(ta, tb, tb2, args, st);
-    case GEMM_DGRAD:
-      if (bn == 256) return launch<256, 0, 1, 0>(ta, tb, tb2, args, st);
-      if (bn == 128) return launch<128, 0, 1, 0>(ta, tb, tb2, args, st);
-      return launch<64, 0, 1, 0>(ta, tb, tb2, args, st);
+    case GEMM_FWD: return dispatch<0, 0, 0>(tl, ta, tb, tb2, args, st);
+    case GEMM_DGRAD: return dispatch<0, 1, 0>(tl, ta, tb, tb2, args, st);
     case GEMM_WGRAD:
-      if (args.epi == EPI_SGD) {
-        if (bn == 256) return launch<256, 1, 1, 0, 1>(ta, tb, tb2, args, st);
-        if (bn == 128) return launch<128, 1, 1, 0, 1>(ta, tb, tb2, args, st);
-        return launch<64, 1, 1, 0, 1>(ta, tb, tb2, args, st);
-      }
-      if (bn == 256) return launch<256, 1, 1, 0>(ta, tb, tb2, args, st);
-      if (bn == 128) return launch<128, 1, 1, 0>(ta, tb, tb2, args, st);
-      return launch<64, 1, 1, 0>(ta, tb, tb2, args, st);
-    case GEMM_DGRAD_BLEND:
-      return launch<128, 0, 1, 1>(ta, tb, tb2, args, st);
+      if (sgd) return dispatch<1, 1, 1>(tl, ta, tb, tb2, args, st);
+      return dispatch<1, 1, 0>(tl, ta, tb, tb2, args, st);
+    case GEMM_DGRAD_BLEND: return launch<128, 0, 1, 1, 0, 1>(ta, tb, tb2, args, st);
   }
   return cudaErrorInvalidValue;
 }
