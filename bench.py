@@ -195,14 +195,18 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dims, bounds = model(S)
-    ids = None
-    if S > 1:
-        obj = [b"".join(tps.nccl_unique_id() for _ in range(2 * (S - 1)))] if rank == 0 else [None]
-        dist.broadcast_object_list(obj, src=0)
-        ids = obj[0]
     stream = torch.cuda.current_stream().cuda_stream
 
+    def fresh_ids():
+        # an ncclUniqueId bootstraps exactly one communicator: new ids for every pipeline
+        if S == 1:
+            return None
+        obj = [b"".join(tps.nccl_unique_id() for _ in range(2 * (S - 1)))] if rank == 0 else [None]
+        dist.broadcast_object_list(obj, src=0)
+        return obj[0]
+
     def make(variant):
+        ids = fresh_ids()
         spec = tps.StageSpec(dims=dims, stage_bounds=bounds, stage_id=rank, micro_batches=MICRO_M,
                              micro_batch_size=MICRO_B, fwd_group=args.fwd_group, variant=variant,
                              blend=tps.TPS_BLEND_EQ1, lam=LAM, lr=LR, momentum=MU,

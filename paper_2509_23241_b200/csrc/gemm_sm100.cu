@@ -225,8 +225,25 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
     // 8 warps: warp w reads TMEM lane quarter (w % 4) and handles every other 32-column chunk.
     const int e = warp - 2;
     const int q = warp & 3;                 // TMEM lane quarter this warp may access
-    const int half = e >> 2;
+    const int half = e >> 2;                // which half of the tile's columns this warp owns
+    constexpr int CPW = BN / 64;            // 32-column chunks per warp per tile
     float* stg = epi_stage + e * (32 * 33);
+    // SGD: pull this warp's rows of w and v for tile `tt` into L2 ahead of its epilogue
+    // (one bulk prefetch per row and array, issued while the tensor cores are still busy)
+    auto prefetch_state = [&](int tt) {
+      if (!SGD || tt >= num_tiles) return;
+      int pmb, pnb;
+      tile_coords(tt, num_m, num_n, pmb, pnb);
+      const int prow = pmb * BM * CG + static_cast<int>(rank) * BM + q * 32 + lane;
+      const int pcol = pnb * BN + half * (BN / 2);
+      if (prow < args.M && pcol < args.N) {
+        const uint32_t bytes = static_cast<uint32_t>(min(BN / 2, args.N - pcol)) * 4u;
+        const size_t off = static_cast<size_t>(prow) * args.ldo + pcol;
+        ptx::bulk_prefetch_l2(args.w + off, bytes);
+        if (args.mu != 0.0f) ptx::bulk_prefetch_l2(args.v + off, bytes);
+      }
+    };
+    prefetch_state(cid);
     int it = 0;
     for (int t = cid; t < num_tiles; t += ncl, ++it) {
       int mb, nb;
@@ -235,13 +252,15 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
       const uint32_t acc_phase = (it >> 1) & 1;
       ptx::mbar_wait(&tmem_full[acc], acc_phase);
       ptx::tc_fence_after();
+      prefetch_state(t + ncl);
       const int row0 = mb * BM * CG + static_cast<int>(rank) * BM + q * 32;
 #pragma unroll 1
-      for (int c = half; c < BN / 32; c += 2) {
+      for (int ci = 0; ci < CPW; ++ci) {
+        const int c = half * CPW + ci;
         uint32_t r[32];
         ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c * 32, r);
         ptx::tmem_ld_wait();
-        if (c + 2 >= BN / 32) {             // last TMEM read of this warp for this tile
+        if (ci == CPW - 1) {                // last TMEM read of this warp for this tile
           ptx::tc_fence_before();
           __syncwarp();
           if (lane == 0) {
