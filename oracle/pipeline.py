@@ -1,4 +1,4 @@
-"""Whole-pipeline replay of V- and I-TiMePReSt on an MLP (TEST INFRASTRUCTURE ONLY).
+"""Whole-pipeline replay of V- and I-TiMePReSt on an MLP or a conv net (TEST INFRASTRUCTURE ONLY).
 
 All S stages live in one address space and fire in the order produced by
 `schedule.execute` (a dependency-driven round-robin over the static per-stage
@@ -23,12 +23,13 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from . import mlp, schedule, staleness
+from . import conv, mlp, schedule, staleness
 
 
 @dataclass
 class Config:
-    dims: list[int]                  # [d0, d1, ..., dL]; layer l maps d_l -> d_{l+1}
+    dims: list[int]                  # MLP: [d0, d1, ..., dL]; layer l maps d_l -> d_{l+1}
+                                     # (image nets: [input features, ..., classes], informational)
     stage_bounds: list[int]          # S+1 entries, stage s owns layers [b[s], b[s+1])
     m: int                           # micro-batches per mini-batch
     b: int                           # rows per micro-batch
@@ -40,6 +41,11 @@ class Config:
     momentum: float = 0.0
     wd: float = 0.0
     exact: bool = False
+    # optional layer list for image nets (oracle/conv.py); None => Linear layers from dims.
+    # entries: {"kind": "linear", "in", "out"} | {"kind": "conv3", "cin", "cout", "h", "w"}
+    #          | {"kind": "pool2", "c", "h", "w"}; every layer but the last is followed by ReLU
+    #          (pools pass values through); the last is the Linear head.
+    layers: list | None = None
 
     @property
     def S(self) -> int:
@@ -47,7 +53,12 @@ class Config:
 
     @property
     def L(self) -> int:
-        return len(self.dims) - 1
+        return len(self.layers) if self.layers else len(self.dims) - 1
+
+    def specs(self) -> list[dict]:
+        if self.layers:
+            return self.layers
+        return [{"kind": "linear", "in": self.dims[l], "out": self.dims[l + 1]} for l in range(self.L)]
 
     @property
     def B(self) -> int:
@@ -90,17 +101,20 @@ def run(cfg: Config, xs: list[np.ndarray], ys: list[np.ndarray],
         for l in range(cfg.stage_bounds[s], cfg.stage_bounds[s + 1]):
             stage_of[l] = s
 
-    W = [np.asarray(w, np.float32).astype(np.float64) for w in w0]   # fp32 masters (as fp64 values)
-    bias = [np.asarray(x, np.float32).astype(np.float64) for x in b0]
-    VW = [np.zeros_like(w) for w in W]
-    Vb = [np.zeros_like(x) for x in bias]
-    if cfg.exact:
-        W = [np.asarray(w, np.float64) for w in w0]
-        bias = [np.asarray(x, np.float64) for x in b0]
+    spec = cfg.specs()
+    has_w = [sp["kind"] != "pool2" for sp in spec]
+    cast = (lambda a: np.asarray(a, np.float64)) if cfg.exact else (lambda a: np.asarray(a, np.float32).astype(np.float64))
+    W = [cast(w) if has_w[l] else None for l, w in enumerate(w0)]      # fp32 masters (as fp64 values)
+    bias = [cast(x) if has_w[l] else None for l, x in enumerate(b0)]
+    VW = [np.zeros_like(w) if w is not None else None for w in W]
+    Vb = [np.zeros_like(x) if x is not None else None for x in bias]
 
     # versions[s][v] = [bf16 copy of W_l for l in stage s]
     layers = [list(range(cfg.stage_bounds[s], cfg.stage_bounds[s + 1])) for s in range(S)]
-    versions = [{0: [prec.store(W[l]) for l in layers[s]]} for s in range(S)]
+    def store_w(l):
+        return prec.store(W[l]) if has_w[l] else None
+
+    versions = [{0: [store_w(l) for l in layers[s]]} for s in range(S)]
     latest = [0] * S
     consumers: list[dict[int, set[int]]] = [dict() for _ in range(S)]
     peak = [1] * S
@@ -128,7 +142,15 @@ def run(cfg: Config, xs: list[np.ndarray], ys: list[np.ndarray],
             ins = []
             for k, l in enumerate(ls):
                 ins.append(X)
-                Z = mlp.linear_forward(X, Wv[k], bias[l])
+                sp = spec[l]
+                if sp["kind"] == "pool2":
+                    X = conv.maxpool2_forward(X.reshape(-1, sp["h"], sp["w"], sp["c"])).reshape(X.shape[0], -1)
+                    continue
+                if sp["kind"] == "conv3":
+                    Z = conv.conv3x3_forward(X.reshape(-1, sp["h"], sp["w"], sp["cin"]), Wv[k], bias[l])
+                    Z = Z.reshape(X.shape[0], -1)
+                else:
+                    Z = mlp.linear_forward(X, Wv[k], bias[l])
                 if l < L - 1:
                     X = prec.store(mlp.relu(Z))
                 else:
@@ -162,11 +184,27 @@ def run(cfg: Config, xs: list[np.ndarray], ys: list[np.ndarray],
             dWs, dbs = [None] * len(ls), [None] * len(ls)
             for k in reversed(range(len(ls))):
                 l = ls[k]
-                dW, db = mlp.wgrad(G, ins[k])
+                sp = spec[l]
+                X = ins[k]
+                if sp["kind"] == "pool2":
+                    # route to the first window maximum; no rounding (values are copied)
+                    G = conv.maxpool2_backward(X.reshape(-1, sp["h"], sp["w"], sp["c"]),
+                                               G.reshape(-1, sp["h"] // 2, sp["w"] // 2, sp["c"])).reshape(X.shape[0], -1)
+                    continue
+                if sp["kind"] == "conv3":
+                    X4 = X.reshape(-1, sp["h"], sp["w"], sp["cin"])
+                    G4 = G.reshape(-1, sp["h"], sp["w"], sp["cout"])
+                    dW, db = conv.conv3x3_wgrad(G4, X4)
+                else:
+                    dW, db = mlp.wgrad(G, X)
                 dWs[k], dbs[k] = prec.f32(dW), prec.f32(db)
                 if l > 0:
                     Wres = mlp.resolve_backward_weight(Wst[k], Wl[k], alpha, beta)
-                    G = prec.store(mlp.dgrad(G, Wres, ins[k]))
+                    if sp["kind"] == "conv3":
+                        dX = conv.conv3x3_dgrad(G4, Wres).reshape(X.shape[0], -1)
+                    else:
+                        dX = G @ Wres
+                    G = prec.store(dX * (X > 0))     # ReLU mask from the stored input (Z15)
             if s > 0:
                 bwd_msg[(s - 1, j)] = G
             grads[(s, j)] = (dWs, dbs)
@@ -179,13 +217,15 @@ def run(cfg: Config, xs: list[np.ndarray], ys: list[np.ndarray],
             j = e.mb
             dWs, dbs = grads.pop((s, j))
             for k, l in enumerate(ls):
+                if not has_w[l]:
+                    continue
                 W[l], VW[l] = mlp.sgd_update(W[l], VW[l], dWs[k], cfg.lr, cfg.momentum, cfg.wd, cfg.exact)
                 bias[l], Vb[l] = mlp.sgd_update(bias[l], Vb[l], dbs[k], cfg.lr, cfg.momentum, cfg.wd, cfg.exact)
                 W[l] = np.asarray(W[l], np.float64); VW[l] = np.asarray(VW[l], np.float64)
                 bias[l] = np.asarray(bias[l], np.float64); Vb[l] = np.asarray(Vb[l], np.float64)
             old = latest[s]
             latest[s] = old + 1
-            versions[s][latest[s]] = [prec.store(W[l]) for l in ls]
+            versions[s][latest[s]] = [store_w(l) for l in ls]
             peak[s] = max(peak[s], len(versions[s]))   # transient: old + new coexist
             if cfg.variant == staleness.V_VARIANT or not consumers[s].get(old):
                 versions[s].pop(old, None)            # V drops the superseded version at once
@@ -194,10 +234,10 @@ def run(cfg: Config, xs: list[np.ndarray], ys: list[np.ndarray],
     peak_boundary = _peak_at_boundaries(cfg, trace)
     return Result(
         losses=loss_sum / B,
-        weights=[np.asarray(w, np.float32) if not cfg.exact else w for w in W],
-        biases=[np.asarray(x, np.float32) if not cfg.exact else x for x in bias],
-        mom_w=[np.asarray(x, np.float32) for x in VW],
-        mom_b=[np.asarray(x, np.float32) for x in Vb],
+        weights=[(np.asarray(w, np.float32) if not cfg.exact else w) if w is not None else None for w in W],
+        biases=[(np.asarray(x, np.float32) if not cfg.exact else x) if x is not None else None for x in bias],
+        mom_w=[np.asarray(x, np.float32) if x is not None else None for x in VW],
+        mom_b=[np.asarray(x, np.float32) if x is not None else None for x in Vb],
         trace=trace,
         peak_versions=peak_boundary,
         versions_bf16=[versions[stage_of[l]][latest[stage_of[l]]][layers[stage_of[l]].index(l)]
