@@ -83,6 +83,23 @@ typedef struct {
   float alpha, beta;
 } tps_event;
 
+/* Layer description for image networks (BASELINE.json configs[2]: VGG-16 on 32x32
+ * inputs).  Activations are NHWC bf16; a sample's row is its H·W·C values.
+ *   LINEAR:   out_c = dims out, in_c = dims in (a conv/pool output is flattened in
+ *             (h, w, c) order); followed by ReLU unless it is the last layer.
+ *   CONV3X3:  stride 1, zero padding 1, in_h x in_w x in_c -> in_h x in_w x out_c,
+ *             weight [out_c, 3, 3, in_c] (= [out_c, 9·in_c] rows), + bias, ReLU.
+ *             in_c % 64 == 0, out_c % 64 == 0, except the network's first layer, which
+ *             may have any in_c (it runs as a GEMM on explicit patches).
+ *   MAXPOOL2: 2x2 / stride 2, in_c channels (no parameters).                    */
+typedef enum { TPS_LAYER_LINEAR = 0, TPS_LAYER_CONV3X3 = 1, TPS_LAYER_MAXPOOL2 = 2 } tps_layer_kind;
+typedef struct {
+  int32_t kind;
+  int32_t in_c, out_c;
+  int32_t in_h, in_w;
+  int32_t reserved[3];
+} tps_layer;
+
 /* Pipeline configuration (read once by tps_pipeline_init; arrays are copied).
  * Network: num_layers Linear layers; layer l maps dims[l] -> dims[l+1]; every
  * layer but the last is followed by ReLU; the last produces dims[L] logits for a
@@ -118,7 +135,10 @@ typedef struct {
                                    pre-update weights); tps_stage_update then only commits the
                                    new version.  Legal because U(j) always directly follows
                                    B(j) in the static order (reading Z7).  0 => separate kernel. */
-  int32_t reserved[6];
+  int32_t num_layer_specs;      /* 0 => MLP from dims; else == num_layers entries below  */
+  const tps_layer* layer_specs; /* host; image networks (dims[0] = H·W·C of the input,
+                                   dims[num_layers] = classes; other dims ignored)    */
+  int32_t reserved[4];
 } tps_config;
 
 typedef struct tps_pipeline tps_pipeline;  /* opaque; one per stage */
@@ -244,6 +264,18 @@ tps_status tps_gemm(int32_t mode, int32_t M, int32_t N, int32_t K,
                     const void* A, int32_t lda, const void* B, int32_t ldb, const void* B2,
                     void* out, int32_t ldo, int32_t out_f32, const float* bias, int32_t relu,
                     float alpha, float beta, const void* mask, int32_t ldm, uint64_t stream);
+
+/* ---- raw 3x3 convolution GEMMs (implicit im2col via 4-D TMA; unit tests) ----
+ * NHWC bf16 device tensors, stride 1, padding 1, Ci % 64 == 0, Co % 64 == 0.
+ * mode 0 (forward): out[N·H·W, Co] = conv(X[N,H,W,Ci]; W[Co,3,3,Ci]) + bias, ReLU if relu.
+ * mode 1 (dgrad):   out[N·H·W, Ci] = alpha · conv_transpose(dY[N,H,W,Co]; W), zero where
+ *                   mask[N·H·W, Ci] <= 0 (mask may be NULL).
+ * mode 2 (wgrad):   out[Co, 9·Ci] (fp32) = dY[N·H·W, Co]ᵀ · im2col(X[N,H,W,Ci]).
+ * mode 3 (dgrad, blended operand): as mode 1 with W = alpha·W + beta·W2 formed on load.   */
+tps_status tps_conv_gemm(int32_t mode, int32_t N, int32_t H, int32_t W, int32_t Ci, int32_t Co,
+                         const void* A, const void* Wt, const void* W2, void* out, int32_t out_f32,
+                         const float* bias, int32_t relu, float alpha, float beta, const void* mask,
+                         uint64_t stream);
 
 #ifdef __cplusplus
 }

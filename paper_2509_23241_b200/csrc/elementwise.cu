@@ -8,6 +8,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <cmath>
 #include <cstdint>
 
 #include "kernels.h"
@@ -223,6 +224,119 @@ __global__ void fill_synthetic_kernel(int kind, uint64_t key, int64_t rows, int6
   }
 }
 
+// ------------------------------------------------------------------ image-net helpers (NHWC, bf16)
+// 2x2/stride-2 max pool; 8 channels (16 B) per thread
+__global__ void maxpool2_fwd_kernel(const uint16_t* __restrict__ X, uint16_t* __restrict__ Y, int N, int H, int W,
+                                    int C) {
+  const int C8 = C / 8, Ho = H / 2, Wo = W / 2;
+  const int64_t total = static_cast<int64_t>(N) * Ho * Wo * C8;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int c8 = static_cast<int>(i % C8);
+    int64_t t = i / C8;
+    const int wo = static_cast<int>(t % Wo);
+    t /= Wo;
+    const int ho = static_cast<int>(t % Ho);
+    const int64_t n = t / Ho;
+    const uint16_t* base = X + ((n * H + 2 * ho) * W + 2 * wo) * C + c8 * 8;
+    uint4 q[4];
+    q[0] = __ldg(reinterpret_cast<const uint4*>(base));
+    q[1] = __ldg(reinterpret_cast<const uint4*>(base + C));
+    q[2] = __ldg(reinterpret_cast<const uint4*>(base + static_cast<size_t>(W) * C));
+    q[3] = __ldg(reinterpret_cast<const uint4*>(base + static_cast<size_t>(W) * C + C));
+    uint32_t out[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      uint32_t packed = 0;
+#pragma unroll
+      for (int h2 = 0; h2 < 2; ++h2) {
+        float best = -INFINITY;
+        uint32_t bits = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t word = (&q[k].x)[e];
+          const uint32_t hb = (word >> (16 * h2)) & 0xFFFFu;
+          const float v = bf2f(hb);
+          if (k == 0 || v > best) { best = v; bits = hb; }
+        }
+        packed |= bits << (16 * h2);
+      }
+      out[e] = packed;
+    }
+    reinterpret_cast<uint4*>(Y)[i] = make_uint4(out[0], out[1], out[2], out[3]);
+  }
+}
+
+// gradient of the 2x2 max pool: dY goes to the FIRST maximum of the window in row-major
+// order (reading Z15); the other three positions get 0.  Each thread owns one window x 8 ch.
+__global__ void maxpool2_bwd_kernel(const uint16_t* __restrict__ X, const uint16_t* __restrict__ dY,
+                                    uint16_t* __restrict__ dX, int N, int H, int W, int C) {
+  const int C8 = C / 8, Ho = H / 2, Wo = W / 2;
+  const int64_t total = static_cast<int64_t>(N) * Ho * Wo * C8;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int c8 = static_cast<int>(i % C8);
+    int64_t t = i / C8;
+    const int wo = static_cast<int>(t % Wo);
+    t /= Wo;
+    const int ho = static_cast<int>(t % Ho);
+    const int64_t n = t / Ho;
+    const size_t off[4] = {static_cast<size_t>(((n * H + 2 * ho) * W + 2 * wo) * C + c8 * 8),
+                           static_cast<size_t>(((n * H + 2 * ho) * W + 2 * wo + 1) * C + c8 * 8),
+                           static_cast<size_t>(((n * H + 2 * ho + 1) * W + 2 * wo) * C + c8 * 8),
+                           static_cast<size_t>(((n * H + 2 * ho + 1) * W + 2 * wo + 1) * C + c8 * 8)};
+    uint4 q[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) q[k] = __ldg(reinterpret_cast<const uint4*>(X + off[k]));
+    const uint4 g = __ldg(reinterpret_cast<const uint4*>(dY) + i);
+    uint32_t o[4][4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      uint32_t res[4] = {0, 0, 0, 0};
+#pragma unroll
+      for (int h2 = 0; h2 < 2; ++h2) {
+        float best = -INFINITY;
+        int arg = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float v = bf2f(((&q[k].x)[e] >> (16 * h2)) & 0xFFFFu);
+          if (k == 0 || v > best) { best = v; arg = k; }
+        }
+        const uint32_t gb = ((&g.x)[e] >> (16 * h2)) & 0xFFFFu;
+        res[arg] |= gb << (16 * h2);
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) o[k][e] = res[k];
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      *reinterpret_cast<uint4*>(dX + off[k]) = make_uint4(o[k][0], o[k][1], o[k][2], o[k][3]);
+  }
+}
+
+// explicit 3x3/pad-1 patches for a first layer with few channels: P[(n,h,w), (kh,kw,c)], zero
+// padded columns up to ldp
+__global__ void im2col3x3_kernel(const uint16_t* __restrict__ X, uint16_t* __restrict__ P, int N, int H, int W,
+                                 int C, int ldp) {
+  const int64_t total = static_cast<int64_t>(N) * H * W * ldp;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int col = static_cast<int>(i % ldp);
+    const int64_t pix = i / ldp;
+    uint16_t v = 0;
+    if (col < 9 * C) {
+      const int khw = col / C, c = col - khw * C;
+      const int w = static_cast<int>(pix % W);
+      const int64_t t = pix / W;
+      const int h = static_cast<int>(t % H);
+      const int64_t n = t / H;
+      const int hh = h + khw / 3 - 1, ww = w + khw % 3 - 1;
+      if (hh >= 0 && hh < H && ww >= 0 && ww < W) v = X[((n * H + hh) * W + ww) * C + c];
+    }
+    P[i] = v;
+  }
+}
+
 uint64_t host_mix64(uint64_t x) {
   uint64_t z = x + 0x9E3779B97F4A7C15ull;
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
@@ -286,6 +400,30 @@ cudaError_t launch_blend_materialize(const uint16_t* s, const uint16_t* l, uint1
                                      cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   blend_materialize_kernel<<<grid_for(n, 256), 256, 0, st>>>(s, l, out, n, a, b);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_maxpool2_fwd(const uint16_t* X, uint16_t* Y, int N, int H, int W, int C, cudaStream_t st) {
+  if (C % 8 || H % 2 || W % 2) return cudaErrorInvalidValue;
+  const int64_t total = static_cast<int64_t>(N) * (H / 2) * (W / 2) * (C / 8);
+  if (total <= 0) return cudaSuccess;
+  maxpool2_fwd_kernel<<<grid_for(total, 256), 256, 0, st>>>(X, Y, N, H, W, C);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_maxpool2_bwd(const uint16_t* X, const uint16_t* dY, uint16_t* dX, int N, int H, int W, int C,
+                                cudaStream_t st) {
+  if (C % 8 || H % 2 || W % 2) return cudaErrorInvalidValue;
+  const int64_t total = static_cast<int64_t>(N) * (H / 2) * (W / 2) * (C / 8);
+  if (total <= 0) return cudaSuccess;
+  maxpool2_bwd_kernel<<<grid_for(total, 256), 256, 0, st>>>(X, dY, dX, N, H, W, C);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_im2col3x3(const uint16_t* X, uint16_t* P, int N, int H, int W, int C, int ldp, cudaStream_t st) {
+  const int64_t total = static_cast<int64_t>(N) * H * W * ldp;
+  if (total <= 0) return cudaSuccess;
+  im2col3x3_kernel<<<grid_for(total, 256), 256, 0, st>>>(X, P, N, H, W, C, ldp);
   return cudaGetLastError();
 }
 

@@ -6,12 +6,28 @@
 
 namespace tps {
 
-enum GemmMode { GEMM_FWD = 0, GEMM_DGRAD = 1, GEMM_WGRAD = 2, GEMM_DGRAD_BLEND = 3 };
+enum GemmMode {
+  GEMM_FWD = 0, GEMM_DGRAD = 1, GEMM_WGRAD = 2, GEMM_DGRAD_BLEND = 3,
+  // 3x3 / stride 1 / pad 1 convolutions as implicit GEMMs over NHWC tensors (4-D TMA boxes)
+  GEMM_CONV_FWD = 4,          // Y[NHW, Co]   = im2col(X)[NHW, 9Ci] · W[Co, 9Ci]ᵀ
+  GEMM_CONV_DGRAD = 5,        // dX[NHW, Ci]  = im2col(dY)[NHW, 9Co] · flip(W)[9Co, Ci]
+  GEMM_CONV_DGRAD_BLEND = 6,  // same, flip(α·W_stash + β·W_latest) formed in shared memory
+  GEMM_CONV_WGRAD = 7         // dW[Co, 9Ci]  = dY[NHW, Co]ᵀ · im2col(X)[NHW, 9Ci]
+};
+enum ConvKind { CONV_NONE = 0, CONV_FWD = 1, CONV_DGRAD = 2, CONV_WGRAD = 3 };
+
+// geometry of the gathered NHWC tensor (stride 1, pad 1, 3x3): fwd: X (C = Ci);
+// dgrad: dY (C = Co, also the K blocks of the flipped weight); wgrad: X (C = Ci).
+struct ConvGeom {
+  int N, H, W, C;
+};
 
 struct GemmOperands {
   const void* A;  int lda;    // bf16
   const void* B;  int ldb;    // bf16
   const void* B2;             // bf16, BLEND only (the latest weight; same ld as B)
+  ConvGeom cv;                // conv modes only
+  int Cw;                     // conv dgrad: Ci of the weight [Co,3,3,Ci] (the GEMM N)
 };
 
 // Passed by value to the kernel.
@@ -27,6 +43,7 @@ struct GemmArgs {
   int epi;
   float* w; float* v; uint16_t* ver;
   float lr, mu, wd;
+  ConvGeom cv;                // copied from GemmOperands by gemm_run
 };
 
 enum GemmEpilogue { EPI_STORE = 0, EPI_SGD = 1 };

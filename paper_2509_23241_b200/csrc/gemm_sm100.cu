@@ -74,7 +74,7 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
-template <int BN, int A_MN, int B_MN, int BLEND, int SGD, int CG>
+template <int BN, int A_MN, int B_MN, int BLEND, int SGD, int CG, int CONV>
 __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmB2, const GemmArgs args) {
@@ -143,39 +143,64 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
           uint8_t* sA = stages + stage * C::STAGE_BYTES;
           uint8_t* sB = sA + A_BYTES;
           if (rank == 0) ptx::mbar_expect_tx(&full[stage], C::TX);
-          if (CG == 2) {
-            const uint32_t fb = ptx::mapa(ptx::smem_u32(&full[stage]), 0);   // leader's barrier
-            if (!A_MN) {
-              ptx::tma_load_2d_cg2(sA, &tmA, fb, kb * BK, m0);
-            } else {
-#pragma unroll
-              for (int i = 0; i < BM / 64; ++i) ptx::tma_load_2d_cg2(sA + i * 8192, &tmA, fb, m0 + 64 * i, kb * BK);
-            }
-            if (!B_MN) {
-              ptx::tma_load_2d_cg2(sB, &tmB, fb, kb * BK, n0);
-            } else {
-#pragma unroll
-              for (int i = 0; i < BN / CG / 64; ++i) ptx::tma_load_2d_cg2(sB + i * 8192, &tmB, fb, n0 + 64 * i, kb * BK);
-            }
+          // every load of this stage completes on the leader CTA's full barrier
+          const uint32_t fb = CG == 2 ? ptx::mapa(ptx::smem_u32(&full[stage]), 0) : 0u;
+          auto ld2 = [&](void* dst, const CUtensorMap* m, int x, int y) {
+            if (CG == 2) ptx::tma_load_2d_cg2(dst, m, fb, x, y);
+            else ptx::tma_load_2d(dst, m, &full[stage], x, y);
+          };
+          auto ld4 = [&](void* dst, const CUtensorMap* m, int c0, int c1, int c2, int c3) {
+            if (CG == 2) ptx::tma_load_4d_cg2(dst, m, fb, c0, c1, c2, c3);
+            else ptx::tma_load_4d(dst, m, &full[stage], c0, c1, c2, c3);
+          };
+          // ---- A tile: 128 rows x 64 K
+          if (CONV == CONV_FWD || CONV == CONV_DGRAD) {
+            // implicit im2col: K block kb = (kh, kw, 64-channel block); the 128 output pixels
+            // of this M block form one (w, h, n) box of the NHWC input, shifted by (kh-1, kw-1);
+            // TMA zero-fills the out-of-image halo (= the padding)
+            const int cpb = args.cv.C / 64;
+            const int khw = kb / cpb, c0 = (kb - khw * cpb) * 64;
+            const int P = args.cv.H * args.cv.W;
+            const int n_img = m0 / P, rem = m0 - n_img * P, h0 = rem / args.cv.W, w0 = rem - h0 * args.cv.W;
+            ld4(sA, &tmA, c0, w0 + khw % 3 - 1, h0 + khw / 3 - 1, n_img);
+          } else if (!A_MN) {
+            ld2(sA, &tmA, kb * BK, m0);
           } else {
-            if (!A_MN) {
-              ptx::tma_load_2d(sA, &tmA, &full[stage], kb * BK, m0);
-            } else {
 #pragma unroll
-              for (int i = 0; i < BM / 64; ++i)
-                ptx::tma_load_2d(sA + i * 8192, &tmA, &full[stage], m0 + 64 * i, kb * BK);
+            for (int i = 0; i < BM / 64; ++i) ld2(sA + i * 8192, &tmA, m0 + 64 * i, kb * BK);
+          }
+          // ---- B tile: BN/CG rows (K-major) or BN/CG columns (MN-major) x 64 K
+          // BLEND: stash -> staging 1, latest -> staging 2; transform warps fill sB
+          uint8_t* dB = BLEND ? sB + C::B_BYTES : sB;
+          if (CONV == CONV_DGRAD) {
+            // B[(kh',kw',co), ci] = W[co, 2-kh', 2-kw', ci]: the flipped kernel, read in place
+            const int cpb = args.cv.C / 64;
+            const int khw = kb / cpb, co0 = (kb - khw * cpb) * 64;
+            const int kh = khw / 3, kw = khw % 3;
+#pragma unroll
+            for (int i = 0; i < BN / CG / 64; ++i) {
+              ld4(dB + i * 8192, &tmB, n0 + 64 * i, 2 - kw, 2 - kh, co0);
+              if (BLEND) ld4(dB + C::B_BYTES + i * 8192, &tmB2, n0 + 64 * i, 2 - kw, 2 - kh, co0);
             }
-            // BLEND: stash -> staging 1, latest -> staging 2; transform warps fill sB
-            uint8_t* dB = BLEND ? sB + C::B_BYTES : sB;
-            if (!B_MN) {
-              ptx::tma_load_2d(dB, &tmB, &full[stage], kb * BK, n0);
-              if (BLEND) ptx::tma_load_2d(dB + C::B_BYTES, &tmB2, &full[stage], kb * BK, n0);
-            } else {
+          } else if (CONV == CONV_WGRAD) {
+            // B = im2col(X): K block = 64 pixels (one (w,h,n) box), column (kh, kw, ci)
+            const int P = args.cv.H * args.cv.W;
+            const int p0 = kb * BK;
+            const int n_img = p0 / P, rem = p0 - n_img * P, h0 = rem / args.cv.W, w0 = rem - h0 * args.cv.W;
 #pragma unroll
-              for (int i = 0; i < BN / 64; ++i) {
-                ptx::tma_load_2d(dB + i * 8192, &tmB, &full[stage], n0 + 64 * i, kb * BK);
-                if (BLEND) ptx::tma_load_2d(dB + C::B_BYTES + i * 8192, &tmB2, &full[stage], n0 + 64 * i, kb * BK);
-              }
+            for (int i = 0; i < BN / CG / 64; ++i) {
+              const int col = n0 + 64 * i;
+              const int khw = col / args.cv.C, ci0 = col - khw * args.cv.C;
+              ld4(dB + i * 8192, &tmB, ci0, w0 + khw % 3 - 1, h0 + khw / 3 - 1, n_img);
+            }
+          } else if (!B_MN) {
+            ld2(dB, &tmB, kb * BK, n0);
+            if (BLEND) ld2(dB + C::B_BYTES, &tmB2, kb * BK, n0);
+          } else {
+#pragma unroll
+            for (int i = 0; i < BN / CG / 64; ++i) {
+              ld2(dB + i * 8192, &tmB, n0 + 64 * i, kb * BK);
+              if (BLEND) ld2(dB + C::B_BYTES + i * 8192, &tmB2, n0 + 64 * i, kb * BK);
             }
           }
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
@@ -461,6 +486,35 @@ bool make_tmap(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, u
   return r == CUDA_SUCCESS;
 }
 
+// 4-D bf16 NHWC-style tensor: dims {d0 (contiguous), d1, d2, d3}, box {64, b1, b2, b3}, 128B swizzle.
+bool make_tmap4(CUtensorMap* m, const void* base, const uint64_t (&d)[4], const uint32_t (&box)[4]) {
+  EncodeTiledFn enc = get_encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[4] = {d[0], d[1], d[2], d[3]};
+  cuuint64_t strides[3] = {d[0] * 2, d[0] * d[1] * 2, d[0] * d[1] * d[2] * 2};
+  cuuint32_t bx[4] = {box[0], box[1], box[2], box[3]};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, bx, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+// (w, h, n) extent of a box holding `pixels` consecutive NHWC pixels (row-major n, h, w)
+bool pixel_box(int pixels, int H, int W, uint32_t (&box)[4]) {
+  const int P = H * W;
+  if (W > 256 || H > 256) return false;
+  if (P >= pixels) {
+    if (pixels % W || P % pixels) return false;
+    box[1] = W; box[2] = pixels / W; box[3] = 1;
+  } else {
+    if (pixels % P || pixels / P > 256) return false;
+    box[1] = W; box[2] = H; box[3] = pixels / P;
+  }
+  box[0] = 64;
+  return true;
+}
+
 int num_sms() {
   static int n = 0;
   if (!n) {
@@ -472,11 +526,11 @@ int num_sms() {
   return n;
 }
 
-template <int BN, int A_MN, int B_MN, int BLEND, int SGD = 0, int CG = 1>
+template <int BN, int A_MN, int B_MN, int BLEND, int SGD = 0, int CG = 1, int CONV = CONV_NONE>
 cudaError_t launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& b2, const GemmArgs& args,
                    cudaStream_t st) {
   using C = Cfg<BN, BLEND, SGD, CG>;
-  auto kern = gemm_kernel<BN, A_MN, B_MN, BLEND, SGD, CG>;
+  auto kern = gemm_kernel<BN, A_MN, B_MN, BLEND, SGD, CG, CONV>;
   static bool attr_set = false;   // per instantiation
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
@@ -510,7 +564,7 @@ struct Tiling {
 // traffic per SM by a third; they are used when M fills at least two 128-row blocks and the
 // pair grid still covers the chip.  Env TPS_GEMM_CG=1 forces single-CTA tiles.
 Tiling pick_tiling(int M, int N, int mode, bool sgd) {
-  if (mode == GEMM_DGRAD_BLEND) return {1, 128};
+  if (mode == GEMM_DGRAD_BLEND || mode == GEMM_CONV_DGRAD_BLEND) return {1, 128};
   const int sms = num_sms();
   static int force_cg = -1;
   if (force_cg < 0) {
@@ -537,16 +591,16 @@ Tiling pick_tiling(int M, int N, int mode, bool sgd) {
   return {1, 64};
 }
 
-template <int A_MN, int B_MN, int SGD>
+template <int A_MN, int B_MN, int SGD, int CONV = CONV_NONE>
 cudaError_t dispatch(const Tiling& tl, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tb2,
                      const GemmArgs& args, cudaStream_t st) {
   if (tl.cg == 2) {
-    if (tl.bn == 256) return launch<256, A_MN, B_MN, 0, SGD, 2>(ta, tb, tb2, args, st);
-    return launch<128, A_MN, B_MN, 0, SGD, 2>(ta, tb, tb2, args, st);
+    if (tl.bn == 256) return launch<256, A_MN, B_MN, 0, SGD, 2, CONV>(ta, tb, tb2, args, st);
+    return launch<128, A_MN, B_MN, 0, SGD, 2, CONV>(ta, tb, tb2, args, st);
   }
-  if (tl.bn == 256) return launch<256, A_MN, B_MN, 0, SGD, 1>(ta, tb, tb2, args, st);
-  if (tl.bn == 128) return launch<128, A_MN, B_MN, 0, SGD, 1>(ta, tb, tb2, args, st);
-  return launch<64, A_MN, B_MN, 0, SGD, 1>(ta, tb, tb2, args, st);
+  if (tl.bn == 256) return launch<256, A_MN, B_MN, 0, SGD, 1, CONV>(ta, tb, tb2, args, st);
+  if (tl.bn == 128) return launch<128, A_MN, B_MN, 0, SGD, 1, CONV>(ta, tb, tb2, args, st);
+  return launch<64, A_MN, B_MN, 0, SGD, 1, CONV>(ta, tb, tb2, args, st);
 }
 
 }  // namespace
@@ -557,6 +611,10 @@ const char* gemm_mode_name(int mode) {
     case GEMM_DGRAD: return "dgrad";
     case GEMM_WGRAD: return "wgrad";
     case GEMM_DGRAD_BLEND: return "dgrad_blend";
+    case GEMM_CONV_FWD: return "conv_fwd";
+    case GEMM_CONV_DGRAD: return "conv_dgrad";
+    case GEMM_CONV_DGRAD_BLEND: return "conv_dgrad_blend";
+    case GEMM_CONV_WGRAD: return "conv_wgrad";
   }
   return "?";
 }
@@ -564,22 +622,49 @@ const char* gemm_mode_name(int mode) {
 cudaError_t gemm_run(int mode, const GemmOperands& op, const GemmArgs& args_in, cudaStream_t st, int* bn_out) {
   GemmArgs args = args_in;
   if (args.M <= 0 || args.N <= 0 || args.K <= 0) return cudaSuccess;
-  const bool sgd = (mode == GEMM_WGRAD && args.epi == EPI_SGD);
-  const Tiling tl = pick_tiling(args.M, args.N, mode, sgd);
-  if (bn_out) *bn_out = tl.bn * 10 + tl.cg;
+  const bool sgd = ((mode == GEMM_WGRAD || mode == GEMM_CONV_WGRAD) && args.epi == EPI_SGD);
+  Tiling tl = pick_tiling(args.M, args.N, mode, sgd);
   CUtensorMap ta, tb, tb2;
-  const bool a_mn = (mode == GEMM_WGRAD);
-  const bool b_mn = (mode != GEMM_FWD);
   bool ok = true;
-  // A: K-major [M,K] -> box {64 K, 128 rows}; MN-major stored [K,M] -> box {64 M, 64 K}
-  // B: K-major [N,K] -> box {64 K, BN/CG rows} (each CTA of a pair loads its share)
-  if (!a_mn) ok &= make_tmap(&ta, op.A, args.M, args.K, op.lda, BM);
-  else ok &= make_tmap(&ta, op.A, args.K, args.M, op.lda, 64);
-  if (!b_mn) ok &= make_tmap(&tb, op.B, args.N, args.K, op.ldb, tl.bn / tl.cg);
-  else ok &= make_tmap(&tb, op.B, args.K, args.N, op.ldb, 64);
-  if (mode == GEMM_DGRAD_BLEND) ok &= make_tmap(&tb2, op.B2, args.K, args.N, op.ldb, 64);
-  else tb2 = tb;
+  if (mode >= GEMM_CONV_FWD) {
+    const ConvGeom& g = op.cv;
+    args.cv = g;
+    if (g.C % 64 || g.N * g.H * g.W <= 0) return cudaErrorInvalidValue;
+    const uint64_t act_dims[4] = {static_cast<uint64_t>(g.C), static_cast<uint64_t>(g.W),
+                                  static_cast<uint64_t>(g.H), static_cast<uint64_t>(g.N)};
+    uint32_t box128[4], box64[4];
+    if (!pixel_box(128, g.H, g.W, box128) || !pixel_box(64, g.H, g.W, box64)) return cudaErrorInvalidValue;
+    if (mode == GEMM_CONV_FWD) {
+      ok &= make_tmap4(&ta, op.A, act_dims, box128);                              // X (NHWC)
+      ok &= make_tmap(&tb, op.B, args.N, args.K, op.ldb, tl.bn / tl.cg);           // W [Co, 9Ci]
+      tb2 = tb;
+    } else if (mode == GEMM_CONV_DGRAD || mode == GEMM_CONV_DGRAD_BLEND) {
+      ok &= make_tmap4(&ta, op.A, act_dims, box128);                              // dY (NHWC, C = Co)
+      const uint64_t wd[4] = {static_cast<uint64_t>(op.Cw), 3, 3, static_cast<uint64_t>(g.C)};
+      const uint32_t wb[4] = {64, 1, 1, 64};
+      ok &= make_tmap4(&tb, op.B, wd, wb);                                        // W [Co,3,3,Ci]
+      if (mode == GEMM_CONV_DGRAD_BLEND) ok &= make_tmap4(&tb2, op.B2, wd, wb);
+      else tb2 = tb;
+      if (op.Cw % 64) return cudaErrorInvalidValue;
+    } else {  // GEMM_CONV_WGRAD
+      ok &= make_tmap(&ta, op.A, args.K, args.M, op.lda, 64);                     // dY [NHW, Co], MN-major
+      ok &= make_tmap4(&tb, op.B, act_dims, box64);                               // X (NHWC)
+      tb2 = tb;
+    }
+  } else {
+    const bool a_mn = (mode == GEMM_WGRAD);
+    const bool b_mn = (mode != GEMM_FWD);
+    // A: K-major [M,K] -> box {64 K, 128 rows}; MN-major stored [K,M] -> box {64 M, 64 K}
+    // B: K-major [N,K] -> box {64 K, BN/CG rows} (each CTA of a pair loads its share)
+    if (!a_mn) ok &= make_tmap(&ta, op.A, args.M, args.K, op.lda, BM);
+    else ok &= make_tmap(&ta, op.A, args.K, args.M, op.lda, 64);
+    if (!b_mn) ok &= make_tmap(&tb, op.B, args.N, args.K, op.ldb, tl.bn / tl.cg);
+    else ok &= make_tmap(&tb, op.B, args.K, args.N, op.ldb, 64);
+    if (mode == GEMM_DGRAD_BLEND) ok &= make_tmap(&tb2, op.B2, args.K, args.N, op.ldb, 64);
+    else tb2 = tb;
+  }
   if (!ok) return cudaErrorInvalidValue;
+  if (bn_out) *bn_out = tl.bn * 10 + tl.cg;
   switch (mode) {
     case GEMM_FWD: return dispatch<0, 0, 0>(tl, ta, tb, tb2, args, st);
     case GEMM_DGRAD: return dispatch<0, 1, 0>(tl, ta, tb, tb2, args, st);
@@ -587,6 +672,12 @@ cudaError_t gemm_run(int mode, const GemmOperands& op, const GemmArgs& args_in, 
       if (sgd) return dispatch<1, 1, 1>(tl, ta, tb, tb2, args, st);
       return dispatch<1, 1, 0>(tl, ta, tb, tb2, args, st);
     case GEMM_DGRAD_BLEND: return launch<128, 0, 1, 1, 0, 1>(ta, tb, tb2, args, st);
+    case GEMM_CONV_FWD: return dispatch<0, 0, 0, CONV_FWD>(tl, ta, tb, tb2, args, st);
+    case GEMM_CONV_DGRAD: return dispatch<0, 1, 0, CONV_DGRAD>(tl, ta, tb, tb2, args, st);
+    case GEMM_CONV_DGRAD_BLEND: return launch<128, 0, 1, 1, 0, 1, CONV_DGRAD>(ta, tb, tb2, args, st);
+    case GEMM_CONV_WGRAD:
+      if (sgd) return dispatch<1, 1, 1, CONV_WGRAD>(tl, ta, tb, tb2, args, st);
+      return dispatch<1, 1, 0, CONV_WGRAD>(tl, ta, tb, tb2, args, st);
   }
   return cudaErrorInvalidValue;
 }

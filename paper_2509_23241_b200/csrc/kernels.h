@@ -35,6 +35,13 @@ cudaError_t launch_f32_to_bf16(const float* in, uint16_t* out, int64_t n, cudaSt
 cudaError_t launch_blend_materialize(const uint16_t* s, const uint16_t* l, uint16_t* out, int64_t n, float a,
                                      float b, cudaStream_t st);
 
+// image nets (NHWC bf16): 2x2/stride-2 max pool, its gradient (first maximum of each window,
+// reading Z15), and explicit 3x3/pad-1 patches [(n,h,w), (kh,kw,c)] zero-padded to ldp columns.
+cudaError_t launch_maxpool2_fwd(const uint16_t* X, uint16_t* Y, int N, int H, int W, int C, cudaStream_t st);
+cudaError_t launch_maxpool2_bwd(const uint16_t* X, const uint16_t* dY, uint16_t* dX, int N, int H, int W, int C,
+                                cudaStream_t st);
+cudaError_t launch_im2col3x3(const uint16_t* X, uint16_t* P, int N, int H, int W, int C, int ldp, cudaStream_t st);
+
 // synthgen-identical counter-based generator (see synthgen/__init__.py)
 //   kind 0/1: bf16 inputs into dst[rows, ld] (cols valid); kind 2: int32 labels[rows];
 //   kind 3: fp32 weights [rows=out, ld] (cols=in valid), scale 2^-(23 + shift).

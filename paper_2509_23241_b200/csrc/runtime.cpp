@@ -89,9 +89,19 @@ tps_status check_arch(int device) {
 }
 
 struct Layer {
-  int gidx = 0, in = 0, out = 0, Kp = 0, Np = 0;
+  int gidx = 0;
+  int kind = TPS_LAYER_LINEAR;
+  bool im2col = false;      // conv run as a GEMM on explicit patches (network layer 0, few channels)
+  // parameters (none for pools): logical [out, in], stored [Np, Kp]
+  int in = 0, out = 0, Kp = 0, Np = 0;
+  // activation geometry: a sample's input is hw_in pixels x ld_in channels (linear: 1 x Kp)
+  int H = 1, Wd = 1, Ci = 0, Co = 0;
+  int hw_in = 1, ld_in = 0, hw_out = 1, ld_out = 0;
   float *W = nullptr, *b = nullptr, *mW = nullptr, *mb = nullptr, *dW = nullptr, *db = nullptr;
   std::vector<uint16_t*> ver;  // R bf16 [Np, Kp] slots
+  bool has_w() const { return kind != TPS_LAYER_MAXPOOL2; }
+  int64_t in_elems() const { return static_cast<int64_t>(hw_in) * ld_in; }    // per sample (stash)
+  int64_t out_elems() const { return static_cast<int64_t>(hw_out) * ld_out; }
 };
 
 struct Msg {  // LOCAL transport mailbox entry
@@ -123,7 +133,9 @@ struct tps_pipeline {
   int classes = 0;
 
   // ---- device buffers
-  std::vector<std::vector<uint16_t*>> act;  // act[slot][k]  bf16 [B, Kp_k]   (slot count A0 for k=0, Kmax else)
+  std::vector<std::vector<uint16_t*>> act;  // act[slot][k]  bf16 [B, in_elems_k]  (slot count A0 for k=0, Kmax else)
+  std::vector<uint16_t*> x_stage;           // im2col first layer: raw input [B, H·W·C] per input slot
+  int64_t in0_elems = 0;                    // per-sample elements of the stage input as received
   uint16_t* send_fwd[2] = {nullptr, nullptr};
   uint16_t* gin[2] = {nullptr, nullptr};
   uint16_t* gout[2] = {nullptr, nullptr};
@@ -437,6 +449,31 @@ void update_stash_peak(tps_pipeline* p) {
 }
 
 // ------------------------------------------------------------------ the three events
+// one layer's forward on rows [r0, r0+nr) of the group: input Xin (this layer's stash rows),
+// output `out` (next layer's stash rows, the send buffer, or fp32 logits)
+tps_status layer_forward(tps_pipeline* p, Layer& Lk, int nr, const uint16_t* Xin, void* out, bool logits,
+                         int64_t v) {
+  const bool relu = !logits;
+  if (Lk.kind == TPS_LAYER_MAXPOOL2) {
+    CUDA_OK(tps::launch_maxpool2_fwd(Xin, static_cast<uint16_t*>(out), nr, Lk.H, Lk.Wd, Lk.Ci, p->cs));
+    p->launches += 1;
+    return TPS_OK;
+  }
+  tps::GemmArgs ga{};
+  ga.alpha = 1.f; ga.bias = Lk.b; ga.xa = 1.f; ga.xb = 0.f; ga.relu = relu ? 1 : 0; ga.out_f32 = logits ? 1 : 0;
+  ga.out = out; ga.ldo = Lk.Np;
+  ga.M = nr * Lk.hw_out; ga.N = Lk.Np; ga.K = Lk.Kp;
+  if (Lk.kind == TPS_LAYER_CONV3X3 && !Lk.im2col) {
+    // implicit im2col: Y[n·H·W, Co] = conv3x3(X) via 4-D TMA boxes of the NHWC input
+    tps::GemmOperands op{Xin, 0, Lk.ver[v % p->R], Lk.Kp, nullptr};
+    op.cv = tps::ConvGeom{nr, Lk.H, Lk.Wd, Lk.Ci};
+    return run_gemm(p, tps::GEMM_CONV_FWD, op, ga, 0);
+  }
+  // Linear, or the first conv on its explicit patches [n·H·W, Kp]
+  tps::GemmOperands op{Xin, Lk.Kp, Lk.ver[v % p->R], Lk.Kp, nullptr};
+  return run_gemm(p, tps::GEMM_FWD, op, ga, 0);
+}
+
 tps_status do_forward(tps_pipeline* p, int64_t j, int a0, int cnt, const void* x, const int32_t* labels) {
   TPS_TRY(expect(p, TPS_EV_F, j, a0, cnt));
   if (p->first && !x) return fail(TPS_E_INVALID_ARG, "stage 0 forward needs x");
@@ -448,17 +485,29 @@ tps_status do_forward(tps_pipeline* p, int64_t j, int a0, int cnt, const void* x
   const int slot0 = static_cast<int>(j % p->A0);
   const int slot = static_cast<int>(j % p->Kmax);
   Layer& L0 = p->layers[0];
-  uint16_t* X = p->act[slot0][0] + static_cast<size_t>(r0) * L0.Kp;
+  uint16_t* X = p->act[slot0][0] + static_cast<size_t>(r0) * L0.in_elems();
   if (p->first) {
     // input copy (device pool or pinned host) on the input stream: with the extra input
     // slot it overlaps the backward/update still running on the compute stream
-    const size_t w = static_cast<size_t>(L0.in) * 2;
     CUDA_OK(cudaStreamWaitEvent(p->s_fin, p->ev_act_free[slot0], 0));
-    CUDA_OK(cudaMemcpy2DAsync(X, static_cast<size_t>(L0.Kp) * 2, x, w, w, nr, cudaMemcpyDefault, p->s_fin));
+    if (L0.im2col) {
+      uint16_t* xs = p->x_stage[slot0] + static_cast<size_t>(r0) * p->in0_elems;
+      CUDA_OK(cudaMemcpyAsync(xs, x, static_cast<size_t>(nr) * p->in0_elems * 2, cudaMemcpyDefault, p->s_fin));
+    } else if (L0.kind == TPS_LAYER_LINEAR) {
+      const size_t w = static_cast<size_t>(L0.in) * 2;
+      CUDA_OK(cudaMemcpy2DAsync(X, static_cast<size_t>(L0.Kp) * 2, x, w, w, nr, cudaMemcpyDefault, p->s_fin));
+    } else {
+      CUDA_OK(cudaMemcpyAsync(X, x, static_cast<size_t>(nr) * L0.in_elems() * 2, cudaMemcpyDefault, p->s_fin));
+    }
     CUDA_OK(cudaEventRecord(p->ev_recv, p->s_fin));
     CUDA_OK(cudaStreamWaitEvent(p->cs, p->ev_recv, 0));
+    if (L0.im2col) {
+      CUDA_OK(tps::launch_im2col3x3(p->x_stage[slot0] + static_cast<size_t>(r0) * p->in0_elems, X, nr, L0.H, L0.Wd,
+                                    L0.Ci, L0.Kp, p->cs));
+      p->launches += 1;
+    }
   } else {
-    TPS_TRY(recv_fwd(p, j, grp, X, static_cast<size_t>(nr) * L0.Kp * 2));
+    TPS_TRY(recv_fwd(p, j, grp, X, static_cast<size_t>(nr) * L0.in_elems() * 2));
   }
   if (!p->last) {  // the send buffer of mb j-2 must have left
     CUDA_OK(cudaStreamWaitEvent(p->cs, p->ev_fwd_sent[static_cast<int>(j & 1) * p->ng + grp], 0));
@@ -467,24 +516,13 @@ tps_status do_forward(tps_pipeline* p, int64_t j, int a0, int cnt, const void* x
   const uint16_t* Xin = X;
   for (int k = 0; k < nl; ++k) {
     Layer& Lk = p->layers[k];
-    CUDA_OK(cudaStreamWaitEvent(p->cs, p->ev_upd_done[k], 0));   // latest version of layer k written
-    tps::GemmOperands op{Xin, Lk.Kp, Lk.ver[v % p->R], Lk.Kp, nullptr};
-    tps::GemmArgs ga{};
-    ga.M = nr; ga.N = Lk.Np; ga.K = Lk.Kp; ga.alpha = 1.f; ga.bias = Lk.b; ga.xa = 1.f; ga.xb = 0.f;
+    if (Lk.has_w()) CUDA_OK(cudaStreamWaitEvent(p->cs, p->ev_upd_done[k], 0));   // latest version written
     void* out;
-    if (k < nl - 1) {
-      out = p->act[slot][k + 1] + static_cast<size_t>(r0) * Lk.Np;
-      ga.relu = 1;
-    } else if (!p->last) {
-      out = p->send_fwd[j & 1] + static_cast<size_t>(r0) * Lk.Np;
-      ga.relu = 1;
-    } else {
-      out = p->logits + static_cast<size_t>(r0) * Lk.Np;
-      ga.relu = 0;
-      ga.out_f32 = 1;
-    }
-    ga.out = out; ga.ldo = Lk.Np;
-    TPS_TRY(run_gemm(p, tps::GEMM_FWD, op, ga, 0));
+    const bool logits = (k == nl - 1) && p->last;
+    if (k < nl - 1) out = p->act[slot][k + 1] + static_cast<size_t>(r0) * Lk.out_elems();
+    else if (!p->last) out = p->send_fwd[j & 1] + static_cast<size_t>(r0) * Lk.out_elems();
+    else out = p->logits + static_cast<size_t>(r0) * Lk.Np;
+    TPS_TRY(layer_forward(p, Lk, nr, Xin, out, logits, v));
     Xin = static_cast<const uint16_t*>(out);
   }
   if (p->last) {
@@ -505,8 +543,8 @@ tps_status do_forward(tps_pipeline* p, int64_t j, int a0, int cnt, const void* x
     }
   } else {
     Layer& Ll = p->layers[nl - 1];
-    TPS_TRY(send_fwd(p, j, grp, p->send_fwd[j & 1] + static_cast<size_t>(r0) * Ll.Np,
-                     static_cast<size_t>(nr) * Ll.Np * 2));
+    TPS_TRY(send_fwd(p, j, grp, p->send_fwd[j & 1] + static_cast<size_t>(r0) * Ll.out_elems(),
+                     static_cast<size_t>(nr) * Ll.out_elems() * 2));
   }
   tps_event e{};
   e.stage = p->s; e.kind = TPS_EV_F; e.micro = a0; e.micro_count = cnt; e.mb = j;
@@ -544,19 +582,21 @@ tps_status do_backward(tps_pipeline* p, int64_t j, int staleness) {
   if (p->last) {
     G = p->gce;
   } else {
-    TPS_TRY(recv_bwd(p, j, p->gin[j & 1], static_cast<size_t>(p->B) * Ll.Np * 2));
+    TPS_TRY(recv_bwd(p, j, p->gin[j & 1], static_cast<size_t>(p->B) * Ll.out_elems() * 2));
     G = p->gin[j & 1];
   }
   const int slot0 = static_cast<int>(j % p->A0);
   const int slot = static_cast<int>(j % p->Kmax);
+  const int B = p->B;
   int wbuf = 0;
   const int64_t vn = vl + 1;   // version the update of this mini-batch produces
+  const bool blend_on_load = p->variant == TPS_I && delta > 0 && (p->blend == TPS_BLEND_CONVEX || p->eq1_on_load);
   for (int k = nl - 1; k >= 0; --k) {
     Layer& Lk = p->layers[k];
     const uint16_t* X = (k == 0) ? p->act[slot0][0] : p->act[slot][k];
-    // dgrad first: it must read this layer's weights before a fused update rewrites them
+    // input gradient first: it must read this layer's weights before a fused update rewrites them
     uint16_t* dst = nullptr;
-    if (Lk.gidx > 0) {  // the network's first layer has no dgrad
+    if (Lk.gidx > 0) {  // the network's first layer has no input gradient
       if (k > 0) {
         dst = p->gwork[wbuf];
         wbuf ^= 1;
@@ -564,65 +604,83 @@ tps_status do_backward(tps_pipeline* p, int64_t j, int staleness) {
         CUDA_OK(cudaStreamWaitEvent(p->cs, p->ev_bwd_sent[j & 1], 0));  // gout of mb j-2 has left
         dst = p->gout[j & 1];
       }
-      const uint16_t* Ws = Lk.ver[v_used % p->R];
-      const uint16_t* Wl = Lk.ver[vl % p->R];
-      tps::GemmArgs ga{};
-      ga.M = p->B; ga.N = Lk.Kp; ga.K = Lk.Np; ga.out = dst; ga.ldo = Lk.Kp; ga.out_f32 = 0;
-      ga.mask = X; ga.ldm = Lk.Kp; ga.alpha = 1.f; ga.xa = 1.f; ga.xb = 0.f;
-      const bool blend_on_load =
-          p->variant == TPS_I && delta > 0 && (p->blend == TPS_BLEND_CONVEX || p->eq1_on_load);
-      if (blend_on_load) {
-        tps::GemmOperands op{G, Lk.Np, Ws, Lk.Kp, Wl};
-        ga.xa = alpha; ga.xb = beta;
-        TPS_TRY(run_gemm(p, tps::GEMM_DGRAD_BLEND, op, ga, 1));
+      if (Lk.kind == TPS_LAYER_MAXPOOL2) {
+        // gradient to the first window maximum; the ReLU mask was applied by the layer above
+        CUDA_OK(tps::launch_maxpool2_bwd(X, G, dst, B, Lk.H, Lk.Wd, Lk.Ci, p->cs));
+        p->launches += 1;
       } else {
+        const uint16_t* Ws = Lk.ver[v_used % p->R];
+        const uint16_t* Wl = Lk.ver[vl % p->R];
+        tps::GemmArgs ga{};
+        ga.out = dst; ga.out_f32 = 0; ga.mask = X; ga.ldm = Lk.ld_in; ga.ldo = Lk.ld_in;
+        ga.alpha = 1.f; ga.xa = 1.f; ga.xb = 0.f;
+        const bool conv = Lk.kind == TPS_LAYER_CONV3X3;
+        ga.M = B * Lk.hw_in; ga.N = conv ? Lk.Ci : Lk.Kp; ga.K = Lk.Np;
+        if (conv) ga.K = 9 * Lk.Co;
         tps::GemmOperands op{G, Lk.Np, Ws, Lk.Kp, nullptr};
-        ga.alpha = (p->variant == TPS_I) ? alpha : 1.f;   // EQ1: α·(G·W_stash) = G·(α·W_stash)
-        TPS_TRY(run_gemm(p, tps::GEMM_DGRAD, op, ga, 1));
+        if (conv) {
+          op.cv = tps::ConvGeom{B, Lk.H, Lk.Wd, Lk.Co};
+          op.Cw = Lk.Ci;
+        }
+        if (blend_on_load) {
+          op.B2 = Wl;
+          ga.xa = alpha; ga.xb = beta;
+          TPS_TRY(run_gemm(p, conv ? tps::GEMM_CONV_DGRAD_BLEND : tps::GEMM_DGRAD_BLEND, op, ga, 1));
+        } else {
+          ga.alpha = (p->variant == TPS_I) ? alpha : 1.f;   // EQ1: α·(G·W_stash) = G·(α·W_stash)
+          TPS_TRY(run_gemm(p, conv ? tps::GEMM_CONV_DGRAD : tps::GEMM_DGRAD, op, ga, 1));
+        }
       }
     }
-    // wgrad: dW[Np, Kp] = Gᵀ·X   (A = G stored [B, Np], B = X stored [B, Kp]); with fuse_update
-    // the epilogue applies the SGD/momentum step and writes version vn instead of storing dW
-    {
-      tps::GemmOperands op{G, Lk.Np, X, Lk.Kp, nullptr};
+    if (Lk.has_w()) {
+      // weight gradient: dW[Np, Kp] = Gᵀ·X (Linear / patch layer) or conv wgrad (implicit im2col);
+      // with fuse_update the epilogue applies the SGD/momentum step and writes version vn
+      const int rows = B * Lk.hw_out;
       tps::GemmArgs ga{};
-      ga.M = Lk.Np; ga.N = Lk.Kp; ga.K = p->B; ga.out = Lk.dW; ga.ldo = Lk.Kp; ga.out_f32 = 1;
+      ga.M = Lk.Np; ga.N = Lk.Kp; ga.K = rows; ga.out = Lk.dW; ga.ldo = Lk.Kp; ga.out_f32 = 1;
       ga.alpha = 1.f; ga.xa = 1.f;
       if (p->fuse_update) {
         ga.epi = tps::EPI_SGD;
         ga.w = Lk.W; ga.v = Lk.mW; ga.ver = Lk.ver[vn % p->R];
         ga.lr = p->lr; ga.mu = p->mu; ga.wd = p->wd;
       }
-      TPS_TRY(run_gemm(p, tps::GEMM_WGRAD, op, ga, 2));
-    }
-    CUDA_OK(tps::launch_bias_grad(G, p->B, Lk.Np, Lk.Np, Lk.db, p->scratch, p->cs));
-    p->launches += 2;
-    // U(j) always directly follows B(j) in the static order (reading Z7), so the update of
-    // this layer is issued now: either it already ran in the wgrad epilogue (fuse_update), or
-    // it runs on the optimizer stream, HBM-bound, underneath the remaining tensor-bound GEMMs
-    // of this backward.  The next forward of layer k waits for ev_upd_done[k].
-    cudaStream_t us = p->fuse_update ? p->cs : p->s_upd;
-    if (!p->fuse_update) {
-      CUDA_OK(cudaEventRecord(p->ev_grad_ready[k], p->cs));
-      CUDA_OK(cudaStreamWaitEvent(us, p->ev_grad_ready[k], 0));
-      const int64_t n = static_cast<int64_t>(Lk.Np) * Lk.Kp;
-      TimedLaunch tl{};
-      TPS_TRY(time_begin(p, &tl, 4, (p->mu != 0.f ? 22.0 : 14.0) * n, us));
-      CUDA_OK(tps::launch_sgd_update(Lk.W, Lk.mW, Lk.dW, Lk.ver[vn % p->R], n, p->lr, p->mu, p->wd, us,
-                                     p->upd_blocks_per_sm));
-      TPS_TRY(time_end(p, &tl, us));
+      if (Lk.kind == TPS_LAYER_CONV3X3 && !Lk.im2col) {
+        tps::GemmOperands op{G, Lk.Np, X, 0, nullptr};
+        op.cv = tps::ConvGeom{B, Lk.H, Lk.Wd, Lk.Ci};
+        TPS_TRY(run_gemm(p, tps::GEMM_CONV_WGRAD, op, ga, 2));
+      } else {
+        tps::GemmOperands op{G, Lk.Np, X, Lk.Kp, nullptr};
+        TPS_TRY(run_gemm(p, tps::GEMM_WGRAD, op, ga, 2));
+      }
+      CUDA_OK(tps::launch_bias_grad(G, rows, Lk.Np, Lk.Np, Lk.db, p->scratch, p->cs));
+      p->launches += 2;
+      // U(j) always directly follows B(j) in the static order (reading Z7), so the update of
+      // this layer is issued now: either it already ran in the wgrad epilogue (fuse_update), or
+      // it runs on the optimizer stream, HBM-bound, underneath the remaining tensor-bound GEMMs
+      // of this backward.  The next forward of layer k waits for ev_upd_done[k].
+      cudaStream_t us = p->fuse_update ? p->cs : p->s_upd;
+      if (!p->fuse_update) {
+        CUDA_OK(cudaEventRecord(p->ev_grad_ready[k], p->cs));
+        CUDA_OK(cudaStreamWaitEvent(us, p->ev_grad_ready[k], 0));
+        const int64_t n = static_cast<int64_t>(Lk.Np) * Lk.Kp;
+        TimedLaunch tl{};
+        TPS_TRY(time_begin(p, &tl, 4, (p->mu != 0.f ? 22.0 : 14.0) * n, us));
+        CUDA_OK(tps::launch_sgd_update(Lk.W, Lk.mW, Lk.dW, Lk.ver[vn % p->R], n, p->lr, p->mu, p->wd, us,
+                                       p->upd_blocks_per_sm));
+        TPS_TRY(time_end(p, &tl, us));
+        p->launches += 1;
+      }
+      CUDA_OK(tps::launch_sgd_update(Lk.b, Lk.mb, Lk.db, nullptr, Lk.Np, p->lr, p->mu, p->wd, us));
       p->launches += 1;
+      CUDA_OK(cudaEventRecord(p->ev_upd_done[k], us));
     }
-    CUDA_OK(tps::launch_sgd_update(Lk.b, Lk.mb, Lk.db, nullptr, Lk.Np, p->lr, p->mu, p->wd, us));
-    p->launches += 1;
-    CUDA_OK(cudaEventRecord(p->ev_upd_done[k], us));
     if (dst) G = dst;
   }
   // the input slot and the received gradient buffer may now be refilled
   CUDA_OK(cudaEventRecord(p->ev_act_free[slot0], p->cs));
   if (!p->last) CUDA_OK(cudaEventRecord(p->ev_gin_free[j & 1], p->cs));
   if (!p->first) {
-    TPS_TRY(send_bwd(p, j, p->gout[j & 1], static_cast<size_t>(p->B) * p->layers[0].Kp * 2));
+    TPS_TRY(send_bwd(p, j, p->gout[j & 1], static_cast<size_t>(p->B) * p->in0_elems * 2));
   }
   tps_event e{};
   e.stage = p->s; e.kind = TPS_EV_B; e.micro = -1; e.mb = j;
@@ -715,6 +773,40 @@ tps_status tps_schedule_events(int32_t S, int32_t s, int32_t m, int32_t fwd_grou
   return TPS_OK;
 }
 
+// image-net layer list: kinds, shapes and chaining (include/tps.h, tps_layer)
+tps_status validate_specs(const tps_config* c) {
+  if (c->num_layer_specs != c->num_layers || !c->layer_specs) return fail(TPS_E_CONFIG, "need num_layers layer specs");
+  int64_t prev_feat = -1;
+  int ph = 0, pw = 0, pc = 0;   // spatial output of the previous conv/pool layer
+  for (int l = 0; l < c->num_layers; ++l) {
+    const tps_layer& sp = c->layer_specs[l];
+    if (sp.kind == TPS_LAYER_LINEAR) {
+      if (sp.in_c < 1 || sp.out_c < 1) return fail(TPS_E_CONFIG, "layer %d: bad linear dims", l);
+      if (pc != 0 && sp.in_c % 16) return fail(TPS_E_CONFIG, "layer %d: flattened conv output must be a multiple of 16", l);
+      if (prev_feat >= 0 && sp.in_c != prev_feat) return fail(TPS_E_CONFIG, "layer %d: in %d != %lld", l, sp.in_c, (long long)prev_feat);
+      prev_feat = sp.out_c;
+      ph = pw = pc = 0;
+    } else if (sp.kind == TPS_LAYER_CONV3X3 || sp.kind == TPS_LAYER_MAXPOOL2) {
+      if (sp.in_h < 1 || sp.in_w < 1 || sp.in_c < 1) return fail(TPS_E_CONFIG, "layer %d: bad shape", l);
+      if (l > 0 && (pc == 0 || sp.in_h != ph || sp.in_w != pw || sp.in_c != pc))
+        return fail(TPS_E_CONFIG, "layer %d: input %dx%dx%d does not match the previous output", l, sp.in_h, sp.in_w, sp.in_c);
+      if (sp.kind == TPS_LAYER_CONV3X3) {
+        if (sp.out_c % 64) return fail(TPS_E_CONFIG, "layer %d: conv out_c must be a multiple of 64", l);
+        if (l > 0 && sp.in_c % 64) return fail(TPS_E_CONFIG, "layer %d: conv in_c must be a multiple of 64", l);
+        ph = sp.in_h; pw = sp.in_w; pc = sp.out_c;
+      } else {
+        if (sp.in_h % 2 || sp.in_w % 2 || sp.in_c % 8) return fail(TPS_E_CONFIG, "layer %d: pool needs even H, W and C %% 8", l);
+        ph = sp.in_h / 2; pw = sp.in_w / 2; pc = sp.in_c;
+      }
+      prev_feat = static_cast<int64_t>(ph) * pw * pc;
+    } else {
+      return fail(TPS_E_CONFIG, "layer %d: unknown kind %d", l, sp.kind);
+    }
+  }
+  if (c->layer_specs[c->num_layers - 1].kind != TPS_LAYER_LINEAR) return fail(TPS_E_CONFIG, "the last layer must be Linear");
+  return TPS_OK;
+}
+
 tps_status tps_pipeline_init(const tps_config* c, tps_pipeline** out) {
   if (!c || !out) return fail(TPS_E_INVALID_ARG, "null argument");
   *out = nullptr;
@@ -725,8 +817,12 @@ tps_status tps_pipeline_init(const tps_config* c, tps_pipeline** out) {
   if (c->variant != TPS_V && c->variant != TPS_I) return fail(TPS_E_CONFIG, "bad variant");
   if (c->blend != TPS_BLEND_EQ1 && c->blend != TPS_BLEND_CONVEX) return fail(TPS_E_CONFIG, "bad blend");
   if (c->variant == TPS_I && !(c->lambda > 0)) return fail(TPS_E_CONFIG, "lambda must be > 0 (P:227)");
-  for (int l = 0; l <= c->num_layers; ++l)
-    if (c->dims[l] < 1) return fail(TPS_E_CONFIG, "dims[%d] < 1", l);
+  if (c->num_layer_specs > 0) {
+    TPS_TRY(validate_specs(c));
+  } else {
+    for (int l = 0; l <= c->num_layers; ++l)
+      if (c->dims[l] < 1) return fail(TPS_E_CONFIG, "dims[%d] < 1", l);
+  }
   if (c->stage_bounds[0] != 0 || c->stage_bounds[c->num_stages] != c->num_layers)
     return fail(TPS_E_CONFIG, "stage_bounds must start at 0 and end at num_layers");
   for (int s = 0; s < c->num_stages; ++s)
@@ -747,7 +843,7 @@ tps_status tps_pipeline_init(const tps_config* c, tps_pipeline** out) {
   p->device = c->device; p->seed = c->seed;
   p->first = p->s == 0; p->last = p->s == p->S - 1;
   p->dims.assign(c->dims, c->dims + c->num_layers + 1);
-  p->classes = c->dims[c->num_layers];
+  p->classes = c->num_layer_specs > 0 ? c->layer_specs[c->num_layers - 1].out_c : c->dims[c->num_layers];
   p->Kmax = p->S - p->s;                         // in-flight mini-batches (reading Z6)
   p->R = (p->variant == TPS_I) ? p->Kmax : 1;    // weight version ring
   p->A0 = p->Kmax + (c->extra_recv_slot ? 1 : 0);
@@ -761,55 +857,92 @@ tps_status tps_pipeline_init(const tps_config* c, tps_pipeline** out) {
     return st;
   };
   const int lb = c->stage_bounds[p->s], le = c->stage_bounds[p->s + 1];
-  int maxd = 0;
+  int64_t max_elems = 0;
   for (int l = lb; l < le; ++l) {
     Layer L;
-    L.gidx = l; L.in = c->dims[l]; L.out = c->dims[l + 1]; L.Kp = pad16(L.in); L.Np = pad16(L.out);
-    maxd = std::max({maxd, L.Kp, L.Np});
-    const size_t n = static_cast<size_t>(L.Np) * L.Kp;
-    tps_status st;
-    if ((st = alloc_t(p, &L.W, n, &p->mem_weights)) != TPS_OK) return cleanup(st);
-    if ((st = alloc_t(p, &L.b, L.Np, &p->mem_weights)) != TPS_OK) return cleanup(st);
-    if (p->mu != 0.f) {
-      if ((st = alloc_t(p, &L.mW, n, &p->mem_optim)) != TPS_OK) return cleanup(st);
-      if ((st = alloc_t(p, &L.mb, L.Np, &p->mem_optim)) != TPS_OK) return cleanup(st);
+    L.gidx = l;
+    if (c->num_layer_specs > 0) {
+      const tps_layer& sp = c->layer_specs[l];
+      L.kind = sp.kind;
+      if (sp.kind == TPS_LAYER_LINEAR) {
+        L.in = sp.in_c; L.out = sp.out_c; L.Kp = pad16(L.in); L.Np = pad16(L.out);
+        L.ld_in = L.Kp; L.ld_out = L.Np;
+      } else {
+        L.H = sp.in_h; L.Wd = sp.in_w; L.Ci = sp.in_c;
+        L.hw_in = L.H * L.Wd; L.ld_in = L.Ci;
+        if (sp.kind == TPS_LAYER_CONV3X3) {
+          L.Co = sp.out_c;
+          L.in = 9 * L.Ci; L.out = L.Co; L.Np = L.Co;
+          L.im2col = (L.Ci % 64) != 0;
+          L.Kp = L.im2col ? pad16(L.in) : L.in;
+          L.hw_out = L.hw_in; L.ld_out = L.Co;
+          if (L.im2col) L.ld_in = L.Kp;            // the stash holds the patches
+        } else {
+          L.Co = L.Ci;
+          L.hw_out = L.hw_in / 4; L.ld_out = L.Ci;
+        }
+      }
+    } else {
+      L.in = c->dims[l]; L.out = c->dims[l + 1]; L.Kp = pad16(L.in); L.Np = pad16(L.out);
+      L.ld_in = L.Kp; L.ld_out = L.Np;
     }
-    if (!p->fuse_update && (st = alloc_t(p, &L.dW, n, &p->mem_optim)) != TPS_OK) return cleanup(st);
-    if ((st = alloc_t(p, &L.db, L.Np, &p->mem_optim)) != TPS_OK) return cleanup(st);
-    L.ver.resize(p->R);
-    for (int r = 0; r < p->R; ++r)
-      if ((st = alloc_t(p, &L.ver[r], n, r == 0 ? &p->mem_weights : &p->mem_stash)) != TPS_OK) return cleanup(st);
-    p->ver_bytes += static_cast<int64_t>(n) * 2;
+    max_elems = std::max({max_elems, L.in_elems(), L.out_elems()});
+    if (L.has_w()) {
+      const size_t n = static_cast<size_t>(L.Np) * L.Kp;
+      tps_status st;
+      if ((st = alloc_t(p, &L.W, n, &p->mem_weights)) != TPS_OK) return cleanup(st);
+      if ((st = alloc_t(p, &L.b, L.Np, &p->mem_weights)) != TPS_OK) return cleanup(st);
+      if (p->mu != 0.f) {
+        if ((st = alloc_t(p, &L.mW, n, &p->mem_optim)) != TPS_OK) return cleanup(st);
+        if ((st = alloc_t(p, &L.mb, L.Np, &p->mem_optim)) != TPS_OK) return cleanup(st);
+      }
+      if (!p->fuse_update && (st = alloc_t(p, &L.dW, n, &p->mem_optim)) != TPS_OK) return cleanup(st);
+      if ((st = alloc_t(p, &L.db, L.Np, &p->mem_optim)) != TPS_OK) return cleanup(st);
+      L.ver.resize(p->R);
+      for (int r = 0; r < p->R; ++r)
+        if ((st = alloc_t(p, &L.ver[r], n, r == 0 ? &p->mem_weights : &p->mem_stash)) != TPS_OK) return cleanup(st);
+      p->ver_bytes += static_cast<int64_t>(n) * 2;
+    }
     p->layers.push_back(L);
   }
   const int nl = p->nlayers();
   tps_status st;
+  const Layer& L0 = p->layers[0];
+  p->in0_elems = L0.im2col ? static_cast<int64_t>(L0.hw_in) * L0.Ci : L0.in_elems();
   p->act.assign(std::max(p->A0, p->Kmax), std::vector<uint16_t*>(nl, nullptr));
   for (int slot = 0; slot < static_cast<int>(p->act.size()); ++slot)
     for (int k = 0; k < nl; ++k) {
       const bool need = (k == 0) ? slot < p->A0 : slot < p->Kmax;
-      if (need && (st = alloc_t(p, &p->act[slot][k], static_cast<size_t>(p->B) * p->layers[k].Kp, &p->mem_acts)) != TPS_OK)
+      if (need && (st = alloc_t(p, &p->act[slot][k], static_cast<size_t>(p->B) * p->layers[k].in_elems(), &p->mem_acts)) != TPS_OK)
         return cleanup(st);
     }
-  const int NpL = p->layers[nl - 1].Np, Kp0 = p->layers[0].Kp;
+  if (L0.im2col) {
+    p->x_stage.assign(p->A0, nullptr);
+    for (int slot = 0; slot < p->A0; ++slot)
+      if ((st = alloc_t(p, &p->x_stage[slot], static_cast<size_t>(p->B) * p->in0_elems, &p->mem_acts)) != TPS_OK)
+        return cleanup(st);
+  }
+  const int64_t outL = p->layers[nl - 1].out_elems(), in0 = p->in0_elems;
   for (int i = 0; i < 2; ++i) {
     if (!p->last) {
-      if ((st = alloc_t(p, &p->send_fwd[i], static_cast<size_t>(p->B) * NpL, &p->mem_comm)) != TPS_OK) return cleanup(st);
-      if ((st = alloc_t(p, &p->gin[i], static_cast<size_t>(p->B) * NpL, &p->mem_comm)) != TPS_OK) return cleanup(st);
+      if ((st = alloc_t(p, &p->send_fwd[i], static_cast<size_t>(p->B) * outL, &p->mem_comm)) != TPS_OK) return cleanup(st);
+      if ((st = alloc_t(p, &p->gin[i], static_cast<size_t>(p->B) * outL, &p->mem_comm)) != TPS_OK) return cleanup(st);
     }
-    if (!p->first && (st = alloc_t(p, &p->gout[i], static_cast<size_t>(p->B) * Kp0, &p->mem_comm)) != TPS_OK) return cleanup(st);
-    if (nl > 1 && (st = alloc_t(p, &p->gwork[i], static_cast<size_t>(p->B) * maxd, &p->mem_acts)) != TPS_OK) return cleanup(st);
+    if (!p->first && (st = alloc_t(p, &p->gout[i], static_cast<size_t>(p->B) * in0, &p->mem_comm)) != TPS_OK) return cleanup(st);
+    if (nl > 1 && (st = alloc_t(p, &p->gwork[i], static_cast<size_t>(p->B) * max_elems, &p->mem_acts)) != TPS_OK) return cleanup(st);
   }
   if (p->last) {
-    if ((st = alloc_t(p, &p->logits, static_cast<size_t>(p->B) * NpL, &p->mem_acts)) != TPS_OK) return cleanup(st);
-    if ((st = alloc_t(p, &p->gce, static_cast<size_t>(p->B) * NpL, &p->mem_acts)) != TPS_OK) return cleanup(st);
+    if (p->layers[nl - 1].kind != TPS_LAYER_LINEAR) return cleanup(fail(TPS_E_CONFIG, "the last layer must be the Linear head"));
+    if ((st = alloc_t(p, &p->logits, static_cast<size_t>(p->B) * outL, &p->mem_acts)) != TPS_OK) return cleanup(st);
+    if ((st = alloc_t(p, &p->gce, static_cast<size_t>(p->B) * outL, &p->mem_acts)) != TPS_OK) return cleanup(st);
     if ((st = alloc_t(p, &p->loss_rows, p->B, &p->mem_acts)) != TPS_OK) return cleanup(st);
     if ((st = alloc_t(p, &p->labels_dev, p->B, &p->mem_acts)) != TPS_OK) return cleanup(st);
     p->loss_cap = 1 << 20;
     if ((st = alloc_t(p, &p->losses, p->loss_cap, &p->mem_acts)) != TPS_OK) return cleanup(st);
   }
   int64_t scr = 0;
-  for (auto& L : p->layers) scr = std::max(scr, tps::bias_grad_scratch_floats(p->B, L.Np));
+  for (auto& L : p->layers)
+    if (L.has_w()) scr = std::max(scr, tps::bias_grad_scratch_floats(p->B * L.hw_out, L.Np));
   if ((st = alloc_t(p, &p->scratch, scr, &p->mem_optim)) != TPS_OK) return cleanup(st);
 
   // streams and events
@@ -1025,6 +1158,7 @@ tps_status tps_intermediate_weight(tps_pipeline* p, int32_t layer, int32_t stale
   if (staleness < 0 || staleness > p->latest || staleness >= p->R) return fail(TPS_E_STALENESS, "no live stash for staleness %d", staleness);
   float a, b;
   compute_coeffs(p->variant, p->blend, staleness, p->lambda, &a, &b);
+  if (!p->layers[layer].has_w()) return fail(TPS_E_INVALID_ARG, "layer %d has no parameters", layer);
   Layer& L = p->layers[layer];
   CUDA_OK(cudaStreamWaitEvent(p->cs, p->ev_upd_done[layer], 0));
   const int64_t vs = p->latest - staleness;
@@ -1038,6 +1172,7 @@ tps_status tps_get_version(tps_pipeline* p, int32_t layer, int32_t staleness, vo
   TPS_TRY(check_usable(p));
   if (layer < 0 || layer >= p->nlayers() || !out_bf16) return fail(TPS_E_INVALID_ARG, "bad layer/out");
   if (staleness < 0 || staleness > p->latest || staleness >= p->R) return fail(TPS_E_STALENESS, "no live version at staleness %d", staleness);
+  if (!p->layers[layer].has_w()) return fail(TPS_E_INVALID_ARG, "layer %d has no parameters", layer);
   Layer& L = p->layers[layer];
   CUDA_OK(cudaStreamWaitEvent(p->cs, p->ev_upd_done[layer], 0));
   CUDA_OK(cudaMemcpyAsync(out_bf16, L.ver[(p->latest - staleness) % p->R], static_cast<size_t>(L.Np) * L.Kp * 2,
@@ -1050,6 +1185,7 @@ tps_status tps_get_weights(tps_pipeline* p, int32_t layer, float* w, float* b, f
   TPS_TRY(check_usable(p));
   if (layer < 0 || layer >= p->nlayers()) return fail(TPS_E_INVALID_ARG, "bad layer %d", layer);
   TPS_TRY(sync_streams(p));
+  if (!p->layers[layer].has_w()) return fail(TPS_E_INVALID_ARG, "layer %d has no parameters", layer);
   Layer& L = p->layers[layer];
   const size_t rowb = static_cast<size_t>(L.in) * 4, ldb = static_cast<size_t>(L.Kp) * 4;
   if (w) CUDA_OK(cudaMemcpy2D(w, rowb, L.W, ldb, rowb, L.out, cudaMemcpyDeviceToHost));
@@ -1069,6 +1205,7 @@ tps_status tps_set_weights(tps_pipeline* p, int32_t layer, const float* w, const
   TPS_TRY(check_usable(p));
   if (layer < 0 || layer >= p->nlayers()) return fail(TPS_E_INVALID_ARG, "bad layer %d", layer);
   TPS_TRY(sync_streams(p));
+  if (!p->layers[layer].has_w()) return fail(TPS_E_INVALID_ARG, "layer %d has no parameters", layer);
   Layer& L = p->layers[layer];
   const size_t rowb = static_cast<size_t>(L.in) * 4, ldb = static_cast<size_t>(L.Kp) * 4;
   const size_t n = static_cast<size_t>(L.Np) * L.Kp;
@@ -1091,6 +1228,7 @@ tps_status tps_set_weights(tps_pipeline* p, int32_t layer, const float* w, const
 tps_status tps_init_weights_synthetic(tps_pipeline* p) {
   TPS_TRY(check_usable(p));
   for (auto& L : p->layers) {
+    if (!L.has_w()) continue;
     const int shift = static_cast<int>(std::lround(std::log2(std::sqrt(static_cast<double>(L.in)))));
     CUDA_OK(cudaMemsetAsync(L.W, 0, static_cast<size_t>(L.Np) * L.Kp * 4, p->cs));
     CUDA_OK(tps::launch_fill_synthetic(3, p->seed, 0x0100 + static_cast<uint64_t>(L.gidx), L.out, L.in, L.Kp, 0, shift,
@@ -1176,6 +1314,43 @@ tps_status tps_fill_synthetic(int32_t kind, uint64_t seed, uint64_t tid, int64_t
   TPS_TRY(check_arch(dev));
   CUDA_OK(tps::launch_fill_synthetic(kind, seed, tid, rows, cols, cols, classes, 0, dst,
                                      reinterpret_cast<cudaStream_t>(stream)));
+  return TPS_OK;
+}
+
+tps_status tps_conv_gemm(int32_t mode, int32_t N, int32_t H, int32_t W, int32_t Ci, int32_t Co, const void* A,
+                         const void* Wt, const void* W2, void* out, int32_t out_f32, const float* bias, int32_t relu,
+                         float alpha, float beta, const void* mask, uint64_t stream) {
+  if (mode < 0 || mode > 3 || N < 1 || H < 1 || W < 1 || !A || !Wt || !out) return fail(TPS_E_INVALID_ARG, "bad conv operands");
+  if (Ci % 64 || Co % 64) return fail(TPS_E_INVALID_ARG, "Ci and Co must be multiples of 64");
+  if (mode == 3 && !W2) return fail(TPS_E_INVALID_ARG, "blend mode needs W2");
+  int dev = 0;
+  CUDA_OK(cudaGetDevice(&dev));
+  TPS_TRY(check_arch(dev));
+  const int P = N * H * W;
+  tps::GemmOperands op{};
+  tps::GemmArgs ga{};
+  ga.out = out; ga.out_f32 = out_f32; ga.alpha = 1.f; ga.xa = 1.f; ga.xb = 0.f;
+  int gm;
+  if (mode == 0) {
+    op = tps::GemmOperands{A, 0, Wt, 9 * Ci, nullptr};
+    op.cv = tps::ConvGeom{N, H, W, Ci};
+    ga.M = P; ga.N = Co; ga.K = 9 * Ci; ga.ldo = Co; ga.bias = bias; ga.relu = relu;
+    gm = tps::GEMM_CONV_FWD;
+  } else if (mode == 2) {
+    op = tps::GemmOperands{A, Co, Wt, 0, nullptr};
+    op.cv = tps::ConvGeom{N, H, W, Ci};
+    ga.M = Co; ga.N = 9 * Ci; ga.K = P; ga.ldo = 9 * Ci; ga.out_f32 = 1;
+    gm = tps::GEMM_CONV_WGRAD;
+  } else {
+    op = tps::GemmOperands{A, Co, Wt, 9 * Ci, mode == 3 ? W2 : nullptr};
+    op.cv = tps::ConvGeom{N, H, W, Co};
+    op.Cw = Ci;
+    ga.M = P; ga.N = Ci; ga.K = 9 * Co; ga.ldo = Ci;
+    ga.mask = static_cast<const uint16_t*>(mask); ga.ldm = Ci;
+    if (mode == 3) { ga.xa = alpha; ga.xb = beta; } else { ga.alpha = alpha; }
+    gm = mode == 3 ? tps::GEMM_CONV_DGRAD_BLEND : tps::GEMM_CONV_DGRAD;
+  }
+  CUDA_OK(tps::gemm_run(gm, op, ga, reinterpret_cast<cudaStream_t>(stream)));
   return TPS_OK;
 }
 

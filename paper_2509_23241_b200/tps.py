@@ -31,7 +31,9 @@ EXPORTS = [
     "tps_intermediate_weight", "tps_get_version", "tps_schedule_events", "tps_get_weights", "tps_set_weights",
     "tps_init_weights_synthetic", "tps_get_losses", "tps_get_trace", "tps_clear_trace", "tps_memory_stats",
     "tps_set_profiling", "tps_kernel_stats", "tps_launch_count", "tps_fill_synthetic", "tps_gemm",
+    "tps_conv_gemm",
 ]
+TPS_LAYER_LINEAR, TPS_LAYER_CONV3X3, TPS_LAYER_MAXPOOL2 = 0, 1, 2
 
 
 class TpsError(RuntimeError):
@@ -46,6 +48,11 @@ class Event(C.Structure):
                 ("alpha", C.c_float), ("beta", C.c_float)]
 
 
+class Layer(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("in_c", C.c_int32), ("out_c", C.c_int32), ("in_h", C.c_int32),
+                ("in_w", C.c_int32), ("reserved", C.c_int32 * 3)]
+
+
 class Config(C.Structure):
     _fields_ = [("num_layers", C.c_int32), ("dims", C.POINTER(C.c_int32)), ("num_stages", C.c_int32),
                 ("stage_bounds", C.POINTER(C.c_int32)), ("stage_id", C.c_int32), ("micro_batches", C.c_int32),
@@ -54,7 +61,7 @@ class Config(C.Structure):
                 ("weight_decay", C.c_float), ("transport", C.c_int32), ("nccl_ids", C.c_void_p),
                 ("device", C.c_int32), ("seed", C.c_uint64), ("compute_stream", C.c_uint64),
                 ("extra_recv_slot", C.c_int32), ("fuse_update", C.c_int32),
-                ("reserved", C.c_int32 * 6)]
+                ("num_layer_specs", C.c_int32), ("layer_specs", C.POINTER(Layer)), ("reserved", C.c_int32 * 4)]
 
 
 _LIB = None
@@ -99,6 +106,7 @@ def lib() -> C.CDLL:
             "tps_launch_count": (I32, [P, C.POINTER(I64)]),
             "tps_fill_synthetic": (I32, [I32, U64, U64, I64, I64, I32, P, U64]),
             "tps_gemm": (I32, [I32, I32, I32, I32, P, I32, P, I32, P, P, I32, I32, P, I32, F, F, P, I32, U64]),
+            "tps_conv_gemm": (I32, [I32, I32, I32, I32, I32, I32, P, P, P, P, I32, P, I32, F, F, P, U64]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -153,6 +161,25 @@ def gemm(mode, M, N, K, A, lda, B, ldb, out, ldo, out_f32=0, bias=None, relu=0, 
                          alpha, beta, ptr(mask), ldm, stream))
 
 
+def conv_gemm(mode, N, H, W, Ci, Co, A, Wt, out, out_f32=0, bias=None, relu=0, alpha=1.0, beta=0.0, mask=None,
+              W2=None, stream: int = 0) -> None:
+    check(lib().tps_conv_gemm(mode, N, H, W, Ci, Co, ptr(A), ptr(Wt), ptr(W2), ptr(out), out_f32, ptr(bias), relu,
+                              alpha, beta, ptr(mask), stream))
+
+
+def layer_specs(specs: list[dict]):
+    """oracle-style layer dicts -> ctypes tps_layer array."""
+    arr = (Layer * len(specs))()
+    for i, sp in enumerate(specs):
+        if sp["kind"] == "linear":
+            arr[i] = Layer(TPS_LAYER_LINEAR, sp["in"], sp["out"], 1, 1)
+        elif sp["kind"] == "conv3":
+            arr[i] = Layer(TPS_LAYER_CONV3X3, sp["cin"], sp["cout"], sp["h"], sp["w"])
+        else:
+            arr[i] = Layer(TPS_LAYER_MAXPOOL2, sp["c"], sp["c"], sp["h"], sp["w"])
+    return arr
+
+
 # ------------------------------------------------------------------ handle wrapper
 @dataclass
 class StageSpec:
@@ -175,6 +202,7 @@ class StageSpec:
     compute_stream: int = 0
     extra_recv_slot: int = 1
     fuse_update: int = 1
+    layers: list | None = None       # oracle-style layer dicts (image nets); None => MLP from dims
     _keep: list = field(default_factory=list)
 
 
@@ -183,10 +211,18 @@ class Pipeline:
 
     def __init__(self, spec: StageSpec):
         self.spec = spec
-        L = len(spec.dims) - 1
-        dims = (C.c_int32 * (L + 1))(*spec.dims)
+        if spec.layers:
+            L = len(spec.layers)
+            s0 = spec.layers[0]
+            feat = s0["h"] * s0["w"] * s0["cin"] if s0["kind"] == "conv3" else s0["in"]
+            dvals = [feat] + [0] * (L - 1) + [spec.layers[-1]["out"]]
+        else:
+            L = len(spec.dims) - 1
+            dvals = list(spec.dims)
+        dims = (C.c_int32 * (L + 1))(*dvals)
         bounds = (C.c_int32 * len(spec.stage_bounds))(*spec.stage_bounds)
         ids = C.create_string_buffer(spec.nccl_ids, len(spec.nccl_ids)) if spec.nccl_ids else None
+        specs = layer_specs(spec.layers) if spec.layers else None
         cfg = Config(num_layers=L, dims=dims, num_stages=len(spec.stage_bounds) - 1, stage_bounds=bounds,
                      stage_id=spec.stage_id, micro_batches=spec.micro_batches,
                      micro_batch_size=spec.micro_batch_size, fwd_group=spec.fwd_group, variant=spec.variant,
@@ -194,12 +230,21 @@ class Pipeline:
                      weight_decay=spec.weight_decay, transport=spec.transport,
                      nccl_ids=C.cast(ids, C.c_void_p) if ids is not None else None, device=spec.device,
                      seed=spec.seed, compute_stream=spec.compute_stream, extra_recv_slot=spec.extra_recv_slot,
-                     fuse_update=spec.fuse_update)
+                     fuse_update=spec.fuse_update, num_layer_specs=len(spec.layers) if spec.layers else 0,
+                     layer_specs=specs)
         h = C.c_void_p()
         check(lib().tps_pipeline_init(C.byref(cfg), C.byref(h)))
         self.h = h
         self.S = len(spec.stage_bounds) - 1
         self.layers = list(range(spec.stage_bounds[spec.stage_id], spec.stage_bounds[spec.stage_id + 1]))
+        self.shapes = []   # logical [out, in] of each stage-local layer (None for pools)
+        for g in self.layers:
+            if spec.layers:
+                sp = spec.layers[g]
+                self.shapes.append(None if sp["kind"] == "pool2" else
+                                   (sp["cout"], 9 * sp["cin"]) if sp["kind"] == "conv3" else (sp["out"], sp["in"]))
+            else:
+                self.shapes.append((spec.dims[g + 1], spec.dims[g]))
 
     def close(self):
         if self.h:
@@ -243,8 +288,7 @@ class Pipeline:
 
     def get_weights(self, layer: int):
         import numpy as np
-        g = self.layers[layer]
-        out_f, in_f = self.spec.dims[g + 1], self.spec.dims[g]
+        out_f, in_f = self.shapes[layer]
         w = np.zeros((out_f, in_f), np.float32)
         b = np.zeros(out_f, np.float32)
         mw = np.zeros_like(w)

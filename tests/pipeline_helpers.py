@@ -18,21 +18,50 @@ def workload(dims, m, b, M, seed=0, kind=synthgen.X_SIGNED):
     return xs, ys, w0, b0
 
 
-def run_oracle(dims, bounds, m, b, M, variant, blend, lam, lr, mu, wd=0.0, seed=0, kind=synthgen.X_SIGNED):
-    xs, ys, w0, b0 = workload(dims, m, b, M, seed, kind)
-    cfg = opipe.Config(dims, bounds, m, b, M, variant=variant, blend=blend, lam=lam, lr=lr, momentum=mu, wd=wd)
+def net_workload(layers, m, b, M, seed=0, kind=synthgen.X_UNIT):
+    """Image-net inputs (flattened NHWC rows) and synthgen weights ([Co,3,3,Ci] for convs)."""
+    s0 = layers[0]
+    feat = s0["h"] * s0["w"] * s0["cin"]
+    classes = layers[-1]["out"]
+    xs = [synthgen.inputs(seed, j, m * b, feat, kind) for j in range(M)]
+    ys = [synthgen.labels(seed, j, m * b, classes) for j in range(M)]
+    w0, b0 = [], []
+    for l, sp in enumerate(layers):
+        if sp["kind"] == "pool2":
+            w0.append(None)
+            b0.append(None)
+        elif sp["kind"] == "conv3":
+            w0.append(synthgen.weights(seed, l, sp["cout"], 9 * sp["cin"]).reshape(sp["cout"], 3, 3, sp["cin"]))
+            b0.append(np.zeros(sp["cout"], np.float32))
+        else:
+            w0.append(synthgen.weights(seed, l, sp["out"], sp["in"]))
+            b0.append(np.zeros(sp["out"], np.float32))
+    return xs, ys, w0, b0
+
+
+def run_oracle(dims, bounds, m, b, M, variant, blend, lam, lr, mu, wd=0.0, seed=0, kind=synthgen.X_SIGNED,
+               layers=None):
+    if layers:
+        xs, ys, w0, b0 = net_workload(layers, m, b, M, seed, kind)
+    else:
+        xs, ys, w0, b0 = workload(dims, m, b, M, seed, kind)
+    cfg = opipe.Config(dims, bounds, m, b, M, variant=variant, blend=blend, lam=lam, lr=lr, momentum=mu, wd=wd,
+                       layers=layers)
     return opipe.run(cfg, xs, ys, w0, b0)
 
 
 def run_gpu(dims, bounds, m, b, M, variant, blend, lam, lr, mu, wd=0.0, seed=0, kind=synthgen.X_SIGNED,
-            fwd_group=0, init="set", extra_recv_slot=1, fuse_update=1):
+            fwd_group=0, init="set", extra_recv_slot=1, fuse_update=1, layers=None):
     """All S stages as LOCAL-transport handles on cuda:0; returns (stages, losses)."""
     import torch
 
     from paper_2509_23241_b200 import tps
 
     S = len(bounds) - 1
-    xs, ys, w0, b0 = workload(dims, m, b, M, seed, kind)
+    if layers:
+        xs, ys, w0, b0 = net_workload(layers, m, b, M, seed, kind)
+    else:
+        xs, ys, w0, b0 = workload(dims, m, b, M, seed, kind)
     x_pool = torch.from_numpy(np.stack(xs)).to(torch.bfloat16).cuda().contiguous()
     y_pool = torch.from_numpy(np.stack(ys)).cuda().contiguous()
     V = tps.TPS_V if variant == ost.V_VARIANT else tps.TPS_I
@@ -42,11 +71,12 @@ def run_gpu(dims, bounds, m, b, M, variant, blend, lam, lr, mu, wd=0.0, seed=0, 
         spec = tps.StageSpec(dims=dims, stage_bounds=bounds, stage_id=s, micro_batches=m, micro_batch_size=b,
                              fwd_group=fwd_group, variant=V, blend=BL, lam=lam, lr=lr, momentum=mu, weight_decay=wd,
                              transport=tps.TPS_TRANSPORT_LOCAL if S > 1 else tps.TPS_TRANSPORT_NONE, seed=seed,
-                             extra_recv_slot=extra_recv_slot, fuse_update=fuse_update)
+                             extra_recv_slot=extra_recv_slot, fuse_update=fuse_update, layers=layers)
         st = tps.Pipeline(spec)
         if init == "set":
             for k, l in enumerate(st.layers):
-                st.set_weights(k, w0[l], b0[l])
+                if w0[l] is not None:
+                    st.set_weights(k, np.asarray(w0[l]).reshape(w0[l].shape[0], -1), b0[l])
         else:
             st.init_weights_synthetic()
         stages.append(st)
