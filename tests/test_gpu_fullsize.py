@@ -1,0 +1,50 @@
+"""Parity at BASELINE.json's full sizes, in the launch configuration bench.py times.
+
+* C5 (the bench workload): 16 x Linear(4096,4096)+ReLU + head, B = 2048 (32 micro-batches of
+  64, all forwards in one launch), I-TiMePReSt EQ1, SGD momentum 0.9, S = 1 — the oracle replays
+  the whole first mini-batch (forward, collective backward, update of all 270M parameters).
+* C2: 4-stage 4096-wide MLP, 8 micro-batches of 64, staleness 3/2/1/0 by stage — the full
+  pipeline for 6 mini-batches on one GPU (LOCAL transport) against the oracle.
+Both: trace bit-exact, losses within 1e-3 relative, weights within 5e-3 (Z19).
+"""
+import numpy as np
+import pytest
+
+import synthgen
+from oracle import staleness as ost
+from pipeline_helpers import expand_gpu_trace, layer_rel_err, oracle_trace, run_gpu, run_oracle, weight_rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+def check(stages, losses, ref):
+    assert expand_gpu_trace(stages) == oracle_trace(ref)
+    np.testing.assert_allclose(losses, ref.losses, rtol=1e-3, atol=0)
+    for st in stages:
+        for k, l in enumerate(st.layers):
+            w, bb, _, _ = st.get_weights(k)
+            assert weight_rel_err(w, ref.weights[l]) <= 5e-3, l
+            assert layer_rel_err(w, bb, ref.weights[l], ref.biases[l]) <= 5e-3, l
+
+
+@pytest.mark.timeout(900)
+def test_c5_bench_config_first_step(gpu_lib):
+    dims = [4096] * 17 + [10]
+    bounds = [0, 17]
+    args = (dims, bounds, 32, 64, 1, ost.I_VARIANT, ost.EQ1, 0.05, 0.01, 0.9)
+    ref = run_oracle(*args, kind=synthgen.X_SIGNED)
+    stages, losses = run_gpu(*args, kind=synthgen.X_SIGNED, init="synthetic", fuse_update=0)
+    check(stages, losses, ref)
+
+
+@pytest.mark.timeout(900)
+@pytest.mark.parametrize("blend", [ost.EQ1, ost.CONVEX])
+def test_c2_four_stage_staleness_sweep(gpu_lib, blend):
+    dims = [4096] * 9 + [10]
+    bounds = [0, 2, 4, 6, 9]
+    args = (dims, bounds, 8, 64, 6, ost.I_VARIANT, blend, 0.05, 0.01, 0.9)
+    ref = run_oracle(*args, kind=synthgen.X_SIGNED)
+    stages, losses = run_gpu(*args, kind=synthgen.X_SIGNED, init="synthetic", fuse_update=0)
+    check(stages, losses, ref)
+    deltas = sorted({(e.stage, e.delta) for st in stages for e in st.trace() if e.kind == 1})
+    assert max(d for s, d in deltas if s == 0) == 3 and max(d for s, d in deltas if s == 3) == 0
