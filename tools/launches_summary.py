@@ -13,6 +13,23 @@ LABEL = {"gemm_kernel<256, 0, 0, 0>": "gemm fwd (BN=256)", "gemm_kernel<256, 0, 
 UNIT = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}
 
 
+def family(name):
+    """gemm_kernel<BN, A_MN, B_MN, BLEND, SGD, CG, CONV> -> readable label; other kernels by prefix."""
+    import re
+    m = re.search(r"gemm_kernel<\s*(\d+),\s*(\d),\s*(\d),\s*(\d),\s*(\d),\s*(\d),\s*(\d)>", name.replace("(int)", ""))
+    if m:
+        bn, amn, bmn, blend, sgd, cg, conv = (int(x) for x in m.groups())
+        kind = {(0, 0): "fwd", (0, 1): "dgrad", (1, 1): "wgrad"}[(amn, bmn)]
+        if conv:
+            kind = "conv " + kind
+        if blend:
+            kind += " blend-on-load"
+        if sgd:
+            kind += "+update"
+        return f"gemm {kind} (BN={bn}, {'CTA pair' if cg == 2 else '1 CTA'})"
+    return next((f for f in FAMILIES if f in name), name[:50])
+
+
 def main(path, out, src):
     rows = list(csv.reader(open(path)))
     hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
@@ -22,8 +39,7 @@ def main(path, out, src):
     for r in rows[hi + 1:]:
         if len(r) <= vi:
             continue
-        name = next((f for f in FAMILIES if f in r[ki]), r[ki][:50])
-        name = LABEL.get(name, name)
+        name = family(r[ki])
         agg[name][0] += 1
         agg[name][1] += float(r[vi].replace(",", "")) * UNIT.get(r[ui], 1.0)
     tot = sum(v[1] for v in agg.values())
