@@ -47,7 +47,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-v", action="store_true")
     ap.add_argument("--fwd-group", type=int, default=0)
-    ap.add_argument("--fuse-update", type=int, default=0, help="1: SGD update in the wgrad epilogue")
+    ap.add_argument("--fuse-update", type=int, default=1, help="1: SGD update in the wgrad epilogue (TMA-fed)")
     return ap.parse_args()
 
 

@@ -40,18 +40,29 @@ constexpr int BK = 64;                     // 64 bf16 = 128 B = one swizzle atom
 constexpr int A_BYTES = BM * BK * 2;       // 16 KiB
 constexpr int SMEM_BUDGET = 227 * 1024;
 constexpr int EPI_WARPS = 8;
-constexpr int EPI_SMEM = EPI_WARPS * 32 * 33 * 4;   // per-warp 32x33 fp32 transpose buffer
+// fused-update epilogue: 4 warps, each with SGD_NB buffers of one 32x32 chunk of w, v (fp32,
+// 128B-swizzled TMA boxes) and the new bf16 version (64B-swizzled), refilled SGD_NB-1 chunks ahead
+constexpr int SGD_WARPS = 4;
+#ifndef TPS_SGD_NB
+#define TPS_SGD_NB 2
+#endif
+constexpr int SGD_NB = TPS_SGD_NB;
+constexpr int SGD_BUF = 32 * 32 * 4 * 2 + 32 * 32 * 2;   // 10 KiB
 
 template <int BN, int BLEND, int SGD = 0, int CG = 1>
 struct Cfg {
-  static constexpr int EPI = SGD ? EPI_SMEM : 0;   // transpose buffer only for the fused update
+  static constexpr int NEPI = SGD ? SGD_WARPS : EPI_WARPS;            // epilogue warps
+  static constexpr int EPI = SGD ? SGD_WARPS * SGD_NB * SGD_BUF : 0;  // fused-update buffers
   static constexpr int B_BYTES = (BN / CG) * BK * 2;   // this CTA's share of the B tile
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES * (BLEND ? 3 : 1);
   static constexpr int STAGES_RAW = (SMEM_BUDGET - 2048 - EPI) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
-  static constexpr int THREADS = 32 * (2 + EPI_WARPS + (BLEND ? 4 : 0));
-  static constexpr int TMEM_COLS = 2 * BN;
-  static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + EPI + 256;
+  static constexpr int THREADS = 32 * (2 + NEPI + (BLEND ? 4 : 0));
+  // accumulator stages in TMEM: the fused-update variant keeps up to 4 so the MMAs can run
+  // several tiles ahead of its HBM-bound epilogue
+  static constexpr int ACC = (SGD && 512 / BN >= 4) ? 4 : 2;
+  static constexpr int TMEM_COLS = ACC * BN;
+  static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + 1024 + EPI;   // ring | barriers | epilogue
   // bytes the leader's full barrier waits for per stage (both CTAs of a pair land on it)
   static constexpr uint32_t TX = (A_BYTES + B_BYTES * (BLEND ? 2 : 1)) * CG;
 };
@@ -77,7 +88,8 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 template <int BN, int A_MN, int B_MN, int BLEND, int SGD, int CG, int CONV>
 __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                const __grid_constant__ CUtensorMap tmB2, const GemmArgs args) {
+                const __grid_constant__ CUtensorMap tmB2, const __grid_constant__ CUtensorMap tmW,
+                const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmQ, const GemmArgs args) {
   // CG = 2: a cluster of two CTAs on one TPC computes a 256 x BN tile with one
   // tcgen05.mma.cta_group::2 stream issued by the leader; each CTA stages its own 128 rows
   // of A and half of the B tile, so per-SM operand traffic drops by a third.
@@ -90,9 +102,10 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
   uint64_t* empty = full + C::STAGES;
   uint64_t* xform = empty + C::STAGES;
   uint64_t* tmem_full = xform + C::STAGES;
-  uint64_t* tmem_empty = tmem_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
-  float* epi_stage = reinterpret_cast<float*>(smem + C::STAGES * C::STAGE_BYTES + 256);
+  uint64_t* tmem_empty = tmem_full + C::ACC;
+  uint64_t* sgd_bar = tmem_empty + C::ACC;                                  // SGD_WARPS * SGD_NB
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sgd_bar + SGD_WARPS * SGD_NB);
+  uint8_t* epi_smem = smem + C::STAGES * C::STAGE_BYTES + 1024;       // 1 KiB aligned
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -112,10 +125,12 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
       ptx::mbar_init(&empty[s], 1);
       ptx::mbar_init(&xform[s], 128);
     }
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < C::ACC; ++a) {
       ptx::mbar_init(&tmem_full[a], 1);
-      ptx::mbar_init(&tmem_empty[a], EPI_WARPS * CG);
+      ptx::mbar_init(&tmem_empty[a], C::NEPI * CG);
     }
+    if (SGD)
+      for (int i = 0; i < SGD_WARPS * SGD_NB; ++i) ptx::mbar_init(&sgd_bar[i], 1);
     ptx::fence_barrier_init();
   }
   if (warp == 1) {
@@ -215,8 +230,8 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
       uint32_t phase = 0;
       int it = 0;
       for (int t = cid; t < num_tiles; t += ncl, ++it) {
-        const int acc = it & 1;
-        const uint32_t acc_phase = (it >> 1) & 1;
+        const int acc = it % C::ACC;
+        const uint32_t acc_phase = (it / C::ACC) & 1;
         ptx::mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
@@ -245,39 +260,118 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
         else ptx::umma_commit(&tmem_full[acc]);
       }
     }
-  } else if (warp < 2 + EPI_WARPS) {
+  } else if (SGD && warp < 2 + SGD_WARPS) {
+    // ===================== fused SGD/momentum update epilogue (row a10) =====================
+    // Each warp owns TMEM lane quarter q (32 rows of the CTA's 128) and walks the tile's 32-column
+    // chunks.  w and v of a chunk arrive by TMA (128B-swizzled 32x32 fp32 boxes) SGD_NB-1 chunks
+    // ahead; thread = row updates its row in place (g' = g + wd·w; v = μ·v + g'; w = w - lr·v),
+    // writes bf16(w) into a 64B-swizzled box, and TMA stores write w, v, bf16(w) back.  No dW
+    // round trip and no register-bound load latency.
+    const int e = warp - 2;
+    const int q = warp & 3;
+    uint8_t* ebase = epi_smem + e * (SGD_NB * SGD_BUF);
+    uint64_t* ebar = sgd_bar + e * SGD_NB;
+    constexpr int NCH = BN / 32;
+    const bool mom = args.mu != 0.0f;
+    auto issue = [&](int i) {            // lane 0: TMA loads of chunk i into buffer i % SGD_NB
+      const int ti = i / NCH, c = i - ti * NCH;
+      const int t = cid + ti * ncl;
+      if (t >= num_tiles) return;
+      int mb, nb;
+      tile_coords(t, num_m, num_n, mb, nb);
+      const int row0 = mb * BM * CG + static_cast<int>(rank) * BM + q * 32;
+      const int col0 = nb * BN + c * 32;
+      const int buf = i % SGD_NB;
+      uint8_t* w_s = ebase + buf * SGD_BUF;
+      ptx::mbar_expect_tx(&ebar[buf], mom ? 8192u : 4096u);
+      ptx::tma_load_2d(w_s, &tmW, &ebar[buf], col0, row0);
+      if (mom) ptx::tma_load_2d(w_s + 4096, &tmV, &ebar[buf], col0, row0);
+    };
+    if (lane == 0)
+      for (int i = 0; i < SGD_NB; ++i) issue(i);
+    int i = 0, it = 0;
+    for (int t = cid; t < num_tiles; t += ncl, ++it) {
+      int mb, nb;
+      tile_coords(t, num_m, num_n, mb, nb);
+      const int acc = it % C::ACC;
+      const uint32_t acc_phase = (it / C::ACC) & 1;
+      ptx::mbar_wait(&tmem_full[acc], acc_phase);
+      ptx::tc_fence_after();
+      const int row0 = mb * BM * CG + static_cast<int>(rank) * BM + q * 32;
+#pragma unroll 1
+      for (int c = 0; c < NCH; ++c, ++i) {
+        uint32_t r[32];
+        ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c * 32, r);
+        ptx::tmem_ld_wait();
+        if (c == NCH - 1) {
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            if (CG == 2) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&tmem_empty[acc]), 0));
+            else ptx::mbar_arrive(&tmem_empty[acc]);
+          }
+        }
+        const int buf = i % SGD_NB;
+        ptx::mbar_wait(&ebar[buf], (i / SGD_NB) & 1);
+        uint8_t* w_s = ebase + buf * SGD_BUF;
+        float4* wrow = reinterpret_cast<float4*>(w_s + lane * 128);
+        float4* vrow = reinterpret_cast<float4*>(w_s + 4096 + lane * 128);
+        uint8_t* qrow = w_s + 8192 + lane * 64;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int pos = j ^ (lane & 7);                 // 128B swizzle: 16B chunk j of row `lane`
+          float4 wv = wrow[pos];
+          float4 vv = mom ? vrow[pos] : make_float4(0.f, 0.f, 0.f, 0.f);
+          float* wp = &wv.x;
+          float* vp = &vv.x;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const float g = __uint_as_float(r[4 * j + k]);
+            const float gp = __fadd_rn(g, __fmul_rn(args.wd, wp[k]));
+            float upd = gp;
+            if (mom) {
+              vp[k] = __fadd_rn(__fmul_rn(args.mu, vp[k]), gp);
+              upd = vp[k];
+            }
+            wp[k] = __fsub_rn(wp[k], __fmul_rn(args.lr, upd));
+          }
+          wrow[pos] = wv;
+          if (mom) vrow[pos] = vv;
+          const int qpos = (j >> 1) ^ ((lane >> 1) & 3);  // 64B swizzle of the bf16 row
+          *reinterpret_cast<uint2*>(qrow + qpos * 16 + (j & 1) * 8) =
+              make_uint2(pack_bf16(wv.x, wv.y), pack_bf16(wv.z, wv.w));
+        }
+        ptx::fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          const int col0 = nb * BN + c * 32;
+          ptx::tma_store_2d(&tmW, w_s, col0, row0);
+          if (mom) ptx::tma_store_2d(&tmV, w_s + 4096, col0, row0);
+          ptx::tma_store_2d(&tmQ, w_s + 8192, col0, row0);
+          ptx::bulk_commit();
+          ptx::bulk_wait_read<0>();       // the buffer may be refilled once the stores read it
+          issue(i + SGD_NB);
+        }
+        __syncwarp();
+      }
+    }
+    if (lane == 0) ptx::bulk_wait_all();
+  } else if (!SGD && warp < 2 + EPI_WARPS) {
     // ===================== epilogue =====================
-    // 8 warps: warp w reads TMEM lane quarter (w % 4) and handles every other 32-column chunk.
+    // 8 warps: warp w reads TMEM lane quarter (w % 4) and handles one half of the tile's
+    // 32-column chunks; thread = row, 16-byte vector loads/stores along the row.
     const int e = warp - 2;
     const int q = warp & 3;                 // TMEM lane quarter this warp may access
     const int half = e >> 2;                // which half of the tile's columns this warp owns
     constexpr int CPW = BN / 64;            // 32-column chunks per warp per tile
-    float* stg = epi_stage + e * (32 * 33);
-    // SGD: pull this warp's rows of w and v for tile `tt` into L2 ahead of its epilogue
-    // (one bulk prefetch per row and array, issued while the tensor cores are still busy)
-    auto prefetch_state = [&](int tt) {
-      if (!SGD || tt >= num_tiles) return;
-      int pmb, pnb;
-      tile_coords(tt, num_m, num_n, pmb, pnb);
-      const int prow = pmb * BM * CG + static_cast<int>(rank) * BM + q * 32 + lane;
-      const int pcol = pnb * BN + half * (BN / 2);
-      if (prow < args.M && pcol < args.N) {
-        const uint32_t bytes = static_cast<uint32_t>(min(BN / 2, args.N - pcol)) * 4u;
-        const size_t off = static_cast<size_t>(prow) * args.ldo + pcol;
-        ptx::bulk_prefetch_l2(args.w + off, bytes);
-        if (args.mu != 0.0f) ptx::bulk_prefetch_l2(args.v + off, bytes);
-      }
-    };
-    prefetch_state(cid);
     int it = 0;
     for (int t = cid; t < num_tiles; t += ncl, ++it) {
       int mb, nb;
       tile_coords(t, num_m, num_n, mb, nb);
-      const int acc = it & 1;
-      const uint32_t acc_phase = (it >> 1) & 1;
+      const int acc = it % C::ACC;
+      const uint32_t acc_phase = (it / C::ACC) & 1;
       ptx::mbar_wait(&tmem_full[acc], acc_phase);
       ptx::tc_fence_after();
-      prefetch_state(t + ncl);
       const int row0 = mb * BM * CG + static_cast<int>(rank) * BM + q * 32;
 #pragma unroll 1
       for (int ci = 0; ci < CPW; ++ci) {
@@ -292,44 +386,6 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
             if (CG == 2) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&tmem_empty[acc]), 0));
             else ptx::mbar_arrive(&tmem_empty[acc]);
           }
-        }
-        if (SGD) {
-          // fused update (row a10), staged through smem so lane = column and every access is a
-          // coalesced 128-byte row segment:  g' = g + wd·w ; v = μ·v + g' ; w = w - lr·v ; bf16(w)
-#pragma unroll
-          for (int i = 0; i < 32; ++i) stg[lane * 33 + i] = __uint_as_float(r[i]);
-          __syncwarp();
-          const int gcol = nb * BN + c * 32 + lane;
-          const bool col_ok = gcol < args.N;
-          const int rows = min(32, args.M - row0);
-#pragma unroll 1
-          for (int r0 = 0; r0 < rows; r0 += 16) {
-            float wv[16], vv[16];
-#pragma unroll
-            for (int k = 0; k < 16; ++k) {
-              const size_t off = static_cast<size_t>(row0 + r0 + k) * args.ldo + gcol;
-              const bool ok = col_ok && (r0 + k) < rows;
-              wv[k] = ok ? args.w[off] : 0.0f;
-              vv[k] = (ok && args.mu != 0.0f) ? args.v[off] : 0.0f;
-            }
-#pragma unroll
-            for (int k = 0; k < 16; ++k) {
-              if (!col_ok || (r0 + k) >= rows) continue;
-              const size_t off = static_cast<size_t>(row0 + r0 + k) * args.ldo + gcol;
-              const float g = stg[(r0 + k) * 33 + lane];
-              const float gp = __fadd_rn(g, __fmul_rn(args.wd, wv[k]));
-              float upd = gp;
-              if (args.mu != 0.0f) {
-                upd = __fadd_rn(__fmul_rn(args.mu, vv[k]), gp);
-                args.v[off] = upd;
-              }
-              const float wn = __fsub_rn(wv[k], __fmul_rn(args.lr, upd));
-              args.w[off] = wn;
-              reinterpret_cast<__nv_bfloat16*>(args.ver)[off] = __float2bfloat16_rn(wn);
-            }
-          }
-          __syncwarp();
-          continue;
         }
         // plain epilogue: thread = row, 16-byte vector loads/stores along the row
         const int grow = row0 + lane;
@@ -409,7 +465,7 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
     }
   } else if (BLEND) {
     // ===================== operand transform: W_res = α·W_stash + β·W_latest =====================
-    const int tt = threadIdx.x - (2 + EPI_WARPS) * 32;    // 0..127
+    const int tt = threadIdx.x - (2 + C::NEPI) * 32;    // 0..127
     const float xa = args.xa, xb = args.xb;
     int stage = 0;
     uint32_t phase = 0;
@@ -486,6 +542,20 @@ bool make_tmap(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, u
   return r == CUDA_SUCCESS;
 }
 
+// 2-D tensor of any element type with an explicit box and swizzle (fused-update epilogue boxes)
+bool make_tmap_box(CUtensorMap* m, const void* base, CUtensorMapDataType dt, uint32_t esize, uint64_t rows,
+                   uint64_t cols, uint64_t ld, uint32_t box_cols, uint32_t box_rows, CUtensorMapSwizzle sw) {
+  EncodeTiledFn enc = get_encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {ld * esize};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(m, dt, 2, const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 // 4-D bf16 NHWC-style tensor: dims {d0 (contiguous), d1, d2, d3}, box {64, b1, b2, b3}, 128B swizzle.
 bool make_tmap4(CUtensorMap* m, const void* base, const uint64_t (&d)[4], const uint32_t (&box)[4]) {
   EncodeTiledFn enc = get_encode_fn();
@@ -526,9 +596,13 @@ int num_sms() {
   return n;
 }
 
+struct EpiMaps {
+  CUtensorMap w, v, q;   // fused update: fp32 master, fp32 momentum, bf16 version (32x32 boxes)
+};
+
 template <int BN, int A_MN, int B_MN, int BLEND, int SGD = 0, int CG = 1, int CONV = CONV_NONE>
-cudaError_t launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& b2, const GemmArgs& args,
-                   cudaStream_t st) {
+cudaError_t launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& b2, const EpiMaps& em,
+                   const GemmArgs& args, cudaStream_t st) {
   using C = Cfg<BN, BLEND, SGD, CG>;
   auto kern = gemm_kernel<BN, A_MN, B_MN, BLEND, SGD, CG, CONV>;
   static bool attr_set = false;   // per instantiation
@@ -551,7 +625,7 @@ cudaError_t launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a, b, b2, args);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a, b, b2, em.w, em.v, em.q, args);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
@@ -587,20 +661,19 @@ Tiling pick_tiling(int M, int N, int mode, bool sgd) {
     const int tiles = tm * ((N + bn - 1) / bn);
     if (tiles >= (sms * 3) / 4 || bn == 64) return {1, bn};
   }
-  (void)sgd;
   return {1, 64};
 }
 
 template <int A_MN, int B_MN, int SGD, int CONV = CONV_NONE>
 cudaError_t dispatch(const Tiling& tl, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tb2,
-                     const GemmArgs& args, cudaStream_t st) {
+                     const EpiMaps& em, const GemmArgs& args, cudaStream_t st) {
   if (tl.cg == 2) {
-    if (tl.bn == 256) return launch<256, A_MN, B_MN, 0, SGD, 2, CONV>(ta, tb, tb2, args, st);
-    return launch<128, A_MN, B_MN, 0, SGD, 2, CONV>(ta, tb, tb2, args, st);
+    if (tl.bn == 256) return launch<256, A_MN, B_MN, 0, SGD, 2, CONV>(ta, tb, tb2, em, args, st);
+    return launch<128, A_MN, B_MN, 0, SGD, 2, CONV>(ta, tb, tb2, em, args, st);
   }
-  if (tl.bn == 256) return launch<256, A_MN, B_MN, 0, SGD, 1, CONV>(ta, tb, tb2, args, st);
-  if (tl.bn == 128) return launch<128, A_MN, B_MN, 0, SGD, 1, CONV>(ta, tb, tb2, args, st);
-  return launch<64, A_MN, B_MN, 0, SGD, 1, CONV>(ta, tb, tb2, args, st);
+  if (tl.bn == 256) return launch<256, A_MN, B_MN, 0, SGD, 1, CONV>(ta, tb, tb2, em, args, st);
+  if (tl.bn == 128) return launch<128, A_MN, B_MN, 0, SGD, 1, CONV>(ta, tb, tb2, em, args, st);
+  return launch<64, A_MN, B_MN, 0, SGD, 1, CONV>(ta, tb, tb2, em, args, st);
 }
 
 }  // namespace
@@ -663,21 +736,32 @@ cudaError_t gemm_run(int mode, const GemmOperands& op, const GemmArgs& args_in, 
     if (mode == GEMM_DGRAD_BLEND) ok &= make_tmap(&tb2, op.B2, args.K, args.N, op.ldb, 64);
     else tb2 = tb;
   }
+  EpiMaps em;
+  em.w = em.v = em.q = ta;   // unused unless sgd
+  if (sgd) {
+    ok &= make_tmap_box(&em.w, args.w, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, args.M, args.N, args.ldo, 32, 32,
+                        CU_TENSOR_MAP_SWIZZLE_128B);
+    if (args.mu != 0.0f)
+      ok &= make_tmap_box(&em.v, args.v, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, args.M, args.N, args.ldo, 32, 32,
+                          CU_TENSOR_MAP_SWIZZLE_128B);
+    ok &= make_tmap_box(&em.q, args.ver, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, args.M, args.N, args.ldo, 32, 32,
+                        CU_TENSOR_MAP_SWIZZLE_64B);
+  }
   if (!ok) return cudaErrorInvalidValue;
   if (bn_out) *bn_out = tl.bn * 10 + tl.cg;
   switch (mode) {
-    case GEMM_FWD: return dispatch<0, 0, 0>(tl, ta, tb, tb2, args, st);
-    case GEMM_DGRAD: return dispatch<0, 1, 0>(tl, ta, tb, tb2, args, st);
+    case GEMM_FWD: return dispatch<0, 0, 0>(tl, ta, tb, tb2, em, args, st);
+    case GEMM_DGRAD: return dispatch<0, 1, 0>(tl, ta, tb, tb2, em, args, st);
     case GEMM_WGRAD:
-      if (sgd) return dispatch<1, 1, 1>(tl, ta, tb, tb2, args, st);
-      return dispatch<1, 1, 0>(tl, ta, tb, tb2, args, st);
-    case GEMM_DGRAD_BLEND: return launch<128, 0, 1, 1, 0, 1>(ta, tb, tb2, args, st);
-    case GEMM_CONV_FWD: return dispatch<0, 0, 0, CONV_FWD>(tl, ta, tb, tb2, args, st);
-    case GEMM_CONV_DGRAD: return dispatch<0, 1, 0, CONV_DGRAD>(tl, ta, tb, tb2, args, st);
-    case GEMM_CONV_DGRAD_BLEND: return launch<128, 0, 1, 1, 0, 1, CONV_DGRAD>(ta, tb, tb2, args, st);
+      if (sgd) return dispatch<1, 1, 1>(tl, ta, tb, tb2, em, args, st);
+      return dispatch<1, 1, 0>(tl, ta, tb, tb2, em, args, st);
+    case GEMM_DGRAD_BLEND: return launch<128, 0, 1, 1, 0, 1>(ta, tb, tb2, em, args, st);
+    case GEMM_CONV_FWD: return dispatch<0, 0, 0, CONV_FWD>(tl, ta, tb, tb2, em, args, st);
+    case GEMM_CONV_DGRAD: return dispatch<0, 1, 0, CONV_DGRAD>(tl, ta, tb, tb2, em, args, st);
+    case GEMM_CONV_DGRAD_BLEND: return launch<128, 0, 1, 1, 0, 1, CONV_DGRAD>(ta, tb, tb2, em, args, st);
     case GEMM_CONV_WGRAD:
-      if (sgd) return dispatch<1, 1, 1, CONV_WGRAD>(tl, ta, tb, tb2, args, st);
-      return dispatch<1, 1, 0, CONV_WGRAD>(tl, ta, tb, tb2, args, st);
+      if (sgd) return dispatch<1, 1, 1, CONV_WGRAD>(tl, ta, tb, tb2, em, args, st);
+      return dispatch<1, 1, 0, CONV_WGRAD>(tl, ta, tb, tb2, em, args, st);
   }
   return cudaErrorInvalidValue;
 }

@@ -12,7 +12,7 @@ import os
 from dataclasses import dataclass, field
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libtps.so")
+LIB_PATH = os.environ.get("TPS_LIB") or os.path.join(HERE, "lib", "libtps.so")
 
 TPS_V, TPS_I = 0, 1
 TPS_BLEND_EQ1, TPS_BLEND_CONVEX = 0, 1
