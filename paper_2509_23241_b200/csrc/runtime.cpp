@@ -1229,7 +1229,8 @@ tps_status tps_init_weights_synthetic(tps_pipeline* p) {
   TPS_TRY(check_usable(p));
   for (auto& L : p->layers) {
     if (!L.has_w()) continue;
-    const int shift = static_cast<int>(std::lround(std::log2(std::sqrt(static_cast<double>(L.in)))));
+    // round half to even, like synthgen (Python round): fan_in = 512 -> log2(sqrt) = 4.5 -> 4
+    const int shift = static_cast<int>(std::nearbyint(std::log2(std::sqrt(static_cast<double>(L.in)))));
     CUDA_OK(cudaMemsetAsync(L.W, 0, static_cast<size_t>(L.Np) * L.Kp * 4, p->cs));
     CUDA_OK(tps::launch_fill_synthetic(3, p->seed, 0x0100 + static_cast<uint64_t>(L.gidx), L.out, L.in, L.Kp, 0, shift,
                                        L.W, p->cs));

@@ -48,3 +48,40 @@ def test_c2_four_stage_staleness_sweep(gpu_lib, blend):
     check(stages, losses, ref)
     deltas = sorted({(e.stage, e.delta) for st in stages for e in st.trace() if e.kind == 1})
     assert max(d for s, d in deltas if s == 0) == 3 and max(d for s, d in deltas if s == 3) == 0
+
+
+def vgg16_cifar(classes=10):
+    """VGG-16 on 32x32x3 (BASELINE.json configs[2]): 13 conv3x3 + 5 max-pools + FC 512-4096-4096-classes."""
+    layers, H, C = [], 32, 3
+    for block, (width, n) in enumerate([(64, 2), (128, 2), (256, 3), (512, 3), (512, 3)]):
+        for _ in range(n):
+            layers.append({"kind": "conv3", "cin": C, "cout": width, "h": H, "w": H})
+            C = width
+        layers.append({"kind": "pool2", "c": C, "h": H, "w": H})
+        H //= 2
+    layers += [{"kind": "linear", "in": 512, "out": 4096}, {"kind": "linear", "in": 4096, "out": 4096},
+               {"kind": "linear", "in": 4096, "out": classes}]
+    return layers
+
+
+# stage partition by conv block (SURVEY §8(d) C3): [c1,c2 + pools] [c3 + pool] [c4 + pool] [c5 + pool + FCs]
+VGG_BOUNDS = [0, 6, 10, 14, 21]
+
+
+@pytest.mark.timeout(900)
+def test_c3_vgg16_four_stage(gpu_lib):
+    layers = vgg16_cifar()
+    dims = [32 * 32 * 3, 10]
+    args = (dims, VGG_BOUNDS, 2, 64, 4, ost.I_VARIANT, ost.EQ1, 0.05, 0.01, 0.9)
+    ref = run_oracle(*args, kind=synthgen.X_UNIT, layers=layers)
+    stages, losses = run_gpu(*args, kind=synthgen.X_UNIT, init="synthetic", layers=layers)
+    assert expand_gpu_trace(stages) == oracle_trace(ref)
+    np.testing.assert_allclose(losses, ref.losses, rtol=1e-3, atol=0)
+    for st in stages:
+        for k, l in enumerate(st.layers):
+            if ref.weights[l] is None:
+                continue
+            w, bb, _, _ = st.get_weights(k)
+            wr = ref.weights[l].reshape(w.shape)
+            assert weight_rel_err(w, wr) <= 5e-3, l
+            assert layer_rel_err(w, bb, wr, ref.biases[l]) <= 5e-3, l

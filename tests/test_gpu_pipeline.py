@@ -93,10 +93,12 @@ def test_i_eq1_freeze_at_ln2_on_gpu(gpu_lib):
     assert alphas == [1.0] + [0.0] * 5
 
 
-def test_device_init_matches_synthgen(gpu_lib):
-    dims, bounds = [200, 136, 10], [0, 2]
+@pytest.mark.parametrize("dims", [[200, 136, 10], [512, 2048, 32, 16], [128, 8, 16]])
+def test_device_init_matches_synthgen(gpu_lib, dims):
+    # fan_in 512 / 2048 / 8 put log2(sqrt(fan_in)) exactly on a .5 tie (rounded to even)
+    bounds = [0, len(dims) - 1]
     st, _ = run_gpu(dims, bounds, 2, 8, 0 + 1, ost.V_VARIANT, ost.EQ1, 0.05, 0.0, 0.0, init="synthetic", seed=3)
-    for k in range(2):
+    for k in range(len(dims) - 1):
         w = st[0].get_weights(k)[0]
         np.testing.assert_array_equal(w, synthgen.weights(3, k, dims[k + 1], dims[k]))
 
