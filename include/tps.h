@@ -265,6 +265,21 @@ tps_status tps_gemm(int32_t mode, int32_t M, int32_t N, int32_t K,
                     void* out, int32_t ldo, int32_t out_f32, const float* bias, int32_t relu,
                     float alpha, float beta, const void* mask, int32_t ldm, uint64_t stream);
 
+/* ---- stage partitioner ("distribute the DNNs ... in such a way
+ * that a balance is maintained between the memory consumptions in each node") ----------
+ * Splits L layers into S consecutive non-empty stages minimising the largest per-stage
+ * cost (exact dynamic programme).  Per layer (host arrays): param_bytes = bytes of one copy
+ * of its parameters' fp32 master, act_bytes = bytes of its stashed input for one mini-batch,
+ * flops = its training FLOPs per mini-batch.  objective 0 = memory, 1 = time (flops).
+ * Memory of stage s (0-based) holding layers P:
+ *   Σ_P param_bytes·(1 + momentum + 0.5·R_s) + K_s·Σ_P act_bytes,  K_s = S - s,
+ *   R_s = K_s for I-TiMePReSt (the bf16 version ring) and 1 for V,
+ *   momentum = 1 if mu != 0 (fp32 momentum) else 0.
+ * bounds_out: S+1 entries; stage_cost_out: S entries (may be NULL).                       */
+tps_status tps_partition(int32_t num_layers, const double* param_bytes, const double* act_bytes,
+                         const double* flops, int32_t num_stages, int32_t variant, int32_t momentum,
+                         int32_t objective, int32_t* bounds_out, double* stage_cost_out);
+
 /* ---- raw 3x3 convolution GEMMs (implicit im2col via 4-D TMA; unit tests) ----
  * NHWC bf16 device tensors, stride 1, padding 1, Ci % 64 == 0, Co % 64 == 0.
  * mode 0 (forward): out[N·H·W, Co] = conv(X[N,H,W,Ci]; W[Co,3,3,Ci]) + bias, ReLU if relu.

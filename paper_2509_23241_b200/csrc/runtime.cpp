@@ -1318,6 +1318,51 @@ tps_status tps_fill_synthetic(int32_t kind, uint64_t seed, uint64_t tid, int64_t
   return TPS_OK;
 }
 
+tps_status tps_partition(int32_t L, const double* pb, const double* ab, const double* fl, int32_t S, int32_t variant,
+                         int32_t momentum, int32_t objective, int32_t* bounds, double* cost_out) {
+  if (L < 1 || S < 1 || S > L || !bounds) return fail(TPS_E_INVALID_ARG, "need 1 <= S <= L and an output array");
+  if (objective == 0 && (!pb || !ab)) return fail(TPS_E_INVALID_ARG, "memory objective needs param/act bytes");
+  if (objective == 1 && !fl) return fail(TPS_E_INVALID_ARG, "time objective needs flops");
+  if (objective != 0 && objective != 1) return fail(TPS_E_INVALID_ARG, "bad objective");
+  // cost(s, i, j): cost of stage s holding layers [i, j)
+  std::vector<double> P(L + 1, 0.0), A(L + 1, 0.0), F(L + 1, 0.0);
+  for (int l = 0; l < L; ++l) {
+    P[l + 1] = P[l] + (pb ? pb[l] : 0.0);
+    A[l + 1] = A[l] + (ab ? ab[l] : 0.0);
+    F[l + 1] = F[l] + (fl ? fl[l] : 0.0);
+  }
+  auto cost = [&](int s, int i, int j) {
+    if (objective == 1) return F[j] - F[i];
+    const double K = static_cast<double>(S - s);
+    const double R = variant == TPS_I ? K : 1.0;
+    return (P[j] - P[i]) * (1.0 + (momentum ? 1.0 : 0.0) + 0.5 * R) + K * (A[j] - A[i]);
+  };
+  const double INF = 1e300;
+  // best[s][j]: minimal max-cost of placing layers [0, j) on stages 0..s-1
+  std::vector<std::vector<double>> best(S + 1, std::vector<double>(L + 1, INF));
+  std::vector<std::vector<int>> arg(S + 1, std::vector<int>(L + 1, -1));
+  best[0][0] = 0.0;
+  for (int s = 1; s <= S; ++s)
+    for (int j = s; j <= L - (S - s); ++j)
+      for (int i = s - 1; i < j; ++i) {
+        if (best[s - 1][i] >= INF) continue;
+        const double c = std::max(best[s - 1][i], cost(s - 1, i, j));
+        if (c < best[s][j]) {
+          best[s][j] = c;
+          arg[s][j] = i;
+        }
+      }
+  int j = L;
+  bounds[S] = L;
+  for (int s = S; s >= 1; --s) {
+    const int i = arg[s][j];
+    bounds[s - 1] = i;
+    if (cost_out) cost_out[s - 1] = cost(s - 1, i, j);
+    j = i;
+  }
+  return TPS_OK;
+}
+
 tps_status tps_conv_gemm(int32_t mode, int32_t N, int32_t H, int32_t W, int32_t Ci, int32_t Co, const void* A,
                          const void* Wt, const void* W2, void* out, int32_t out_f32, const float* bias, int32_t relu,
                          float alpha, float beta, const void* mask, uint64_t stream) {

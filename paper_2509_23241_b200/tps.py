@@ -31,7 +31,7 @@ EXPORTS = [
     "tps_intermediate_weight", "tps_get_version", "tps_schedule_events", "tps_get_weights", "tps_set_weights",
     "tps_init_weights_synthetic", "tps_get_losses", "tps_get_trace", "tps_clear_trace", "tps_memory_stats",
     "tps_set_profiling", "tps_kernel_stats", "tps_launch_count", "tps_fill_synthetic", "tps_gemm",
-    "tps_conv_gemm",
+    "tps_conv_gemm", "tps_partition",
 ]
 TPS_LAYER_LINEAR, TPS_LAYER_CONV3X3, TPS_LAYER_MAXPOOL2 = 0, 1, 2
 
@@ -107,6 +107,7 @@ def lib() -> C.CDLL:
             "tps_fill_synthetic": (I32, [I32, U64, U64, I64, I64, I32, P, U64]),
             "tps_gemm": (I32, [I32, I32, I32, I32, P, I32, P, I32, P, P, I32, I32, P, I32, F, F, P, I32, U64]),
             "tps_conv_gemm": (I32, [I32, I32, I32, I32, I32, I32, P, P, P, P, I32, P, I32, F, F, P, U64]),
+            "tps_partition": (I32, [I32, P, P, P, I32, I32, I32, I32, P, P]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -165,6 +166,19 @@ def conv_gemm(mode, N, H, W, Ci, Co, A, Wt, out, out_f32=0, bias=None, relu=0, a
               W2=None, stream: int = 0) -> None:
     check(lib().tps_conv_gemm(mode, N, H, W, Ci, Co, ptr(A), ptr(Wt), ptr(W2), ptr(out), out_f32, ptr(bias), relu,
                               alpha, beta, ptr(mask), stream))
+
+
+def partition(param_bytes, act_bytes, flops, S: int, variant: int = TPS_I, momentum: bool = True,
+              objective: int = 0):
+    """Balanced consecutive stage partition (C++ DP in libtps); returns (bounds, stage costs)."""
+    import numpy as np
+    L = len(param_bytes if param_bytes is not None else flops)
+    arrs = [None if a is None else np.ascontiguousarray(a, dtype=np.float64) for a in (param_bytes, act_bytes, flops)]
+    bounds = np.zeros(S + 1, np.int32)
+    cost = np.zeros(S, np.float64)
+    check(lib().tps_partition(L, *[None if a is None else a.ctypes.data for a in arrs], S, variant,
+                              1 if momentum else 0, objective, bounds.ctypes.data, cost.ctypes.data))
+    return bounds.tolist(), cost.tolist()
 
 
 def layer_specs(specs: list[dict]):
