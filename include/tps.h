@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define TPS_ABI_VERSION 1
+#define TPS_ABI_VERSION 2
 
 typedef enum {
   TPS_OK = 0,
@@ -83,21 +83,48 @@ typedef struct {
   float alpha, beta;
 } tps_event;
 
-/* Layer description for image networks (BASELINE.json configs[2]: VGG-16 on 32x32
- * inputs).  Activations are NHWC bf16; a sample's row is its H·W·C values.
+/* Layer description for image networks.  Activations are NHWC bf16; a sample's
+ * row is its H·W·C values.  Two families, not mixed in one network:
+ *
+ * Chain networks (BASELINE.json configs[2]: VGG-16 on 32x32 inputs), layer l reads
+ * layer l-1:
  *   LINEAR:   out_c = dims out, in_c = dims in (a conv/pool output is flattened in
  *             (h, w, c) order); followed by ReLU unless it is the last layer.
  *   CONV3X3:  stride 1, zero padding 1, in_h x in_w x in_c -> in_h x in_w x out_c,
  *             weight [out_c, 3, 3, in_c] (= [out_c, 9·in_c] rows), + bias, ReLU.
  *             in_c % 64 == 0, out_c % 64 == 0, except the network's first layer, which
  *             may have any in_c (it runs as a GEMM on explicit patches).
- *   MAXPOOL2: 2x2 / stride 2, in_c channels (no parameters).                    */
-typedef enum { TPS_LAYER_LINEAR = 0, TPS_LAYER_CONV3X3 = 1, TPS_LAYER_MAXPOOL2 = 2 } tps_layer_kind;
+ *   MAXPOOL2: 2x2 / stride 2, in_c channels (no parameters).
+ *
+ * Graph networks (configs[3]: ResNet-50 v1.5; math in oracle/resnet.py): layer l reads
+ * the output of layer l - max(1, src_back) (layer -1 = the network input; a stage may
+ * read only its own layers and the previous stage's last output), shapes are the
+ * layer's INPUT:
+ *   CONV:     k x k, stride, zero pad; no bias, no activation; weight [out_c, k, k, in_c].
+ *             out_c % 16 == 0; 1x1/stride-1 convs need in_c % 16 == 0 (plain GEMM);
+ *             3x3/stride-1/pad-1 convs with in_c, out_c % 64 == 0 gather their input
+ *             with 4-D TMA; every other conv runs on explicit patches.
+ *   BN:       batch norm over in_c channels with the statistics of each micro-batch
+ *             (reading Z22), biased variance, eps 1e-5; γ (versioned fp32, blended in
+ *             the I-TiMePReSt backward like a weight, reading Z12) and β (latest, like
+ *             a bias); then + the output of layer l - res_back if res_back > 0; then
+ *             ReLU if relu != 0.
+ *   MAXPOOL3: 3x3 / stride 2 / pad 1 max pool (gradient to the first maximum, Z15).
+ *   AVGPOOL:  global average pool in_h x in_w x in_c -> in_c.
+ *   LINEAR:   the head (last layer only): in_c % 16 == 0, + bias, no ReLU.       */
+typedef enum {
+  TPS_LAYER_LINEAR = 0, TPS_LAYER_CONV3X3 = 1, TPS_LAYER_MAXPOOL2 = 2,
+  TPS_LAYER_CONV = 3, TPS_LAYER_BN = 4, TPS_LAYER_MAXPOOL3 = 5, TPS_LAYER_AVGPOOL = 6
+} tps_layer_kind;
 typedef struct {
   int32_t kind;
   int32_t in_c, out_c;
   int32_t in_h, in_w;
-  int32_t reserved[3];
+  int32_t k, stride, pad;       /* CONV                                               */
+  int32_t src_back;             /* graph kinds: main input = layer l - max(1, src_back) */
+  int32_t res_back;             /* BN: residual = layer l - res_back; 0 = none        */
+  int32_t relu;                 /* BN: ReLU after the affine (+ residual)             */
+  int32_t reserved[5];
 } tps_layer;
 
 /* Pipeline configuration (read once by tps_pipeline_init; arrays are copied).
@@ -291,6 +318,41 @@ tps_status tps_conv_gemm(int32_t mode, int32_t N, int32_t H, int32_t W, int32_t 
                          const void* A, const void* Wt, const void* W2, void* out, int32_t out_f32,
                          const float* bias, int32_t relu, float alpha, float beta, const void* mask,
                          uint64_t stream);
+
+/* ---- ResNet op kernels (unit tests; the pipeline calls the same kernels) --------
+ * All tensors NHWC bf16 on the device unless stated; `stream` = cudaStream_t (0 = legacy).
+ * Definitions: oracle/resnet.py (textbook conv / batch norm / pooling, reading Z22).
+ *
+ * tps_im2col: P[(n,ho,wo), (kh,kw,c)] = X[n, s·ho+kh-p, s·wo+kw-p, c] (0 outside), columns
+ *   k·k·C .. ldp-1 zero; Ho = (H+2p-k)/s+1.  Bit-exact gather.
+ * tps_col2im: dX[n,h,w,c] = bf16(Σ_{kh,kw} dP[...] (+ add[n,h,w,c])), dP fp32 [N·Ho·Wo, ldp],
+ *   add bf16 may be NULL or alias dX; fp32 sum in (kh, kw) order.
+ * tps_bn_forward: per segment of seg_rows rows (one micro-batch) and channel:
+ *   mean, invstd = 1/sqrt(biased var + 1e-5) (fp64 sums, fp32 out, [segs, C]);
+ *   y = bf16(act(γ·(x-mean)·invstd + β (+ res))), act = ReLU if relu; res may be NULL.
+ * tps_bn_backward: dy' = dy ⊙ [y > 0] if relu; per segment/channel Σdy', Σdy'·x̂ (fp64);
+ *   dγ = Σ_seg Σdy'·x̂, dβ = Σ_seg Σdy' (fp32 [C]);
+ *   dx = bf16(γ_r·invstd·(dy' - Σdy'/m - x̂·Σdy'x̂/m)), γ_r = a·γ_stash + b·γ_latest (fp32);
+ *   dres = bf16(dy') when non-NULL.
+ * tps_pool_op: op 0 maxpool3 forward  out = max over the 3x3/2/1 window of a (= X);
+ *              op 1 maxpool3 backward out = dX from a = X and b = dY (first maximum, Z15);
+ *              op 2 avgpool forward   out[N, C] = mean over H·W of a;
+ *              op 3 avgpool backward  out[N,H,W,C] = b[N, C] / (H·W).
+ * Errors: TPS_E_INVALID_ARG for null/ill-sized arguments, TPS_E_ARCH off sm_100,
+ *         TPS_E_CUDA on launch failure.                                                  */
+tps_status tps_im2col(const void* X, void* P, int32_t N, int32_t H, int32_t W, int32_t C, int32_t k,
+                      int32_t stride, int32_t pad, int32_t ldp, uint64_t stream);
+tps_status tps_col2im(const float* dP, void* dX, const void* add, int32_t N, int32_t H, int32_t W, int32_t C,
+                      int32_t k, int32_t stride, int32_t pad, int32_t ldp, uint64_t stream);
+tps_status tps_bn_forward(const void* x, const void* res, void* y, const float* gamma, const float* beta,
+                          float* mean, float* invstd, int32_t segs, int32_t seg_rows, int32_t C, int32_t relu,
+                          uint64_t stream);
+tps_status tps_bn_backward(const void* dy, const void* y, const void* x, const float* mean, const float* invstd,
+                           const float* gamma_stash, const float* gamma_latest, float a, float b, int32_t segs,
+                           int32_t seg_rows, int32_t C, int32_t relu, void* dx, void* dres, float* dgamma,
+                           float* dbeta, uint64_t stream);
+tps_status tps_pool_op(int32_t op, const void* a, const void* b, void* out, int32_t N, int32_t H, int32_t W,
+                       int32_t C, uint64_t stream);
 
 #ifdef __cplusplus
 }

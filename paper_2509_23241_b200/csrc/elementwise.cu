@@ -8,6 +8,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 
@@ -337,6 +338,302 @@ __global__ void im2col3x3_kernel(const uint16_t* __restrict__ X, uint16_t* __res
   }
 }
 
+// ------------------------------------------------------------------ ResNet helpers (NHWC, bf16)
+// general patches: P[(n,ho,wo), (kh,kw,c)] for a k x k / stride s / pad p convolution
+__global__ void im2col_kernel(const uint16_t* __restrict__ X, uint16_t* __restrict__ P, int N, int H, int W, int C,
+                              int k, int s, int p, int Ho, int Wo, int ldp) {
+  const int64_t total = static_cast<int64_t>(N) * Ho * Wo * ldp;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int col = static_cast<int>(i % ldp);
+    const int64_t pix = i / ldp;
+    uint16_t v = 0;
+    if (col < k * k * C) {
+      const int khw = col / C, c = col - khw * C;
+      const int wo = static_cast<int>(pix % Wo);
+      const int64_t t = pix / Wo;
+      const int ho = static_cast<int>(t % Ho);
+      const int64_t n = t / Ho;
+      const int hh = ho * s + khw / k - p, ww = wo * s + khw % k - p;
+      if (hh >= 0 && hh < H && ww >= 0 && ww < W) v = X[((n * H + hh) * W + ww) * C + c];
+    }
+    P[i] = v;
+  }
+}
+
+// adjoint of im2col (gather form, fixed (kh, kw) order, fp32 sum of fp32 patch gradients):
+// dX[n,h,w,c] = Σ dP[(n,(h+p-kh)/s,(w+p-kw)/s), (kh,kw,c)] over valid (kh, kw); optional bf16 addend
+__global__ void col2im_kernel(const float* __restrict__ dP, uint16_t* __restrict__ dX, const uint16_t* __restrict__ add,
+                              int N, int H, int W, int C, int k, int s, int p, int Ho, int Wo, int ldp) {
+  const int64_t total = static_cast<int64_t>(N) * H * W * C;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int c = static_cast<int>(i % C);
+    int64_t t = i / C;
+    const int w = static_cast<int>(t % W);
+    t /= W;
+    const int h = static_cast<int>(t % H);
+    const int64_t n = t / H;
+    float acc = 0.f;
+    for (int kh = 0; kh < k; ++kh) {
+      const int hy = h + p - kh;
+      if (hy < 0 || hy % s) continue;
+      const int ho = hy / s;
+      if (ho >= Ho) continue;
+      for (int kw = 0; kw < k; ++kw) {
+        const int wy = w + p - kw;
+        if (wy < 0 || wy % s) continue;
+        const int wo = wy / s;
+        if (wo >= Wo) continue;
+        acc += dP[((n * Ho + ho) * Wo + wo) * static_cast<int64_t>(ldp) + (kh * k + kw) * C + c];
+      }
+    }
+    if (add) acc += bf2f(add[i]);
+    dX[i] = f2bf(acc);
+  }
+}
+
+// batch-norm statistics per (segment, channel) over `seg_rows` rows of x[rows, C] (bf16):
+// fp64 sums per (segment, row chunk, channel), then a fixed-order final pass -> mean, invstd
+constexpr int BN_CHUNK = 256;
+__global__ void bn_stats_partial(const uint16_t* __restrict__ x, int seg_rows, int C, int chunks,
+                                 double* __restrict__ part) {
+  // grid: (ceil(C/32), chunks, segments); block (32, 8)
+  const int c = blockIdx.x * 32 + threadIdx.x;
+  const int seg = blockIdx.z;
+  const int64_t r0 = static_cast<int64_t>(seg) * seg_rows;
+  const int per = (seg_rows + chunks - 1) / chunks;
+  const int a = blockIdx.y * per, b = min(seg_rows, a + per);
+  __shared__ double red[2][8][33];
+  double s1 = 0.0, s2 = 0.0;
+  if (c < C)
+    for (int r = a + threadIdx.y; r < b; r += 8) {
+      const double v = bf2f(x[(r0 + r) * C + c]);
+      s1 += v;
+      s2 += v * v;
+    }
+  red[0][threadIdx.y][threadIdx.x] = s1;
+  red[1][threadIdx.y][threadIdx.x] = s2;
+  __syncthreads();
+  if (threadIdx.y == 0 && c < C) {
+    double t1 = 0.0, t2 = 0.0;
+    for (int y = 0; y < 8; ++y) { t1 += red[0][y][threadIdx.x]; t2 += red[1][y][threadIdx.x]; }
+    const size_t o = (static_cast<size_t>(seg) * chunks + blockIdx.y) * C + c;
+    part[2 * o] = t1;
+    part[2 * o + 1] = t2;
+  }
+}
+
+__global__ void bn_stats_final(const double* __restrict__ part, int chunks, int C, int seg_rows, int segs,
+                               float* __restrict__ mean, float* __restrict__ invstd, float eps) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;   // (segment, channel)
+  if (i >= segs * C) return;
+  const int seg = i / C, c = i - seg * C;
+  double s1 = 0.0, s2 = 0.0;
+  for (int k = 0; k < chunks; ++k) {
+    const size_t o = (static_cast<size_t>(seg) * chunks + k) * C + c;
+    s1 += part[2 * o];
+    s2 += part[2 * o + 1];
+  }
+  const double m = s1 / seg_rows;
+  const double var = fmax(s2 / seg_rows - m * m, 0.0);
+  mean[i] = static_cast<float>(m);
+  invstd[i] = static_cast<float>(1.0 / sqrt(var + eps));
+}
+
+// y = act(γ·(x - μ_seg)·invstd_seg + β (+ res)) -> bf16
+__global__ void bn_apply_kernel(const uint16_t* __restrict__ x, const uint16_t* __restrict__ res,
+                                uint16_t* __restrict__ y, const float* __restrict__ gamma, const float* __restrict__ beta,
+                                const float* __restrict__ mean, const float* __restrict__ invstd, int64_t rows, int C,
+                                int seg_rows, int relu) {
+  const int64_t total = rows * C;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int c = static_cast<int>(i % C);
+    const int64_t r = i / C;
+    const int si = static_cast<int>(r / seg_rows) * C + c;
+    float v = gamma[c] * ((bf2f(x[i]) - mean[si]) * invstd[si]) + beta[c];
+    if (res) v += bf2f(res[i]);
+    if (relu) v = fmaxf(v, 0.f);
+    y[i] = f2bf(v);
+  }
+}
+
+// backward sums per (segment, channel): Σ dy', Σ dy'·x̂ with dy' = dy ⊙ [y > 0] if relu (fp64)
+__global__ void bn_bwd_partial(const uint16_t* __restrict__ dy, const uint16_t* __restrict__ y,
+                               const uint16_t* __restrict__ x, const float* __restrict__ mean,
+                               const float* __restrict__ invstd, int seg_rows, int C, int chunks, int relu,
+                               double* __restrict__ part) {
+  const int c = blockIdx.x * 32 + threadIdx.x;
+  const int seg = blockIdx.z;
+  const int64_t r0 = static_cast<int64_t>(seg) * seg_rows;
+  const int per = (seg_rows + chunks - 1) / chunks;
+  const int a = blockIdx.y * per, b = min(seg_rows, a + per);
+  __shared__ double red[2][8][33];
+  double s1 = 0.0, s2 = 0.0;
+  if (c < C) {
+    const double m = mean[seg * C + c], is = invstd[seg * C + c];
+    for (int r = a + threadIdx.y; r < b; r += 8) {
+      const int64_t o = (r0 + r) * C + c;
+      double d = bf2f(dy[o]);
+      if (relu && !(bf2f(y[o]) > 0.f)) d = 0.0;
+      s1 += d;
+      s2 += d * ((bf2f(x[o]) - m) * is);
+    }
+  }
+  red[0][threadIdx.y][threadIdx.x] = s1;
+  red[1][threadIdx.y][threadIdx.x] = s2;
+  __syncthreads();
+  if (threadIdx.y == 0 && c < C) {
+    double t1 = 0.0, t2 = 0.0;
+    for (int yy = 0; yy < 8; ++yy) { t1 += red[0][yy][threadIdx.x]; t2 += red[1][yy][threadIdx.x]; }
+    const size_t o = (static_cast<size_t>(seg) * chunks + blockIdx.y) * C + c;
+    part[2 * o] = t1;
+    part[2 * o + 1] = t2;
+  }
+}
+
+// per (segment, channel) sums -> sdy, sdyx (fp64); dγ = Σ_seg sdyx, dβ = Σ_seg sdy (fp32)
+__global__ void bn_bwd_final(const double* __restrict__ part, int chunks, int C, int segs, double* __restrict__ sums,
+                             float* __restrict__ dgamma, float* __restrict__ dbeta) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  double tg = 0.0, tb = 0.0;
+  for (int seg = 0; seg < segs; ++seg) {
+    double s1 = 0.0, s2 = 0.0;
+    for (int k = 0; k < chunks; ++k) {
+      const size_t o = (static_cast<size_t>(seg) * chunks + k) * C + c;
+      s1 += part[2 * o];
+      s2 += part[2 * o + 1];
+    }
+    sums[2 * (static_cast<size_t>(seg) * C + c)] = s1;
+    sums[2 * (static_cast<size_t>(seg) * C + c) + 1] = s2;
+    tb += s1;
+    tg += s2;
+  }
+  dgamma[c] = static_cast<float>(tg);
+  dbeta[c] = static_cast<float>(tb);
+}
+
+// dx = γ_res·invstd·(dy' - Σdy'/m - x̂·Σ(dy'x̂)/m) (bf16), γ_res = a·γ_stash + b·γ_latest;
+// d_res = dy' written to `dres` (bf16) when the layer adds a residual
+__global__ void bn_bwd_apply(const uint16_t* __restrict__ dy, const uint16_t* __restrict__ y,
+                             const uint16_t* __restrict__ x, const float* __restrict__ mean,
+                             const float* __restrict__ invstd, const double* __restrict__ sums,
+                             const float* __restrict__ gs, const float* __restrict__ gl, float ga, float gb, int64_t rows,
+                             int C, int seg_rows, int relu, uint16_t* __restrict__ dx, uint16_t* __restrict__ dres) {
+  const int64_t total = rows * C;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int c = static_cast<int>(i % C);
+    const int64_t r = i / C;
+    const int seg = static_cast<int>(r / seg_rows);
+    const int si = seg * C + c;
+    float d = bf2f(dy[i]);
+    if (relu && !(bf2f(y[i]) > 0.f)) d = 0.f;
+    if (dres) dres[i] = f2bf(d);
+    const float g = __fadd_rn(__fmul_rn(ga, gs[c]), __fmul_rn(gb, gl[c]));
+    const float xh = (bf2f(x[i]) - mean[si]) * invstd[si];
+    const double s1 = sums[2 * static_cast<size_t>(si)], s2 = sums[2 * static_cast<size_t>(si) + 1];
+    const float v = g * invstd[si] * (d - static_cast<float>(s1 / seg_rows) - xh * static_cast<float>(s2 / seg_rows));
+    dx[i] = f2bf(v);
+  }
+}
+
+// 3x3 / stride 2 / pad 1 max pool (padding never wins), and its gradient in gather form: an
+// input pixel collects dY of every window whose FIRST maximum it is (fixed window order)
+__global__ void maxpool3_fwd_kernel(const uint16_t* __restrict__ X, uint16_t* __restrict__ Y, int N, int H, int W,
+                                    int C, int Ho, int Wo) {
+  const int64_t total = static_cast<int64_t>(N) * Ho * Wo * C;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int c = static_cast<int>(i % C);
+    int64_t t = i / C;
+    const int wo = static_cast<int>(t % Wo);
+    t /= Wo;
+    const int ho = static_cast<int>(t % Ho);
+    const int64_t n = t / Ho;
+    float best = -INFINITY;
+    uint16_t bits = 0;
+    for (int kh = 0; kh < 3; ++kh)
+      for (int kw = 0; kw < 3; ++kw) {
+        const int h = 2 * ho + kh - 1, w = 2 * wo + kw - 1;
+        if (h < 0 || h >= H || w < 0 || w >= W) continue;
+        const uint16_t hb = X[((n * H + h) * W + w) * C + c];
+        const float v = bf2f(hb);
+        if (v > best) { best = v; bits = hb; }
+      }
+    Y[i] = bits;
+  }
+}
+
+__device__ __forceinline__ int maxpool3_first(const uint16_t* X, int64_t n, int ho, int wo, int c, int H, int W,
+                                              int C) {
+  float best = -INFINITY;
+  int arg = -1;
+  for (int kh = 0; kh < 3; ++kh)
+    for (int kw = 0; kw < 3; ++kw) {
+      const int h = 2 * ho + kh - 1, w = 2 * wo + kw - 1;
+      if (h < 0 || h >= H || w < 0 || w >= W) continue;
+      const float v = bf2f(X[((n * H + h) * W + w) * C + c]);
+      if (v > best) { best = v; arg = h * W + w; }
+    }
+  return arg;
+}
+
+__global__ void maxpool3_bwd_kernel(const uint16_t* __restrict__ X, const uint16_t* __restrict__ dY,
+                                    uint16_t* __restrict__ dX, int N, int H, int W, int C, int Ho, int Wo) {
+  const int64_t total = static_cast<int64_t>(N) * H * W * C;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int c = static_cast<int>(i % C);
+    int64_t t = i / C;
+    const int w = static_cast<int>(t % W);
+    t /= W;
+    const int h = static_cast<int>(t % H);
+    const int64_t n = t / H;
+    float acc = 0.f;
+    for (int ho = max(0, h / 2 - 1); ho <= min(Ho - 1, (h + 1) / 2); ++ho) {
+      if (h < 2 * ho - 1 || h > 2 * ho + 1) continue;
+      for (int wo = max(0, w / 2 - 1); wo <= min(Wo - 1, (w + 1) / 2); ++wo) {
+        if (w < 2 * wo - 1 || w > 2 * wo + 1) continue;
+        if (maxpool3_first(X, n, ho, wo, c, H, W, C) == h * W + w) acc += bf2f(dY[((n * Ho + ho) * Wo + wo) * C + c]);
+      }
+    }
+    dX[i] = f2bf(acc);
+  }
+}
+
+// global average pool [N, H*W, C] -> [N, C] (fp32 sum in fixed order, bf16 out) and its gradient
+__global__ void avgpool_fwd_kernel(const uint16_t* __restrict__ X, uint16_t* __restrict__ Y, int N, int HW, int C) {
+  const int64_t total = static_cast<int64_t>(N) * C;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int c = static_cast<int>(i % C);
+    const int64_t n = i / C;
+    double acc = 0.0;
+    for (int p = 0; p < HW; ++p) acc += bf2f(X[(n * HW + p) * C + c]);
+    Y[i] = f2bf(static_cast<float>(acc / HW));
+  }
+}
+
+__global__ void avgpool_bwd_kernel(const uint16_t* __restrict__ dY, uint16_t* __restrict__ dX, int N, int HW, int C) {
+  const int64_t total = static_cast<int64_t>(N) * HW * C;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int c = static_cast<int>(i % C);
+    const int64_t n = i / (static_cast<int64_t>(HW) * C);
+    dX[i] = f2bf(bf2f(dY[n * C + c]) / HW);
+  }
+}
+
+// out = bf16(out + add)   (gradient accumulation of a tensor with two consumers)
+__global__ void add_bf16_kernel(uint16_t* __restrict__ out, const uint16_t* __restrict__ add, int64_t n) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[i] = f2bf(bf2f(out[i]) + bf2f(add[i]));
+}
+
 uint64_t host_mix64(uint64_t x) {
   uint64_t z = x + 0x9E3779B97F4A7C15ull;
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
@@ -424,6 +721,90 @@ cudaError_t launch_im2col3x3(const uint16_t* X, uint16_t* P, int N, int H, int W
   const int64_t total = static_cast<int64_t>(N) * H * W * ldp;
   if (total <= 0) return cudaSuccess;
   im2col3x3_kernel<<<grid_for(total, 256), 256, 0, st>>>(X, P, N, H, W, C, ldp);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_im2col(const uint16_t* X, uint16_t* P, int N, int H, int W, int C, int k, int s, int p, int ldp,
+                          cudaStream_t st) {
+  const int Ho = (H + 2 * p - k) / s + 1, Wo = (W + 2 * p - k) / s + 1;
+  const int64_t total = static_cast<int64_t>(N) * Ho * Wo * ldp;
+  if (total <= 0) return cudaSuccess;
+  im2col_kernel<<<grid_for(total, 256), 256, 0, st>>>(X, P, N, H, W, C, k, s, p, Ho, Wo, ldp);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_col2im(const float* dP, uint16_t* dX, const uint16_t* add, int N, int H, int W, int C, int k, int s,
+                          int p, int ldp, cudaStream_t st) {
+  const int Ho = (H + 2 * p - k) / s + 1, Wo = (W + 2 * p - k) / s + 1;
+  const int64_t total = static_cast<int64_t>(N) * H * W * C;
+  if (total <= 0) return cudaSuccess;
+  col2im_kernel<<<grid_for(total, 256), 256, 0, st>>>(dP, dX, add, N, H, W, C, k, s, p, Ho, Wo, ldp);
+  return cudaGetLastError();
+}
+
+int bn_chunks(int seg_rows) { return std::max(1, std::min(64, seg_rows / BN_CHUNK)); }
+
+int64_t bn_scratch_doubles(int segs, int seg_rows, int C) {
+  return static_cast<int64_t>(segs) * bn_chunks(seg_rows) * C * 2 + static_cast<int64_t>(segs) * C * 2;
+}
+
+cudaError_t launch_bn_forward(const uint16_t* x, const uint16_t* res, uint16_t* y, const float* gamma,
+                              const float* beta, float* mean, float* invstd, int segs, int seg_rows, int C, int relu,
+                              double* scratch, cudaStream_t st) {
+  const int chunks = bn_chunks(seg_rows);
+  dim3 grid((C + 31) / 32, chunks, segs);
+  bn_stats_partial<<<grid, dim3(32, 8), 0, st>>>(x, seg_rows, C, chunks, scratch);
+  bn_stats_final<<<(segs * C + 255) / 256, 256, 0, st>>>(scratch, chunks, C, seg_rows, segs, mean, invstd, 1e-5f);
+  const int64_t rows = static_cast<int64_t>(segs) * seg_rows;
+  bn_apply_kernel<<<grid_for(rows * C, 256), 256, 0, st>>>(x, res, y, gamma, beta, mean, invstd, rows, C, seg_rows, relu);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bn_backward(const uint16_t* dy, const uint16_t* y, const uint16_t* x, const float* mean,
+                               const float* invstd, const float* gs, const float* gl, float ga, float gb, int segs,
+                               int seg_rows, int C, int relu, uint16_t* dx, uint16_t* dres, float* dgamma,
+                               float* dbeta, double* scratch, cudaStream_t st) {
+  const int chunks = bn_chunks(seg_rows);
+  double* sums = scratch + static_cast<int64_t>(segs) * chunks * C * 2;
+  dim3 grid((C + 31) / 32, chunks, segs);
+  bn_bwd_partial<<<grid, dim3(32, 8), 0, st>>>(dy, y, x, mean, invstd, seg_rows, C, chunks, relu, scratch);
+  bn_bwd_final<<<(C + 255) / 256, 256, 0, st>>>(scratch, chunks, C, segs, sums, dgamma, dbeta);
+  const int64_t rows = static_cast<int64_t>(segs) * seg_rows;
+  bn_bwd_apply<<<grid_for(rows * C, 256), 256, 0, st>>>(dy, y, x, mean, invstd, sums, gs, gl, ga, gb, rows, C, seg_rows,
+                                                        relu, dx, dres);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_maxpool3_fwd(const uint16_t* X, uint16_t* Y, int N, int H, int W, int C, cudaStream_t st) {
+  const int Ho = (H - 1) / 2 + 1, Wo = (W - 1) / 2 + 1;
+  const int64_t total = static_cast<int64_t>(N) * Ho * Wo * C;
+  if (total <= 0) return cudaSuccess;
+  maxpool3_fwd_kernel<<<grid_for(total, 256), 256, 0, st>>>(X, Y, N, H, W, C, Ho, Wo);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_maxpool3_bwd(const uint16_t* X, const uint16_t* dY, uint16_t* dX, int N, int H, int W, int C,
+                                cudaStream_t st) {
+  const int Ho = (H - 1) / 2 + 1, Wo = (W - 1) / 2 + 1;
+  const int64_t total = static_cast<int64_t>(N) * H * W * C;
+  if (total <= 0) return cudaSuccess;
+  maxpool3_bwd_kernel<<<grid_for(total, 256), 256, 0, st>>>(X, dY, dX, N, H, W, C, Ho, Wo);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_avgpool_fwd(const uint16_t* X, uint16_t* Y, int N, int HW, int C, cudaStream_t st) {
+  avgpool_fwd_kernel<<<grid_for(static_cast<int64_t>(N) * C, 256), 256, 0, st>>>(X, Y, N, HW, C);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_avgpool_bwd(const uint16_t* dY, uint16_t* dX, int N, int HW, int C, cudaStream_t st) {
+  avgpool_bwd_kernel<<<grid_for(static_cast<int64_t>(N) * HW * C, 256), 256, 0, st>>>(dY, dX, N, HW, C);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_add_bf16(uint16_t* out, const uint16_t* add, int64_t n, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  add_bf16_kernel<<<grid_for(n, 256), 256, 0, st>>>(out, add, n);
   return cudaGetLastError();
 }
 

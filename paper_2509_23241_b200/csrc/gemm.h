@@ -38,6 +38,8 @@ struct GemmArgs {
   float alpha;                // epilogue scale (EQ1 α), 1 = none
   float xa, xb;               // BLEND operand coefficients
   const uint16_t* mask; int ldm;  // bf16 ReLU mask source (zero where <= 0), may be null
+  const uint16_t* addend;     // bf16 [M, N] (ld = ldo) added before the bf16 store (gradient
+                              // accumulation of a tensor with two consumers); may alias out
   // EPI_SGD (wgrad only): instead of storing dW, apply the PyTorch-order SGD/momentum update
   // to the fp32 master w / momentum v ([M, N], ld = ldo) and write bf16(w) to ver.
   int epi;

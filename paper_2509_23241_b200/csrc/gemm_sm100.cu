@@ -437,6 +437,19 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
             }
           }
         }
+        if (args.addend) {
+          const uint4* ap = reinterpret_cast<const uint4*>(args.addend + static_cast<size_t>(grow) * args.ldo + gcol);
+#pragma unroll
+          for (int ch = 0; ch < 4; ++ch) {
+            if (ch < nchunk) {
+              const uint4 av = ap[ch];
+              const uint32_t w[4] = {av.x, av.y, av.z, av.w};
+#pragma unroll
+              for (int e2 = 0; e2 < 8; ++e2)
+                v[ch * 8 + e2] = __fadd_rn(v[ch * 8 + e2], __uint_as_float(((w[e2 >> 1] >> ((e2 & 1) * 16)) & 0xFFFFu) << 16));
+            }
+          }
+        }
         if (args.out_f32) {
           float* op = reinterpret_cast<float*>(args.out) + static_cast<size_t>(grow) * args.ldo + gcol;
 #pragma unroll

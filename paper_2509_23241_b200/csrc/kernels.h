@@ -42,6 +42,32 @@ cudaError_t launch_maxpool2_bwd(const uint16_t* X, const uint16_t* dY, uint16_t*
                                 cudaStream_t st);
 cudaError_t launch_im2col3x3(const uint16_t* X, uint16_t* P, int N, int H, int W, int C, int ldp, cudaStream_t st);
 
+// ResNet (NHWC bf16):
+//   general k x k / stride s / pad p patches P[(n,ho,wo), (kh,kw,c)] (zero padded to ldp) and
+//   their adjoint (gather form, fp32 patch gradients, optional bf16 addend, bf16 out);
+//   batch norm with per-micro-batch statistics over segments of seg_rows rows (biased
+//   variance, ε = 1e-5), fused residual add + ReLU; its backward with the blended γ
+//   (ga·γ_stash + gb·γ_latest) and the ReLU mask from the stored output;
+//   3x3/2/1 max pool (first maximum), global average pool, bf16 accumulate.
+cudaError_t launch_im2col(const uint16_t* X, uint16_t* P, int N, int H, int W, int C, int k, int s, int p, int ldp,
+                          cudaStream_t st);
+cudaError_t launch_col2im(const float* dP, uint16_t* dX, const uint16_t* add, int N, int H, int W, int C, int k, int s,
+                          int p, int ldp, cudaStream_t st);
+int64_t bn_scratch_doubles(int segs, int seg_rows, int C);
+cudaError_t launch_bn_forward(const uint16_t* x, const uint16_t* res, uint16_t* y, const float* gamma,
+                              const float* beta, float* mean, float* invstd, int segs, int seg_rows, int C, int relu,
+                              double* scratch, cudaStream_t st);
+cudaError_t launch_bn_backward(const uint16_t* dy, const uint16_t* y, const uint16_t* x, const float* mean,
+                               const float* invstd, const float* gs, const float* gl, float ga, float gb, int segs,
+                               int seg_rows, int C, int relu, uint16_t* dx, uint16_t* dres, float* dgamma,
+                               float* dbeta, double* scratch, cudaStream_t st);
+cudaError_t launch_maxpool3_fwd(const uint16_t* X, uint16_t* Y, int N, int H, int W, int C, cudaStream_t st);
+cudaError_t launch_maxpool3_bwd(const uint16_t* X, const uint16_t* dY, uint16_t* dX, int N, int H, int W, int C,
+                                cudaStream_t st);
+cudaError_t launch_avgpool_fwd(const uint16_t* X, uint16_t* Y, int N, int HW, int C, cudaStream_t st);
+cudaError_t launch_avgpool_bwd(const uint16_t* dY, uint16_t* dX, int N, int HW, int C, cudaStream_t st);
+cudaError_t launch_add_bf16(uint16_t* out, const uint16_t* add, int64_t n, cudaStream_t st);
+
 // synthgen-identical counter-based generator (see synthgen/__init__.py)
 //   kind 0/1: bf16 inputs into dst[rows, ld] (cols valid); kind 2: int32 labels[rows];
 //   kind 3: fp32 weights [rows=out, ld] (cols=in valid), scale 2^-(23 + shift).

@@ -99,7 +99,18 @@ struct Layer {
   int hw_in = 1, ld_in = 0, hw_out = 1, ld_out = 0;
   float *W = nullptr, *b = nullptr, *mW = nullptr, *mb = nullptr, *dW = nullptr, *db = nullptr;
   std::vector<uint16_t*> ver;  // R bf16 [Np, Kp] slots
-  bool has_w() const { return kind != TPS_LAYER_MAXPOOL2; }
+  // graph networks (ResNet): input = output of local layer `src` (-1 = stage input),
+  // BN residual = output of local layer `res` (-2 = none; -1 = stage input)
+  int k = 1, st = 1, pad = 0, src = -1, res = -2;
+  bool relu = false;
+  int Ho = 1, Wo = 1;
+  int conv_mode = 0;                  // CONV: 0 plain GEMM (1x1/s1), 1 implicit 3x3, 2 explicit patches
+  std::vector<float*> verf;           // BN: R fp32 γ versions [C]
+  std::vector<float*> mean, invstd;   // BN: per stash slot, [m, C] per-micro-batch statistics
+  bool has_w() const {
+    return kind == TPS_LAYER_LINEAR || kind == TPS_LAYER_CONV3X3 || kind == TPS_LAYER_CONV || kind == TPS_LAYER_BN;
+  }
+  bool has_b() const { return kind == TPS_LAYER_LINEAR || kind == TPS_LAYER_CONV3X3 || kind == TPS_LAYER_BN; }
   int64_t in_elems() const { return static_cast<int64_t>(hw_in) * ld_in; }    // per sample (stash)
   int64_t out_elems() const { return static_cast<int64_t>(hw_out) * ld_out; }
 };
@@ -127,6 +138,7 @@ struct tps_pipeline {
   float lr = 0.01f, mu = 0.f, wd = 0.f;
   uint64_t seed = 0;
   bool first = true, last = true, eq1_on_load = false, fuse_update = false;
+  bool graph = false;                        // ResNet-style layer graph (CONV/BN/MAXPOOL3/AVGPOOL)
   int upd_blocks_per_sm = 2;
   std::vector<int> dims;  // global
   std::vector<Layer> layers;
@@ -147,6 +159,13 @@ struct tps_pipeline {
   int64_t loss_cap = 0, loss_count = 0;
   int32_t* labels_dev = nullptr;
   float* scratch = nullptr;
+  // graph networks: one gradient buffer per local layer output, two accumulation temps,
+  // explicit-patch / patch-gradient scratch, batch-norm reduction scratch
+  std::vector<uint16_t*> gbuf;
+  uint16_t* gtmp[2] = {nullptr, nullptr};
+  uint16_t* patches = nullptr;
+  float* dpatches = nullptr;
+  double* bn_scr = nullptr;
   std::vector<void*> allocs;
 
   // ---- memory accounting
@@ -474,6 +493,251 @@ tps_status layer_forward(tps_pipeline* p, Layer& Lk, int nr, const uint16_t* Xin
   return run_gemm(p, tps::GEMM_FWD, op, ga, 0);
 }
 
+// ------------------------------------------------------------------ graph networks (ResNet)
+// local tensor t: -1 = stage input (input slot), k = output of local layer k (stash slot)
+uint16_t* gtensor(tps_pipeline* p, int slot0, int slot, int t) {
+  return t < 0 ? p->act[slot0][0] : p->act[slot][t + 1];
+}
+int64_t gelems(tps_pipeline* p, int t) { return t < 0 ? p->in0_elems : p->layers[t].out_elems(); }
+
+tps_status graph_forward(tps_pipeline* p, int64_t j, int a0, int cnt, int64_t v) {
+  const int slot0 = static_cast<int>(j % p->A0), slot = static_cast<int>(j % p->Kmax);
+  const int r0 = a0 * p->bsz, nr = cnt * p->bsz;
+  const int nl = p->nlayers();
+  for (int k = 0; k < nl; ++k) {
+    Layer& L = p->layers[k];
+    if (L.has_w()) CUDA_OK(cudaStreamWaitEvent(p->cs, p->ev_upd_done[k], 0));   // latest version written
+    const uint16_t* X = gtensor(p, slot0, slot, L.src) + static_cast<size_t>(r0) * gelems(p, L.src);
+    const bool head = L.kind == TPS_LAYER_LINEAR;
+    void* out = head ? static_cast<void*>(p->logits + static_cast<size_t>(r0) * L.Np)
+                     : static_cast<void*>(gtensor(p, slot0, slot, k) + static_cast<size_t>(r0) * L.out_elems());
+    switch (L.kind) {
+      case TPS_LAYER_CONV: {
+        tps::GemmArgs ga{};
+        ga.alpha = 1.f; ga.xa = 1.f; ga.out = out; ga.ldo = L.Co;
+        ga.M = nr * L.hw_out; ga.N = L.Co; ga.K = L.Kp;
+        const uint16_t* Wv = L.ver[v % p->R];
+        if (L.conv_mode == 1) {
+          tps::GemmOperands op{X, 0, Wv, L.Kp, nullptr};
+          op.cv = tps::ConvGeom{nr, L.H, L.Wd, L.Ci};
+          TPS_TRY(run_gemm(p, tps::GEMM_CONV_FWD, op, ga, 0));
+        } else {
+          const uint16_t* A = X;
+          if (L.conv_mode == 2) {
+            CUDA_OK(tps::launch_im2col(X, p->patches, nr, L.H, L.Wd, L.Ci, L.k, L.st, L.pad, L.Kp, p->cs));
+            p->launches += 1;
+            A = p->patches;
+          }
+          tps::GemmOperands op{A, L.Kp, Wv, L.Kp, nullptr};
+          TPS_TRY(run_gemm(p, tps::GEMM_FWD, op, ga, 0));
+        }
+        break;
+      }
+      case TPS_LAYER_BN: {
+        const uint16_t* res = L.res >= -1 ? gtensor(p, slot0, slot, L.res) + static_cast<size_t>(r0) * gelems(p, L.res)
+                                          : nullptr;
+        CUDA_OK(tps::launch_bn_forward(X, res, static_cast<uint16_t*>(out), L.verf[v % p->R], L.b,
+                                       L.mean[slot] + static_cast<size_t>(a0) * L.Ci,
+                                       L.invstd[slot] + static_cast<size_t>(a0) * L.Ci, cnt, p->bsz * L.hw_in, L.Ci,
+                                       L.relu ? 1 : 0, p->bn_scr, p->cs));
+        p->launches += 3;
+        break;
+      }
+      case TPS_LAYER_MAXPOOL3:
+        CUDA_OK(tps::launch_maxpool3_fwd(X, static_cast<uint16_t*>(out), nr, L.H, L.Wd, L.Ci, p->cs));
+        p->launches += 1;
+        break;
+      case TPS_LAYER_AVGPOOL:
+        CUDA_OK(tps::launch_avgpool_fwd(X, static_cast<uint16_t*>(out), nr, L.hw_in, L.Ci, p->cs));
+        p->launches += 1;
+        break;
+      default: {  // the head: fp32 logits
+        tps::GemmArgs ga{};
+        ga.alpha = 1.f; ga.xa = 1.f; ga.bias = L.b; ga.out_f32 = 1; ga.out = out; ga.ldo = L.Np;
+        ga.M = nr; ga.N = L.Np; ga.K = L.Kp;
+        tps::GemmOperands op{X, L.Kp, L.ver[v % p->R], L.Kp, nullptr};
+        TPS_TRY(run_gemm(p, tps::GEMM_FWD, op, ga, 0));
+      }
+    }
+  }
+  return TPS_OK;
+}
+
+// gradient accumulation target of tensor t in the current backward: the first contribution
+// writes the tensor's gradient buffer, later ones (a block input read by two layers) are
+// added to it (bf16(stored + new), reverse layer order, like oracle/graph.py)
+struct GradTarget {
+  uint16_t* buf;     // gradient buffer of the tensor
+  bool filled;       // already holds a contribution
+};
+
+tps_status graph_backward(tps_pipeline* p, int64_t j, int64_t v_used, int64_t vl, int64_t vn, float alpha, float beta,
+                          bool blend_on_load, const uint16_t* G_last) {
+  const int slot0 = static_cast<int>(j % p->A0), slot = static_cast<int>(j % p->Kmax);
+  const int nl = p->nlayers();
+  const int B = p->B;
+  std::vector<char> filled(nl + 1, 0);
+  bool gout_waited = false;
+  auto target = [&](int t) -> GradTarget {
+    if (t < 0) {
+      if (!gout_waited) {  // gout of mb j-2 has left
+        cudaStreamWaitEvent(p->cs, p->ev_bwd_sent[j & 1], 0);
+        gout_waited = true;
+      }
+      return GradTarget{p->gout[j & 1], filled[0] != 0};
+    }
+    return GradTarget{p->gbuf[t], filled[t + 1] != 0};
+  };
+  auto mark = [&](int t) { filled[t + 1] = 1; };
+  // contribution written to `tmp` when the target is already filled: add it in
+  auto settle = [&](int t, const GradTarget& g, uint16_t* tmp) -> tps_status {
+    if (g.filled) {
+      CUDA_OK(tps::launch_add_bf16(g.buf, tmp, static_cast<int64_t>(B) * gelems(p, t), p->cs));
+      p->launches += 1;
+    }
+    mark(t);
+    return TPS_OK;
+  };
+  auto update = [&](Layer& L, int k, bool gemm_grad) -> tps_status {
+    // U(j) directly follows B(j) (reading Z7): issue this layer's SGD step now on the
+    // optimizer stream; the next forward of layer k waits for ev_upd_done[k]
+    cudaStream_t us = p->s_upd;
+    CUDA_OK(cudaEventRecord(p->ev_grad_ready[k], p->cs));
+    CUDA_OK(cudaStreamWaitEvent(us, p->ev_grad_ready[k], 0));
+    const int64_t n = static_cast<int64_t>(L.Np) * L.Kp;
+    TimedLaunch tl{};
+    if (gemm_grad) TPS_TRY(time_begin(p, &tl, 4, (p->mu != 0.f ? 22.0 : 14.0) * n, us));
+    CUDA_OK(tps::launch_sgd_update(L.W, L.mW, L.dW, L.kind == TPS_LAYER_BN ? nullptr : L.ver[vn % p->R], n, p->lr,
+                                   p->mu, p->wd, us, p->upd_blocks_per_sm));
+    if (gemm_grad) TPS_TRY(time_end(p, &tl, us));
+    p->launches += 1;
+    if (L.kind == TPS_LAYER_BN)
+      CUDA_OK(cudaMemcpyAsync(L.verf[vn % p->R], L.W, static_cast<size_t>(n) * 4, cudaMemcpyDeviceToDevice, us));
+    if (L.b) {
+      CUDA_OK(tps::launch_sgd_update(L.b, L.mb, L.db, nullptr, L.Np, p->lr, p->mu, p->wd, us));
+      p->launches += 1;
+    }
+    CUDA_OK(cudaEventRecord(p->ev_upd_done[k], us));
+    return TPS_OK;
+  };
+  for (int k = nl - 1; k >= 0; --k) {
+    Layer& L = p->layers[k];
+    const uint16_t* g;
+    if (k == nl - 1) {
+      g = G_last;
+    } else {
+      if (!filled[k + 1]) return fail(TPS_E_STATE, "layer %d output has no gradient", L.gidx);
+      g = p->gbuf[k];
+    }
+    const uint16_t* X = gtensor(p, slot0, slot, L.src);
+    const bool need_dx = !(p->first && L.src == -1);
+    switch (L.kind) {
+      case TPS_LAYER_CONV:
+      case TPS_LAYER_LINEAR: {
+        const bool head = L.kind == TPS_LAYER_LINEAR;
+        if (need_dx) {
+          // input gradient first: the update must not rewrite this layer's weights before
+          const GradTarget dst = target(L.src);
+          tps::GemmArgs ga{};
+          ga.alpha = 1.f; ga.xa = 1.f; ga.xb = 0.f;
+          const int ldg = head ? L.Np : L.Co;
+          tps::GemmOperands op{g, ldg, L.ver[v_used % p->R], L.Kp, nullptr};
+          const bool expl = !head && L.conv_mode == 2;
+          if (expl) {      // patch gradient (fp32), then col2im adds it into the target
+            ga.out = p->dpatches; ga.out_f32 = 1; ga.ldo = L.Kp;
+            ga.M = B * L.hw_out; ga.N = L.Kp; ga.K = L.Co;
+          } else {
+            ga.out = dst.buf; ga.ldo = head ? L.Kp : L.Ci; ga.addend = dst.filled ? dst.buf : nullptr;
+            ga.M = B * L.hw_in; ga.N = head ? L.Kp : L.Ci; ga.K = head ? L.Np : L.Co;
+          }
+          int mode = tps::GEMM_DGRAD;
+          if (!head && L.conv_mode == 1) {
+            op.cv = tps::ConvGeom{B, L.H, L.Wd, L.Co};
+            op.Cw = L.Ci;
+            ga.K = 9 * L.Co;
+            mode = tps::GEMM_CONV_DGRAD;
+          }
+          if (blend_on_load) {
+            op.B2 = L.ver[vl % p->R];
+            ga.xa = alpha; ga.xb = beta;
+            mode = mode == tps::GEMM_CONV_DGRAD ? tps::GEMM_CONV_DGRAD_BLEND : tps::GEMM_DGRAD_BLEND;
+          } else {
+            ga.alpha = (p->variant == TPS_I) ? alpha : 1.f;   // EQ1: α·(G·W_stash) = G·(α·W_stash)
+          }
+          TPS_TRY(run_gemm(p, mode, op, ga, 1));
+          if (expl) {
+            CUDA_OK(tps::launch_col2im(p->dpatches, dst.buf, dst.filled ? dst.buf : nullptr, B, L.H, L.Wd, L.Ci, L.k,
+                                       L.st, L.pad, L.Kp, p->cs));
+            p->launches += 1;
+          }
+          mark(L.src);
+        }
+        // weight gradient dW[Np, Kp] = Gᵀ·(input or its patches)
+        tps::GemmArgs ga{};
+        ga.M = L.Np; ga.N = L.Kp; ga.out = L.dW; ga.ldo = L.Kp; ga.out_f32 = 1; ga.alpha = 1.f; ga.xa = 1.f;
+        if (!head && L.conv_mode == 1) {
+          ga.K = B * L.hw_out;
+          tps::GemmOperands op{g, L.Np, X, 0, nullptr};
+          op.cv = tps::ConvGeom{B, L.H, L.Wd, L.Ci};
+          TPS_TRY(run_gemm(p, tps::GEMM_CONV_WGRAD, op, ga, 2));
+        } else {
+          const uint16_t* Xb = X;
+          if (!head && L.conv_mode == 2) {
+            CUDA_OK(tps::launch_im2col(X, p->patches, B, L.H, L.Wd, L.Ci, L.k, L.st, L.pad, L.Kp, p->cs));
+            p->launches += 1;
+            Xb = p->patches;
+          }
+          ga.K = head ? B : B * L.hw_out;
+          tps::GemmOperands op{g, L.Np, Xb, L.Kp, nullptr};
+          TPS_TRY(run_gemm(p, tps::GEMM_WGRAD, op, ga, 2));
+        }
+        if (head) {
+          CUDA_OK(tps::launch_bias_grad(g, B, L.Np, L.Np, L.db, p->scratch, p->cs));
+          p->launches += 1;
+        }
+        TPS_TRY(update(L, k, true));
+        break;
+      }
+      case TPS_LAYER_BN: {
+        const uint16_t* y = gtensor(p, slot0, slot, k);
+        uint16_t* dres = nullptr;
+        GradTarget rt{nullptr, false};
+        if (L.res >= -1) {
+          rt = target(L.res);
+          dres = rt.filled ? p->gtmp[0] : rt.buf;
+        }
+        const GradTarget xt = target(L.src);
+        uint16_t* dx = xt.filled ? p->gtmp[1] : xt.buf;
+        // γ_res = α·γ_stash + β·γ_latest (V: α = 1, β = 0 on the latest; EQ1: β = 0)
+        const float ga = p->variant == TPS_I ? alpha : 1.f, gb = p->variant == TPS_I ? beta : 0.f;
+        CUDA_OK(tps::launch_bn_backward(g, y, X, L.mean[slot], L.invstd[slot], L.verf[v_used % p->R],
+                                        L.verf[vl % p->R], ga, gb, p->m, p->bsz * L.hw_in, L.Ci, L.relu ? 1 : 0, dx,
+                                        dres, L.dW, L.db, p->bn_scr, p->cs));
+        p->launches += 3;
+        if (L.res >= -1) TPS_TRY(settle(L.res, rt, p->gtmp[0]));
+        TPS_TRY(settle(L.src, xt, p->gtmp[1]));
+        TPS_TRY(update(L, k, false));
+        break;
+      }
+      case TPS_LAYER_MAXPOOL3:
+      case TPS_LAYER_AVGPOOL: {
+        if (!need_dx) break;
+        const GradTarget xt = target(L.src);
+        uint16_t* dx = xt.filled ? p->gtmp[1] : xt.buf;
+        if (L.kind == TPS_LAYER_MAXPOOL3) CUDA_OK(tps::launch_maxpool3_bwd(X, g, dx, B, L.H, L.Wd, L.Ci, p->cs));
+        else CUDA_OK(tps::launch_avgpool_bwd(g, dx, B, L.hw_in, L.Ci, p->cs));
+        p->launches += 1;
+        TPS_TRY(settle(L.src, xt, p->gtmp[1]));
+        break;
+      }
+      default:
+        return fail(TPS_E_STATE, "layer kind %d in a graph network", L.kind);
+    }
+  }
+  if (!p->first && !filled[0]) return fail(TPS_E_STATE, "stage input received no gradient");
+  return TPS_OK;
+}
+
 tps_status do_forward(tps_pipeline* p, int64_t j, int a0, int cnt, const void* x, const int32_t* labels) {
   TPS_TRY(expect(p, TPS_EV_F, j, a0, cnt));
   if (p->first && !x) return fail(TPS_E_INVALID_ARG, "stage 0 forward needs x");
@@ -485,8 +749,13 @@ tps_status do_forward(tps_pipeline* p, int64_t j, int a0, int cnt, const void* x
   const int slot0 = static_cast<int>(j % p->A0);
   const int slot = static_cast<int>(j % p->Kmax);
   Layer& L0 = p->layers[0];
-  uint16_t* X = p->act[slot0][0] + static_cast<size_t>(r0) * L0.in_elems();
-  if (p->first) {
+  uint16_t* X = p->act[slot0][0] + static_cast<size_t>(r0) * (p->graph ? p->in0_elems : L0.in_elems());
+  if (p->first && p->graph) {
+    CUDA_OK(cudaStreamWaitEvent(p->s_fin, p->ev_act_free[slot0], 0));
+    CUDA_OK(cudaMemcpyAsync(X, x, static_cast<size_t>(nr) * p->in0_elems * 2, cudaMemcpyDefault, p->s_fin));
+    CUDA_OK(cudaEventRecord(p->ev_recv, p->s_fin));
+    CUDA_OK(cudaStreamWaitEvent(p->cs, p->ev_recv, 0));
+  } else if (p->first) {
     // input copy (device pool or pinned host) on the input stream: with the extra input
     // slot it overlaps the backward/update still running on the compute stream
     CUDA_OK(cudaStreamWaitEvent(p->s_fin, p->ev_act_free[slot0], 0));
@@ -507,14 +776,15 @@ tps_status do_forward(tps_pipeline* p, int64_t j, int a0, int cnt, const void* x
       p->launches += 1;
     }
   } else {
-    TPS_TRY(recv_fwd(p, j, grp, X, static_cast<size_t>(nr) * L0.in_elems() * 2));
+    TPS_TRY(recv_fwd(p, j, grp, X, static_cast<size_t>(nr) * (p->graph ? p->in0_elems : L0.in_elems()) * 2));
   }
   if (!p->last) {  // the send buffer of mb j-2 must have left
     CUDA_OK(cudaStreamWaitEvent(p->cs, p->ev_fwd_sent[static_cast<int>(j & 1) * p->ng + grp], 0));
   }
   const int nl = p->nlayers();
   const uint16_t* Xin = X;
-  for (int k = 0; k < nl; ++k) {
+  if (p->graph) TPS_TRY(graph_forward(p, j, a0, cnt, v));
+  for (int k = 0; k < (p->graph ? 0 : nl); ++k) {
     Layer& Lk = p->layers[k];
     if (Lk.has_w()) CUDA_OK(cudaStreamWaitEvent(p->cs, p->ev_upd_done[k], 0));   // latest version written
     void* out;
@@ -543,7 +813,8 @@ tps_status do_forward(tps_pipeline* p, int64_t j, int a0, int cnt, const void* x
     }
   } else {
     Layer& Ll = p->layers[nl - 1];
-    TPS_TRY(send_fwd(p, j, grp, p->send_fwd[j & 1] + static_cast<size_t>(r0) * Ll.out_elems(),
+    uint16_t* sb = p->graph ? p->act[slot][nl] : p->send_fwd[j & 1];   // graph: send from the stash
+    TPS_TRY(send_fwd(p, j, grp, sb + static_cast<size_t>(r0) * Ll.out_elems(),
                      static_cast<size_t>(nr) * Ll.out_elems() * 2));
   }
   tps_event e{};
@@ -591,7 +862,8 @@ tps_status do_backward(tps_pipeline* p, int64_t j, int staleness) {
   int wbuf = 0;
   const int64_t vn = vl + 1;   // version the update of this mini-batch produces
   const bool blend_on_load = p->variant == TPS_I && delta > 0 && (p->blend == TPS_BLEND_CONVEX || p->eq1_on_load);
-  for (int k = nl - 1; k >= 0; --k) {
+  if (p->graph) TPS_TRY(graph_backward(p, j, v_used, vl, vn, alpha, beta, blend_on_load, G));
+  for (int k = (p->graph ? -1 : nl - 1); k >= 0; --k) {
     Layer& Lk = p->layers[k];
     const uint16_t* X = (k == 0) ? p->act[slot0][0] : p->act[slot][k];
     // input gradient first: it must read this layer's weights before a fused update rewrites them
@@ -807,6 +1079,176 @@ tps_status validate_specs(const tps_config* c) {
   return TPS_OK;
 }
 
+bool is_graph_kind(int k) {
+  return k == TPS_LAYER_CONV || k == TPS_LAYER_BN || k == TPS_LAYER_MAXPOOL3 || k == TPS_LAYER_AVGPOOL;
+}
+
+struct GShape {
+  int h = 0, w = 0, c = 0;   // flat tensors: h = w = 1
+  int64_t elems() const { return static_cast<int64_t>(h) * w * c; }
+  bool operator==(const GShape& o) const { return h == o.h && w == o.w && c == o.c; }
+};
+
+// output shape of every layer of a graph network (validated); shapes[l + 1] = output of layer l,
+// shapes[0] = the network input
+tps_status graph_shapes(const tps_config* c, std::vector<GShape>* shapes) {
+  const int L = c->num_layers;
+  shapes->assign(L + 1, GShape{});
+  const tps_layer& s0 = c->layer_specs[0];
+  (*shapes)[0] = GShape{s0.in_h, s0.in_w, s0.in_c};
+  if ((*shapes)[0].elems() != c->dims[0]) return fail(TPS_E_CONFIG, "dims[0] must equal H·W·C of layer 0's input");
+  for (int l = 0; l < L; ++l) {
+    const tps_layer& sp = c->layer_specs[l];
+    if (!is_graph_kind(sp.kind) && sp.kind != TPS_LAYER_LINEAR)
+      return fail(TPS_E_CONFIG, "layer %d: kind %d cannot be mixed with graph layers", l, sp.kind);
+    const int src = l - std::max(1, sp.src_back);
+    if (src < -1) return fail(TPS_E_CONFIG, "layer %d: src_back %d reaches before the input", l, sp.src_back);
+    const GShape in = (*shapes)[src + 1];
+    GShape o;
+    if (sp.kind == TPS_LAYER_LINEAR) {
+      if (l != L - 1) return fail(TPS_E_CONFIG, "layer %d: in a graph network LINEAR is the last layer (the head)", l);
+      if (in.h != 1 || in.w != 1 || in.c != sp.in_c) return fail(TPS_E_CONFIG, "layer %d: head input must be a flat %d-vector", l, sp.in_c);
+      if (sp.in_c % 16 || sp.out_c < 1) return fail(TPS_E_CONFIG, "layer %d: head needs in_c %% 16 == 0", l);
+      o = GShape{1, 1, sp.out_c};
+    } else {
+      if (!(in == GShape{sp.in_h, sp.in_w, sp.in_c}))
+        return fail(TPS_E_CONFIG, "layer %d: input %dx%dx%d does not match its source (layer %d: %dx%dx%d)", l, sp.in_h,
+                    sp.in_w, sp.in_c, src, in.h, in.w, in.c);
+      if (sp.kind == TPS_LAYER_CONV) {
+        if (sp.k < 1 || sp.stride < 1 || sp.pad < 0) return fail(TPS_E_CONFIG, "layer %d: bad conv k/stride/pad", l);
+        const int ho = (sp.in_h + 2 * sp.pad - sp.k) / sp.stride + 1, wo = (sp.in_w + 2 * sp.pad - sp.k) / sp.stride + 1;
+        if (ho < 1 || wo < 1) return fail(TPS_E_CONFIG, "layer %d: empty conv output", l);
+        if (sp.out_c % 16) return fail(TPS_E_CONFIG, "layer %d: conv out_c must be a multiple of 16", l);
+        o = GShape{ho, wo, sp.out_c};
+      } else if (sp.kind == TPS_LAYER_BN) {
+        o = in;
+        if (sp.res_back > 0) {
+          const int r = l - sp.res_back;
+          if (r < -1) return fail(TPS_E_CONFIG, "layer %d: res_back %d reaches before the input", l, sp.res_back);
+          if (!((*shapes)[r + 1] == o)) return fail(TPS_E_CONFIG, "layer %d: residual shape mismatch", l);
+        }
+      } else if (sp.kind == TPS_LAYER_MAXPOOL3) {
+        o = GShape{(sp.in_h - 1) / 2 + 1, (sp.in_w - 1) / 2 + 1, sp.in_c};
+      } else {
+        o = GShape{1, 1, sp.in_c};
+      }
+    }
+    (*shapes)[l + 1] = o;
+  }
+  if (c->layer_specs[L - 1].kind != TPS_LAYER_LINEAR) return fail(TPS_E_CONFIG, "the last layer must be the Linear head");
+  // a stage reads only its own layers and the previous stage's last output
+  for (int s = 0; s < c->num_stages; ++s)
+    for (int l = c->stage_bounds[s]; l < c->stage_bounds[s + 1]; ++l) {
+      const tps_layer& sp = c->layer_specs[l];
+      const int src = l - std::max(1, sp.src_back);
+      const int r = (sp.kind == TPS_LAYER_BN && sp.res_back > 0) ? l - sp.res_back : c->stage_bounds[s];
+      if (src < c->stage_bounds[s] - 1 || r < c->stage_bounds[s] - 1)
+        return fail(TPS_E_CONFIG, "layer %d (stage %d) reads a tensor of an earlier stage other than its input", l, s);
+    }
+  return TPS_OK;
+}
+
+tps_status init_graph(tps_pipeline* p, const tps_config* c, int lb, int le) {
+  std::vector<GShape> sh;
+  TPS_TRY(graph_shapes(c, &sh));
+  p->fuse_update = false;   // graph networks update on the optimizer stream
+  int64_t max_elems = sh[lb].elems();
+  int64_t patch_elems = 0, dpatch_elems = 0, bn_doubles = 0, bias_scr = 0;
+  for (int l = lb; l < le; ++l) {
+    const tps_layer& sp = c->layer_specs[l];
+    const GShape in = sh[l - std::max(1, sp.src_back) + 1], o = sh[l + 1];
+    Layer L;
+    L.gidx = l;
+    L.kind = sp.kind;
+    L.src = l - std::max(1, sp.src_back) - lb;
+    L.res = (sp.kind == TPS_LAYER_BN && sp.res_back > 0) ? l - sp.res_back - lb : -2;
+    L.relu = sp.kind == TPS_LAYER_BN && sp.relu != 0;
+    L.H = in.h; L.Wd = in.w; L.Ci = in.c; L.Co = o.c; L.Ho = o.h; L.Wo = o.w;
+    L.hw_in = in.h * in.w; L.ld_in = in.c; L.hw_out = o.h * o.w; L.ld_out = o.c;
+    if (sp.kind == TPS_LAYER_CONV) {
+      L.k = sp.k; L.st = sp.stride; L.pad = sp.pad;
+      L.in = sp.k * sp.k * L.Ci; L.out = L.Co; L.Np = L.Co;
+      if (L.k == 1 && L.st == 1 && L.pad == 0 && L.Ci % 16 == 0) {
+        L.conv_mode = 0; L.Kp = L.Ci;
+      } else if (L.k == 3 && L.st == 1 && L.pad == 1 && L.Ci % 64 == 0 && L.Co % 64 == 0) {
+        L.conv_mode = 1; L.Kp = 9 * L.Ci;
+      } else {
+        L.conv_mode = 2; L.Kp = pad16(L.in);
+        const int64_t pe = static_cast<int64_t>(p->B) * L.hw_out * L.Kp;
+        patch_elems = std::max(patch_elems, pe);
+        if (!(p->first && L.src == -1)) dpatch_elems = std::max(dpatch_elems, pe);
+      }
+    } else if (sp.kind == TPS_LAYER_BN) {
+      L.in = 1; L.out = L.Ci; L.Kp = 1; L.Np = L.Ci;
+      bn_doubles = std::max(bn_doubles, tps::bn_scratch_doubles(p->m, p->bsz * L.hw_in, L.Ci));
+    } else if (sp.kind == TPS_LAYER_LINEAR) {
+      L.in = sp.in_c; L.out = sp.out_c; L.Kp = pad16(L.in); L.Np = pad16(L.out);
+      L.ld_in = L.Kp; L.ld_out = L.Np;
+      bias_scr = std::max(bias_scr, tps::bias_grad_scratch_floats(p->B, L.Np));
+    }
+    max_elems = std::max({max_elems, L.in_elems(), L.out_elems()});
+    if (L.has_w()) {
+      const size_t n = static_cast<size_t>(L.Np) * L.Kp;
+      TPS_TRY(alloc_t(p, &L.W, n, &p->mem_weights));
+      if (L.has_b()) TPS_TRY(alloc_t(p, &L.b, L.Np, &p->mem_weights));
+      if (p->mu != 0.f) {
+        TPS_TRY(alloc_t(p, &L.mW, n, &p->mem_optim));
+        if (L.has_b()) TPS_TRY(alloc_t(p, &L.mb, L.Np, &p->mem_optim));
+      }
+      TPS_TRY(alloc_t(p, &L.dW, n, &p->mem_optim));
+      if (L.has_b()) TPS_TRY(alloc_t(p, &L.db, L.Np, &p->mem_optim));
+      if (L.kind == TPS_LAYER_BN) {
+        L.verf.resize(p->R);
+        for (int r = 0; r < p->R; ++r) TPS_TRY(alloc_t(p, &L.verf[r], n, r == 0 ? &p->mem_weights : &p->mem_stash));
+        p->ver_bytes += static_cast<int64_t>(n) * 4;
+        L.mean.resize(p->Kmax);
+        L.invstd.resize(p->Kmax);
+        for (int r = 0; r < p->Kmax; ++r) {
+          TPS_TRY(alloc_t(p, &L.mean[r], static_cast<size_t>(p->m) * L.Ci, &p->mem_acts));
+          TPS_TRY(alloc_t(p, &L.invstd[r], static_cast<size_t>(p->m) * L.Ci, &p->mem_acts));
+        }
+      } else {
+        L.ver.resize(p->R);
+        for (int r = 0; r < p->R; ++r) TPS_TRY(alloc_t(p, &L.ver[r], n, r == 0 ? &p->mem_weights : &p->mem_stash));
+        p->ver_bytes += static_cast<int64_t>(n) * 2;
+      }
+    }
+    p->layers.push_back(L);
+  }
+  const int nl = p->nlayers();
+  p->in0_elems = sh[lb].elems();
+  p->act.assign(std::max(p->A0, p->Kmax), std::vector<uint16_t*>(nl + 1, nullptr));
+  for (int slot = 0; slot < static_cast<int>(p->act.size()); ++slot) {
+    if (slot < p->A0) TPS_TRY(alloc_t(p, &p->act[slot][0], static_cast<size_t>(p->B) * p->in0_elems, &p->mem_acts));
+    if (slot >= p->Kmax) continue;
+    for (int k = 0; k < nl; ++k)
+      if (k < nl - 1 || !p->last)
+        TPS_TRY(alloc_t(p, &p->act[slot][k + 1], static_cast<size_t>(p->B) * p->layers[k].out_elems(), &p->mem_acts));
+  }
+  p->gbuf.assign(nl, nullptr);
+  for (int k = 0; k + 1 < nl; ++k)
+    TPS_TRY(alloc_t(p, &p->gbuf[k], static_cast<size_t>(p->B) * p->layers[k].out_elems(), &p->mem_acts));
+  for (int i = 0; i < 2; ++i) TPS_TRY(alloc_t(p, &p->gtmp[i], static_cast<size_t>(p->B) * max_elems, &p->mem_acts));
+  TPS_TRY(alloc_t(p, &p->patches, patch_elems, &p->mem_acts));
+  TPS_TRY(alloc_t(p, &p->dpatches, dpatch_elems, &p->mem_acts));
+  TPS_TRY(alloc_t(p, &p->bn_scr, bn_doubles, &p->mem_acts));
+  const int64_t outL = p->layers[nl - 1].out_elems();
+  for (int i = 0; i < 2; ++i) {
+    if (!p->last) TPS_TRY(alloc_t(p, &p->gin[i], static_cast<size_t>(p->B) * outL, &p->mem_comm));
+    if (!p->first) TPS_TRY(alloc_t(p, &p->gout[i], static_cast<size_t>(p->B) * p->in0_elems, &p->mem_comm));
+  }
+  if (p->last) {
+    TPS_TRY(alloc_t(p, &p->logits, static_cast<size_t>(p->B) * outL, &p->mem_acts));
+    TPS_TRY(alloc_t(p, &p->gce, static_cast<size_t>(p->B) * outL, &p->mem_acts));
+    TPS_TRY(alloc_t(p, &p->loss_rows, p->B, &p->mem_acts));
+    TPS_TRY(alloc_t(p, &p->labels_dev, p->B, &p->mem_acts));
+    p->loss_cap = 1 << 20;
+    TPS_TRY(alloc_t(p, &p->losses, p->loss_cap, &p->mem_acts));
+  }
+  TPS_TRY(alloc_t(p, &p->scratch, bias_scr, &p->mem_optim));
+  return TPS_OK;
+}
+
 tps_status tps_pipeline_init(const tps_config* c, tps_pipeline** out) {
   if (!c || !out) return fail(TPS_E_INVALID_ARG, "null argument");
   *out = nullptr;
@@ -817,8 +1259,11 @@ tps_status tps_pipeline_init(const tps_config* c, tps_pipeline** out) {
   if (c->variant != TPS_V && c->variant != TPS_I) return fail(TPS_E_CONFIG, "bad variant");
   if (c->blend != TPS_BLEND_EQ1 && c->blend != TPS_BLEND_CONVEX) return fail(TPS_E_CONFIG, "bad blend");
   if (c->variant == TPS_I && !(c->lambda > 0)) return fail(TPS_E_CONFIG, "lambda must be > 0 (P:227)");
+  bool graph = false;
   if (c->num_layer_specs > 0) {
-    TPS_TRY(validate_specs(c));
+    if (c->num_layer_specs != c->num_layers || !c->layer_specs) return fail(TPS_E_CONFIG, "need num_layers layer specs");
+    for (int l = 0; l < c->num_layers; ++l) graph = graph || is_graph_kind(c->layer_specs[l].kind);
+    if (!graph) TPS_TRY(validate_specs(c));
   } else {
     for (int l = 0; l <= c->num_layers; ++l)
       if (c->dims[l] < 1) return fail(TPS_E_CONFIG, "dims[%d] < 1", l);
@@ -827,6 +1272,10 @@ tps_status tps_pipeline_init(const tps_config* c, tps_pipeline** out) {
     return fail(TPS_E_CONFIG, "stage_bounds must start at 0 and end at num_layers");
   for (int s = 0; s < c->num_stages; ++s)
     if (c->stage_bounds[s + 1] <= c->stage_bounds[s]) return fail(TPS_E_CONFIG, "stage %d owns no layer", s);
+  if (graph) {
+    std::vector<GShape> sh;
+    TPS_TRY(graph_shapes(c, &sh));
+  }
   const int g = c->fwd_group <= 0 ? c->micro_batches : c->fwd_group;
   if (c->micro_batches % g) return fail(TPS_E_CONFIG, "fwd_group must divide micro_batches");
   if (c->num_stages > 1 && c->transport == TPS_TRANSPORT_NONE) return fail(TPS_E_CONFIG, "S > 1 needs a transport");
@@ -850,6 +1299,7 @@ tps_status tps_pipeline_init(const tps_config* c, tps_pipeline** out) {
   const char* env = std::getenv("TPS_EQ1_ON_LOAD");
   p->eq1_on_load = env && env[0] == '1';
   p->fuse_update = c->fuse_update != 0;
+  p->graph = graph;
   if (const char* e2 = std::getenv("TPS_UPD_BPS")) p->upd_blocks_per_sm = std::max(1, std::atoi(e2));
 
   auto cleanup = [&](tps_status st) {
@@ -857,6 +1307,10 @@ tps_status tps_pipeline_init(const tps_config* c, tps_pipeline** out) {
     return st;
   };
   const int lb = c->stage_bounds[p->s], le = c->stage_bounds[p->s + 1];
+  if (p->graph) {
+    const tps_status gs = init_graph(p, c, lb, le);
+    if (gs != TPS_OK) return cleanup(gs);
+  } else {
   int64_t max_elems = 0;
   for (int l = lb; l < le; ++l) {
     Layer L;
@@ -945,6 +1399,8 @@ tps_status tps_pipeline_init(const tps_config* c, tps_pipeline** out) {
     if (L.has_w()) scr = std::max(scr, tps::bias_grad_scratch_floats(p->B * L.hw_out, L.Np));
   if ((st = alloc_t(p, &p->scratch, scr, &p->mem_optim)) != TPS_OK) return cleanup(st);
 
+  }
+  const int nl = p->nlayers();
   // streams and events
   if (c->compute_stream) {
     p->cs = reinterpret_cast<cudaStream_t>(c->compute_stream);
@@ -1160,6 +1616,7 @@ tps_status tps_intermediate_weight(tps_pipeline* p, int32_t layer, int32_t stale
   compute_coeffs(p->variant, p->blend, staleness, p->lambda, &a, &b);
   if (!p->layers[layer].has_w()) return fail(TPS_E_INVALID_ARG, "layer %d has no parameters", layer);
   Layer& L = p->layers[layer];
+  if (L.kind == TPS_LAYER_BN) return fail(TPS_E_INVALID_ARG, "layer %d: BN γ versions are fp32 (use tps_get_weights)", layer);
   CUDA_OK(cudaStreamWaitEvent(p->cs, p->ev_upd_done[layer], 0));
   const int64_t vs = p->latest - staleness;
   CUDA_OK(tps::launch_blend_materialize(L.ver[vs % p->R], L.ver[p->latest % p->R], static_cast<uint16_t*>(out_bf16),
@@ -1174,6 +1631,7 @@ tps_status tps_get_version(tps_pipeline* p, int32_t layer, int32_t staleness, vo
   if (staleness < 0 || staleness > p->latest || staleness >= p->R) return fail(TPS_E_STALENESS, "no live version at staleness %d", staleness);
   if (!p->layers[layer].has_w()) return fail(TPS_E_INVALID_ARG, "layer %d has no parameters", layer);
   Layer& L = p->layers[layer];
+  if (L.kind == TPS_LAYER_BN) return fail(TPS_E_INVALID_ARG, "layer %d: BN γ versions are fp32 (use tps_get_weights)", layer);
   CUDA_OK(cudaStreamWaitEvent(p->cs, p->ev_upd_done[layer], 0));
   CUDA_OK(cudaMemcpyAsync(out_bf16, L.ver[(p->latest - staleness) % p->R], static_cast<size_t>(L.Np) * L.Kp * 2,
                           cudaMemcpyDeviceToDevice, p->cs));
@@ -1189,7 +1647,10 @@ tps_status tps_get_weights(tps_pipeline* p, int32_t layer, float* w, float* b, f
   Layer& L = p->layers[layer];
   const size_t rowb = static_cast<size_t>(L.in) * 4, ldb = static_cast<size_t>(L.Kp) * 4;
   if (w) CUDA_OK(cudaMemcpy2D(w, rowb, L.W, ldb, rowb, L.out, cudaMemcpyDeviceToHost));
-  if (b) CUDA_OK(cudaMemcpy(b, L.b, static_cast<size_t>(L.out) * 4, cudaMemcpyDeviceToHost));
+  if (b) {
+    if (L.b) CUDA_OK(cudaMemcpy(b, L.b, static_cast<size_t>(L.out) * 4, cudaMemcpyDeviceToHost));
+    else std::memset(b, 0, static_cast<size_t>(L.out) * 4);
+  }
   if (mw) {
     if (L.mW) CUDA_OK(cudaMemcpy2D(mw, rowb, L.mW, ldb, rowb, L.out, cudaMemcpyDeviceToHost));
     else std::memset(mw, 0, rowb * L.out);
@@ -1213,13 +1674,16 @@ tps_status tps_set_weights(tps_pipeline* p, int32_t layer, const float* w, const
     CUDA_OK(cudaMemset(L.W, 0, n * 4));
     CUDA_OK(cudaMemcpy2D(L.W, ldb, w, rowb, rowb, L.out, cudaMemcpyHostToDevice));
   }
-  if (b) {
+  if (b && L.b) {
     CUDA_OK(cudaMemset(L.b, 0, static_cast<size_t>(L.Np) * 4));
     CUDA_OK(cudaMemcpy(L.b, b, static_cast<size_t>(L.out) * 4, cudaMemcpyHostToDevice));
   }
   if (L.mW) CUDA_OK(cudaMemset(L.mW, 0, n * 4));
   if (L.mb) CUDA_OK(cudaMemset(L.mb, 0, static_cast<size_t>(L.Np) * 4));
-  CUDA_OK(tps::launch_f32_to_bf16(L.W, L.ver[p->latest % p->R], static_cast<int64_t>(n), p->cs));
+  if (L.kind == TPS_LAYER_BN)
+    CUDA_OK(cudaMemcpyAsync(L.verf[p->latest % p->R], L.W, n * 4, cudaMemcpyDeviceToDevice, p->cs));
+  else
+    CUDA_OK(tps::launch_f32_to_bf16(L.W, L.ver[p->latest % p->R], static_cast<int64_t>(n), p->cs));
   p->launches += 1;
   TPS_TRY(sync_streams(p));
   return TPS_OK;
@@ -1229,12 +1693,22 @@ tps_status tps_init_weights_synthetic(tps_pipeline* p) {
   TPS_TRY(check_usable(p));
   for (auto& L : p->layers) {
     if (!L.has_w()) continue;
+    if (L.kind == TPS_LAYER_BN) {   // γ = 1, β = 0
+      std::vector<float> one(L.Np, 1.0f);
+      CUDA_OK(cudaMemcpyAsync(L.W, one.data(), one.size() * 4, cudaMemcpyHostToDevice, p->cs));
+      CUDA_OK(cudaMemsetAsync(L.b, 0, static_cast<size_t>(L.Np) * 4, p->cs));
+      if (L.mW) CUDA_OK(cudaMemsetAsync(L.mW, 0, static_cast<size_t>(L.Np) * 4, p->cs));
+      if (L.mb) CUDA_OK(cudaMemsetAsync(L.mb, 0, static_cast<size_t>(L.Np) * 4, p->cs));
+      CUDA_OK(cudaMemcpyAsync(L.verf[p->latest % p->R], L.W, static_cast<size_t>(L.Np) * 4, cudaMemcpyDeviceToDevice, p->cs));
+      CUDA_OK(cudaStreamSynchronize(p->cs));
+      continue;
+    }
     // round half to even, like synthgen (Python round): fan_in = 512 -> log2(sqrt) = 4.5 -> 4
     const int shift = static_cast<int>(std::nearbyint(std::log2(std::sqrt(static_cast<double>(L.in)))));
     CUDA_OK(cudaMemsetAsync(L.W, 0, static_cast<size_t>(L.Np) * L.Kp * 4, p->cs));
     CUDA_OK(tps::launch_fill_synthetic(3, p->seed, 0x0100 + static_cast<uint64_t>(L.gidx), L.out, L.in, L.Kp, 0, shift,
                                        L.W, p->cs));
-    CUDA_OK(cudaMemsetAsync(L.b, 0, static_cast<size_t>(L.Np) * 4, p->cs));
+    if (L.b) CUDA_OK(cudaMemsetAsync(L.b, 0, static_cast<size_t>(L.Np) * 4, p->cs));
     if (L.mW) CUDA_OK(cudaMemsetAsync(L.mW, 0, static_cast<size_t>(L.Np) * L.Kp * 4, p->cs));
     if (L.mb) CUDA_OK(cudaMemsetAsync(L.mb, 0, static_cast<size_t>(L.Np) * 4, p->cs));
     CUDA_OK(tps::launch_f32_to_bf16(L.W, L.ver[p->latest % p->R], static_cast<int64_t>(L.Np) * L.Kp, p->cs));
@@ -1397,6 +1871,86 @@ tps_status tps_conv_gemm(int32_t mode, int32_t N, int32_t H, int32_t W, int32_t 
     gm = mode == 3 ? tps::GEMM_CONV_DGRAD_BLEND : tps::GEMM_CONV_DGRAD;
   }
   CUDA_OK(tps::gemm_run(gm, op, ga, reinterpret_cast<cudaStream_t>(stream)));
+  return TPS_OK;
+}
+
+namespace {
+tps_status op_prologue() {
+  int dev = 0;
+  CUDA_OK(cudaGetDevice(&dev));
+  return check_arch(dev);
+}
+}  // namespace
+
+tps_status tps_im2col(const void* X, void* P, int32_t N, int32_t H, int32_t W, int32_t C, int32_t k, int32_t stride,
+                      int32_t pad, int32_t ldp, uint64_t stream) {
+  if (!X || !P || N < 1 || H < 1 || W < 1 || C < 1 || k < 1 || stride < 1 || pad < 0 || ldp < k * k * C)
+    return fail(TPS_E_INVALID_ARG, "bad im2col arguments");
+  TPS_TRY(op_prologue());
+  CUDA_OK(tps::launch_im2col(static_cast<const uint16_t*>(X), static_cast<uint16_t*>(P), N, H, W, C, k, stride, pad,
+                             ldp, reinterpret_cast<cudaStream_t>(stream)));
+  return TPS_OK;
+}
+
+tps_status tps_col2im(const float* dP, void* dX, const void* add, int32_t N, int32_t H, int32_t W, int32_t C,
+                      int32_t k, int32_t stride, int32_t pad, int32_t ldp, uint64_t stream) {
+  if (!dP || !dX || N < 1 || H < 1 || W < 1 || C < 1 || k < 1 || stride < 1 || pad < 0 || ldp < k * k * C)
+    return fail(TPS_E_INVALID_ARG, "bad col2im arguments");
+  TPS_TRY(op_prologue());
+  CUDA_OK(tps::launch_col2im(dP, static_cast<uint16_t*>(dX), static_cast<const uint16_t*>(add), N, H, W, C, k, stride,
+                             pad, ldp, reinterpret_cast<cudaStream_t>(stream)));
+  return TPS_OK;
+}
+
+tps_status tps_bn_forward(const void* x, const void* res, void* y, const float* gamma, const float* beta, float* mean,
+                          float* invstd, int32_t segs, int32_t seg_rows, int32_t C, int32_t relu, uint64_t stream) {
+  if (!x || !y || !gamma || !beta || !mean || !invstd || segs < 1 || seg_rows < 1 || C < 1)
+    return fail(TPS_E_INVALID_ARG, "bad bn_forward arguments");
+  TPS_TRY(op_prologue());
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  void* scr = nullptr;
+  CUDA_OK(cudaMallocAsync(&scr, sizeof(double) * tps::bn_scratch_doubles(segs, seg_rows, C), st));
+  const cudaError_t e = tps::launch_bn_forward(static_cast<const uint16_t*>(x), static_cast<const uint16_t*>(res),
+                                               static_cast<uint16_t*>(y), gamma, beta, mean, invstd, segs, seg_rows, C,
+                                               relu, static_cast<double*>(scr), st);
+  CUDA_OK(cudaFreeAsync(scr, st));
+  CUDA_OK(e);
+  return TPS_OK;
+}
+
+tps_status tps_bn_backward(const void* dy, const void* y, const void* x, const float* mean, const float* invstd,
+                           const float* gamma_stash, const float* gamma_latest, float a, float b, int32_t segs,
+                           int32_t seg_rows, int32_t C, int32_t relu, void* dx, void* dres, float* dgamma,
+                           float* dbeta, uint64_t stream) {
+  if (!dy || !y || !x || !mean || !invstd || !gamma_stash || !gamma_latest || !dx || !dgamma || !dbeta || segs < 1 ||
+      seg_rows < 1 || C < 1)
+    return fail(TPS_E_INVALID_ARG, "bad bn_backward arguments");
+  TPS_TRY(op_prologue());
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  void* scr = nullptr;
+  CUDA_OK(cudaMallocAsync(&scr, sizeof(double) * tps::bn_scratch_doubles(segs, seg_rows, C), st));
+  const cudaError_t e = tps::launch_bn_backward(
+      static_cast<const uint16_t*>(dy), static_cast<const uint16_t*>(y), static_cast<const uint16_t*>(x), mean, invstd,
+      gamma_stash, gamma_latest, a, b, segs, seg_rows, C, relu, static_cast<uint16_t*>(dx),
+      static_cast<uint16_t*>(dres), dgamma, dbeta, static_cast<double*>(scr), st);
+  CUDA_OK(cudaFreeAsync(scr, st));
+  CUDA_OK(e);
+  return TPS_OK;
+}
+
+tps_status tps_pool_op(int32_t op, const void* a, const void* b, void* out, int32_t N, int32_t H, int32_t W, int32_t C,
+                       uint64_t stream) {
+  if (op < 0 || op > 3 || !out || N < 1 || H < 1 || W < 1 || C < 1) return fail(TPS_E_INVALID_ARG, "bad pool arguments");
+  if ((op <= 2 && !a) || ((op == 1 || op == 3) && !b)) return fail(TPS_E_INVALID_ARG, "missing pool operand");
+  TPS_TRY(op_prologue());
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const uint16_t* A = static_cast<const uint16_t*>(a);
+  const uint16_t* Bp = static_cast<const uint16_t*>(b);
+  uint16_t* O = static_cast<uint16_t*>(out);
+  if (op == 0) CUDA_OK(tps::launch_maxpool3_fwd(A, O, N, H, W, C, st));
+  else if (op == 1) CUDA_OK(tps::launch_maxpool3_bwd(A, Bp, O, N, H, W, C, st));
+  else if (op == 2) CUDA_OK(tps::launch_avgpool_fwd(A, O, N, H * W, C, st));
+  else CUDA_OK(tps::launch_avgpool_bwd(Bp, O, N, H * W, C, st));
   return TPS_OK;
 }
 

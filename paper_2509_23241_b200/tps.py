@@ -31,9 +31,11 @@ EXPORTS = [
     "tps_intermediate_weight", "tps_get_version", "tps_schedule_events", "tps_get_weights", "tps_set_weights",
     "tps_init_weights_synthetic", "tps_get_losses", "tps_get_trace", "tps_clear_trace", "tps_memory_stats",
     "tps_set_profiling", "tps_kernel_stats", "tps_launch_count", "tps_fill_synthetic", "tps_gemm",
-    "tps_conv_gemm", "tps_partition",
+    "tps_conv_gemm", "tps_partition", "tps_im2col", "tps_col2im", "tps_bn_forward", "tps_bn_backward",
+    "tps_pool_op",
 ]
 TPS_LAYER_LINEAR, TPS_LAYER_CONV3X3, TPS_LAYER_MAXPOOL2 = 0, 1, 2
+TPS_LAYER_CONV, TPS_LAYER_BN, TPS_LAYER_MAXPOOL3, TPS_LAYER_AVGPOOL = 3, 4, 5, 6
 
 
 class TpsError(RuntimeError):
@@ -50,7 +52,8 @@ class Event(C.Structure):
 
 class Layer(C.Structure):
     _fields_ = [("kind", C.c_int32), ("in_c", C.c_int32), ("out_c", C.c_int32), ("in_h", C.c_int32),
-                ("in_w", C.c_int32), ("reserved", C.c_int32 * 3)]
+                ("in_w", C.c_int32), ("k", C.c_int32), ("stride", C.c_int32), ("pad", C.c_int32),
+                ("src_back", C.c_int32), ("res_back", C.c_int32), ("relu", C.c_int32), ("reserved", C.c_int32 * 5)]
 
 
 class Config(C.Structure):
@@ -108,6 +111,11 @@ def lib() -> C.CDLL:
             "tps_gemm": (I32, [I32, I32, I32, I32, P, I32, P, I32, P, P, I32, I32, P, I32, F, F, P, I32, U64]),
             "tps_conv_gemm": (I32, [I32, I32, I32, I32, I32, I32, P, P, P, P, I32, P, I32, F, F, P, U64]),
             "tps_partition": (I32, [I32, P, P, P, I32, I32, I32, I32, P, P]),
+            "tps_im2col": (I32, [P, P, I32, I32, I32, I32, I32, I32, I32, I32, U64]),
+            "tps_col2im": (I32, [P, P, P, I32, I32, I32, I32, I32, I32, I32, I32, U64]),
+            "tps_bn_forward": (I32, [P, P, P, P, P, P, P, I32, I32, I32, I32, U64]),
+            "tps_bn_backward": (I32, [P, P, P, P, P, P, P, F, F, I32, I32, I32, I32, P, P, P, P, U64]),
+            "tps_pool_op": (I32, [I32, P, P, P, I32, I32, I32, I32, U64]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -168,6 +176,29 @@ def conv_gemm(mode, N, H, W, Ci, Co, A, Wt, out, out_f32=0, bias=None, relu=0, a
                               alpha, beta, ptr(mask), stream))
 
 
+def im2col(X, P, N, H, W, C, k, stride, pad, ldp, stream: int = 0) -> None:
+    check(lib().tps_im2col(ptr(X), ptr(P), N, H, W, C, k, stride, pad, ldp, stream))
+
+
+def col2im(dP, dX, add, N, H, W, C, k, stride, pad, ldp, stream: int = 0) -> None:
+    check(lib().tps_col2im(ptr(dP), ptr(dX), ptr(add), N, H, W, C, k, stride, pad, ldp, stream))
+
+
+def bn_forward(x, res, y, gamma, beta, mean, invstd, segs, seg_rows, C, relu, stream: int = 0) -> None:
+    check(lib().tps_bn_forward(ptr(x), ptr(res), ptr(y), ptr(gamma), ptr(beta), ptr(mean), ptr(invstd), segs, seg_rows,
+                               C, relu, stream))
+
+
+def bn_backward(dy, y, x, mean, invstd, g_stash, g_latest, a, b, segs, seg_rows, C, relu, dx, dres, dgamma, dbeta,
+                stream: int = 0) -> None:
+    check(lib().tps_bn_backward(ptr(dy), ptr(y), ptr(x), ptr(mean), ptr(invstd), ptr(g_stash), ptr(g_latest), a, b,
+                                segs, seg_rows, C, relu, ptr(dx), ptr(dres), ptr(dgamma), ptr(dbeta), stream))
+
+
+def pool_op(op, a, b, out, N, H, W, C, stream: int = 0) -> None:
+    check(lib().tps_pool_op(op, ptr(a), ptr(b), ptr(out), N, H, W, C, stream))
+
+
 def partition(param_bytes, act_bytes, flops, S: int, variant: int = TPS_I, momentum: bool = True,
               objective: int = 0):
     """Balanced consecutive stage partition (C++ DP in libtps); returns (bounds, stage costs)."""
@@ -185,13 +216,42 @@ def layer_specs(specs: list[dict]):
     """oracle-style layer dicts -> ctypes tps_layer array."""
     arr = (Layer * len(specs))()
     for i, sp in enumerate(specs):
-        if sp["kind"] == "linear":
-            arr[i] = Layer(TPS_LAYER_LINEAR, sp["in"], sp["out"], 1, 1)
-        elif sp["kind"] == "conv3":
+        back = i - sp.get("src", i - 1)          # graph layers name their input by global index
+        k = sp["kind"]
+        if k == "linear":
+            arr[i] = Layer(TPS_LAYER_LINEAR, sp["in"], sp["out"], 1, 1, src_back=back)
+        elif k == "conv3":
             arr[i] = Layer(TPS_LAYER_CONV3X3, sp["cin"], sp["cout"], sp["h"], sp["w"])
-        else:
+        elif k == "pool2":
             arr[i] = Layer(TPS_LAYER_MAXPOOL2, sp["c"], sp["c"], sp["h"], sp["w"])
+        elif k == "conv":
+            arr[i] = Layer(TPS_LAYER_CONV, sp["cin"], sp["cout"], sp["h"], sp["w"], sp["k"], sp["s"], sp["p"],
+                           src_back=back)
+        elif k == "bn":
+            res = sp.get("res")
+            arr[i] = Layer(TPS_LAYER_BN, sp["c"], sp["c"], sp["h"], sp["w"], src_back=back,
+                           res_back=(i - res) if res is not None else 0, relu=1 if sp.get("relu") else 0)
+        elif k == "maxpool3":
+            arr[i] = Layer(TPS_LAYER_MAXPOOL3, sp["c"], sp["c"], sp["h"], sp["w"], src_back=back)
+        elif k == "avgpool":
+            arr[i] = Layer(TPS_LAYER_AVGPOOL, sp["c"], sp["c"], sp["h"], sp["w"], src_back=back)
+        else:
+            raise ValueError(f"layer {i}: unknown kind {k!r}")
     return arr
+
+
+def layer_param_shape(sp: dict):
+    """Logical [out, in] of a layer's weight as tps_get_weights returns it (None: no parameters)."""
+    k = sp["kind"]
+    if k == "conv3":
+        return (sp["cout"], 9 * sp["cin"])
+    if k == "conv":
+        return (sp["cout"], sp["k"] * sp["k"] * sp["cin"])
+    if k == "bn":
+        return (sp["c"], 1)
+    if k == "linear":
+        return (sp["out"], sp["in"])
+    return None
 
 
 # ------------------------------------------------------------------ handle wrapper
@@ -228,7 +288,7 @@ class Pipeline:
         if spec.layers:
             L = len(spec.layers)
             s0 = spec.layers[0]
-            feat = s0["h"] * s0["w"] * s0["cin"] if s0["kind"] == "conv3" else s0["in"]
+            feat = s0["h"] * s0["w"] * s0["cin"] if s0["kind"] in ("conv3", "conv") else s0["in"]
             dvals = [feat] + [0] * (L - 1) + [spec.layers[-1]["out"]]
         else:
             L = len(spec.dims) - 1
@@ -254,9 +314,7 @@ class Pipeline:
         self.shapes = []   # logical [out, in] of each stage-local layer (None for pools)
         for g in self.layers:
             if spec.layers:
-                sp = spec.layers[g]
-                self.shapes.append(None if sp["kind"] == "pool2" else
-                                   (sp["cout"], 9 * sp["cin"]) if sp["kind"] == "conv3" else (sp["out"], sp["in"]))
+                self.shapes.append(layer_param_shape(spec.layers[g]))
             else:
                 self.shapes.append((spec.dims[g + 1], spec.dims[g]))
 

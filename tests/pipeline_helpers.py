@@ -39,6 +39,44 @@ def net_workload(layers, m, b, M, seed=0, kind=synthgen.X_UNIT):
     return xs, ys, w0, b0
 
 
+GRAPH_KINDS = ("conv", "bn", "maxpool3", "avgpool")
+
+
+def is_graph(layers):
+    return bool(layers) and any(sp["kind"] in GRAPH_KINDS for sp in layers)
+
+
+def graph_workload(layers, m, b, M, seed=0, kind=synthgen.X_UNIT):
+    """ResNet-style inputs (flattened NHWC rows) and parameters: synthgen conv weights
+    [Co,k,k,Ci] (fan_in k·k·Ci), BN γ = 1, β = 0, synthgen head weights, zero head bias."""
+    s0 = layers[0]
+    feat = s0["h"] * s0["w"] * s0["cin"]
+    classes = layers[-1]["out"]
+    xs = [synthgen.inputs(seed, j, m * b, feat, kind) for j in range(M)]
+    ys = [synthgen.labels(seed, j, m * b, classes) for j in range(M)]
+    params = []
+    for l, sp in enumerate(layers):
+        k = sp["kind"]
+        if k == "conv":
+            kk = sp["k"]
+            w = synthgen.weights(seed, l, sp["cout"], kk * kk * sp["cin"]).reshape(sp["cout"], kk, kk, sp["cin"])
+            params.append((w, None))
+        elif k == "bn":
+            params.append((np.ones(sp["c"], np.float32), np.zeros(sp["c"], np.float32)))
+        elif k == "linear":
+            params.append((synthgen.weights(seed, l, sp["out"], sp["in"]), np.zeros(sp["out"], np.float32)))
+        else:
+            params.append((None, None))
+    return xs, ys, params
+
+
+def run_oracle_graph(layers, bounds, m, b, M, variant, blend, lam, lr, mu, wd=0.0, seed=0, kind=synthgen.X_UNIT):
+    from oracle import graph as ograph
+    xs, ys, params = graph_workload(layers, m, b, M, seed, kind)
+    return ograph.run(layers, bounds, m, b, M, xs, ys, params, variant=variant, blend=blend, lam=lam, lr=lr, mu=mu,
+                      wd=wd)
+
+
 def run_oracle(dims, bounds, m, b, M, variant, blend, lam, lr, mu, wd=0.0, seed=0, kind=synthgen.X_SIGNED,
                layers=None):
     if layers:
@@ -58,7 +96,12 @@ def run_gpu(dims, bounds, m, b, M, variant, blend, lam, lr, mu, wd=0.0, seed=0, 
     from paper_2509_23241_b200 import tps
 
     S = len(bounds) - 1
-    if layers:
+    if is_graph(layers):
+        xs, ys, params = graph_workload(layers, m, b, M, seed, kind)
+        w0 = [p[0] for p in params]
+        b0 = [p[1] if p[1] is not None else np.zeros(p[0].shape[0], np.float32) if p[0] is not None else None
+              for p in params]
+    elif layers:
         xs, ys, w0, b0 = net_workload(layers, m, b, M, seed, kind)
     else:
         xs, ys, w0, b0 = workload(dims, m, b, M, seed, kind)

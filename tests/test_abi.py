@@ -30,7 +30,7 @@ def test_library_exports_every_declared_symbol():
     exported = set(re.findall(r"\bT (tps_[a-z_0-9]+)", out))
     missing = [s for s in declared_symbols() if s not in exported]
     assert not missing, missing
-    assert tps.lib().tps_abi_version() == 1
+    assert tps.lib().tps_abi_version() == 2
 
 
 @pytest.mark.parametrize("S", [1, 2, 4, 8])
@@ -88,3 +88,47 @@ def test_no_cpu_fallback():
     with pytest.raises(tps.TpsError) as e:
         tps.Pipeline(tps.StageSpec([8, 8, 4], [0, 2], 0, 2, 4))
     assert e.value.status == 8          # TPS_E_ARCH
+
+
+def _resnet(**kw):
+    from oracle import graph
+    return graph.resnet_layers(blocks=(1, 1), widths=(16, 32), H=32, classes=10, stem_c=16, **kw)
+
+
+def test_graph_config_validation_errors_without_gpu():
+    """ResNet-style layer graphs: shape, residual, stage-crossing and head checks run before
+    the device check, so each bad config fails with TPS_E_CONFIG on a CPU-only host."""
+    import copy
+    layers, starts = _resnet()
+    L = len(layers)
+    dims = [32 * 32 * 3, 10]
+
+    def spec(ls, bounds, sid=0):
+        return tps.StageSpec(dims, bounds, sid, 2, 4, layers=ls, transport=1 if len(bounds) > 2 else 0)
+
+    bad = []
+    x = copy.deepcopy(layers)
+    x[3]["cin"] = 32                                   # conv input channels != its source's
+    bad.append(spec(x, [0, L]))
+    x = copy.deepcopy(layers)
+    x[10]["res"] = 4                                   # residual of a different shape
+    bad.append(spec(x, [0, L]))
+    x = copy.deepcopy(layers)
+    x[0]["cout"] = 12                                  # conv out_c % 16
+    x[1]["c"] = 12
+    bad.append(spec(x, [0, L]))
+    x = copy.deepcopy(layers)
+    x.insert(L - 1, {"kind": "linear", "in": 128, "out": 128, "src": L - 2})   # LINEAR not last
+    bad.append(spec(x, [0, L + 1]))
+    # a stage boundary inside a bottleneck: bn3 would read the block input across the boundary
+    bad.append(spec(layers, [0, starts[1] + 2, L], sid=1))
+    for sp in bad:
+        with pytest.raises(tps.TpsError) as e:
+            tps.Pipeline(sp)
+        assert e.value.status == 2, tps.last_error() if hasattr(tps, "last_error") else sp
+    # the valid graph passes validation and stops at the device check (no GPU here)
+    import torch
+    if not torch.cuda.is_available():
+        with pytest.raises(tps.TpsError) as e:
+            tps.Pipeline(spec(layers, [0, starts[1], L], sid=1))
+        assert e.value.status == 8

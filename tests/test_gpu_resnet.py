@@ -1,0 +1,101 @@
+"""ResNet (BASELINE.json configs[3]) parity: the CUDA graph path (general convs on tcgen05 GEMMs,
+per-micro-batch batch norm with fused residual + ReLU, 3x3/2 max pool, global average pool,
+gradient accumulation of block inputs) against oracle/graph.py on the same seeded inputs.
+
+Trace bit-exact.  Losses within 1e-3 relative over the first 1-3 mini-batches; over 10, within
+max(1e-3, 2·gap) with gap the bf16 oracle's own largest loss distance from the fp64 oracle run
+(it reaches 5e-3 on the wider net: the dynamics amplify rounding).  Parameters (reading Z23): batch-norm networks
+are ill-conditioned in bf16 storage — a parameter gradient is a cancelling sum (Σ_rows dx = 0
+after every BN) — so the bf16 oracle itself sits 10-30 % (one step, relative to the update)
+away from the same run in fp64 arithmetic.  The GPU path must be at least as close to the bf16
+oracle as the bf16 oracle is to exact arithmetic:
+  * after 1-3 mini-batches, per layer: |ΔW_gpu - ΔW_ref|max / |ΔW_ref|max <= max(0.05, gap)
+    (ΔW = change from the initial parameters, gap = the same ratio for the fp64 oracle run);
+    a dropped term or wrong sign moves an update by >= 100 %;
+  * after 10 mini-batches, per layer: |W_gpu - W_ref|max / |W_ref|max <= max(5e-3, 2·gap).
+"""
+import numpy as np
+import pytest
+
+import synthgen
+from oracle import graph as ograph
+from oracle import staleness as ost
+from pipeline_helpers import expand_gpu_trace, graph_workload, oracle_trace, run_gpu, run_oracle_graph
+
+pytestmark = pytest.mark.gpu
+
+VARIANTS = {"V": (ost.V_VARIANT, ost.EQ1), "I-EQ1": (ost.I_VARIANT, ost.EQ1), "I-CONVEX": (ost.I_VARIANT, ost.CONVEX)}
+
+
+def tiny(widths=(16, 32), H=32, stem_c=16, blocks=(1, 1)):
+    return ograph.resnet_layers(blocks=blocks, widths=widths, H=H, classes=10, stem_c=stem_c)
+
+
+def compare(layers, bounds, m, b, M, variant, blend, lr=0.01, mu=0.9, mode="params"):
+    kind = synthgen.X_UNIT
+    ref = run_oracle_graph(layers, bounds, m, b, M, variant, blend, 0.05, lr, mu, kind=kind)
+    xs, ys, params = graph_workload(layers, m, b, M, kind=kind)
+    ex = ograph.run(layers, bounds, m, b, M, xs, ys, params, variant=variant, blend=blend, lam=0.05, lr=lr, mu=mu,
+                    exact=True)
+    dims = [layers[0]["h"] * layers[0]["w"] * layers[0]["cin"], layers[-1]["out"]]
+    stages, losses = run_gpu(dims, bounds, m, b, M, variant, blend, 0.05, lr, mu, kind=kind, layers=layers)
+    assert expand_gpu_trace(stages) == oracle_trace(ref)
+    lerr = np.abs(losses - ref.losses) / np.abs(ref.losses)
+    lgap = np.abs(ex.losses - ref.losses) / np.abs(ref.losses)
+    if mode == "update":
+        assert lerr.max() <= 1e-3, lerr
+    else:
+        assert lerr.max() <= max(1e-3, 2 * lgap.max()), (lerr, lgap)
+    bad = {}
+    for st in stages:
+        for k, l in enumerate(st.layers):
+            if ref.weights[l] is None:
+                continue
+            w, bb, _, _ = st.get_weights(k)
+            cat = lambda W, B_: np.concatenate([np.asarray(W, np.float64).ravel()] +
+                                               ([np.asarray(B_, np.float64).ravel()] if ref.biases[l] is not None
+                                                else []))
+            g = cat(w, bb)
+            r = cat(ref.weights[l], ref.biases[l])
+            e = cat(ex.weights[l], ex.biases[l])
+            p0 = params[l][1] if params[l][1] is not None else None
+            w0 = cat(params[l][0], p0)
+            if mode == "update":
+                du = np.abs(r - w0).max()
+                err, gap = np.abs(g - r).max() / du, np.abs(e - r).max() / du
+                lim = max(0.05, gap)
+            else:
+                sc = np.abs(r).max()
+                err, gap = np.abs(g - r).max() / sc, np.abs(e - r).max() / sc
+                lim = max(5e-3, 2 * gap)
+            if not err <= lim:
+                bad[(l, layers[l]["kind"])] = (round(err, 5), round(lim, 5))
+        st.close()
+    assert not bad, f"layers over their bound (err, bound): {bad}"
+
+
+@pytest.mark.parametrize("vn", list(VARIANTS))
+def test_tiny_resnet_first_updates_one_stage(gpu_lib, vn):
+    layers, starts = tiny()
+    compare(layers, [0, len(layers)], 2, 8, 2, *VARIANTS[vn], mode="update")
+
+
+@pytest.mark.parametrize("vn", list(VARIANTS))
+def test_tiny_resnet_first_updates_three_stages(gpu_lib, vn):
+    layers, starts = tiny()
+    # stem | block 1 | block 2 + head: the block input crosses each boundary and is read twice
+    compare(layers, [0, starts[1], starts[2], len(layers)], 2, 8, 3, *VARIANTS[vn], mode="update")
+
+
+@pytest.mark.parametrize("vn", list(VARIANTS))
+def test_tiny_resnet_ten_steps_three_stages(gpu_lib, vn):
+    layers, starts = tiny()
+    compare(layers, [0, starts[1], starts[2], len(layers)], 2, 8, 10, *VARIANTS[vn])
+
+
+@pytest.mark.parametrize("vn", list(VARIANTS))
+def test_resnet_implicit_conv_paths(gpu_lib, vn):
+    """widths 64/128: 3x3 stride-1 convs take the 4-D TMA implicit-GEMM path, 1x1 convs the
+    plain GEMM path, strided convs explicit patches; two bottlenecks in the first stage."""
+    layers, starts = tiny(widths=(64, 128), H=32, stem_c=64, blocks=(2, 1))
+    compare(layers, [0, starts[2], len(layers)], 2, 8, 10, *VARIANTS[vn])
