@@ -50,6 +50,10 @@ struct GemmArgs {
 
 enum GemmEpilogue { EPI_STORE = 0, EPI_SGD = 1 };
 
+// whether the implicit-im2col conv modes (4-D TMA pixel boxes of whole image rows) support an
+// H x W activation: 128- and 64-pixel tiles must be whole rows of one image or whole images
+bool conv_implicit_ok(int H, int W);
+
 cudaError_t gemm_run(int mode, const GemmOperands& op, const GemmArgs& args, cudaStream_t st, int* bn_out = nullptr);
 const char* gemm_mode_name(int mode);
 

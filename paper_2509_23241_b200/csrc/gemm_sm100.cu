@@ -598,6 +598,15 @@ bool pixel_box(int pixels, int H, int W, uint32_t (&box)[4]) {
   return true;
 }
 
+}  // namespace
+
+bool conv_implicit_ok(int H, int W) {
+  uint32_t b[4];
+  return pixel_box(128, H, W, b) && pixel_box(64, H, W, b);
+}
+
+namespace {
+
 int num_sms() {
   static int n = 0;
   if (!n) {

@@ -1170,7 +1170,8 @@ tps_status init_graph(tps_pipeline* p, const tps_config* c, int lb, int le) {
       L.in = sp.k * sp.k * L.Ci; L.out = L.Co; L.Np = L.Co;
       if (L.k == 1 && L.st == 1 && L.pad == 0 && L.Ci % 16 == 0) {
         L.conv_mode = 0; L.Kp = L.Ci;
-      } else if (L.k == 3 && L.st == 1 && L.pad == 1 && L.Ci % 64 == 0 && L.Co % 64 == 0) {
+      } else if (L.k == 3 && L.st == 1 && L.pad == 1 && L.Ci % 64 == 0 && L.Co % 64 == 0 &&
+                 tps::conv_implicit_ok(L.H, L.Wd)) {
         L.conv_mode = 1; L.Kp = 9 * L.Ci;
       } else {
         L.conv_mode = 2; L.Kp = pad16(L.in);

@@ -2,9 +2,9 @@
 per-micro-batch batch norm with fused residual + ReLU, 3x3/2 max pool, global average pool,
 gradient accumulation of block inputs) against oracle/graph.py on the same seeded inputs.
 
-Trace bit-exact.  Losses within 1e-3 relative over the first 1-3 mini-batches; over 10, within
-max(1e-3, 2·gap) with gap the bf16 oracle's own largest loss distance from the fp64 oracle run
-(it reaches 5e-3 on the wider net: the dynamics amplify rounding).  Parameters (reading Z23): batch-norm networks
+Trace bit-exact.  Losses within max(1e-3, 2·gap), gap = the bf16 oracle's own largest loss
+distance from the same run in fp64 arithmetic (tiny nets: gap < 5e-4, so 1e-3 binds; the wider
+net reaches 5e-3 after 10 steps; ResNet-50's first forward alone is 1.4e-3 away from fp64).  Parameters (reading Z23): batch-norm networks
 are ill-conditioned in bf16 storage — a parameter gradient is a cancelling sum (Σ_rows dx = 0
 after every BN) — so the bf16 oracle itself sits 10-30 % (one step, relative to the update)
 away from the same run in fp64 arithmetic.  The GPU path must be at least as close to the bf16
@@ -42,10 +42,7 @@ def compare(layers, bounds, m, b, M, variant, blend, lr=0.01, mu=0.9, mode="para
     assert expand_gpu_trace(stages) == oracle_trace(ref)
     lerr = np.abs(losses - ref.losses) / np.abs(ref.losses)
     lgap = np.abs(ex.losses - ref.losses) / np.abs(ref.losses)
-    if mode == "update":
-        assert lerr.max() <= 1e-3, lerr
-    else:
-        assert lerr.max() <= max(1e-3, 2 * lgap.max()), (lerr, lgap)
+    assert lerr.max() <= max(1e-3, 2 * lgap.max()), (lerr, lgap)
     bad = {}
     for st in stages:
         for k, l in enumerate(st.layers):
@@ -99,3 +96,17 @@ def test_resnet_implicit_conv_paths(gpu_lib, vn):
     plain GEMM path, strided convs explicit patches; two bottlenecks in the first stage."""
     layers, starts = tiny(widths=(64, 128), H=32, stem_c=64, blocks=(2, 1))
     compare(layers, [0, starts[2], len(layers)], 2, 8, 10, *VARIANTS[vn])
+
+
+# SURVEY §8 C4: ResNet-50 v1.5 / 224 / 1000 classes, 8 stages at bottleneck granularity:
+# [stem..l1.1] [l1.2..l2.0] [l2.1..l2.2] [l2.3..l3.0] [l3.1..l3.2] [l3.3..l3.5] [l4.0] [l4.1..fc]
+def resnet50_bounds(starts, L):
+    return [0, starts[3], starts[5], starts[7], starts[9], starts[11], starts[14], starts[15], L]
+
+
+@pytest.mark.timeout(1500)
+def test_resnet50_full_size_eight_stages(gpu_lib):
+    """Full ResNet-50 at 224x224, 8 stages on one GPU (LOCAL transport), the SURVEY's 10-step
+    parity batch B = 16 (m = 2, b = 8), I-TiMePReSt EQ1; the oracle replays 2 mini-batches."""
+    layers, starts = ograph.resnet_layers()
+    compare(layers, resnet50_bounds(starts, len(layers)), 2, 8, 2, ost.I_VARIANT, ost.EQ1, mode="update")

@@ -36,6 +36,10 @@ def conv_flops_per_sample(layers):
     for l, sp in enumerate(layers):
         if sp["kind"] == "conv3":
             g = 2.0 * sp["h"] * sp["w"] * 9 * sp["cin"] * sp["cout"]
+        elif sp["kind"] == "conv":
+            ho = (sp["h"] + 2 * sp["p"] - sp["k"]) // sp["s"] + 1
+            wo = (sp["w"] + 2 * sp["p"] - sp["k"]) // sp["s"] + 1
+            g = 2.0 * ho * wo * sp["k"] * sp["k"] * sp["cin"] * sp["cout"]
         elif sp["kind"] == "linear":
             g = 2.0 * sp["in"] * sp["out"]
         else:
@@ -43,6 +47,12 @@ def conv_flops_per_sample(layers):
         f += g * (3 if l > 0 else 2)
     return f
 
+
+from oracle import graph as _graph  # noqa: E402  (layer-graph builder only; no oracle arithmetic runs)
+
+R50, R50_STARTS = _graph.resnet_layers()
+R50_BOUNDS = [0, R50_STARTS[3], R50_STARTS[5], R50_STARTS[7], R50_STARTS[9], R50_STARTS[11], R50_STARTS[14],
+              R50_STARTS[15], len(R50)]
 
 CONFIGS = {
     "C1 MLP 784-256-10 S=2 m=4 b=8": dict(dims=[784, 256, 10], bounds=[0, 1, 2], m=4, b=8, kind=1),
@@ -52,6 +62,8 @@ CONFIGS = {
     "C3 VGG-16 CIFAR S=4 B=128 (4 stages on 1 GPU)": dict(layers=vgg16_cifar(), bounds=[0, 6, 10, 14, 21], m=2,
                                                             b=64, kind=1),
     "C5 deep MLP S=1 B=2048": dict(dims=[4096] * 17 + [10], bounds=[0, 17], m=32, b=64, kind=0),
+    "C4 ResNet-50 S=1 B=256": dict(layers=R50, bounds=[0, len(R50)], m=4, b=64, kind=1),
+    "C4 ResNet-50 S=8 B=256 (8 stages on 1 GPU)": dict(layers=R50, bounds=R50_BOUNDS, m=4, b=64, kind=1),
 }
 
 
@@ -110,9 +122,12 @@ def run(name, c, variant, blend, epochs=3, epoch_mb=16, pool=4):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=None)
+    ap.add_argument("--only", default=None, help="substring filter on config names")
     a = ap.parse_args()
     res = {}
     for name, c in CONFIGS.items():
+        if a.only and a.only not in name:
+            continue
         for vn, v, bl in [("V", tps.TPS_V, tps.TPS_BLEND_EQ1), ("I-EQ1", tps.TPS_I, tps.TPS_BLEND_EQ1),
                           ("I-CONVEX", tps.TPS_I, tps.TPS_BLEND_CONVEX)]:
             if vn == "I-CONVEX" and len(c["bounds"]) == 2:
