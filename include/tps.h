@@ -153,7 +153,10 @@ typedef struct {
                                    backward comm of edge e (e+1 -> e)                 */
   int32_t device;               /* CUDA device ordinal                               */
   uint64_t seed;                /* synthetic-init seed (tps_init_weights_synthetic)  */
-  uint64_t compute_stream;      /* cudaStream_t to enqueue on; 0 => handle-owned     */
+  uint64_t compute_stream;      /* cudaStream_t to enqueue on; 0 => handle-owned.  A run
+                                   (tps_begin_run / tps_run_schedule*) reads its inputs after
+                                   all work already submitted to this stream (0: to the legacy
+                                   default stream) when the run begins                      */
   int32_t extra_recv_slot;      /* 1 => one extra input slot so the next forward's
                                    receive overlaps the backward (costs B·d_in·2 B)   */
   int32_t fuse_update;          /* 1 => the SGD/momentum update of each layer runs in the
@@ -318,6 +321,17 @@ tps_status tps_conv_gemm(int32_t mode, int32_t N, int32_t H, int32_t W, int32_t 
                          const void* A, const void* Wt, const void* W2, void* out, int32_t out_f32,
                          const float* bias, int32_t relu, float alpha, float beta, const void* mask,
                          uint64_t stream);
+
+/* ---- general convolution GEMMs (TMA im2col-mode loads; unit tests) ------------
+ * NHWC bf16 device tensors; k x k filter, stride, zero padding pad; Ho = (H+2pad-k)/stride+1.
+ * Ci % 64 == 0, Co % 64 == 0.  No bias / activation.
+ * mode 0 (forward): out[N·Ho·Wo, Co] = conv(X[N,H,W,Ci]; W[Co,k,k,Ci]) (bf16, or fp32 if out_f32).
+ * mode 1 (dgrad, k = 3, stride 1, pad 1): out[N·H·W, Ci] = alpha · conv_transpose(dY; W) (bf16).
+ * mode 2 (wgrad):   out[Co, k·k·Ci] (fp32) = dY[N·Ho·Wo, Co]ᵀ · im2col(X).
+ * mode 3 (dgrad, blended operand): as mode 1 with W = alpha·W + beta·W2 formed on load.       */
+tps_status tps_conv2d_gemm(int32_t mode, int32_t N, int32_t H, int32_t W, int32_t Ci, int32_t Co, int32_t k,
+                           int32_t stride, int32_t pad, const void* A, const void* Wt, const void* W2, void* out,
+                           int32_t out_f32, float alpha, float beta, uint64_t stream);
 
 /* ---- ResNet op kernels (unit tests; the pipeline calls the same kernels) --------
  * All tensors NHWC bf16 on the device unless stated; `stream` = cudaStream_t (0 = legacy).

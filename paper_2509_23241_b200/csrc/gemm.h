@@ -20,6 +20,9 @@ enum ConvKind { CONV_NONE = 0, CONV_FWD = 1, CONV_DGRAD = 2, CONV_WGRAD = 3 };
 // dgrad: dY (C = Co, also the K blocks of the flipped weight); wgrad: X (C = Ci).
 struct ConvGeom {
   int N, H, W, C;
+  // im2col != 0: the activation operand is read with TMA im2col-mode loads (any H, W; k x k
+  // filter, stride s, zero padding p; output Ho x Wo) instead of whole-row pixel boxes
+  int im2col, k, s, p, Ho, Wo;
 };
 
 struct GemmOperands {
@@ -46,7 +49,14 @@ struct GemmArgs {
   float* w; float* v; uint16_t* ver;
   float lr, mu, wd;
   ConvGeom cv;                // copied from GemmOperands by gemm_run
+  // split-K (weight gradients whose output tiles cannot fill the GPU): fp32 workspace of
+  // ws_floats floats supplied by the caller; gemm_run sets splits / kper and reduces
+  float* ws; int64_t ws_floats;
+  int splits, kper;           // set by gemm_run
 };
+
+// floats of split-K workspace gemm_run needs for this weight-gradient GEMM (0: no split)
+int64_t gemm_splitk_floats(int mode, int M, int N, int K, int ldo);
 
 enum GemmEpilogue { EPI_STORE = 0, EPI_SGD = 1 };
 

@@ -78,6 +78,15 @@ __device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int& mb
   nb = r / gm;
 }
 
+__device__ __forceinline__ void tile_split(int t, int num_m, int num_n, int num_k, int kper, int& mb, int& nb,
+                                           int& kb0, int& kb1) {
+  const int tiles = num_m * num_n;
+  const int ks = t / tiles;
+  tile_coords(t - ks * tiles, num_m, num_n, mb, nb);
+  kb0 = ks * kper;
+  kb1 = min(num_k, kb0 + kper);
+}
+
 __device__ __forceinline__ float bf16_bits_to_f32(uint32_t h) { return __uint_as_float(h << 16); }
 
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
@@ -114,7 +123,9 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
   const int num_m = (args.M + BM * CG - 1) / (BM * CG);
   const int num_n = (args.N + BN - 1) / BN;
   const int num_k = (args.K + BK - 1) / BK;
-  const int num_tiles = num_m * num_n;
+  // split-K (args.splits > 1, plain fp32 epilogue only): tile t covers K blocks
+  // [ks·kper, min(num_k, (ks+1)·kper)) of output tile t mod (num_m·num_n), ks = t / (num_m·num_n)
+  const int num_tiles = num_m * num_n * args.splits;
 
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&tmA);
@@ -149,11 +160,11 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int t = cid; t < num_tiles; t += ncl) {
-        int mb, nb;
-        tile_coords(t, num_m, num_n, mb, nb);
+        int mb, nb, kb0, kb1;
+        tile_split(t, num_m, num_n, num_k, args.kper, mb, nb, kb0, kb1);
         const int m0 = mb * BM * CG + static_cast<int>(rank) * BM;          // this CTA's 128 rows
         const int n0 = nb * BN + static_cast<int>(rank) * (BN / CG);       // this CTA's B share
-        for (int kb = 0; kb < num_k; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sA = stages + stage * C::STAGE_BYTES;
           uint8_t* sB = sA + A_BYTES;
@@ -168,8 +179,26 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
             if (CG == 2) ptx::tma_load_4d_cg2(dst, m, fb, c0, c1, c2, c3);
             else ptx::tma_load_4d(dst, m, &full[stage], c0, c1, c2, c3);
           };
+          auto ldi = [&](void* dst, const CUtensorMap* m, int c, int w, int h, int n, int ow, int oh) {
+            if (CG == 2)
+              ptx::tma_load_im2col_4d_cg2(dst, m, fb, c, w, h, n, static_cast<uint16_t>(ow), static_cast<uint16_t>(oh));
+            else
+              ptx::tma_load_im2col_4d(dst, m, &full[stage], c, w, h, n, static_cast<uint16_t>(ow),
+                                      static_cast<uint16_t>(oh));
+          };
           // ---- A tile: 128 rows x 64 K
-          if (CONV == CONV_FWD || CONV == CONV_DGRAD) {
+          if ((CONV == CONV_FWD || CONV == CONV_DGRAD) && args.cv.im2col) {
+            // im2col-mode TMA: K block kb = (filter tap, 64-channel block); the 128 output pixels
+            // of this M block are 128 consecutive receptive-field origins of the traversal,
+            // shifted by the tap (kw, kh); out-of-image taps read zeros (= the padding)
+            const ConvGeom& g = args.cv;
+            const int cpb = g.C / 64;
+            const int tap = kb / cpb, c0 = (kb - tap * cpb) * 64;
+            const int kh = tap / g.k, kw = tap - kh * g.k;
+            const int PQ = g.Ho * g.Wo;
+            const int n_img = m0 / PQ, rem = m0 - n_img * PQ, ho = rem / g.Wo, wo = rem - ho * g.Wo;
+            ldi(sA, &tmA, c0, wo * g.s - g.p, ho * g.s - g.p, n_img, kw, kh);
+          } else if (CONV == CONV_FWD || CONV == CONV_DGRAD) {
             // implicit im2col: K block kb = (kh, kw, 64-channel block); the 128 output pixels
             // of this M block form one (w, h, n) box of the NHWC input, shifted by (kh-1, kw-1);
             // TMA zero-fills the out-of-image halo (= the padding)
@@ -196,6 +225,19 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
             for (int i = 0; i < BN / CG / 64; ++i) {
               ld4(dB + i * 8192, &tmB, n0 + 64 * i, 2 - kw, 2 - kh, co0);
               if (BLEND) ld4(dB + C::B_BYTES + i * 8192, &tmB2, n0 + 64 * i, 2 - kw, 2 - kh, co0);
+            }
+          } else if (CONV == CONV_WGRAD && args.cv.im2col) {
+            // B = im2col(X): K block = 64 consecutive output pixels, column (kh, kw, ci)
+            const ConvGeom& g = args.cv;
+            const int PQ = g.Ho * g.Wo;
+            const int p0 = kb * BK;
+            const int n_img = p0 / PQ, rem = p0 - n_img * PQ, ho = rem / g.Wo, wo = rem - ho * g.Wo;
+#pragma unroll
+            for (int i = 0; i < BN / CG / 64; ++i) {
+              const int col = n0 + 64 * i;
+              const int tap = col / g.C, ci0 = col - tap * g.C;
+              const int kh = tap / g.k, kw = tap - kh * g.k;
+              ldi(dB + i * 8192, &tmB, ci0, wo * g.s - g.p, ho * g.s - g.p, n_img, kw, kh);
             }
           } else if (CONV == CONV_WGRAD) {
             // B = im2col(X): K block = 64 pixels (one (w,h,n) box), column (kh, kw, ci)
@@ -235,7 +277,9 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
         ptx::mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = 0; kb < num_k; ++kb) {
+        int mb_, nb_, kb0, kb1;
+        tile_split(t, num_m, num_n, num_k, args.kper, mb_, nb_, kb0, kb1);
+        for (int kb = kb0; kb < kb1; ++kb) {
           ptx::mbar_wait(&full[stage], phase);
           if (BLEND) ptx::mbar_wait(&xform[stage], phase);
           ptx::tc_fence_after();
@@ -249,8 +293,8 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
                                      : ptx::make_sdesc_sw128(a_addr + kk * 32, 16, 1024);
             const uint64_t bd = B_MN ? ptx::make_sdesc_sw128(b_addr + kk * 2048, 8192, 1024)
                                      : ptx::make_sdesc_sw128(b_addr + kk * 32, 16, 1024);
-            if (CG == 2) ptx::umma_f16_cg2(d_tmem, ad, bd, idesc, (kb | kk) != 0);
-            else ptx::umma_f16(d_tmem, ad, bd, idesc, (kb | kk) != 0);
+            if (CG == 2) ptx::umma_f16_cg2(d_tmem, ad, bd, idesc, (kb != kb0) || (kk != 0));
+            else ptx::umma_f16(d_tmem, ad, bd, idesc, (kb != kb0) || (kk != 0));
           }
           if (CG == 2) ptx::umma_commit_cg2_mc(&empty[stage], 0x3);
           else ptx::umma_commit(&empty[stage]);
@@ -366,8 +410,12 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
     constexpr int CPW = BN / 64;            // 32-column chunks per warp per tile
     int it = 0;
     for (int t = cid; t < num_tiles; t += ncl, ++it) {
-      int mb, nb;
-      tile_coords(t, num_m, num_n, mb, nb);
+      int mb, nb, kb0, kb1;
+      tile_split(t, num_m, num_n, num_k, args.kper, mb, nb, kb0, kb1);
+      // split-K partials go to slice ks of the fp32 workspace (same ld), reduced afterwards
+      void* const outp = args.splits > 1
+          ? static_cast<void*>(args.ws + static_cast<size_t>(kb0 / args.kper) * args.M * args.ldo)
+          : args.out;
       const int acc = it % C::ACC;
       const uint32_t acc_phase = (it / C::ACC) & 1;
       ptx::mbar_wait(&tmem_full[acc], acc_phase);
@@ -451,7 +499,7 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
           }
         }
         if (args.out_f32) {
-          float* op = reinterpret_cast<float*>(args.out) + static_cast<size_t>(grow) * args.ldo + gcol;
+          float* op = reinterpret_cast<float*>(outp) + static_cast<size_t>(grow) * args.ldo + gcol;
 #pragma unroll
           for (int ch = 0; ch < 4; ++ch) {
             if (ch < nchunk) {
@@ -461,7 +509,7 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
             }
           }
         } else {
-          __nv_bfloat16* op = reinterpret_cast<__nv_bfloat16*>(args.out) + static_cast<size_t>(grow) * args.ldo + gcol;
+          __nv_bfloat16* op = reinterpret_cast<__nv_bfloat16*>(outp) + static_cast<size_t>(grow) * args.ldo + gcol;
 #pragma unroll
           for (int ch = 0; ch < 4; ++ch) {
             if (ch < nchunk) {
@@ -583,6 +631,36 @@ bool make_tmap4(CUtensorMap* m, const void* base, const uint64_t (&d)[4], const 
   return r == CUDA_SUCCESS;
 }
 
+typedef CUresult (*EncodeIm2colFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const int*, const int*, cuuint32_t, cuuint32_t,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+// im2col-mode map of an NHWC bf16 tensor [N, H, W, C] for a k x k / stride s / pad p filter:
+// each load walks `pixels` receptive-field origins (W fastest, then H, then N) within the box
+// [-p, dim - 1 + p - (k - 1)] per spatial dim, stepping by s, 64 channels per pixel, 128B swizzle
+bool make_tmap_im2col(CUtensorMap* m, const void* base, const ConvGeom& g, int C, uint32_t pixels) {
+  static EncodeIm2colFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeIm2colFn>(p);
+    if (!fn) return false;
+  }
+  cuuint64_t dims[4] = {static_cast<cuuint64_t>(C), static_cast<cuuint64_t>(g.W), static_cast<cuuint64_t>(g.H),
+                        static_cast<cuuint64_t>(g.N)};
+  cuuint64_t strides[3] = {dims[0] * 2, dims[0] * dims[1] * 2, dims[0] * dims[1] * dims[2] * 2};
+  const int lower[2] = {-g.p, -g.p};                              // {W, H}
+  const int upper[2] = {g.p - (g.k - 1), g.p - (g.k - 1)};
+  cuuint32_t es[4] = {1, static_cast<cuuint32_t>(g.s), static_cast<cuuint32_t>(g.s), 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, lower, upper, 64,
+                  pixels, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 // (w, h, n) extent of a box holding `pixels` consecutive NHWC pixels (row-major n, h, w)
 bool pixel_box(int pixels, int H, int W, uint32_t (&box)[4]) {
   const int P = H * W;
@@ -596,6 +674,18 @@ bool pixel_box(int pixels, int H, int W, uint32_t (&box)[4]) {
   }
   box[0] = 64;
   return true;
+}
+
+__global__ void splitk_reduce(const float4* __restrict__ ws, float4* __restrict__ out, int64_t n4, int splits) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float4 a = ws[i];
+    for (int k = 1; k < splits; ++k) {
+      const float4 b = ws[i + k * n4];
+      a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+    }
+    out[i] = a;
+  }
 }
 
 }  // namespace
@@ -633,7 +723,7 @@ cudaError_t launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  const int tiles = ((args.M + BM * CG - 1) / (BM * CG)) * ((args.N + BN - 1) / BN);
+  const int tiles = ((args.M + BM * CG - 1) / (BM * CG)) * ((args.N + BN - 1) / BN) * std::max(1, args.splits);
   const int clusters = std::max(1, std::min(tiles, num_sms() / CG));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(clusters * CG);
@@ -654,13 +744,35 @@ cudaError_t launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap
 
 struct Tiling {
   int cg, bn;
+  int splits = 1, kper = 0;
 };
 
 // Pick the CTA-pair mode and tile width.  Pairs (256 x BN tiles, cta_group::2) cut operand
 // traffic per SM by a third; they are used when M fills at least two 128-row blocks and the
 // pair grid still covers the chip.  Env TPS_GEMM_CG=1 forces single-CTA tiles.
-Tiling pick_tiling(int M, int N, int mode, bool sgd) {
+Tiling pick_tiling(int M, int N, int K, int mode, bool sgd) {
   if (mode == GEMM_DGRAD_BLEND || mode == GEMM_CONV_DGRAD_BLEND) return {1, 128};
+  const int sms0 = num_sms();
+  static int no_split = -1;
+  if (no_split < 0) {
+    const char* e = std::getenv("TPS_NO_SPLITK");
+    no_split = (e && e[0] == '1') ? 1 : 0;
+  }
+  if ((mode == GEMM_WGRAD || mode == GEMM_CONV_WGRAD) && !sgd && !no_split) {
+    // weight gradients of convolutions: small M x N, K = every pixel of the batch.  When the
+    // output tiles cannot fill the GPU, split K across CTAs (fp32 partials + ordered reduce)
+    const int bn = N <= 64 ? 64 : (N <= 128 ? 128 : 256);
+    const int tiles = ((M + BM - 1) / BM) * ((N + bn - 1) / bn);
+    const int num_k = (K + BK - 1) / BK;
+    if (tiles < sms0 * 3 / 4 && num_k >= 16) {
+      int splits = std::min({(sms0 + tiles - 1) / tiles, num_k / 8, 64});
+      if (splits > 1) {
+        const int kper = (num_k + splits - 1) / splits;
+        splits = (num_k + kper - 1) / kper;          // every split non-empty
+        return {1, bn, splits, kper};
+      }
+    }
+  }
   const int sms = num_sms();
   static int force_cg = -1;
   if (force_cg < 0) {
@@ -718,7 +830,13 @@ cudaError_t gemm_run(int mode, const GemmOperands& op, const GemmArgs& args_in, 
   GemmArgs args = args_in;
   if (args.M <= 0 || args.N <= 0 || args.K <= 0) return cudaSuccess;
   const bool sgd = ((mode == GEMM_WGRAD || mode == GEMM_CONV_WGRAD) && args.epi == EPI_SGD);
-  Tiling tl = pick_tiling(args.M, args.N, mode, sgd);
+  Tiling tl = pick_tiling(args.M, args.N, args.K, mode, sgd);
+  if (tl.splits > 1 &&
+      (!args.ws || args.ws_floats < static_cast<int64_t>(tl.splits) * args.M * args.ldo || !args.out_f32 ||
+       args.ldo != args.N))
+    tl.splits = 1;                                   // no workspace supplied: one pass over K
+  args.splits = tl.splits;
+  args.kper = tl.splits > 1 ? tl.kper : (args.K + BK - 1) / BK;
   CUtensorMap ta, tb, tb2;
   bool ok = true;
   if (mode >= GEMM_CONV_FWD) {
@@ -728,8 +846,32 @@ cudaError_t gemm_run(int mode, const GemmOperands& op, const GemmArgs& args_in, 
     const uint64_t act_dims[4] = {static_cast<uint64_t>(g.C), static_cast<uint64_t>(g.W),
                                   static_cast<uint64_t>(g.H), static_cast<uint64_t>(g.N)};
     uint32_t box128[4], box64[4];
-    if (!pixel_box(128, g.H, g.W, box128) || !pixel_box(64, g.H, g.W, box64)) return cudaErrorInvalidValue;
-    if (mode == GEMM_CONV_FWD) {
+    if (g.im2col) {
+      if (g.k < 1 || g.s < 1 || g.s > 8 || g.p < 0 || g.Ho < 1 || g.Wo < 1) return cudaErrorInvalidValue;
+      if ((mode == GEMM_CONV_DGRAD || mode == GEMM_CONV_DGRAD_BLEND) && (g.k != 3 || g.s != 1 || g.p != 1))
+        return cudaErrorInvalidValue;
+    } else if (!pixel_box(128, g.H, g.W, box128) || !pixel_box(64, g.H, g.W, box64)) {
+      return cudaErrorInvalidValue;
+    }
+    if (g.im2col) {
+      if (mode == GEMM_CONV_FWD) {
+        ok &= make_tmap_im2col(&ta, op.A, g, g.C, 128);                             // X (NHWC)
+        ok &= make_tmap(&tb, op.B, args.N, args.K, op.ldb, tl.bn / tl.cg);         // W [Co, k·k·Ci]
+        tb2 = tb;
+      } else if (mode == GEMM_CONV_DGRAD || mode == GEMM_CONV_DGRAD_BLEND) {
+        ok &= make_tmap_im2col(&ta, op.A, g, g.C, 128);                             // dY (NHWC, C = Co)
+        const uint64_t wd[4] = {static_cast<uint64_t>(op.Cw), 3, 3, static_cast<uint64_t>(g.C)};
+        const uint32_t wb[4] = {64, 1, 1, 64};
+        ok &= make_tmap4(&tb, op.B, wd, wb);
+        if (mode == GEMM_CONV_DGRAD_BLEND) ok &= make_tmap4(&tb2, op.B2, wd, wb);
+        else tb2 = tb;
+        if (op.Cw % 64) return cudaErrorInvalidValue;
+      } else {
+        ok &= make_tmap(&ta, op.A, args.K, args.M, op.lda, 64);                     // dY [N·Ho·Wo, Co]
+        ok &= make_tmap_im2col(&tb, op.B, g, g.C, 64);                              // X (NHWC)
+        tb2 = tb;
+      }
+    } else if (mode == GEMM_CONV_FWD) {
       ok &= make_tmap4(&ta, op.A, act_dims, box128);                              // X (NHWC)
       ok &= make_tmap(&tb, op.B, args.N, args.K, op.ldb, tl.bn / tl.cg);           // W [Co, 9Ci]
       tb2 = tb;
@@ -771,21 +913,35 @@ cudaError_t gemm_run(int mode, const GemmOperands& op, const GemmArgs& args_in, 
   }
   if (!ok) return cudaErrorInvalidValue;
   if (bn_out) *bn_out = tl.bn * 10 + tl.cg;
+  cudaError_t e = cudaErrorInvalidValue;
   switch (mode) {
-    case GEMM_FWD: return dispatch<0, 0, 0>(tl, ta, tb, tb2, em, args, st);
-    case GEMM_DGRAD: return dispatch<0, 1, 0>(tl, ta, tb, tb2, em, args, st);
+    case GEMM_FWD: e = dispatch<0, 0, 0>(tl, ta, tb, tb2, em, args, st); break;
+    case GEMM_DGRAD: e = dispatch<0, 1, 0>(tl, ta, tb, tb2, em, args, st); break;
     case GEMM_WGRAD:
-      if (sgd) return dispatch<1, 1, 1>(tl, ta, tb, tb2, em, args, st);
-      return dispatch<1, 1, 0>(tl, ta, tb, tb2, em, args, st);
-    case GEMM_DGRAD_BLEND: return launch<128, 0, 1, 1, 0, 1>(ta, tb, tb2, em, args, st);
-    case GEMM_CONV_FWD: return dispatch<0, 0, 0, CONV_FWD>(tl, ta, tb, tb2, em, args, st);
-    case GEMM_CONV_DGRAD: return dispatch<0, 1, 0, CONV_DGRAD>(tl, ta, tb, tb2, em, args, st);
-    case GEMM_CONV_DGRAD_BLEND: return launch<128, 0, 1, 1, 0, 1, CONV_DGRAD>(ta, tb, tb2, em, args, st);
+      e = sgd ? dispatch<1, 1, 1>(tl, ta, tb, tb2, em, args, st) : dispatch<1, 1, 0>(tl, ta, tb, tb2, em, args, st);
+      break;
+    case GEMM_DGRAD_BLEND: e = launch<128, 0, 1, 1, 0, 1>(ta, tb, tb2, em, args, st); break;
+    case GEMM_CONV_FWD: e = dispatch<0, 0, 0, CONV_FWD>(tl, ta, tb, tb2, em, args, st); break;
+    case GEMM_CONV_DGRAD: e = dispatch<0, 1, 0, CONV_DGRAD>(tl, ta, tb, tb2, em, args, st); break;
+    case GEMM_CONV_DGRAD_BLEND: e = launch<128, 0, 1, 1, 0, 1, CONV_DGRAD>(ta, tb, tb2, em, args, st); break;
     case GEMM_CONV_WGRAD:
-      if (sgd) return dispatch<1, 1, 1, CONV_WGRAD>(tl, ta, tb, tb2, em, args, st);
-      return dispatch<1, 1, 0, CONV_WGRAD>(tl, ta, tb, tb2, em, args, st);
+      e = sgd ? dispatch<1, 1, 1, CONV_WGRAD>(tl, ta, tb, tb2, em, args, st)
+              : dispatch<1, 1, 0, CONV_WGRAD>(tl, ta, tb, tb2, em, args, st);
+      break;
   }
-  return cudaErrorInvalidValue;
+  if (e != cudaSuccess || tl.splits <= 1) return e;
+  // ordered reduction of the split-K partials: out = Σ_ks ws[ks] (deterministic)
+  const int64_t n4 = static_cast<int64_t>(args.M) * args.ldo / 4;
+  const int blocks = static_cast<int>(std::min<int64_t>((n4 + 255) / 256, static_cast<int64_t>(num_sms()) * 8));
+  splitk_reduce<<<blocks, 256, 0, st>>>(reinterpret_cast<const float4*>(args.ws), reinterpret_cast<float4*>(args.out),
+                                        n4, tl.splits);
+  return cudaGetLastError();
+}
+
+int64_t gemm_splitk_floats(int mode, int M, int N, int K, int ldo) {
+  if (M <= 0 || N <= 0 || K <= 0) return 0;
+  const Tiling tl = pick_tiling(M, N, K, mode, false);
+  return tl.splits > 1 ? static_cast<int64_t>(tl.splits) * M * ldo : 0;
 }
 
 }  // namespace tps

@@ -166,6 +166,8 @@ struct tps_pipeline {
   uint16_t* patches = nullptr;
   float* dpatches = nullptr;
   double* bn_scr = nullptr;
+  float* splitk_ws = nullptr;               // split-K partials of weight-gradient GEMMs
+  int64_t splitk_floats = 0;
   std::vector<void*> allocs;
 
   // ---- memory accounting
@@ -188,6 +190,8 @@ struct tps_pipeline {
   bool own_cs = false;
   cudaStream_t s_fin = nullptr, s_fout = nullptr, s_bin = nullptr, s_bout = nullptr;
   cudaStream_t s_upd = nullptr;                        // optimizer stream (overlaps the next GEMMs)
+  cudaStream_t caller = cudaStreamLegacy;              // whose prior work a run's inputs depend on
+  cudaEvent_t ev_caller = nullptr;
   std::vector<cudaEvent_t> ev_grad_ready, ev_upd_done;  // per layer
   std::vector<cudaEvent_t> ev_fwd_ready, ev_fwd_sent;  // [2 * ng]
   std::vector<cudaEvent_t> ev_act_free;                // [A0]
@@ -299,7 +303,10 @@ tps_status run_gemm(tps_pipeline* p, int mode, const tps::GemmOperands& op, cons
     tl.b = p->ev_pool.back(); p->ev_pool.pop_back();
     CUDA_OK(cudaEventRecord(tl.a, p->cs));
   }
-  CUDA_OK(tps::gemm_run(mode, op, args, p->cs));
+  tps::GemmArgs a2 = args;
+  a2.ws = p->splitk_ws;
+  a2.ws_floats = p->splitk_floats;
+  CUDA_OK(tps::gemm_run(mode, op, a2, p->cs));
   p->launches += 1;
   if (p->profiling) {
     CUDA_OK(cudaEventRecord(tl.b, p->cs));
@@ -517,9 +524,9 @@ tps_status graph_forward(tps_pipeline* p, int64_t j, int a0, int cnt, int64_t v)
         ga.alpha = 1.f; ga.xa = 1.f; ga.out = out; ga.ldo = L.Co;
         ga.M = nr * L.hw_out; ga.N = L.Co; ga.K = L.Kp;
         const uint16_t* Wv = L.ver[v % p->R];
-        if (L.conv_mode == 1) {
+        if (L.conv_mode == 1 || L.conv_mode == 3) {
           tps::GemmOperands op{X, 0, Wv, L.Kp, nullptr};
-          op.cv = tps::ConvGeom{nr, L.H, L.Wd, L.Ci};
+          op.cv = tps::ConvGeom{nr, L.H, L.Wd, L.Ci, 1, L.k, L.st, L.pad, L.Ho, L.Wo};
           TPS_TRY(run_gemm(p, tps::GEMM_CONV_FWD, op, ga, 0));
         } else {
           const uint16_t* A = X;
@@ -622,6 +629,9 @@ tps_status graph_backward(tps_pipeline* p, int64_t j, int64_t v_used, int64_t vl
   };
   for (int k = nl - 1; k >= 0; --k) {
     Layer& L = p->layers[k];
+    // the previous update of this layer (optimizer stream) must be done: it reads dW / db,
+    // which this backward rewrites, and (V) it writes the weights this backward reads
+    if (L.has_w()) CUDA_OK(cudaStreamWaitEvent(p->cs, p->ev_upd_done[k], 0));
     const uint16_t* g;
     if (k == nl - 1) {
       g = G_last;
@@ -642,7 +652,7 @@ tps_status graph_backward(tps_pipeline* p, int64_t j, int64_t v_used, int64_t vl
           ga.alpha = 1.f; ga.xa = 1.f; ga.xb = 0.f;
           const int ldg = head ? L.Np : L.Co;
           tps::GemmOperands op{g, ldg, L.ver[v_used % p->R], L.Kp, nullptr};
-          const bool expl = !head && L.conv_mode == 2;
+          const bool expl = !head && (L.conv_mode == 2 || L.conv_mode == 3);
           if (expl) {      // patch gradient (fp32), then col2im adds it into the target
             ga.out = p->dpatches; ga.out_f32 = 1; ga.ldo = L.Kp;
             ga.M = B * L.hw_out; ga.N = L.Kp; ga.K = L.Co;
@@ -652,7 +662,7 @@ tps_status graph_backward(tps_pipeline* p, int64_t j, int64_t v_used, int64_t vl
           }
           int mode = tps::GEMM_DGRAD;
           if (!head && L.conv_mode == 1) {
-            op.cv = tps::ConvGeom{B, L.H, L.Wd, L.Co};
+            op.cv = tps::ConvGeom{B, L.H, L.Wd, L.Co, 1, 3, 1, 1, L.H, L.Wd};
             op.Cw = L.Ci;
             ga.K = 9 * L.Co;
             mode = tps::GEMM_CONV_DGRAD;
@@ -675,10 +685,10 @@ tps_status graph_backward(tps_pipeline* p, int64_t j, int64_t v_used, int64_t vl
         // weight gradient dW[Np, Kp] = Gᵀ·(input or its patches)
         tps::GemmArgs ga{};
         ga.M = L.Np; ga.N = L.Kp; ga.out = L.dW; ga.ldo = L.Kp; ga.out_f32 = 1; ga.alpha = 1.f; ga.xa = 1.f;
-        if (!head && L.conv_mode == 1) {
+        if (!head && (L.conv_mode == 1 || L.conv_mode == 3)) {
           ga.K = B * L.hw_out;
           tps::GemmOperands op{g, L.Np, X, 0, nullptr};
-          op.cv = tps::ConvGeom{B, L.H, L.Wd, L.Ci};
+          op.cv = tps::ConvGeom{B, L.H, L.Wd, L.Ci, 1, L.k, L.st, L.pad, L.Ho, L.Wo};
           TPS_TRY(run_gemm(p, tps::GEMM_CONV_WGRAD, op, ga, 2));
         } else {
           const uint16_t* Xb = X;
@@ -865,6 +875,9 @@ tps_status do_backward(tps_pipeline* p, int64_t j, int staleness) {
   if (p->graph) TPS_TRY(graph_backward(p, j, v_used, vl, vn, alpha, beta, blend_on_load, G));
   for (int k = (p->graph ? -1 : nl - 1); k >= 0; --k) {
     Layer& Lk = p->layers[k];
+    // the previous update of this layer must be done: it reads dW / db (rewritten below) and,
+    // for V, writes the weights this backward reads
+    if (Lk.has_w()) CUDA_OK(cudaStreamWaitEvent(p->cs, p->ev_upd_done[k], 0));
     const uint16_t* X = (k == 0) ? p->act[slot0][0] : p->act[slot][k];
     // input gradient first: it must read this layer's weights before a fused update rewrites them
     uint16_t* dst = nullptr;
@@ -985,6 +998,11 @@ tps_status do_update(tps_pipeline* p, int64_t j) {
 tps_status begin_run(tps_pipeline* p, int64_t first, int64_t n) {
   if (n <= 0 || first < 0) return fail(TPS_E_INVALID_ARG, "bad run [%lld, +%lld)", (long long)first, (long long)n);
   if (p->in_run) return fail(TPS_E_ORDER, "stage %d: previous run not finished", p->s);
+  // inputs of the run (device pools, labels) may have been produced on the caller's stream:
+  // the handle's streams start after everything already submitted there (the configured
+  // compute stream, else the legacy default stream)
+  CUDA_OK(cudaEventRecord(p->ev_caller, p->caller));
+  for (cudaStream_t st : {p->cs, p->s_fin, p->s_upd}) CUDA_OK(cudaStreamWaitEvent(st, p->ev_caller, 0));
   build_order(p->S, p->s, p->m, p->g, first, n, &p->order);
   p->pos = 0;
   p->run_first = first;
@@ -1170,9 +1188,14 @@ tps_status init_graph(tps_pipeline* p, const tps_config* c, int lb, int le) {
       L.in = sp.k * sp.k * L.Ci; L.out = L.Co; L.Np = L.Co;
       if (L.k == 1 && L.st == 1 && L.pad == 0 && L.Ci % 16 == 0) {
         L.conv_mode = 0; L.Kp = L.Ci;
-      } else if (L.k == 3 && L.st == 1 && L.pad == 1 && L.Ci % 64 == 0 && L.Co % 64 == 0 &&
-                 tps::conv_implicit_ok(L.H, L.Wd)) {
-        L.conv_mode = 1; L.Kp = 9 * L.Ci;
+      } else if (L.k == 3 && L.st == 1 && L.pad == 1 && L.Ci % 64 == 0 && L.Co % 64 == 0) {
+        L.conv_mode = 1; L.Kp = 9 * L.Ci;     // implicit GEMM: TMA im2col-mode loads, all three GEMMs
+      } else if (L.Ci % 64 == 0 && L.Co % 64 == 0) {
+        // strided conv: implicit forward / weight gradient; the input gradient of a strided conv
+        // is a patch-gradient GEMM + col2im
+        L.conv_mode = 3; L.Kp = L.k * L.k * L.Ci;
+        if (!(p->first && L.src == -1))
+          dpatch_elems = std::max(dpatch_elems, static_cast<int64_t>(p->B) * L.hw_out * L.Kp);
       } else {
         L.conv_mode = 2; L.Kp = pad16(L.in);
         const int64_t pe = static_cast<int64_t>(p->B) * L.hw_out * L.Kp;
@@ -1402,9 +1425,27 @@ tps_status tps_pipeline_init(const tps_config* c, tps_pipeline** out) {
 
   }
   const int nl = p->nlayers();
+  {
+    // split-K workspace for the weight-gradient GEMMs whose output tiles cannot fill the GPU
+    int64_t wsf = 0;
+    for (const Layer& L : p->layers) {
+      if (!L.has_w() || L.kind == TPS_LAYER_BN) continue;
+      const bool implicit = (L.kind == TPS_LAYER_CONV3X3 && !L.im2col) ||
+                            (L.kind == TPS_LAYER_CONV && (L.conv_mode == 1 || L.conv_mode == 3));
+      const int K = p->B * (L.kind == TPS_LAYER_LINEAR ? 1 : L.hw_out);
+      wsf = std::max(wsf, tps::gemm_splitk_floats(implicit ? tps::GEMM_CONV_WGRAD : tps::GEMM_WGRAD, L.Np, L.Kp, K, L.Kp));
+    }
+    if (!p->fuse_update || p->graph) {
+      const tps_status ws_st = alloc_t(p, &p->splitk_ws, wsf, &p->mem_optim);
+      if (ws_st != TPS_OK) return cleanup(ws_st);
+      p->splitk_floats = wsf;
+    }
+  }
   // streams and events
+  p->ev_caller = new_event();
   if (c->compute_stream) {
     p->cs = reinterpret_cast<cudaStream_t>(c->compute_stream);
+    p->caller = p->cs;
   } else {
     if (cudaStreamCreateWithFlags(&p->cs, cudaStreamNonBlocking) != cudaSuccess) return cleanup(fail(TPS_E_CUDA, "stream create"));
     p->own_cs = true;
@@ -1476,7 +1517,7 @@ tps_status tps_pipeline_destroy(tps_pipeline* p) {
   for (auto e : p->ev_upd_done) kill_ev(e);
   for (auto e : p->ev_pool) kill_ev(e);
   for (auto& t : p->timed) { kill_ev(t.a); kill_ev(t.b); }
-  for (cudaEvent_t e : {p->ev_recv, p->ev_gout_ready, p->ev_gin_ready, p->ev_gin_free[0], p->ev_gin_free[1],
+  for (cudaEvent_t e : {p->ev_caller, p->ev_recv, p->ev_gout_ready, p->ev_gin_ready, p->ev_gin_free[0], p->ev_gin_free[1],
                         p->ev_bwd_sent[0], p->ev_bwd_sent[1]})
     kill_ev(e);
   for (cudaStream_t s : {p->s_fin, p->s_fout, p->s_bin, p->s_bout, p->s_upd})
@@ -1671,16 +1712,19 @@ tps_status tps_set_weights(tps_pipeline* p, int32_t layer, const float* w, const
   Layer& L = p->layers[layer];
   const size_t rowb = static_cast<size_t>(L.in) * 4, ldb = static_cast<size_t>(L.Kp) * 4;
   const size_t n = static_cast<size_t>(L.Np) * L.Kp;
+  // stream-ordered on the compute stream: a synchronous cudaMemcpy from pageable memory may
+  // return before its DMA lands, and the legacy stream does not order the handle's
+  // non-blocking streams
   if (w) {
-    CUDA_OK(cudaMemset(L.W, 0, n * 4));
-    CUDA_OK(cudaMemcpy2D(L.W, ldb, w, rowb, rowb, L.out, cudaMemcpyHostToDevice));
+    CUDA_OK(cudaMemsetAsync(L.W, 0, n * 4, p->cs));
+    CUDA_OK(cudaMemcpy2DAsync(L.W, ldb, w, rowb, rowb, L.out, cudaMemcpyHostToDevice, p->cs));
   }
   if (b && L.b) {
-    CUDA_OK(cudaMemset(L.b, 0, static_cast<size_t>(L.Np) * 4));
-    CUDA_OK(cudaMemcpy(L.b, b, static_cast<size_t>(L.out) * 4, cudaMemcpyHostToDevice));
+    CUDA_OK(cudaMemsetAsync(L.b, 0, static_cast<size_t>(L.Np) * 4, p->cs));
+    CUDA_OK(cudaMemcpyAsync(L.b, b, static_cast<size_t>(L.out) * 4, cudaMemcpyHostToDevice, p->cs));
   }
-  if (L.mW) CUDA_OK(cudaMemset(L.mW, 0, n * 4));
-  if (L.mb) CUDA_OK(cudaMemset(L.mb, 0, static_cast<size_t>(L.Np) * 4));
+  if (L.mW) CUDA_OK(cudaMemsetAsync(L.mW, 0, n * 4, p->cs));
+  if (L.mb) CUDA_OK(cudaMemsetAsync(L.mb, 0, static_cast<size_t>(L.Np) * 4, p->cs));
   if (L.kind == TPS_LAYER_BN)
     CUDA_OK(cudaMemcpyAsync(L.verf[p->latest % p->R], L.W, n * 4, cudaMemcpyDeviceToDevice, p->cs));
   else
@@ -1838,6 +1882,64 @@ tps_status tps_partition(int32_t L, const double* pb, const double* ab, const do
   return TPS_OK;
 }
 
+namespace {
+// raw GEMM entry points: a stream-ordered split-K workspace when the shape splits
+tps_status gemm_with_ws(int mode, const tps::GemmOperands& op, tps::GemmArgs ga, cudaStream_t st) {
+  const int64_t wsf = ga.out_f32 ? tps::gemm_splitk_floats(mode, ga.M, ga.N, ga.K, ga.ldo) : 0;
+  void* ws = nullptr;
+  if (wsf > 0) CUDA_OK(cudaMallocAsync(&ws, static_cast<size_t>(wsf) * 4, st));
+  ga.ws = static_cast<float*>(ws);
+  ga.ws_floats = wsf;
+  const cudaError_t e = tps::gemm_run(mode, op, ga, st);
+  if (ws) CUDA_OK(cudaFreeAsync(ws, st));
+  CUDA_OK(e);
+  return TPS_OK;
+}
+
+tps_status op_prologue() {
+  int dev = 0;
+  CUDA_OK(cudaGetDevice(&dev));
+  return check_arch(dev);
+}
+}  // namespace
+
+tps_status tps_conv2d_gemm(int32_t mode, int32_t N, int32_t H, int32_t W, int32_t Ci, int32_t Co, int32_t k,
+                           int32_t stride, int32_t pad, const void* A, const void* Wt, const void* W2, void* out,
+                           int32_t out_f32, float alpha, float beta, uint64_t stream) {
+  if (mode < 0 || mode > 3 || N < 1 || H < 1 || W < 1 || k < 1 || stride < 1 || stride > 8 || pad < 0 || !A || !Wt ||
+      !out)
+    return fail(TPS_E_INVALID_ARG, "bad conv operands");
+  if (Ci % 64 || Co % 64) return fail(TPS_E_INVALID_ARG, "Ci and Co must be multiples of 64");
+  if ((mode == 1 || mode == 3) && (k != 3 || stride != 1 || pad != 1)) return fail(TPS_E_INVALID_ARG, "dgrad: 3x3/1/1 only");
+  if (mode == 3 && !W2) return fail(TPS_E_INVALID_ARG, "blend mode needs W2");
+  const int Ho = (H + 2 * pad - k) / stride + 1, Wo = (W + 2 * pad - k) / stride + 1;
+  if (Ho < 1 || Wo < 1) return fail(TPS_E_INVALID_ARG, "empty conv output");
+  TPS_TRY(op_prologue());
+  tps::GemmOperands op{};
+  tps::GemmArgs ga{};
+  ga.out = out; ga.out_f32 = out_f32; ga.alpha = 1.f; ga.xa = 1.f; ga.xb = 0.f;
+  int gm;
+  if (mode == 0) {
+    op = tps::GemmOperands{A, 0, Wt, k * k * Ci, nullptr};
+    op.cv = tps::ConvGeom{N, H, W, Ci, 1, k, stride, pad, Ho, Wo};
+    ga.M = N * Ho * Wo; ga.N = Co; ga.K = k * k * Ci; ga.ldo = Co;
+    gm = tps::GEMM_CONV_FWD;
+  } else if (mode == 2) {
+    op = tps::GemmOperands{A, Co, Wt, 0, nullptr};
+    op.cv = tps::ConvGeom{N, H, W, Ci, 1, k, stride, pad, Ho, Wo};
+    ga.M = Co; ga.N = k * k * Ci; ga.K = N * Ho * Wo; ga.ldo = k * k * Ci; ga.out_f32 = 1;
+    gm = tps::GEMM_CONV_WGRAD;
+  } else {
+    op = tps::GemmOperands{A, Co, Wt, 9 * Ci, mode == 3 ? W2 : nullptr};
+    op.cv = tps::ConvGeom{N, H, W, Co, 1, 3, 1, 1, H, W};
+    op.Cw = Ci;
+    ga.M = N * H * W; ga.N = Ci; ga.K = 9 * Co; ga.ldo = Ci;
+    if (mode == 3) { ga.xa = alpha; ga.xb = beta; } else { ga.alpha = alpha; }
+    gm = mode == 3 ? tps::GEMM_CONV_DGRAD_BLEND : tps::GEMM_CONV_DGRAD;
+  }
+  return gemm_with_ws(gm, op, ga, reinterpret_cast<cudaStream_t>(stream));
+}
+
 tps_status tps_conv_gemm(int32_t mode, int32_t N, int32_t H, int32_t W, int32_t Ci, int32_t Co, const void* A,
                          const void* Wt, const void* W2, void* out, int32_t out_f32, const float* bias, int32_t relu,
                          float alpha, float beta, const void* mask, uint64_t stream) {
@@ -1871,17 +1973,9 @@ tps_status tps_conv_gemm(int32_t mode, int32_t N, int32_t H, int32_t W, int32_t 
     if (mode == 3) { ga.xa = alpha; ga.xb = beta; } else { ga.alpha = alpha; }
     gm = mode == 3 ? tps::GEMM_CONV_DGRAD_BLEND : tps::GEMM_CONV_DGRAD;
   }
-  CUDA_OK(tps::gemm_run(gm, op, ga, reinterpret_cast<cudaStream_t>(stream)));
-  return TPS_OK;
+  return gemm_with_ws(gm, op, ga, reinterpret_cast<cudaStream_t>(stream));
 }
 
-namespace {
-tps_status op_prologue() {
-  int dev = 0;
-  CUDA_OK(cudaGetDevice(&dev));
-  return check_arch(dev);
-}
-}  // namespace
 
 tps_status tps_im2col(const void* X, void* P, int32_t N, int32_t H, int32_t W, int32_t C, int32_t k, int32_t stride,
                       int32_t pad, int32_t ldp, uint64_t stream) {
@@ -1970,8 +2064,7 @@ tps_status tps_gemm(int32_t mode, int32_t M, int32_t N, int32_t K, const void* A
   ga.M = M; ga.N = N; ga.K = K; ga.out = out; ga.ldo = ldo; ga.out_f32 = out_f32; ga.bias = bias; ga.relu = relu;
   ga.alpha = mode == 3 ? 1.f : alpha; ga.xa = alpha; ga.xb = beta;
   ga.mask = static_cast<const uint16_t*>(mask); ga.ldm = ldm;
-  CUDA_OK(tps::gemm_run(mode, op, ga, reinterpret_cast<cudaStream_t>(stream)));
-  return TPS_OK;
+  return gemm_with_ws(mode, op, ga, reinterpret_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

@@ -32,7 +32,7 @@ EXPORTS = [
     "tps_init_weights_synthetic", "tps_get_losses", "tps_get_trace", "tps_clear_trace", "tps_memory_stats",
     "tps_set_profiling", "tps_kernel_stats", "tps_launch_count", "tps_fill_synthetic", "tps_gemm",
     "tps_conv_gemm", "tps_partition", "tps_im2col", "tps_col2im", "tps_bn_forward", "tps_bn_backward",
-    "tps_pool_op",
+    "tps_pool_op", "tps_conv2d_gemm",
 ]
 TPS_LAYER_LINEAR, TPS_LAYER_CONV3X3, TPS_LAYER_MAXPOOL2 = 0, 1, 2
 TPS_LAYER_CONV, TPS_LAYER_BN, TPS_LAYER_MAXPOOL3, TPS_LAYER_AVGPOOL = 3, 4, 5, 6
@@ -116,6 +116,7 @@ def lib() -> C.CDLL:
             "tps_bn_forward": (I32, [P, P, P, P, P, P, P, I32, I32, I32, I32, U64]),
             "tps_bn_backward": (I32, [P, P, P, P, P, P, P, F, F, I32, I32, I32, I32, P, P, P, P, U64]),
             "tps_pool_op": (I32, [I32, P, P, P, I32, I32, I32, I32, U64]),
+            "tps_conv2d_gemm": (I32, [I32, I32, I32, I32, I32, I32, I32, I32, I32, P, P, P, P, I32, F, F, U64]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -174,6 +175,12 @@ def conv_gemm(mode, N, H, W, Ci, Co, A, Wt, out, out_f32=0, bias=None, relu=0, a
               W2=None, stream: int = 0) -> None:
     check(lib().tps_conv_gemm(mode, N, H, W, Ci, Co, ptr(A), ptr(Wt), ptr(W2), ptr(out), out_f32, ptr(bias), relu,
                               alpha, beta, ptr(mask), stream))
+
+
+def conv2d_gemm(mode, N, H, W, Ci, Co, k, stride, pad, A, Wt, out, out_f32=0, alpha=1.0, beta=0.0, W2=None,
+                stream: int = 0) -> None:
+    check(lib().tps_conv2d_gemm(mode, N, H, W, Ci, Co, k, stride, pad, ptr(A), ptr(Wt), ptr(W2), ptr(out), out_f32,
+                                alpha, beta, stream))
 
 
 def im2col(X, P, N, H, W, C, k, stride, pad, ldp, stream: int = 0) -> None:

@@ -131,3 +131,54 @@ def test_image_net_parity_with_oracle(gpu_lib, name):
             wr = ref.weights[l].reshape(w.shape)
             assert weight_rel_err(w, wr) <= 5e-3, (name, l)
             assert layer_rel_err(w, bb, wr, ref.biases[l]) <= 5e-3, (name, l)
+
+
+# ---- TMA im2col-mode convolutions (ResNet-50 geometry: any H, W; stride 2; 1x1 / 3x3) ----------
+IM2COL = [  # N, H, W, Ci, Co, k, stride, pad
+    (2, 56, 56, 64, 64, 3, 1, 1), (2, 28, 28, 128, 128, 3, 1, 1), (3, 7, 7, 64, 128, 3, 1, 1),
+    (2, 14, 14, 256, 64, 3, 1, 1), (2, 56, 56, 128, 128, 3, 2, 1), (2, 28, 28, 256, 128, 1, 2, 0),
+    (3, 7, 9, 64, 64, 3, 2, 1), (2, 32, 32, 64, 64, 3, 1, 1),
+]
+
+
+def conv_ref(X, Wt, s, p):
+    y = F.conv2d(X.double().permute(0, 3, 1, 2), Wt.double().permute(0, 3, 1, 2), stride=s, padding=p)
+    return y.permute(0, 2, 3, 1)
+
+
+@pytest.mark.parametrize("N,H,W,Ci,Co,k,s,p", IM2COL)
+def test_conv2d_im2col_forward_and_wgrad(gpu_lib, N, H, W, Ci, Co, k, s, p):
+    g = torch.Generator(device="cuda").manual_seed(N * H + Ci + k)
+    X = torch.randn(N, H, W, Ci, generator=g, device="cuda").to(torch.bfloat16)
+    Wt = (torch.randn(Co, k, k, Ci, generator=g, device="cuda") * (k * k * Ci) ** -0.5).to(torch.bfloat16)
+    Ho, Wo = (H + 2 * p - k) // s + 1, (W + 2 * p - k) // s + 1
+    out = torch.full((N * Ho * Wo, Co), float("nan"), device="cuda", dtype=torch.bfloat16)
+    tps.conv2d_gemm(0, N, H, W, Ci, Co, k, s, p, X, Wt, out)
+    dY = torch.randn(N, Ho, Wo, Co, generator=g, device="cuda").to(torch.bfloat16)
+    dW = torch.full((Co, k * k * Ci), float("nan"), device="cuda", dtype=torch.float32)
+    tps.conv2d_gemm(2, N, H, W, Ci, Co, k, s, p, dY, X, dW, 1)
+    torch.cuda.synchronize()
+    close(out, conv_ref(X, Wt, s, p).reshape(N * Ho * Wo, Co), k * k * Ci)
+    ref = torch.nn.grad.conv2d_weight(X.double().permute(0, 3, 1, 2), (Co, Ci, k, k),
+                                      dY.double().permute(0, 3, 1, 2), stride=s, padding=p)
+    ref = ref.permute(0, 2, 3, 1).reshape(Co, k * k * Ci)
+    K = N * Ho * Wo
+    torch.testing.assert_close(dW.double(), ref, rtol=1e-5, atol=2e-6 * K ** 0.5 * ref.abs().max().item())
+
+
+@pytest.mark.parametrize("N,H,W,Ci,Co,k,s,p", [c for c in IM2COL if c[5:] == (3, 1, 1)])
+@pytest.mark.parametrize("blend", [False, True])
+def test_conv2d_im2col_dgrad(gpu_lib, N, H, W, Ci, Co, k, s, p, blend):
+    g = torch.Generator(device="cuda").manual_seed(5 * N + W + Co)
+    dY = torch.randn(N, H, W, Co, generator=g, device="cuda").to(torch.bfloat16)
+    Wt = (torch.randn(Co, 3, 3, Ci, generator=g, device="cuda") * (9 * Co) ** -0.5).to(torch.bfloat16)
+    W2 = (torch.randn(Co, 3, 3, Ci, generator=g, device="cuda") * (9 * Co) ** -0.5).to(torch.bfloat16)
+    out = torch.full((N * H * W, Ci), float("nan"), device="cuda", dtype=torch.bfloat16)
+    a, b = (0.7, 0.3) if blend else (0.8948, 0.0)
+    tps.conv2d_gemm(3 if blend else 1, N, H, W, Ci, Co, 3, 1, 1, dY, Wt, out, 0, a, b, W2=W2 if blend else None)
+    torch.cuda.synchronize()
+    Wr = ((torch.tensor(a) * Wt.float()) + (torch.tensor(b) * W2.float())).to(torch.bfloat16) if blend else Wt
+    ref = torch.nn.grad.conv2d_input((N, Ci, H, W), Wr.double().permute(0, 3, 1, 2), dY.double().permute(0, 3, 1, 2),
+                                     padding=1)
+    ref = ref.permute(0, 2, 3, 1).reshape(N * H * W, Ci) * (1.0 if blend else a)
+    close(out, ref, 9 * Co)

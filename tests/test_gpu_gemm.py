@@ -69,8 +69,11 @@ def test_dgrad_mn_major_weight_alpha_mask(gpu_lib, M, N, K, alpha):
     close_bf16(out, ref, K)
 
 
-@pytest.mark.parametrize("M,N,K", [(256, 784, 32), (16, 256, 32), (136, 264, 300), (4096, 4096, 512), (1024, 512, 2048)])
+@pytest.mark.parametrize("M,N,K", [(256, 784, 32), (16, 256, 32), (136, 264, 300), (4096, 4096, 512), (1024, 512, 2048),
+                                   (64, 64, 65536), (128, 576, 50176), (256, 2304, 12544), (72, 136, 40000)])
 def test_wgrad_both_mn_major(gpu_lib, M, N, K):
+    """The last four are ResNet-style weight gradients (few output tiles, K = every pixel of the
+    batch): they take the split-K path (fp32 partials per K range, ordered reduction)."""
     # dW [M, N] = Gᵀ·X with G stored [K, M] and X stored [K, N]; fp32 out
     g = torch.Generator(device="cuda").manual_seed(M + N + K * 5)
     G = bf16_rand(K, M, gen=g)
