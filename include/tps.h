@@ -351,7 +351,10 @@ tps_status tps_conv2d_gemm(int32_t mode, int32_t N, int32_t H, int32_t W, int32_
  * tps_pool_op: op 0 maxpool3 forward  out = max over the 3x3/2/1 window of a (= X);
  *              op 1 maxpool3 backward out = dX from a = X and b = dY (first maximum, Z15);
  *              op 2 avgpool forward   out[N, C] = mean over H·W of a;
- *              op 3 avgpool backward  out[N,H,W,C] = b[N, C] / (H·W).
+ *              op 3 avgpool backward  out[N,H,W,C] = b[N, C] / (H·W);
+ *              op 4 maxpool3 forward recording taps: out = Y, b = uint8 tap (0..8, row-major
+ *                   in the window) of the first maximum per output (written), C % 8 == 0;
+ *              op 5 maxpool3 backward from recorded taps: a = taps, b = dY, out = dX.
  * Errors: TPS_E_INVALID_ARG for null/ill-sized arguments, TPS_E_ARCH off sm_100,
  *         TPS_E_CUDA on launch failure.                                                  */
 tps_status tps_im2col(const void* X, void* P, int32_t N, int32_t H, int32_t W, int32_t C, int32_t k,

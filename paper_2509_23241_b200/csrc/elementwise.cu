@@ -339,28 +339,6 @@ __global__ void im2col3x3_kernel(const uint16_t* __restrict__ X, uint16_t* __res
 }
 
 // ------------------------------------------------------------------ ResNet helpers (NHWC, bf16)
-// general patches: P[(n,ho,wo), (kh,kw,c)] for a k x k / stride s / pad p convolution
-__global__ void im2col_kernel(const uint16_t* __restrict__ X, uint16_t* __restrict__ P, int N, int H, int W, int C,
-                              int k, int s, int p, int Ho, int Wo, int ldp) {
-  const int64_t total = static_cast<int64_t>(N) * Ho * Wo * ldp;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int col = static_cast<int>(i % ldp);
-    const int64_t pix = i / ldp;
-    uint16_t v = 0;
-    if (col < k * k * C) {
-      const int khw = col / C, c = col - khw * C;
-      const int wo = static_cast<int>(pix % Wo);
-      const int64_t t = pix / Wo;
-      const int ho = static_cast<int>(t % Ho);
-      const int64_t n = t / Ho;
-      const int hh = ho * s + khw / k - p, ww = wo * s + khw % k - p;
-      if (hh >= 0 && hh < H && ww >= 0 && ww < W) v = X[((n * H + hh) * W + ww) * C + c];
-    }
-    P[i] = v;
-  }
-}
-
 // adjoint of im2col (gather form, fixed (kh, kw) order, fp32 sum of fp32 patch gradients):
 // dX[n,h,w,c] = Σ dP[(n,(h+p-kh)/s,(w+p-kw)/s), (kh,kw,c)] over valid (kh, kw); optional bf16 addend
 __global__ void col2im_kernel(const float* __restrict__ dP, uint16_t* __restrict__ dX, const uint16_t* __restrict__ add,
@@ -634,6 +612,375 @@ __global__ void add_bf16_kernel(uint16_t* __restrict__ out, const uint16_t* __re
     out[i] = f2bf(bf2f(out[i]) + bf2f(add[i]));
 }
 
+// ------------------------------------------------------------------ vectorised ResNet kernels
+// 8 channels (16 bytes) per thread; used when C % 8 == 0 (every ResNet-50 layer)
+__device__ __forceinline__ void unpack8(const uint4& v, float (&f)[8]) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int e = 0; e < 8; ++e) f[e] = bf2f((w[e >> 1] >> ((e & 1) * 16)) & 0xFFFFu);
+}
+
+__device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
+  uint4 o;
+  o.x = static_cast<uint32_t>(f2bf(f[0])) | (static_cast<uint32_t>(f2bf(f[1])) << 16);
+  o.y = static_cast<uint32_t>(f2bf(f[2])) | (static_cast<uint32_t>(f2bf(f[3])) << 16);
+  o.z = static_cast<uint32_t>(f2bf(f[4])) | (static_cast<uint32_t>(f2bf(f[5])) << 16);
+  o.w = static_cast<uint32_t>(f2bf(f[6])) | (static_cast<uint32_t>(f2bf(f[7])) << 16);
+  return o;
+}
+
+__device__ __forceinline__ void load8f(const float* p, float (&f)[8]) {
+  const float4 a = *reinterpret_cast<const float4*>(p), b = *reinterpret_cast<const float4*>(p + 4);
+  f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w; f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+}
+
+__global__ void bn_apply_vec(const uint4* __restrict__ x, const uint4* __restrict__ res, uint4* __restrict__ y,
+                             const float* __restrict__ gamma, const float* __restrict__ beta,
+                             const float* __restrict__ mean, const float* __restrict__ invstd, int64_t nvec, int C8,
+                             int seg_rows, int relu) {
+  const int C = C8 * 8;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < nvec;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / C8;
+    const int c0 = static_cast<int>(i - r * C8) * 8;
+    const int sc = static_cast<int>(r / seg_rows) * C + c0;
+    float xv[8], g[8], bt[8], m[8], is[8], v[8];
+    unpack8(x[i], xv);
+    load8f(gamma + c0, g);
+    load8f(beta + c0, bt);
+    load8f(mean + sc, m);
+    load8f(invstd + sc, is);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) v[e] = g[e] * ((xv[e] - m[e]) * is[e]) + bt[e];
+    if (res) {
+      float rv[8];
+      unpack8(res[i], rv);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) v[e] += rv[e];
+    }
+    if (relu) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) v[e] = fmaxf(v[e], 0.f);
+    }
+    y[i] = pack8(v);
+  }
+}
+
+// per (segment, chunk) partial sums over 8 channels per thread, fp64:
+//   MODE 0 (statistics): Σx, Σx²;  MODE 1 (backward): Σdy', Σdy'·x̂ (dy' = dy ⊙ [y > 0] if relu)
+// block: tx = min(C8, 256) channel groups x ty = 256 / tx rows; grid (ceil(C8/tx), chunks, segs)
+template <int MODE>
+__global__ void __launch_bounds__(256) bn_partial_vec(const uint4* __restrict__ a, const uint4* __restrict__ yv,
+                                                      const uint4* __restrict__ xv, const float* __restrict__ mean,
+                                                      const float* __restrict__ invstd, int seg_rows, int C8,
+                                                      int chunks, int relu, double* __restrict__ part) {
+  extern __shared__ double red[];            // [ty][tx][16]
+  const int tx = min(C8, 256), ty = blockDim.x / tx;
+  const int lx = threadIdx.x % tx, ly = threadIdx.x / tx;
+  const int cg = blockIdx.x * tx + lx;       // channel group
+  const int seg = blockIdx.z;
+  const int C = C8 * 8;
+  const int64_t r0 = static_cast<int64_t>(seg) * seg_rows;
+  const int per = (seg_rows + chunks - 1) / chunks;
+  const int lo = blockIdx.y * per, hi = min(seg_rows, lo + per);
+  double s1[8], s2[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) s1[e] = s2[e] = 0.0;
+  if (cg < C8) {
+    float m[8], is[8];
+    if (MODE == 1) {
+      load8f(mean + seg * C + cg * 8, m);
+      load8f(invstd + seg * C + cg * 8, is);
+    }
+    for (int r = lo + ly; r < hi; r += ty) {
+      const int64_t o = (r0 + r) * C8 + cg;
+      float v[8];
+      unpack8(a[o], v);
+      if (MODE == 0) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          s1[e] += v[e];
+          s2[e] += static_cast<double>(v[e]) * v[e];
+        }
+      } else {
+        float yy[8], xx[8];
+        unpack8(xv[o], xx);
+        if (relu) unpack8(yv[o], yy);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const double d = (relu && !(yy[e] > 0.f)) ? 0.0 : static_cast<double>(v[e]);
+          s1[e] += d;
+          s2[e] += d * ((static_cast<double>(xx[e]) - m[e]) * is[e]);
+        }
+      }
+    }
+  }
+  double* mine = red + (static_cast<size_t>(ly) * tx + lx) * 16;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    mine[e] = s1[e];
+    mine[8 + e] = s2[e];
+  }
+  __syncthreads();
+  if (ly == 0 && cg < C8) {
+    for (int yy = 1; yy < ty; ++yy) {
+      const double* o = red + (static_cast<size_t>(yy) * tx + lx) * 16;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        s1[e] += o[e];
+        s2[e] += o[8 + e];
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const size_t o = (static_cast<size_t>(seg) * chunks + blockIdx.y) * C + cg * 8 + e;
+      part[2 * o] = s1[e];
+      part[2 * o + 1] = s2[e];
+    }
+  }
+}
+
+// backward coefficients per (segment, channel), packed float4 {γ_r·invstd, Σdy'/m, Σdy'x̂/m, mean}
+// with γ_r = a·γ_stash + b·γ_latest; and dγ, dβ summed over segments
+// one warp per channel: lanes stride the chunks, shuffle tree (fixed order), lane 0 writes
+__global__ void bn_bwd_coef(const double* __restrict__ part, int chunks, int C, int segs, int seg_rows,
+                            const float* __restrict__ mean, const float* __restrict__ invstd,
+                            const float* __restrict__ gs, const float* __restrict__ gl, float ga, float gb,
+                            float4* __restrict__ coef, float* __restrict__ dgamma, float* __restrict__ dbeta) {
+  const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (c >= C) return;
+  const float g = __fadd_rn(__fmul_rn(ga, gs[c]), __fmul_rn(gb, gl[c]));
+  double tg = 0.0, tb = 0.0;
+  for (int seg = 0; seg < segs; ++seg) {
+    double s1 = 0.0, s2 = 0.0;
+    for (int k = lane; k < chunks; k += 32) {
+      const size_t o = (static_cast<size_t>(seg) * chunks + k) * C + c;
+      s1 += part[2 * o];
+      s2 += part[2 * o + 1];
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      s1 += __shfl_xor_sync(0xffffffffu, s1, off);
+      s2 += __shfl_xor_sync(0xffffffffu, s2, off);
+    }
+    if (lane) continue;
+    tb += s1;
+    tg += s2;
+    const int sc = seg * C + c;
+    coef[sc] = make_float4(g * invstd[sc], static_cast<float>(s1 / seg_rows), static_cast<float>(s2 / seg_rows),
+                           mean[sc]);
+  }
+  if (lane) return;
+  dgamma[c] = static_cast<float>(tg);
+  dbeta[c] = static_cast<float>(tb);
+}
+
+__global__ void bn_bwd_apply_vec(const uint4* __restrict__ dy, const uint4* __restrict__ yv,
+                                 const uint4* __restrict__ xv, const float4* __restrict__ coef,
+                                 const float* __restrict__ invstd, int64_t nvec, int C8, int seg_rows, int relu,
+                                 uint4* __restrict__ dx, uint4* __restrict__ dres) {
+  const int C = C8 * 8;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < nvec;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / C8;
+    const int c0 = static_cast<int>(i - r * C8) * 8;
+    const int sc = static_cast<int>(r / seg_rows) * C + c0;
+    float d[8], xx[8], is[8], o[8];
+    unpack8(dy[i], d);
+    unpack8(xv[i], xx);
+    if (relu) {
+      float yy[8];
+      unpack8(yv[i], yy);
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        if (!(yy[e] > 0.f)) d[e] = 0.f;
+    }
+    if (dres) dres[i] = pack8(d);
+    load8f(invstd + sc, is);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float4 k = coef[sc + e];
+      const float xh = (xx[e] - k.w) * is[e];
+      o[e] = k.x * (d[e] - k.y - xh * k.z);
+    }
+    dx[i] = pack8(o);
+  }
+}
+
+// 3x3/2/1 max pool over 8 channels per thread, recording the first-max tap (0..8) per output
+__global__ void maxpool3_fwd_vec(const uint4* __restrict__ X, uint4* __restrict__ Y, uint2* __restrict__ idx, int N,
+                                 int H, int W, int C8, int Ho, int Wo) {
+  const int64_t total = static_cast<int64_t>(N) * Ho * Wo * C8;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int cv = static_cast<int>(i % C8);
+    int64_t t = i / C8;
+    const int wo = static_cast<int>(t % Wo);
+    t /= Wo;
+    const int ho = static_cast<int>(t % Ho);
+    const int64_t n = t / Ho;
+    float best[8];
+    uint32_t bits[8], arg[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) { best[e] = -INFINITY; bits[e] = 0; arg[e] = 0; }
+    for (int kh = 0; kh < 3; ++kh) {
+      const int h = 2 * ho + kh - 1;
+      if (h < 0 || h >= H) continue;
+      for (int kw = 0; kw < 3; ++kw) {
+        const int w = 2 * wo + kw - 1;
+        if (w < 0 || w >= W) continue;
+        const uint4 v = X[((n * H + h) * W + w) * C8 + cv];
+        const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const uint32_t hb = (wv[e >> 1] >> ((e & 1) * 16)) & 0xFFFFu;
+          const float f = bf2f(hb);
+          if (f > best[e]) { best[e] = f; bits[e] = hb; arg[e] = kh * 3 + kw; }
+        }
+      }
+    }
+    uint4 o;
+    o.x = bits[0] | (bits[1] << 16); o.y = bits[2] | (bits[3] << 16);
+    o.z = bits[4] | (bits[5] << 16); o.w = bits[6] | (bits[7] << 16);
+    Y[i] = o;
+    idx[i] = make_uint2(arg[0] | (arg[1] << 8) | (arg[2] << 16) | (arg[3] << 24),
+                        arg[4] | (arg[5] << 8) | (arg[6] << 16) | (arg[7] << 24));
+  }
+}
+
+// gradient in gather form from the recorded taps: dX[n,h,w,c] = Σ dY of windows whose first max
+// is (h, w), windows in (ho, wo) order
+__global__ void maxpool3_bwd_vec(const uint2* __restrict__ idx, const uint4* __restrict__ dY, uint4* __restrict__ dX,
+                                 int N, int H, int W, int C8, int Ho, int Wo) {
+  const int64_t total = static_cast<int64_t>(N) * H * W * C8;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int cv = static_cast<int>(i % C8);
+    int64_t t = i / C8;
+    const int w = static_cast<int>(t % W);
+    t /= W;
+    const int h = static_cast<int>(t % H);
+    const int64_t n = t / H;
+    float acc[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+    for (int ho = max(0, h / 2 - 1); ho <= min(Ho - 1, (h + 1) / 2); ++ho) {
+      const int kh = h - (2 * ho - 1);
+      if (kh < 0 || kh > 2) continue;
+      for (int wo = max(0, w / 2 - 1); wo <= min(Wo - 1, (w + 1) / 2); ++wo) {
+        const int kw = w - (2 * wo - 1);
+        if (kw < 0 || kw > 2) continue;
+        const uint32_t tap = kh * 3 + kw;
+        const int64_t o = ((n * Ho + ho) * Wo + wo) * C8 + cv;
+        const uint2 a = idx[o];
+        const uint32_t av[2] = {a.x, a.y};
+        float g[8];
+        unpack8(dY[o], g);
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+          if (((av[e >> 2] >> ((e & 3) * 8)) & 0xFFu) == tap) acc[e] += g[e];
+      }
+    }
+    dX[i] = pack8(acc);
+  }
+}
+
+// patch gradients back to the image, 4 channels per thread (C % 4 == 0)
+__global__ void col2im_vec4(const float* __restrict__ dP, uint2* __restrict__ dX, const uint2* __restrict__ add, int N,
+                            int H, int W, int C, int k, int s, int p, int Ho, int Wo, int ldp) {
+  const int C4 = C / 4;
+  const int64_t total = static_cast<int64_t>(N) * H * W * C4;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int c = static_cast<int>(i % C4) * 4;
+    int64_t t = i / C4;
+    const int w = static_cast<int>(t % W);
+    t /= W;
+    const int h = static_cast<int>(t % H);
+    const int64_t n = t / H;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int kh = 0; kh < k; ++kh) {
+      const int hy = h + p - kh;
+      if (hy < 0 || hy % s) continue;
+      const int ho = hy / s;
+      if (ho >= Ho) continue;
+      for (int kw = 0; kw < k; ++kw) {
+        const int wy = w + p - kw;
+        if (wy < 0 || wy % s) continue;
+        const int wo = wy / s;
+        if (wo >= Wo) continue;
+        const float4 v = *reinterpret_cast<const float4*>(
+            dP + ((n * Ho + ho) * Wo + wo) * static_cast<int64_t>(ldp) + (kh * k + kw) * C + c);
+        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+      }
+    }
+    if (add) {
+      const uint2 a = add[i];
+      acc.x += bf2f(a.x & 0xFFFFu); acc.y += bf2f(a.x >> 16); acc.z += bf2f(a.y & 0xFFFFu); acc.w += bf2f(a.y >> 16);
+    }
+    dX[i] = make_uint2(static_cast<uint32_t>(f2bf(acc.x)) | (static_cast<uint32_t>(f2bf(acc.y)) << 16),
+                       static_cast<uint32_t>(f2bf(acc.z)) | (static_cast<uint32_t>(f2bf(acc.w)) << 16));
+  }
+}
+
+// explicit patches, 8 consecutive columns per thread (one 16-byte store), ldp % 8 == 0
+__global__ void im2col_vec8(const uint16_t* __restrict__ X, uint4* __restrict__ P, int H, int W, int C, int k, int s,
+                            int p, int Ho, int Wo, int ldp8, int64_t nvec) {
+  const int kkC = k * k * C;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < nvec;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / ldp8;
+    const int col0 = static_cast<int>(i - r * ldp8) * 8;
+    const int wo = static_cast<int>(r % Wo);
+    const int64_t t = r / Wo;
+    const int ho = static_cast<int>(t % Ho);
+    const int64_t n = t / Ho;
+    const uint16_t* xb = X + n * H * W * static_cast<int64_t>(C);
+    int tap = col0 / C, c = col0 - tap * C;
+    int kh = tap / k, kw = tap - kh * k;
+    uint32_t v[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      uint32_t val = 0;
+      if (col0 + e < kkC) {
+        const int hh = ho * s + kh - p, ww = wo * s + kw - p;
+        if (hh >= 0 && hh < H && ww >= 0 && ww < W) val = xb[(hh * W + ww) * C + c];
+      }
+      v[e] = val;
+      if (++c == C) {
+        c = 0;
+        if (++kw == k) { kw = 0; ++kh; }
+      }
+    }
+    P[i] = make_uint4(v[0] | (v[1] << 16), v[2] | (v[3] << 16), v[4] | (v[5] << 16), v[6] | (v[7] << 16));
+  }
+}
+
+// explicit patches, one output pixel row per block iteration (32-bit index math per element)
+__global__ void im2col_rows(const uint16_t* __restrict__ X, uint16_t* __restrict__ P, int N, int H, int W, int C,
+                            int k, int s, int p, int Ho, int Wo, int ldp, int64_t rows) {
+  const int kkC = k * k * C;
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+    const int wo = static_cast<int>(r % Wo);
+    const int64_t t = r / Wo;
+    const int ho = static_cast<int>(t % Ho);
+    const int64_t n = t / Ho;
+    const uint16_t* xb = X + n * H * W * static_cast<int64_t>(C);
+    uint16_t* pr = P + r * ldp;
+    for (int col = threadIdx.x; col < ldp; col += blockDim.x) {
+      uint16_t v = 0;
+      if (col < kkC) {
+        const int tap = col / C, c = col - tap * C;
+        const int kh = tap / k, kw = tap - kh * k;
+        const int hh = ho * s + kh - p, ww = wo * s + kw - p;
+        if (hh >= 0 && hh < H && ww >= 0 && ww < W) v = xb[(hh * W + ww) * C + c];
+      }
+      pr[col] = v;
+    }
+  }
+}
+
 uint64_t host_mix64(uint64_t x) {
   uint64_t z = x + 0x9E3779B97F4A7C15ull;
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
@@ -727,9 +1074,17 @@ cudaError_t launch_im2col3x3(const uint16_t* X, uint16_t* P, int N, int H, int W
 cudaError_t launch_im2col(const uint16_t* X, uint16_t* P, int N, int H, int W, int C, int k, int s, int p, int ldp,
                           cudaStream_t st) {
   const int Ho = (H + 2 * p - k) / s + 1, Wo = (W + 2 * p - k) / s + 1;
-  const int64_t total = static_cast<int64_t>(N) * Ho * Wo * ldp;
-  if (total <= 0) return cudaSuccess;
-  im2col_kernel<<<grid_for(total, 256), 256, 0, st>>>(X, P, N, H, W, C, k, s, p, Ho, Wo, ldp);
+  const int64_t rows = static_cast<int64_t>(N) * Ho * Wo;
+  if (rows <= 0) return cudaSuccess;
+  if (ldp % 8 == 0) {
+    const int64_t nvec = rows * (ldp / 8);
+    im2col_vec8<<<grid_for(nvec, 256), 256, 0, st>>>(X, reinterpret_cast<uint4*>(P), H, W, C, k, s, p, Ho, Wo, ldp / 8,
+                                                     nvec);
+    return cudaGetLastError();
+  }
+  const int threads = ldp >= 256 ? 256 : (ldp >= 128 ? 128 : 64);
+  const int blocks = static_cast<int>(std::min<int64_t>(rows, 148LL * 16));
+  im2col_rows<<<blocks, threads, 0, st>>>(X, P, N, H, W, C, k, s, p, Ho, Wo, ldp, rows);
   return cudaGetLastError();
 }
 
@@ -738,7 +1093,13 @@ cudaError_t launch_col2im(const float* dP, uint16_t* dX, const uint16_t* add, in
   const int Ho = (H + 2 * p - k) / s + 1, Wo = (W + 2 * p - k) / s + 1;
   const int64_t total = static_cast<int64_t>(N) * H * W * C;
   if (total <= 0) return cudaSuccess;
-  col2im_kernel<<<grid_for(total, 256), 256, 0, st>>>(dP, dX, add, N, H, W, C, k, s, p, Ho, Wo, ldp);
+  if (C % 4 == 0 && ldp % 4 == 0) {
+    col2im_vec4<<<grid_for(total / 4, 256), 256, 0, st>>>(dP, reinterpret_cast<uint2*>(dX),
+                                                          reinterpret_cast<const uint2*>(add), N, H, W, C, k, s, p, Ho,
+                                                          Wo, ldp);
+  } else {
+    col2im_kernel<<<grid_for(total, 256), 256, 0, st>>>(dP, dX, add, N, H, W, C, k, s, p, Ho, Wo, ldp);
+  }
   return cudaGetLastError();
 }
 
@@ -752,10 +1113,22 @@ cudaError_t launch_bn_forward(const uint16_t* x, const uint16_t* res, uint16_t* 
                               const float* beta, float* mean, float* invstd, int segs, int seg_rows, int C, int relu,
                               double* scratch, cudaStream_t st) {
   const int chunks = bn_chunks(seg_rows);
+  const int64_t rows = static_cast<int64_t>(segs) * seg_rows;
+  if (C % 8 == 0) {
+    const int C8 = C / 8, tx = std::min(C8, 256);
+    dim3 grid((C8 + tx - 1) / tx, chunks, segs);
+    bn_partial_vec<0><<<grid, tx * (256 / tx), 256 * 16 * sizeof(double), st>>>(reinterpret_cast<const uint4*>(x), nullptr,
+                                                                     nullptr, nullptr, nullptr, seg_rows, C8, chunks,
+                                                                     0, scratch);
+    bn_stats_final<<<(segs * C + 255) / 256, 256, 0, st>>>(scratch, chunks, C, seg_rows, segs, mean, invstd, 1e-5f);
+    bn_apply_vec<<<grid_for(rows * C8, 256), 256, 0, st>>>(
+        reinterpret_cast<const uint4*>(x), reinterpret_cast<const uint4*>(res), reinterpret_cast<uint4*>(y), gamma,
+        beta, mean, invstd, rows * C8, C8, seg_rows, relu);
+    return cudaGetLastError();
+  }
   dim3 grid((C + 31) / 32, chunks, segs);
   bn_stats_partial<<<grid, dim3(32, 8), 0, st>>>(x, seg_rows, C, chunks, scratch);
   bn_stats_final<<<(segs * C + 255) / 256, 256, 0, st>>>(scratch, chunks, C, seg_rows, segs, mean, invstd, 1e-5f);
-  const int64_t rows = static_cast<int64_t>(segs) * seg_rows;
   bn_apply_kernel<<<grid_for(rows * C, 256), 256, 0, st>>>(x, res, y, gamma, beta, mean, invstd, rows, C, seg_rows, relu);
   return cudaGetLastError();
 }
@@ -766,6 +1139,21 @@ cudaError_t launch_bn_backward(const uint16_t* dy, const uint16_t* y, const uint
                                float* dbeta, double* scratch, cudaStream_t st) {
   const int chunks = bn_chunks(seg_rows);
   double* sums = scratch + static_cast<int64_t>(segs) * chunks * C * 2;
+  if (C % 8 == 0) {
+    const int C8 = C / 8, tx = std::min(C8, 256);
+    const int64_t rows = static_cast<int64_t>(segs) * seg_rows;
+    dim3 grid((C8 + tx - 1) / tx, chunks, segs);
+    bn_partial_vec<1><<<grid, tx * (256 / tx), 256 * 16 * sizeof(double), st>>>(
+        reinterpret_cast<const uint4*>(dy), reinterpret_cast<const uint4*>(y), reinterpret_cast<const uint4*>(x), mean,
+        invstd, seg_rows, C8, chunks, relu, scratch);
+    float4* coef = reinterpret_cast<float4*>(sums);   // segs·C float4 = the sums region
+    bn_bwd_coef<<<(C * 32 + 255) / 256, 256, 0, st>>>(scratch, chunks, C, segs, seg_rows, mean, invstd, gs, gl, ga,
+                                                      gb, coef, dgamma, dbeta);
+    bn_bwd_apply_vec<<<grid_for(rows * C8, 256), 256, 0, st>>>(
+        reinterpret_cast<const uint4*>(dy), reinterpret_cast<const uint4*>(y), reinterpret_cast<const uint4*>(x), coef,
+        invstd, rows * C8, C8, seg_rows, relu, reinterpret_cast<uint4*>(dx), reinterpret_cast<uint4*>(dres));
+    return cudaGetLastError();
+  }
   dim3 grid((C + 31) / 32, chunks, segs);
   bn_bwd_partial<<<grid, dim3(32, 8), 0, st>>>(dy, y, x, mean, invstd, seg_rows, C, chunks, relu, scratch);
   bn_bwd_final<<<(C + 255) / 256, 256, 0, st>>>(scratch, chunks, C, segs, sums, dgamma, dbeta);
@@ -789,6 +1177,29 @@ cudaError_t launch_maxpool3_bwd(const uint16_t* X, const uint16_t* dY, uint16_t*
   const int64_t total = static_cast<int64_t>(N) * H * W * C;
   if (total <= 0) return cudaSuccess;
   maxpool3_bwd_kernel<<<grid_for(total, 256), 256, 0, st>>>(X, dY, dX, N, H, W, C, Ho, Wo);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_maxpool3_fwd_idx(const uint16_t* X, uint16_t* Y, uint8_t* idx, int N, int H, int W, int C,
+                                    cudaStream_t st) {
+  if (C % 8) return cudaErrorInvalidValue;
+  const int Ho = (H - 1) / 2 + 1, Wo = (W - 1) / 2 + 1;
+  const int64_t total = static_cast<int64_t>(N) * Ho * Wo * (C / 8);
+  if (total <= 0) return cudaSuccess;
+  maxpool3_fwd_vec<<<grid_for(total, 256), 256, 0, st>>>(reinterpret_cast<const uint4*>(X), reinterpret_cast<uint4*>(Y),
+                                                         reinterpret_cast<uint2*>(idx), N, H, W, C / 8, Ho, Wo);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_maxpool3_bwd_idx(const uint8_t* idx, const uint16_t* dY, uint16_t* dX, int N, int H, int W, int C,
+                                    cudaStream_t st) {
+  if (C % 8) return cudaErrorInvalidValue;
+  const int Ho = (H - 1) / 2 + 1, Wo = (W - 1) / 2 + 1;
+  const int64_t total = static_cast<int64_t>(N) * H * W * (C / 8);
+  if (total <= 0) return cudaSuccess;
+  maxpool3_bwd_vec<<<grid_for(total, 256), 256, 0, st>>>(reinterpret_cast<const uint2*>(idx),
+                                                         reinterpret_cast<const uint4*>(dY), reinterpret_cast<uint4*>(dX),
+                                                         N, H, W, C / 8, Ho, Wo);
   return cudaGetLastError();
 }
 

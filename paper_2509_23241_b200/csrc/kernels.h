@@ -64,6 +64,12 @@ cudaError_t launch_bn_backward(const uint16_t* dy, const uint16_t* y, const uint
 cudaError_t launch_maxpool3_fwd(const uint16_t* X, uint16_t* Y, int N, int H, int W, int C, cudaStream_t st);
 cudaError_t launch_maxpool3_bwd(const uint16_t* X, const uint16_t* dY, uint16_t* dX, int N, int H, int W, int C,
                                 cudaStream_t st);
+// 3x3/2/1 max pool recording the first-max tap (uint8 [N, Ho, Wo, C]) and its gradient from
+// the recorded taps (C % 8 == 0)
+cudaError_t launch_maxpool3_fwd_idx(const uint16_t* X, uint16_t* Y, uint8_t* idx, int N, int H, int W, int C,
+                                    cudaStream_t st);
+cudaError_t launch_maxpool3_bwd_idx(const uint8_t* idx, const uint16_t* dY, uint16_t* dX, int N, int H, int W, int C,
+                                    cudaStream_t st);
 cudaError_t launch_avgpool_fwd(const uint16_t* X, uint16_t* Y, int N, int HW, int C, cudaStream_t st);
 cudaError_t launch_avgpool_bwd(const uint16_t* dY, uint16_t* dX, int N, int HW, int C, cudaStream_t st);
 cudaError_t launch_add_bf16(uint16_t* out, const uint16_t* add, int64_t n, cudaStream_t st);

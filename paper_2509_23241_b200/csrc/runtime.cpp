@@ -107,6 +107,7 @@ struct Layer {
   int conv_mode = 0;                  // CONV: 0 plain GEMM (1x1/s1), 1 implicit 3x3, 2 explicit patches
   std::vector<float*> verf;           // BN: R fp32 γ versions [C]
   std::vector<float*> mean, invstd;   // BN: per stash slot, [m, C] per-micro-batch statistics
+  std::vector<uint8_t*> argmax;       // MAXPOOL3 (C % 8 == 0): per stash slot, first-max tap per output
   bool has_w() const {
     return kind == TPS_LAYER_LINEAR || kind == TPS_LAYER_CONV3X3 || kind == TPS_LAYER_CONV || kind == TPS_LAYER_BN;
   }
@@ -551,7 +552,12 @@ tps_status graph_forward(tps_pipeline* p, int64_t j, int a0, int cnt, int64_t v)
         break;
       }
       case TPS_LAYER_MAXPOOL3:
-        CUDA_OK(tps::launch_maxpool3_fwd(X, static_cast<uint16_t*>(out), nr, L.H, L.Wd, L.Ci, p->cs));
+        if (!L.argmax.empty())
+          CUDA_OK(tps::launch_maxpool3_fwd_idx(X, static_cast<uint16_t*>(out),
+                                               L.argmax[slot] + static_cast<size_t>(r0) * L.out_elems(), nr, L.H,
+                                               L.Wd, L.Ci, p->cs));
+        else
+          CUDA_OK(tps::launch_maxpool3_fwd(X, static_cast<uint16_t*>(out), nr, L.H, L.Wd, L.Ci, p->cs));
         p->launches += 1;
         break;
       case TPS_LAYER_AVGPOOL:
@@ -734,7 +740,10 @@ tps_status graph_backward(tps_pipeline* p, int64_t j, int64_t v_used, int64_t vl
         if (!need_dx) break;
         const GradTarget xt = target(L.src);
         uint16_t* dx = xt.filled ? p->gtmp[1] : xt.buf;
-        if (L.kind == TPS_LAYER_MAXPOOL3) CUDA_OK(tps::launch_maxpool3_bwd(X, g, dx, B, L.H, L.Wd, L.Ci, p->cs));
+        if (L.kind == TPS_LAYER_MAXPOOL3 && !L.argmax.empty())
+          CUDA_OK(tps::launch_maxpool3_bwd_idx(L.argmax[slot], g, dx, B, L.H, L.Wd, L.Ci, p->cs));
+        else if (L.kind == TPS_LAYER_MAXPOOL3)
+          CUDA_OK(tps::launch_maxpool3_bwd(X, g, dx, B, L.H, L.Wd, L.Ci, p->cs));
         else CUDA_OK(tps::launch_avgpool_bwd(g, dx, B, L.hw_in, L.Ci, p->cs));
         p->launches += 1;
         TPS_TRY(settle(L.src, xt, p->gtmp[1]));
@@ -1209,6 +1218,10 @@ tps_status init_graph(tps_pipeline* p, const tps_config* c, int lb, int le) {
       L.in = sp.in_c; L.out = sp.out_c; L.Kp = pad16(L.in); L.Np = pad16(L.out);
       L.ld_in = L.Kp; L.ld_out = L.Np;
       bias_scr = std::max(bias_scr, tps::bias_grad_scratch_floats(p->B, L.Np));
+    } else if (sp.kind == TPS_LAYER_MAXPOOL3 && L.Ci % 8 == 0) {
+      L.argmax.resize(p->Kmax);
+      for (int r = 0; r < p->Kmax; ++r)
+        TPS_TRY(alloc_t(p, &L.argmax[r], static_cast<size_t>(p->B) * L.out_elems(), &p->mem_acts));
     }
     max_elems = std::max({max_elems, L.in_elems(), L.out_elems()});
     if (L.has_w()) {
@@ -2035,8 +2048,9 @@ tps_status tps_bn_backward(const void* dy, const void* y, const void* x, const f
 
 tps_status tps_pool_op(int32_t op, const void* a, const void* b, void* out, int32_t N, int32_t H, int32_t W, int32_t C,
                        uint64_t stream) {
-  if (op < 0 || op > 3 || !out || N < 1 || H < 1 || W < 1 || C < 1) return fail(TPS_E_INVALID_ARG, "bad pool arguments");
-  if ((op <= 2 && !a) || ((op == 1 || op == 3) && !b)) return fail(TPS_E_INVALID_ARG, "missing pool operand");
+  if (op < 0 || op > 5 || !out || N < 1 || H < 1 || W < 1 || C < 1) return fail(TPS_E_INVALID_ARG, "bad pool arguments");
+  if ((op != 3 && !a) || (op != 0 && op != 2 && !b)) return fail(TPS_E_INVALID_ARG, "missing pool operand");
+  if (op >= 4 && C % 8) return fail(TPS_E_INVALID_ARG, "recorded-tap max pool needs C %% 8 == 0");
   TPS_TRY(op_prologue());
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const uint16_t* A = static_cast<const uint16_t*>(a);
@@ -2045,7 +2059,9 @@ tps_status tps_pool_op(int32_t op, const void* a, const void* b, void* out, int3
   if (op == 0) CUDA_OK(tps::launch_maxpool3_fwd(A, O, N, H, W, C, st));
   else if (op == 1) CUDA_OK(tps::launch_maxpool3_bwd(A, Bp, O, N, H, W, C, st));
   else if (op == 2) CUDA_OK(tps::launch_avgpool_fwd(A, O, N, H * W, C, st));
-  else CUDA_OK(tps::launch_avgpool_bwd(Bp, O, N, H * W, C, st));
+  else if (op == 3) CUDA_OK(tps::launch_avgpool_bwd(Bp, O, N, H * W, C, st));
+  else if (op == 4) CUDA_OK(tps::launch_maxpool3_fwd_idx(A, O, static_cast<uint8_t*>(const_cast<void*>(b)), N, H, W, C, st));
+  else CUDA_OK(tps::launch_maxpool3_bwd_idx(static_cast<const uint8_t*>(a), Bp, O, N, H, W, C, st));
   return TPS_OK;
 }
 

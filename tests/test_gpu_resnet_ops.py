@@ -75,17 +75,27 @@ def test_maxpool3_and_avgpool(gpu_lib):
     dA = torch.empty_like(Xd)
     tps.pool_op(3, None, gd, dA, N, H, W, C)
     torch.cuda.synchronize()
+    Y2 = torch.empty_like(Y)
+    idx = torch.empty(N, Ho, Wo, C, dtype=torch.uint8, device="cuda")
+    tps.pool_op(4, Xd, idx, Y2, N, H, W, C)                      # recorded first-max taps
+    dX2 = torch.empty_like(Xd)
+    tps.pool_op(5, idx, dYd, dX2, N, H, W, C)
+    torch.cuda.synchronize()
     assert np.array_equal(host(Y), resnet.maxpool3_forward(X))
+    assert np.array_equal(host(Y2), host(Y))
+    assert np.array_equal(host(dX2), host(dX))
     close_bf16(host(dX), resnet.maxpool3_backward(X, dY))
     close_bf16(host(A), resnet.avgpool_forward(X))
     close_bf16(host(dA), resnet.avgpool_backward(X.shape, g))
 
 
-@pytest.mark.parametrize("relu,res", [(True, False), (True, True), (False, False)])
-def test_batchnorm_forward_backward(gpu_lib, relu, res):
+@pytest.mark.parametrize("relu,res,C", [(True, False, 40), (True, True, 40), (False, False, 40), (True, True, 64),
+                                        (False, False, 256), (True, False, 24)])
+def test_batchnorm_forward_backward(gpu_lib, relu, res, C):
+    """C % 8 == 0 takes the 16-byte vector kernels, C = 40 / 24 with odd channel groups too."""
     from paper_2509_23241_b200 import tps
-    rng = np.random.default_rng(7)
-    segs, b, H, W, C = 3, 4, 5, 6, 40
+    rng = np.random.default_rng(7 + C)
+    segs, b, H, W = 3, 4, 5, 6
     rows = b * H * W
     X, Xd = bf(1.5 + 2.0 * rng.standard_normal((segs * b, H, W, C)))
     R, Rd = bf(rng.standard_normal((segs * b, H, W, C)))
