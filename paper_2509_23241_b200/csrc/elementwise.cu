@@ -373,7 +373,6 @@ __global__ void col2im_kernel(const float* __restrict__ dP, uint16_t* __restrict
 
 // batch-norm statistics per (segment, channel) over `seg_rows` rows of x[rows, C] (bf16):
 // fp64 sums per (segment, row chunk, channel), then a fixed-order final pass -> mean, invstd
-constexpr int BN_CHUNK = 256;
 __global__ void bn_stats_partial(const uint16_t* __restrict__ x, int seg_rows, int C, int chunks,
                                  double* __restrict__ part) {
   // grid: (ceil(C/32), chunks, segments); block (32, 8)
@@ -402,17 +401,25 @@ __global__ void bn_stats_partial(const uint16_t* __restrict__ x, int seg_rows, i
   }
 }
 
+// one warp per (segment, channel): lanes stride the chunks, fixed shuffle tree
 __global__ void bn_stats_final(const double* __restrict__ part, int chunks, int C, int seg_rows, int segs,
                                float* __restrict__ mean, float* __restrict__ invstd, float eps) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;   // (segment, channel)
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;   // (segment, channel)
+  const int lane = threadIdx.x & 31;
   if (i >= segs * C) return;
   const int seg = i / C, c = i - seg * C;
   double s1 = 0.0, s2 = 0.0;
-  for (int k = 0; k < chunks; ++k) {
+  for (int k = lane; k < chunks; k += 32) {
     const size_t o = (static_cast<size_t>(seg) * chunks + k) * C + c;
     s1 += part[2 * o];
     s2 += part[2 * o + 1];
   }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    s1 += __shfl_xor_sync(0xffffffffu, s1, off);
+    s2 += __shfl_xor_sync(0xffffffffu, s2, off);
+  }
+  if (lane) return;
   const double m = s1 / seg_rows;
   const double var = fmax(s2 / seg_rows - m * m, 0.0);
   mean[i] = static_cast<float>(m);
@@ -668,14 +675,14 @@ __global__ void bn_apply_vec(const uint4* __restrict__ x, const uint4* __restric
 
 // per (segment, chunk) partial sums over 8 channels per thread, fp64:
 //   MODE 0 (statistics): Σx, Σx²;  MODE 1 (backward): Σdy', Σdy'·x̂ (dy' = dy ⊙ [y > 0] if relu)
-// block: tx = min(C8, 256) channel groups x ty = 256 / tx rows; grid (ceil(C8/tx), chunks, segs)
+// block: tx = min(C8, 32) channel groups x ty = 256 / tx rows; grid (ceil(C8/tx), chunks, segs)
 template <int MODE>
 __global__ void __launch_bounds__(256) bn_partial_vec(const uint4* __restrict__ a, const uint4* __restrict__ yv,
                                                       const uint4* __restrict__ xv, const float* __restrict__ mean,
                                                       const float* __restrict__ invstd, int seg_rows, int C8,
                                                       int chunks, int relu, double* __restrict__ part) {
   extern __shared__ double red[];            // [ty][tx][16]
-  const int tx = min(C8, 256), ty = blockDim.x / tx;
+  const int tx = min(C8, 32), ty = blockDim.x / tx;
   const int lx = threadIdx.x % tx, ly = threadIdx.x / tx;
   const int cg = blockIdx.x * tx + lx;       // channel group
   const int seg = blockIdx.z;
@@ -1103,7 +1110,8 @@ cudaError_t launch_col2im(const float* dP, uint16_t* dX, const uint16_t* add, in
   return cudaGetLastError();
 }
 
-int bn_chunks(int seg_rows) { return std::max(1, std::min(64, seg_rows / BN_CHUNK)); }
+// row chunks per segment: enough blocks to fill the GPU with >= 64 rows per chunk
+int bn_chunks(int seg_rows) { return std::max(1, std::min(256, seg_rows / 64)); }
 
 int64_t bn_scratch_doubles(int segs, int seg_rows, int C) {
   return static_cast<int64_t>(segs) * bn_chunks(seg_rows) * C * 2 + static_cast<int64_t>(segs) * C * 2;
@@ -1115,12 +1123,12 @@ cudaError_t launch_bn_forward(const uint16_t* x, const uint16_t* res, uint16_t* 
   const int chunks = bn_chunks(seg_rows);
   const int64_t rows = static_cast<int64_t>(segs) * seg_rows;
   if (C % 8 == 0) {
-    const int C8 = C / 8, tx = std::min(C8, 256);
+    const int C8 = C / 8, tx = std::min(C8, 32);
     dim3 grid((C8 + tx - 1) / tx, chunks, segs);
     bn_partial_vec<0><<<grid, tx * (256 / tx), 256 * 16 * sizeof(double), st>>>(reinterpret_cast<const uint4*>(x), nullptr,
                                                                      nullptr, nullptr, nullptr, seg_rows, C8, chunks,
                                                                      0, scratch);
-    bn_stats_final<<<(segs * C + 255) / 256, 256, 0, st>>>(scratch, chunks, C, seg_rows, segs, mean, invstd, 1e-5f);
+    bn_stats_final<<<(segs * C * 32 + 255) / 256, 256, 0, st>>>(scratch, chunks, C, seg_rows, segs, mean, invstd, 1e-5f);
     bn_apply_vec<<<grid_for(rows * C8, 256), 256, 0, st>>>(
         reinterpret_cast<const uint4*>(x), reinterpret_cast<const uint4*>(res), reinterpret_cast<uint4*>(y), gamma,
         beta, mean, invstd, rows * C8, C8, seg_rows, relu);
@@ -1128,7 +1136,7 @@ cudaError_t launch_bn_forward(const uint16_t* x, const uint16_t* res, uint16_t* 
   }
   dim3 grid((C + 31) / 32, chunks, segs);
   bn_stats_partial<<<grid, dim3(32, 8), 0, st>>>(x, seg_rows, C, chunks, scratch);
-  bn_stats_final<<<(segs * C + 255) / 256, 256, 0, st>>>(scratch, chunks, C, seg_rows, segs, mean, invstd, 1e-5f);
+  bn_stats_final<<<(segs * C * 32 + 255) / 256, 256, 0, st>>>(scratch, chunks, C, seg_rows, segs, mean, invstd, 1e-5f);
   bn_apply_kernel<<<grid_for(rows * C, 256), 256, 0, st>>>(x, res, y, gamma, beta, mean, invstd, rows, C, seg_rows, relu);
   return cudaGetLastError();
 }
@@ -1140,7 +1148,7 @@ cudaError_t launch_bn_backward(const uint16_t* dy, const uint16_t* y, const uint
   const int chunks = bn_chunks(seg_rows);
   double* sums = scratch + static_cast<int64_t>(segs) * chunks * C * 2;
   if (C % 8 == 0) {
-    const int C8 = C / 8, tx = std::min(C8, 256);
+    const int C8 = C / 8, tx = std::min(C8, 32);
     const int64_t rows = static_cast<int64_t>(segs) * seg_rows;
     dim3 grid((C8 + tx - 1) / tx, chunks, segs);
     bn_partial_vec<1><<<grid, tx * (256 / tx), 256 * 16 * sizeof(double), st>>>(
