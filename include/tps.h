@@ -280,6 +280,12 @@ tps_status tps_launch_count(tps_pipeline* p, int64_t* n);
 tps_status tps_fill_synthetic(int32_t kind, uint64_t seed, uint64_t tid, int64_t rows,
                               int64_t cols, int32_t classes, void* dst, uint64_t stream);
 
+/* ---- debugging: progress of a handle's static order (safe to call from another host thread
+ * while a run is in progress).  pos = index of the next event, n_events = events in the run,
+ * busy = bitmask of streams with pending work (compute, fwd-in, fwd-out, bwd-in, bwd-out,
+ * optimizer).                                                                              */
+tps_status tps_debug_progress(tps_pipeline* p, int64_t* pos, int64_t* n_events, int32_t* busy);
+
 /* ---- raw stage GEMM (kernel unit tests / microbenchmarks) -------------------- */
 /* D[M,N] = alpha · A·Bᵀ (fp32 accumulate on tcgen05), A and B bf16, device.
  * mode 0 (forward):  A [M,K] ld=lda (K-major), B [N,K] ld=ldb (K-major);

@@ -1602,6 +1602,10 @@ tps_status tps_run_schedule_local(tps_pipeline* const* st, int32_t S, int64_t fi
   // input has been enqueued and the buffer it overwrites has been consumed downstream.
   std::vector<int64_t> fcount(S, 0), bcount(S, 0);
   const int ng = st[0]->ng;
+  static const bool trace_fire = [] {
+    const char* e = std::getenv("TPS_TRACE_FIRE");
+    return e && e[0] == '1';
+  }();
   for (;;) {
     bool all_done = true, progress = false;
     for (int s = 0; s < S; ++s) {
@@ -1619,6 +1623,10 @@ tps_status tps_run_schedule_local(tps_pipeline* const* st, int32_t S, int64_t fi
         if (s < S - 1 && bcount[s + 1] <= jr) continue;                      // gradient not produced
         if (s > 0 && jr >= 2 && bcount[s - 1] <= jr - 2) continue;           // gout buffer busy
       }
+      if (trace_fire) {
+        std::fprintf(stderr, "[tps] fire s=%d kind=%d mb=%lld micro=%d\n", s, e.kind, (long long)e.mb, e.micro);
+        std::fflush(stderr);
+      }
       TPS_TRY(fire(p, e, x_pool, y_pool, pool));
       if (e.kind == TPS_EV_F) fcount[s] += 1;
       if (e.kind == TPS_EV_B) bcount[s] += 1;
@@ -1628,6 +1636,22 @@ tps_status tps_run_schedule_local(tps_pipeline* const* st, int32_t S, int64_t fi
     if (!progress) return fail(TPS_E_STATE, "local schedule deadlock");
   }
   for (int s = 0; s < S; ++s) TPS_TRY(join_update_stream(st[s]));
+  return TPS_OK;
+}
+
+tps_status tps_debug_progress(tps_pipeline* p, int64_t* pos, int64_t* n_events, int32_t* busy) {
+  if (!p) return fail(TPS_E_INVALID_ARG, "null handle");
+  if (pos) *pos = static_cast<int64_t>(p->pos);
+  if (n_events) *n_events = static_cast<int64_t>(p->order.size());
+  if (busy) {
+    int b = 0, i = 0;
+    for (cudaStream_t st : {p->cs, p->s_fin, p->s_fout, p->s_bin, p->s_bout, p->s_upd}) {
+      if (st && cudaStreamQuery(st) == cudaErrorNotReady) b |= 1 << i;
+      ++i;
+    }
+    cudaGetLastError();
+    *busy = b;
+  }
   return TPS_OK;
 }
 

@@ -32,7 +32,7 @@ EXPORTS = [
     "tps_init_weights_synthetic", "tps_get_losses", "tps_get_trace", "tps_clear_trace", "tps_memory_stats",
     "tps_set_profiling", "tps_kernel_stats", "tps_launch_count", "tps_fill_synthetic", "tps_gemm",
     "tps_conv_gemm", "tps_partition", "tps_im2col", "tps_col2im", "tps_bn_forward", "tps_bn_backward",
-    "tps_pool_op", "tps_conv2d_gemm",
+    "tps_pool_op", "tps_conv2d_gemm", "tps_debug_progress",
 ]
 TPS_LAYER_LINEAR, TPS_LAYER_CONV3X3, TPS_LAYER_MAXPOOL2 = 0, 1, 2
 TPS_LAYER_CONV, TPS_LAYER_BN, TPS_LAYER_MAXPOOL3, TPS_LAYER_AVGPOOL = 3, 4, 5, 6
@@ -116,6 +116,7 @@ def lib() -> C.CDLL:
             "tps_bn_forward": (I32, [P, P, P, P, P, P, P, I32, I32, I32, I32, U64]),
             "tps_bn_backward": (I32, [P, P, P, P, P, P, P, F, F, I32, I32, I32, I32, P, P, P, P, U64]),
             "tps_pool_op": (I32, [I32, P, P, P, I32, I32, I32, I32, U64]),
+            "tps_debug_progress": (I32, [P, P, P, P]),
             "tps_conv2d_gemm": (I32, [I32, I32, I32, I32, I32, I32, I32, I32, I32, P, P, P, P, I32, F, F, U64]),
         }
         for name, (res, args) in sig.items():
