@@ -33,16 +33,22 @@ def nvcc() -> str:
     return "nvcc"
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
+def build(verbose: bool = False, force: bool = False, out: str | None = None, extra: list | None = None,
+          objdir: str | None = None) -> str:
+    """out / extra / objdir: build a variant library (e.g. -DTPS_SGD_NB=3) for experiments."""
     os.makedirs(LIBDIR, exist_ok=True)
     inc, lib = nccl_dirs()
+    target = out or LIB
+    odir = objdir or LIBDIR
+    os.makedirs(odir, exist_ok=True)
     deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(ROOT, "include", "tps.h")]
-    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= max(os.path.getmtime(d) for d in deps):
-        return LIB
+    if not force and os.path.exists(target) and os.path.getmtime(target) >= max(os.path.getmtime(d) for d in deps):
+        return target
     objs = []
     common = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"), "-I", inc]
+    common += list(extra or [])
     for src in SOURCES:
-        obj = os.path.join(LIBDIR, src.rsplit(".", 1)[0] + ".o")
+        obj = os.path.join(odir, src.rsplit(".", 1)[0] + ".o")
         cmd = [nvcc()] + ARCH + common + ["-c", os.path.join(CSRC, src), "-o", obj]
         if src.endswith(".cu"):
             cmd += ["-Xptxas", "-v"] if verbose else []
@@ -52,12 +58,12 @@ def build(verbose: bool = False, force: bool = False) -> str:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)
         objs.append(obj)
-    cmd = [nvcc()] + ARCH + ["-shared", "-Xcompiler", "-fPIC", "-o", LIB] + objs + [
+    cmd = [nvcc()] + ARCH + ["-shared", "-Xcompiler", "-fPIC", "-o", target] + objs + [
         "-L", lib, "-l:libnccl.so.2", "-Xlinker", "-rpath=" + lib]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.run(cmd, check=True)
-    return LIB
+    return target
 
 
 if __name__ == "__main__":

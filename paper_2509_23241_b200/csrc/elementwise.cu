@@ -641,27 +641,39 @@ __device__ __forceinline__ void load8f(const float* p, float (&f)[8]) {
   f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w; f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
 }
 
-__global__ void bn_apply_vec(const uint4* __restrict__ x, const uint4* __restrict__ res, uint4* __restrict__ y,
-                             const float* __restrict__ gamma, const float* __restrict__ beta,
-                             const float* __restrict__ mean, const float* __restrict__ invstd, int64_t nvec, int C8,
-                             int seg_rows, int relu) {
-  const int C = C8 * 8;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < nvec;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t r = i / C8;
-    const int c0 = static_cast<int>(i - r * C8) * 8;
-    const int sc = static_cast<int>(r / seg_rows) * C + c0;
-    float xv[8], g[8], bt[8], m[8], is[8], v[8];
-    unpack8(x[i], xv);
-    load8f(gamma + c0, g);
-    load8f(beta + c0, bt);
-    load8f(mean + sc, m);
-    load8f(invstd + sc, is);
+// Row-mapped BN apply kernels: a thread owns one 8-channel group and walks rows, so the
+// per-channel parameters (γ, β, and the current segment's statistics / backward coefficients)
+// stay in registers; a warp covers 512 contiguous bytes of a row (or of 32/tx adjacent rows).
+// block = tx channel groups x ty rows (tx = min(C8, 32)), grid = (ceil(C8/tx), row blocks).
+__global__ void __launch_bounds__(256) bn_apply_rows(const uint4* __restrict__ x, const uint4* __restrict__ res,
+                                                     uint4* __restrict__ y, const float* __restrict__ gamma,
+                                                     const float* __restrict__ beta, const float* __restrict__ mean,
+                                                     const float* __restrict__ invstd, int rows, int C8, int seg_rows,
+                                                     int relu) {
+  const int tx = min(C8, 32), ty = blockDim.x / tx;
+  const int cg = blockIdx.x * tx + static_cast<int>(threadIdx.x) % tx;
+  if (cg >= C8 || static_cast<int>(threadIdx.x) >= tx * ty) return;
+  const int C = C8 * 8, c0 = cg * 8;
+  float g[8], bt[8], m[8], is[8];
+  load8f(gamma + c0, g);
+  load8f(beta + c0, bt);
+  int cur = -1;
+  const int step = gridDim.y * ty;
+  for (int r = blockIdx.y * ty + static_cast<int>(threadIdx.x) / tx; r < rows; r += step) {
+    const int seg = r / seg_rows;
+    if (seg != cur) {
+      cur = seg;
+      load8f(mean + seg * C + c0, m);
+      load8f(invstd + seg * C + c0, is);
+    }
+    const size_t o = static_cast<size_t>(r) * C8 + cg;
+    float xv[8], v[8];
+    unpack8(x[o], xv);
 #pragma unroll
     for (int e = 0; e < 8; ++e) v[e] = g[e] * ((xv[e] - m[e]) * is[e]) + bt[e];
     if (res) {
       float rv[8];
-      unpack8(res[i], rv);
+      unpack8(res[o], rv);
 #pragma unroll
       for (int e = 0; e < 8; ++e) v[e] += rv[e];
     }
@@ -669,7 +681,52 @@ __global__ void bn_apply_vec(const uint4* __restrict__ x, const uint4* __restric
 #pragma unroll
       for (int e = 0; e < 8; ++e) v[e] = fmaxf(v[e], 0.f);
     }
-    y[i] = pack8(v);
+    y[o] = pack8(v);
+  }
+}
+
+__global__ void __launch_bounds__(256) bn_bwd_apply_rows(const uint4* __restrict__ dy, const uint4* __restrict__ yv,
+                                                         const uint4* __restrict__ xv, const float4* __restrict__ coef,
+                                                         const float* __restrict__ invstd, int rows, int C8,
+                                                         int seg_rows, int relu, uint4* __restrict__ dx,
+                                                         uint4* __restrict__ dres) {
+  const int tx = min(C8, 32), ty = blockDim.x / tx;
+  const int cg = blockIdx.x * tx + static_cast<int>(threadIdx.x) % tx;
+  if (cg >= C8 || static_cast<int>(threadIdx.x) >= tx * ty) return;
+  const int C = C8 * 8, c0 = cg * 8;
+  float ka[8], kb[8], kc[8], km[8], is[8];
+  int cur = -1;
+  const int step = gridDim.y * ty;
+  for (int r = blockIdx.y * ty + static_cast<int>(threadIdx.x) / tx; r < rows; r += step) {
+    const int seg = r / seg_rows;
+    if (seg != cur) {
+      cur = seg;
+      const int sc = seg * C + c0;
+      load8f(invstd + sc, is);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float4 k = coef[sc + e];
+        ka[e] = k.x; kb[e] = k.y; kc[e] = k.z; km[e] = k.w;
+      }
+    }
+    const size_t o = static_cast<size_t>(r) * C8 + cg;
+    float d[8], xx[8], out[8];
+    unpack8(dy[o], d);
+    unpack8(xv[o], xx);
+    if (relu) {
+      float yy[8];
+      unpack8(yv[o], yy);
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        if (!(yy[e] > 0.f)) d[e] = 0.f;
+    }
+    if (dres) dres[o] = pack8(d);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float xh = (xx[e] - km[e]) * is[e];
+      out[e] = ka[e] * (d[e] - kb[e] - xh * kc[e]);
+    }
+    dx[o] = pack8(out);
   }
 }
 
@@ -699,6 +756,7 @@ __global__ void __launch_bounds__(256) bn_partial_vec(const uint4* __restrict__ 
       load8f(mean + seg * C + cg * 8, m);
       load8f(invstd + seg * C + cg * 8, is);
     }
+#pragma unroll 4
     for (int r = lo + ly; r < hi; r += ty) {
       const int64_t o = (r0 + r) * C8 + cg;
       float v[8];
@@ -781,38 +839,6 @@ __global__ void bn_bwd_coef(const double* __restrict__ part, int chunks, int C, 
   if (lane) return;
   dgamma[c] = static_cast<float>(tg);
   dbeta[c] = static_cast<float>(tb);
-}
-
-__global__ void bn_bwd_apply_vec(const uint4* __restrict__ dy, const uint4* __restrict__ yv,
-                                 const uint4* __restrict__ xv, const float4* __restrict__ coef,
-                                 const float* __restrict__ invstd, int64_t nvec, int C8, int seg_rows, int relu,
-                                 uint4* __restrict__ dx, uint4* __restrict__ dres) {
-  const int C = C8 * 8;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < nvec;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t r = i / C8;
-    const int c0 = static_cast<int>(i - r * C8) * 8;
-    const int sc = static_cast<int>(r / seg_rows) * C + c0;
-    float d[8], xx[8], is[8], o[8];
-    unpack8(dy[i], d);
-    unpack8(xv[i], xx);
-    if (relu) {
-      float yy[8];
-      unpack8(yv[i], yy);
-#pragma unroll
-      for (int e = 0; e < 8; ++e)
-        if (!(yy[e] > 0.f)) d[e] = 0.f;
-    }
-    if (dres) dres[i] = pack8(d);
-    load8f(invstd + sc, is);
-#pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const float4 k = coef[sc + e];
-      const float xh = (xx[e] - k.w) * is[e];
-      o[e] = k.x * (d[e] - k.y - xh * k.z);
-    }
-    dx[i] = pack8(o);
-  }
 }
 
 // 3x3/2/1 max pool over 8 channels per thread, recording the first-max tap (0..8) per output
@@ -1111,6 +1137,13 @@ cudaError_t launch_col2im(const float* dP, uint16_t* dX, const uint16_t* add, in
 }
 
 // row chunks per segment: enough blocks to fill the GPU with >= 64 rows per chunk
+dim3 bn_rows_grid(int rows, int C8) {
+  const int tx = std::min(C8, 32), ty = 256 / tx;
+  const int gx = (C8 + tx - 1) / tx;
+  const int gy = std::max(1, std::min((rows + ty - 1) / ty, (148 * 8 + gx - 1) / gx));
+  return dim3(gx, gy);
+}
+
 int bn_chunks(int seg_rows) { return std::max(1, std::min(256, seg_rows / 64)); }
 
 int64_t bn_scratch_doubles(int segs, int seg_rows, int C) {
@@ -1129,9 +1162,12 @@ cudaError_t launch_bn_forward(const uint16_t* x, const uint16_t* res, uint16_t* 
                                                                      nullptr, nullptr, nullptr, seg_rows, C8, chunks,
                                                                      0, scratch);
     bn_stats_final<<<(segs * C * 32 + 255) / 256, 256, 0, st>>>(scratch, chunks, C, seg_rows, segs, mean, invstd, 1e-5f);
-    bn_apply_vec<<<grid_for(rows * C8, 256), 256, 0, st>>>(
-        reinterpret_cast<const uint4*>(x), reinterpret_cast<const uint4*>(res), reinterpret_cast<uint4*>(y), gamma,
-        beta, mean, invstd, rows * C8, C8, seg_rows, relu);
+    {
+      const int C8r = C8, tx = std::min(C8r, 32);
+      bn_apply_rows<<<bn_rows_grid(static_cast<int>(rows), C8r), tx * (256 / tx), 0, st>>>(
+          reinterpret_cast<const uint4*>(x), reinterpret_cast<const uint4*>(res), reinterpret_cast<uint4*>(y), gamma,
+          beta, mean, invstd, static_cast<int>(rows), C8r, seg_rows, relu);
+    }
     return cudaGetLastError();
   }
   dim3 grid((C + 31) / 32, chunks, segs);
@@ -1157,9 +1193,13 @@ cudaError_t launch_bn_backward(const uint16_t* dy, const uint16_t* y, const uint
     float4* coef = reinterpret_cast<float4*>(sums);   // segs·C float4 = the sums region
     bn_bwd_coef<<<(C * 32 + 255) / 256, 256, 0, st>>>(scratch, chunks, C, segs, seg_rows, mean, invstd, gs, gl, ga,
                                                       gb, coef, dgamma, dbeta);
-    bn_bwd_apply_vec<<<grid_for(rows * C8, 256), 256, 0, st>>>(
-        reinterpret_cast<const uint4*>(dy), reinterpret_cast<const uint4*>(y), reinterpret_cast<const uint4*>(x), coef,
-        invstd, rows * C8, C8, seg_rows, relu, reinterpret_cast<uint4*>(dx), reinterpret_cast<uint4*>(dres));
+    {
+      const int C8r = C8, tx = std::min(C8r, 32);
+      bn_bwd_apply_rows<<<bn_rows_grid(static_cast<int>(rows), C8r), tx * (256 / tx), 0, st>>>(
+          reinterpret_cast<const uint4*>(dy), reinterpret_cast<const uint4*>(y), reinterpret_cast<const uint4*>(x),
+          coef, invstd, static_cast<int>(rows), C8r, seg_rows, relu, reinterpret_cast<uint4*>(dx),
+          reinterpret_cast<uint4*>(dres));
+    }
     return cudaGetLastError();
   }
   dim3 grid((C + 31) / 32, chunks, segs);

@@ -779,6 +779,12 @@ Tiling pick_tiling(int M, int N, int K, int mode, bool sgd) {
     const char* e = std::getenv("TPS_GEMM_CG");
     force_cg = e ? std::atoi(e) : 0;
   }
+  static int sgd_bn = -1;
+  if (sgd_bn < 0) {
+    const char* e = std::getenv("TPS_SGD_BN");
+    sgd_bn = e ? std::atoi(e) : 0;
+  }
+  if (sgd && sgd_bn && force_cg != 1 && M >= 256) return {2, sgd_bn};
   if (force_cg != 1 && M >= 256) {
     const int tm = (M + 255) / 256;
     for (int bn : {256, 128}) {

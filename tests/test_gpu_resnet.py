@@ -34,14 +34,14 @@ def tiny(widths=(16, 32), H=32, stem_c=16, blocks=(1, 1)):
     return ograph.resnet_layers(blocks=blocks, widths=widths, H=H, classes=10, stem_c=stem_c)
 
 
-def compare(layers, bounds, m, b, M, variant, blend, lr=0.01, mu=0.9, mode="params"):
+def compare(layers, bounds, m, b, M, variant, blend, lr=0.01, mu=0.9, mode="params", **gpu_kw):
     kind = synthgen.X_UNIT
     ref = run_oracle_graph(layers, bounds, m, b, M, variant, blend, 0.05, lr, mu, kind=kind)
     xs, ys, params = graph_workload(layers, m, b, M, kind=kind)
     ex = ograph.run(layers, bounds, m, b, M, xs, ys, params, variant=variant, blend=blend, lam=0.05, lr=lr, mu=mu,
                     exact=True)
     dims = [layers[0]["h"] * layers[0]["w"] * layers[0]["cin"], layers[-1]["out"]]
-    stages, losses = run_gpu(dims, bounds, m, b, M, variant, blend, 0.05, lr, mu, kind=kind, layers=layers)
+    stages, losses = run_gpu(dims, bounds, m, b, M, variant, blend, 0.05, lr, mu, kind=kind, layers=layers, **gpu_kw)
     assert expand_gpu_trace(stages) == oracle_trace(ref)
     lerr = np.abs(losses - ref.losses) / np.abs(ref.losses)
     lgap = np.abs(ex.losses - ref.losses) / np.abs(ref.losses)
@@ -96,6 +96,16 @@ def test_tiny_resnet_first_updates_three_stages(gpu_lib, vn):
 def test_tiny_resnet_ten_steps_three_stages(gpu_lib, vn):
     layers, starts = tiny()
     compare(layers, [0, starts[1], starts[2], len(layers)], 2, 8, 10, *VARIANTS[vn])
+
+
+@pytest.mark.parametrize("fwd_group,extra_slot", [(1, 1), (2, 0)])
+def test_tiny_resnet_forward_groups(gpu_lib, fwd_group, extra_slot):
+    """Micro-batch forwards issued one (or two) at a time: each group's BN statistics are
+    computed over its own micro-batches (Z22) into the mini-batch's stash slot; without the
+    extra receive slot the input copy waits for the backward that frees the slot."""
+    layers, starts = tiny()
+    compare(layers, [0, starts[1], starts[2], len(layers)], 4, 4, 5, ost.I_VARIANT, ost.EQ1, mode="update",
+            fwd_group=fwd_group, extra_recv_slot=extra_slot)
 
 
 @pytest.mark.parametrize("vn", list(VARIANTS))
