@@ -990,6 +990,51 @@ __global__ void im2col_vec8(const uint16_t* __restrict__ X, uint4* __restrict__ 
   }
 }
 
+// explicit patches for one output row (n, ho) per block: the k input rows it reads are staged in
+// shared memory with the zero padding materialised, a per-column offset table maps patch
+// column (kh, kw, c) to its smem element, and the patch rows are written as 16-byte vectors
+__global__ void __launch_bounds__(256) im2col_rowtile(const uint16_t* __restrict__ X, uint4* __restrict__ P, int H,
+                                                      int W, int C, int k, int s, int p, int Ho, int Wo, int ldp) {
+  extern __shared__ uint16_t sm[];
+  const int Wp = W + 2 * p;                       // padded row length (pixels)
+  const int rowlen = Wp * C;
+  uint16_t* tile = sm;                            // [k][Wp][C]
+  int* off = reinterpret_cast<int*>(sm + ((k * rowlen + 1) & ~1));   // [ldp]
+  const int n = blockIdx.x / Ho, ho = blockIdx.x - n * Ho;
+  const int h0 = ho * s - p;
+  for (int i = threadIdx.x; i < k * rowlen; i += blockDim.x) {
+    const int kh = i / rowlen, rem = i - kh * rowlen;
+    const int wp = rem / C, c = rem - wp * C;
+    const int h = h0 + kh, w = wp - p;
+    uint16_t v = 0;
+    if (h >= 0 && h < H && w >= 0 && w < W) v = X[((static_cast<int64_t>(n) * H + h) * W + w) * C + c];
+    tile[i] = v;
+  }
+  const int kkC = k * k * C;
+  for (int col = threadIdx.x; col < ldp; col += blockDim.x) {
+    int o = -1;
+    if (col < kkC) {
+      const int kh = col / (k * C), rem = col - kh * k * C;    // rem = kw·C + c
+      o = kh * rowlen + rem;
+    }
+    off[col] = o;
+  }
+  __syncthreads();
+  const int v8 = ldp / 8;
+  uint4* prow = P + (static_cast<int64_t>(n) * Ho + ho) * Wo * v8;
+  for (int i = threadIdx.x; i < Wo * v8; i += blockDim.x) {
+    const int wo = i / v8, cv = i - wo * v8;
+    const int base = wo * s * C;
+    uint32_t v[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int o = off[cv * 8 + e];
+      v[e] = o >= 0 ? tile[o + base] : 0u;
+    }
+    prow[i] = make_uint4(v[0] | (v[1] << 16), v[2] | (v[3] << 16), v[4] | (v[5] << 16), v[6] | (v[7] << 16));
+  }
+}
+
 // explicit patches, one output pixel row per block iteration (32-bit index math per element)
 __global__ void im2col_rows(const uint16_t* __restrict__ X, uint16_t* __restrict__ P, int N, int H, int W, int C,
                             int k, int s, int p, int Ho, int Wo, int ldp, int64_t rows) {
@@ -1109,6 +1154,12 @@ cudaError_t launch_im2col(const uint16_t* X, uint16_t* P, int N, int H, int W, i
   const int Ho = (H + 2 * p - k) / s + 1, Wo = (W + 2 * p - k) / s + 1;
   const int64_t rows = static_cast<int64_t>(N) * Ho * Wo;
   if (rows <= 0) return cudaSuccess;
+  const size_t smem = static_cast<size_t>((k * (W + 2 * p) * C + 1) & ~1) * 2 + static_cast<size_t>(ldp) * 4;
+  if (ldp % 8 == 0 && smem <= 48 * 1024) {
+    im2col_rowtile<<<static_cast<unsigned>(static_cast<int64_t>(N) * Ho), 256, smem, st>>>(
+        X, reinterpret_cast<uint4*>(P), H, W, C, k, s, p, Ho, Wo, ldp);
+    return cudaGetLastError();
+  }
   if (ldp % 8 == 0) {
     const int64_t nvec = rows * (ldp / 8);
     im2col_vec8<<<grid_for(nvec, 256), 256, 0, st>>>(X, reinterpret_cast<uint4*>(P), H, W, C, k, s, p, Ho, Wo, ldp / 8,
