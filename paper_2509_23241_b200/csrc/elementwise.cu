@@ -85,6 +85,7 @@ __global__ void __launch_bounds__(256) sgd_update_kernel(float* __restrict__ w, 
 // ------------------------------------------------------------------ bias gradient
 constexpr int BG_COLS = 256;   // columns per block (32 threads x 8 columns)
 constexpr int BG_ROWS = 8;     // row lanes per block
+constexpr int BG_CNT = 64;     // arrival counters at the head of the scratch (cols <= 64·BG_COLS)
 
 __global__ void __launch_bounds__(256) bias_grad_partial(const uint16_t* __restrict__ G, int rows, int cols, int ldg,
                                                          int rows_per_split, float* __restrict__ part) {
@@ -111,6 +112,61 @@ __global__ void __launch_bounds__(256) bias_grad_partial(const uint16_t* __restr
 #pragma unroll
   for (int y = 0; y < BG_ROWS; ++y) s += red[y][t];
   if (c < cols) part[static_cast<size_t>(blockIdx.y) * cols + c] = s;
+}
+
+// One launch for the bias of a Linear layer (rows a8 + a10): the partial column sums of
+// bias_grad_partial, then the LAST block of each column block (arrival counter, self-resetting)
+// sums the splits in fixed order (deterministic, same bits as bias_grad_final) and, if b != null,
+// applies the SGD/momentum step of sgd_update_kernel to the fp32 bias and its momentum.
+__global__ void __launch_bounds__(256) bias_grad_fused(const uint16_t* __restrict__ G, int rows, int cols, int ldg,
+                                                       int rows_per_split, float* __restrict__ part,
+                                                       unsigned int* __restrict__ cnt, float* __restrict__ db,
+                                                       float* __restrict__ b, float* __restrict__ vb, float lr,
+                                                       float mu, float wd) {
+  __shared__ float red[BG_ROWS][BG_COLS + 4];
+  __shared__ bool last;
+  const int c0 = blockIdx.x * BG_COLS + threadIdx.x * 8;
+  const int r_begin = blockIdx.y * rows_per_split;
+  const int r_end = min(rows, r_begin + rows_per_split);
+  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  if (c0 < cols) {
+    for (int r = r_begin + threadIdx.y; r < r_end; r += BG_ROWS) {
+      const uint4 u = __ldg(reinterpret_cast<const uint4*>(G + static_cast<size_t>(r) * ldg + c0));
+      const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] += bf2f((w[e >> 1] >> ((e & 1) * 16)) & 0xFFFFu);
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < 8; ++e) red[threadIdx.y][threadIdx.x * 8 + e] = acc[e];
+  __syncthreads();
+  const int t = threadIdx.y * 32 + threadIdx.x;   // 0..255 -> one column each
+  const int c = blockIdx.x * BG_COLS + t;
+  float s = 0.f;
+#pragma unroll
+  for (int y = 0; y < BG_ROWS; ++y) s += red[y][t];
+  if (c < cols) part[static_cast<size_t>(blockIdx.y) * cols + c] = s;
+  __threadfence();
+  __syncthreads();
+  if (t == 0) last = atomicAdd(&cnt[blockIdx.x], 1u) == gridDim.y - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (t == 0) cnt[blockIdx.x] = 0u;               // ready for the next launch (stream-ordered)
+  if (c >= cols) return;
+  float d = 0.f;
+  for (int k = 0; k < static_cast<int>(gridDim.y); ++k) d += __ldcg(part + static_cast<size_t>(k) * cols + c);
+  db[c] = d;
+  if (!b) return;
+  float w = b[c];
+  const float gp = __fadd_rn(d, __fmul_rn(wd, w));
+  float upd = gp;
+  if (mu != 0.f) {
+    const float v = __fadd_rn(__fmul_rn(mu, vb[c]), gp);
+    vb[c] = v;
+    upd = v;
+  }
+  b[c] = __fsub_rn(w, __fmul_rn(lr, upd));
 }
 
 __global__ void bias_grad_final(const float* __restrict__ part, int splits, int cols, float* __restrict__ db) {
@@ -1083,7 +1139,23 @@ cudaError_t launch_sgd_update(float* w, float* v, const float* g, uint16_t* ver,
 }
 
 int64_t bias_grad_scratch_floats(int rows, int cols) {
-  return static_cast<int64_t>(bias_grad_splits(rows, cols)) * cols;
+  // BG_CNT arrival counters of bias_grad_fused (zero at allocation, self-resetting) at a fixed
+  // offset, then the partial sums
+  return BG_CNT + static_cast<int64_t>(bias_grad_splits(rows, cols)) * cols;
+}
+
+cudaError_t launch_bias_grad_sgd(const uint16_t* G, int rows, int cols, int ldg, float* db, float* scratch, float* b,
+                                 float* vb, float lr, float mu, float wd, cudaStream_t st) {
+  if (cols <= 0) return cudaSuccess;
+  if (cols % 8 || ldg % 8) return cudaErrorInvalidValue;
+  const int splits = bias_grad_splits(rows, cols);
+  const int rps = (rows + splits - 1) / splits;
+  dim3 grid((cols + BG_COLS - 1) / BG_COLS, splits);
+  if (static_cast<int>(grid.x) > BG_CNT) return cudaErrorInvalidValue;
+  unsigned int* cnt = reinterpret_cast<unsigned int*>(scratch);
+  bias_grad_fused<<<grid, dim3(32, BG_ROWS), 0, st>>>(G, rows, cols, ldg, rps, scratch + BG_CNT, cnt, db, b, vb, lr,
+                                                      mu, wd);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_bias_grad(const uint16_t* G, int rows, int cols, int ldg, float* db, float* scratch,
@@ -1093,8 +1165,8 @@ cudaError_t launch_bias_grad(const uint16_t* G, int rows, int cols, int ldg, flo
   const int splits = bias_grad_splits(rows, cols);
   const int rps = (rows + splits - 1) / splits;
   dim3 grid((cols + BG_COLS - 1) / BG_COLS, splits);
-  bias_grad_partial<<<grid, dim3(32, BG_ROWS), 0, st>>>(G, rows, cols, ldg, rps, scratch);
-  bias_grad_final<<<(cols + 255) / 256, 256, 0, st>>>(scratch, splits, cols, db);
+  bias_grad_partial<<<grid, dim3(32, BG_ROWS), 0, st>>>(G, rows, cols, ldg, rps, scratch + BG_CNT);
+  bias_grad_final<<<(cols + 255) / 256, 256, 0, st>>>(scratch + BG_CNT, splits, cols, db);
   return cudaGetLastError();
 }
 

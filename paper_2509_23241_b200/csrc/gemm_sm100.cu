@@ -16,7 +16,7 @@
 //   warp 1      MMA issuer (one lane): tcgen05.mma kind::f16, fp32 accumulators in TMEM
 //   warps 2..9  epilogue: tcgen05.ld TMEM -> registers -> smem transpose -> bias/ReLU/α/mask
 //               (or the fused SGD update) -> coalesced global row segments
-//   warps 10..13 (BLEND only) operand transform warps
+//   warps 10..17 (BLEND only) operand transform warps (blend in place on the stash tile)
 // TMEM holds two accumulators (2·BN columns) so the epilogue of tile i overlaps the
 // MMAs of tile i+1.
 #include <cuda.h>
@@ -47,17 +47,24 @@ constexpr int SGD_WARPS = 4;
 #define TPS_SGD_NB 2
 #endif
 constexpr int SGD_NB = TPS_SGD_NB;
+#ifndef TPS_SGD_L2HINT
+#define TPS_SGD_L2HINT 1   // fused update: w / v streamed evict-first, GEMM operands evict-last in L2
+#endif
+#ifndef TPS_SGD_PF
+#define TPS_SGD_PF 0       // fused update: L2 prefetch distance in chunks (0 = off)
+#endif
 constexpr int SGD_BUF = 32 * 32 * 4 * 2 + 32 * 32 * 2;   // 10 KiB
+constexpr int XF_WARPS = 8;                                // BLEND operand transform warps
 
 template <int BN, int BLEND, int SGD = 0, int CG = 1>
 struct Cfg {
   static constexpr int NEPI = SGD ? SGD_WARPS : EPI_WARPS;            // epilogue warps
   static constexpr int EPI = SGD ? SGD_WARPS * SGD_NB * SGD_BUF : 0;  // fused-update buffers
   static constexpr int B_BYTES = (BN / CG) * BK * 2;   // this CTA's share of the B tile
-  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES * (BLEND ? 3 : 1);
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES * (BLEND ? 2 : 1);
   static constexpr int STAGES_RAW = (SMEM_BUDGET - 2048 - EPI) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
-  static constexpr int THREADS = 32 * (2 + NEPI + (BLEND ? 4 : 0));
+  static constexpr int THREADS = 32 * (2 + NEPI + (BLEND ? XF_WARPS : 0));
   // accumulator stages in TMEM: the fused-update variant keeps up to 4 so the MMAs can run
   // several tiles ahead of its HBM-bound epilogue
   static constexpr int ACC = (SGD && 512 / BN >= 4) ? 4 : 2;
@@ -87,7 +94,6 @@ __device__ __forceinline__ void tile_split(int t, int num_m, int num_n, int num_
   kb1 = min(num_k, kb0 + kper);
 }
 
-__device__ __forceinline__ float bf16_bits_to_f32(uint32_t h) { return __uint_as_float(h << 16); }
 
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
@@ -134,7 +140,7 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
     for (int s = 0; s < C::STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], 1);
-      ptx::mbar_init(&xform[s], 128);
+      ptx::mbar_init(&xform[s], XF_WARPS * 32);
     }
     for (int a = 0; a < C::ACC; ++a) {
       ptx::mbar_init(&tmem_full[a], 1);
@@ -157,6 +163,7 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
   if (warp == 0) {
     // ===================== TMA producer =====================
     if (lane == 0) {
+      const uint64_t pol_keep = (SGD && TPS_SGD_L2HINT) ? ptx::policy_evict_last() : 0ull;
       int stage = 0;
       uint32_t phase = 0;
       for (int t = cid; t < num_tiles; t += ncl) {
@@ -172,8 +179,14 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
           // every load of this stage completes on the leader CTA's full barrier
           const uint32_t fb = CG == 2 ? ptx::mapa(ptx::smem_u32(&full[stage]), 0) : 0u;
           auto ld2 = [&](void* dst, const CUtensorMap* m, int x, int y) {
-            if (CG == 2) ptx::tma_load_2d_cg2(dst, m, fb, x, y);
-            else ptx::tma_load_2d(dst, m, &full[stage], x, y);
+            if (SGD && TPS_SGD_L2HINT) {   // keep the operands resident while w / v stream through L2
+              if (CG == 2) ptx::tma_load_2d_cg2_hint(dst, m, fb, x, y, pol_keep);
+              else ptx::tma_load_2d_hint(dst, m, &full[stage], x, y, pol_keep);
+            } else if (CG == 2) {
+              ptx::tma_load_2d_cg2(dst, m, fb, x, y);
+            } else {
+              ptx::tma_load_2d(dst, m, &full[stage], x, y);
+            }
           };
           auto ld4 = [&](void* dst, const CUtensorMap* m, int c0, int c1, int c2, int c3) {
             if (CG == 2) ptx::tma_load_4d_cg2(dst, m, fb, c0, c1, c2, c3);
@@ -214,8 +227,9 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
             for (int i = 0; i < BM / 64; ++i) ld2(sA + i * 8192, &tmA, m0 + 64 * i, kb * BK);
           }
           // ---- B tile: BN/CG rows (K-major) or BN/CG columns (MN-major) x 64 K
-          // BLEND: stash -> staging 1, latest -> staging 2; transform warps fill sB
-          uint8_t* dB = BLEND ? sB + C::B_BYTES : sB;
+          // BLEND: stash -> sB (the MMA operand slot), latest -> sB + B_BYTES; the transform
+          // warps overwrite sB with the blend in place
+          uint8_t* dB = sB;
           if (CONV == CONV_DGRAD) {
             // B[(kh',kw',co), ci] = W[co, 2-kh', 2-kw', ci]: the flipped kernel, read in place
             const int cpb = args.cv.C / 64;
@@ -317,6 +331,7 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
     uint64_t* ebar = sgd_bar + e * SGD_NB;
     constexpr int NCH = BN / 32;
     const bool mom = args.mu != 0.0f;
+    const uint64_t pol_stream = TPS_SGD_L2HINT ? ptx::policy_evict_first() : 0ull;
     auto issue = [&](int i) {            // lane 0: TMA loads of chunk i into buffer i % SGD_NB
       const int ti = i / NCH, c = i - ti * NCH;
       const int t = cid + ti * ncl;
@@ -328,11 +343,31 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
       const int buf = i % SGD_NB;
       uint8_t* w_s = ebase + buf * SGD_BUF;
       ptx::mbar_expect_tx(&ebar[buf], mom ? 8192u : 4096u);
-      ptx::tma_load_2d(w_s, &tmW, &ebar[buf], col0, row0);
-      if (mom) ptx::tma_load_2d(w_s + 4096, &tmV, &ebar[buf], col0, row0);
+      if (TPS_SGD_L2HINT) {
+        ptx::tma_load_2d_hint(w_s, &tmW, &ebar[buf], col0, row0, pol_stream);
+        if (mom) ptx::tma_load_2d_hint(w_s + 4096, &tmV, &ebar[buf], col0, row0, pol_stream);
+      } else {
+        ptx::tma_load_2d(w_s, &tmW, &ebar[buf], col0, row0);
+        if (mom) ptx::tma_load_2d(w_s + 4096, &tmV, &ebar[buf], col0, row0);
+      }
     };
-    if (lane == 0)
+    // L2 prefetch of chunk i (TPS_SGD_PF chunks ahead of its shared-memory load), so that load
+    // hits L2 instead of waiting a full DRAM round trip; no shared memory or registers held
+    auto prefetch = [&](int i) {
+      const int ti = i / NCH, c = i - ti * NCH;
+      const int t = cid + ti * ncl;
+      if (t >= num_tiles) return;
+      int mb, nb;
+      tile_coords(t, num_m, num_n, mb, nb);
+      const int row0 = mb * BM * CG + static_cast<int>(rank) * BM + q * 32;
+      ptx::tma_prefetch_2d(&tmW, nb * BN + c * 32, row0);
+      if (mom) ptx::tma_prefetch_2d(&tmV, nb * BN + c * 32, row0);
+    };
+    if (lane == 0) {
+      if (TPS_SGD_PF)
+        for (int i = SGD_NB; i < SGD_NB + TPS_SGD_PF; ++i) prefetch(i);
       for (int i = 0; i < SGD_NB; ++i) issue(i);
+    }
     int i = 0, it = 0;
     for (int t = cid; t < num_tiles; t += ncl, ++it) {
       int mb, nb;
@@ -389,12 +424,19 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
         __syncwarp();
         if (lane == 0) {
           const int col0 = nb * BN + c * 32;
-          ptx::tma_store_2d(&tmW, w_s, col0, row0);
-          if (mom) ptx::tma_store_2d(&tmV, w_s + 4096, col0, row0);
-          ptx::tma_store_2d(&tmQ, w_s + 8192, col0, row0);
+          if (TPS_SGD_L2HINT) {
+            ptx::tma_store_2d_hint(&tmW, w_s, col0, row0, pol_stream);
+            if (mom) ptx::tma_store_2d_hint(&tmV, w_s + 4096, col0, row0, pol_stream);
+            ptx::tma_store_2d_hint(&tmQ, w_s + 8192, col0, row0, pol_stream);
+          } else {
+            ptx::tma_store_2d(&tmW, w_s, col0, row0);
+            if (mom) ptx::tma_store_2d(&tmV, w_s + 4096, col0, row0);
+            ptx::tma_store_2d(&tmQ, w_s + 8192, col0, row0);
+          }
           ptx::bulk_commit();
           ptx::bulk_wait_read<0>();       // the buffer may be refilled once the stores read it
           issue(i + SGD_NB);
+          if (TPS_SGD_PF) prefetch(i + SGD_NB + TPS_SGD_PF);
         }
         __syncwarp();
       }
@@ -526,34 +568,25 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
     }
   } else if (BLEND) {
     // ===================== operand transform: W_res = α·W_stash + β·W_latest =====================
-    const int tt = threadIdx.x - (2 + C::NEPI) * 32;    // 0..127
-    const float xa = args.xa, xb = args.xb;
+    // identical swizzled layouts: the blend is elementwise on raw 16-byte chunks, written back
+    // over the stash tile (each thread reads and writes only its own chunks); packed fp32x2
+    // arithmetic: bf16(fma(β, W_latest, fp32(α·W_stash))) (reading Z14)
+    const int tt = threadIdx.x - (2 + C::NEPI) * 32;    // 0 .. 32·XF_WARPS-1
+    const uint64_t xa2 = ptx::f32x2_splat(args.xa), xb2 = ptx::f32x2_splat(args.xb);
     int stage = 0;
     uint32_t phase = 0;
     for (int t = cid; t < num_tiles; t += ncl) {
       for (int kb = 0; kb < num_k; ++kb) {
         ptx::mbar_wait(&full[stage], phase);
         uint8_t* sB = stages + stage * C::STAGE_BYTES + A_BYTES;
-        const uint4* s = reinterpret_cast<const uint4*>(sB + C::B_BYTES);
-        const uint4* l = reinterpret_cast<const uint4*>(sB + 2 * C::B_BYTES);
-        uint4* o = reinterpret_cast<uint4*>(sB);
-        // identical swizzled layouts: the blend is elementwise on raw 16-byte chunks
-#pragma unroll 4
-        for (int i = tt; i < C::B_BYTES / 16; i += 128) {
+        uint4* s = reinterpret_cast<uint4*>(sB);
+        const uint4* l = reinterpret_cast<const uint4*>(sB + C::B_BYTES);
+#pragma unroll
+        for (int i = tt; i < C::B_BYTES / 16; i += XF_WARPS * 32) {
           const uint4 a = s[i];
           const uint4 b = l[i];
-          const uint32_t aw[4] = {a.x, a.y, a.z, a.w};
-          const uint32_t bw[4] = {b.x, b.y, b.z, b.w};
-          uint32_t ow[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float a0 = bf16_bits_to_f32(aw[e] & 0xFFFFu), a1 = bf16_bits_to_f32(aw[e] >> 16);
-            const float b0 = bf16_bits_to_f32(bw[e] & 0xFFFFu), b1 = bf16_bits_to_f32(bw[e] >> 16);
-            const float r0 = __fadd_rn(__fmul_rn(xa, a0), __fmul_rn(xb, b0));
-            const float r1 = __fadd_rn(__fmul_rn(xa, a1), __fmul_rn(xb, b1));
-            ow[e] = pack_bf16(r0, r1);
-          }
-          o[i] = make_uint4(ow[0], ow[1], ow[2], ow[3]);
+          s[i] = make_uint4(ptx::blend_bf16x2(a.x, b.x, xa2, xb2), ptx::blend_bf16x2(a.y, b.y, xa2, xb2),
+                            ptx::blend_bf16x2(a.z, b.z, xa2, xb2), ptx::blend_bf16x2(a.w, b.w, xa2, xb2));
         }
         ptx::fence_proxy_async_smem();
         ptx::mbar_arrive(&xform[stage]);

@@ -18,6 +18,12 @@ cudaError_t launch_sgd_update(float* w, float* v, const float* g, uint16_t* ver,
 int64_t bias_grad_scratch_floats(int rows, int cols);
 cudaError_t launch_bias_grad(const uint16_t* G, int rows, int cols, int ldg, float* db, float* scratch,
                              cudaStream_t st);
+// The same column sums in ONE launch (the last block of each column block finishes the
+// fixed-order reduction; its arrival counters live at the end of `scratch` and reset
+// themselves), followed, if b != nullptr, by the SGD/momentum step of launch_sgd_update on the
+// fp32 bias b and its momentum vb (same operations, same bits).  Bit-identical db.
+cudaError_t launch_bias_grad_sgd(const uint16_t* G, int rows, int cols, int ldg, float* db, float* scratch, float* b,
+                                 float* vb, float lr, float mu, float wd, cudaStream_t st);
 
 // Softmax cross-entropy forward+backward for `rows` rows of fp32 logits [rows, ldl] with
 // `classes` valid columns: loss_rows[r] = logsumexp(z) - z_y ;

@@ -91,6 +91,32 @@ __device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) 
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<uint64_t>(p)), "r"(bytes)
                : "memory");
 }
+// tensor-map box prefetch into L2 (TMA unit; fire and forget, no shared memory used)
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* m, int32_t x, int32_t y) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(reinterpret_cast<uint64_t>(m)),
+               "r"(x), "r"(y)
+               : "memory");
+}
+// ---- packed fp32x2 arithmetic (sm_100) ---------------------------------------------
+__device__ __forceinline__ uint64_t f32x2_splat(float x) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(r) : "f"(x));
+  return r;
+}
+// bf16(fma(xb, b, fp32(xa·a))) on both halves of two bf16x2 words: one rounded multiply, one
+// fused multiply-add (a single rounding), round-to-nearest-even to bf16 (reading Z14)
+__device__ __forceinline__ uint32_t blend_bf16x2(uint32_t a, uint32_t b, uint64_t xa2, uint64_t xb2) {
+  uint32_t out;
+  asm("{\n\t.reg .b64 pa, pb;\n\t.reg .b32 alo, ahi, blo, bhi, rlo, rhi;\n\t"
+      "shl.b32 alo, %1, 16;\n\tand.b32 ahi, %1, 0xFFFF0000;\n\t"
+      "shl.b32 blo, %2, 16;\n\tand.b32 bhi, %2, 0xFFFF0000;\n\t"
+      "mov.b64 pa, {alo, ahi};\n\tmov.b64 pb, {blo, bhi};\n\t"
+      "mul.rn.f32x2 pa, pa, %3;\n\tfma.rn.f32x2 pa, pb, %4, pa;\n\t"
+      "mov.b64 {rlo, rhi}, pa;\n\tcvt.rn.bf16x2.f32 %0, rhi, rlo;\n\t}"
+      : "=r"(out)
+      : "r"(a), "r"(b), "l"(xa2), "l"(xb2));
+  return out;
+}
 // generic-proxy smem writes -> visible to the async proxy (tensor core / TMA)
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -141,6 +167,41 @@ __device__ __forceinline__ void tma_load_im2col_4d_cg2(void* dst, const CUtensor
           smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(m)), "r"(bar_cluster_addr), "r"(c), "r"(w), "r"(h), "r"(n), "h"(ow), "h"(oh)
       : "memory");
+}
+
+// ---- L2 cache policies (createpolicy) and hinted TMA ------------------------------
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void tma_load_2d_hint(void* dst, const CUtensorMap* m, uint64_t* bar, int32_t x, int32_t y,
+                                                 uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(x), "r"(y), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_cg2_hint(void* dst, const CUtensorMap* m, uint32_t bar_cluster_addr,
+                                                     int32_t x, int32_t y, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(bar_cluster_addr), "r"(x), "r"(y), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_2d_hint(const CUtensorMap* m, const void* src, int32_t x, int32_t y,
+                                                  uint64_t pol) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%2, %3}], [%1], %4;" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(smem_u32(src)), "r"(x), "r"(y), "l"(pol)
+               : "memory");
 }
 
 // ---- tcgen05 ------------------------------------------------------------------

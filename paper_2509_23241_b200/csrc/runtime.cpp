@@ -946,8 +946,10 @@ tps_status do_backward(tps_pipeline* p, int64_t j, int staleness) {
         tps::GemmOperands op{G, Lk.Np, X, Lk.Kp, nullptr};
         TPS_TRY(run_gemm(p, tps::GEMM_WGRAD, op, ga, 2));
       }
-      CUDA_OK(tps::launch_bias_grad(G, rows, Lk.Np, Lk.Np, Lk.db, p->scratch, p->cs));
-      p->launches += 2;
+      // bias gradient and the bias's SGD/momentum step in one launch on the compute stream
+      CUDA_OK(tps::launch_bias_grad_sgd(G, rows, Lk.Np, Lk.Np, Lk.db, p->scratch, Lk.b, Lk.mb, p->lr, p->mu, p->wd,
+                                        p->cs));
+      p->launches += 1;
       // U(j) always directly follows B(j) in the static order (reading Z7), so the update of
       // this layer is issued now: either it already ran in the wgrad epilogue (fuse_update), or
       // it runs on the optimizer stream, HBM-bound, underneath the remaining tensor-bound GEMMs
@@ -964,8 +966,6 @@ tps_status do_backward(tps_pipeline* p, int64_t j, int staleness) {
         TPS_TRY(time_end(p, &tl, us));
         p->launches += 1;
       }
-      CUDA_OK(tps::launch_sgd_update(Lk.b, Lk.mb, Lk.db, nullptr, Lk.Np, p->lr, p->mu, p->wd, us));
-      p->launches += 1;
       CUDA_OK(cudaEventRecord(p->ev_upd_done[k], us));
     }
     if (dst) G = dst;

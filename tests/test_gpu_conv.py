@@ -82,7 +82,9 @@ def test_conv_dgrad_blended_operand(gpu_lib, N, H, W, Ci, Co):
     a, b = 0.7408182, 0.2591818
     tps.conv_gemm(3, N, H, W, Ci, Co, dY, Ws, out, 0, None, 0, a, b, None, W2=Wl)
     torch.cuda.synchronize()
-    Wr = ((torch.tensor(a) * Ws.float()) + (torch.tensor(b) * Wl.float())).to(torch.bfloat16)
+    # fp32 α·W_stash, then one fused multiply-add with β·W_latest (reading Z14), RNE to bf16
+    Wr = ((torch.tensor(a) * Ws.float()).double() + torch.tensor(b, dtype=torch.float32).double() * Wl.double()).float()
+    Wr = Wr.to(torch.bfloat16)
     ref = torch.nn.grad.conv2d_input((N, Ci, H, W), Wr.double().permute(0, 3, 1, 2),
                                      dY.double().permute(0, 3, 1, 2), padding=1)
     close(out, ref.permute(0, 2, 3, 1).reshape(N * H * W, Ci), 9 * Co)
@@ -177,7 +179,9 @@ def test_conv2d_im2col_dgrad(gpu_lib, N, H, W, Ci, Co, k, s, p, blend):
     a, b = (0.7, 0.3) if blend else (0.8948, 0.0)
     tps.conv2d_gemm(3 if blend else 1, N, H, W, Ci, Co, 3, 1, 1, dY, Wt, out, 0, a, b, W2=W2 if blend else None)
     torch.cuda.synchronize()
-    Wr = ((torch.tensor(a) * Wt.float()) + (torch.tensor(b) * W2.float())).to(torch.bfloat16) if blend else Wt
+    # blend on load (reading Z14): fp32 α·W_stash, one fused multiply-add with β·W_latest, RNE to bf16
+    Wr = ((torch.tensor(a) * Wt.float()).double() + torch.tensor(b, dtype=torch.float32).double() * W2.double()).float()
+    Wr = Wr.to(torch.bfloat16) if blend else Wt
     ref = torch.nn.grad.conv2d_input((N, Ci, H, W), Wr.double().permute(0, 3, 1, 2), dY.double().permute(0, 3, 1, 2),
                                      padding=1)
     ref = ref.permute(0, 2, 3, 1).reshape(N * H * W, Ci) * (1.0 if blend else a)

@@ -98,6 +98,7 @@ def test_dgrad_blended_operand(gpu_lib, M, N, K, a, b):
     tps.gemm(tps.GEMM_DGRAD_BLEND, M, N, K, G, K, Ws, N, out, N, 0, None, 0, a, b, X, N, B2=Wl)
     torch.cuda.synchronize()
     af, bf = torch.tensor(a, dtype=torch.float32), torch.tensor(b, dtype=torch.float32)
-    Wr = ((af * Ws.float()) + (bf * Wl.float())).to(torch.bfloat16)   # fp32 mul, fp32 add, RNE
+    # fp32 α·W_stash, then one fused multiply-add with β·W_latest (exact in fp64, one fp32 rounding), RNE
+    Wr = ((af * Ws.float()).double() + bf.double() * Wl.double()).float().to(torch.bfloat16)
     ref = (G.double() @ Wr.double()) * (X > 0).double()
     close_bf16(out, ref, K)
