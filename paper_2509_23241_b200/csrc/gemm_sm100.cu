@@ -50,10 +50,22 @@ constexpr int SGD_NB = TPS_SGD_NB;
 #ifndef TPS_SGD_L2HINT
 #define TPS_SGD_L2HINT 1   // fused update: w / v streamed evict-first, GEMM operands evict-last in L2
 #endif
+#ifndef TPS_SGD_STG
+#define TPS_SGD_STG 1      // fused update: coalesced STG write-back (0 = TMA stores)
+#endif
+// diagnostics only (never set in a product build): 1 = skip the blend arithmetic / the
+// fused-update memory traffic, to measure what the rest of the kernel costs
+#ifndef TPS_DBG_XF
+#define TPS_DBG_XF 0
+#endif
+#ifndef TPS_DBG_SGD
+#define TPS_DBG_SGD 0
+#endif
 #ifndef TPS_SGD_PF
 #define TPS_SGD_PF 0       // fused update: L2 prefetch distance in chunks (0 = off)
 #endif
-constexpr int SGD_BUF = 32 * 32 * 4 * 2 + 32 * 32 * 2;   // 10 KiB
+// w, v fp32 32x32 boxes (+ the bf16 version box when it is TMA-stored)
+constexpr int SGD_BUF = 32 * 32 * 4 * 2 + (TPS_SGD_STG ? 0 : 32 * 32 * 2);
 constexpr int XF_WARPS = 8;                                // BLEND operand transform warps
 
 template <int BN, int BLEND, int SGD = 0, int CG = 1>
@@ -70,8 +82,9 @@ struct Cfg {
   static constexpr int ACC = (SGD && 512 / BN >= 4) ? 4 : 2;
   static constexpr int TMEM_COLS = ACC * BN;
   static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + 1024 + EPI;   // ring | barriers | epilogue
-  // bytes the leader's full barrier waits for per stage (both CTAs of a pair land on it)
-  static constexpr uint32_t TX = (A_BYTES + B_BYTES * (BLEND ? 2 : 1)) * CG;
+  // bytes the leader's full barrier waits for per stage: both CTAs' A (and, without BLEND, B)
+  // land on it; with BLEND each CTA counts its own stash + latest B tiles on its own barrier
+  static constexpr uint32_t TX = A_BYTES * CG + (BLEND ? 2 * B_BYTES : B_BYTES * CG);
 };
 
 __device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int& mb, int& nb) {
@@ -109,9 +122,11 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
   // tcgen05.mma.cta_group::2 stream issued by the leader; each CTA stages its own 128 rows
   // of A and half of the B tile, so per-SM operand traffic drops by a third.
   using C = Cfg<BN, BLEND, SGD, CG>;
-  static_assert(CG == 1 || (!BLEND && BN / CG >= 64), "pair mode: no blend, >= 64 B columns per CTA");
+  static_assert(CG == 1 || BN / CG >= 64, "pair mode: >= 64 B columns per CTA");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1 KiB alignment by pointer arithmetic on the __shared__ array itself, so every derived
+  // pointer keeps the shared address space (LDS/STS rather than generic LD/ST)
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* stages = smem;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
   uint64_t* empty = full + C::STAGES;
@@ -140,7 +155,7 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
     for (int s = 0; s < C::STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], 1);
-      ptx::mbar_init(&xform[s], XF_WARPS * 32);
+      ptx::mbar_init(&xform[s], XF_WARPS * CG);   // one arrival per transform warp (leader's is used)
     }
     for (int a = 0; a < C::ACC; ++a) {
       ptx::mbar_init(&tmem_full[a], 1);
@@ -176,6 +191,7 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
           uint8_t* sA = stages + stage * C::STAGE_BYTES;
           uint8_t* sB = sA + A_BYTES;
           if (rank == 0) ptx::mbar_expect_tx(&full[stage], C::TX);
+          else if (BLEND) ptx::mbar_expect_tx(&full[stage], 2 * C::B_BYTES);   // own B tiles, own barrier
           // every load of this stage completes on the leader CTA's full barrier
           const uint32_t fb = CG == 2 ? ptx::mapa(ptx::smem_u32(&full[stage]), 0) : 0u;
           auto ld2 = [&](void* dst, const CUtensorMap* m, int x, int y) {
@@ -191,6 +207,15 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
           auto ld4 = [&](void* dst, const CUtensorMap* m, int c0, int c1, int c2, int c3) {
             if (CG == 2) ptx::tma_load_4d_cg2(dst, m, fb, c0, c1, c2, c3);
             else ptx::tma_load_4d(dst, m, &full[stage], c0, c1, c2, c3);
+          };
+          // BLEND B tiles complete on this CTA's own barrier: its transform warps wait there
+          auto ldb2 = [&](void* dst, const CUtensorMap* m, int x, int y) {
+            if (BLEND) ptx::tma_load_2d(dst, m, &full[stage], x, y);
+            else ld2(dst, m, x, y);
+          };
+          auto ldb4 = [&](void* dst, const CUtensorMap* m, int c0, int c1, int c2, int c3) {
+            if (BLEND) ptx::tma_load_4d(dst, m, &full[stage], c0, c1, c2, c3);
+            else ld4(dst, m, c0, c1, c2, c3);
           };
           auto ldi = [&](void* dst, const CUtensorMap* m, int c, int w, int h, int n, int ow, int oh) {
             if (CG == 2)
@@ -237,8 +262,8 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
             const int kh = khw / 3, kw = khw % 3;
 #pragma unroll
             for (int i = 0; i < BN / CG / 64; ++i) {
-              ld4(dB + i * 8192, &tmB, n0 + 64 * i, 2 - kw, 2 - kh, co0);
-              if (BLEND) ld4(dB + C::B_BYTES + i * 8192, &tmB2, n0 + 64 * i, 2 - kw, 2 - kh, co0);
+              ldb4(dB + i * 8192, &tmB, n0 + 64 * i, 2 - kw, 2 - kh, co0);
+              if (BLEND) ldb4(dB + C::B_BYTES + i * 8192, &tmB2, n0 + 64 * i, 2 - kw, 2 - kh, co0);
             }
           } else if (CONV == CONV_WGRAD && args.cv.im2col) {
             // B = im2col(X): K block = 64 consecutive output pixels, column (kh, kw, ci)
@@ -265,13 +290,13 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
               ld4(dB + i * 8192, &tmB, ci0, w0 + khw % 3 - 1, h0 + khw / 3 - 1, n_img);
             }
           } else if (!B_MN) {
-            ld2(dB, &tmB, kb * BK, n0);
-            if (BLEND) ld2(dB + C::B_BYTES, &tmB2, kb * BK, n0);
+            ldb2(dB, &tmB, kb * BK, n0);
+            if (BLEND) ldb2(dB + C::B_BYTES, &tmB2, kb * BK, n0);
           } else {
 #pragma unroll
             for (int i = 0; i < BN / CG / 64; ++i) {
-              ld2(dB + i * 8192, &tmB, n0 + 64 * i, kb * BK);
-              if (BLEND) ld2(dB + C::B_BYTES + i * 8192, &tmB2, n0 + 64 * i, kb * BK);
+              ldb2(dB + i * 8192, &tmB, n0 + 64 * i, kb * BK);
+              if (BLEND) ldb2(dB + C::B_BYTES + i * 8192, &tmB2, n0 + 64 * i, kb * BK);
             }
           }
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
@@ -331,6 +356,7 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
     uint64_t* ebar = sgd_bar + e * SGD_NB;
     constexpr int NCH = BN / 32;
     const bool mom = args.mu != 0.0f;
+    const int ncb = (args.N + 31) >> 5;   // 32-column chunks per row block (blocked layout)
     const uint64_t pol_stream = TPS_SGD_L2HINT ? ptx::policy_evict_first() : 0ull;
     auto issue = [&](int i) {            // lane 0: TMA loads of chunk i into buffer i % SGD_NB
       const int ti = i / NCH, c = i - ti * NCH;
@@ -343,7 +369,12 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
       const int buf = i % SGD_NB;
       uint8_t* w_s = ebase + buf * SGD_BUF;
       ptx::mbar_expect_tx(&ebar[buf], mom ? 8192u : 4096u);
-      if (TPS_SGD_L2HINT) {
+      if (args.blk) {
+        // chunk-blocked master / momentum: the 32x32 chunk is one contiguous, pre-swizzled 4 KiB
+        const size_t off = (static_cast<size_t>(row0 >> 5) * ncb + (col0 >> 5)) * 1024;
+        ptx::bulk_load(w_s, args.w + off, 4096u, &ebar[buf]);
+        if (mom) ptx::bulk_load(w_s + 4096, args.v + off, 4096u, &ebar[buf]);
+      } else if (TPS_SGD_L2HINT) {
         ptx::tma_load_2d_hint(w_s, &tmW, &ebar[buf], col0, row0, pol_stream);
         if (mom) ptx::tma_load_2d_hint(w_s + 4096, &tmV, &ebar[buf], col0, row0, pol_stream);
       } else {
@@ -363,7 +394,7 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
       ptx::tma_prefetch_2d(&tmW, nb * BN + c * 32, row0);
       if (mom) ptx::tma_prefetch_2d(&tmV, nb * BN + c * 32, row0);
     };
-    if (lane == 0) {
+    if (lane == 0 && !TPS_DBG_SGD) {
       if (TPS_SGD_PF)
         for (int i = SGD_NB; i < SGD_NB + TPS_SGD_PF; ++i) prefetch(i);
       for (int i = 0; i < SGD_NB; ++i) issue(i);
@@ -386,10 +417,11 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
           ptx::tc_fence_before();
           __syncwarp();
           if (lane == 0) {
-            if (CG == 2) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&tmem_empty[acc]), 0));
+            if (CG == 2) ptx::mbar_arrive_remote(ptx::mapa(ptx::smem_u32(&tmem_empty[acc]), 0));
             else ptx::mbar_arrive(&tmem_empty[acc]);
           }
         }
+        if (TPS_DBG_SGD) continue;
         const int buf = i % SGD_NB;
         ptx::mbar_wait(&ebar[buf], (i / SGD_NB) & 1);
         uint8_t* w_s = ebase + buf * SGD_BUF;
@@ -416,9 +448,61 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
           }
           wrow[pos] = wv;
           if (mom) vrow[pos] = vv;
-          const int qpos = (j >> 1) ^ ((lane >> 1) & 3);  // 64B swizzle of the bf16 row
-          *reinterpret_cast<uint2*>(qrow + qpos * 16 + (j & 1) * 8) =
-              make_uint2(pack_bf16(wv.x, wv.y), pack_bf16(wv.z, wv.w));
+          if (!TPS_SGD_STG) {
+            const int qpos = (j >> 1) ^ ((lane >> 1) & 3);  // 64B swizzle of the bf16 row
+            *reinterpret_cast<uint2*>(qrow + qpos * 16 + (j & 1) * 8) =
+                make_uint2(pack_bf16(wv.x, wv.y), pack_bf16(wv.z, wv.w));
+          }
+        }
+        if (TPS_SGD_STG) {
+          // coalesced write-back: after the row pass, lanes re-read the (swizzled) buffer by
+          // 16-byte column chunks so each store instruction writes whole 128-byte row segments;
+          // the buffer can be refilled as soon as its contents sit in registers
+          __syncwarp();
+          const int col0 = nb * BN + c * 32;
+          const size_t ld = static_cast<size_t>(args.ldo);
+          if (args.blk) {
+            // the chunk's global image equals the buffer: lane-linear, 512 contiguous bytes per
+            // store instruction; the bf16 version goes to its row-major place
+            const size_t off = (static_cast<size_t>(row0 >> 5) * ncb + (col0 >> 5)) * 1024;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              const int o = (k * 32 + lane) * 4;                   // float offset in the chunk
+              const int rr = o >> 5, c4 = ((o >> 2) & 7) ^ (rr & 7);
+              const float4 wv = *reinterpret_cast<const float4*>(w_s + o * 4);
+              __stcs(reinterpret_cast<float4*>(args.w + off + o), wv);
+              if (mom) __stcs(reinterpret_cast<float4*>(args.v + off + o),
+                              *reinterpret_cast<const float4*>(w_s + 4096 + o * 4));
+              const int grow = row0 + rr, gcol = col0 + c4 * 4;
+              if (grow < args.M && gcol < args.N)
+                *reinterpret_cast<uint2*>(args.ver + grow * ld + gcol) =
+                    make_uint2(pack_bf16(wv.x, wv.y), pack_bf16(wv.z, wv.w));
+            }
+          } else {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const int rr = 4 * k + (lane >> 3), ch = lane & 7;
+            const int pos = ch ^ (rr & 7);
+            const int grow = row0 + rr, gcol = col0 + ch * 4;
+            const float4 wv = *reinterpret_cast<const float4*>(w_s + rr * 128 + pos * 16);
+            float4 vv;
+            if (mom) vv = *reinterpret_cast<const float4*>(w_s + 4096 + rr * 128 + pos * 16);
+            if (grow < args.M && gcol < args.N) {
+              __stcs(reinterpret_cast<float4*>(args.w + grow * ld + gcol), wv);
+              if (mom) __stcs(reinterpret_cast<float4*>(args.v + grow * ld + gcol), vv);
+              *reinterpret_cast<uint2*>(args.ver + grow * ld + gcol) =
+                  make_uint2(pack_bf16(wv.x, wv.y), pack_bf16(wv.z, wv.w));   // new bf16 version
+            }
+          }
+          }
+          ptx::fence_proxy_async_smem();   // generic reads of the buffer before the async refill
+          __syncwarp();
+          if (lane == 0) {
+            issue(i + SGD_NB);
+            if (TPS_SGD_PF) prefetch(i + SGD_NB + TPS_SGD_PF);
+          }
+          __syncwarp();
+          continue;
         }
         ptx::fence_proxy_async_smem();
         __syncwarp();
@@ -473,7 +557,7 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
           ptx::tc_fence_before();
           __syncwarp();
           if (lane == 0) {
-            if (CG == 2) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&tmem_empty[acc]), 0));
+            if (CG == 2) ptx::mbar_arrive_remote(ptx::mapa(ptx::smem_u32(&tmem_empty[acc]), 0));
             else ptx::mbar_arrive(&tmem_empty[acc]);
           }
         }
@@ -582,14 +666,18 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
         uint4* s = reinterpret_cast<uint4*>(sB);
         const uint4* l = reinterpret_cast<const uint4*>(sB + C::B_BYTES);
 #pragma unroll
-        for (int i = tt; i < C::B_BYTES / 16; i += XF_WARPS * 32) {
+        for (int i = tt; i < (TPS_DBG_XF ? 0 : C::B_BYTES / 16); i += XF_WARPS * 32) {
           const uint4 a = s[i];
           const uint4 b = l[i];
           s[i] = make_uint4(ptx::blend_bf16x2(a.x, b.x, xa2, xb2), ptx::blend_bf16x2(a.y, b.y, xa2, xb2),
                             ptx::blend_bf16x2(a.z, b.z, xa2, xb2), ptx::blend_bf16x2(a.w, b.w, xa2, xb2));
         }
         ptx::fence_proxy_async_smem();
-        ptx::mbar_arrive(&xform[stage]);
+        __syncwarp();                   // one arrival per warp once all its lanes have fenced
+        if (lane == 0) {
+          if (CG == 2) ptx::mbar_arrive_remote(ptx::mapa(ptx::smem_u32(&xform[stage]), 0));
+          else ptx::mbar_arrive(&xform[stage]);
+        }
         if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
       }
     }
@@ -784,7 +872,18 @@ struct Tiling {
 // traffic per SM by a third; they are used when M fills at least two 128-row blocks and the
 // pair grid still covers the chip.  Env TPS_GEMM_CG=1 forces single-CTA tiles.
 Tiling pick_tiling(int M, int N, int K, int mode, bool sgd) {
-  if (mode == GEMM_DGRAD_BLEND || mode == GEMM_CONV_DGRAD_BLEND) return {1, 128};
+  if (mode == GEMM_DGRAD_BLEND || mode == GEMM_CONV_DGRAD_BLEND) {
+    // three operand tiles per stage: CTA pairs (256 x 256 tiles) halve the L2 -> SM operand
+    // bytes per FLOP, which is what bounds the blended dgrad
+    static int force_cg_b = -1;
+    if (force_cg_b < 0) {
+      const char* e = std::getenv("TPS_GEMM_CG");
+      force_cg_b = e ? std::atoi(e) : 0;
+    }
+    if (force_cg_b != 1 && M >= 256 && N > 128 && ((M + 255) / 256) * ((N + 255) / 256) >= num_sms() / 2 * 3 / 4)
+      return {2, 256};
+    return {1, 128};
+  }
   const int sms0 = num_sms();
   static int no_split = -1;
   if (no_split < 0) {
@@ -959,10 +1058,16 @@ cudaError_t gemm_run(int mode, const GemmOperands& op, const GemmArgs& args_in, 
     case GEMM_WGRAD:
       e = sgd ? dispatch<1, 1, 1>(tl, ta, tb, tb2, em, args, st) : dispatch<1, 1, 0>(tl, ta, tb, tb2, em, args, st);
       break;
-    case GEMM_DGRAD_BLEND: e = launch<128, 0, 1, 1, 0, 1>(ta, tb, tb2, em, args, st); break;
+    case GEMM_DGRAD_BLEND:
+      e = tl.cg == 2 ? launch<256, 0, 1, 1, 0, 2>(ta, tb, tb2, em, args, st)
+                     : launch<128, 0, 1, 1, 0, 1>(ta, tb, tb2, em, args, st);
+      break;
     case GEMM_CONV_FWD: e = dispatch<0, 0, 0, CONV_FWD>(tl, ta, tb, tb2, em, args, st); break;
     case GEMM_CONV_DGRAD: e = dispatch<0, 1, 0, CONV_DGRAD>(tl, ta, tb, tb2, em, args, st); break;
-    case GEMM_CONV_DGRAD_BLEND: e = launch<128, 0, 1, 1, 0, 1, CONV_DGRAD>(ta, tb, tb2, em, args, st); break;
+    case GEMM_CONV_DGRAD_BLEND:
+      e = tl.cg == 2 ? launch<256, 0, 1, 1, 0, 2, CONV_DGRAD>(ta, tb, tb2, em, args, st)
+                     : launch<128, 0, 1, 1, 0, 1, CONV_DGRAD>(ta, tb, tb2, em, args, st);
+      break;
     case GEMM_CONV_WGRAD:
       e = sgd ? dispatch<1, 1, 1, CONV_WGRAD>(tl, ta, tb, tb2, em, args, st)
               : dispatch<1, 1, 0, CONV_WGRAD>(tl, ta, tb, tb2, em, args, st);
