@@ -113,6 +113,28 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
+// TPS_HANG_DETECT (debug builds only): every mbarrier wait gives up after ~20 s of spinning,
+// prints which barrier of which GEMM it was stuck on and traps, turning a hang into an error
+#ifndef TPS_HANG_DETECT
+#define TPS_HANG_DETECT 0
+#endif
+#if TPS_HANG_DETECT
+#define MBAR_WAIT(tag, bar, par)                                                                             \
+  do {                                                                                                       \
+    const long long t0_ = clock64();                                                                         \
+    while (!ptx::mbar_try_wait((bar), (par))) {                                                              \
+      if (clock64() - t0_ > 40000000000LL) {                                                                 \
+        printf("TPS HANG gemm<BN=%d A_MN=%d B_MN=%d BLEND=%d SGD=%d CG=%d CONV=%d> M=%d N=%d K=%d splits=%d "  \
+               "im2col=%d tag=%d block=%d warp=%d par=%u\n", BN, A_MN, B_MN, BLEND, SGD, CG, CONV, args.M,      \
+               args.N, args.K, args.splits, args.cv.im2col, (tag), blockIdx.x, threadIdx.x >> 5, (par));     \
+        __trap();                                                                                            \
+      }                                                                                                      \
+    }                                                                                                        \
+  } while (0)
+#else
+#define MBAR_WAIT(tag, bar, par) ptx::mbar_wait((bar), (par))
+#endif
+
 template <int BN, int A_MN, int B_MN, int BLEND, int SGD, int CG, int CONV>
 __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -187,7 +209,7 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
         const int m0 = mb * BM * CG + static_cast<int>(rank) * BM;          // this CTA's 128 rows
         const int n0 = nb * BN + static_cast<int>(rank) * (BN / CG);       // this CTA's B share
         for (int kb = kb0; kb < kb1; ++kb) {
-          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          MBAR_WAIT(1, &empty[stage], phase ^ 1);
           uint8_t* sA = stages + stage * C::STAGE_BYTES;
           uint8_t* sB = sA + A_BYTES;
           if (rank == 0) ptx::mbar_expect_tx(&full[stage], C::TX);
@@ -313,14 +335,14 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
       for (int t = cid; t < num_tiles; t += ncl, ++it) {
         const int acc = it % C::ACC;
         const uint32_t acc_phase = (it / C::ACC) & 1;
-        ptx::mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
+        MBAR_WAIT(2, &tmem_empty[acc], acc_phase ^ 1);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
         int mb_, nb_, kb0, kb1;
         tile_split(t, num_m, num_n, num_k, args.kper, mb_, nb_, kb0, kb1);
         for (int kb = kb0; kb < kb1; ++kb) {
-          ptx::mbar_wait(&full[stage], phase);
-          if (BLEND) ptx::mbar_wait(&xform[stage], phase);
+          MBAR_WAIT(3, &full[stage], phase);
+          if (BLEND) MBAR_WAIT(4, &xform[stage], phase);
           ptx::tc_fence_after();
           const uint32_t a_addr = ptx::smem_u32(stages + stage * C::STAGE_BYTES);
           const uint32_t b_addr = a_addr + A_BYTES;
@@ -405,7 +427,7 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
       tile_coords(t, num_m, num_n, mb, nb);
       const int acc = it % C::ACC;
       const uint32_t acc_phase = (it / C::ACC) & 1;
-      ptx::mbar_wait(&tmem_full[acc], acc_phase);
+      MBAR_WAIT(5, &tmem_full[acc], acc_phase);
       ptx::tc_fence_after();
       const int row0 = mb * BM * CG + static_cast<int>(rank) * BM + q * 32;
 #pragma unroll 1
@@ -423,7 +445,7 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
         }
         if (TPS_DBG_SGD) continue;
         const int buf = i % SGD_NB;
-        ptx::mbar_wait(&ebar[buf], (i / SGD_NB) & 1);
+        MBAR_WAIT(6, &ebar[buf], (i / SGD_NB) & 1);
         uint8_t* w_s = ebase + buf * SGD_BUF;
         float4* wrow = reinterpret_cast<float4*>(w_s + lane * 128);
         float4* vrow = reinterpret_cast<float4*>(w_s + 4096 + lane * 128);
@@ -544,7 +566,7 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
           : args.out;
       const int acc = it % C::ACC;
       const uint32_t acc_phase = (it / C::ACC) & 1;
-      ptx::mbar_wait(&tmem_full[acc], acc_phase);
+      MBAR_WAIT(7, &tmem_full[acc], acc_phase);
       ptx::tc_fence_after();
       const int row0 = mb * BM * CG + static_cast<int>(rank) * BM + q * 32;
 #pragma unroll 1
@@ -661,7 +683,7 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
     uint32_t phase = 0;
     for (int t = cid; t < num_tiles; t += ncl) {
       for (int kb = 0; kb < num_k; ++kb) {
-        ptx::mbar_wait(&full[stage], phase);
+        MBAR_WAIT(8, &full[stage], phase);
         uint8_t* sB = stages + stage * C::STAGE_BYTES + A_BYTES;
         uint4* s = reinterpret_cast<uint4*>(sB);
         const uint4* l = reinterpret_cast<const uint4*>(sB + C::B_BYTES);
@@ -969,6 +991,9 @@ cudaError_t gemm_run(int mode, const GemmOperands& op, const GemmArgs& args_in, 
   if (args.M <= 0 || args.N <= 0 || args.K <= 0) return cudaSuccess;
   const bool sgd = ((mode == GEMM_WGRAD || mode == GEMM_CONV_WGRAD) && args.epi == EPI_SGD);
   Tiling tl = pick_tiling(args.M, args.N, args.K, mode, sgd);
+#ifdef TPS_DIAG_BLK
+  if (sgd) args.blk = 1;   // timing diagnostic build only: wrong layout, numbers not meaningful
+#endif
   if (tl.splits > 1 &&
       (!args.ws || args.ws_floats < static_cast<int64_t>(tl.splits) * args.M * args.ldo || !args.out_f32 ||
        args.ldo != args.N))

@@ -6,7 +6,7 @@ import json
 import sys
 
 FAMILIES = ["gemm_kernel<256, 0, 0, 0>", "gemm_kernel<256, 0, 1, 0>", "gemm_kernel<256, 1, 1, 0>",
-            "gemm_kernel<128, 0, 1, 1>", "gemm_kernel<64", "gemm_kernel<128", "sgd_update", "bias_grad_partial",
+            "gemm_kernel<128, 0, 1, 1>", "gemm_kernel<64", "gemm_kernel<128", "sgd_update", "bias_grad_fused", "bias_grad_partial",
             "bias_grad_final", "softmax", "loss_mean", "fill_synthetic", "f32_to_bf16", "nccl"]
 LABEL = {"gemm_kernel<256, 0, 0, 0>": "gemm fwd (BN=256)", "gemm_kernel<256, 0, 1, 0>": "gemm dgrad (BN=256)",
          "gemm_kernel<256, 1, 1, 0>": "gemm wgrad (BN=256)", "gemm_kernel<128, 0, 1, 1>": "gemm dgrad blend-on-load"}
