@@ -187,6 +187,11 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
       for (int i = 0; i < SGD_WARPS * SGD_NB; ++i) ptx::mbar_init(&sgd_bar[i], 1);
     ptx::fence_barrier_init();
   }
+  // CTA pairs: the cta_group::2 TMEM allocation handshakes through the PEER's shared memory
+  // (reserved words + a barrier), so both CTAs must be running before either allocates; without
+  // this cluster barrier a leader that starts first can arrive before its peer exists and the
+  // peer then waits for that arrival forever (the rare multi-stream hang, found with cuda-gdb)
+  if (CG == 2) ptx::cluster_sync();
   if (warp == 1) {
     if (CG == 2) ptx::tmem_alloc_cg2(tmem_slot, C::TMEM_COLS);
     else ptx::tmem_alloc(tmem_slot, C::TMEM_COLS);
@@ -710,8 +715,13 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
   else __syncthreads();
   if (warp == 1) {
     ptx::tc_fence_after();
-    if (CG == 2) ptx::tmem_dealloc_cg2(tmem_base, C::TMEM_COLS);
-    else ptx::tmem_dealloc(tmem_base, C::TMEM_COLS);
+    if (CG == 2) {
+      ptx::tmem_relinquish_cg2();
+      ptx::tmem_dealloc_cg2(tmem_base, C::TMEM_COLS);
+    } else {
+      ptx::tmem_relinquish();
+      ptx::tmem_dealloc(tmem_base, C::TMEM_COLS);
+    }
   }
 }
 

@@ -122,7 +122,7 @@ def resnet50_bounds(starts, L):
     return [0, starts[3], starts[5], starts[7], starts[9], starts[11], starts[14], starts[15], L]
 
 
-@pytest.mark.timeout(1500)
+@pytest.mark.timeout(600, method="thread")   # a hung device call cannot block the suite
 def test_resnet50_full_size_eight_stages(gpu_lib):
     """Full ResNet-50 at 224x224, 8 stages on one GPU (LOCAL transport), the SURVEY's 10-step
     parity batch B = 16 (m = 2, b = 8), I-TiMePReSt EQ1; the oracle replays 2 mini-batches."""
