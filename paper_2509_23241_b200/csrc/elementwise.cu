@@ -130,7 +130,8 @@ __global__ void __launch_bounds__(256) bias_grad_fused(const uint16_t* __restric
   const int r_end = min(rows, r_begin + rows_per_split);
   float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   if (c0 < cols) {
-    for (int r = r_begin + threadIdx.y; r < r_end; r += BG_ROWS) {
+#pragma unroll 8
+    for (int r = r_begin + threadIdx.y; r < r_end; r += BG_ROWS) {   // unrolled: loads in flight, same add order
       const uint4 u = __ldg(reinterpret_cast<const uint4*>(G + static_cast<size_t>(r) * ldg + c0));
       const uint32_t w[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
@@ -155,6 +156,7 @@ __global__ void __launch_bounds__(256) bias_grad_fused(const uint16_t* __restric
   if (t == 0) cnt[blockIdx.x] = 0u;               // ready for the next launch (stream-ordered)
   if (c >= cols) return;
   float d = 0.f;
+#pragma unroll 8
   for (int k = 0; k < static_cast<int>(gridDim.y); ++k) d += __ldcg(part + static_cast<size_t>(k) * cols + c);
   db[c] = d;
   if (!b) return;
