@@ -717,7 +717,8 @@ __global__ void __launch_bounds__(256) bn_apply_rows(const uint4* __restrict__ x
   load8f(beta + c0, bt);
   int cur = -1;
   const int step = gridDim.y * ty;
-  for (int r = blockIdx.y * ty + static_cast<int>(threadIdx.x) / tx; r < rows; r += step) {
+#pragma unroll 4
+  for (int r = blockIdx.y * ty + static_cast<int>(threadIdx.x) / tx; r < rows; r += step) {   // loads of 4 rows in flight
     const int seg = r / seg_rows;
     if (seg != cur) {
       cur = seg;
@@ -755,7 +756,8 @@ __global__ void __launch_bounds__(256) bn_bwd_apply_rows(const uint4* __restrict
   float ka[8], kb[8], kc[8], km[8], is[8];
   int cur = -1;
   const int step = gridDim.y * ty;
-  for (int r = blockIdx.y * ty + static_cast<int>(threadIdx.x) / tx; r < rows; r += step) {
+#pragma unroll 4
+  for (int r = blockIdx.y * ty + static_cast<int>(threadIdx.x) / tx; r < rows; r += step) {   // loads of 4 rows in flight
     const int seg = r / seg_rows;
     if (seg != cur) {
       cur = seg;
@@ -1269,16 +1271,26 @@ dim3 bn_rows_grid(int rows, int C8) {
   return dim3(gx, gy);
 }
 
-int bn_chunks(int seg_rows) { return std::max(1, std::min(256, seg_rows / 64)); }
+// row chunks per (segment, channel block) of the partial-sum kernels: enough blocks to fill the
+// GPU (~8 per SM), but at least 16 rows per thread so the per-block fp64 shared-memory
+// reduction stays small next to the streaming loop (64-row chunks made it dominate)
+int bn_chunks(int segs, int seg_rows, int C) {
+  const int C8 = C / 8;
+  const int tx = (C % 8 == 0) ? std::min(C8, 32) : 32, ty = (C % 8 == 0) ? 256 / tx : 8;
+  const int gx = (C % 8 == 0) ? (C8 + tx - 1) / tx : (C + 31) / 32;
+  const int want = (8 * 148 + gx * segs - 1) / (gx * segs);
+  const int cap = std::max(1, seg_rows / (16 * ty));
+  return std::max(1, std::min({256, want, cap}));
+}
 
 int64_t bn_scratch_doubles(int segs, int seg_rows, int C) {
-  return static_cast<int64_t>(segs) * bn_chunks(seg_rows) * C * 2 + static_cast<int64_t>(segs) * C * 2;
+  return static_cast<int64_t>(segs) * bn_chunks(segs, seg_rows, C) * C * 2 + static_cast<int64_t>(segs) * C * 2;
 }
 
 cudaError_t launch_bn_forward(const uint16_t* x, const uint16_t* res, uint16_t* y, const float* gamma,
                               const float* beta, float* mean, float* invstd, int segs, int seg_rows, int C, int relu,
                               double* scratch, cudaStream_t st) {
-  const int chunks = bn_chunks(seg_rows);
+  const int chunks = bn_chunks(segs, seg_rows, C);
   const int64_t rows = static_cast<int64_t>(segs) * seg_rows;
   if (C % 8 == 0) {
     const int C8 = C / 8, tx = std::min(C8, 32);
@@ -1306,7 +1318,7 @@ cudaError_t launch_bn_backward(const uint16_t* dy, const uint16_t* y, const uint
                                const float* invstd, const float* gs, const float* gl, float ga, float gb, int segs,
                                int seg_rows, int C, int relu, uint16_t* dx, uint16_t* dres, float* dgamma,
                                float* dbeta, double* scratch, cudaStream_t st) {
-  const int chunks = bn_chunks(seg_rows);
+  const int chunks = bn_chunks(segs, seg_rows, C);
   double* sums = scratch + static_cast<int64_t>(segs) * chunks * C * 2;
   if (C % 8 == 0) {
     const int C8 = C / 8, tx = std::min(C8, 32);
