@@ -307,6 +307,24 @@ def main():
         except Exception:
             traffic = None
 
+    # per-kind tensor-pipe / DRAM utilisation from the committed ncu --set full capture (one
+    # launch of each stage-GEMM kind at these shapes; read, not measured, by this run)
+    ncu_kinds = None
+    ncu_path = os.path.join(ROOT, "profiles", "r01_ncu_full_summary.json")
+    if os.path.exists(ncu_path):
+        try:
+            names = {"<256, 1, 1, 0, 1, 2, 0>": "wgrad+update", "<256, 0, 0, 0, 0, 2, 0>": "fwd",
+                     "<256, 0, 1, 0, 0, 2, 0>": "dgrad"}
+            ncu_kinds = {"source": "profiles/r01_ncu_full_summary.json (ncu --set full --clock-control none)"}
+            for r in json.load(open(ncu_path)):
+                for key, kind in names.items():
+                    if key in r["kernel"]:
+                        ncu_kinds[kind] = {"time_us": r["time_us"], "tensor_pipe_pct": r["tensor_pipe_pct"],
+                                           "dram_pct": r["dram_pct"],
+                                           "dram_bytes": round((r["dram_read_MB"] + r["dram_write_MB"]) * 1e6)}
+        except Exception:
+            ncu_kinds = None
+
     # ---- e2e: host pools (pinned), H2D inside the timed region, D2H of losses
     e2e = None
     if not args.no_e2e:
@@ -343,7 +361,7 @@ def main():
                  "mem_bytes": memV}
         pV.close()
 
-    mem_all = [memI]
+    mem_all = [{"I": memI, "V": v_out["mem_bytes"] if v_out else None}]
     if world > 1:
         mem_all = [None] * world
         dist.all_gather_object(mem_all, {"I": memI, "V": v_out["mem_bytes"] if v_out else None})
@@ -365,7 +383,7 @@ def main():
                          "frac_of_burst_peak": (achieved / peaks["bf16_tflops"]) if achieved else None,
                          "peak_source": f"{src} bf16_tflops_sustained (MEASURED_PEAKS.json)",
                          "gemm_launches": n_g, "gemm_ms": ms_g, "gemm_share_of_step": gemm_share,
-                         "per_kind": per_kind,
+                         "per_kind": per_kind, "ncu_per_kind": ncu_kinds,
                          "step_tensor_frac": fps * value / world / 1e12 / peak,
                          "update_kernel": {"bound": "hbm", "achieved_gbs": (by_u / (ms_u * 1e-3) / 1e9) if n_u else None,
                                            "peak_gbs": peaks.get("hbm_gbs"), "launches": n_u, "ms": ms_u}},

@@ -194,6 +194,7 @@ struct tps_pipeline {
   cudaStream_t caller = cudaStreamLegacy;              // whose prior work a run's inputs depend on
   cudaEvent_t ev_caller = nullptr;
   std::vector<cudaEvent_t> ev_grad_ready, ev_upd_done;  // per layer
+  cudaEvent_t ev_bias_in = nullptr, ev_bias_done = nullptr;   // bias step on the optimizer stream
   std::vector<cudaEvent_t> ev_fwd_ready, ev_fwd_sent;  // [2 * ng]
   std::vector<cudaEvent_t> ev_act_free;                // [A0]
   cudaEvent_t ev_recv = nullptr, ev_gin_free[2] = {nullptr, nullptr}, ev_gout_ready = nullptr,
@@ -888,6 +889,22 @@ tps_status do_backward(tps_pipeline* p, int64_t j, int staleness) {
     // for V, writes the weights this backward reads
     if (Lk.has_w()) CUDA_OK(cudaStreamWaitEvent(p->cs, p->ev_upd_done[k], 0));
     const uint16_t* X = (k == 0) ? p->act[slot0][0] : p->act[slot][k];
+    // fused update: the bias gradient + bias step only needs G, so it runs on the optimizer
+    // stream underneath this layer's dgrad / wgrad GEMMs; the compute stream waits for it
+    // (ev_bias_done) before the next layer's dgrad overwrites G's ping-pong buffer
+    static const bool bias_side_on = [] {
+      const char* e = std::getenv("TPS_BIAS_SIDE");
+      return !(e && e[0] == '0');
+    }();
+    const bool bias_side = bias_side_on && p->fuse_update && Lk.has_w();
+    if (bias_side) {
+      CUDA_OK(cudaEventRecord(p->ev_bias_in, p->cs));
+      CUDA_OK(cudaStreamWaitEvent(p->s_upd, p->ev_bias_in, 0));
+      CUDA_OK(tps::launch_bias_grad_sgd(G, B * Lk.hw_out, Lk.Np, Lk.Np, Lk.db, p->scratch, Lk.b, Lk.mb, p->lr, p->mu,
+                                        p->wd, p->s_upd));
+      CUDA_OK(cudaEventRecord(p->ev_bias_done, p->s_upd));
+      p->launches += 1;
+    }
     // input gradient first: it must read this layer's weights before a fused update rewrites them
     uint16_t* dst = nullptr;
     if (Lk.gidx > 0) {  // the network's first layer has no input gradient
@@ -946,10 +963,11 @@ tps_status do_backward(tps_pipeline* p, int64_t j, int staleness) {
         tps::GemmOperands op{G, Lk.Np, X, Lk.Kp, nullptr};
         TPS_TRY(run_gemm(p, tps::GEMM_WGRAD, op, ga, 2));
       }
-      // bias gradient and the bias's SGD/momentum step in one launch on the compute stream
-      CUDA_OK(tps::launch_bias_grad_sgd(G, rows, Lk.Np, Lk.Np, Lk.db, p->scratch, Lk.b, Lk.mb, p->lr, p->mu, p->wd,
-                                        p->cs));
-      p->launches += 1;
+      if (!bias_side) {   // bias gradient and the bias's SGD/momentum step in one launch
+        CUDA_OK(tps::launch_bias_grad_sgd(G, rows, Lk.Np, Lk.Np, Lk.db, p->scratch, Lk.b, Lk.mb, p->lr, p->mu, p->wd,
+                                          p->cs));
+        p->launches += 1;
+      }
       // U(j) always directly follows B(j) in the static order (reading Z7), so the update of
       // this layer is issued now: either it already ran in the wgrad epilogue (fuse_update), or
       // it runs on the optimizer stream, HBM-bound, underneath the remaining tensor-bound GEMMs
@@ -966,7 +984,16 @@ tps_status do_backward(tps_pipeline* p, int64_t j, int staleness) {
         TPS_TRY(time_end(p, &tl, us));
         p->launches += 1;
       }
-      CUDA_OK(cudaEventRecord(p->ev_upd_done[k], us));
+      if (bias_side) {
+        // layer k's parameters are final once both the fused wgrad+update (compute stream) and
+        // the bias step (optimizer stream) are done; G may be overwritten once the bias read it
+        CUDA_OK(cudaEventRecord(p->ev_grad_ready[k], p->cs));
+        CUDA_OK(cudaStreamWaitEvent(p->s_upd, p->ev_grad_ready[k], 0));
+        CUDA_OK(cudaEventRecord(p->ev_upd_done[k], p->s_upd));
+        CUDA_OK(cudaStreamWaitEvent(p->cs, p->ev_bias_done, 0));
+      } else {
+        CUDA_OK(cudaEventRecord(p->ev_upd_done[k], us));
+      }
     }
     if (dst) G = dst;
   }
@@ -1479,6 +1506,8 @@ tps_status tps_pipeline_init(const tps_config* c, tps_pipeline** out) {
   }
   p->ev_grad_ready.resize(nl);
   p->ev_upd_done.resize(nl);
+  p->ev_bias_in = new_event();
+  p->ev_bias_done = new_event();
   for (int k = 0; k < nl; ++k) {
     p->ev_grad_ready[k] = new_event();
     p->ev_upd_done[k] = new_event();
@@ -1526,6 +1555,8 @@ tps_status tps_pipeline_destroy(tps_pipeline* p) {
   for (auto e : p->ev_fwd_ready) kill_ev(e);
   for (auto e : p->ev_fwd_sent) kill_ev(e);
   for (auto e : p->ev_act_free) kill_ev(e);
+  kill_ev(p->ev_bias_in);
+  kill_ev(p->ev_bias_done);
   for (auto e : p->ev_grad_ready) kill_ev(e);
   for (auto e : p->ev_upd_done) kill_ev(e);
   for (auto e : p->ev_pool) kill_ev(e);

@@ -1,0 +1,8 @@
+#!/bin/bash
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests/test_gpu_pipeline.py tests/test_gpu_fused_update.py tests/test_gpu_conv.py tests/test_gpu_fullsize.py -q -x -p no:cacheprovider --timeout=900 > gpurun_out/r2v_tests.log 2>&1
+: > gpurun_out/r2v_ab.log
+for v in 1 0 1 0; do
+  TPS_BIAS_SIDE=$v timeout 300 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e --no-v 2>/dev/null | tail -1 | python -c "
+import json,sys; d=json.loads(sys.stdin.read()); print('side=$v', round(d['value']), d['ms_per_step'], {k:v['ms'] for k,v in d['roofline']['per_kind'].items()}, d['clocks']['sm_mhz'], d['losses_first_last'])" >> gpurun_out/r2v_ab.log 2>&1
+done
