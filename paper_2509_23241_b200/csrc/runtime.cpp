@@ -782,9 +782,11 @@ tps_status do_forward(tps_pipeline* p, int64_t j, int a0, int cnt, const void* x
     if (L0.im2col) {
       uint16_t* xs = p->x_stage[slot0] + static_cast<size_t>(r0) * p->in0_elems;
       CUDA_OK(cudaMemcpyAsync(xs, x, static_cast<size_t>(nr) * p->in0_elems * 2, cudaMemcpyDefault, p->s_fin));
-    } else if (L0.kind == TPS_LAYER_LINEAR) {
-      const size_t w = static_cast<size_t>(L0.in) * 2;
+    } else if (L0.kind == TPS_LAYER_LINEAR && L0.in != L0.Kp) {
+      const size_t w = static_cast<size_t>(L0.in) * 2;   // pad the rows to the 16-aligned ld
       CUDA_OK(cudaMemcpy2DAsync(X, static_cast<size_t>(L0.Kp) * 2, x, w, w, nr, cudaMemcpyDefault, p->s_fin));
+    } else if (L0.kind == TPS_LAYER_LINEAR) {
+      CUDA_OK(cudaMemcpyAsync(X, x, static_cast<size_t>(nr) * L0.Kp * 2, cudaMemcpyDefault, p->s_fin));
     } else {
       CUDA_OK(cudaMemcpyAsync(X, x, static_cast<size_t>(nr) * L0.in_elems() * 2, cudaMemcpyDefault, p->s_fin));
     }
@@ -896,7 +898,10 @@ tps_status do_backward(tps_pipeline* p, int64_t j, int staleness) {
       const char* e = std::getenv("TPS_BIAS_SIDE");
       return !(e && e[0] == '0');
     }();
-    const bool bias_side = bias_side_on && p->fuse_update && Lk.has_w();
+    // only where the bias pass is worth hiding: for small layers the two extra cross-stream
+    // events cost more latency than the pass itself (C1 lost 30 % with it)
+    const bool bias_side = bias_side_on && p->fuse_update && Lk.has_w() &&
+                           static_cast<int64_t>(B) * Lk.hw_out * Lk.Np >= (int64_t{1} << 20);
     if (bias_side) {
       CUDA_OK(cudaEventRecord(p->ev_bias_in, p->cs));
       CUDA_OK(cudaStreamWaitEvent(p->s_upd, p->ev_bias_in, 0));
