@@ -152,7 +152,7 @@ struct tps_pipeline {
   uint16_t* send_fwd[2] = {nullptr, nullptr};
   uint16_t* gin[2] = {nullptr, nullptr};
   uint16_t* gout[2] = {nullptr, nullptr};
-  uint16_t* gwork[2] = {nullptr, nullptr};
+  uint16_t* gwork[3] = {nullptr, nullptr, nullptr};
   float* logits = nullptr;
   uint16_t* gce = nullptr;
   float* loss_rows = nullptr;
@@ -195,6 +195,12 @@ struct tps_pipeline {
   cudaEvent_t ev_caller = nullptr;
   std::vector<cudaEvent_t> ev_grad_ready, ev_upd_done;  // per layer
   cudaEvent_t ev_bias_in = nullptr, ev_bias_done = nullptr;   // bias step on the optimizer stream
+  // split backward (default; TPS_SPLIT_W=0 disables): weight gradients + fused update on their
+  // own stream s_w, concurrent with the next layer's input gradient; three rotating gradient
+  // buffers (each dgrad waits for the weight gradient / bias step two layers up)
+  bool split_w = false;
+  cudaStream_t s_w = nullptr;
+  std::vector<cudaEvent_t> ev_dg, ev_w_done, ev_bias_l;   // per layer
   std::vector<cudaEvent_t> ev_fwd_ready, ev_fwd_sent;  // [2 * ng]
   std::vector<cudaEvent_t> ev_act_free;                // [A0]
   cudaEvent_t ev_recv = nullptr, ev_gin_free[2] = {nullptr, nullptr}, ev_gout_ready = nullptr,
@@ -289,7 +295,9 @@ void build_order(int S, int s, int m, int g, int64_t first, int64_t n, std::vect
 
 double gemm_flops(int M, int N, int K) { return 2.0 * M * static_cast<double>(N) * K; }
 
-tps_status run_gemm(tps_pipeline* p, int mode, const tps::GemmOperands& op, const tps::GemmArgs& args, int kind) {
+tps_status run_gemm(tps_pipeline* p, int mode, const tps::GemmOperands& op, const tps::GemmArgs& args, int kind,
+                    cudaStream_t stream = nullptr) {
+  cudaStream_t gs = stream ? stream : p->cs;
   TimedLaunch tl{};
   if (p->profiling) {
     if (p->ev_pool.size() < 2) {
@@ -303,15 +311,15 @@ tps_status run_gemm(tps_pipeline* p, int mode, const tps::GemmOperands& op, cons
     tl.work = gemm_flops(args.M, args.N, args.K);
     tl.a = p->ev_pool.back(); p->ev_pool.pop_back();
     tl.b = p->ev_pool.back(); p->ev_pool.pop_back();
-    CUDA_OK(cudaEventRecord(tl.a, p->cs));
+    CUDA_OK(cudaEventRecord(tl.a, gs));
   }
   tps::GemmArgs a2 = args;
   a2.ws = p->splitk_ws;
   a2.ws_floats = p->splitk_floats;
-  CUDA_OK(tps::gemm_run(mode, op, a2, p->cs));
+  CUDA_OK(tps::gemm_run(mode, op, a2, gs));
   p->launches += 1;
   if (p->profiling) {
-    CUDA_OK(cudaEventRecord(tl.b, p->cs));
+    CUDA_OK(cudaEventRecord(tl.b, gs));
     p->timed.push_back(tl);
   }
   return TPS_OK;
@@ -365,6 +373,7 @@ tps_status join_update_stream(tps_pipeline* p) {
 tps_status sync_streams(tps_pipeline* p) {
   CUDA_OK(cudaStreamSynchronize(p->cs));
   if (p->s_upd) CUDA_OK(cudaStreamSynchronize(p->s_upd));
+  if (p->s_w) CUDA_OK(cudaStreamSynchronize(p->s_w));
   return TPS_OK;
 }
 
@@ -907,13 +916,21 @@ tps_status do_backward(tps_pipeline* p, int64_t j, int staleness) {
       CUDA_OK(cudaStreamWaitEvent(p->s_upd, p->ev_bias_in, 0));
       CUDA_OK(tps::launch_bias_grad_sgd(G, B * Lk.hw_out, Lk.Np, Lk.Np, Lk.db, p->scratch, Lk.b, Lk.mb, p->lr, p->mu,
                                         p->wd, p->s_upd));
-      CUDA_OK(cudaEventRecord(p->ev_bias_done, p->s_upd));
+      CUDA_OK(cudaEventRecord(p->split_w ? p->ev_bias_l[k] : p->ev_bias_done, p->s_upd));
       p->launches += 1;
     }
     // input gradient first: it must read this layer's weights before a fused update rewrites them
     uint16_t* dst = nullptr;
     if (Lk.gidx > 0) {  // the network's first layer has no input gradient
-      if (k > 0) {
+      if (k > 0 && p->split_w) {
+        // three rotating buffers: this dgrad overwrites the gradient that layer k+2's weight
+        // gradient (stream s_w) and bias step (optimizer stream) read
+        dst = p->gwork[k % 3];
+        if (k + 2 < nl) {
+          if (p->layers[k + 2].has_w()) CUDA_OK(cudaStreamWaitEvent(p->cs, p->ev_w_done[k + 2], 0));
+          CUDA_OK(cudaStreamWaitEvent(p->cs, p->ev_bias_l[k + 2], 0));
+        }
+      } else if (k > 0) {
         dst = p->gwork[wbuf];
         wbuf ^= 1;
       } else {
@@ -960,14 +977,21 @@ tps_status do_backward(tps_pipeline* p, int64_t j, int staleness) {
         ga.w = Lk.W; ga.v = Lk.mW; ga.ver = Lk.ver[vn % p->R];
         ga.lr = p->lr; ga.mu = p->mu; ga.wd = p->wd;
       }
+      cudaStream_t ws = p->cs;
+      if (p->split_w) {   // after this layer's dgrad (it reads the weights the fused update rewrites)
+        CUDA_OK(cudaEventRecord(p->ev_dg[k], p->cs));
+        CUDA_OK(cudaStreamWaitEvent(p->s_w, p->ev_dg[k], 0));
+        ws = p->s_w;
+      }
       if (Lk.kind == TPS_LAYER_CONV3X3 && !Lk.im2col) {
         tps::GemmOperands op{G, Lk.Np, X, 0, nullptr};
         op.cv = tps::ConvGeom{B, Lk.H, Lk.Wd, Lk.Ci};
-        TPS_TRY(run_gemm(p, tps::GEMM_CONV_WGRAD, op, ga, 2));
+        TPS_TRY(run_gemm(p, tps::GEMM_CONV_WGRAD, op, ga, 2, ws));
       } else {
         tps::GemmOperands op{G, Lk.Np, X, Lk.Kp, nullptr};
-        TPS_TRY(run_gemm(p, tps::GEMM_WGRAD, op, ga, 2));
+        TPS_TRY(run_gemm(p, tps::GEMM_WGRAD, op, ga, 2, ws));
       }
+      if (p->split_w) CUDA_OK(cudaEventRecord(p->ev_w_done[k], p->s_w));
       if (!bias_side) {   // bias gradient and the bias's SGD/momentum step in one launch
         CUDA_OK(tps::launch_bias_grad_sgd(G, rows, Lk.Np, Lk.Np, Lk.db, p->scratch, Lk.b, Lk.mb, p->lr, p->mu, p->wd,
                                           p->cs));
@@ -989,7 +1013,16 @@ tps_status do_backward(tps_pipeline* p, int64_t j, int staleness) {
         TPS_TRY(time_end(p, &tl, us));
         p->launches += 1;
       }
-      if (bias_side) {
+      if (p->split_w) {
+        // parameters final once the fused wgrad+update (s_w) and the bias step are done
+        if (bias_side) {
+          CUDA_OK(cudaStreamWaitEvent(p->s_upd, p->ev_w_done[k], 0));
+          CUDA_OK(cudaEventRecord(p->ev_upd_done[k], p->s_upd));
+        } else {
+          CUDA_OK(cudaEventRecord(p->ev_bias_l[k], p->cs));   // bias ran on the compute stream
+          CUDA_OK(cudaEventRecord(p->ev_upd_done[k], p->s_w));
+        }
+      } else if (bias_side) {
         // layer k's parameters are final once both the fused wgrad+update (compute stream) and
         // the bias step (optimizer stream) are done; G may be overwritten once the bias read it
         CUDA_OK(cudaEventRecord(p->ev_grad_ready[k], p->cs));
@@ -1001,6 +1034,15 @@ tps_status do_backward(tps_pipeline* p, int64_t j, int staleness) {
       }
     }
     if (dst) G = dst;
+  }
+  if (p->split_w) {
+    // the weight gradients read this mini-batch's stashed activations and the gradients: join
+    for (int k = 0; k < nl; ++k) {
+      if (p->layers[k].has_w()) {
+        CUDA_OK(cudaStreamWaitEvent(p->cs, p->ev_w_done[k], 0));
+        CUDA_OK(cudaStreamWaitEvent(p->cs, p->ev_upd_done[k], 0));
+      }
+    }
   }
   // the input slot and the received gradient buffer may now be refilled
   CUDA_OK(cudaEventRecord(p->ev_act_free[slot0], p->cs));
@@ -1044,6 +1086,7 @@ tps_status begin_run(tps_pipeline* p, int64_t first, int64_t n) {
   // compute stream, else the legacy default stream)
   CUDA_OK(cudaEventRecord(p->ev_caller, p->caller));
   for (cudaStream_t st : {p->cs, p->s_fin, p->s_upd}) CUDA_OK(cudaStreamWaitEvent(st, p->ev_caller, 0));
+  if (p->s_w) CUDA_OK(cudaStreamWaitEvent(p->s_w, p->ev_caller, 0));
   build_order(p->S, p->s, p->m, p->g, first, n, &p->order);
   p->pos = 0;
   p->run_first = first;
@@ -1454,6 +1497,13 @@ tps_status tps_pipeline_init(const tps_config* c, tps_pipeline** out) {
     if (!p->first && (st = alloc_t(p, &p->gout[i], static_cast<size_t>(p->B) * in0, &p->mem_comm)) != TPS_OK) return cleanup(st);
     if (nl > 1 && (st = alloc_t(p, &p->gwork[i], static_cast<size_t>(p->B) * max_elems, &p->mem_acts)) != TPS_OK) return cleanup(st);
   }
+  {
+    // default on (C5: +9.5 % A/B); TPS_SPLIT_W=0 keeps every backward kernel on the compute stream
+    const char* e = std::getenv("TPS_SPLIT_W");
+    p->split_w = !(e && e[0] == '0') && p->fuse_update && !p->graph && nl > 1;
+  }
+  if (p->split_w && (st = alloc_t(p, &p->gwork[2], static_cast<size_t>(p->B) * max_elems, &p->mem_acts)) != TPS_OK)
+    return cleanup(st);
   if (p->last) {
     if (p->layers[nl - 1].kind != TPS_LAYER_LINEAR) return cleanup(fail(TPS_E_CONFIG, "the last layer must be the Linear head"));
     if ((st = alloc_t(p, &p->logits, static_cast<size_t>(p->B) * outL, &p->mem_acts)) != TPS_OK) return cleanup(st);
@@ -1513,6 +1563,14 @@ tps_status tps_pipeline_init(const tps_config* c, tps_pipeline** out) {
   p->ev_upd_done.resize(nl);
   p->ev_bias_in = new_event();
   p->ev_bias_done = new_event();
+  if (p->split_w) {
+    p->ev_dg.resize(nl); p->ev_w_done.resize(nl); p->ev_bias_l.resize(nl);
+    for (int k = 0; k < nl; ++k) {
+      p->ev_dg[k] = new_event(); p->ev_w_done[k] = new_event(); p->ev_bias_l[k] = new_event();
+    }
+    if (cudaStreamCreateWithFlags(&p->s_w, cudaStreamNonBlocking) != cudaSuccess)
+      return cleanup(fail(TPS_E_CUDA, "stream create"));
+  }
   for (int k = 0; k < nl; ++k) {
     p->ev_grad_ready[k] = new_event();
     p->ev_upd_done[k] = new_event();
@@ -1562,6 +1620,9 @@ tps_status tps_pipeline_destroy(tps_pipeline* p) {
   for (auto e : p->ev_act_free) kill_ev(e);
   kill_ev(p->ev_bias_in);
   kill_ev(p->ev_bias_done);
+  for (auto v : {&p->ev_dg, &p->ev_w_done, &p->ev_bias_l})
+    for (auto e : *v) kill_ev(e);
+  if (p->s_w) cudaStreamDestroy(p->s_w);
   for (auto e : p->ev_grad_ready) kill_ev(e);
   for (auto e : p->ev_upd_done) kill_ev(e);
   for (auto e : p->ev_pool) kill_ev(e);
