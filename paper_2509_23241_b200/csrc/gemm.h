@@ -48,8 +48,6 @@ struct GemmArgs {
   int epi;
   float* w; float* v; uint16_t* ver;
   float lr, mu, wd;
-  int blk;                    // 1: w / v stored chunk-blocked (each 32x32 chunk one contiguous,
-                              // 128B-swizzled 4 KiB image); experimental, not used by the runtime
   ConvGeom cv;                // copied from GemmOperands by gemm_run
   // split-K (weight gradients whose output tiles cannot fill the GPU): fp32 workspace of
   // ws_floats floats supplied by the caller; gemm_run sets splits / kper and reduces

@@ -387,7 +387,6 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
     uint64_t* ebar = sgd_bar + e * SGD_NB;
     constexpr int NCH = BN / 32;
     const bool mom = args.mu != 0.0f;
-    const int ncb = (args.N + 31) >> 5;   // 32-column chunks per row block (blocked layout)
     const uint64_t pol_stream = TPS_SGD_L2HINT ? ptx::policy_evict_first() : 0ull;
     auto issue = [&](int i) {            // lane 0: TMA loads of chunk i into buffer i % SGD_NB
       const int ti = i / NCH, c = i - ti * NCH;
@@ -400,12 +399,7 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
       const int buf = i % SGD_NB;
       uint8_t* w_s = ebase + buf * SGD_BUF;
       ptx::mbar_expect_tx(&ebar[buf], mom ? 8192u : 4096u);
-      if (args.blk) {
-        // chunk-blocked master / momentum: the 32x32 chunk is one contiguous, pre-swizzled 4 KiB
-        const size_t off = (static_cast<size_t>(row0 >> 5) * ncb + (col0 >> 5)) * 1024;
-        ptx::bulk_load(w_s, args.w + off, 4096u, &ebar[buf]);
-        if (mom) ptx::bulk_load(w_s + 4096, args.v + off, 4096u, &ebar[buf]);
-      } else if (TPS_SGD_L2HINT) {
+      if (TPS_SGD_L2HINT) {
         ptx::tma_load_2d_hint(w_s, &tmW, &ebar[buf], col0, row0, pol_stream);
         if (mom) ptx::tma_load_2d_hint(w_s + 4096, &tmV, &ebar[buf], col0, row0, pol_stream);
       } else {
@@ -492,24 +486,6 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
           __syncwarp();
           const int col0 = nb * BN + c * 32;
           const size_t ld = static_cast<size_t>(args.ldo);
-          if (args.blk) {
-            // the chunk's global image equals the buffer: lane-linear, 512 contiguous bytes per
-            // store instruction; the bf16 version goes to its row-major place
-            const size_t off = (static_cast<size_t>(row0 >> 5) * ncb + (col0 >> 5)) * 1024;
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-              const int o = (k * 32 + lane) * 4;                   // float offset in the chunk
-              const int rr = o >> 5, c4 = ((o >> 2) & 7) ^ (rr & 7);
-              const float4 wv = *reinterpret_cast<const float4*>(w_s + o * 4);
-              __stcs(reinterpret_cast<float4*>(args.w + off + o), wv);
-              if (mom) __stcs(reinterpret_cast<float4*>(args.v + off + o),
-                              *reinterpret_cast<const float4*>(w_s + 4096 + o * 4));
-              const int grow = row0 + rr, gcol = col0 + c4 * 4;
-              if (grow < args.M && gcol < args.N)
-                *reinterpret_cast<uint2*>(args.ver + grow * ld + gcol) =
-                    make_uint2(pack_bf16(wv.x, wv.y), pack_bf16(wv.z, wv.w));
-            }
-          } else {
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
             const int rr = 4 * k + (lane >> 3), ch = lane & 7;
@@ -524,7 +500,6 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
               *reinterpret_cast<uint2*>(args.ver + grow * ld + gcol) =
                   make_uint2(pack_bf16(wv.x, wv.y), pack_bf16(wv.z, wv.w));   // new bf16 version
             }
-          }
           }
           ptx::fence_proxy_async_smem();   // generic reads of the buffer before the async refill
           __syncwarp();
@@ -1013,9 +988,6 @@ cudaError_t gemm_run(int mode, const GemmOperands& op, const GemmArgs& args_in, 
   if (args.M <= 0 || args.N <= 0 || args.K <= 0) return cudaSuccess;
   const bool sgd = ((mode == GEMM_WGRAD || mode == GEMM_CONV_WGRAD) && args.epi == EPI_SGD);
   Tiling tl = pick_tiling(args.M, args.N, args.K, mode, sgd);
-#ifdef TPS_DIAG_BLK
-  if (sgd) args.blk = 1;   // timing diagnostic build only: wrong layout, numbers not meaningful
-#endif
   if (tl.splits > 1 &&
       (!args.ws || args.ws_floats < static_cast<int64_t>(tl.splits) * args.M * args.ldo || !args.out_f32 ||
        args.ldo != args.N))

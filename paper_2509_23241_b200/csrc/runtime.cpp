@@ -1568,7 +1568,14 @@ tps_status tps_pipeline_init(const tps_config* c, tps_pipeline** out) {
     for (int k = 0; k < nl; ++k) {
       p->ev_dg[k] = new_event(); p->ev_w_done[k] = new_event(); p->ev_bias_l[k] = new_event();
     }
-    if (cudaStreamCreateWithFlags(&p->s_w, cudaStreamNonBlocking) != cudaSuccess)
+    // TPS_SW_PRIO: 0 = default priority (default), 1 = lowest (the dgrad chain is the critical
+    // path), 2 = highest
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    const char* e = std::getenv("TPS_SW_PRIO");
+    const int mode = e ? std::atoi(e) : 0;
+    if (cudaStreamCreateWithPriority(&p->s_w, cudaStreamNonBlocking, mode == 1 ? lo : (mode == 2 ? hi : 0)) !=
+        cudaSuccess)
       return cleanup(fail(TPS_E_CUDA, "stream create"));
   }
   for (int k = 0; k < nl; ++k) {
