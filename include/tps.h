@@ -25,8 +25,8 @@
  *     next tps_synchronize().  Device-side failures are latched and reported by
  *     tps_synchronize() (TPS_E_CUDA / TPS_E_NCCL).
  *   - one host thread drives a handle; handles are not re-entrant.
- *   - the handle owns every device allocation it makes (cudaMalloc) and frees
- *     them in tps_pipeline_destroy().
+ *   - the handle owns every device allocation it makes (cudaMalloc, or the
+ *     caller's dev_alloc hook) and frees them in tps_pipeline_destroy().
  *   - there is no CPU fallback: without an sm_100 device every compute call
  *     returns TPS_E_ARCH.
  */
@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define TPS_ABI_VERSION 2
+#define TPS_ABI_VERSION 3
 
 typedef enum {
   TPS_OK = 0,
@@ -168,6 +168,24 @@ typedef struct {
   int32_t num_layer_specs;      /* 0 => MLP from dims; else == num_layers entries below  */
   const tps_layer* layer_specs; /* host; image networks (dims[0] = H·W·C of the input,
                                    dims[num_layers] = classes; other dims ignored)    */
+  int32_t max_inflight;         /* mini-batches in flight K; 0 => K_s = S - s (reading Z6).
+                                   Another value is accepted for S = 1 only: a one-stage
+                                   pipeline with K in flight sees the steady staleness
+                                   δ = K - 1 of a stage at depth K (the staleness sweep of
+                                   BASELINE.json configs[1] on one GPU); TPS_E_CONFIG else */
+  int32_t staleness_mode;       /* 0 => an explicit staleness passed to tps_stage_backward
+                                   must equal the logged δ (scheduled run).  1 => standalone
+                                   microbenchmark: any δ >= 0 whose version is still in the
+                                   ring (v_latest - δ >= max(0, v_latest - R + 1)) is used
+                                   as given (SURVEY §8(b) "staleness override")          */
+  /* Optional device allocator (e.g. PyTorch's caching allocator, so the framework's
+   * memory accounting sees the handle's buffers).  NULL => cudaMalloc / cudaFree.
+   * dev_alloc returns a device pointer (256-byte aligned) or NULL on failure
+   * (=> TPS_E_OOM); dev_free is called for every such pointer by
+   * tps_pipeline_destroy after a device synchronize.                               */
+  void* (*dev_alloc)(size_t bytes, void* ctx);
+  void (*dev_free)(void* ptr, void* ctx);
+  void* alloc_ctx;
   int32_t reserved[4];
 } tps_config;
 
@@ -204,7 +222,11 @@ tps_status tps_stage_forward(tps_pipeline* p, int64_t mb, int32_t micro, int32_t
 /* Collective backward of mini-batch mb on the resolved weight:
  * V: latest; I: α·W_stash(v_fwd) + β·W_latest with δ = v_latest - v_fwd.
  * staleness = -1 => δ from the version log; >= 0 => must equal the logged δ in
- * a scheduled run (TPS_E_STALENESS otherwise).                                */
+ * a scheduled run (staleness_mode 0), or (staleness_mode 1, microbenchmark) any δ
+ * whose version is still live in the ring.  TPS_E_STALENESS when δ != the logged
+ * value (mode 0), when V is given δ > 0 (V has no stash), or when version
+ * v_latest - δ is no longer (or not yet) held; nothing is enqueued then and the
+ * call may be retried.  TPS_E_ORDER if B(mb) is not the stage's next event.     */
 tps_status tps_stage_backward(tps_pipeline* p, int64_t mb, int32_t staleness);
 /* SGD/momentum update of every layer of the stage from the gradients of mb;
  * writes the new bf16 version into a free ring slot (I) or in place (V); the
@@ -260,9 +282,14 @@ tps_status tps_init_weights_synthetic(tps_pipeline* p);
 tps_status tps_get_losses(tps_pipeline* p, float* out, int64_t cap, int64_t* n);
 tps_status tps_get_trace(tps_pipeline* p, tps_event* out, int64_t cap, int64_t* n);
 tps_status tps_clear_trace(tps_pipeline* p);
-/* Bytes held by category; peak = max over the handle's life of their sum. */
+/* Bytes held by category; peak = max over the handle's life of their sum (the library's
+ * own allocation arithmetic; every buffer is allocated by tps_pipeline_init).       */
 tps_status tps_memory_stats(tps_pipeline* p, int64_t* weights, int64_t* stash, int64_t* acts,
                             int64_t* optim, int64_t* comm, int64_t* peak);
+/* Device-observed bytes: the drop of cudaMemGetInfo's free memory across the allocations
+ * of tps_pipeline_init (allocation granularity included; 0 when a dev_alloc hook served
+ * them from a cache).  Meaningful when nothing else allocates concurrently.          */
+tps_status tps_memory_observed(tps_pipeline* p, int64_t* device_bytes);
 /* Kernel timing: when enabled, CUDA events bracket every GEMM launch on the
  * compute stream; tps_kernel_stats returns launch count, summed device ms and
  * summed algorithmic FLOPs of GEMM kind `which` (0 fwd, 1 dgrad, 2 wgrad,

@@ -46,6 +46,8 @@ class Config:
     #          | {"kind": "pool2", "c", "h", "w"}; every layer but the last is followed by ReLU
     #          (pools pass values through); the last is the Linear head.
     layers: list | None = None
+    # mini-batches in flight for a ONE-stage pipeline (0 => S - s; schedule.inflight)
+    max_inflight: int = 0
 
     @property
     def S(self) -> int:
@@ -128,7 +130,7 @@ def run(cfg: Config, xs: list[np.ndarray], ys: list[np.ndarray],
     grads: dict[tuple[int, int], tuple[list, list]] = {}      # (s, j) -> (dW list, db list)
     trace: list[TraceRow] = []
 
-    fired, _ = schedule.execute(S, m, cfg.M)
+    fired, _ = schedule.execute(S, m, cfg.M, cfg.max_inflight)
     for s, e in fired:
         ls = layers[s]
         if e.kind == "F":

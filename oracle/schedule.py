@@ -31,14 +31,19 @@ class Event:
     micro: int = -1    # micro-batch index a for "F"; -1 otherwise
 
 
-def inflight(S: int, s: int, M: int) -> int:
-    """K_s = min(S - s, M) (reading Z6)."""
+def inflight(S: int, s: int, M: int, K: int = 0) -> int:
+    """K_s = min(S - s, M) (reading Z6).  K > 0 overrides S - s for a ONE-stage pipeline
+    (tps_config.max_inflight): a single stage keeping K mini-batches in flight, i.e. the
+    staleness a stage at depth K sees (the staleness sweep of BASELINE.json configs[1])."""
+    if K:
+        assert S == 1, "an in-flight override is defined for S = 1 only"
+        return min(K, M)
     return min(S - s, M)
 
 
-def stage_order(S: int, s: int, m: int, M: int) -> list[Event]:
+def stage_order(S: int, s: int, m: int, M: int, K: int = 0) -> list[Event]:
     """Static per-stage event list L_s (reading Z7; SURVEY Appendix A rule)."""
-    K = inflight(S, s, M)
+    K = inflight(S, s, M, K)
     ev: list[Event] = []
     for j in range(K):
         ev += [Event("F", j, a) for a in range(m)]
@@ -61,14 +66,14 @@ class TraceRow:
     delta: int         # B only: v_latest - v_used (reading Z5); 0 otherwise
 
 
-def execute(S: int, m: int, M: int) -> tuple[list[tuple[int, Event]], list[TraceRow]]:
+def execute(S: int, m: int, M: int, K: int = 0) -> tuple[list[tuple[int, Event]], list[TraceRow]]:
     """Dependency-driven replay of all stages' static orders.
 
     Dependencies: F(j,a)@s needs F(j,a)@s-1; B(j)@s needs B(j)@s+1
     (the last stage needs its own F(j, m-1), implied by its order); U(j) follows
     B(j) on the same stage.  Returns the global firing order and the trace.
     """
-    orders = [stage_order(S, s, m, M) for s in range(S)]
+    orders = [stage_order(S, s, m, M, K) for s in range(S)]
     ptr = [0] * S
     done: set[tuple[int, Event]] = set()
     version = [0] * S                       # stage-local update counter

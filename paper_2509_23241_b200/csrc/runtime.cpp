@@ -140,6 +140,11 @@ struct tps_pipeline {
   uint64_t seed = 0;
   bool first = true, last = true, eq1_on_load = false, fuse_update = false;
   bool graph = false;                        // ResNet-style layer graph (CONV/BN/MAXPOOL3/AVGPOOL)
+  int staleness_mode = 0;                    // 1: explicit δ may be any live version (microbenchmark)
+  void* (*alloc_fn)(size_t, void*) = nullptr;   // caller's device allocator (tps_config.dev_alloc)
+  void (*free_fn)(void*, void*) = nullptr;
+  void* alloc_ctx = nullptr;
+  int64_t observed_bytes = 0;                // device free-memory drop across the allocations of init
   int upd_blocks_per_sm = 2;
   std::vector<int> dims;  // global
   std::vector<Layer> layers;
@@ -159,7 +164,8 @@ struct tps_pipeline {
   float* losses = nullptr;
   int64_t loss_cap = 0, loss_count = 0;
   int32_t* labels_dev = nullptr;
-  float* scratch = nullptr;
+  float* scratch = nullptr;        // bias-gradient reduction scratch of the compute stream
+  float* scratch_side = nullptr;   // ... of the optimizer stream (bias steps moved under the GEMMs)
   // graph networks: one gradient buffer per local layer output, two accumulation temps,
   // explicit-patch / patch-gradient scratch, batch-norm reduction scratch
   std::vector<uint16_t*> gbuf;
@@ -229,10 +235,15 @@ namespace {
 tps_status dev_alloc(tps_pipeline* p, void** out, size_t bytes, int64_t* category) {
   *out = nullptr;
   if (bytes == 0) return TPS_OK;
-  cudaError_t e = cudaMalloc(out, bytes);
-  if (e != cudaSuccess) {
-    cudaGetLastError();
-    return fail(TPS_E_OOM, "cudaMalloc(%zu) failed: %s", bytes, cudaGetErrorString(e));
+  if (p->alloc_fn) {
+    *out = p->alloc_fn(bytes, p->alloc_ctx);
+    if (!*out) return fail(TPS_E_OOM, "dev_alloc hook failed for %zu bytes", bytes);
+  } else {
+    cudaError_t e = cudaMalloc(out, bytes);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(TPS_E_OOM, "cudaMalloc(%zu) failed: %s", bytes, cudaGetErrorString(e));
+    }
   }
   CUDA_OK(cudaMemset(*out, 0, bytes));
   p->allocs.push_back(*out);
@@ -271,9 +282,9 @@ void compute_coeffs(int variant, int blend, int delta, double lambda, float* a, 
   }
 }
 
-void build_order(int S, int s, int m, int g, int64_t first, int64_t n, std::vector<tps_event>* out) {
+void build_order(int Kin, int s, int m, int g, int64_t first, int64_t n, std::vector<tps_event>* out) {
   out->clear();
-  const int64_t K = std::min<int64_t>(S - s, n);
+  const int64_t K = std::min<int64_t>(Kin, n);   // K_s mini-batches in flight (Z6)
   auto push_f = [&](int64_t j) {
     for (int a = 0; a < m; a += g) {
       tps_event e{};
@@ -481,7 +492,9 @@ void update_stash_peak(tps_pipeline* p) {
   std::vector<int64_t> live{p->latest};
   for (auto& kv : p->fwd_version)
     if (std::find(live.begin(), live.end(), kv.second) == live.end()) live.push_back(kv.second);
-  const int64_t stash = static_cast<int64_t>(live.size() - 1) * p->ver_bytes;
+  // V keeps one version (R = 1): versions of in-flight forwards are already overwritten
+  const int64_t n_live = std::min<int64_t>(static_cast<int64_t>(live.size()), p->R);
+  const int64_t stash = (n_live - 1) * p->ver_bytes;
   p->peak_stash_live = std::max(p->peak_stash_live, stash);
 }
 
@@ -772,6 +785,9 @@ tps_status do_forward(tps_pipeline* p, int64_t j, int a0, int cnt, const void* x
   if (p->first && !x) return fail(TPS_E_INVALID_ARG, "stage 0 forward needs x");
   if (p->last && !labels) return fail(TPS_E_INVALID_ARG, "last stage forward needs labels");
   const int grp = a0 / p->g;
+  // a rejected call must leave the handle untouched: check the LOCAL mailbox up front
+  if (!p->first && p->transport == TPS_TRANSPORT_LOCAL && !p->mbox_fwd.count({j, grp}))
+    return fail(TPS_E_ORDER, "stage %d: forward input of mb %lld group %d not sent yet", p->s, (long long)j, grp);
   const int r0 = a0 * p->bsz, nr = cnt * p->bsz;
   const int64_t v = p->latest;
   if (a0 == 0) p->fwd_version[j] = v;
@@ -871,15 +887,19 @@ tps_status do_backward(tps_pipeline* p, int64_t j, int staleness) {
     if (staleness > 0) return fail(TPS_E_STALENESS, "V-TiMePReSt has no stash (requested staleness %d)", staleness);
   } else {
     delta = staleness >= 0 ? staleness : dlog;
-    if (staleness >= 0 && staleness != dlog)
+    if (staleness >= 0 && staleness != dlog && p->staleness_mode == 0)
       return fail(TPS_E_STALENESS, "explicit staleness %d != logged %lld for mb %lld", staleness, (long long)dlog, (long long)j);
     v_used = vl - delta;
-    if (v_used < 0 || v_used < vl - p->R + 1) return fail(TPS_E_STALENESS, "no live stash for staleness %lld", (long long)delta);
+    if (v_used < 0 || v_used < vl - p->R + 1)
+      return fail(TPS_E_STALENESS, "no live stash for staleness %lld (latest %lld, ring of %d)", (long long)delta,
+                  (long long)vl, p->R);
   }
   float alpha, beta;
   compute_coeffs(p->variant, p->blend, static_cast<int>(delta), p->lambda, &alpha, &beta);
   const int nl = p->nlayers();
   Layer& Ll = p->layers[nl - 1];
+  if (!p->last && p->transport == TPS_TRANSPORT_LOCAL && !p->mbox_bwd.count(j))
+    return fail(TPS_E_ORDER, "stage %d: gradient of mb %lld not sent yet", p->s, (long long)j);
   const uint16_t* G;
   if (p->last) {
     G = p->gce;
@@ -914,8 +934,9 @@ tps_status do_backward(tps_pipeline* p, int64_t j, int staleness) {
     if (bias_side) {
       CUDA_OK(cudaEventRecord(p->ev_bias_in, p->cs));
       CUDA_OK(cudaStreamWaitEvent(p->s_upd, p->ev_bias_in, 0));
-      CUDA_OK(tps::launch_bias_grad_sgd(G, B * Lk.hw_out, Lk.Np, Lk.Np, Lk.db, p->scratch, Lk.b, Lk.mb, p->lr, p->mu,
-                                        p->wd, p->s_upd));
+      // own scratch: a compute-stream bias step of a narrower layer below may run concurrently
+      CUDA_OK(tps::launch_bias_grad_sgd(G, B * Lk.hw_out, Lk.Np, Lk.Np, Lk.db, p->scratch_side, Lk.b, Lk.mb, p->lr,
+                                        p->mu, p->wd, p->s_upd));
       CUDA_OK(cudaEventRecord(p->split_w ? p->ev_bias_l[k] : p->ev_bias_done, p->s_upd));
       p->launches += 1;
     }
@@ -1087,7 +1108,7 @@ tps_status begin_run(tps_pipeline* p, int64_t first, int64_t n) {
   CUDA_OK(cudaEventRecord(p->ev_caller, p->caller));
   for (cudaStream_t st : {p->cs, p->s_fin, p->s_upd}) CUDA_OK(cudaStreamWaitEvent(st, p->ev_caller, 0));
   if (p->s_w) CUDA_OK(cudaStreamWaitEvent(p->s_w, p->ev_caller, 0));
-  build_order(p->S, p->s, p->m, p->g, first, n, &p->order);
+  build_order(p->Kmax, p->s, p->m, p->g, first, n, &p->order);
   p->pos = 0;
   p->run_first = first;
   p->run_n = n;
@@ -1141,7 +1162,7 @@ tps_status tps_schedule_events(int32_t S, int32_t s, int32_t m, int32_t fwd_grou
   const int g = fwd_group <= 0 ? m : fwd_group;
   if (m % g) return fail(TPS_E_CONFIG, "fwd_group must divide m");
   std::vector<tps_event> ev;
-  if (M > 0) build_order(S, s, m, g, 0, M, &ev);
+  if (M > 0) build_order(S - s, s, m, g, 0, M, &ev);
   *n = static_cast<int64_t>(ev.size());
   if (out) std::memcpy(out, ev.data(), sizeof(tps_event) * static_cast<size_t>(std::min<int64_t>(cap, *n)));
   return TPS_OK;
@@ -1368,6 +1389,10 @@ tps_status tps_pipeline_init(const tps_config* c, tps_pipeline** out) {
   if (c->num_stages < 1) return fail(TPS_E_CONFIG, "num_stages must be >= 1");
   if (c->stage_id < 0 || c->stage_id >= c->num_stages) return fail(TPS_E_CONFIG, "stage_id out of range");
   if (c->micro_batches < 1 || c->micro_batch_size < 1) return fail(TPS_E_CONFIG, "m and b must be >= 1");
+  if (c->max_inflight < 0 || (c->max_inflight > 0 && c->max_inflight != c->num_stages - c->stage_id && c->num_stages != 1))
+    return fail(TPS_E_CONFIG, "max_inflight other than S - s needs S = 1");
+  if (c->staleness_mode != 0 && c->staleness_mode != 1) return fail(TPS_E_CONFIG, "bad staleness_mode");
+  if ((c->dev_alloc == nullptr) != (c->dev_free == nullptr)) return fail(TPS_E_CONFIG, "dev_alloc and dev_free go together");
   if (c->variant != TPS_V && c->variant != TPS_I) return fail(TPS_E_CONFIG, "bad variant");
   if (c->blend != TPS_BLEND_EQ1 && c->blend != TPS_BLEND_CONVEX) return fail(TPS_E_CONFIG, "bad blend");
   if (c->variant == TPS_I && !(c->lambda > 0)) return fail(TPS_E_CONFIG, "lambda must be > 0 (P:227)");
@@ -1406,6 +1431,12 @@ tps_status tps_pipeline_init(const tps_config* c, tps_pipeline** out) {
   p->dims.assign(c->dims, c->dims + c->num_layers + 1);
   p->classes = c->num_layer_specs > 0 ? c->layer_specs[c->num_layers - 1].out_c : c->dims[c->num_layers];
   p->Kmax = p->S - p->s;                         // in-flight mini-batches (reading Z6)
+  if (c->max_inflight > 0) p->Kmax = c->max_inflight;
+  p->staleness_mode = c->staleness_mode;
+  p->alloc_fn = c->dev_alloc; p->free_fn = c->dev_free; p->alloc_ctx = c->alloc_ctx;
+  // negative control of the parity tests (debug only): TPS_FAULT=skip_update makes every
+  // parameter step a no-op (lr = 0), which the parity tests must detect
+  if (const char* f = std::getenv("TPS_FAULT"); f && std::strcmp(f, "skip_update") == 0) p->lr = 0.f;
   p->R = (p->variant == TPS_I) ? p->Kmax : 1;    // weight version ring
   p->A0 = p->Kmax + (c->extra_recv_slot ? 1 : 0);
   const char* env = std::getenv("TPS_EQ1_ON_LOAD");
@@ -1418,6 +1449,9 @@ tps_status tps_pipeline_init(const tps_config* c, tps_pipeline** out) {
     tps_pipeline_destroy(p);
     return st;
   };
+  size_t free0 = 0, total0 = 0;
+  cudaDeviceSynchronize();
+  cudaMemGetInfo(&free0, &total0);
   const int lb = c->stage_bounds[p->s], le = c->stage_bounds[p->s + 1];
   if (p->graph) {
     const tps_status gs = init_graph(p, c, lb, le);
@@ -1517,6 +1551,7 @@ tps_status tps_pipeline_init(const tps_config* c, tps_pipeline** out) {
   for (auto& L : p->layers)
     if (L.has_w()) scr = std::max(scr, tps::bias_grad_scratch_floats(p->B * L.hw_out, L.Np));
   if ((st = alloc_t(p, &p->scratch, scr, &p->mem_optim)) != TPS_OK) return cleanup(st);
+  if (p->fuse_update && (st = alloc_t(p, &p->scratch_side, scr, &p->mem_optim)) != TPS_OK) return cleanup(st);
 
   }
   const int nl = p->nlayers();
@@ -1536,23 +1571,32 @@ tps_status tps_pipeline_init(const tps_config* c, tps_pipeline** out) {
       p->splitk_floats = wsf;
     }
   }
+  {
+    size_t free1 = 0, total1 = 0;
+    cudaDeviceSynchronize();
+    cudaMemGetInfo(&free1, &total1);
+    p->observed_bytes = static_cast<int64_t>(free0) - static_cast<int64_t>(free1);
+  }
   // streams and events
+  int prio_lo = 0, prio_hi = 0;   // least (0) and greatest (< 0) stream priority
+  cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+  if (const char* e = std::getenv("TPS_PRIO"); e && e[0] == '0') prio_hi = prio_lo;
   p->ev_caller = new_event();
   if (c->compute_stream) {
     p->cs = reinterpret_cast<cudaStream_t>(c->compute_stream);
     p->caller = p->cs;
   } else {
-    if (cudaStreamCreateWithFlags(&p->cs, cudaStreamNonBlocking) != cudaSuccess) return cleanup(fail(TPS_E_CUDA, "stream create"));
+    // the library-owned compute stream (forward GEMMs, the dgrad chain: the critical path) at
+    // the greatest priority; the optimizer / weight-gradient streams stay at the least (= the
+    // default, 0).  TPS_PRIO=0 puts every stream at the default priority.
+    if (cudaStreamCreateWithPriority(&p->cs, cudaStreamNonBlocking, prio_hi) != cudaSuccess)
+      return cleanup(fail(TPS_E_CUDA, "stream create"));
     p->own_cs = true;
   }
   for (cudaStream_t* sp : {&p->s_fin, &p->s_fout, &p->s_bin, &p->s_bout})
     if (cudaStreamCreateWithFlags(sp, cudaStreamNonBlocking) != cudaSuccess) return cleanup(fail(TPS_E_CUDA, "stream create"));
-  {
-    int lo = 0, hi = 0;   // optimizer stream at the lowest priority: GEMM CTAs are placed first
-    cudaDeviceGetStreamPriorityRange(&lo, &hi);
-    if (cudaStreamCreateWithPriority(&p->s_upd, cudaStreamNonBlocking, lo) != cudaSuccess)
-      return cleanup(fail(TPS_E_CUDA, "stream create"));
-  }
+  if (cudaStreamCreateWithPriority(&p->s_upd, cudaStreamNonBlocking, prio_lo) != cudaSuccess)
+    return cleanup(fail(TPS_E_CUDA, "stream create"));
   p->ev_fwd_ready.resize(2 * p->ng);
   p->ev_fwd_sent.resize(2 * p->ng);
   for (int i = 0; i < 2 * p->ng; ++i) {
@@ -1568,14 +1612,8 @@ tps_status tps_pipeline_init(const tps_config* c, tps_pipeline** out) {
     for (int k = 0; k < nl; ++k) {
       p->ev_dg[k] = new_event(); p->ev_w_done[k] = new_event(); p->ev_bias_l[k] = new_event();
     }
-    // TPS_SW_PRIO: 0 = default priority (default), 1 = lowest (the dgrad chain is the critical
-    // path), 2 = highest
-    int lo = 0, hi = 0;
-    cudaDeviceGetStreamPriorityRange(&lo, &hi);
-    const char* e = std::getenv("TPS_SW_PRIO");
-    const int mode = e ? std::atoi(e) : 0;
-    if (cudaStreamCreateWithPriority(&p->s_w, cudaStreamNonBlocking, mode == 1 ? lo : (mode == 2 ? hi : 0)) !=
-        cudaSuccess)
+    // weight-gradient stream below the compute stream's dgrad chain (the critical path)
+    if (cudaStreamCreateWithPriority(&p->s_w, cudaStreamNonBlocking, prio_lo) != cudaSuccess)
       return cleanup(fail(TPS_E_CUDA, "stream create"));
   }
   for (int k = 0; k < nl; ++k) {
@@ -1620,7 +1658,10 @@ tps_status tps_pipeline_destroy(tps_pipeline* p) {
   cudaDeviceSynchronize();
   for (ncclComm_t c : {p->c_fin, p->c_fout, p->c_bin, p->c_bout})
     if (c) ncclCommDestroy(c);
-  for (void* a : p->allocs) cudaFree(a);
+  for (void* a : p->allocs) {
+    if (p->free_fn) p->free_fn(a, p->alloc_ctx);
+    else cudaFree(a);
+  }
   auto kill_ev = [](cudaEvent_t e) { if (e) cudaEventDestroy(e); };
   for (auto e : p->ev_fwd_ready) kill_ev(e);
   for (auto e : p->ev_fwd_sent) kill_ev(e);
@@ -1785,8 +1826,9 @@ tps_status tps_stash_info(tps_pipeline* p, int32_t* live, int64_t* stash, int64_
   std::vector<int64_t> lv{p->latest};
   for (auto& kv : p->fwd_version)
     if (std::find(lv.begin(), lv.end(), kv.second) == lv.end()) lv.push_back(kv.second);
-  if (live) *live = static_cast<int32_t>(lv.size());
-  if (stash) *stash = static_cast<int64_t>(lv.size() - 1) * p->ver_bytes;
+  const int64_t n_live = std::min<int64_t>(static_cast<int64_t>(lv.size()), p->R);   // V: R = 1
+  if (live) *live = static_cast<int32_t>(n_live);
+  if (stash) *stash = (n_live - 1) * p->ver_bytes;
   if (peak) *peak = p->peak_stash_live;
   return TPS_OK;
 }
@@ -1937,6 +1979,12 @@ tps_status tps_memory_stats(tps_pipeline* p, int64_t* weights, int64_t* stash, i
   if (optim) *optim = p->mem_optim;
   if (comm) *comm = p->mem_comm;
   if (peak) *peak = p->mem_peak;
+  return TPS_OK;
+}
+
+tps_status tps_memory_observed(tps_pipeline* p, int64_t* device_bytes) {
+  if (!p || !device_bytes) return fail(TPS_E_INVALID_ARG, "null argument");
+  *device_bytes = p->observed_bytes;
   return TPS_OK;
 }
 

@@ -32,7 +32,7 @@ EXPORTS = [
     "tps_init_weights_synthetic", "tps_get_losses", "tps_get_trace", "tps_clear_trace", "tps_memory_stats",
     "tps_set_profiling", "tps_kernel_stats", "tps_launch_count", "tps_fill_synthetic", "tps_gemm",
     "tps_conv_gemm", "tps_partition", "tps_im2col", "tps_col2im", "tps_bn_forward", "tps_bn_backward",
-    "tps_pool_op", "tps_conv2d_gemm", "tps_debug_progress",
+    "tps_pool_op", "tps_conv2d_gemm", "tps_debug_progress", "tps_memory_observed",
 ]
 TPS_LAYER_LINEAR, TPS_LAYER_CONV3X3, TPS_LAYER_MAXPOOL2 = 0, 1, 2
 TPS_LAYER_CONV, TPS_LAYER_BN, TPS_LAYER_MAXPOOL3, TPS_LAYER_AVGPOOL = 3, 4, 5, 6
@@ -64,7 +64,37 @@ class Config(C.Structure):
                 ("weight_decay", C.c_float), ("transport", C.c_int32), ("nccl_ids", C.c_void_p),
                 ("device", C.c_int32), ("seed", C.c_uint64), ("compute_stream", C.c_uint64),
                 ("extra_recv_slot", C.c_int32), ("fuse_update", C.c_int32),
-                ("num_layer_specs", C.c_int32), ("layer_specs", C.POINTER(Layer)), ("reserved", C.c_int32 * 4)]
+                ("num_layer_specs", C.c_int32), ("layer_specs", C.POINTER(Layer)),
+                ("max_inflight", C.c_int32), ("staleness_mode", C.c_int32),
+                ("dev_alloc", C.c_void_p), ("dev_free", C.c_void_p), ("alloc_ctx", C.c_void_p),
+                ("reserved", C.c_int32 * 4)]
+
+
+# tps_config.dev_alloc / dev_free signatures
+ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p)
+FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p)
+
+
+class TorchAllocator:
+    """dev_alloc / dev_free hooks backed by PyTorch's caching allocator, so the handle's
+    buffers show up in torch.cuda.memory_allocated / max_memory_allocated (per-GPU peak
+    memory, BASELINE metric).  Marshalling only: the callbacks forward to torch."""
+
+    def __init__(self, device: int):
+        import torch
+        self.device = device
+
+        def _alloc(nbytes, _ctx):
+            try:
+                return torch.cuda.caching_allocator_alloc(int(nbytes), self.device)
+            except Exception:
+                return None
+
+        def _free(p, _ctx):
+            torch.cuda.caching_allocator_delete(p)
+
+        self.alloc = ALLOC_FN(_alloc)   # keep the ctypes thunks alive with the handle
+        self.free = FREE_FN(_free)
 
 
 _LIB = None
@@ -118,6 +148,7 @@ def lib() -> C.CDLL:
             "tps_pool_op": (I32, [I32, P, P, P, I32, I32, I32, I32, U64]),
             "tps_debug_progress": (I32, [P, P, P, P]),
             "tps_conv2d_gemm": (I32, [I32, I32, I32, I32, I32, I32, I32, I32, I32, P, P, P, P, I32, F, F, U64]),
+            "tps_memory_observed": (I32, [P, C.POINTER(I64)]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -285,6 +316,9 @@ class StageSpec:
     extra_recv_slot: int = 1
     fuse_update: int = 1
     layers: list | None = None       # oracle-style layer dicts (image nets); None => MLP from dims
+    max_inflight: int = 0            # 0 => S - s; S = 1 only otherwise (staleness sweep on one GPU)
+    staleness_mode: int = 0          # 1 => explicit δ may be any live version (microbenchmark)
+    torch_alloc: bool = False        # allocate through PyTorch's caching allocator
     _keep: list = field(default_factory=list)
 
 
@@ -305,6 +339,7 @@ class Pipeline:
         bounds = (C.c_int32 * len(spec.stage_bounds))(*spec.stage_bounds)
         ids = C.create_string_buffer(spec.nccl_ids, len(spec.nccl_ids)) if spec.nccl_ids else None
         specs = layer_specs(spec.layers) if spec.layers else None
+        self._alloc = TorchAllocator(spec.device) if spec.torch_alloc else None
         cfg = Config(num_layers=L, dims=dims, num_stages=len(spec.stage_bounds) - 1, stage_bounds=bounds,
                      stage_id=spec.stage_id, micro_batches=spec.micro_batches,
                      micro_batch_size=spec.micro_batch_size, fwd_group=spec.fwd_group, variant=spec.variant,
@@ -313,7 +348,9 @@ class Pipeline:
                      nccl_ids=C.cast(ids, C.c_void_p) if ids is not None else None, device=spec.device,
                      seed=spec.seed, compute_stream=spec.compute_stream, extra_recv_slot=spec.extra_recv_slot,
                      fuse_update=spec.fuse_update, num_layer_specs=len(spec.layers) if spec.layers else 0,
-                     layer_specs=specs)
+                     layer_specs=specs, max_inflight=spec.max_inflight, staleness_mode=spec.staleness_mode,
+                     dev_alloc=C.cast(self._alloc.alloc, C.c_void_p) if self._alloc else None,
+                     dev_free=C.cast(self._alloc.free, C.c_void_p) if self._alloc else None)
         h = C.c_void_p()
         check(lib().tps_pipeline_init(C.byref(cfg), C.byref(h)))
         self.h = h
@@ -410,6 +447,11 @@ class Pipeline:
         v = [C.c_int64() for _ in range(6)]
         check(lib().tps_memory_stats(self.h, *[C.byref(x) for x in v]))
         return dict(zip(["weights", "stash", "acts", "optim", "comm", "peak"], [x.value for x in v]))
+
+    def memory_observed(self) -> int:
+        n = C.c_int64()
+        check(lib().tps_memory_observed(self.h, C.byref(n)))
+        return n.value
 
     def set_profiling(self, on: bool):
         check(lib().tps_set_profiling(self.h, 1 if on else 0))

@@ -78,19 +78,23 @@ def run_oracle_graph(layers, bounds, m, b, M, variant, blend, lam, lr, mu, wd=0.
 
 
 def run_oracle(dims, bounds, m, b, M, variant, blend, lam, lr, mu, wd=0.0, seed=0, kind=synthgen.X_SIGNED,
-               layers=None):
+               layers=None, max_inflight=0):
     if layers:
         xs, ys, w0, b0 = net_workload(layers, m, b, M, seed, kind)
     else:
         xs, ys, w0, b0 = workload(dims, m, b, M, seed, kind)
     cfg = opipe.Config(dims, bounds, m, b, M, variant=variant, blend=blend, lam=lam, lr=lr, momentum=mu, wd=wd,
-                       layers=layers)
+                       layers=layers, max_inflight=max_inflight)
     return opipe.run(cfg, xs, ys, w0, b0)
 
 
 def run_gpu(dims, bounds, m, b, M, variant, blend, lam, lr, mu, wd=0.0, seed=0, kind=synthgen.X_SIGNED,
-            fwd_group=0, init="set", extra_recv_slot=1, fuse_update=1, layers=None):
-    """All S stages as LOCAL-transport handles on cuda:0; returns (stages, losses)."""
+            fwd_group=0, init="set", extra_recv_slot=1, fuse_update=1, layers=None, drive=None, **spec_kw):
+    """All S stages as LOCAL-transport handles on cuda:0; returns (stages, losses).
+
+    drive: None => tps_run_schedule_local; else a callable(stages, x_pool, y_pool, M) that
+    issues the events itself (e.g. through the step-wise tps_stage_* calls).
+    spec_kw: extra StageSpec fields (max_inflight, staleness_mode, torch_alloc, ...)."""
     import torch
 
     from paper_2509_23241_b200 import tps
@@ -114,7 +118,7 @@ def run_gpu(dims, bounds, m, b, M, variant, blend, lam, lr, mu, wd=0.0, seed=0, 
         spec = tps.StageSpec(dims=dims, stage_bounds=bounds, stage_id=s, micro_batches=m, micro_batch_size=b,
                              fwd_group=fwd_group, variant=V, blend=BL, lam=lam, lr=lr, momentum=mu, weight_decay=wd,
                              transport=tps.TPS_TRANSPORT_LOCAL if S > 1 else tps.TPS_TRANSPORT_NONE, seed=seed,
-                             extra_recv_slot=extra_recv_slot, fuse_update=fuse_update, layers=layers)
+                             extra_recv_slot=extra_recv_slot, fuse_update=fuse_update, layers=layers, **spec_kw)
         st = tps.Pipeline(spec)
         if init == "set":
             for k, l in enumerate(st.layers):
@@ -125,7 +129,10 @@ def run_gpu(dims, bounds, m, b, M, variant, blend, lam, lr, mu, wd=0.0, seed=0, 
         stages.append(st)
     if S > 1:
         tps.local_link(stages)
-    tps.run_schedule_local(stages, 0, M, x_pool, y_pool, M)
+    if drive is None:
+        tps.run_schedule_local(stages, 0, M, x_pool, y_pool, M)
+    else:
+        drive(stages, x_pool, y_pool, M)
     for st in stages:
         st.synchronize()
     return stages, stages[-1].losses()

@@ -30,7 +30,7 @@ def test_library_exports_every_declared_symbol():
     exported = set(re.findall(r"\bT (tps_[a-z_0-9]+)", out))
     missing = [s for s in declared_symbols() if s not in exported]
     assert not missing, missing
-    assert tps.lib().tps_abi_version() == 2
+    assert tps.lib().tps_abi_version() == 3
 
 
 @pytest.mark.parametrize("S", [1, 2, 4, 8])

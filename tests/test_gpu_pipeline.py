@@ -35,6 +35,12 @@ CASES = {
                   synthgen.X_SIGNED),
     "S8-I": ([128] * 9 + [10], [0, 2, 3, 4, 5, 6, 7, 8, 9], 2, 16, 12, ost.I_VARIANT, ost.EQ1, 0.05, 0.05, 0.9,
              synthgen.X_SIGNED),
+    # a stage that WIDENS (256 -> 4096 above 1024 -> 256): the wide layer's bias step runs on the
+    # optimizer stream while the narrow layer's runs on the compute stream (fused update)
+    "S1-widening": ([1024, 256, 4096, 10], [0, 3], 4, 64, 10, ost.I_VARIANT, ost.EQ1, 0.05, 0.05, 0.9,
+                    synthgen.X_SIGNED),
+    "S2-widening": ([1024, 256, 4096, 256, 4096, 10], [0, 3, 5], 4, 64, 10, ost.I_VARIANT, ost.CONVEX, 0.05, 0.05,
+                    0.9, synthgen.X_SIGNED),
 }
 
 
@@ -54,8 +60,8 @@ def test_parity_with_oracle(gpu_lib, name, fuse):
             w, bb, _, _ = st.get_weights(k)
             assert weight_rel_err(w, ref.weights[l]) <= 5e-3, (name, l)
             assert layer_rel_err(w, bb, ref.weights[l], ref.biases[l]) <= 5e-3, (name, l)
-            if np.abs(ref.biases[l]).max() > 0:   # gross-error guard on the bias alone
-                assert weight_rel_err(bb, ref.biases[l]) <= 5e-2, (name, l)
+            if np.abs(ref.biases[l]).max() > 0:   # the bias alone, same 5e-3 bar (Z19)
+                assert weight_rel_err(bb, ref.biases[l]) <= 5e-3, (name, l, weight_rel_err(bb, ref.biases[l]))
 
 
 def test_fwd_groups_and_stepwise_api_agree(gpu_lib):

@@ -262,3 +262,65 @@ def test_resnet_graph_multistage_exact_equals_torch_replay(variant, blend, lam):
         np.testing.assert_allclose(res.weights[l], hw[l][-1].numpy(), rtol=1e-9, atol=1e-12)
         if l in hb:
             np.testing.assert_allclose(res.biases[l], hb[l][-1].numpy(), rtol=1e-9, atol=1e-12)
+
+
+def test_resnet50_graph_is_torchvision_resnet50():
+    """Pins oracle.graph.resnet_layers() (which feeds BOTH the oracle and the GPU path) to an
+    independent library definition: torchvision.models.resnet50 (v1.5).  Same parameter count
+    (25,557,032 at 1000 classes), and at 64x64 inputs one exact-mode training step of the oracle
+    graph (S = 1, BN statistics of the micro-batch) equals torchvision's forward in training
+    mode + autograd + SGD: the same loss and the same updated parameters for all 161 tensors."""
+    tv = pytest.importorskip("torchvision")
+    layers, _ = graph.resnet_layers()
+    n = sum(int(np.prod(p[0].shape)) + (0 if p[1] is None else p[1].size)
+            for p in graph_params(layers) if p[0] is not None)
+    assert n == 25_557_032 == sum(p.numel() for p in tv.models.resnet50(weights=None).parameters())
+
+    classes, H, b = 10, 64, 2
+    layers, _ = graph.resnet_layers(H=H, classes=classes)
+    p0 = graph_params(layers, seed=4)
+    xs, ys = graph_inputs(layers, 1, b, 1, seed=4)
+    res = graph.run(layers, [0, len(layers)], 1, b, 1, xs, ys, p0, lr=0.1, mu=0.9, exact=True)
+
+    net = tv.models.resnet50(weights=None, num_classes=classes).double().train()
+    pairs, prev = [], None        # (conv, bn) in torchvision's conv order: each conv feeds one bn
+    for mod in net.modules():
+        if isinstance(mod, torch.nn.Conv2d):
+            prev = mod
+        elif isinstance(mod, torch.nn.BatchNorm2d):
+            pairs.append((prev, mod))
+    oconv = [l for l, sp in enumerate(layers) if sp["kind"] == "conv"]
+    assert len(oconv) == len(pairs) == 53
+    bn_of = {}
+    with torch.no_grad():
+        for l, (conv, bn) in zip(oconv, pairs):
+            sp = layers[l]
+            assert (conv.in_channels, conv.out_channels, conv.kernel_size[0], conv.stride[0], conv.padding[0]) == \
+                (sp["cin"], sp["cout"], sp["k"], sp["s"], sp["p"]), (l, conv)
+            conv.weight.copy_(torch.from_numpy(np.asarray(p0[l][0], np.float64)).permute(0, 3, 1, 2))
+            bn_of[l] = bn
+        for l, sp in enumerate(layers):
+            if sp["kind"] == "bn":
+                bn = bn_of[sp.get("src", l - 1)]          # the BN that normalises this BN's source conv
+                bn.weight.copy_(torch.from_numpy(np.asarray(p0[l][0], np.float64)))
+                bn.bias.copy_(torch.from_numpy(np.asarray(p0[l][1], np.float64)))
+                bn_of[("bn", l)] = bn
+        net.fc.weight.copy_(torch.from_numpy(np.asarray(p0[-1][0], np.float64)))
+        net.fc.bias.copy_(torch.from_numpy(np.asarray(p0[-1][1], np.float64)))
+    opt = torch.optim.SGD(net.parameters(), lr=0.1, momentum=0.9)
+    x = torch.from_numpy(np.asarray(xs[0], np.float64).reshape(b, H, H, 3)).permute(0, 3, 1, 2)
+    loss = F.cross_entropy(net(x), torch.from_numpy(np.asarray(ys[0], np.int64)))
+    opt.zero_grad()
+    loss.backward()
+    opt.step()
+    assert abs(loss.item() - res.losses[0]) <= 1e-10 * abs(loss.item())
+    with torch.no_grad():
+        for l, (conv, _) in zip(oconv, pairs):
+            np.testing.assert_allclose(res.weights[l], conv.weight.permute(0, 2, 3, 1).numpy(), rtol=1e-8, atol=1e-9 * np.abs(res.weights[l]).max())
+        for l, sp in enumerate(layers):
+            if sp["kind"] == "bn":
+                bn = bn_of[("bn", l)]
+                np.testing.assert_allclose(res.weights[l], bn.weight.numpy(), rtol=1e-8, atol=1e-9 * np.abs(res.weights[l]).max())
+                np.testing.assert_allclose(res.biases[l], bn.bias.numpy(), rtol=1e-8, atol=1e-9)
+        np.testing.assert_allclose(res.weights[-1], net.fc.weight.numpy(), rtol=1e-8, atol=1e-9)
+        np.testing.assert_allclose(res.biases[-1], net.fc.bias.numpy(), rtol=1e-8, atol=1e-9)

@@ -134,3 +134,22 @@ def test_brute_force_timing_independence():
             done.add((s, e)); ptr[s] += 1; moved = True
         assert moved
     assert a == sorted(rows)
+
+
+@pytest.mark.parametrize("K", range(1, 9))
+def test_one_stage_inflight_override_matches_stage_at_depth_k(K):
+    """S = 1 with K mini-batches in flight (tps_config.max_inflight, the one-GPU staleness
+    sweep) is stage s = S - K of an S-stage pipeline as far as versions go: the same static
+    order shape and the same (v_fwd, v_latest, δ) per mini-batch, δ = min(j, K - 1)."""
+    S, m, M = 8, 2, 12
+    _, deep = schedule.execute(S, m, M)
+    _, one = schedule.execute(1, m, M, K)
+    s = S - K
+    deep_b = [(r.mb, r.v_used, r.v_latest, r.delta) for r in deep if r.kind == "B" and r.stage == s]
+    one_b = [(r.mb, r.v_used, r.v_latest, r.delta) for r in one if r.kind == "B"]
+    assert one_b == deep_b
+    assert [d for *_, d in one_b] == [min(j, K - 1) for j in range(M)]
+    assert [(e.kind, e.mb) for e in schedule.stage_order(1, 0, m, M, K)] == \
+        [(e.kind, e.mb) for e in schedule.stage_order(S, s, m, M)]
+    with pytest.raises(AssertionError):
+        schedule.stage_order(2, 0, m, M, K)

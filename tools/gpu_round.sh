@@ -1,0 +1,52 @@
+#!/bin/bash
+# One documented gpurun driver script (replaces the round-1 one-off cmd*.sh files).
+#
+#   gpurun --timeout 3000 -- 'bash tools/gpu_round.sh TAG [STEPS...]'
+#
+# TAG names the outputs (gpurun_out/TAG_*).  STEPS (default: build tests smoke bench) pick
+# what runs, in order:
+#   build    compile libtps.so for sm_100a on the box
+#   tests    pytest -m gpu (full GPU parity suite)
+#   quick    pytest -m gpu on the fast files only (pipeline, fused update, ABI step-wise)
+#   smoke    __graft_entry__.smoke()
+#   bench    bench.py default line (C5, S=1) + the reference arm
+#   configs  tools/bench_configs.py (per-config one-GPU numbers incl. C2/C4 V vs I)
+#   launches ncu launch list of one bench epoch window + its summary
+#   gemm     tools/gemm_bench.py microbenchmarks at the bench shape
+#   sanitize compute-sanitizer racecheck/synccheck/memcheck on small pipeline runs
+# Every step runs under its own timeout so one hang cannot eat the box.
+set -u
+TAG=${1:?tag}; shift
+STEPS=${*:-build tests smoke bench}
+mkdir -p gpurun_out
+O=gpurun_out/${TAG}
+for s in $STEPS; do
+  case $s in
+    build)
+      python -c "import __graft_entry__ as g; g.build()" > ${O}_build.log 2>&1 ;;
+    tests)
+      timeout 2700 python -m pytest tests -q -m gpu --timeout=1500 -p no:cacheprovider --durations=12 > ${O}_tests.log 2>&1 ;;
+    quick)
+      timeout 1500 python -m pytest tests/test_gpu_pipeline.py tests/test_gpu_fused_update.py tests/test_gpu_stepwise.py -q -m gpu --timeout=900 -p no:cacheprovider > ${O}_quick.log 2>&1 ;;
+    smoke)
+      timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > ${O}_smoke.log 2>&1 ;;
+    bench)
+      timeout 900 python bench.py 2>${O}_bench.err | tail -1 > ${O}_bench.json
+      timeout 900 python bench.py --impl reference --steps 2 --warmup 3 2>/dev/null | tail -1 > ${O}_ref.json ;;
+    configs)
+      timeout 1500 python tools/bench_configs.py --out ${O}_configs.json > ${O}_configs.log 2>&1 ;;
+    launches)
+      timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -s 2500 -c 600 --csv \
+        --log-file ${O}_launches.csv python bench.py --steps 1 --warmup 1 --epoch-mb 16 --no-cpu-baseline --no-e2e --no-v > /dev/null 2>&1
+      python tools/launches_summary.py ${O}_launches.csv ${O}_launches_summary.json "bench.py C5 S=1, one epoch window" > /dev/null 2>&1 ;;
+    gemm)
+      timeout 600 python tools/gemm_bench.py > ${O}_gemm.txt 2>&1 ;;
+    sanitize)
+      for tool in racecheck synccheck memcheck; do
+        TPS_SANITIZE=1 timeout 1200 compute-sanitizer --tool $tool --error-exitcode 9 \
+          python -m pytest tests/test_gpu_sanitize.py -q -m gpu -p no:cacheprovider > ${O}_san_${tool}.log 2>&1
+        echo "exit $?" >> ${O}_san_${tool}.log
+      done ;;
+    *) echo "unknown step $s" ;;
+  esac
+done
