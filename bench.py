@@ -48,6 +48,14 @@ def parse():
     ap.add_argument("--no-v", action="store_true")
     ap.add_argument("--fwd-group", type=int, default=0)
     ap.add_argument("--fuse-update", type=int, default=1, help="1: SGD update in the wgrad epilogue (TMA-fed)")
+    ap.add_argument("--transport", default="ipc", choices=["ipc", "nccl"],
+                    help="N > 1: ipc = neighbours' buffers mapped, the producing GEMM stores into them "
+                         "(fused compute + send); nccl = ncclSend/ncclRecv per edge")
+    ap.add_argument("--same-device", action="store_true",
+                    help="N > 1 on ONE GPU: every rank uses cuda:0 (gloo process group); exercises the "
+                         "multi-process path on a one-GPU box (throughput is then time-sliced)")
+    ap.add_argument("--no-method", action="store_true", help="skip the C2 method leg (4 stages, V / I-EQ1 / "
+                    "I-CONVEX, staleness sweep, measured memory)")
     return ap.parse_args()
 
 
@@ -174,6 +182,92 @@ def config_dict(args):
             "fused_update": bool(args.fuse_update), "parallelism": f"pp{S}", "l2": "inputs+weights per step >> 126 MB L2 (no flush needed)"}
 
 
+# ------------------------------------------------------------------ method leg (C2 on one GPU)
+def method_leg(torch, tps, windows=3, epoch=32, pool=4):
+    """BASELINE.json configs[1]: 4-stage MLP, 8 x Linear(4096,4096) + head,
+    m = 8 micro-batches of 64, all 4 stages as LOCAL handles on this GPU (so samples/s is the
+    one-GPU cost of the whole pipeline), staleness 3/2/1/0 by stage; V, I-EQ1 and I-CONVEX
+    through tps_run_schedule_local; per-variant memory measured by the allocator (PyTorch's
+    caching allocator via the dev_alloc hook) and the library's per-stage accounting.  Then the
+    "staleness sweep 0..3": one stage (2 x 4096^2 + head) keeping K = 1..4 mini-batches in
+    flight (tps_config.max_inflight), steady δ = K - 1, I-EQ1 and I-CONVEX."""
+    dims, bounds, m, b = [WIDTH] * 9 + [CLASSES], [0, 2, 4, 6, 9], 8, 64
+    B = m * b
+    cur = torch.cuda.current_stream()
+    x = torch.empty(pool, B, WIDTH, dtype=torch.bfloat16, device="cuda")
+    y = torch.empty(pool, B, dtype=torch.int32, device="cuda")
+    for j in range(pool):
+        tps.fill_synthetic(0, 1, 0x10000 + j, B, WIDTH, 0, x[j], cur.cuda_stream)
+        tps.fill_synthetic(2, 1, 0x20000 + j, B, 1, CLASSES, y[j], cur.cuda_stream)
+    torch.cuda.synchronize()
+    fl_c2 = sum(2.0 * dims[l] * dims[l + 1] * (3 if l > 0 else 2) for l in range(len(dims) - 1))
+
+    def timed(stages, n_windows):
+        mb = 0
+        tps.run_schedule_local(stages, mb, epoch, x, y, pool)          # warm-up epoch
+        mb += epoch
+        torch.cuda.synchronize()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(n_windows + 1)]
+        ev[0].record()
+        for i in range(n_windows):
+            tps.run_schedule_local(stages, mb, epoch, x, y, pool)
+            mb += epoch
+            for st in stages:
+                st.join(cur.cuda_stream)                                  # stream-ordered end of the window
+            ev[i + 1].record()
+        torch.cuda.synchronize()
+        v = sorted(epoch * B / (ev[i].elapsed_time(ev[i + 1]) / 1e3) for i in range(n_windows))
+        return {"median": statistics.median(v), "min": v[0], "max": v[-1], "windows": n_windows,
+                "unit": "samples/s"}
+
+    out = {"workload": "C2 (BASELINE.json configs[1]): 8 x Linear(4096,4096)+ReLU + head, S = 4 stages as LOCAL "
+                       "handles on ONE GPU, m = 8 x b = 64, staleness 3/2/1/0 by stage, SGD momentum 0.9, "
+                       f"lambda {LAM}; {epoch}-mini-batch windows",
+           "flops_per_sample": fl_c2, "variants": {}}
+    for name, var, blend in (("V", tps.TPS_V, tps.TPS_BLEND_EQ1), ("I-EQ1", tps.TPS_I, tps.TPS_BLEND_EQ1),
+                             ("I-CONVEX", tps.TPS_I, tps.TPS_BLEND_CONVEX)):
+        torch.cuda.synchronize()
+        torch.cuda.reset_peak_memory_stats()
+        base = torch.cuda.memory_allocated()
+        stages = [tps.Pipeline(tps.StageSpec(dims=dims, stage_bounds=bounds, stage_id=s, micro_batches=m,
+                                             micro_batch_size=b, variant=var, blend=blend, lam=LAM, lr=LR, momentum=MU,
+                                             transport=tps.TPS_TRANSPORT_LOCAL, seed=1, torch_alloc=True))
+                  for s in range(4)]
+        for st in stages:
+            st.init_weights_synthetic()
+        tps.local_link(stages)
+        held = torch.cuda.memory_allocated() - base
+        t = timed(stages, windows)
+        deltas = sorted({(e.stage, e.delta) for st in stages for e in st.trace() if e.kind == 1})
+        out["variants"][name] = {
+            "samples_per_s": t, "tflops_median": fl_c2 * t["median"] / 1e12,
+            "memory_measured_bytes_all_stages": int(torch.cuda.max_memory_allocated() - base),
+            "memory_held_after_init_bytes": int(held),
+            "per_stage_library_bytes": [st.memory_stats() for st in stages],
+            "per_stage_stash_peak_bytes": [st.stash_info()[2] for st in stages],
+            "max_delta_per_stage": [max(d for s_, d in deltas if s_ == s) for s in range(4)],
+        }
+        for st in stages:
+            st.close()
+    # staleness sweep on one stage
+    dims1 = [WIDTH, WIDTH, WIDTH, CLASSES]
+    fl1 = sum(2.0 * dims1[l] * dims1[l + 1] * (3 if l > 0 else 2) for l in range(3))
+    sweep = {}
+    for name, blend in (("I-EQ1", tps.TPS_BLEND_EQ1), ("I-CONVEX", tps.TPS_BLEND_CONVEX)):
+        for K in (1, 2, 3, 4):
+            st = tps.Pipeline(tps.StageSpec(dims=dims1, stage_bounds=[0, 3], stage_id=0, micro_batches=m,
+                                            micro_batch_size=b, variant=tps.TPS_I, blend=blend, lam=LAM, lr=LR,
+                                            momentum=MU, seed=1, max_inflight=K))
+            st.init_weights_synthetic()
+            t = timed([st], windows)
+            sweep[f"{name} delta={K - 1}"] = {"samples_per_s": t["median"], "tflops": fl1 * t["median"] / 1e12,
+                                              "stash_bytes": st.stash_info()[2]}
+            st.close()
+    out["staleness_sweep"] = {"workload": "one C2 stage (2 x Linear(4096,4096) + head), S = 1 with K = delta+1 "
+                                          "mini-batches in flight, m = 8 x b = 64", "results": sweep}
+    return out
+
+
 # ------------------------------------------------------------------ GPU leg
 def main():
     args = parse()
@@ -190,16 +284,28 @@ def main():
 
     from paper_2509_23241_b200 import tps
 
+    if args.same_device:
+        local = 0
     torch.cuda.set_device(local)
     S = world
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.same_device:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    red_dev = "cpu" if args.same_device else "cuda"
     dims, bounds = model(S)
-    stream = torch.cuda.current_stream().cuda_stream
+    # the compute stream at the greatest priority (the dgrad chain is the critical path; the
+    # library's weight-gradient and optimizer streams run at the least)
+    prio_stream = torch.cuda.Stream(priority=-1)
+    torch.cuda.set_stream(prio_stream)
+    stream = prio_stream.cuda_stream
+
+    use_ipc = S > 1 and args.transport == "ipc"
 
     def fresh_ids():
         # an ncclUniqueId bootstraps exactly one communicator: new ids for every pipeline
-        if S == 1:
+        if S == 1 or use_ipc:
             return None
         obj = [b"".join(tps.nccl_unique_id() for _ in range(2 * (S - 1)))] if rank == 0 else [None]
         dist.broadcast_object_list(obj, src=0)
@@ -210,11 +316,17 @@ def main():
         spec = tps.StageSpec(dims=dims, stage_bounds=bounds, stage_id=rank, micro_batches=MICRO_M,
                              micro_batch_size=MICRO_B, fwd_group=args.fwd_group, variant=variant,
                              blend=tps.TPS_BLEND_EQ1, lam=LAM, lr=LR, momentum=MU,
-                             transport=tps.TPS_TRANSPORT_NCCL if S > 1 else tps.TPS_TRANSPORT_NONE,
+                             transport=(tps.TPS_TRANSPORT_IPC if use_ipc else tps.TPS_TRANSPORT_NCCL) if S > 1
+                             else tps.TPS_TRANSPORT_NONE,
                              nccl_ids=ids, device=local, seed=0, compute_stream=stream,
-                             fuse_update=args.fuse_update)
+                             fuse_update=args.fuse_update, torch_alloc=True)
         p = tps.Pipeline(spec)
         p.init_weights_synthetic()
+        if use_ipc:   # exchange descriptors with the neighbouring stages, map their buffers
+            blobs = [None] * world
+            dist.all_gather_object(blobs, p.ipc_export())
+            p.ipc_connect(blobs[rank - 1] if rank > 0 else None, blobs[rank + 1] if rank < world - 1 else None)
+            dist.barrier()
         return p
 
     B = MICRO_B * MICRO_M
@@ -238,18 +350,21 @@ def main():
     def max_over_ranks(x):
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return t.item()
 
     def sum_over_ranks(x):
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         return t.item()
 
     def timed_epochs(p, steps, warmup, xp, yp, profile=False, clocks=None):
+        """K timed steps (epochs) after W warm-up ones; CUDA events on the compute stream around
+        every step (one window each), barrier + synchronize on both sides.  Returns the total
+        device ms (max over ranks), the per-window ms (max over ranks), launches, clocks."""
         mb = p.next_mb if hasattr(p, "next_mb") else 0
         for _ in range(warmup):
             p.run_schedule(mb, args.epoch_mb, xp, yp, POOL)
@@ -261,29 +376,36 @@ def main():
         if clocks:
             clocks.start()
         barrier()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(steps):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+        ev[0].record()
+        for i in range(steps):
             p.run_schedule(mb, args.epoch_mb, xp, yp, POOL)
             mb += args.epoch_mb
-        e1.record()
+            ev[i + 1].record()
         barrier()
         ck = clocks.stop() if clocks else None
         p.next_mb = mb
-        ms = max_over_ranks(e0.elapsed_time(e1))
+        ms = max_over_ranks(ev[0].elapsed_time(ev[-1]))
+        win = [max_over_ranks(ev[i].elapsed_time(ev[i + 1])) for i in range(steps)]
         launches = sum_over_ranks(p.launch_count() - n0)
-        return ms, launches, ck
+        return ms, win, launches, ck
+
+    def spread(win_ms, samples):
+        v = sorted(samples / (w / 1e3) for w in win_ms)
+        return {"windows": len(v), "median": statistics.median(v), "min": v[0], "max": v[-1],
+                "rel_spread": (v[-1] - v[0]) / statistics.median(v), "unit": "samples/s"}
 
     samples_per_step = args.epoch_mb * B
     # ---- I-TiMePReSt (headline)
+    torch.cuda.reset_peak_memory_stats()
     pI = make(tps.TPS_I)
     clocks = ClockSampler(local)
-    ms, launches, ck = timed_epochs(pI, args.steps, args.warmup, x_pool, y_pool, clocks=clocks)
+    ms, winI, launches, ck = timed_epochs(pI, args.steps, args.warmup, x_pool, y_pool, clocks=clocks)
     value = samples_per_step * args.steps / (ms / 1e3)
+    spreadI = spread(winI, samples_per_step)
     # second timed region with CUDA events around every GEMM / update launch on the compute
     # stream (the events add small gaps, so the headline value above is taken without them)
-    ms_prof, _, _ = timed_epochs(pI, max(1, args.steps // 2), 0, x_pool, y_pool, profile=True)
+    ms_prof, _, _, _ = timed_epochs(pI, max(1, args.steps // 2), 0, x_pool, y_pool, profile=True)
     # per-kernel stats (GEMMs on the compute stream, CUDA events around every launch)
     n_g, ms_g, fl_g = pI.kernel_stats(3)
     per_kind = {}
@@ -293,6 +415,7 @@ def main():
             per_kind[nm] = {"launches": n_k, "ms": round(ms_k, 3), "tflops": round(fl_k / (ms_k * 1e-3) / 1e12, 1)}
     n_u, ms_u, by_u = pI.kernel_stats(4)
     memI = pI.memory_stats()
+    memI["torch_max_allocated"] = int(torch.cuda.max_memory_allocated())   # device-observed (allocator hook)
     lossesI = pI.losses()
     peaks, src = load_peaks()
     achieved = (fl_g / n_g) / (ms_g / n_g * 1e-3) / 1e12 if n_g else None
@@ -354,17 +477,23 @@ def main():
     # ---- V-TiMePReSt (memory + throughput)
     v_out = None
     if not args.no_v:
+        torch.cuda.synchronize()
+        torch.cuda.reset_peak_memory_stats()
         pV = make(tps.TPS_V)
-        msV, _, _ = timed_epochs(pV, max(1, args.steps // 2), 1, x_pool, y_pool)
+        msV, winV, _, _ = timed_epochs(pV, args.steps, 1, x_pool, y_pool)
         memV = pV.memory_stats()
-        v_out = {"value": samples_per_step * max(1, args.steps // 2) / (msV / 1e3), "unit": "samples/s",
-                 "mem_bytes": memV}
+        memV["torch_max_allocated"] = int(torch.cuda.max_memory_allocated())
+        v_out = {"value": samples_per_step * args.steps / (msV / 1e3), "unit": "samples/s",
+                 "spread": spread(winV, samples_per_step), "mem_bytes": memV}
         pV.close()
 
     mem_all = [{"I": memI, "V": v_out["mem_bytes"] if v_out else None}]
     if world > 1:
         mem_all = [None] * world
         dist.all_gather_object(mem_all, {"I": memI, "V": v_out["mem_bytes"] if v_out else None})
+    method = None
+    if world == 1 and not args.no_method:
+        method = method_leg(torch, tps)
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
@@ -399,6 +528,12 @@ def main():
             "clocks": ck, "memory_per_gpu": mem_all, "v_variant": {k: v for k, v in (v_out or {}).items()
                                                                    if k != "mem_bytes"},
             "losses_first_last": [float(lossesI[0]), float(lossesI[-1])] if len(lossesI) else None,
+            "spread": spreadI,
+            "peaks": {"bf16_tflops_burst": peaks.get("bf16_tflops"), "bf16_tflops_sustained": peak,
+                      "hbm_gbs": peaks.get("hbm_gbs"), "source": src,
+                      "measured_at_sm_mhz": (peaks.get("clocks_under_load") or {}).get("sm_mhz_median"),
+                      "bench_sm_mhz": (ck or {}).get("sm_mhz")},
+            "method": method,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -65,8 +65,17 @@ typedef enum { TPS_BLEND_EQ1 = 0, TPS_BLEND_CONVEX = 1 } tps_blend;
 /* How a stage exchanges activations / activation-gradients with its neighbours
  * (one-to-one transfers).  NONE: S = 1.  LOCAL: all stages are handles
  * in one process on one GPU (device copies; used by tests and replicas).
- * NCCL: one process per stage, ncclSend/ncclRecv over NVLink.                    */
-typedef enum { TPS_TRANSPORT_NONE = 0, TPS_TRANSPORT_LOCAL = 1, TPS_TRANSPORT_NCCL = 2 } tps_transport;
+ * NCCL: one process per stage, ncclSend/ncclRecv over NVLink.
+ * IPC: one process per stage; each stage maps its neighbours' receive buffers and flag words
+ * (cudaIpcOpenMemHandle: NVLink peer memory across GPUs, the same HBM for processes sharing a
+ * GPU).  The producing kernel stores straight into the consumer's buffer: the last forward
+ * GEMM's epilogue writes the next stage's input slot and the first layer's input-gradient
+ * GEMM writes the previous stage's gradient buffer (chain networks; graph networks copy from
+ * their stash), and stream memory operations (write / wait on 64-bit flag words) order
+ * producer and consumer with no host round trip and no collective.  Runs of an IPC handle
+ * number their mini-batches contiguously from 0.                                          */
+typedef enum { TPS_TRANSPORT_NONE = 0, TPS_TRANSPORT_LOCAL = 1, TPS_TRANSPORT_NCCL = 2,
+               TPS_TRANSPORT_IPC = 3 } tps_transport;
 
 typedef enum { TPS_EV_F = 0, TPS_EV_B = 1, TPS_EV_U = 2 } tps_event_kind;
 
@@ -205,6 +214,16 @@ tps_status tps_pipeline_init(const tps_config* cfg, tps_pipeline** out);
 tps_status tps_pipeline_destroy(tps_pipeline* p);
 /* LOCAL transport: connect the S handles of one process (stage order). */
 tps_status tps_local_link(tps_pipeline* const* stages, int32_t num_stages);
+/* IPC transport, after tps_pipeline_init on every stage:
+ *   tps_ipc_export writes this stage's exchange descriptor (IPC handles of its input slots,
+ *   gradient receive buffers and flag words; at most TPS_IPC_BLOB_BYTES) into host `out`;
+ *   the caller hands every stage its neighbours' descriptors (e.g. an all-gather over the
+ *   process group); tps_ipc_connect maps them (prev = stage s-1's descriptor, NULL on stage 0;
+ *   next = stage s+1's, NULL on the last stage).  TPS_E_CONFIG for a descriptor of the wrong
+ *   stage or shape, TPS_E_CUDA if a handle cannot be opened.                                  */
+#define TPS_IPC_BLOB_BYTES 2048
+tps_status tps_ipc_export(tps_pipeline* p, void* out, int64_t cap, int64_t* n);
+tps_status tps_ipc_connect(tps_pipeline* p, const void* prev_blob, const void* next_blob);
 
 /* ---- the training step (one mini-batch = B(j) U(j) + m forwards) ----------- */
 /* Declare a run of mini-batches [first_mb, first_mb+n_mb): builds the stage's
@@ -244,6 +263,10 @@ tps_status tps_run_schedule_local(tps_pipeline* const* stages, int32_t num_stage
                                   int64_t first_mb, int64_t n_mb,
                                   const void* x_pool, const int32_t* y_pool, int32_t pool);
 tps_status tps_synchronize(tps_pipeline* p);
+/* Stream-ordered join: `stream` (a cudaStream_t, 0 = legacy default) waits for everything the
+ * handle has enqueued so far on all of its streams (compute, weight-gradient, optimizer,
+ * transfers).  Non-blocking; lets a caller time or consume a run on its own stream.        */
+tps_status tps_join(tps_pipeline* p, uint64_t stream);
 
 /* ---- stash / intermediate-weight management -------------------------------- */
 tps_status tps_blend_coeffs(int32_t variant, int32_t blend, int32_t staleness, double lambda,

@@ -53,6 +53,10 @@ struct GemmArgs {
   // ws_floats floats supplied by the caller; gemm_run sets splits / kper and reduces
   float* ws; int64_t ws_floats;
   int splits, kper;           // set by gemm_run
+  // SMs this launch may occupy (0 = all).  The split backward runs layer k's fused wgrad +
+  // update and layer k-1's input gradient CONCURRENTLY on two streams; capping both persistent
+  // grids partitions the SMs between them so they co-run instead of queueing for SMs.
+  int max_ctas;
 };
 
 // floats of split-K workspace gemm_run needs for this weight-gradient GEMM (0: no split)

@@ -856,7 +856,8 @@ cudaError_t launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap
     attr_set = true;
   }
   const int tiles = ((args.M + BM * CG - 1) / (BM * CG)) * ((args.N + BN - 1) / BN) * std::max(1, args.splits);
-  const int clusters = std::max(1, std::min(tiles, num_sms() / CG));
+  const int sms = args.max_ctas > 0 ? std::min(args.max_ctas, num_sms()) : num_sms();
+  const int clusters = std::max(1, std::min(tiles, sms / CG));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(clusters * CG);
   cfg.blockDim = dim3(C::THREADS);
@@ -890,7 +891,7 @@ struct Tiling {
 // Pick the CTA-pair mode and tile width.  Pairs (256 x BN tiles, cta_group::2) cut operand
 // traffic per SM by a third; they are used when M fills at least two 128-row blocks and the
 // pair grid still covers the chip.  Env TPS_GEMM_CG=1 forces single-CTA tiles.
-Tiling pick_tiling(int M, int N, int K, int mode, bool sgd) {
+Tiling pick_tiling(int M, int N, int K, int mode, bool sgd, int max_ctas = 0) {
   if (mode == GEMM_DGRAD_BLEND || mode == GEMM_CONV_DGRAD_BLEND) {
     // three operand tiles per stage: CTA pairs (256 x 256 tiles) halve the L2 -> SM operand
     // bytes per FLOP, which is what bounds the blended dgrad
@@ -903,7 +904,7 @@ Tiling pick_tiling(int M, int N, int K, int mode, bool sgd) {
       return {2, 256};
     return {1, 128};
   }
-  const int sms0 = num_sms();
+  const int sms0 = max_ctas > 0 ? std::min(max_ctas, num_sms()) : num_sms();
   static int no_split = -1;
   if (no_split < 0) {
     const char* e = std::getenv("TPS_NO_SPLITK");
@@ -924,7 +925,7 @@ Tiling pick_tiling(int M, int N, int K, int mode, bool sgd) {
       }
     }
   }
-  const int sms = num_sms();
+  const int sms = sms0;
   static int force_cg = -1;
   if (force_cg < 0) {
     const char* e = std::getenv("TPS_GEMM_CG");
@@ -938,6 +939,21 @@ Tiling pick_tiling(int M, int N, int K, int mode, bool sgd) {
   if (sgd && sgd_bn && force_cg != 1 && M >= 256) return {2, sgd_bn};
   if (force_cg != 1 && M >= 256) {
     const int tm = (M + 255) / 256;
+    if (max_ctas > 0 && !sgd) {
+      // partitioned grid (split backward): pick the pair tile width with the better last-wave
+      // fill, 256 unless 128 fills the partition's waves clearly better
+      const int cl = std::max(1, sms / 2);
+      double best = -1.0;
+      int best_bn = 256;
+      for (int bn : {256, 128}) {
+        if (N <= bn / 2) continue;
+        const int tiles = tm * ((N + bn - 1) / bn);
+        const int waves = (tiles + cl - 1) / cl;
+        const double fill = static_cast<double>(tiles) / (static_cast<double>(waves) * cl);
+        if (fill > best + 0.05) { best = fill; best_bn = bn; }
+      }
+      if (best > 0) return {2, best_bn};
+    }
     for (int bn : {256, 128}) {
       if (N <= bn / 2) continue;
       const int tiles = tm * ((N + bn - 1) / bn);
@@ -987,7 +1003,7 @@ cudaError_t gemm_run(int mode, const GemmOperands& op, const GemmArgs& args_in, 
   GemmArgs args = args_in;
   if (args.M <= 0 || args.N <= 0 || args.K <= 0) return cudaSuccess;
   const bool sgd = ((mode == GEMM_WGRAD || mode == GEMM_CONV_WGRAD) && args.epi == EPI_SGD);
-  Tiling tl = pick_tiling(args.M, args.N, args.K, mode, sgd);
+  Tiling tl = pick_tiling(args.M, args.N, args.K, mode, sgd, args.max_ctas);
   if (tl.splits > 1 &&
       (!args.ws || args.ws_floats < static_cast<int64_t>(tl.splits) * args.M * args.ldo || !args.out_f32 ||
        args.ldo != args.N))

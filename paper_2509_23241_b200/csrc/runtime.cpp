@@ -12,6 +12,7 @@
 // in the static per-stage order of reading Z7 (K_s = S - s mini-batches in flight).
 // The host only enqueues: kernels on the compute stream, transfers on four comm
 // streams ordered by CUDA events; nothing blocks until tps_synchronize.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -159,7 +160,7 @@ struct tps_pipeline {
   uint16_t* gout[2] = {nullptr, nullptr};
   uint16_t* gwork[3] = {nullptr, nullptr, nullptr};
   float* logits = nullptr;
-  uint16_t* gce = nullptr;
+  uint16_t* gce = nullptr;                  // dlogits, one [B, ld] slot per in-flight mini-batch
   float* loss_rows = nullptr;
   float* losses = nullptr;
   int64_t loss_cap = 0, loss_count = 0;
@@ -206,6 +207,7 @@ struct tps_pipeline {
   // buffers (each dgrad waits for the weight gradient / bias step two layers up)
   bool split_w = false;
   cudaStream_t s_w = nullptr;
+  int nsm = 148, part_dgrad = 0;   // SMs of a concurrent (dgrad, wgrad+update) pair given to the dgrad
   std::vector<cudaEvent_t> ev_dg, ev_w_done, ev_bias_l;   // per layer
   std::vector<cudaEvent_t> ev_fwd_ready, ev_fwd_sent;  // [2 * ng]
   std::vector<cudaEvent_t> ev_act_free;                // [A0]
@@ -214,6 +216,19 @@ struct tps_pipeline {
   ncclComm_t c_fin = nullptr, c_fout = nullptr, c_bin = nullptr, c_bout = nullptr;
   tps_pipeline* prev_local = nullptr;
   tps_pipeline* next_local = nullptr;
+  // IPC transport: own flag words (written by the neighbours, waited on locally)
+  //   [0] fwd_ready     = last forward message (j·ng + grp + 1) stored into my input slots
+  //   [1] bwd_ready     = j + 1 once the gradient of mb j is in my receive buffer
+  //   [2] fwd_slot_free = j + 1 once the next stage freed its input slot of mb j
+  //   [3] bwd_buf_free  = j + 1 once the previous stage finished reading its receive buffer of mb j
+  uint64_t* flags = nullptr;
+  uint64_t* prev_flags = nullptr;             // mapped flag words of stage s-1 / s+1
+  uint64_t* next_flags = nullptr;
+  std::vector<uint16_t*> next_in;             // stage s+1's input slots (its A0)
+  uint16_t* prev_gin[2] = {nullptr, nullptr}; // stage s-1's gradient receive buffers
+  std::vector<void*> ipc_opened;
+  bool ipc_connected = false, ipc_direct = false;
+  int64_t ipc_next_mb = 0;                    // runs number their mini-batches contiguously from 0
   std::map<std::pair<int64_t, int>, Msg> mbox_fwd;  // keyed (mb, group), filled by prev stage
   std::map<int64_t, Msg> mbox_bwd;                  // keyed mb, filled by next stage
 
@@ -395,6 +410,38 @@ tps_status check_usable(tps_pipeline* p) {
   return TPS_OK;
 }
 
+// ------------------------------------------------------------------ IPC flag words
+typedef CUresult (*StreamValue64Fn)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+
+StreamValue64Fn stream_op(const char* name) {
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &fn, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+    return nullptr;
+  return reinterpret_cast<StreamValue64Fn>(fn);
+}
+
+// stream-ordered: `st` stalls (in the GPU front end, no SM held) until *flag >= v
+tps_status flag_wait(cudaStream_t st, const uint64_t* flag, uint64_t v) {
+  static StreamValue64Fn wait = stream_op("cuStreamWaitValue64");
+  if (!wait) return fail(TPS_E_CUDA, "cuStreamWaitValue64 unavailable");
+  const CUresult r = wait(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(flag), v,
+                          CU_STREAM_WAIT_VALUE_GEQ);
+  if (r != CUDA_SUCCESS) return fail(TPS_E_CUDA, "cuStreamWaitValue64 failed (%d)", static_cast<int>(r));
+  return TPS_OK;
+}
+
+// stream-ordered: *flag = v after all prior work of `st` (default flags: with a memory barrier,
+// so the data the flag announces is visible first)
+tps_status flag_write(cudaStream_t st, uint64_t* flag, uint64_t v) {
+  static StreamValue64Fn write = stream_op("cuStreamWriteValue64");
+  if (!write) return fail(TPS_E_CUDA, "cuStreamWriteValue64 unavailable");
+  const CUresult r = write(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(flag), v,
+                           CU_STREAM_WRITE_VALUE_DEFAULT);
+  if (r != CUDA_SUCCESS) return fail(TPS_E_CUDA, "cuStreamWriteValue64 failed (%d)", static_cast<int>(r));
+  return TPS_OK;
+}
+
 // ------------------------------------------------------------------ transport
 tps_status send_fwd(tps_pipeline* p, int64_t j, int grp, const void* src, size_t bytes) {
   const int e = static_cast<int>(j & 1) * p->ng + grp;
@@ -403,6 +450,20 @@ tps_status send_fwd(tps_pipeline* p, int64_t j, int grp, const void* src, size_t
     CUDA_OK(cudaStreamWaitEvent(p->s_fout, p->ev_fwd_ready[e], 0));
     NCCL_OK(ncclSend(src, bytes / 2, ncclBfloat16, 1, p->c_fout, p->s_fout));
     CUDA_OK(cudaEventRecord(p->ev_fwd_sent[e], p->s_fout));
+  } else if (p->transport == TPS_TRANSPORT_IPC) {
+    const uint64_t seq = static_cast<uint64_t>(j) * p->ng + grp + 1;
+    if (!p->ipc_direct) {   // copy into the next stage's input slot once it is free
+      const int nA0 = static_cast<int>(p->next_in.size());
+      CUDA_OK(cudaStreamWaitEvent(p->s_fout, p->ev_fwd_ready[e], 0));
+      TPS_TRY(flag_wait(p->s_fout, &p->flags[2], static_cast<uint64_t>(std::max<int64_t>(0, j - nA0 + 1))));
+      uint16_t* dst = p->next_in[j % nA0] + static_cast<size_t>(grp) * p->g * p->bsz *
+                                                 p->layers[p->nlayers() - 1].out_elems();
+      CUDA_OK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, p->s_fout));
+      TPS_TRY(flag_write(p->s_fout, &p->next_flags[0], seq));
+      CUDA_OK(cudaEventRecord(p->ev_fwd_sent[e], p->s_fout));
+    } else {                // the last forward GEMM already stored into the slot: announce it
+      TPS_TRY(flag_write(p->cs, &p->next_flags[0], seq));
+    }
   } else {
     tps_pipeline* q = p->next_local;
     if (!q) return fail(TPS_E_STATE, "LOCAL transport not linked");
@@ -416,6 +477,9 @@ tps_status recv_fwd(tps_pipeline* p, int64_t j, int grp, void* dst, size_t bytes
   CUDA_OK(cudaStreamWaitEvent(p->s_fin, p->ev_act_free[slot], 0));
   if (p->transport == TPS_TRANSPORT_NCCL) {
     NCCL_OK(ncclRecv(dst, bytes / 2, ncclBfloat16, 0, p->c_fin, p->s_fin));
+  } else if (p->transport == TPS_TRANSPORT_IPC) {
+    // the previous stage stores straight into this slot; wait for its announcement
+    TPS_TRY(flag_wait(p->s_fin, &p->flags[0], static_cast<uint64_t>(j) * p->ng + grp + 1));
   } else {
     auto it = p->mbox_fwd.find({j, grp});
     if (it == p->mbox_fwd.end()) return fail(TPS_E_ORDER, "stage %d: forward input of mb %lld group %d not sent yet", p->s, (long long)j, grp);
@@ -438,6 +502,16 @@ tps_status send_bwd(tps_pipeline* p, int64_t j, const void* src, size_t bytes) {
     CUDA_OK(cudaStreamWaitEvent(p->s_bout, p->ev_gout_ready, 0));
     NCCL_OK(ncclSend(src, bytes / 2, ncclBfloat16, 0, p->c_bout, p->s_bout));
     CUDA_OK(cudaEventRecord(p->ev_bwd_sent[e], p->s_bout));
+  } else if (p->transport == TPS_TRANSPORT_IPC) {
+    if (!p->ipc_direct) {
+      CUDA_OK(cudaStreamWaitEvent(p->s_bout, p->ev_gout_ready, 0));
+      TPS_TRY(flag_wait(p->s_bout, &p->flags[3], static_cast<uint64_t>(std::max<int64_t>(0, j - 1))));
+      CUDA_OK(cudaMemcpyAsync(p->prev_gin[j & 1], src, bytes, cudaMemcpyDeviceToDevice, p->s_bout));
+      TPS_TRY(flag_write(p->s_bout, &p->prev_flags[1], static_cast<uint64_t>(j) + 1));
+      CUDA_OK(cudaEventRecord(p->ev_bwd_sent[e], p->s_bout));
+    } else {                // the first layer's input-gradient GEMM stored into the buffer
+      TPS_TRY(flag_write(p->cs, &p->prev_flags[1], static_cast<uint64_t>(j) + 1));
+    }
   } else {
     tps_pipeline* q = p->prev_local;
     if (!q) return fail(TPS_E_STATE, "LOCAL transport not linked");
@@ -454,6 +528,8 @@ tps_status recv_bwd(tps_pipeline* p, int64_t j, void* dst, size_t bytes) {
   CUDA_OK(cudaStreamWaitEvent(p->s_bin, p->ev_gin_free[e], 0));
   if (p->transport == TPS_TRANSPORT_NCCL) {
     NCCL_OK(ncclRecv(dst, bytes / 2, ncclBfloat16, 1, p->c_bin, p->s_bin));
+  } else if (p->transport == TPS_TRANSPORT_IPC) {
+    TPS_TRY(flag_wait(p->s_bin, &p->flags[1], static_cast<uint64_t>(j) + 1));
   } else {
     auto it = p->mbox_bwd.find(j);
     if (it == p->mbox_bwd.end()) return fail(TPS_E_ORDER, "stage %d: gradient of mb %lld not sent yet", p->s, (long long)j);
@@ -836,9 +912,19 @@ tps_status do_forward(tps_pipeline* p, int64_t j, int a0, int cnt, const void* x
     if (Lk.has_w()) CUDA_OK(cudaStreamWaitEvent(p->cs, p->ev_upd_done[k], 0));   // latest version written
     void* out;
     const bool logits = (k == nl - 1) && p->last;
-    if (k < nl - 1) out = p->act[slot][k + 1] + static_cast<size_t>(r0) * Lk.out_elems();
-    else if (!p->last) out = p->send_fwd[j & 1] + static_cast<size_t>(r0) * Lk.out_elems();
-    else out = p->logits + static_cast<size_t>(r0) * Lk.Np;
+    if (k < nl - 1) {
+      out = p->act[slot][k + 1] + static_cast<size_t>(r0) * Lk.out_elems();
+    } else if (!p->last && p->ipc_direct) {
+      // fused compute + send: the epilogue stores into the next stage's input slot (NVLink peer
+      // memory across GPUs) once that stage has freed it (its backward of mb j - A0_next)
+      const int nA0 = static_cast<int>(p->next_in.size());
+      TPS_TRY(flag_wait(p->cs, &p->flags[2], static_cast<uint64_t>(std::max<int64_t>(0, j - nA0 + 1))));
+      out = p->next_in[j % nA0] + static_cast<size_t>(r0) * Lk.out_elems();
+    } else if (!p->last) {
+      out = p->send_fwd[j & 1] + static_cast<size_t>(r0) * Lk.out_elems();
+    } else {
+      out = p->logits + static_cast<size_t>(r0) * Lk.Np;
+    }
     TPS_TRY(layer_forward(p, Lk, nr, Xin, out, logits, v));
     Xin = static_cast<const uint16_t*>(out);
   }
@@ -850,7 +936,8 @@ tps_status do_forward(tps_pipeline* p, int64_t j, int a0, int cnt, const void* x
       lab = p->labels_dev + r0;
     }
     CUDA_OK(tps::launch_softmax_xent(p->logits + static_cast<size_t>(r0) * Ll.Np, Ll.Np, lab, nr, p->classes, p->B,
-                                     p->loss_rows + r0, p->gce + static_cast<size_t>(r0) * Ll.Np, Ll.Np, p->cs));
+                                     p->loss_rows + r0,
+                                     p->gce + (static_cast<size_t>(slot) * p->B + r0) * Ll.Np, Ll.Np, p->cs));
     p->launches += 1;
     if (a0 + cnt == p->m) {
       if (p->loss_count >= p->loss_cap) return fail(TPS_E_STATE, "loss buffer full (%lld mini-batches)", (long long)p->loss_cap);
@@ -902,7 +989,7 @@ tps_status do_backward(tps_pipeline* p, int64_t j, int staleness) {
     return fail(TPS_E_ORDER, "stage %d: gradient of mb %lld not sent yet", p->s, (long long)j);
   const uint16_t* G;
   if (p->last) {
-    G = p->gce;
+    G = p->gce + static_cast<size_t>(j % p->Kmax) * p->B * Ll.Np;   // slot of mb j (K_s may exceed 1, S = 1)
   } else {
     TPS_TRY(recv_bwd(p, j, p->gin[j & 1], static_cast<size_t>(p->B) * Ll.out_elems() * 2));
     G = p->gin[j & 1];
@@ -954,6 +1041,11 @@ tps_status do_backward(tps_pipeline* p, int64_t j, int staleness) {
       } else if (k > 0) {
         dst = p->gwork[wbuf];
         wbuf ^= 1;
+      } else if (p->ipc_direct) {
+        // fused compute + send: the input gradient goes straight into the previous stage's
+        // receive buffer once that stage finished reading it (its backward of mb j - 2)
+        TPS_TRY(flag_wait(p->cs, &p->flags[3], static_cast<uint64_t>(std::max<int64_t>(0, j - 1))));
+        dst = p->prev_gin[j & 1];
       } else {
         CUDA_OK(cudaStreamWaitEvent(p->cs, p->ev_bwd_sent[j & 1], 0));  // gout of mb j-2 has left
         dst = p->gout[j & 1];
@@ -969,6 +1061,8 @@ tps_status do_backward(tps_pipeline* p, int64_t j, int staleness) {
         ga.out = dst; ga.out_f32 = 0; ga.mask = X; ga.ldm = Lk.ld_in; ga.ldo = Lk.ld_in;
         ga.alpha = 1.f; ga.xa = 1.f; ga.xb = 0.f;
         const bool conv = Lk.kind == TPS_LAYER_CONV3X3;
+        // concurrent with layer k+1's fused wgrad + update on s_w: take the dgrad's share of the SMs
+        if (p->split_w && p->part_dgrad > 0 && k + 1 < nl && p->layers[k + 1].has_w()) ga.max_ctas = p->part_dgrad;
         ga.M = B * Lk.hw_in; ga.N = conv ? Lk.Ci : Lk.Kp; ga.K = Lk.Np;
         if (conv) ga.K = 9 * Lk.Co;
         tps::GemmOperands op{G, Lk.Np, Ws, Lk.Kp, nullptr};
@@ -999,6 +1093,10 @@ tps_status do_backward(tps_pipeline* p, int64_t j, int staleness) {
         ga.lr = p->lr; ga.mu = p->mu; ga.wd = p->wd;
       }
       cudaStream_t ws = p->cs;
+      // concurrent with layer k-1's dgrad on the compute stream: the other share of the SMs
+      if (p->split_w && p->part_dgrad > 0 && k > 0 && p->layers[k - 1].gidx > 0 &&
+          p->layers[k - 1].kind != TPS_LAYER_MAXPOOL2)
+        ga.max_ctas = p->nsm - p->part_dgrad;
       if (p->split_w) {   // after this layer's dgrad (it reads the weights the fused update rewrites)
         CUDA_OK(cudaEventRecord(p->ev_dg[k], p->cs));
         CUDA_OK(cudaStreamWaitEvent(p->s_w, p->ev_dg[k], 0));
@@ -1068,6 +1166,10 @@ tps_status do_backward(tps_pipeline* p, int64_t j, int staleness) {
   // the input slot and the received gradient buffer may now be refilled
   CUDA_OK(cudaEventRecord(p->ev_act_free[slot0], p->cs));
   if (!p->last) CUDA_OK(cudaEventRecord(p->ev_gin_free[j & 1], p->cs));
+  if (p->transport == TPS_TRANSPORT_IPC) {   // tell the neighbours that write into them
+    if (!p->first) TPS_TRY(flag_write(p->cs, &p->prev_flags[2], static_cast<uint64_t>(j) + 1));
+    if (!p->last) TPS_TRY(flag_write(p->cs, &p->next_flags[3], static_cast<uint64_t>(j) + 1));
+  }
   if (!p->first) {
     TPS_TRY(send_bwd(p, j, p->gout[j & 1], static_cast<size_t>(p->B) * p->in0_elems * 2));
   }
@@ -1102,6 +1204,13 @@ tps_status do_update(tps_pipeline* p, int64_t j) {
 tps_status begin_run(tps_pipeline* p, int64_t first, int64_t n) {
   if (n <= 0 || first < 0) return fail(TPS_E_INVALID_ARG, "bad run [%lld, +%lld)", (long long)first, (long long)n);
   if (p->in_run) return fail(TPS_E_ORDER, "stage %d: previous run not finished", p->s);
+  if (p->transport == TPS_TRANSPORT_IPC) {
+    if (!p->ipc_connected) return fail(TPS_E_STATE, "IPC transport: tps_ipc_connect first");
+    if (first != p->ipc_next_mb)
+      return fail(TPS_E_ORDER, "IPC transport: runs number mini-batches contiguously (expected first %lld)",
+                  (long long)p->ipc_next_mb);
+    p->ipc_next_mb = first + n;
+  }
   // inputs of the run (device pools, labels) may have been produced on the caller's stream:
   // the handle's streams start after everything already submitted there (the configured
   // compute stream, else the legacy default stream)
@@ -1372,7 +1481,7 @@ tps_status init_graph(tps_pipeline* p, const tps_config* c, int lb, int le) {
   }
   if (p->last) {
     TPS_TRY(alloc_t(p, &p->logits, static_cast<size_t>(p->B) * outL, &p->mem_acts));
-    TPS_TRY(alloc_t(p, &p->gce, static_cast<size_t>(p->B) * outL, &p->mem_acts));
+    TPS_TRY(alloc_t(p, &p->gce, static_cast<size_t>(p->Kmax) * p->B * outL, &p->mem_acts));
     TPS_TRY(alloc_t(p, &p->loss_rows, p->B, &p->mem_acts));
     TPS_TRY(alloc_t(p, &p->labels_dev, p->B, &p->mem_acts));
     p->loss_cap = 1 << 20;
@@ -1415,6 +1524,7 @@ tps_status tps_pipeline_init(const tps_config* c, tps_pipeline** out) {
   }
   const int g = c->fwd_group <= 0 ? c->micro_batches : c->fwd_group;
   if (c->micro_batches % g) return fail(TPS_E_CONFIG, "fwd_group must divide micro_batches");
+  if (c->transport < TPS_TRANSPORT_NONE || c->transport > TPS_TRANSPORT_IPC) return fail(TPS_E_CONFIG, "bad transport");
   if (c->num_stages > 1 && c->transport == TPS_TRANSPORT_NONE) return fail(TPS_E_CONFIG, "S > 1 needs a transport");
   if (c->transport == TPS_TRANSPORT_NCCL && c->num_stages > 1 && !c->nccl_ids) return fail(TPS_E_CONFIG, "NCCL transport needs ids");
   TPS_TRY(check_arch(c->device));
@@ -1434,6 +1544,10 @@ tps_status tps_pipeline_init(const tps_config* c, tps_pipeline** out) {
   if (c->max_inflight > 0) p->Kmax = c->max_inflight;
   p->staleness_mode = c->staleness_mode;
   p->alloc_fn = c->dev_alloc; p->free_fn = c->dev_free; p->alloc_ctx = c->alloc_ctx;
+  if (p->transport == TPS_TRANSPORT_IPC) {
+    // exported buffers must be whole cudaMalloc allocations (IPC handles name allocations)
+    p->alloc_fn = nullptr; p->free_fn = nullptr;
+  }
   // negative control of the parity tests (debug only): TPS_FAULT=skip_update makes every
   // parameter step a no-op (lr = 0), which the parity tests must detect
   if (const char* f = std::getenv("TPS_FAULT"); f && std::strcmp(f, "skip_update") == 0) p->lr = 0.f;
@@ -1538,10 +1652,19 @@ tps_status tps_pipeline_init(const tps_config* c, tps_pipeline** out) {
   }
   if (p->split_w && (st = alloc_t(p, &p->gwork[2], static_cast<size_t>(p->B) * max_elems, &p->mem_acts)) != TPS_OK)
     return cleanup(st);
+  if (p->split_w) {
+    // SM partition of the concurrent pair (dgrad of layer k-1 | fused wgrad + update of layer k):
+    // TPS_SPLIT_FRAC = the dgrad's fraction (default 0.5; 0 = no partition, both grids full)
+    cudaDeviceGetAttribute(&p->nsm, cudaDevAttrMultiProcessorCount, p->device);
+    double f = 0.5;
+    if (const char* e = std::getenv("TPS_SPLIT_FRAC")) f = std::atof(e);
+    p->part_dgrad = f > 0.0 && f < 1.0 ? std::max(2, static_cast<int>(f * p->nsm + 1.0) / 2 * 2) : 0;
+  }
   if (p->last) {
     if (p->layers[nl - 1].kind != TPS_LAYER_LINEAR) return cleanup(fail(TPS_E_CONFIG, "the last layer must be the Linear head"));
     if ((st = alloc_t(p, &p->logits, static_cast<size_t>(p->B) * outL, &p->mem_acts)) != TPS_OK) return cleanup(st);
-    if ((st = alloc_t(p, &p->gce, static_cast<size_t>(p->B) * outL, &p->mem_acts)) != TPS_OK) return cleanup(st);
+    if ((st = alloc_t(p, &p->gce, static_cast<size_t>(p->Kmax) * p->B * outL, &p->mem_acts)) != TPS_OK)
+      return cleanup(st);
     if ((st = alloc_t(p, &p->loss_rows, p->B, &p->mem_acts)) != TPS_OK) return cleanup(st);
     if ((st = alloc_t(p, &p->labels_dev, p->B, &p->mem_acts)) != TPS_OK) return cleanup(st);
     p->loss_cap = 1 << 20;
@@ -1555,6 +1678,12 @@ tps_status tps_pipeline_init(const tps_config* c, tps_pipeline** out) {
 
   }
   const int nl = p->nlayers();
+  if (p->transport == TPS_TRANSPORT_IPC) {
+    const tps_status fs = alloc_t(p, &p->flags, 4, &p->mem_comm);
+    if (fs != TPS_OK) return cleanup(fs);
+    const char* e = std::getenv("TPS_IPC_DIRECT");
+    p->ipc_direct = !p->graph && !(e && e[0] == '0');
+  }
   {
     // split-K workspace for the weight-gradient GEMMs whose output tiles cannot fill the GPU
     int64_t wsf = 0;
@@ -1658,6 +1787,7 @@ tps_status tps_pipeline_destroy(tps_pipeline* p) {
   cudaDeviceSynchronize();
   for (ncclComm_t c : {p->c_fin, p->c_fout, p->c_bin, p->c_bout})
     if (c) ncclCommDestroy(c);
+  for (void* a : p->ipc_opened) cudaIpcCloseMemHandle(a);
   for (void* a : p->allocs) {
     if (p->free_fn) p->free_fn(a, p->alloc_ctx);
     else cudaFree(a);
@@ -1698,6 +1828,85 @@ tps_status tps_local_link(tps_pipeline* const* st, int32_t n) {
     st[i]->prev_local = i > 0 ? st[i - 1] : nullptr;
     st[i]->next_local = i + 1 < n ? st[i + 1] : nullptr;
   }
+  return TPS_OK;
+}
+
+namespace {
+struct IpcBlob {
+  int32_t magic, stage, num_stages, A0;
+  int64_t in_bytes, gin_bytes;          // bytes of one input slot / one gradient receive buffer
+  cudaIpcMemHandle_t flags, gin[2], in[16];
+};
+static_assert(sizeof(IpcBlob) <= TPS_IPC_BLOB_BYTES, "IPC descriptor too large");
+constexpr int32_t IPC_MAGIC = 0x54505331;   // "TPS1"
+
+tps_status ipc_open(tps_pipeline* p, const cudaIpcMemHandle_t& h, void** out) {
+  CUDA_OK(cudaIpcOpenMemHandle(out, h, cudaIpcMemLazyEnablePeerAccess));
+  p->ipc_opened.push_back(*out);
+  return TPS_OK;
+}
+}  // namespace
+
+tps_status tps_ipc_export(tps_pipeline* p, void* out, int64_t cap, int64_t* n) {
+  TPS_TRY(check_usable(p));
+  if (!out || !n) return fail(TPS_E_INVALID_ARG, "null argument");
+  if (p->transport != TPS_TRANSPORT_IPC) return fail(TPS_E_CONFIG, "handle is not IPC transport");
+  if (cap < static_cast<int64_t>(sizeof(IpcBlob))) return fail(TPS_E_INVALID_ARG, "cap < %zu", sizeof(IpcBlob));
+  if (p->A0 > 16) return fail(TPS_E_UNSUPPORTED, "more than 16 input slots");
+  IpcBlob b{};
+  b.magic = IPC_MAGIC; b.stage = p->s; b.num_stages = p->S; b.A0 = p->A0;
+  b.in_bytes = static_cast<int64_t>(p->B) * p->in0_elems * 2;
+  b.gin_bytes = p->last ? 0 : static_cast<int64_t>(p->B) * p->layers[p->nlayers() - 1].out_elems() * 2;
+  CUDA_OK(cudaIpcGetMemHandle(&b.flags, p->flags));
+  if (!p->first)
+    for (int i = 0; i < p->A0; ++i) CUDA_OK(cudaIpcGetMemHandle(&b.in[i], p->act[i][0]));
+  if (!p->last)
+    for (int i = 0; i < 2; ++i) CUDA_OK(cudaIpcGetMemHandle(&b.gin[i], p->gin[i]));
+  std::memcpy(out, &b, sizeof(b));
+  *n = sizeof(b);
+  return TPS_OK;
+}
+
+tps_status tps_ipc_connect(tps_pipeline* p, const void* prev_blob, const void* next_blob) {
+  TPS_TRY(check_usable(p));
+  if (p->transport != TPS_TRANSPORT_IPC) return fail(TPS_E_CONFIG, "handle is not IPC transport");
+  if (p->ipc_connected) return fail(TPS_E_STATE, "already connected");
+  if (p->first != (prev_blob == nullptr) || p->last != (next_blob == nullptr))
+    return fail(TPS_E_INVALID_ARG, "stage %d needs %s prev and %s next descriptors", p->s, p->first ? "no" : "a",
+                p->last ? "no" : "a");
+  if (prev_blob) {
+    IpcBlob b;
+    std::memcpy(&b, prev_blob, sizeof(b));
+    const int64_t want = static_cast<int64_t>(p->B) * p->in0_elems * 2;
+    if (b.magic != IPC_MAGIC || b.stage != p->s - 1 || b.num_stages != p->S || b.gin_bytes != want)
+      return fail(TPS_E_CONFIG, "bad descriptor for stage %d (stage %d, %lld gradient bytes, want %lld)", p->s - 1,
+                  b.stage, (long long)b.gin_bytes, (long long)want);
+    void* v = nullptr;
+    TPS_TRY(ipc_open(p, b.flags, &v));
+    p->prev_flags = static_cast<uint64_t*>(v);
+    for (int i = 0; i < 2; ++i) {
+      TPS_TRY(ipc_open(p, b.gin[i], &v));
+      p->prev_gin[i] = static_cast<uint16_t*>(v);
+    }
+  }
+  if (next_blob) {
+    IpcBlob b;
+    std::memcpy(&b, next_blob, sizeof(b));
+    const int64_t want = static_cast<int64_t>(p->B) * p->layers[p->nlayers() - 1].out_elems() * 2;
+    if (b.magic != IPC_MAGIC || b.stage != p->s + 1 || b.num_stages != p->S || b.in_bytes != want || b.A0 < 1 ||
+        b.A0 > 16)
+      return fail(TPS_E_CONFIG, "bad descriptor for stage %d (stage %d, %lld input bytes, want %lld)", p->s + 1,
+                  b.stage, (long long)b.in_bytes, (long long)want);
+    void* v = nullptr;
+    TPS_TRY(ipc_open(p, b.flags, &v));
+    p->next_flags = static_cast<uint64_t*>(v);
+    p->next_in.assign(b.A0, nullptr);
+    for (int i = 0; i < b.A0; ++i) {
+      TPS_TRY(ipc_open(p, b.in[i], &v));
+      p->next_in[i] = static_cast<uint16_t*>(v);
+    }
+  }
+  p->ipc_connected = true;
   return TPS_OK;
 }
 
@@ -1781,6 +1990,18 @@ tps_status tps_run_schedule_local(tps_pipeline* const* st, int32_t S, int64_t fi
     if (!progress) return fail(TPS_E_STATE, "local schedule deadlock");
   }
   for (int s = 0; s < S; ++s) TPS_TRY(join_update_stream(st[s]));
+  return TPS_OK;
+}
+
+tps_status tps_join(tps_pipeline* p, uint64_t stream) {
+  TPS_TRY(check_usable(p));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  // record the tail of every stream of the handle and make `st` wait for it
+  for (cudaStream_t hs : {p->cs, p->s_upd, p->s_w, p->s_fin, p->s_fout, p->s_bin, p->s_bout}) {
+    if (!hs || hs == st) continue;
+    CUDA_OK(cudaEventRecord(p->ev_caller, hs));
+    CUDA_OK(cudaStreamWaitEvent(st, p->ev_caller, 0));
+  }
   return TPS_OK;
 }
 

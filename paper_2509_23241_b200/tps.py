@@ -16,7 +16,8 @@ LIB_PATH = os.environ.get("TPS_LIB") or os.path.join(HERE, "lib", "libtps.so")
 
 TPS_V, TPS_I = 0, 1
 TPS_BLEND_EQ1, TPS_BLEND_CONVEX = 0, 1
-TPS_TRANSPORT_NONE, TPS_TRANSPORT_LOCAL, TPS_TRANSPORT_NCCL = 0, 1, 2
+TPS_TRANSPORT_NONE, TPS_TRANSPORT_LOCAL, TPS_TRANSPORT_NCCL, TPS_TRANSPORT_IPC = 0, 1, 2, 3
+TPS_IPC_BLOB_BYTES = 2048
 TPS_EV_F, TPS_EV_B, TPS_EV_U = 0, 1, 2
 GEMM_FWD, GEMM_DGRAD, GEMM_WGRAD, GEMM_DGRAD_BLEND = 0, 1, 2, 3
 STATUS = {0: "TPS_OK", 1: "TPS_E_INVALID_ARG", 2: "TPS_E_CONFIG", 3: "TPS_E_ORDER", 4: "TPS_E_STALENESS",
@@ -32,7 +33,7 @@ EXPORTS = [
     "tps_init_weights_synthetic", "tps_get_losses", "tps_get_trace", "tps_clear_trace", "tps_memory_stats",
     "tps_set_profiling", "tps_kernel_stats", "tps_launch_count", "tps_fill_synthetic", "tps_gemm",
     "tps_conv_gemm", "tps_partition", "tps_im2col", "tps_col2im", "tps_bn_forward", "tps_bn_backward",
-    "tps_pool_op", "tps_conv2d_gemm", "tps_debug_progress", "tps_memory_observed",
+    "tps_pool_op", "tps_conv2d_gemm", "tps_debug_progress", "tps_memory_observed", "tps_join", "tps_ipc_export", "tps_ipc_connect",
 ]
 TPS_LAYER_LINEAR, TPS_LAYER_CONV3X3, TPS_LAYER_MAXPOOL2 = 0, 1, 2
 TPS_LAYER_CONV, TPS_LAYER_BN, TPS_LAYER_MAXPOOL3, TPS_LAYER_AVGPOOL = 3, 4, 5, 6
@@ -149,6 +150,9 @@ def lib() -> C.CDLL:
             "tps_debug_progress": (I32, [P, P, P, P]),
             "tps_conv2d_gemm": (I32, [I32, I32, I32, I32, I32, I32, I32, I32, I32, P, P, P, P, I32, F, F, U64]),
             "tps_memory_observed": (I32, [P, C.POINTER(I64)]),
+            "tps_join": (I32, [P, U64]),
+            "tps_ipc_export": (I32, [P, P, I64, C.POINTER(I64)]),
+            "tps_ipc_connect": (I32, [P, P, P]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -392,6 +396,22 @@ class Pipeline:
 
     def synchronize(self):
         check(lib().tps_synchronize(self.h))
+
+    def ipc_export(self) -> bytes:
+        """This stage's IPC exchange descriptor (send it to the neighbouring stages)."""
+        buf = C.create_string_buffer(TPS_IPC_BLOB_BYTES)
+        n = C.c_int64()
+        check(lib().tps_ipc_export(self.h, buf, TPS_IPC_BLOB_BYTES, C.byref(n)))
+        return buf.raw[: n.value]
+
+    def ipc_connect(self, prev: bytes | None, nxt: bytes | None):
+        pb = C.create_string_buffer(prev, len(prev)) if prev else None
+        nb = C.create_string_buffer(nxt, len(nxt)) if nxt else None
+        check(lib().tps_ipc_connect(self.h, pb, nb))
+
+    def join(self, stream: int):
+        """`stream` waits (stream-ordered) for all work the handle has enqueued."""
+        check(lib().tps_join(self.h, stream))
 
     # state
     def init_weights_synthetic(self):

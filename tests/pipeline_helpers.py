@@ -78,13 +78,13 @@ def run_oracle_graph(layers, bounds, m, b, M, variant, blend, lam, lr, mu, wd=0.
 
 
 def run_oracle(dims, bounds, m, b, M, variant, blend, lam, lr, mu, wd=0.0, seed=0, kind=synthgen.X_SIGNED,
-               layers=None, max_inflight=0):
+               layers=None, max_inflight=0, exact=False):
     if layers:
         xs, ys, w0, b0 = net_workload(layers, m, b, M, seed, kind)
     else:
         xs, ys, w0, b0 = workload(dims, m, b, M, seed, kind)
     cfg = opipe.Config(dims, bounds, m, b, M, variant=variant, blend=blend, lam=lam, lr=lr, momentum=mu, wd=wd,
-                       layers=layers, max_inflight=max_inflight)
+                       layers=layers, max_inflight=max_inflight, exact=exact)
     return opipe.run(cfg, xs, ys, w0, b0)
 
 

@@ -17,6 +17,9 @@ oracle as the bf16 oracle is to exact arithmetic:
     storage (the bf16 oracle's update has cosine 0.1-0.4 with the fp64 one, relative L2
     distance 1.0-1.3), so per layer ‖ΔW_gpu - ΔW_ref‖₂ / ‖ΔW_ref‖₂ <= max(0.05, 1.25·gap₂).
 """
+import json
+import os
+
 import numpy as np
 import pytest
 
@@ -52,6 +55,11 @@ def measure(layers, bounds, m, b, M, variant, blend, lr=0.01, mu=0.9, mode="para
     assert expand_gpu_trace(stages) == oracle_trace(ref)
     lerr = np.abs(losses - ref.losses) / np.abs(ref.losses)
     lgap = np.abs(ex.losses - ref.losses) / np.abs(ref.losses)
+    diag = os.environ.get("TPS_DIAG_DIR")
+    if diag:
+        with open(os.path.join(diag, f"resnet_diag_{len(layers)}_{len(bounds)}_{m}x{b}_{mode}.json"), "a") as fh:
+            fh.write(json.dumps({"lerr": lerr.tolist(), "lgap": lgap.tolist(), "gpu_losses": np.asarray(losses).tolist(),
+                                 "ref_losses": ref.losses.tolist(), "exact_losses": ex.losses.tolist()}) + "\n")
     assert lerr.max() <= max(1e-3, 2 * lgap.max()), (lerr, lgap)
     bad, allv = {}, {}
     for st in stages:
@@ -84,6 +92,9 @@ def measure(layers, bounds, m, b, M, variant, blend, lr=0.01, mu=0.9, mode="para
             if not err <= lim:
                 bad[(l, layers[l]["kind"])] = (round(err, 5), round(lim, 5))
         st.close()
+    if diag:
+        with open(os.path.join(diag, f"resnet_diag_{len(layers)}_{len(bounds)}_{m}x{b}_{mode}.json"), "a") as fh:
+            fh.write(json.dumps({str(k): v for k, v in allv.items()}) + "\n")
     return bad, allv
 
 

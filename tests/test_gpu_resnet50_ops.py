@@ -56,8 +56,8 @@ def pad16(x):
     return -(-x // 16) * 16
 
 
-def conv_shapes():
-    layers, _ = ograph.resnet_layers()
+def conv_shapes(H=224):
+    layers, _ = ograph.resnet_layers(H=H)
     seen, out = set(), []
     for sp in layers:
         if sp["kind"] != "conv":
@@ -81,6 +81,9 @@ def conv_mode(k, s, p, ci, co):
 
 
 SHAPES = conv_shapes()
+# the same network at 64x64 inputs (the reduced-resolution whole-net test): spatial sizes down to
+# 2x2, where the implicit-GEMM tiles span several images
+SHAPES_64 = [sh for sh in conv_shapes(64) if sh not in SHAPES]
 
 
 def test_resnet50_has_the_expected_distinct_conv_shapes():
@@ -90,7 +93,7 @@ def test_resnet50_has_the_expected_distinct_conv_shapes():
     assert {conv_mode(*s[:5]) for s in SHAPES} == {0, 1, 2, 3}
 
 
-@pytest.mark.parametrize("shape", SHAPES, ids=lambda s: "k%d_s%d_p%d_%dto%d_h%d" % s)
+@pytest.mark.parametrize("shape", SHAPES + SHAPES_64, ids=lambda s: "k%d_s%d_p%d_%dto%d_h%d" % s)
 def test_conv_fwd_dgrad_wgrad_at_resnet50_shape(gpu_lib, shape):
     from paper_2509_23241_b200 import tps
     k, s, p, ci, co, H = shape

@@ -242,7 +242,9 @@ def test_torch_allocator_hook(gpu_lib):
     np.testing.assert_array_equal(l_t, l_c)
     for a, c in zip(st_t, st_c):
         np.testing.assert_array_equal(a.get_weights(0)[0], c.get_weights(0)[0])
-        assert c.memory_observed() >= c.memory_stats()["peak"]   # cudaMalloc path: observed by the device
+        # cudaMalloc path: the device's free memory dropped by about the library's own count
+        # (2 MiB pages: small allocations share pages with earlier ones)
+        assert abs(c.memory_observed() - c.memory_stats()["peak"]) <= 4 * 2 ** 20 + c.memory_stats()["peak"] // 10
     for st in st_t + st_c:
         st.close()
     torch.cuda.synchronize()
