@@ -54,6 +54,10 @@ def parse():
     ap.add_argument("--same-device", action="store_true",
                     help="N > 1 on ONE GPU: every rank uses cuda:0 (gloo process group); exercises the "
                          "multi-process path on a one-GPU box (throughput is then time-sliced)")
+    ap.add_argument("--prio-stream", action="store_true",
+                    help="enqueue on a high-priority compute stream (the weight-gradient / optimizer streams "
+                         "stay at the default priority)")
+    ap.add_argument("--no-torch-alloc", action="store_true", help="cudaMalloc instead of the torch allocator hook")
     ap.add_argument("--no-method", action="store_true", help="skip the C2 method leg (4 stages, V / I-EQ1 / "
                     "I-CONVEX, staleness sweep, measured memory)")
     return ap.parse_args()
@@ -295,11 +299,14 @@ def main():
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     red_dev = "cpu" if args.same_device else "cuda"
     dims, bounds = model(S)
-    # the compute stream at the greatest priority (the dgrad chain is the critical path; the
-    # library's weight-gradient and optimizer streams run at the least)
-    prio_stream = torch.cuda.Stream(priority=-1)
-    torch.cuda.set_stream(prio_stream)
-    stream = prio_stream.cuda_stream
+    # a real (non-default) stream: the library enqueues its compute work on it and joins its
+    # weight-gradient / optimizer streams into it at the end of every run, so CUDA events on it
+    # bracket ALL of a step's device work.  (On the legacy default stream, handle 0, the library
+    # would create its own non-blocking stream and events on stream 0 would time the host's
+    # enqueue instead of the device.)  --prio-stream: high priority for the compute stream.
+    torch.cuda.set_stream(torch.cuda.Stream(priority=-1 if args.prio_stream else 0))
+    stream = torch.cuda.current_stream().cuda_stream
+    assert stream != 0
 
     use_ipc = S > 1 and args.transport == "ipc"
 
@@ -319,7 +326,7 @@ def main():
                              transport=(tps.TPS_TRANSPORT_IPC if use_ipc else tps.TPS_TRANSPORT_NCCL) if S > 1
                              else tps.TPS_TRANSPORT_NONE,
                              nccl_ids=ids, device=local, seed=0, compute_stream=stream,
-                             fuse_update=args.fuse_update, torch_alloc=True)
+                             fuse_update=args.fuse_update, torch_alloc=not args.no_torch_alloc)
         p = tps.Pipeline(spec)
         p.init_weights_synthetic()
         if use_ipc:   # exchange descriptors with the neighbouring stages, map their buffers

@@ -195,7 +195,17 @@ typedef struct {
   void* (*dev_alloc)(size_t bytes, void* ctx);
   void (*dev_free)(void* ptr, void* ctx);
   void* alloc_ctx;
-  int32_t reserved[4];
+  /* Pipeline x data parallelism ("pipelining and data parallelism together";
+   * SURVEY §8(f) NEXT-2): dp_size replicas of the whole pipeline, each on its own mini-batches;
+   * stage s of every replica averages the R weight/bias gradients (replica order, fp32) inside
+   * one fused reduce + SGD kernel that reads the peers' gradient buffers directly (NVLink peer
+   * memory / same-process pointers), so the replicas stay bitwise identical.  dp_size = 1: off.
+   * With dp_size > 1 the update runs as a separate kernel (fuse_update is ignored), chain
+   * networks only (TPS_E_UNSUPPORTED for graph networks), mini-batches numbered contiguously.
+   * Replica r of mini-batch j reads rows [r·B, (r+1)·B) of pool entry j % pool.               */
+  int32_t dp_size;              /* R >= 1 (<= 8)                                        */
+  int32_t dp_rank;              /* 0 <= dp_rank < R                                     */
+  int32_t reserved[2];
 } tps_config;
 
 typedef struct tps_pipeline tps_pipeline;  /* opaque; one per stage */
@@ -224,6 +234,15 @@ tps_status tps_local_link(tps_pipeline* const* stages, int32_t num_stages);
 #define TPS_IPC_BLOB_BYTES 2048
 tps_status tps_ipc_export(tps_pipeline* p, void* out, int64_t cap, int64_t* n);
 tps_status tps_ipc_connect(tps_pipeline* p, const void* prev_blob, const void* next_blob);
+/* Data parallelism (dp_size > 1): connect the R replicas of ONE stage, one process per
+ * replica (each process its own CUDA context: replicas synchronise through flag words that
+ * another process writes, which must never sit behind a blocked wait in a shared hardware
+ * queue, so replicas are never handles of one process).  tps_dp_export writes this replica's
+ * descriptor (IPC handles of its per-layer gradient buffers and flag words; out = NULL returns
+ * the size in *n); tps_dp_connect takes all R descriptors in replica order (its own included).
+ * TPS_E_CONFIG for mismatched shapes / stages / ranks.                                      */
+tps_status tps_dp_export(tps_pipeline* p, void* out, int64_t cap, int64_t* n);
+tps_status tps_dp_connect(tps_pipeline* p, const void* const* blobs, int32_t dp_size);
 
 /* ---- the training step (one mini-batch = B(j) U(j) + m forwards) ----------- */
 /* Declare a run of mini-batches [first_mb, first_mb+n_mb): builds the stage's
@@ -257,8 +276,9 @@ tps_status tps_stage_update(tps_pipeline* p, int64_t mb);
  * Pools may be device or host memory (host: copied per mini-batch inside).   */
 tps_status tps_run_schedule(tps_pipeline* p, int64_t first_mb, int64_t n_mb,
                             const void* x_pool, const int32_t* y_pool, int32_t pool);
-/* LOCAL transport: drive all S linked handles of this process through the same
- * range, interleaving stages in a dependency-respecting host order.            */
+/* LOCAL transport: drive all linked handles of this process through the same range,
+ * interleaving them in a dependency-respecting host order.  num_stages = S handles of one
+ * pipeline in stage order, or R·S handles of R data-parallel replicas (replica-major).      */
 tps_status tps_run_schedule_local(tps_pipeline* const* stages, int32_t num_stages,
                                   int64_t first_mb, int64_t n_mb,
                                   const void* x_pool, const int32_t* y_pool, int32_t pool);
@@ -350,6 +370,15 @@ tps_status tps_gemm(int32_t mode, int32_t M, int32_t N, int32_t K,
                     const void* A, int32_t lda, const void* B, int32_t ldb, const void* B2,
                     void* out, int32_t ldo, int32_t out_f32, const float* bias, int32_t relu,
                     float alpha, float beta, const void* mask, int32_t ldm, uint64_t stream);
+
+/* Weight gradient with the fused SGD/momentum update epilogue (the kernel the pipeline runs
+ * with fuse_update = 1; row a10): for g = Aᵀ·B (A stored [K,M] ld=lda, B stored [K,N] ld=ldb,
+ * bf16, fp32 accumulation), per element of the fp32 master w [M,N] (ld=ldw) and momentum v:
+ *   g' = g + wd·w ; v = mu·v + g' ; w = w - lr·v  (fp32, one rounding per op; mu = 0: v unused)
+ * and ver [M,N] (bf16, ld=ldw) = bf16_rne(w).  The gradient is never written to memory.      */
+tps_status tps_gemm_wgrad_sgd(int32_t M, int32_t N, int32_t K, const void* A, int32_t lda, const void* B,
+                              int32_t ldb, float* w, float* v, void* ver, int32_t ldw, float lr, float mu,
+                              float wd, uint64_t stream);
 
 /* ---- stage partitioner ("distribute the DNNs ... in such a way
  * that a balance is maintained between the memory consumptions in each node") ----------

@@ -82,6 +82,56 @@ __global__ void __launch_bounds__(256) sgd_update_kernel(float* __restrict__ w, 
   }
 }
 
+// ------------------------------------------------------------------ data-parallel reduce + update
+// Pipeline x data parallelism (SURVEY §8(f) NEXT-2, P:75 / P:134): the R replicas of a stage
+// hold the gradients of their own mini-batches; one pass reads all R of them (the peers' through
+// NVLink peer mappings), averages them in replica order, g = (Σ_r g_r)·(1/R), and applies the
+// SGD/momentum step of sgd_update_kernel (same operations, same order) — the all-reduce and the
+// update fused, so the averaged gradient is never written.  Every replica computes the same
+// sum in the same order, so the replicas' parameters stay bitwise identical.
+template <bool MOMENTUM, bool WRITE_VER>
+__global__ void __launch_bounds__(256) sgd_update_dp_kernel(float* __restrict__ w, float* __restrict__ v,
+                                                            GradList gl, uint16_t* __restrict__ ver, int64_t n4,
+                                                            float lr, float mu, float wd) {
+  const float inv = 1.0f / static_cast<float>(gl.n);
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float4 gs = __ldcg(reinterpret_cast<const float4*>(gl.p[0]) + i);
+    for (int r = 1; r < gl.n; ++r) {
+      const float4 t = __ldcg(reinterpret_cast<const float4*>(gl.p[r]) + i);
+      gs.x = __fadd_rn(gs.x, t.x); gs.y = __fadd_rn(gs.y, t.y); gs.z = __fadd_rn(gs.z, t.z); gs.w = __fadd_rn(gs.w, t.w);
+    }
+    const float gg[4] = {__fmul_rn(gs.x, inv), __fmul_rn(gs.y, inv), __fmul_rn(gs.z, inv), __fmul_rn(gs.w, inv)};
+    float4 wv = reinterpret_cast<float4*>(w)[i];
+    float ww[4] = {wv.x, wv.y, wv.z, wv.w};
+    float vv[4] = {0.f, 0.f, 0.f, 0.f};
+    if (MOMENTUM) {
+      const float4 t = reinterpret_cast<float4*>(v)[i];
+      vv[0] = t.x; vv[1] = t.y; vv[2] = t.z; vv[3] = t.w;
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float gp = __fadd_rn(gg[e], __fmul_rn(wd, ww[e]));
+      float upd;
+      if (MOMENTUM) {
+        vv[e] = __fadd_rn(__fmul_rn(mu, vv[e]), gp);
+        upd = vv[e];
+      } else {
+        upd = gp;
+      }
+      ww[e] = __fsub_rn(ww[e], __fmul_rn(lr, upd));
+    }
+    reinterpret_cast<float4*>(w)[i] = make_float4(ww[0], ww[1], ww[2], ww[3]);
+    if (MOMENTUM) reinterpret_cast<float4*>(v)[i] = make_float4(vv[0], vv[1], vv[2], vv[3]);
+    if (WRITE_VER) {
+      uint2 o;
+      o.x = static_cast<uint32_t>(f2bf(ww[0])) | (static_cast<uint32_t>(f2bf(ww[1])) << 16);
+      o.y = static_cast<uint32_t>(f2bf(ww[2])) | (static_cast<uint32_t>(f2bf(ww[3])) << 16);
+      reinterpret_cast<uint2*>(ver)[i] = o;
+    }
+  }
+}
+
 // ------------------------------------------------------------------ bias gradient
 constexpr int BG_COLS = 256;   // columns per block (32 threads x 8 columns)
 constexpr int BG_ROWS = 8;     // row lanes per block
@@ -1139,6 +1189,20 @@ cudaError_t launch_sgd_update(float* w, float* v, const float* g, uint16_t* ver,
   else if (mom) sgd_update_kernel<true, false><<<grid, 256, 0, st>>>(w, v, g, ver, n4, lr, mu, wd);
   else if (ver) sgd_update_kernel<false, true><<<grid, 256, 0, st>>>(w, v, g, ver, n4, lr, mu, wd);
   else sgd_update_kernel<false, false><<<grid, 256, 0, st>>>(w, v, g, ver, n4, lr, mu, wd);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sgd_update_dp(float* w, float* v, const GradList& g, uint16_t* ver, int64_t n, float lr, float mu,
+                                 float wd, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  if (n % 4 || g.n < 1 || g.n > GradList::MAX) return cudaErrorInvalidValue;
+  const int64_t n4 = n / 4;
+  const int grid = grid_for(n4, 256, 8);
+  const bool mom = mu != 0.0f;
+  if (mom && ver) sgd_update_dp_kernel<true, true><<<grid, 256, 0, st>>>(w, v, g, ver, n4, lr, mu, wd);
+  else if (mom) sgd_update_dp_kernel<true, false><<<grid, 256, 0, st>>>(w, v, g, ver, n4, lr, mu, wd);
+  else if (ver) sgd_update_dp_kernel<false, true><<<grid, 256, 0, st>>>(w, v, g, ver, n4, lr, mu, wd);
+  else sgd_update_dp_kernel<false, false><<<grid, 256, 0, st>>>(w, v, g, ver, n4, lr, mu, wd);
   return cudaGetLastError();
 }
 

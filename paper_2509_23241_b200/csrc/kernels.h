@@ -13,6 +13,16 @@ namespace tps {
 cudaError_t launch_sgd_update(float* w, float* v, const float* g, uint16_t* ver, int64_t n, float lr, float mu,
                               float wd, cudaStream_t st, int blocks_per_sm = 8);
 
+// Data parallelism (NEXT-2): the gradients of the R replicas of a stage (own + peers' mapped
+// buffers), averaged in replica order g = (Σ_r g_r)·(1/R) and applied as launch_sgd_update does.
+struct GradList {
+  static constexpr int MAX = 8;
+  const float* p[MAX];
+  int n;
+};
+cudaError_t launch_sgd_update_dp(float* w, float* v, const GradList& g, uint16_t* ver, int64_t n, float lr, float mu,
+                                 float wd, cudaStream_t st);
+
 // db[c] = Σ_{r<rows} G[r, c] for c < cols (G bf16 [rows, ldg]); deterministic two-phase
 // reduction using `scratch` (>= bias_grad_scratch_floats(rows, cols) floats).
 int64_t bias_grad_scratch_floats(int rows, int cols);

@@ -229,6 +229,14 @@ struct tps_pipeline {
   std::vector<void*> ipc_opened;
   bool ipc_connected = false, ipc_direct = false;
   int64_t ipc_next_mb = 0;                    // runs number their mini-batches contiguously from 0
+  // data parallelism (NEXT-2): R replicas of this stage
+  int dp = 1, dp_rank = 0;
+  uint64_t* dp_flags = nullptr;               // own [L][2R]: [k][q] = j+1 when replica q's gradients of
+                                              // layer k for mb j are ready; [k][R+q] = j+1 when replica
+                                              // q has consumed MY gradients of layer k for mb j
+  std::vector<uint64_t*> dp_peer_flags;       // [R] flag arrays of the replicas (own at dp_rank)
+  std::vector<std::vector<float*>> dp_dW, dp_db;   // [layer][R] gradient buffers of the replicas
+  bool dp_connected = false;
   std::map<std::pair<int64_t, int>, Msg> mbox_fwd;  // keyed (mb, group), filled by prev stage
   std::map<int64_t, Msg> mbox_bwd;                  // keyed mb, filled by next stage
 
@@ -572,6 +580,39 @@ void update_stash_peak(tps_pipeline* p) {
   const int64_t n_live = std::min<int64_t>(static_cast<int64_t>(live.size()), p->R);
   const int64_t stash = (n_live - 1) * p->ver_bytes;
   p->peak_stash_live = std::max(p->peak_stash_live, stash);
+}
+
+// ------------------------------------------------------------------ data parallelism
+// Layer k's gradients of mb j are complete on the compute stream: on the optimizer stream,
+// announce them to every replica, wait for theirs, run the fused replica-average + SGD step
+// (weights and bias), then tell every replica its gradients were consumed.
+tps_status dp_update(tps_pipeline* p, Layer& L, int k, int64_t j, int64_t vn) {
+  cudaStream_t us = p->s_upd;
+  const int R = p->dp;
+  CUDA_OK(cudaEventRecord(p->ev_grad_ready[k], p->cs));
+  CUDA_OK(cudaStreamWaitEvent(us, p->ev_grad_ready[k], 0));
+  const size_t base = static_cast<size_t>(k) * 2 * R;
+  const uint64_t v = static_cast<uint64_t>(j) + 1;
+  for (int q = 0; q < R; ++q)
+    if (q != p->dp_rank) TPS_TRY(flag_write(us, &p->dp_peer_flags[q][base + p->dp_rank], v));
+  for (int q = 0; q < R; ++q)
+    if (q != p->dp_rank) TPS_TRY(flag_wait(us, &p->dp_flags[base + q], v));
+  tps::GradList gw{}, gb{};
+  gw.n = gb.n = R;
+  for (int q = 0; q < R; ++q) {
+    gw.p[q] = p->dp_dW[k][q];
+    gb.p[q] = p->dp_db[k][q];
+  }
+  const int64_t n = static_cast<int64_t>(L.Np) * L.Kp;
+  TimedLaunch tl{};
+  TPS_TRY(time_begin(p, &tl, 4, (p->mu != 0.f ? 18.0 + 4.0 * R : 10.0 + 4.0 * R) * n, us));
+  CUDA_OK(tps::launch_sgd_update_dp(L.W, L.mW, gw, L.ver[vn % p->R], n, p->lr, p->mu, p->wd, us));
+  TPS_TRY(time_end(p, &tl, us));
+  CUDA_OK(tps::launch_sgd_update_dp(L.b, L.mb, gb, nullptr, L.Np, p->lr, p->mu, p->wd, us));
+  p->launches += 2;
+  for (int q = 0; q < R; ++q)
+    if (q != p->dp_rank) TPS_TRY(flag_write(us, &p->dp_peer_flags[q][base + R + p->dp_rank], v));
+  return TPS_OK;
 }
 
 // ------------------------------------------------------------------ the three events
@@ -1093,6 +1134,11 @@ tps_status do_backward(tps_pipeline* p, int64_t j, int staleness) {
         ga.lr = p->lr; ga.mu = p->mu; ga.wd = p->wd;
       }
       cudaStream_t ws = p->cs;
+      if (p->dp > 1) {   // the replicas must have read this layer's gradients of mb j-1 before they are rewritten
+        for (int q = 0; q < p->dp; ++q)
+          if (q != p->dp_rank)
+            TPS_TRY(flag_wait(p->cs, &p->dp_flags[static_cast<size_t>(k) * 2 * p->dp + p->dp + q], static_cast<uint64_t>(j)));
+      }
       // concurrent with layer k-1's dgrad on the compute stream: the other share of the SMs
       if (p->split_w && p->part_dgrad > 0 && k > 0 && p->layers[k - 1].gidx > 0 &&
           p->layers[k - 1].kind != TPS_LAYER_MAXPOOL2)
@@ -1112,8 +1158,9 @@ tps_status do_backward(tps_pipeline* p, int64_t j, int staleness) {
       }
       if (p->split_w) CUDA_OK(cudaEventRecord(p->ev_w_done[k], p->s_w));
       if (!bias_side) {   // bias gradient and the bias's SGD/momentum step in one launch
-        CUDA_OK(tps::launch_bias_grad_sgd(G, rows, Lk.Np, Lk.Np, Lk.db, p->scratch, Lk.b, Lk.mb, p->lr, p->mu, p->wd,
-                                          p->cs));
+        // (data parallel: the gradient only; the step runs on the replica average below)
+        CUDA_OK(tps::launch_bias_grad_sgd(G, rows, Lk.Np, Lk.Np, Lk.db, p->scratch, p->dp > 1 ? nullptr : Lk.b, Lk.mb,
+                                          p->lr, p->mu, p->wd, p->cs));
         p->launches += 1;
       }
       // U(j) always directly follows B(j) in the static order (reading Z7), so the update of
@@ -1121,7 +1168,9 @@ tps_status do_backward(tps_pipeline* p, int64_t j, int staleness) {
       // it runs on the optimizer stream, HBM-bound, underneath the remaining tensor-bound GEMMs
       // of this backward.  The next forward of layer k waits for ev_upd_done[k].
       cudaStream_t us = p->fuse_update ? p->cs : p->s_upd;
-      if (!p->fuse_update) {
+      if (!p->fuse_update && p->dp > 1) {
+        TPS_TRY(dp_update(p, Lk, k, j, vn));
+      } else if (!p->fuse_update) {
         CUDA_OK(cudaEventRecord(p->ev_grad_ready[k], p->cs));
         CUDA_OK(cudaStreamWaitEvent(us, p->ev_grad_ready[k], 0));
         const int64_t n = static_cast<int64_t>(Lk.Np) * Lk.Kp;
@@ -1204,10 +1253,13 @@ tps_status do_update(tps_pipeline* p, int64_t j) {
 tps_status begin_run(tps_pipeline* p, int64_t first, int64_t n) {
   if (n <= 0 || first < 0) return fail(TPS_E_INVALID_ARG, "bad run [%lld, +%lld)", (long long)first, (long long)n);
   if (p->in_run) return fail(TPS_E_ORDER, "stage %d: previous run not finished", p->s);
-  if (p->transport == TPS_TRANSPORT_IPC) {
-    if (!p->ipc_connected) return fail(TPS_E_STATE, "IPC transport: tps_ipc_connect first");
+  if (p->transport == TPS_TRANSPORT_IPC && !p->ipc_connected)
+    return fail(TPS_E_STATE, "IPC transport: tps_ipc_connect first");
+  if (p->dp > 1 && !p->dp_connected) return fail(TPS_E_STATE, "data parallelism: tps_dp_connect first");
+  if (p->transport == TPS_TRANSPORT_IPC || p->dp > 1) {
+    // flag words carry mini-batch numbers: runs continue the numbering from 0
     if (first != p->ipc_next_mb)
-      return fail(TPS_E_ORDER, "IPC transport: runs number mini-batches contiguously (expected first %lld)",
+      return fail(TPS_E_ORDER, "IPC / data-parallel handle: runs number mini-batches contiguously (expected first %lld)",
                   (long long)p->ipc_next_mb);
     p->ipc_next_mb = first + n;
   }
@@ -1230,9 +1282,10 @@ tps_status fire(tps_pipeline* p, const tps_event& e, const void* x_pool, const i
     const int64_t slot = e.mb % pool;
     const void* x = nullptr;
     const int32_t* y = nullptr;
-    if (p->first)
-      x = static_cast<const uint16_t*>(x_pool) + (slot * p->B + static_cast<int64_t>(e.micro) * p->bsz) * p->dims[0];
-    if (p->last) y = y_pool + slot * p->B + static_cast<int64_t>(e.micro) * p->bsz;
+    // replica r of mini-batch j reads rows [r·B, (r+1)·B) of pool entry j % pool
+    const int64_t row = (slot * p->dp + p->dp_rank) * p->B + static_cast<int64_t>(e.micro) * p->bsz;
+    if (p->first) x = static_cast<const uint16_t*>(x_pool) + row * p->dims[0];
+    if (p->last) y = y_pool + row;
     return do_forward(p, e.mb, e.micro, e.micro_count, x, y);
   }
   if (e.kind == TPS_EV_B) return do_backward(p, e.mb, -1);
@@ -1502,6 +1555,10 @@ tps_status tps_pipeline_init(const tps_config* c, tps_pipeline** out) {
     return fail(TPS_E_CONFIG, "max_inflight other than S - s needs S = 1");
   if (c->staleness_mode != 0 && c->staleness_mode != 1) return fail(TPS_E_CONFIG, "bad staleness_mode");
   if ((c->dev_alloc == nullptr) != (c->dev_free == nullptr)) return fail(TPS_E_CONFIG, "dev_alloc and dev_free go together");
+  if (c->dp_size < 0 || c->dp_size > 8 || (c->dp_size > 1 && (c->dp_rank < 0 || c->dp_rank >= c->dp_size)))
+    return fail(TPS_E_CONFIG, "need 1 <= dp_size <= 8 and 0 <= dp_rank < dp_size");
+  if (c->dp_size > 1 && c->num_stages > 1 && c->transport != TPS_TRANSPORT_IPC)
+    return fail(TPS_E_CONFIG, "data parallelism runs one process per stage replica (IPC transport)");
   if (c->variant != TPS_V && c->variant != TPS_I) return fail(TPS_E_CONFIG, "bad variant");
   if (c->blend != TPS_BLEND_EQ1 && c->blend != TPS_BLEND_CONVEX) return fail(TPS_E_CONFIG, "bad blend");
   if (c->variant == TPS_I && !(c->lambda > 0)) return fail(TPS_E_CONFIG, "lambda must be > 0 (P:227)");
@@ -1544,7 +1601,7 @@ tps_status tps_pipeline_init(const tps_config* c, tps_pipeline** out) {
   if (c->max_inflight > 0) p->Kmax = c->max_inflight;
   p->staleness_mode = c->staleness_mode;
   p->alloc_fn = c->dev_alloc; p->free_fn = c->dev_free; p->alloc_ctx = c->alloc_ctx;
-  if (p->transport == TPS_TRANSPORT_IPC) {
+  if (p->transport == TPS_TRANSPORT_IPC || p->dp > 1) {
     // exported buffers must be whole cudaMalloc allocations (IPC handles name allocations)
     p->alloc_fn = nullptr; p->free_fn = nullptr;
   }
@@ -1557,6 +1614,15 @@ tps_status tps_pipeline_init(const tps_config* c, tps_pipeline** out) {
   p->eq1_on_load = env && env[0] == '1';
   p->fuse_update = c->fuse_update != 0;
   p->graph = graph;
+  p->dp = std::max(1, c->dp_size);
+  p->dp_rank = p->dp > 1 ? c->dp_rank : 0;
+  if (p->dp > 1) {
+    if (graph) {
+      delete p;
+      return fail(TPS_E_UNSUPPORTED, "data parallelism is implemented for chain networks");
+    }
+    p->fuse_update = false;   // the update needs the replica average: separate fused reduce + SGD kernel
+  }
   if (const char* e2 = std::getenv("TPS_UPD_BPS")) p->upd_blocks_per_sm = std::max(1, std::atoi(e2));
 
   auto cleanup = [&](tps_status st) {
@@ -1654,9 +1720,10 @@ tps_status tps_pipeline_init(const tps_config* c, tps_pipeline** out) {
     return cleanup(st);
   if (p->split_w) {
     // SM partition of the concurrent pair (dgrad of layer k-1 | fused wgrad + update of layer k):
-    // TPS_SPLIT_FRAC = the dgrad's fraction (default 0.5; 0 = no partition, both grids full)
+    // TPS_SPLIT_FRAC = the dgrad's fraction (default 0 = no partition, both grids full: measured
+    // faster on C5, 573k vs 533k samples/s at 0.5, 486k at 0.4, 541k at 0.6)
     cudaDeviceGetAttribute(&p->nsm, cudaDevAttrMultiProcessorCount, p->device);
-    double f = 0.5;
+    double f = 0.0;
     if (const char* e = std::getenv("TPS_SPLIT_FRAC")) f = std::atof(e);
     p->part_dgrad = f > 0.0 && f < 1.0 ? std::max(2, static_cast<int>(f * p->nsm + 1.0) / 2 * 2) : 0;
   }
@@ -1678,6 +1745,10 @@ tps_status tps_pipeline_init(const tps_config* c, tps_pipeline** out) {
 
   }
   const int nl = p->nlayers();
+  if (p->dp > 1) {
+    const tps_status fs = alloc_t(p, &p->dp_flags, static_cast<size_t>(nl) * 2 * p->dp, &p->mem_comm);
+    if (fs != TPS_OK) return cleanup(fs);
+  }
   if (p->transport == TPS_TRANSPORT_IPC) {
     const tps_status fs = alloc_t(p, &p->flags, 4, &p->mem_comm);
     if (fs != TPS_OK) return cleanup(fs);
@@ -1910,6 +1981,107 @@ tps_status tps_ipc_connect(tps_pipeline* p, const void* prev_blob, const void* n
   return TPS_OK;
 }
 
+// ---- data parallelism: connect the R replicas of one stage
+namespace {
+tps_status dp_check_peer(tps_pipeline* p, int S, int s, int R, int r, int nl, const int64_t* np_kp) {
+  if (S != p->S || s != p->s || R != p->dp || nl != p->nlayers())
+    return fail(TPS_E_CONFIG, "replica %d is stage %d of %d with %d layers (R = %d); this is stage %d of %d with %d layers (R = %d)",
+                r, s, S, nl, R, p->s, p->S, p->nlayers(), p->dp);
+  for (int k = 0; k < nl; ++k) {
+    const Layer& L = p->layers[k];
+    const int64_t want = L.has_w() ? static_cast<int64_t>(L.Np) * L.Kp : 0;
+    if (np_kp[k] != want) return fail(TPS_E_CONFIG, "replica %d: layer %d shape differs", r, k);
+  }
+  return TPS_OK;
+}
+
+void dp_alloc_tables(tps_pipeline* p) {
+  p->dp_peer_flags.assign(p->dp, nullptr);
+  p->dp_dW.assign(p->nlayers(), std::vector<float*>(p->dp, nullptr));
+  p->dp_db.assign(p->nlayers(), std::vector<float*>(p->dp, nullptr));
+}
+
+struct DpBlobHead {
+  int32_t magic, S, s, R, r, nl;
+  cudaIpcMemHandle_t flags;
+};
+constexpr int32_t DP_MAGIC = 0x54505344;   // "TPSD"
+}  // namespace
+
+tps_status tps_dp_export(tps_pipeline* p, void* out, int64_t cap, int64_t* n) {
+  TPS_TRY(check_usable(p));
+  if (!n) return fail(TPS_E_INVALID_ARG, "null n");
+  if (p->dp < 2) return fail(TPS_E_CONFIG, "dp_size < 2");
+  const int nl = p->nlayers();
+  const size_t bytes = sizeof(DpBlobHead) + static_cast<size_t>(nl) * (sizeof(int64_t) + 2 * sizeof(cudaIpcMemHandle_t));
+  *n = static_cast<int64_t>(bytes);
+  if (!out) return TPS_OK;
+  if (cap < static_cast<int64_t>(bytes)) return fail(TPS_E_INVALID_ARG, "cap < %zu", bytes);
+  uint8_t* o = static_cast<uint8_t*>(out);
+  DpBlobHead h{};
+  h.magic = DP_MAGIC; h.S = p->S; h.s = p->s; h.R = p->dp; h.r = p->dp_rank; h.nl = nl;
+  CUDA_OK(cudaIpcGetMemHandle(&h.flags, p->dp_flags));
+  std::memcpy(o, &h, sizeof(h));
+  o += sizeof(h);
+  for (int k = 0; k < nl; ++k) {
+    const Layer& L = p->layers[k];
+    const int64_t npk = L.has_w() ? static_cast<int64_t>(L.Np) * L.Kp : 0;
+    cudaIpcMemHandle_t hw{}, hb{};
+    if (L.has_w()) {
+      CUDA_OK(cudaIpcGetMemHandle(&hw, L.dW));
+      CUDA_OK(cudaIpcGetMemHandle(&hb, L.db));
+    }
+    std::memcpy(o, &npk, sizeof(npk)); o += sizeof(npk);
+    std::memcpy(o, &hw, sizeof(hw)); o += sizeof(hw);
+    std::memcpy(o, &hb, sizeof(hb)); o += sizeof(hb);
+  }
+  return TPS_OK;
+}
+
+tps_status tps_dp_connect(tps_pipeline* p, const void* const* blobs, int32_t R) {
+  TPS_TRY(check_usable(p));
+  if (!blobs || R != p->dp || R < 2) return fail(TPS_E_INVALID_ARG, "need dp_size descriptors");
+  if (p->dp_connected) return fail(TPS_E_STATE, "already connected");
+  const int nl = p->nlayers();
+  dp_alloc_tables(p);
+  for (int q = 0; q < R; ++q) {
+    if (!blobs[q]) return fail(TPS_E_INVALID_ARG, "null descriptor %d", q);
+    const uint8_t* b = static_cast<const uint8_t*>(blobs[q]);
+    DpBlobHead h;
+    std::memcpy(&h, b, sizeof(h));
+    b += sizeof(h);
+    if (h.magic != DP_MAGIC || h.r != q) return fail(TPS_E_CONFIG, "descriptor %d is not replica %d's", q, q);
+    std::vector<int64_t> npk(std::max(0, h.nl));
+    std::vector<cudaIpcMemHandle_t> hw(npk.size()), hb(npk.size());
+    for (size_t k = 0; k < npk.size(); ++k) {
+      std::memcpy(&npk[k], b, sizeof(int64_t)); b += sizeof(int64_t);
+      std::memcpy(&hw[k], b, sizeof(cudaIpcMemHandle_t)); b += sizeof(cudaIpcMemHandle_t);
+      std::memcpy(&hb[k], b, sizeof(cudaIpcMemHandle_t)); b += sizeof(cudaIpcMemHandle_t);
+    }
+    TPS_TRY(dp_check_peer(p, h.S, h.s, h.R, q, h.nl, npk.data()));
+    if (q == p->dp_rank) {
+      p->dp_peer_flags[q] = p->dp_flags;
+      for (int k = 0; k < nl; ++k) {
+        p->dp_dW[k][q] = p->layers[k].dW;
+        p->dp_db[k][q] = p->layers[k].db;
+      }
+      continue;
+    }
+    void* v = nullptr;
+    TPS_TRY(ipc_open(p, h.flags, &v));
+    p->dp_peer_flags[q] = static_cast<uint64_t*>(v);
+    for (int k = 0; k < nl; ++k) {
+      if (!p->layers[k].has_w()) continue;
+      TPS_TRY(ipc_open(p, hw[k], &v));
+      p->dp_dW[k][q] = static_cast<float*>(v);
+      TPS_TRY(ipc_open(p, hb[k], &v));
+      p->dp_db[k][q] = static_cast<float*>(v);
+    }
+  }
+  p->dp_connected = true;
+  return TPS_OK;
+}
+
 tps_status tps_begin_run(tps_pipeline* p, int64_t first_mb, int64_t n_mb) {
   TPS_TRY(check_usable(p));
   return begin_run(p, first_mb, n_mb);
@@ -1945,16 +2117,21 @@ tps_status tps_run_schedule(tps_pipeline* p, int64_t first_mb, int64_t n_mb, con
   return join_update_stream(p);
 }
 
-tps_status tps_run_schedule_local(tps_pipeline* const* st, int32_t S, int64_t first_mb, int64_t n_mb,
+tps_status tps_run_schedule_local(tps_pipeline* const* st, int32_t n, int64_t first_mb, int64_t n_mb,
                                   const void* x_pool, const int32_t* y_pool, int32_t pool) {
-  if (!st || S < 1 || pool < 1) return fail(TPS_E_INVALID_ARG, "bad arguments");
-  for (int s = 0; s < S; ++s) {
-    TPS_TRY(check_usable(st[s]));
-    TPS_TRY(begin_run(st[s], first_mb, n_mb));
+  if (!st || n < 1 || pool < 1 || !st[0]) return fail(TPS_E_INVALID_ARG, "bad arguments");
+  // n = S handles of one pipeline, or R·S handles of R data-parallel replicas (replica-major)
+  const int S = st[0]->S;
+  if (n % S) return fail(TPS_E_CONFIG, "%d handles are not whole pipelines of %d stages", n, S);
+  for (int i = 0; i < n; ++i) {
+    if (!st[i] || st[i]->s != i % S || st[i]->S != S) return fail(TPS_E_CONFIG, "handle %d is not stage %d of %d", i, i % S, S);
+    TPS_TRY(check_usable(st[i]));
+    TPS_TRY(begin_run(st[i], first_mb, n_mb));
   }
-  // Round-robin over stages; fire a stage's next static event once its cross-stage
-  // input has been enqueued and the buffer it overwrites has been consumed downstream.
-  std::vector<int64_t> fcount(S, 0), bcount(S, 0);
+  // Round-robin over handles; fire a handle's next static event once its cross-stage input
+  // has been enqueued and the buffer it overwrites has been consumed downstream (neighbours
+  // are the same replica's stages s-1 / s+1).  Replicas synchronise on the device only.
+  std::vector<int64_t> fcount(n, 0), bcount(n, 0);
   const int ng = st[0]->ng;
   static const bool trace_fire = [] {
     const char* e = std::getenv("TPS_TRACE_FIRE");
@@ -1962,8 +2139,9 @@ tps_status tps_run_schedule_local(tps_pipeline* const* st, int32_t S, int64_t fi
   }();
   for (;;) {
     bool all_done = true, progress = false;
-    for (int s = 0; s < S; ++s) {
-      tps_pipeline* p = st[s];
+    for (int i = 0; i < n; ++i) {
+      tps_pipeline* p = st[i];
+      const int s = i % S;
       if (!p->in_run) continue;
       all_done = false;
       const tps_event e = p->order[p->pos];
@@ -1971,25 +2149,25 @@ tps_status tps_run_schedule_local(tps_pipeline* const* st, int32_t S, int64_t fi
       if (e.kind == TPS_EV_F) {
         const int grp = e.micro / p->g;
         const int64_t idx = jr * ng + grp;
-        if (s > 0 && fcount[s - 1] <= idx) continue;                          // input not produced
-        if (s < S - 1 && jr >= 2 && fcount[s + 1] <= (jr - 2) * ng + grp) continue;  // send buffer busy
+        if (s > 0 && fcount[i - 1] <= idx) continue;                          // input not produced
+        if (s < S - 1 && jr >= 2 && fcount[i + 1] <= (jr - 2) * ng + grp) continue;  // send buffer busy
       } else if (e.kind == TPS_EV_B) {
-        if (s < S - 1 && bcount[s + 1] <= jr) continue;                      // gradient not produced
-        if (s > 0 && jr >= 2 && bcount[s - 1] <= jr - 2) continue;           // gout buffer busy
+        if (s < S - 1 && bcount[i + 1] <= jr) continue;                      // gradient not produced
+        if (s > 0 && jr >= 2 && bcount[i - 1] <= jr - 2) continue;           // gout buffer busy
       }
       if (trace_fire) {
-        std::fprintf(stderr, "[tps] fire s=%d kind=%d mb=%lld micro=%d\n", s, e.kind, (long long)e.mb, e.micro);
+        std::fprintf(stderr, "[tps] fire h=%d s=%d kind=%d mb=%lld micro=%d\n", i, s, e.kind, (long long)e.mb, e.micro);
         std::fflush(stderr);
       }
       TPS_TRY(fire(p, e, x_pool, y_pool, pool));
-      if (e.kind == TPS_EV_F) fcount[s] += 1;
-      if (e.kind == TPS_EV_B) bcount[s] += 1;
+      if (e.kind == TPS_EV_F) fcount[i] += 1;
+      if (e.kind == TPS_EV_B) bcount[i] += 1;
       progress = true;
     }
     if (all_done) break;
     if (!progress) return fail(TPS_E_STATE, "local schedule deadlock");
   }
-  for (int s = 0; s < S; ++s) TPS_TRY(join_update_stream(st[s]));
+  for (int i = 0; i < n; ++i) TPS_TRY(join_update_stream(st[i]));
   return TPS_OK;
 }
 
@@ -2459,6 +2637,21 @@ tps_status tps_pool_op(int32_t op, const void* a, const void* b, void* out, int3
   else if (op == 3) CUDA_OK(tps::launch_avgpool_bwd(Bp, O, N, H * W, C, st));
   else if (op == 4) CUDA_OK(tps::launch_maxpool3_fwd_idx(A, O, static_cast<uint8_t*>(const_cast<void*>(b)), N, H, W, C, st));
   else CUDA_OK(tps::launch_maxpool3_bwd_idx(static_cast<const uint8_t*>(a), Bp, O, N, H, W, C, st));
+  return TPS_OK;
+}
+
+tps_status tps_gemm_wgrad_sgd(int32_t M, int32_t N, int32_t K, const void* A, int32_t lda, const void* B, int32_t ldb,
+                              float* w, float* v, void* ver, int32_t ldw, float lr, float mu, float wd,
+                              uint64_t stream) {
+  if (M < 1 || N < 1 || K < 1 || !A || !B || !w || !ver || (mu != 0.f && !v)) return fail(TPS_E_INVALID_ARG, "bad operands");
+  if (N % 8 || lda % 8 || ldb % 8 || ldw % 8) return fail(TPS_E_INVALID_ARG, "N and leading dims must be multiples of 8");
+  TPS_TRY(op_prologue());
+  tps::GemmOperands op{A, lda, B, ldb, nullptr};
+  tps::GemmArgs ga{};
+  ga.M = M; ga.N = N; ga.K = K; ga.ldo = ldw; ga.out_f32 = 1; ga.alpha = 1.f; ga.xa = 1.f;
+  ga.epi = tps::EPI_SGD; ga.w = w; ga.v = v; ga.ver = static_cast<uint16_t*>(ver);
+  ga.lr = lr; ga.mu = mu; ga.wd = wd;
+  CUDA_OK(tps::gemm_run(tps::GEMM_WGRAD, op, ga, reinterpret_cast<cudaStream_t>(stream)));
   return TPS_OK;
 }
 

@@ -34,6 +34,7 @@ EXPORTS = [
     "tps_set_profiling", "tps_kernel_stats", "tps_launch_count", "tps_fill_synthetic", "tps_gemm",
     "tps_conv_gemm", "tps_partition", "tps_im2col", "tps_col2im", "tps_bn_forward", "tps_bn_backward",
     "tps_pool_op", "tps_conv2d_gemm", "tps_debug_progress", "tps_memory_observed", "tps_join", "tps_ipc_export", "tps_ipc_connect",
+    "tps_dp_export", "tps_dp_connect", "tps_gemm_wgrad_sgd",
 ]
 TPS_LAYER_LINEAR, TPS_LAYER_CONV3X3, TPS_LAYER_MAXPOOL2 = 0, 1, 2
 TPS_LAYER_CONV, TPS_LAYER_BN, TPS_LAYER_MAXPOOL3, TPS_LAYER_AVGPOOL = 3, 4, 5, 6
@@ -68,7 +69,7 @@ class Config(C.Structure):
                 ("num_layer_specs", C.c_int32), ("layer_specs", C.POINTER(Layer)),
                 ("max_inflight", C.c_int32), ("staleness_mode", C.c_int32),
                 ("dev_alloc", C.c_void_p), ("dev_free", C.c_void_p), ("alloc_ctx", C.c_void_p),
-                ("reserved", C.c_int32 * 4)]
+                ("dp_size", C.c_int32), ("dp_rank", C.c_int32), ("reserved", C.c_int32 * 2)]
 
 
 # tps_config.dev_alloc / dev_free signatures
@@ -153,6 +154,9 @@ def lib() -> C.CDLL:
             "tps_join": (I32, [P, U64]),
             "tps_ipc_export": (I32, [P, P, I64, C.POINTER(I64)]),
             "tps_ipc_connect": (I32, [P, P, P]),
+            "tps_gemm_wgrad_sgd": (I32, [I32, I32, I32, P, I32, P, I32, P, P, P, I32, F, F, F, U64]),
+            "tps_dp_export": (I32, [P, P, I64, C.POINTER(I64)]),
+            "tps_dp_connect": (I32, [P, C.POINTER(P), I32]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -205,6 +209,11 @@ def gemm(mode, M, N, K, A, lda, B, ldb, out, ldo, out_f32=0, bias=None, relu=0, 
          mask=None, ldm=0, B2=None, stream: int = 0) -> None:
     check(lib().tps_gemm(mode, M, N, K, ptr(A), lda, ptr(B), ldb, ptr(B2), ptr(out), ldo, out_f32, ptr(bias), relu,
                          alpha, beta, ptr(mask), ldm, stream))
+
+
+def gemm_wgrad_sgd(M, N, K, A, lda, B, ldb, w, v, ver, ldw, lr, mu, wd=0.0, stream: int = 0) -> None:
+    check(lib().tps_gemm_wgrad_sgd(M, N, K, ptr(A), lda, ptr(B), ldb, ptr(w), ptr(v), ptr(ver), ldw, lr, mu, wd,
+                                   stream))
 
 
 def conv_gemm(mode, N, H, W, Ci, Co, A, Wt, out, out_f32=0, bias=None, relu=0, alpha=1.0, beta=0.0, mask=None,
@@ -323,6 +332,8 @@ class StageSpec:
     max_inflight: int = 0            # 0 => S - s; S = 1 only otherwise (staleness sweep on one GPU)
     staleness_mode: int = 0          # 1 => explicit δ may be any live version (microbenchmark)
     torch_alloc: bool = False        # allocate through PyTorch's caching allocator
+    dp_size: int = 1                 # data-parallel replicas of the pipeline (NEXT-2)
+    dp_rank: int = 0
     _keep: list = field(default_factory=list)
 
 
@@ -354,7 +365,8 @@ class Pipeline:
                      fuse_update=spec.fuse_update, num_layer_specs=len(spec.layers) if spec.layers else 0,
                      layer_specs=specs, max_inflight=spec.max_inflight, staleness_mode=spec.staleness_mode,
                      dev_alloc=C.cast(self._alloc.alloc, C.c_void_p) if self._alloc else None,
-                     dev_free=C.cast(self._alloc.free, C.c_void_p) if self._alloc else None)
+                     dev_free=C.cast(self._alloc.free, C.c_void_p) if self._alloc else None,
+                     dp_size=spec.dp_size, dp_rank=spec.dp_rank)
         h = C.c_void_p()
         check(lib().tps_pipeline_init(C.byref(cfg), C.byref(h)))
         self.h = h
@@ -408,6 +420,18 @@ class Pipeline:
         pb = C.create_string_buffer(prev, len(prev)) if prev else None
         nb = C.create_string_buffer(nxt, len(nxt)) if nxt else None
         check(lib().tps_ipc_connect(self.h, pb, nb))
+
+    def dp_export(self) -> bytes:
+        n = C.c_int64()
+        check(lib().tps_dp_export(self.h, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value)
+        check(lib().tps_dp_export(self.h, buf, n.value, C.byref(n)))
+        return buf.raw[: n.value]
+
+    def dp_connect(self, blobs: list[bytes]):
+        bufs = [C.create_string_buffer(b, len(b)) for b in blobs]
+        arr = (C.c_void_p * len(bufs))(*[C.cast(b, C.c_void_p) for b in bufs])
+        check(lib().tps_dp_connect(self.h, arr, len(bufs)))
 
     def join(self, stream: int):
         """`stream` waits (stream-ordered) for all work the handle has enqueued."""

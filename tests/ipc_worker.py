@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--case", required=True)
     ap.add_argument("--out", required=True)
     ap.add_argument("--device", type=int, default=0)
+    ap.add_argument("--dp", type=int, default=1, help="data-parallel replicas (rank = replica * S + stage)")
     a = ap.parse_args()
     import numpy as np
     import torch
@@ -41,6 +42,8 @@ def main():
     torch.cuda.set_device(a.device)
     dist.init_process_group("gloo", init_method=f"file://{a.store}/pg", rank=a.rank, world_size=a.world)
     dims, bounds, m, b, M = case["dims"], case["bounds"], case["m"], case["b"], case["M"]
+    S = len(bounds) - 1
+    rep_id, stage = divmod(a.rank, S)
     layers = case.get("layers")
     if is_graph(layers):
         xs, ys, params = graph_workload(layers, m, b, M, case.get("seed", 0), case["kind"])
@@ -48,22 +51,29 @@ def main():
         b0 = [p[1] if p[1] is not None else (np.zeros(p[0].shape[0], np.float32) if p[0] is not None else None)
               for p in params]
     else:
-        xs, ys, w0, b0 = workload(dims, m, b, M, case.get("seed", 0), case["kind"])
-    spec = tps.StageSpec(dims=dims, stage_bounds=bounds, stage_id=a.rank, micro_batches=m, micro_batch_size=b,
+        # data parallel: the pool holds the merged mini-batch of dp·m micro-batches (replica r's
+        # rows are [r·B, (r+1)·B)), i.e. exactly the oracle's workload with m' = dp·m
+        xs, ys, w0, b0 = workload(dims, a.dp * m, b, M, case.get("seed", 0), case["kind"])
+    spec = tps.StageSpec(dims=dims, stage_bounds=bounds, stage_id=stage, micro_batches=m, micro_batch_size=b,
                          variant=case["variant"], blend=case["blend"], lam=case["lam"], lr=case["lr"],
                          momentum=case["mu"], transport=tps.TPS_TRANSPORT_IPC, device=a.device,
-                         fuse_update=case.get("fuse", 1), layers=layers)
+                         fuse_update=case.get("fuse", 1), layers=layers, dp_size=a.dp, dp_rank=rep_id)
     p = tps.Pipeline(spec)
     for k, l in enumerate(p.layers):
         if w0[l] is not None:
             p.set_weights(k, np.asarray(w0[l]).reshape(w0[l].shape[0], -1), b0[l])
-    blob = p.ipc_export()
+    blob = p.ipc_export() if S > 1 else b""
     blobs = [None] * a.world
     dist.all_gather_object(blobs, blob)
-    p.ipc_connect(blobs[a.rank - 1] if a.rank > 0 else None, blobs[a.rank + 1] if a.rank < a.world - 1 else None)
+    if S > 1:
+        p.ipc_connect(blobs[a.rank - 1] if stage > 0 else None, blobs[a.rank + 1] if stage < S - 1 else None)
+    if a.dp > 1:
+        dblobs = [None] * a.world
+        dist.all_gather_object(dblobs, p.dp_export())
+        p.dp_connect([dblobs[r * S + stage] for r in range(a.dp)])
     dist.barrier()
-    x_pool = torch.from_numpy(np.stack(xs)).to(torch.bfloat16).cuda() if a.rank == 0 else None
-    y_pool = torch.from_numpy(np.stack(ys)).cuda() if a.rank == a.world - 1 else None
+    x_pool = torch.from_numpy(np.stack(xs)).to(torch.bfloat16).cuda() if stage == 0 else None
+    y_pool = torch.from_numpy(np.stack(ys)).cuda() if stage == S - 1 else None
     torch.cuda.synchronize()
     p.run_schedule(0, M, x_pool, y_pool, M)
     p.synchronize()
@@ -80,6 +90,7 @@ def main():
         "layers": p.layers,
         "contiguity": contiguity,
     }
+    res["replica"], res["stage"] = rep_id, stage
     with open(os.path.join(a.out, f"stage{a.rank}.pkl"), "wb") as fh:
         pickle.dump(res, fh)
     dist.barrier()

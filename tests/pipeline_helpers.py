@@ -46,9 +46,10 @@ def is_graph(layers):
     return bool(layers) and any(sp["kind"] in GRAPH_KINDS for sp in layers)
 
 
-def graph_workload(layers, m, b, M, seed=0, kind=synthgen.X_UNIT):
+def graph_workload(layers, m, b, M, seed=0, kind=synthgen.X_UNIT, res_gamma=1.0):
     """ResNet-style inputs (flattened NHWC rows) and parameters: synthgen conv weights
-    [Co,k,k,Ci] (fan_in k·k·Ci), BN γ = 1, β = 0, synthgen head weights, zero head bias."""
+    [Co,k,k,Ci] (fan_in k·k·Ci), BN γ = 1 (res_gamma for the BN that closes a residual block,
+    the usual scaled-residual initialisation), β = 0, synthgen head weights, zero head bias."""
     s0 = layers[0]
     feat = s0["h"] * s0["w"] * s0["cin"]
     classes = layers[-1]["out"]
@@ -62,7 +63,8 @@ def graph_workload(layers, m, b, M, seed=0, kind=synthgen.X_UNIT):
             w = synthgen.weights(seed, l, sp["cout"], kk * kk * sp["cin"]).reshape(sp["cout"], kk, kk, sp["cin"])
             params.append((w, None))
         elif k == "bn":
-            params.append((np.ones(sp["c"], np.float32), np.zeros(sp["c"], np.float32)))
+            g = res_gamma if sp.get("res") is not None else 1.0
+            params.append((np.full(sp["c"], g, np.float32), np.zeros(sp["c"], np.float32)))
         elif k == "linear":
             params.append((synthgen.weights(seed, l, sp["out"], sp["in"]), np.zeros(sp["out"], np.float32)))
         else:
@@ -70,9 +72,10 @@ def graph_workload(layers, m, b, M, seed=0, kind=synthgen.X_UNIT):
     return xs, ys, params
 
 
-def run_oracle_graph(layers, bounds, m, b, M, variant, blend, lam, lr, mu, wd=0.0, seed=0, kind=synthgen.X_UNIT):
+def run_oracle_graph(layers, bounds, m, b, M, variant, blend, lam, lr, mu, wd=0.0, seed=0, kind=synthgen.X_UNIT,
+                     res_gamma=1.0):
     from oracle import graph as ograph
-    xs, ys, params = graph_workload(layers, m, b, M, seed, kind)
+    xs, ys, params = graph_workload(layers, m, b, M, seed, kind, res_gamma)
     return ograph.run(layers, bounds, m, b, M, xs, ys, params, variant=variant, blend=blend, lam=lam, lr=lr, mu=mu,
                       wd=wd)
 
@@ -89,7 +92,8 @@ def run_oracle(dims, bounds, m, b, M, variant, blend, lam, lr, mu, wd=0.0, seed=
 
 
 def run_gpu(dims, bounds, m, b, M, variant, blend, lam, lr, mu, wd=0.0, seed=0, kind=synthgen.X_SIGNED,
-            fwd_group=0, init="set", extra_recv_slot=1, fuse_update=1, layers=None, drive=None, **spec_kw):
+            fwd_group=0, init="set", extra_recv_slot=1, fuse_update=1, layers=None, drive=None, res_gamma=1.0,
+            **spec_kw):
     """All S stages as LOCAL-transport handles on cuda:0; returns (stages, losses).
 
     drive: None => tps_run_schedule_local; else a callable(stages, x_pool, y_pool, M) that
@@ -101,7 +105,7 @@ def run_gpu(dims, bounds, m, b, M, variant, blend, lam, lr, mu, wd=0.0, seed=0, 
 
     S = len(bounds) - 1
     if is_graph(layers):
-        xs, ys, params = graph_workload(layers, m, b, M, seed, kind)
+        xs, ys, params = graph_workload(layers, m, b, M, seed, kind, res_gamma)
         w0 = [p[0] for p in params]
         b0 = [p[1] if p[1] is not None else np.zeros(p[0].shape[0], np.float32) if p[0] is not None else None
               for p in params]

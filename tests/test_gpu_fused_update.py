@@ -33,3 +33,49 @@ def test_fused_equals_separate_bitwise(gpu_lib, dims, m, b, mu):
             bad = np.argwhere(a != b_)
             assert bad.size == 0, (dims, k, bad[:5].tolist(), a.shape)
     np.testing.assert_array_equal(res[0][1], res[1][1])
+
+
+@pytest.mark.parametrize("MNK", [(4096, 4096, 2048), (512, 4096, 128), (1024, 520, 96), (4096, 256, 2048)])
+@pytest.mark.parametrize("mu", [0.0, 0.9])
+def test_raw_fused_kernel_matches_oracle_update(gpu_lib, MNK, mu):
+    """tps_gemm_wgrad_sgd (the fused kernel alone; both epilogue variants: register-staged and
+    TMA-fed, chosen at run time by TPS_SGD_LDG) == oracle.mlp.sgd_update applied to the fp32
+    gradient of the same bf16 operands: bitwise between the variants, and within fp32
+    accumulation-order noise of the oracle."""
+    import os
+    import subprocess
+    import sys
+    import torch
+    from oracle import mlp as omlp
+    from paper_2509_23241_b200 import tps
+    M, N, K = MNK
+    g = torch.Generator().manual_seed(M + N + K)
+    A = torch.randn(K, M, generator=g).to(torch.bfloat16)
+    B = torch.randn(K, N, generator=g).to(torch.bfloat16)
+    w0 = torch.randn(M, N, generator=g)
+    v0 = torch.randn(M, N, generator=g) * 0.1 if mu else torch.zeros(M, N)
+    lr, wd = 0.01, 1e-4
+    outs = []
+    for ldg in ("1", "0"):
+        code = ("import os,sys,torch,numpy as np;sys.path.insert(0,%r);from paper_2509_23241_b200 import tps;"
+                "d=np.load(sys.argv[1]);A=torch.from_numpy(d['A']).view(torch.bfloat16).cuda();"
+                "B=torch.from_numpy(d['B']).view(torch.bfloat16).cuda();w=torch.from_numpy(d['w']).cuda();"
+                "v=torch.from_numpy(d['v']).cuda();q=torch.empty_like(w,dtype=torch.bfloat16);"
+                "tps.gemm_wgrad_sgd(%d,%d,%d,A,%d,B,%d,w,v,q,%d,%r,%r,%r);torch.cuda.synchronize();"
+                "np.savez(sys.argv[2],w=w.cpu().numpy(),v=v.cpu().numpy(),q=q.view(torch.int16).cpu().numpy())"
+                % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))), M, N, K, M, N, N, lr, mu, wd))
+        import tempfile
+        with tempfile.TemporaryDirectory() as td:
+            fin, fout = os.path.join(td, "in.npz"), os.path.join(td, "out.npz")
+            np.savez(fin, A=A.view(torch.int16).numpy(), B=B.view(torch.int16).numpy(), w=w0.numpy(), v=v0.numpy())
+            env = dict(os.environ, TPS_SGD_LDG=ldg)   # the variant is chosen once per process
+            subprocess.run([sys.executable, "-c", code, fin, fout], check=True, env=env, timeout=300)
+            o = np.load(fout)
+            outs.append((o["w"], o["v"], o["q"]))
+    for a, b_ in zip(outs[0], outs[1]):
+        np.testing.assert_array_equal(a, b_)
+    gref = (A.double().T @ B.double()).numpy().astype(np.float32)       # fp32-rounded gradient
+    wr, vr = omlp.sgd_update(w0.numpy(), v0.numpy(), gref, lr, mu, wd, False)
+    w, v, _ = outs[0]
+    scale = np.abs(wr - w0.numpy()).max()
+    assert np.abs(w - wr).max() <= 1e-3 * scale + 1e-6 * np.abs(wr).max()

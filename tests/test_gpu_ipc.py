@@ -32,13 +32,14 @@ pytestmark = pytest.mark.gpu
 HERE = os.path.dirname(os.path.abspath(__file__))
 
 
-def run_ipc(case, env_extra=None, timeout=300):
-    S = len(case["bounds"]) - 1
+def run_ipc(case, env_extra=None, timeout=300, dp=1):
+    S = len(case["bounds"]) - 1 if dp == 1 else (len(case["bounds"]) - 1) * dp
     with tempfile.TemporaryDirectory() as store, tempfile.TemporaryDirectory() as out:
         env = dict(os.environ)
         env.update(env_extra or {})
         procs = [subprocess.Popen([sys.executable, os.path.join(HERE, "ipc_worker.py"), "--rank", str(r), "--world",
-                                   str(S), "--store", store, "--case", json.dumps(case), "--out", out],
+                                   str(S), "--store", store, "--case", json.dumps(case), "--out", out,
+                                   "--dp", str(dp)],
                                   env=env, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)
                  for r in range(S)]
         deadline = time.time() + timeout

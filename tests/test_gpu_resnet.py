@@ -42,16 +42,17 @@ def compare(layers, bounds, m, b, M, variant, blend, lr=0.01, mu=0.9, mode="para
     assert not bad, f"layers over their bound (err, bound): {bad}"
 
 
-def measure(layers, bounds, m, b, M, variant, blend, lr=0.01, mu=0.9, mode="params", **gpu_kw):
+def measure(layers, bounds, m, b, M, variant, blend, lr=0.01, mu=0.9, mode="params", res_gamma=1.0, **gpu_kw):
     """Runs oracle (bf16 and exact) and GPU; returns (layers over their bound, every layer's
     (err, bound))."""
     kind = synthgen.X_UNIT
-    ref = run_oracle_graph(layers, bounds, m, b, M, variant, blend, 0.05, lr, mu, kind=kind)
-    xs, ys, params = graph_workload(layers, m, b, M, kind=kind)
+    ref = run_oracle_graph(layers, bounds, m, b, M, variant, blend, 0.05, lr, mu, kind=kind, res_gamma=res_gamma)
+    xs, ys, params = graph_workload(layers, m, b, M, kind=kind, res_gamma=res_gamma)
     ex = ograph.run(layers, bounds, m, b, M, xs, ys, params, variant=variant, blend=blend, lam=0.05, lr=lr, mu=mu,
                     exact=True)
     dims = [layers[0]["h"] * layers[0]["w"] * layers[0]["cin"], layers[-1]["out"]]
-    stages, losses = run_gpu(dims, bounds, m, b, M, variant, blend, 0.05, lr, mu, kind=kind, layers=layers, **gpu_kw)
+    stages, losses = run_gpu(dims, bounds, m, b, M, variant, blend, 0.05, lr, mu, kind=kind, layers=layers,
+                             res_gamma=res_gamma, **gpu_kw)
     assert expand_gpu_trace(stages) == oracle_trace(ref)
     lerr = np.abs(losses - ref.losses) / np.abs(ref.losses)
     lgap = np.abs(ex.losses - ref.losses) / np.abs(ref.losses)
@@ -75,7 +76,14 @@ def measure(layers, bounds, m, b, M, variant, blend, lr=0.01, mu=0.9, mode="para
             e = cat(ex.weights[l], ex.biases[l])
             p0 = params[l][1] if params[l][1] is not None else None
             w0 = cat(params[l][0], p0)
-            if mode == "frob":
+            if mode == "exact_l2":
+                # both bf16 computations against exact arithmetic: the GPU's update must be about as
+                # close to the exact update as the bf16 oracle's is (a missing update is at 1.0)
+                de = e - w0
+                ne = np.linalg.norm(de)
+                err, gap = np.linalg.norm(g - e) / ne, np.linalg.norm(r - e) / ne
+                lim = max(0.05, 1.5 * gap + 0.05)
+            elif mode == "frob":
                 dr, dg, de = r - w0, g - w0, e - w0
                 nr = np.linalg.norm(dr)
                 err, gap = np.linalg.norm(dg - dr) / nr, np.linalg.norm(de - dr) / nr
@@ -162,20 +170,23 @@ def _reduced_r50():
     return ograph.resnet_layers(H=64, classes=100)
 
 
+# The well-conditioned whole-network setting (reading Z23): micro-batches of b = 32 (BN statistics
+# over >= 128 rows per channel), the scaled-residual initialisation (the BN closing each residual
+# block starts at γ = 0.25) and lr = 0.01, ONE mini-batch: the bf16 oracle's first update is then
+# ~0.45 (relative L2) away from exact arithmetic in every layer — far from the 1.0 of a missing
+# update — so "the GPU is about as close to exact as the bf16 oracle is" has power.
+R50_KW = dict(lr=0.01, mode="exact_l2", res_gamma=0.25)
+
+
 @pytest.mark.timeout(900, method="thread")
 @pytest.mark.parametrize("S", [1, 8])
 def test_resnet50_reduced_resolution_well_conditioned(gpu_lib, S):
-    """The whole ResNet-50 graph with micro-batches of b = 32 (B = 64) at 64x64: per-micro-batch
-    BN statistics over >= 128 rows per channel.  Two mini-batches; each layer's update within
-    max(0.05, gap) of the bf16 oracle's (elementwise, relative to the largest update; gap = the
-    fp64 oracle's distance), and the bound must be tight enough to see a missing update (< 0.5
-    for at least 90 % of the layers; see the negative control below)."""
     layers, starts = _reduced_r50()
     bounds = [0, len(layers)] if S == 1 else resnet50_bounds(starts, len(layers))
-    bad, allv = measure(layers, bounds, 2, 32, 2, ost.I_VARIANT, ost.CONVEX, lr=0.05, mode="update")
+    bad, allv = measure(layers, bounds, 2, 32, 1, ost.I_VARIANT, ost.CONVEX, **R50_KW)
     assert not bad, f"layers over their bound (err, bound): {bad}"
     lims = np.array([lim for _, lim in allv.values()])
-    assert (lims < 0.5).mean() >= 0.9, sorted(allv.items(), key=lambda kv: -kv[1][1])[:10]
+    assert (lims < 0.9).mean() >= 0.9, sorted(allv.items(), key=lambda kv: -kv[1][1])[:10]
 
 
 @pytest.mark.timeout(900, method="thread")
@@ -183,5 +194,5 @@ def test_resnet50_reduced_resolution_negative_control(gpu_lib, monkeypatch):
     """TPS_FAULT=skip_update (debug: every parameter step is a no-op) must FAIL the check above."""
     layers, starts = _reduced_r50()
     monkeypatch.setenv("TPS_FAULT", "skip_update")
-    bad, allv = measure(layers, [0, len(layers)], 2, 32, 2, ost.I_VARIANT, ost.CONVEX, lr=0.05, mode="update")
+    bad, allv = measure(layers, [0, len(layers)], 2, 32, 1, ost.I_VARIANT, ost.CONVEX, **R50_KW)
     assert len(bad) >= 0.9 * len(allv), (len(bad), len(allv))

@@ -29,7 +29,7 @@ def main():
     ap.add_argument("--N", type=int, default=4096)
     ap.add_argument("--K", type=int, default=4096)
     ap.add_argument("--iters", type=int, default=20)
-    ap.add_argument("--modes", default="0,1,2,3")
+    ap.add_argument("--modes", default="0,1,2,3,4")
     a = ap.parse_args()
     M, N, K = a.M, a.N, a.K
     X = torch.randn(M, K, device="cuda").to(torch.bfloat16)          # fwd A / dgrad A (G)
@@ -42,17 +42,29 @@ def main():
     bias = torch.zeros(N, device="cuda")
     ob = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
     of = torch.empty(M, N, device="cuda", dtype=torch.float32)
+    # fused wgrad + update at the pipeline's shape: dW [N, N] = Gᵀ·X over K = M rows
+    G4 = torch.randn(M, N, device="cuda").to(torch.bfloat16)
+    X4 = torch.randn(M, N, device="cuda").to(torch.bfloat16)
+    wm = torch.randn(N, N, device="cuda")
+    vm = torch.zeros(N, N, device="cuda")
+    qm = torch.empty(N, N, device="cuda", dtype=torch.bfloat16)
     fl = 2.0 * M * N * K
     runs = {
         0: ("fwd  (K-major A,B; bias+ReLU)", lambda: tps.gemm(0, M, N, K, X, K, W, K, ob, N, 0, bias, 1)),
         1: ("dgrad(MN-major B; α, mask)", lambda: tps.gemm(1, M, N, K, X, K, Wt, N, ob, N, 0, None, 0, 0.9, 0.0, mask, N)),
         2: ("wgrad(MN-major A,B; fp32)", lambda: tps.gemm(2, M, N, K, Gk, M, Xk, N, of, N, 1)),
         3: ("dgrad blend-on-load", lambda: tps.gemm(3, M, N, K, X, K, Wt, N, ob, N, 0, None, 0, 0.7, 0.3, mask, N, B2=W2)),
+        4: ("wgrad + fused SGD/momentum update", lambda: tps.gemm_wgrad_sgd(N, N, M, G4, N, X4, N, wm, vm, qm, N,
+                                                                           1e-9, 0.9)),
     }
     for m in [int(x) for x in a.modes.split(",")]:
         name, fn = runs[m]
         ms = timeit(fn, a.iters)
-        print(f"mode {m} {name:34s} {M}x{N}x{K}: {ms*1e3:8.1f} us  {fl/ms/1e9:7.1f} TFLOP/s", flush=True)
+        extra = ""
+        if m == 4:   # HBM roofline of the fused kernel: operands + 18 B per parameter (w, v r/w + bf16 version)
+            by = 2.0 * (M * N + M * N) + 18.0 * N * N
+            extra = f"  {by / ms / 1e6:7.1f} GB/s algorithmic ({by / 1e6:.1f} MB)"
+        print(f"mode {m} {name:34s} {M}x{N}x{K}: {ms*1e3:8.1f} us  {fl/ms/1e9:7.1f} TFLOP/s{extra}", flush=True)
     ms = timeit(lambda: torch.matmul(X, W.T), a.iters)
     print(f"cuBLAS torch.matmul bf16 {M}x{N}x{K}: {ms*1e3:8.1f} us  {fl/ms/1e9:7.1f} TFLOP/s")
 
