@@ -58,6 +58,9 @@ def parse():
                     help="enqueue on a high-priority compute stream (the weight-gradient / optimizer streams "
                          "stay at the default priority)")
     ap.add_argument("--no-torch-alloc", action="store_true", help="cudaMalloc instead of the torch allocator hook")
+    ap.add_argument("--graph", type=int, default=1,
+                    help="N = 1: capture one epoch as a CUDA graph (tps_graph_capture) and replay it for every "
+                         "step (0 = walk the static order from the host every step)")
     ap.add_argument("--no-method", action="store_true", help="skip the C2 method leg (4 stages, V / I-EQ1 / "
                     "I-CONVEX, staleness sweep, measured memory)")
     return ap.parse_args()
@@ -183,7 +186,9 @@ def config_dict(args):
             "stages": S, "micro_batch": MICRO_B, "micro_batches": MICRO_M, "global_batch": MICRO_B * MICRO_M,
             "variant": "I-TiMePReSt EQ1", "lambda": LAM, "optimizer": f"SGD lr={LR} momentum={MU}",
             "step": f"one pipeline epoch = {args.epoch_mb} mini-batches (fill+steady+drain)",
-            "fused_update": bool(args.fuse_update), "parallelism": f"pp{S}", "l2": "inputs+weights per step >> 126 MB L2 (no flush needed)"}
+            "fused_update": bool(args.fuse_update), "parallelism": f"pp{S}",
+            "issue": "CUDA graph of one epoch, replayed per step" if (args.graph and S == 1) else
+                     "host walker (tps_run_schedule) per step", "l2": "inputs+weights per step >> 126 MB L2 (no flush needed)"}
 
 
 # ------------------------------------------------------------------ method leg (C2 on one GPU)
@@ -373,8 +378,21 @@ def main():
         every step (one window each), barrier + synchronize on both sides.  Returns the total
         device ms (max over ranks), the per-window ms (max over ranks), launches, clocks."""
         mb = p.next_mb if hasattr(p, "next_mb") else 0
+        graph = None
+        if args.graph and world == 1 and not profile:
+            # the first warm-up epoch is captured (and run); every later epoch replays the graph
+            graph = tps.Graph([p], mb, args.epoch_mb, xp, yp, POOL, stream)
+            mb += args.epoch_mb
+            warmup = max(0, warmup - 1)
+
+        def step(mb_):
+            if graph is not None:
+                graph.replay()
+            else:
+                p.run_schedule(mb_, args.epoch_mb, xp, yp, POOL)
+
         for _ in range(warmup):
-            p.run_schedule(mb, args.epoch_mb, xp, yp, POOL)
+            step(mb)
             mb += args.epoch_mb
         barrier()
         if profile:
@@ -386,7 +404,7 @@ def main():
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
         ev[0].record()
         for i in range(steps):
-            p.run_schedule(mb, args.epoch_mb, xp, yp, POOL)
+            step(mb)
             mb += args.epoch_mb
             ev[i + 1].record()
         barrier()
@@ -395,6 +413,8 @@ def main():
         ms = max_over_ranks(ev[0].elapsed_time(ev[-1]))
         win = [max_over_ranks(ev[i].elapsed_time(ev[i + 1])) for i in range(steps)]
         launches = sum_over_ranks(p.launch_count() - n0)
+        if graph is not None:
+            graph.close()
         return ms, win, launches, ck
 
     def spread(win_ms, samples):

@@ -283,6 +283,25 @@ tps_status tps_run_schedule_local(tps_pipeline* const* stages, int32_t num_stage
                                   int64_t first_mb, int64_t n_mb,
                                   const void* x_pool, const int32_t* y_pool, int32_t pool);
 tps_status tps_synchronize(tps_pipeline* p);
+
+/* ---- CUDA-graph replay of whole runs (capture the periodic steady
+ * state; P:136's nF1B order is static, so a run's work is identical from run to run) --------
+ * tps_graph_capture walks the run [first_mb, first_mb + n_mb) of the linked handles exactly like
+ * tps_run_schedule_local (same events, trace, host state), records the device work into one
+ * CUDA graph instead of issuing it, and launches the graph once on `stream` (a real stream, not
+ * 0).  tps_graph_replay launches it again for the NEXT n_mb mini-batches and advances the host
+ * state as a walk would; valid because n_mb must be a multiple of the schedule period (lcm of 2,
+ * pool and every handle's input slots, stash slots and version-ring size): every buffer slot,
+ * ring slot and pool slot then repeats from run to run, and the loss slot is a device counter.
+ * Requirements: LOCAL or single-stage handles (TPS_E_UNSUPPORTED otherwise), no per-launch
+ * profiling, the caller leaves the handles and the pools (same contents per slot) alone between
+ * replays (TPS_E_STATE if a handle's version moved).  Errors from the walk are returned as is. */
+typedef struct tps_graph tps_graph;
+tps_status tps_graph_capture(tps_pipeline* const* stages, int32_t num_handles, int64_t first_mb, int64_t n_mb,
+                             const void* x_pool, const int32_t* y_pool, int32_t pool, uint64_t stream,
+                             tps_graph** out);
+tps_status tps_graph_replay(tps_graph* g);
+tps_status tps_graph_destroy(tps_graph* g);
 /* Stream-ordered join: `stream` (a cudaStream_t, 0 = legacy default) waits for everything the
  * handle has enqueued so far on all of its streams (compute, weight-gradient, optimizer,
  * transfers).  Non-blocking; lets a caller time or consume a run on its own stream.        */

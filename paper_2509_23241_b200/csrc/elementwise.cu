@@ -270,7 +270,7 @@ __global__ void __launch_bounds__(256) softmax_xent_kernel(const float* __restri
 }
 
 __global__ void loss_mean_kernel(const float* __restrict__ loss_rows, int rows, float* __restrict__ losses,
-                                 int64_t idx) {
+                                 int64_t* __restrict__ ctr) {
   __shared__ double red[256];
   double s = 0.0;
   for (int r = threadIdx.x; r < rows; r += blockDim.x) s += loss_rows[r];
@@ -280,7 +280,11 @@ __global__ void loss_mean_kernel(const float* __restrict__ loss_rows, int rows, 
     if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
     __syncthreads();
   }
-  if (threadIdx.x == 0) losses[idx] = static_cast<float>(red[0] / rows);
+  if (threadIdx.x == 0) {   // the slot index lives on the device so a replayed CUDA graph appends
+    const int64_t idx = *ctr;
+    losses[idx] = static_cast<float>(red[0] / rows);
+    *ctr = idx + 1;
+  }
 }
 
 // ------------------------------------------------------------------ conversions
@@ -1247,8 +1251,8 @@ cudaError_t launch_softmax_xent(const float* logits, int ldl, const int32_t* lab
   return cudaGetLastError();
 }
 
-cudaError_t launch_loss_mean(const float* loss_rows, int rows, float* losses, int64_t idx, cudaStream_t st) {
-  loss_mean_kernel<<<1, 256, 0, st>>>(loss_rows, rows, losses, idx);
+cudaError_t launch_loss_mean(const float* loss_rows, int rows, float* losses, int64_t* ctr, cudaStream_t st) {
+  loss_mean_kernel<<<1, 256, 0, st>>>(loss_rows, rows, losses, ctr);
   return cudaGetLastError();
 }
 

@@ -64,22 +64,27 @@ constexpr int SGD_NB = TPS_SGD_NB;
 #ifndef TPS_SGD_PF
 #define TPS_SGD_PF 0       // fused update: L2 prefetch distance in chunks (0 = off)
 #endif
-// fused update, experimental variant (TPS_SGD_LDG=1 at run time): w / v streamed global ->
-// registers (row per thread, the next 32-column chunk in flight) instead of TMA -> shared
-// memory.  Measured SLOWER at the C5 shape (141.7 us vs 88.1 us per launch; bench 480k vs 581k
-// samples/s): each warp load touches 32 rows, so the L1/L2 request rate, not DRAM, limits it.
-#ifndef TPS_SGD_LDG
-#define TPS_SGD_LDG 0
-#endif
+// (Register-staged alternatives to the TMA-fed fused-update epilogue were measured and
+// dropped: w / v streamed global -> registers row per thread 142.9 us, or coalesced through a
+// transposed accumulator 163.8 us, vs 88.3 us TMA-fed, at 4096 x 4096 x 2048.)
 // w, v fp32 32x32 boxes (+ the bf16 version box when it is TMA-stored)
-constexpr int SGD_BUF = 32 * 32 * 4 * 2 + (TPS_SGD_STG ? 0 : 32 * 32 * 2);
+// fused update: columns per w / v chunk (32: 128B-swizzled 32x32 fp32 boxes; 16: 64B-swizzled
+// 32x16 boxes, half the bytes per buffer, so twice the buffers fit the same shared memory and
+// more chunks are in flight per warp)
+#ifndef TPS_SGD_CW
+#define TPS_SGD_CW 32
+#endif
+constexpr int SGD_CW = TPS_SGD_CW;
+static_assert(SGD_CW == 32 || (SGD_CW == 16 && TPS_SGD_STG), "16-column chunks need the STG write-back");
+constexpr int SGD_WBYTES = 32 * SGD_CW * 4;                 // one 32-row chunk of w (or v)
+constexpr int SGD_BUF = 2 * SGD_WBYTES + (TPS_SGD_STG ? 0 : 32 * 32 * 2);
 constexpr int XF_WARPS = 8;                                // BLEND operand transform warps
 
 template <int BN, int BLEND, int SGD = 0, int CG = 1>
 struct Cfg {
   static constexpr int NEPI = SGD ? SGD_WARPS : EPI_WARPS;            // epilogue warps
   // fused-update buffers (SGD = 1: TMA-fed shared-memory chunks; SGD = 2: register-staged, none)
-  static constexpr int EPI = SGD == 1 ? SGD_WARPS * SGD_NB * SGD_BUF : 0;
+  static constexpr int EPI = SGD ? SGD_WARPS * SGD_NB * SGD_BUF : 0;  // fused-update buffers
   static constexpr int B_BYTES = (BN / CG) * BK * 2;   // this CTA's share of the B tile
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES * (BLEND ? 2 : 1);
   static constexpr int STAGES_RAW = (SMEM_BUDGET - 2048 - EPI) / STAGE_BYTES;
@@ -382,113 +387,7 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
         else ptx::umma_commit(&tmem_full[acc]);
       }
     }
-  } else if (SGD == 2 && warp < 2 + SGD_WARPS) {
-    // ===================== fused SGD/momentum update epilogue, register-staged (row a10) ========
-    // Warp q owns TMEM lane quarter q = 32 rows; thread = row.  For each 32-column chunk the
-    // thread's w / v row segments (2 x 128 B) are loaded straight into registers one chunk
-    // ahead (512 B in flight per thread, 64 KiB per CTA, no shared memory), updated in place
-    // against the accumulator row from TMEM (g' = g + wd·w; v = μ·v + g'; w = w - lr·v, one
-    // rounding per op), and stored back with bf16(w) as the new version.  Per-thread row
-    // segments are whole 32-byte sectors over consecutive instructions, so DRAM moves exactly
-    // the algorithmic bytes (L1/L2 merge the 16-byte halves).
-    const int q = warp & 3;
-    constexpr int NCH = BN / 32;
-    const bool mom = args.mu != 0.0f;
-    const size_t ld = static_cast<size_t>(args.ldo);
-    float wa[32], va[32], wb[32], vb[32];
-    // chunk index i -> (tile, chunk); loads row `lane` of chunk i into (w_, v_)
-    auto load = [&](int i, float (&w_)[32], float (&v_)[32]) {
-      const int ti = i / NCH, c = i - ti * NCH;
-      const int t = cid + ti * ncl;
-      if (t >= num_tiles) return;
-      int mb, nb;
-      tile_coords(t, num_m, num_n, mb, nb);
-      const int grow = mb * BM * CG + static_cast<int>(rank) * BM + q * 32 + lane;
-      const int gcol = nb * BN + c * 32;
-      if (grow >= args.M || gcol >= args.N) return;
-      const int nv = min(8, (args.N - gcol) >> 2);   // float4 groups inside N (N % 8 == 0)
-      const float4* wp = reinterpret_cast<const float4*>(args.w + grow * ld + gcol);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const float4 x = j < nv ? __ldcs(wp + j) : make_float4(0.f, 0.f, 0.f, 0.f);
-        w_[4 * j] = x.x; w_[4 * j + 1] = x.y; w_[4 * j + 2] = x.z; w_[4 * j + 3] = x.w;
-      }
-      if (mom) {
-        const float4* vp = reinterpret_cast<const float4*>(args.v + grow * ld + gcol);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const float4 x = j < nv ? __ldcs(vp + j) : make_float4(0.f, 0.f, 0.f, 0.f);
-          v_[4 * j] = x.x; v_[4 * j + 1] = x.y; v_[4 * j + 2] = x.z; v_[4 * j + 3] = x.w;
-        }
-      }
-    };
-    auto step = [&](int i, int t, int mb, int nb, int c, float (&w_)[32], float (&v_)[32], const uint32_t (&r)[32]) {
-      const int grow = mb * BM * CG + static_cast<int>(rank) * BM + q * 32 + lane;
-      const int gcol = nb * BN + c * 32;
-      if (TPS_DBG_SGD || grow >= args.M || gcol >= args.N) return;
-#pragma unroll
-      for (int k = 0; k < 32; ++k) {
-        const float g = __uint_as_float(r[k]);
-        const float gp = __fadd_rn(g, __fmul_rn(args.wd, w_[k]));
-        float upd = gp;
-        if (mom) {
-          v_[k] = __fadd_rn(__fmul_rn(args.mu, v_[k]), gp);
-          upd = v_[k];
-        }
-        w_[k] = __fsub_rn(w_[k], __fmul_rn(args.lr, upd));
-      }
-      const int nv = min(8, (args.N - gcol) >> 2);
-      float4* wp = reinterpret_cast<float4*>(args.w + grow * ld + gcol);
-#pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if (j < nv) __stcs(wp + j, make_float4(w_[4 * j], w_[4 * j + 1], w_[4 * j + 2], w_[4 * j + 3]));
-      if (mom) {
-        float4* vp = reinterpret_cast<float4*>(args.v + grow * ld + gcol);
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-          if (j < nv) __stcs(vp + j, make_float4(v_[4 * j], v_[4 * j + 1], v_[4 * j + 2], v_[4 * j + 3]));
-      }
-      uint4* qp = reinterpret_cast<uint4*>(args.ver + grow * ld + gcol);
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if (2 * j < nv)
-          qp[j] = make_uint4(pack_bf16(w_[8 * j], w_[8 * j + 1]), pack_bf16(w_[8 * j + 2], w_[8 * j + 3]),
-                             pack_bf16(w_[8 * j + 4], w_[8 * j + 5]), pack_bf16(w_[8 * j + 6], w_[8 * j + 7]));
-      (void)i; (void)t;
-    };
-    if (!TPS_DBG_SGD) load(0, wa, va);
-    int i = 0, it = 0;
-    for (int t = cid; t < num_tiles; t += ncl, ++it) {
-      int mb, nb;
-      tile_coords(t, num_m, num_n, mb, nb);
-      const int acc = it % C::ACC;
-      const uint32_t acc_phase = (it / C::ACC) & 1;
-      MBAR_WAIT(5, &tmem_full[acc], acc_phase);
-      ptx::tc_fence_after();
-#pragma unroll 1
-      for (int c = 0; c < NCH; c += 2, i += 2) {
-        // two chunks per iteration so the register double buffer needs no copies:
-        // chunk i uses (wa, va) while i+1 loads into (wb, vb), then the roles swap
-        uint32_t r[32];
-        if (!TPS_DBG_SGD) load(i + 1, wb, vb);
-        ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c * 32, r);
-        ptx::tmem_ld_wait();
-        step(i, t, mb, nb, c, wa, va, r);
-        if (!TPS_DBG_SGD) load(i + 2, wa, va);
-        ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + (c + 1) * 32, r);
-        ptx::tmem_ld_wait();
-        if (c + 2 == NCH) {               // last TMEM read of this warp for this tile
-          ptx::tc_fence_before();
-          __syncwarp();
-          if (lane == 0) {
-            if (CG == 2) ptx::mbar_arrive_remote(ptx::mapa(ptx::smem_u32(&tmem_empty[acc]), 0));
-            else ptx::mbar_arrive(&tmem_empty[acc]);
-          }
-        }
-        step(i + 1, t, mb, nb, c + 1, wb, vb, r);
-      }
-    }
-  } else if (SGD == 1 && warp < 2 + SGD_WARPS) {
+  } else if (SGD && warp < 2 + SGD_WARPS) {
     // ===================== fused SGD/momentum update epilogue (row a10) =====================
     // Each warp owns TMEM lane quarter q (32 rows of the CTA's 128) and walks the tile's 32-column
     // chunks.  w and v of a chunk arrive by TMA (128B-swizzled 32x32 fp32 boxes) SGD_NB-1 chunks
@@ -499,9 +398,12 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
     const int q = warp & 3;
     uint8_t* ebase = epi_smem + e * (SGD_NB * SGD_BUF);
     uint64_t* ebar = sgd_bar + e * SGD_NB;
-    constexpr int NCH = BN / 32;
+    constexpr int CW = SGD_CW, ROWB = CW * 4, NCH = BN / CW;
     const bool mom = args.mu != 0.0f;
     const uint64_t pol_stream = TPS_SGD_L2HINT ? ptx::policy_evict_first() : 0ull;
+    // 16-byte chunk `ch` of row `row` in the swizzled box (128B swizzle for 128-byte rows, 64B
+    // swizzle for 64-byte rows)
+    auto swz = [](int row, int ch) { return CW == 32 ? (ch ^ (row & 7)) : (ch ^ ((row >> 1) & 3)); };
     auto issue = [&](int i) {            // lane 0: TMA loads of chunk i into buffer i % SGD_NB
       const int ti = i / NCH, c = i - ti * NCH;
       const int t = cid + ti * ncl;
@@ -509,16 +411,16 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
       int mb, nb;
       tile_coords(t, num_m, num_n, mb, nb);
       const int row0 = mb * BM * CG + static_cast<int>(rank) * BM + q * 32;
-      const int col0 = nb * BN + c * 32;
+      const int col0 = nb * BN + c * CW;
       const int buf = i % SGD_NB;
       uint8_t* w_s = ebase + buf * SGD_BUF;
-      ptx::mbar_expect_tx(&ebar[buf], mom ? 8192u : 4096u);
+      ptx::mbar_expect_tx(&ebar[buf], mom ? 2u * SGD_WBYTES : 1u * SGD_WBYTES);
       if (TPS_SGD_L2HINT) {
         ptx::tma_load_2d_hint(w_s, &tmW, &ebar[buf], col0, row0, pol_stream);
-        if (mom) ptx::tma_load_2d_hint(w_s + 4096, &tmV, &ebar[buf], col0, row0, pol_stream);
+        if (mom) ptx::tma_load_2d_hint(w_s + SGD_WBYTES, &tmV, &ebar[buf], col0, row0, pol_stream);
       } else {
         ptx::tma_load_2d(w_s, &tmW, &ebar[buf], col0, row0);
-        if (mom) ptx::tma_load_2d(w_s + 4096, &tmV, &ebar[buf], col0, row0);
+        if (mom) ptx::tma_load_2d(w_s + SGD_WBYTES, &tmV, &ebar[buf], col0, row0);
       }
     };
     // L2 prefetch of chunk i (TPS_SGD_PF chunks ahead of its shared-memory load), so that load
@@ -530,8 +432,8 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
       int mb, nb;
       tile_coords(t, num_m, num_n, mb, nb);
       const int row0 = mb * BM * CG + static_cast<int>(rank) * BM + q * 32;
-      ptx::tma_prefetch_2d(&tmW, nb * BN + c * 32, row0);
-      if (mom) ptx::tma_prefetch_2d(&tmV, nb * BN + c * 32, row0);
+      ptx::tma_prefetch_2d(&tmW, nb * BN + c * CW, row0);
+      if (mom) ptx::tma_prefetch_2d(&tmV, nb * BN + c * CW, row0);
     };
     if (lane == 0 && !TPS_DBG_SGD) {
       if (TPS_SGD_PF)
@@ -549,8 +451,13 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
       const int row0 = mb * BM * CG + static_cast<int>(rank) * BM + q * 32;
 #pragma unroll 1
       for (int c = 0; c < NCH; ++c, ++i) {
-        uint32_t r[32];
-        ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c * 32, r);
+        uint32_t r[CW];
+        if constexpr (CW == 32)
+          ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c * CW,
+                                  *reinterpret_cast<uint32_t(*)[32]>(r));
+        else
+          ptx::tmem_ld_32x32b_x16(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c * CW,
+                                  *reinterpret_cast<uint32_t(*)[16]>(r));
         ptx::tmem_ld_wait();
         if (c == NCH - 1) {
           ptx::tc_fence_before();
@@ -564,12 +471,12 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
         const int buf = i % SGD_NB;
         MBAR_WAIT(6, &ebar[buf], (i / SGD_NB) & 1);
         uint8_t* w_s = ebase + buf * SGD_BUF;
-        float4* wrow = reinterpret_cast<float4*>(w_s + lane * 128);
-        float4* vrow = reinterpret_cast<float4*>(w_s + 4096 + lane * 128);
-        uint8_t* qrow = w_s + 8192 + lane * 64;
+        float4* wrow = reinterpret_cast<float4*>(w_s + lane * ROWB);
+        float4* vrow = reinterpret_cast<float4*>(w_s + SGD_WBYTES + lane * ROWB);
+        uint8_t* qrow = w_s + 2 * SGD_WBYTES + lane * 64;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const int pos = j ^ (lane & 7);                 // 128B swizzle: 16B chunk j of row `lane`
+        for (int j = 0; j < CW / 4; ++j) {
+          const int pos = swz(lane, j);                   // 16B chunk j of row `lane`
           float4 wv = wrow[pos];
           float4 vv = mom ? vrow[pos] : make_float4(0.f, 0.f, 0.f, 0.f);
           float* wp = &wv.x;
@@ -598,16 +505,17 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
           // 16-byte column chunks so each store instruction writes whole 128-byte row segments;
           // the buffer can be refilled as soon as its contents sit in registers
           __syncwarp();
-          const int col0 = nb * BN + c * 32;
+          const int col0 = nb * BN + c * CW;
           const size_t ld = static_cast<size_t>(args.ldo);
+          constexpr int LPR = CW / 4;                     // lanes per row segment (16 B each)
 #pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            const int rr = 4 * k + (lane >> 3), ch = lane & 7;
-            const int pos = ch ^ (rr & 7);
+          for (int k = 0; k < 32 / (32 / LPR); ++k) {
+            const int rr = (32 / LPR) * k + lane / LPR, ch = lane % LPR;
+            const int pos = swz(rr, ch);
             const int grow = row0 + rr, gcol = col0 + ch * 4;
-            const float4 wv = *reinterpret_cast<const float4*>(w_s + rr * 128 + pos * 16);
+            const float4 wv = *reinterpret_cast<const float4*>(w_s + rr * ROWB + pos * 16);
             float4 vv;
-            if (mom) vv = *reinterpret_cast<const float4*>(w_s + 4096 + rr * 128 + pos * 16);
+            if (mom) vv = *reinterpret_cast<const float4*>(w_s + SGD_WBYTES + rr * ROWB + pos * 16);
             if (grow < args.M && gcol < args.N) {
               __stcs(reinterpret_cast<float4*>(args.w + grow * ld + gcol), wv);
               if (mom) __stcs(reinterpret_cast<float4*>(args.v + grow * ld + gcol), vv);
@@ -627,15 +535,15 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
         ptx::fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-          const int col0 = nb * BN + c * 32;
+          const int col0 = nb * BN + c * CW;
           if (TPS_SGD_L2HINT) {
             ptx::tma_store_2d_hint(&tmW, w_s, col0, row0, pol_stream);
-            if (mom) ptx::tma_store_2d_hint(&tmV, w_s + 4096, col0, row0, pol_stream);
-            ptx::tma_store_2d_hint(&tmQ, w_s + 8192, col0, row0, pol_stream);
+            if (mom) ptx::tma_store_2d_hint(&tmV, w_s + SGD_WBYTES, col0, row0, pol_stream);
+            ptx::tma_store_2d_hint(&tmQ, w_s + 2 * SGD_WBYTES, col0, row0, pol_stream);
           } else {
             ptx::tma_store_2d(&tmW, w_s, col0, row0);
-            if (mom) ptx::tma_store_2d(&tmV, w_s + 4096, col0, row0);
-            ptx::tma_store_2d(&tmQ, w_s + 8192, col0, row0);
+            if (mom) ptx::tma_store_2d(&tmV, w_s + SGD_WBYTES, col0, row0);
+            ptx::tma_store_2d(&tmQ, w_s + 2 * SGD_WBYTES, col0, row0);
           }
           ptx::bulk_commit();
           ptx::bulk_wait_read<0>();       // the buffer may be refilled once the stores read it
@@ -1099,16 +1007,6 @@ cudaError_t dispatch(const Tiling& tl, const CUtensorMap& ta, const CUtensorMap&
 
 }  // namespace
 
-namespace {
-bool sgd_ldg() {   // fused-update epilogue variant: register-staged (default) or TMA-fed
-  static const int v = [] {
-    const char* e = std::getenv("TPS_SGD_LDG");
-    return e ? std::atoi(e) : TPS_SGD_LDG;
-  }();
-  return v != 0;
-}
-}  // namespace
-
 const char* gemm_mode_name(int mode) {
   switch (mode) {
     case GEMM_FWD: return "fwd";
@@ -1200,11 +1098,10 @@ cudaError_t gemm_run(int mode, const GemmOperands& op, const GemmArgs& args_in, 
   EpiMaps em;
   em.w = em.v = em.q = ta;   // unused unless sgd
   if (sgd) {
-    ok &= make_tmap_box(&em.w, args.w, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, args.M, args.N, args.ldo, 32, 32,
-                        CU_TENSOR_MAP_SWIZZLE_128B);
+    const CUtensorMapSwizzle wsw = SGD_CW == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
+    ok &= make_tmap_box(&em.w, args.w, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, args.M, args.N, args.ldo, SGD_CW, 32, wsw);
     if (args.mu != 0.0f)
-      ok &= make_tmap_box(&em.v, args.v, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, args.M, args.N, args.ldo, 32, 32,
-                          CU_TENSOR_MAP_SWIZZLE_128B);
+      ok &= make_tmap_box(&em.v, args.v, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, args.M, args.N, args.ldo, SGD_CW, 32, wsw);
     ok &= make_tmap_box(&em.q, args.ver, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, args.M, args.N, args.ldo, 32, 32,
                         CU_TENSOR_MAP_SWIZZLE_64B);
   }
@@ -1215,9 +1112,7 @@ cudaError_t gemm_run(int mode, const GemmOperands& op, const GemmArgs& args_in, 
     case GEMM_FWD: e = dispatch<0, 0, 0>(tl, ta, tb, tb2, em, args, st); break;
     case GEMM_DGRAD: e = dispatch<0, 1, 0>(tl, ta, tb, tb2, em, args, st); break;
     case GEMM_WGRAD:
-      e = sgd ? (sgd_ldg() ? dispatch<1, 1, 2>(tl, ta, tb, tb2, em, args, st)
-                           : dispatch<1, 1, 1>(tl, ta, tb, tb2, em, args, st))
-              : dispatch<1, 1, 0>(tl, ta, tb, tb2, em, args, st);
+      e = sgd ? dispatch<1, 1, 1>(tl, ta, tb, tb2, em, args, st) : dispatch<1, 1, 0>(tl, ta, tb, tb2, em, args, st);
       break;
     case GEMM_DGRAD_BLEND:
       e = tl.cg == 2 ? launch<256, 0, 1, 1, 0, 2>(ta, tb, tb2, em, args, st)
@@ -1230,8 +1125,7 @@ cudaError_t gemm_run(int mode, const GemmOperands& op, const GemmArgs& args_in, 
                      : launch<128, 0, 1, 1, 0, 1, CONV_DGRAD>(ta, tb, tb2, em, args, st);
       break;
     case GEMM_CONV_WGRAD:
-      e = sgd ? (sgd_ldg() ? dispatch<1, 1, 2, CONV_WGRAD>(tl, ta, tb, tb2, em, args, st)
-                           : dispatch<1, 1, 1, CONV_WGRAD>(tl, ta, tb, tb2, em, args, st))
+      e = sgd ? dispatch<1, 1, 1, CONV_WGRAD>(tl, ta, tb, tb2, em, args, st)
               : dispatch<1, 1, 0, CONV_WGRAD>(tl, ta, tb, tb2, em, args, st);
       break;
   }

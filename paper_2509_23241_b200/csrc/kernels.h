@@ -41,8 +41,9 @@ cudaError_t launch_bias_grad_sgd(const uint16_t* G, int rows, int cols, int ldg,
 cudaError_t launch_softmax_xent(const float* logits, int ldl, const int32_t* labels, int rows, int classes,
                                 int batch, float* loss_rows, uint16_t* G, int ldg, cudaStream_t st);
 
-// losses[idx] = (Σ_{r<rows} loss_rows[r]) / rows   (fixed-order fp64 reduction, one block)
-cudaError_t launch_loss_mean(const float* loss_rows, int rows, float* losses, int64_t idx, cudaStream_t st);
+// losses[*ctr] = (Σ_{r<rows} loss_rows[r]) / rows, then ++*ctr  (fixed-order fp64 reduction, one
+// block; the device-side slot counter lets a replayed CUDA graph append)
+cudaError_t launch_loss_mean(const float* loss_rows, int rows, float* losses, int64_t* ctr, cudaStream_t st);
 
 // fp32 -> bf16 RNE, n elements
 cudaError_t launch_f32_to_bf16(const float* in, uint16_t* out, int64_t n, cudaStream_t st);

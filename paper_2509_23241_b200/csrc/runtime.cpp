@@ -163,6 +163,7 @@ struct tps_pipeline {
   uint16_t* gce = nullptr;                  // dlogits, one [B, ld] slot per in-flight mini-batch
   float* loss_rows = nullptr;
   float* losses = nullptr;
+  int64_t* loss_ctr = nullptr;               // device: next loss slot (== loss_count once drained)
   int64_t loss_cap = 0, loss_count = 0;
   int32_t* labels_dev = nullptr;
   float* scratch = nullptr;        // bias-gradient reduction scratch of the compute stream
@@ -982,7 +983,7 @@ tps_status do_forward(tps_pipeline* p, int64_t j, int a0, int cnt, const void* x
     p->launches += 1;
     if (a0 + cnt == p->m) {
       if (p->loss_count >= p->loss_cap) return fail(TPS_E_STATE, "loss buffer full (%lld mini-batches)", (long long)p->loss_cap);
-      CUDA_OK(tps::launch_loss_mean(p->loss_rows, p->B, p->losses, p->loss_count, p->cs));
+      CUDA_OK(tps::launch_loss_mean(p->loss_rows, p->B, p->losses, p->loss_ctr, p->cs));
       p->loss_count += 1;
       p->launches += 1;
     }
@@ -1539,6 +1540,7 @@ tps_status init_graph(tps_pipeline* p, const tps_config* c, int lb, int le) {
     TPS_TRY(alloc_t(p, &p->labels_dev, p->B, &p->mem_acts));
     p->loss_cap = 1 << 20;
     TPS_TRY(alloc_t(p, &p->losses, p->loss_cap, &p->mem_acts));
+    TPS_TRY(alloc_t(p, &p->loss_ctr, 1, &p->mem_acts));
   }
   TPS_TRY(alloc_t(p, &p->scratch, bias_scr, &p->mem_optim));
   return TPS_OK;
@@ -1736,6 +1738,7 @@ tps_status tps_pipeline_init(const tps_config* c, tps_pipeline** out) {
     if ((st = alloc_t(p, &p->labels_dev, p->B, &p->mem_acts)) != TPS_OK) return cleanup(st);
     p->loss_cap = 1 << 20;
     if ((st = alloc_t(p, &p->losses, p->loss_cap, &p->mem_acts)) != TPS_OK) return cleanup(st);
+    if ((st = alloc_t(p, &p->loss_ctr, 1, &p->mem_acts)) != TPS_OK) return cleanup(st);
   }
   int64_t scr = 0;
   for (auto& L : p->layers)
@@ -2117,8 +2120,178 @@ tps_status tps_run_schedule(tps_pipeline* p, int64_t first_mb, int64_t n_mb, con
   return join_update_stream(p);
 }
 
+namespace {
+tps_status local_walk(tps_pipeline* const* st, int32_t n, int64_t first_mb, int64_t n_mb, const void* x_pool,
+                      const int32_t* y_pool, int32_t pool);
+}  // namespace
+
 tps_status tps_run_schedule_local(tps_pipeline* const* st, int32_t n, int64_t first_mb, int64_t n_mb,
                                   const void* x_pool, const int32_t* y_pool, int32_t pool) {
+  return local_walk(st, n, first_mb, n_mb, x_pool, y_pool, pool);
+}
+
+// ---- CUDA-graph capture / replay of whole runs
+struct tps_graph {
+  std::vector<tps_pipeline*> h;
+  cudaGraphExec_t exec = nullptr;
+  cudaStream_t origin = nullptr;
+  int64_t n = 0, next = 0, replays = 0;
+  cudaEvent_t done = nullptr;                  // recorded after every launch; the handles' streams wait on it
+  std::vector<std::vector<tps_event>> slice;   // per handle: the captured run's trace
+  std::vector<int64_t> launches, latest_after; // per handle: kernels per run, version after last run
+};
+
+namespace {
+int64_t lcm64(int64_t a, int64_t b) {
+  int64_t x = a, y = b;
+  while (y) { const int64_t t = x % y; x = y; y = t; }
+  return a / x * b;
+}
+
+// re-record every persistent event of the handle on `st` (inside a capture: later waits then
+// refer to nodes of the graph, never to work recorded before the capture began)
+tps_status rearm_events(tps_pipeline* p, cudaStream_t st) {
+  auto rec = [&](cudaEvent_t e) -> tps_status {
+    if (e) CUDA_OK(cudaEventRecord(e, st));
+    return TPS_OK;
+  };
+  for (auto* v : {&p->ev_fwd_ready, &p->ev_fwd_sent, &p->ev_act_free, &p->ev_grad_ready, &p->ev_upd_done, &p->ev_dg,
+                  &p->ev_w_done, &p->ev_bias_l})
+    for (cudaEvent_t e : *v) TPS_TRY(rec(e));
+  for (cudaEvent_t e : {p->ev_bias_in, p->ev_bias_done, p->ev_recv, p->ev_gout_ready, p->ev_gin_ready, p->ev_gin_free[0],
+                        p->ev_gin_free[1], p->ev_bwd_sent[0], p->ev_bwd_sent[1]})
+    TPS_TRY(rec(e));
+  return TPS_OK;
+}
+}  // namespace
+
+namespace {
+// launch, then order every stream of every handle after the graph (later walks, readbacks and
+// synchronisations of the handles see its work)
+tps_status graph_launch(tps_graph* g) {
+  CUDA_OK(cudaGraphLaunch(g->exec, g->origin));
+  // events recorded inside the capture cannot be waited on by later (uncaptured) work: re-record
+  // them after the graph so the next walk orders after it
+  for (tps_pipeline* p : g->h) TPS_TRY(rearm_events(p, g->origin));
+  CUDA_OK(cudaEventRecord(g->done, g->origin));
+  for (tps_pipeline* p : g->h)
+    for (cudaStream_t hs : {p->cs, p->s_upd, p->s_w, p->s_fin, p->s_fout, p->s_bin, p->s_bout})
+      if (hs && hs != g->origin) CUDA_OK(cudaStreamWaitEvent(hs, g->done, 0));
+  return TPS_OK;
+}
+}  // namespace
+
+tps_status tps_graph_capture(tps_pipeline* const* st, int32_t n, int64_t first_mb, int64_t n_mb, const void* x_pool,
+                             const int32_t* y_pool, int32_t pool, uint64_t stream, tps_graph** out) {
+  if (!st || n < 1 || !out || stream == 0 || pool < 1) return fail(TPS_E_INVALID_ARG, "bad arguments (stream must not be 0)");
+  *out = nullptr;
+  cudaStream_t origin = reinterpret_cast<cudaStream_t>(stream);
+  int64_t period = lcm64(2, pool);
+  for (int i = 0; i < n; ++i) {
+    tps_pipeline* p = st[i];
+    TPS_TRY(check_usable(p));
+    if (p->transport == TPS_TRANSPORT_IPC || p->transport == TPS_TRANSPORT_NCCL || p->dp > 1)
+      return fail(TPS_E_UNSUPPORTED, "graph capture: LOCAL / single-stage handles only");
+    if (p->profiling) return fail(TPS_E_STATE, "graph capture with per-launch profiling enabled");
+    if (p->in_run) return fail(TPS_E_ORDER, "handle %d is inside a run", i);
+    period = lcm64(period, lcm64(lcm64(p->A0, p->Kmax), p->R));
+  }
+  if (n_mb < period || n_mb % period)
+    return fail(TPS_E_CONFIG, "a replayable run covers a multiple of the schedule period %lld mini-batches", (long long)period);
+  tps_graph* g = new tps_graph();
+  g->h.assign(st, st + n);
+  g->origin = origin;
+  g->n = n_mb;
+  std::vector<size_t> t0(n);
+  std::vector<int64_t> l0(n);
+  std::vector<cudaStream_t> callers(n);
+  for (int i = 0; i < n; ++i) {
+    t0[i] = st[i]->trace.size();
+    l0[i] = st[i]->launches;
+    callers[i] = st[i]->caller;
+    st[i]->caller = origin;
+  }
+  // the capture starts once everything before it has finished (events recorded earlier are
+  // re-armed inside the capture)
+  CUDA_OK(cudaDeviceSynchronize());
+  CUDA_OK(cudaStreamBeginCapture(origin, cudaStreamCaptureModeRelaxed));
+  tps_status ws = TPS_OK;
+  for (int i = 0; i < n && ws == TPS_OK; ++i) ws = rearm_events(st[i], origin);
+  if (ws == TPS_OK) ws = local_walk(st, n, first_mb, n_mb, x_pool, y_pool, pool);
+  for (int i = 0; i < n && ws == TPS_OK; ++i) ws = tps_join(st[i], stream);
+  const std::string werr = g_err;
+  cudaGraph_t graph = nullptr;
+  const cudaError_t ce = cudaStreamEndCapture(origin, &graph);
+  for (int i = 0; i < n; ++i) st[i]->caller = callers[i];
+  if (ws != TPS_OK || ce != cudaSuccess) {
+    if (graph) cudaGraphDestroy(graph);
+    cudaGetLastError();
+    delete g;
+    if (ws != TPS_OK) return fail(ws, "graph capture: %s", werr.c_str());
+    return fail(TPS_E_CUDA, "cudaStreamEndCapture: %s", cudaGetErrorString(ce));
+  }
+  const cudaError_t ie = cudaGraphInstantiate(&g->exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (ie != cudaSuccess) {
+    delete g;
+    return fail(TPS_E_CUDA, "cudaGraphInstantiate: %s", cudaGetErrorString(ie));
+  }
+  for (int i = 0; i < n; ++i) {
+    tps_pipeline* p = st[i];
+    g->slice.emplace_back(p->trace.begin() + static_cast<std::ptrdiff_t>(t0[i]), p->trace.end());
+    g->launches.push_back(p->launches - l0[i]);
+    g->latest_after.push_back(p->latest);
+  }
+  g->next = first_mb + n_mb;
+  g->done = new_event();
+  // the walk advanced the host state; now run the captured work once
+  TPS_TRY(graph_launch(g));
+  *out = g;
+  return TPS_OK;
+}
+
+tps_status tps_graph_replay(tps_graph* g) {
+  if (!g || !g->exec) return fail(TPS_E_INVALID_ARG, "null graph");
+  for (size_t i = 0; i < g->h.size(); ++i) {
+    tps_pipeline* p = g->h[i];
+    TPS_TRY(check_usable(p));
+    if (p->in_run || p->latest != g->latest_after[i])
+      return fail(TPS_E_STATE, "handle %zu changed since the graph's last run (replay continues that run)", i);
+  }
+  TPS_TRY(graph_launch(g));
+  g->replays += 1;
+  const int64_t shift = g->replays * g->n;     // mini-batches and versions both advance by n per run
+  for (size_t i = 0; i < g->h.size(); ++i) {
+    tps_pipeline* p = g->h[i];
+    for (tps_event e : g->slice[i]) {
+      e.mb += shift;
+      e.v_used += shift;
+      e.v_latest += shift;
+      p->trace.push_back(e);
+    }
+    p->latest += g->n;
+    g->latest_after[i] = p->latest;
+    if (p->last) p->loss_count += g->n;
+    p->launches += g->launches[i];
+  }
+  g->next += g->n;
+  return TPS_OK;
+}
+
+tps_status tps_graph_destroy(tps_graph* g) {
+  if (!g) return TPS_OK;
+  if (g->exec) {
+    cudaStreamSynchronize(g->origin);
+    cudaGraphExecDestroy(g->exec);
+  }
+  if (g->done) cudaEventDestroy(g->done);
+  delete g;
+  return TPS_OK;
+}
+
+namespace {
+tps_status local_walk(tps_pipeline* const* st, int32_t n, int64_t first_mb, int64_t n_mb, const void* x_pool,
+                      const int32_t* y_pool, int32_t pool) {
   if (!st || n < 1 || pool < 1 || !st[0]) return fail(TPS_E_INVALID_ARG, "bad arguments");
   // n = S handles of one pipeline, or R·S handles of R data-parallel replicas (replica-major)
   const int S = st[0]->S;
@@ -2170,13 +2343,22 @@ tps_status tps_run_schedule_local(tps_pipeline* const* st, int32_t n, int64_t fi
   for (int i = 0; i < n; ++i) TPS_TRY(join_update_stream(st[i]));
   return TPS_OK;
 }
+}  // namespace
 
 tps_status tps_join(tps_pipeline* p, uint64_t stream) {
   TPS_TRY(check_usable(p));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  // record the tail of every stream of the handle and make `st` wait for it
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  CUDA_OK(cudaStreamIsCapturing(st, &cap));
+  // record the tail of every stream of the handle and make `st` wait for it (while `st` is being
+  // captured, only the streams the capture pulled in: the others hold no work of the graph)
   for (cudaStream_t hs : {p->cs, p->s_upd, p->s_w, p->s_fin, p->s_fout, p->s_bin, p->s_bout}) {
     if (!hs || hs == st) continue;
+    if (cap == cudaStreamCaptureStatusActive) {
+      cudaStreamCaptureStatus hc = cudaStreamCaptureStatusNone;
+      CUDA_OK(cudaStreamIsCapturing(hs, &hc));
+      if (hc != cudaStreamCaptureStatusActive) continue;
+    }
     CUDA_OK(cudaEventRecord(p->ev_caller, hs));
     CUDA_OK(cudaStreamWaitEvent(st, p->ev_caller, 0));
   }

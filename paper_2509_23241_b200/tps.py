@@ -34,7 +34,8 @@ EXPORTS = [
     "tps_set_profiling", "tps_kernel_stats", "tps_launch_count", "tps_fill_synthetic", "tps_gemm",
     "tps_conv_gemm", "tps_partition", "tps_im2col", "tps_col2im", "tps_bn_forward", "tps_bn_backward",
     "tps_pool_op", "tps_conv2d_gemm", "tps_debug_progress", "tps_memory_observed", "tps_join", "tps_ipc_export", "tps_ipc_connect",
-    "tps_dp_export", "tps_dp_connect", "tps_gemm_wgrad_sgd",
+    "tps_dp_export", "tps_dp_connect", "tps_gemm_wgrad_sgd", "tps_graph_capture", "tps_graph_replay",
+    "tps_graph_destroy",
 ]
 TPS_LAYER_LINEAR, TPS_LAYER_CONV3X3, TPS_LAYER_MAXPOOL2 = 0, 1, 2
 TPS_LAYER_CONV, TPS_LAYER_BN, TPS_LAYER_MAXPOOL3, TPS_LAYER_AVGPOOL = 3, 4, 5, 6
@@ -155,6 +156,9 @@ def lib() -> C.CDLL:
             "tps_ipc_export": (I32, [P, P, I64, C.POINTER(I64)]),
             "tps_ipc_connect": (I32, [P, P, P]),
             "tps_gemm_wgrad_sgd": (I32, [I32, I32, I32, P, I32, P, I32, P, P, P, I32, F, F, F, U64]),
+            "tps_graph_capture": (I32, [C.POINTER(P), I32, I64, I64, P, P, I32, U64, C.POINTER(P)]),
+            "tps_graph_replay": (I32, [P]),
+            "tps_graph_destroy": (I32, [P]),
             "tps_dp_export": (I32, [P, P, I64, C.POINTER(I64)]),
             "tps_dp_connect": (I32, [P, C.POINTER(P), I32]),
         }
@@ -514,6 +518,35 @@ class Pipeline:
 def local_link(stages: list[Pipeline]):
     arr = (C.c_void_p * len(stages))(*[s.h.value for s in stages])
     check(lib().tps_local_link(arr, len(stages)))
+
+
+class Graph:
+    """A captured run of linked handles (tps_graph_capture); replay() runs the next n_mb mini-batches."""
+
+    def __init__(self, stages: list[Pipeline], first_mb: int, n_mb: int, x_pool, y_pool, pool: int, stream: int):
+        arr = (C.c_void_p * len(stages))(*[s.h.value for s in stages])
+        g = C.c_void_p()
+        check(lib().tps_graph_capture(arr, len(stages), first_mb, n_mb, ptr(x_pool), ptr(y_pool), pool, stream,
+                                      C.byref(g)))
+        self.g = g
+        self.stages = stages           # keep the handles alive with the graph
+        self.n_mb = n_mb
+        self.next_mb = first_mb + n_mb
+
+    def replay(self):
+        check(lib().tps_graph_replay(self.g))
+        self.next_mb += self.n_mb
+
+    def close(self):
+        if self.g:
+            check(lib().tps_graph_destroy(self.g))
+            self.g = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def run_schedule_local(stages: list[Pipeline], first_mb: int, n_mb: int, x_pool=None, y_pool=None, pool: int = 1):

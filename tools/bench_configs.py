@@ -5,6 +5,7 @@ samples/s is the single-GPU cost of the whole pipeline, not the S-GPU throughput
 Usage: python tools/bench_configs.py [--out profiles/r01_configs.json]
 """
 import argparse
+import math
 import json
 import os
 import sys
@@ -67,8 +68,23 @@ CONFIGS = {
 }
 
 
-def run(name, c, variant, blend, epochs=3, epoch_mb=16, pool=4):
+def schedule_period(S, variant, pool):
+    """Mini-batches after which every slot index of the static order repeats (tps_graph_capture)."""
+    per = math.lcm(2, pool)
+    for s in range(S):
+        K = S - s
+        per = math.lcm(per, K + 1, K, K if variant == tps.TPS_I else 1)
+    return per
+
+
+def run(name, c, variant, blend, epochs=3, epoch_mb=16, pool=4, graph=False):
     S = len(c["bounds"]) - 1
+    if graph:
+        per = schedule_period(S, variant, pool)
+        if per > 64:            # e.g. 8 stages: lcm(9, 8, 7, ...) mini-batches per replayable run
+            graph = False
+        else:
+            epoch_mb = -(-epoch_mb // per) * per
     layers = c.get("layers")
     dims = c.get("dims") or [layers[0]["h"] * layers[0]["w"] * layers[0]["cin"], layers[-1]["out"]]
     B = c["m"] * c["b"]
@@ -91,10 +107,16 @@ def run(name, c, variant, blend, epochs=3, epoch_mb=16, pool=4):
         tps.fill_synthetic(2, 0, 0x20000 + j, B, 1, classes, yp[j])
     torch.cuda.synchronize()
     mb = 0
+    stream = torch.cuda.Stream()
+    g = None
 
     def epoch():
-        nonlocal mb
-        if S > 1:
+        nonlocal mb, g
+        if graph and g is None:
+            g = tps.Graph(stages, mb, epoch_mb, xp, yp, pool, stream.cuda_stream)
+        elif graph:
+            g.replay()
+        elif S > 1:
             tps.run_schedule_local(stages, mb, epoch_mb, xp, yp, pool)
         else:
             stages[0].run_schedule(mb, epoch_mb, xp, yp, pool)
@@ -106,16 +128,19 @@ def run(name, c, variant, blend, epochs=3, epoch_mb=16, pool=4):
     t0 = time.perf_counter()
     for _ in range(epochs):
         epoch()
+    stream.synchronize()
     for st in stages:
         st.synchronize()
     dt = time.perf_counter() - t0
+    if g is not None:
+        g.close()
     sps = epochs * epoch_mb * B / dt
     mem = [st.memory_stats() for st in stages]
     fps = conv_flops_per_sample(layers) if layers else sum(2.0 * dims[l] * dims[l + 1] * (3 if l else 2)
                                                            for l in range(len(dims) - 1))
     for st in stages:
         st.close()
-    return {"samples_per_s": round(sps, 1), "tflops_effective": round(sps * fps / 1e12, 1),
+    return {"samples_per_s": round(sps, 1), "tflops_effective": round(sps * fps / 1e12, 1), "epoch_mb": epoch_mb,
             "stash_bytes_per_stage": [m["stash"] for m in mem], "peak_bytes_per_stage": [m["peak"] for m in mem]}
 
 
@@ -123,6 +148,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=None)
     ap.add_argument("--only", default=None, help="substring filter on config names")
+    ap.add_argument("--graph", action="store_true", help="replay each epoch as a captured CUDA graph")
     a = ap.parse_args()
     res = {}
     for name, c in CONFIGS.items():
@@ -132,7 +158,7 @@ def main():
                           ("I-CONVEX", tps.TPS_I, tps.TPS_BLEND_CONVEX)]:
             if vn == "I-CONVEX" and len(c["bounds"]) == 2:
                 continue
-            r = run(name, c, v, bl)
+            r = run(name, c, v, bl, graph=a.graph)
             res[f"{name} | {vn}"] = r
             print(json.dumps({f"{name} | {vn}": r}), flush=True)
     if a.out:
