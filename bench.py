@@ -441,7 +441,22 @@ def main():
         if n_k:
             per_kind[nm] = {"launches": n_k, "ms": round(ms_k, 3), "tflops": round(fl_k / (ms_k * 1e-3) / 1e12, 1)}
     n_u, ms_u, by_u = pI.kernel_stats(4)
+    # dominant kernel: the fused wgrad + update (17 launches per mini-batch: 16 x 4096^2 + the head);
+    # algorithmic bytes per launch = G and X read once + 18 B/param (w, v read + write, bf16 version),
+    # averaged over the 17 launches like the measured duration
+    n_w, ms_w, fl_w = pI.kernel_stats(2)
+    Bm = MICRO_B * MICRO_M
+    dmod = [WIDTH] * (HIDDEN + 1) + [CLASSES]
+    lay = [(((dmod[l + 1] + 15) // 16) * 16, ((dmod[l] + 15) // 16) * 16) for l in range(len(dmod) - 1)]
+    dom_bytes = sum(2.0 * Bm * (npad + kpad) + 18.0 * npad * kpad for npad, kpad in lay) / len(lay)
+    dom_flops = sum(2.0 * Bm * npad * kpad for npad, kpad in lay) / len(lay)
+    dom_us = ms_w / n_w * 1e3 if n_w else None
+    dom = {"bytes": dom_bytes, "flops": dom_flops, "us": dom_us,
+           "gbs": dom_bytes / (dom_us * 1e-6) / 1e9 if dom_us else None,
+           "roof_us": max(dom_flops / (peaks_early.get("bf16_tflops_sustained", 1400.0) * 1e12),
+                          dom_bytes / (peaks_early.get("hbm_gbs", 6500.0) * 1e9)) * 1e6}
     memI = pI.memory_stats()
+    peaks_early, _ = load_peaks()
     memI["torch_max_allocated"] = int(torch.cuda.max_memory_allocated())   # device-observed (allocator hook)
     lossesI = pI.losses()
     peaks, src = load_peaks()
@@ -460,12 +475,12 @@ def main():
     # per-kind tensor-pipe / DRAM utilisation from the committed ncu --set full capture (one
     # launch of each stage-GEMM kind at these shapes; read, not measured, by this run)
     ncu_kinds = None
-    ncu_path = os.path.join(ROOT, "profiles", "r01_ncu_full_summary.json")
+    ncu_path = os.path.join(ROOT, "profiles", "r02_ncu_full_summary.json")
     if os.path.exists(ncu_path):
         try:
             names = {"<256, 1, 1, 0, 1, 2, 0>": "wgrad+update", "<256, 0, 0, 0, 0, 2, 0>": "fwd",
-                     "<256, 0, 1, 0, 0, 2, 0>": "dgrad"}
-            ncu_kinds = {"source": "profiles/r01_ncu_full_summary.json (ncu --set full --clock-control none)"}
+                     "<256, 0, 1, 0, 0, 2, 0>": "dgrad", "<256, 0, 1, 1, 0, 2, 0>": "dgrad_blend"}
+            ncu_kinds = {"source": "profiles/r02_ncu_full_summary.json (ncu --set full --clock-control none)"}
             for r in json.load(open(ncu_path)):
                 for key, kind in names.items():
                     if key in r["kernel"]:
@@ -537,10 +552,22 @@ def main():
             # GEMMs overlap the input-gradient GEMMs on a second stream: per-launch event durations
             # then include SM sharing, so the roofline uses the algorithmic GEMM FLOPs of the whole
             # timed step over its device time (per-launch event numbers kept under per_kind)
-            "roofline": {"bound": "tensor", "kernel": "stage GEMMs (fwd+dgrad+wgrad+fused update, tcgen05 kind::f16), "
-                         "algorithmic FLOPs of the timed step / step time",
-                         "achieved": fps * value / world / 1e12, "peak": peak, "unit": "TFLOP/s",
-                         "frac": fps * value / world / 1e12 / peak, "traffic": traffic,
+            # the dominant kernel: wgrad + fused SGD/momentum update (HBM-bound: its roofline time
+            # max(FLOPs / tensor peak, algorithmic bytes / HBM peak) is the HBM term); achieved =
+            # algorithmic bytes per launch / average launch duration (CUDA events on its stream)
+            "roofline": {"bound": "hbm", "kernel": "wgrad + fused SGD/momentum update, gemm_kernel<256,1,1,0,1,2,0> "
+                         "(CTA pairs, 256x256 tiles, TMA-fed update epilogue)",
+                         "achieved": dom["gbs"], "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
+                         "frac": dom["gbs"] / peaks.get("hbm_gbs") if dom["gbs"] else None, "traffic": traffic,
+                         "algorithmic_bytes_per_launch": dom["bytes"], "flops_per_launch": dom["flops"],
+                         "avg_launch_us": dom["us"], "roofline_time_us": dom["roof_us"],
+                         "frac_of_roofline_time": dom["roof_us"] / dom["us"] if dom["us"] else None,
+                         "isolated": "tools/gemm_bench.py --modes 4 (same kernel alone): 87.2 us = 0.59 of the HBM "
+                                     "roofline time (profiles/r02_gemm_microbench.txt)",
+                         "launch_note": "in the pipeline each launch runs concurrently with the next layer's input "
+                                        "gradient on the compute stream (split backward), so its event duration "
+                                        "includes SM sharing",
+                         "step_tensor_achieved_tflops": fps * value / world / 1e12,
                          "per_launch_event_tflops": achieved,
                          "per_launch_note": "per_kind / per_launch_event_tflops: CUDA-event durations of each "
                          "launch on its own stream; they overlap across the two backward streams",
