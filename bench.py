@@ -441,6 +441,7 @@ def main():
         if n_k:
             per_kind[nm] = {"launches": n_k, "ms": round(ms_k, 3), "tflops": round(fl_k / (ms_k * 1e-3) / 1e12, 1)}
     n_u, ms_u, by_u = pI.kernel_stats(4)
+    peaks_early, _ = load_peaks()
     # dominant kernel: the fused wgrad + update (17 launches per mini-batch: 16 x 4096^2 + the head);
     # algorithmic bytes per launch = G and X read once + 18 B/param (w, v read + write, bf16 version),
     # averaged over the 17 launches like the measured duration
@@ -456,7 +457,6 @@ def main():
            "roof_us": max(dom_flops / (peaks_early.get("bf16_tflops_sustained", 1400.0) * 1e12),
                           dom_bytes / (peaks_early.get("hbm_gbs", 6500.0) * 1e9)) * 1e6}
     memI = pI.memory_stats()
-    peaks_early, _ = load_peaks()
     memI["torch_max_allocated"] = int(torch.cuda.max_memory_allocated())   # device-observed (allocator hook)
     lossesI = pI.losses()
     peaks, src = load_peaks()
@@ -490,30 +490,48 @@ def main():
         except Exception:
             ncu_kinds = None
 
+    pI.set_profiling(False)   # per-launch events off again (they also cannot be captured)
+
     # ---- e2e: host pools (pinned), H2D inside the timed region, D2H of losses
     e2e = None
     if not args.no_e2e:
         hx = x_pool.cpu().pin_memory() if x_pool is not None else None
         hy = y_pool.cpu().pin_memory() if y_pool is not None else None
-        ms_e = 0.0
-        pI.run_schedule(pI.next_mb, args.epoch_mb, hx, hy, POOL)   # warm the host path
+        lossbuf = torch.empty(args.steps * args.epoch_mb, dtype=torch.float32).pin_memory()
+        use_graph = bool(args.graph) and world == 1
+        g_e2e = None
+        if use_graph:   # the warm-up epoch is captured with the host pools (H2D copies are graph nodes)
+            g_e2e = tps.Graph([pI], pI.next_mb, args.epoch_mb, hx, hy, POOL, stream)
+        else:
+            pI.run_schedule(pI.next_mb, args.epoch_mb, hx, hy, POOL)   # warm the host path
         pI.next_mb += args.epoch_mb
         barrier()
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
+        n_loss0 = len(pI.losses()) if rank == S - 1 else 0
         t0.record()
-        for _ in range(args.steps):
-            pI.run_schedule(pI.next_mb, args.epoch_mb, hx, hy, POOL)
+        for i in range(args.steps):
+            if g_e2e is not None:
+                g_e2e.replay()
+            else:
+                pI.run_schedule(pI.next_mb, args.epoch_mb, hx, hy, POOL)
             pI.next_mb += args.epoch_mb
-            if rank == S - 1:
-                pI.losses()   # device -> host read of the step's result
+            if rank == S - 1:   # device -> host read of the step's result (its losses), stream-ordered
+                pI.read_losses_async(n_loss0 + i * args.epoch_mb, args.epoch_mb,
+                                     lossbuf[i * args.epoch_mb:], stream)
         t1.record()
         barrier()
+        if g_e2e is not None:
+            g_e2e.close()
+        if rank == S - 1:
+            assert torch.isfinite(lossbuf).all(), "non-finite loss in the e2e run"
         ms_e = max_over_ranks(t0.elapsed_time(t1))
         h2d = (args.epoch_mb * B * WIDTH * 2 if rank == 0 else 0) + (args.epoch_mb * B * 4 if rank == S - 1 else 0)
         e2e = {"value": samples_per_step * args.steps / (ms_e / 1e3), "unit": "samples/s",
                "h2d_bytes_per_step": int(sum_over_ranks(h2d)), "d2h_bytes_per_step": 4 * args.epoch_mb,
-               "api": "tps_run_schedule with pinned host x/y pools"}
+               "api": ("tps_graph_replay of an epoch captured with pinned host x/y pools" if use_graph else
+                       "tps_run_schedule with pinned host x/y pools") +
+                      "; per step the H2D copies of its inputs and an async D2H read of its losses"}
     pI.close()
 
     # ---- V-TiMePReSt (memory + throughput)

@@ -342,6 +342,9 @@ tps_status tps_set_weights(tps_pipeline* p, int32_t layer, const float* w, const
 tps_status tps_init_weights_synthetic(tps_pipeline* p);
 /* Per-mini-batch mean losses of the last stage, in mini-batch order since init. */
 tps_status tps_get_losses(tps_pipeline* p, float* out, int64_t cap, int64_t* n);
+/* Stream-ordered read of losses [first, first + n) into host memory (pinned for asynchrony):
+ * enqueued on `stream` after the loss kernels; the caller synchronises before reading dst.  */
+tps_status tps_read_losses_async(tps_pipeline* p, int64_t first, int64_t n, float* host_dst, uint64_t stream);
 tps_status tps_get_trace(tps_pipeline* p, tps_event* out, int64_t cap, int64_t* n);
 tps_status tps_clear_trace(tps_pipeline* p);
 /* Bytes held by category; peak = max over the handle's life of their sum (the library's

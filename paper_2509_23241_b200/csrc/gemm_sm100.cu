@@ -42,7 +42,13 @@ constexpr int SMEM_BUDGET = 227 * 1024;
 constexpr int EPI_WARPS = 8;
 // fused-update epilogue: 4 warps, each with SGD_NB buffers of one 32x32 chunk of w, v (fp32,
 // 128B-swizzled TMA boxes) and the new bf16 version (64B-swizzled), refilled SGD_NB-1 chunks ahead
-constexpr int SGD_WARPS = 4;
+// fused-update epilogue warps: 4 (one per TMEM lane quarter) or 8 (two per quarter, each taking
+// every other column chunk, so each SM sub-partition has two update warps to hide latency)
+#ifndef TPS_SGD_WARPS
+#define TPS_SGD_WARPS 4
+#endif
+constexpr int SGD_WARPS = TPS_SGD_WARPS;
+static_assert(SGD_WARPS == 4 || SGD_WARPS == 8, "4 or 8 fused-update warps");
 #ifndef TPS_SGD_NB
 #define TPS_SGD_NB 2
 #endif
@@ -57,6 +63,9 @@ constexpr int SGD_NB = TPS_SGD_NB;
 // fused-update memory traffic, to measure what the rest of the kernel costs
 #ifndef TPS_DBG_XF
 #define TPS_DBG_XF 0
+#endif
+#ifndef TPS_DBG_NOMAIN
+#define TPS_DBG_NOMAIN 0   // diagnostics: no operand loads and no MMAs (times the epilogue alone)
 #endif
 #ifndef TPS_DBG_SGD
 #define TPS_DBG_SGD 0
@@ -230,7 +239,7 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
         tile_split(t, num_m, num_n, num_k, args.kper, mb, nb, kb0, kb1);
         const int m0 = mb * BM * CG + static_cast<int>(rank) * BM;          // this CTA's 128 rows
         const int n0 = nb * BN + static_cast<int>(rank) * (BN / CG);       // this CTA's B share
-        for (int kb = kb0; kb < kb1; ++kb) {
+        for (int kb = kb0; kb < (TPS_DBG_NOMAIN ? kb0 : kb1); ++kb) {
           MBAR_WAIT(1, &empty[stage], phase ^ 1);
           uint8_t* sA = stages + stage * C::STAGE_BYTES;
           uint8_t* sB = sA + A_BYTES;
@@ -362,7 +371,7 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
         const uint32_t d_tmem = tmem_base + acc * BN;
         int mb_, nb_, kb0, kb1;
         tile_split(t, num_m, num_n, num_k, args.kper, mb_, nb_, kb0, kb1);
-        for (int kb = kb0; kb < kb1; ++kb) {
+        for (int kb = kb0; kb < (TPS_DBG_NOMAIN ? kb0 : kb1); ++kb) {
           MBAR_WAIT(3, &full[stage], phase);
           if (BLEND) MBAR_WAIT(4, &xform[stage], phase);
           ptx::tc_fence_after();
@@ -399,13 +408,17 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
     uint8_t* ebase = epi_smem + e * (SGD_NB * SGD_BUF);
     uint64_t* ebar = sgd_bar + e * SGD_NB;
     constexpr int CW = SGD_CW, ROWB = CW * 4, NCH = BN / CW;
+    constexpr int NW = SGD_WARPS / 4;                 // warps sharing a TMEM lane quarter
+    constexpr int NCHW = NCH / NW;                    // column chunks per warp per tile
+    static_assert(NCH % NW == 0, "chunks split evenly between the warps of a lane quarter");
+    const int half = e / 4;                            // this warp takes chunks c = half + NW·k
     const bool mom = args.mu != 0.0f;
     const uint64_t pol_stream = TPS_SGD_L2HINT ? ptx::policy_evict_first() : 0ull;
     // 16-byte chunk `ch` of row `row` in the swizzled box (128B swizzle for 128-byte rows, 64B
     // swizzle for 64-byte rows)
     auto swz = [](int row, int ch) { return CW == 32 ? (ch ^ (row & 7)) : (ch ^ ((row >> 1) & 3)); };
-    auto issue = [&](int i) {            // lane 0: TMA loads of chunk i into buffer i % SGD_NB
-      const int ti = i / NCH, c = i - ti * NCH;
+    auto issue = [&](int i) {            // lane 0: TMA loads of this warp's chunk i into buffer i % SGD_NB
+      const int ti = i / NCHW, c = half + NW * (i - ti * NCHW);
       const int t = cid + ti * ncl;
       if (t >= num_tiles) return;
       int mb, nb;
@@ -426,7 +439,7 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
     // L2 prefetch of chunk i (TPS_SGD_PF chunks ahead of its shared-memory load), so that load
     // hits L2 instead of waiting a full DRAM round trip; no shared memory or registers held
     auto prefetch = [&](int i) {
-      const int ti = i / NCH, c = i - ti * NCH;
+      const int ti = i / NCHW, c = half + NW * (i - ti * NCHW);
       const int t = cid + ti * ncl;
       if (t >= num_tiles) return;
       int mb, nb;
@@ -450,7 +463,8 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
       ptx::tc_fence_after();
       const int row0 = mb * BM * CG + static_cast<int>(rank) * BM + q * 32;
 #pragma unroll 1
-      for (int c = 0; c < NCH; ++c, ++i) {
+      for (int ci = 0; ci < NCHW; ++ci, ++i) {
+        const int c = half + NW * ci;
         uint32_t r[CW];
         if constexpr (CW == 32)
           ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c * CW,
@@ -459,7 +473,7 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
           ptx::tmem_ld_32x32b_x16(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c * CW,
                                   *reinterpret_cast<uint32_t(*)[16]>(r));
         ptx::tmem_ld_wait();
-        if (c == NCH - 1) {
+        if (ci == NCHW - 1) {              // last TMEM read of this warp for this tile
           ptx::tc_fence_before();
           __syncwarp();
           if (lane == 0) {

@@ -2538,6 +2538,22 @@ tps_status tps_get_losses(tps_pipeline* p, float* out, int64_t cap, int64_t* n) 
   return TPS_OK;
 }
 
+tps_status tps_read_losses_async(tps_pipeline* p, int64_t first, int64_t n, float* host_dst, uint64_t stream) {
+  TPS_TRY(check_usable(p));
+  if (!p->last) return fail(TPS_E_INVALID_ARG, "losses live on the last stage");
+  if (!host_dst || first < 0 || n < 0 || first + n > p->loss_count)
+    return fail(TPS_E_INVALID_ARG, "losses [%lld, +%lld) not produced (have %lld)", (long long)first, (long long)n,
+                (long long)p->loss_count);
+  if (n == 0) return TPS_OK;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (st != p->cs) {   // the loss kernels run on the compute stream
+    CUDA_OK(cudaEventRecord(p->ev_caller, p->cs));
+    CUDA_OK(cudaStreamWaitEvent(st, p->ev_caller, 0));
+  }
+  CUDA_OK(cudaMemcpyAsync(host_dst, p->losses + first, static_cast<size_t>(n) * sizeof(float), cudaMemcpyDeviceToHost, st));
+  return TPS_OK;
+}
+
 tps_status tps_get_trace(tps_pipeline* p, tps_event* out, int64_t cap, int64_t* n) {
   if (!p || !n) return fail(TPS_E_INVALID_ARG, "null argument");
   *n = static_cast<int64_t>(p->trace.size());

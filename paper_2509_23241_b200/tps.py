@@ -35,7 +35,7 @@ EXPORTS = [
     "tps_conv_gemm", "tps_partition", "tps_im2col", "tps_col2im", "tps_bn_forward", "tps_bn_backward",
     "tps_pool_op", "tps_conv2d_gemm", "tps_debug_progress", "tps_memory_observed", "tps_join", "tps_ipc_export", "tps_ipc_connect",
     "tps_dp_export", "tps_dp_connect", "tps_gemm_wgrad_sgd", "tps_graph_capture", "tps_graph_replay",
-    "tps_graph_destroy",
+    "tps_graph_destroy", "tps_read_losses_async",
 ]
 TPS_LAYER_LINEAR, TPS_LAYER_CONV3X3, TPS_LAYER_MAXPOOL2 = 0, 1, 2
 TPS_LAYER_CONV, TPS_LAYER_BN, TPS_LAYER_MAXPOOL3, TPS_LAYER_AVGPOOL = 3, 4, 5, 6
@@ -159,6 +159,7 @@ def lib() -> C.CDLL:
             "tps_graph_capture": (I32, [C.POINTER(P), I32, I64, I64, P, P, I32, U64, C.POINTER(P)]),
             "tps_graph_replay": (I32, [P]),
             "tps_graph_destroy": (I32, [P]),
+            "tps_read_losses_async": (I32, [P, I64, I64, P, U64]),
             "tps_dp_export": (I32, [P, P, I64, C.POINTER(I64)]),
             "tps_dp_connect": (I32, [P, C.POINTER(P), I32]),
         }
@@ -469,6 +470,10 @@ class Pipeline:
         if n.value:
             check(lib().tps_get_losses(self.h, out.ctypes.data, n.value, C.byref(n)))
         return out
+
+    def read_losses_async(self, first: int, n: int, host_dst, stream: int):
+        """Enqueue a device -> host copy of losses [first, first + n) into (pinned) host_dst."""
+        check(lib().tps_read_losses_async(self.h, first, n, ptr(host_dst), stream))
 
     def trace(self) -> list[Event]:
         n = C.c_int64()

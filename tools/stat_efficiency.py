@@ -62,16 +62,16 @@ def train(variant, blend, lam, args, xpool, ypool, n_mb, seed=7):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--stages", type=int, default=4)
-    ap.add_argument("--epochs", type=int, default=12)
-    ap.add_argument("--width", type=int, default=512)
-    ap.add_argument("--depth", type=int, default=8)
+    ap.add_argument("--epochs", type=int, default=20)
+    ap.add_argument("--width", type=int, default=256)
+    ap.add_argument("--depth", type=int, default=4)
     ap.add_argument("--classes", type=int, default=10)
     ap.add_argument("--m", type=int, default=4)
     ap.add_argument("--b", type=int, default=64)
     ap.add_argument("--batches", type=int, default=32)
-    ap.add_argument("--lr", type=float, default=0.05)
+    ap.add_argument("--lr", type=float, default=0.1)
     ap.add_argument("--mu", type=float, default=0.9)
-    ap.add_argument("--threshold", type=float, default=1.0)
+    ap.add_argument("--threshold", type=float, default=1.2)
     ap.add_argument("--out", default=None)
     ap.add_argument("--seeds", default="0,1,2")
     ap.add_argument("--quick", action="store_true", help="V, I-EQ1 and I-CONVEX at the default lambda only")
