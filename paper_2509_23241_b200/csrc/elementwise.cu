@@ -221,6 +221,43 @@ __global__ void __launch_bounds__(256) bias_grad_fused(const uint16_t* __restric
   b[c] = __fsub_rn(w, __fmul_rn(lr, upd));
 }
 
+// bias gradient from the column partial sums a GEMM epilogue wrote (GemmArgs.colsum: one row of
+// 32-row sums per row group): db[c] = Σ_g part[g·cols + c] in fixed order (fp64 accumulation,
+// rounded once), then, if b != null, the bias's SGD/momentum step (same operations as
+// sgd_update_kernel).  Replaces a full pass over the activation gradient.
+__global__ void __launch_bounds__(256) bias_from_colsum_kernel(const float* __restrict__ part, int groups, int cols,
+                                                               float* __restrict__ db, float* __restrict__ b,
+                                                               float* __restrict__ vb, float lr, float mu, float wd) {
+  // block = 32 columns x 8 row lanes; lane ly sums groups ly, ly+8, ... (independent loads in
+  // flight), then the 8 lane sums are added in fixed order: deterministic
+  __shared__ double red[8][33];
+  const int lx = threadIdx.x & 31, ly = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + lx;
+  double acc = 0.0;
+  if (c < cols) {
+#pragma unroll 4
+    for (int g = ly; g < groups; g += 8) acc += __ldcg(part + static_cast<size_t>(g) * cols + c);
+  }
+  red[ly][lx] = acc;
+  __syncthreads();
+  if (ly != 0 || c >= cols) return;
+  double t = 0.0;
+#pragma unroll
+  for (int y = 0; y < 8; ++y) t += red[y][lx];
+  const float d = static_cast<float>(t);
+  db[c] = d;
+  if (!b) return;
+  const float w = b[c];
+  const float gp = __fadd_rn(d, __fmul_rn(wd, w));
+  float upd = gp;
+  if (mu != 0.f) {
+    const float v = __fadd_rn(__fmul_rn(mu, vb[c]), gp);
+    vb[c] = v;
+    upd = v;
+  }
+  b[c] = __fsub_rn(w, __fmul_rn(lr, upd));
+}
+
 __global__ void bias_grad_final(const float* __restrict__ part, int splits, int cols, float* __restrict__ db) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= cols) return;
@@ -536,6 +573,40 @@ __global__ void bn_stats_final(const double* __restrict__ part, int chunks, int 
   const double var = fmax(s2 / seg_rows - m * m, 0.0);
   mean[i] = static_cast<float>(m);
   invstd[i] = static_cast<float>(1.0 / sqrt(var + eps));
+}
+
+// batch-norm statistics from the column partial sums the producing convolution's epilogue wrote
+// (GemmArgs.colsum with colsum_sq: Σx plane then Σx² plane, one row per 32 output rows; segment
+// `seg` = groups [seg·gps, (seg+1)·gps)): per (segment, row-group chunk, 32 channels) fp64 sums in
+// the layout bn_stats_final reads (the same chunking as the statistics pass it replaces, over
+// 1/32 of the rows)
+__global__ void __launch_bounds__(256) bn_colsum_partial(const float* __restrict__ part, int64_t groups_total,
+                                                         int gps, int C, int chunks, double* __restrict__ out) {
+  __shared__ double red[2][8][33];
+  const int lx = threadIdx.x & 31, ly = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + lx;
+  const int seg = blockIdx.z;
+  const int per = (gps + chunks - 1) / chunks;
+  const int lo = blockIdx.y * per, hi = min(gps, lo + per);
+  double s1 = 0.0, s2 = 0.0;
+  if (c < C) {
+#pragma unroll 4
+    for (int g = lo + ly; g < hi; g += 8) {
+      const size_t o = static_cast<size_t>(seg) * gps + g;
+      s1 += __ldcg(part + o * C + c);
+      s2 += __ldcg(part + (groups_total + o) * C + c);
+    }
+  }
+  red[0][ly][lx] = s1;
+  red[1][ly][lx] = s2;
+  __syncthreads();
+  if (ly != 0 || c >= C) return;
+  double t1 = 0.0, t2 = 0.0;
+#pragma unroll
+  for (int y = 0; y < 8; ++y) { t1 += red[0][y][lx]; t2 += red[1][y][lx]; }
+  const size_t o = (static_cast<size_t>(seg) * chunks + blockIdx.y) * C + c;
+  out[2 * o] = t1;
+  out[2 * o + 1] = t2;
 }
 
 // y = act(γ·(x - μ_seg)·invstd_seg + β (+ res)) -> bf16
@@ -1210,6 +1281,13 @@ cudaError_t launch_sgd_update_dp(float* w, float* v, const GradList& g, uint16_t
   return cudaGetLastError();
 }
 
+cudaError_t launch_bias_from_colsum(const float* part, int groups, int cols, float* db, float* b, float* vb, float lr,
+                                   float mu, float wd, cudaStream_t st) {
+  if (cols <= 0) return cudaSuccess;
+  bias_from_colsum_kernel<<<(cols + 31) / 32, 256, 0, st>>>(part, groups, cols, db, b, vb, lr, mu, wd);
+  return cudaGetLastError();
+}
+
 int64_t bias_grad_scratch_floats(int rows, int cols) {
   // BG_CNT arrival counters of bias_grad_fused (zero at allocation, self-resetting) at a fixed
   // offset, then the partial sums
@@ -1379,6 +1457,23 @@ cudaError_t launch_bn_forward(const uint16_t* x, const uint16_t* res, uint16_t* 
   bn_stats_partial<<<grid, dim3(32, 8), 0, st>>>(x, seg_rows, C, chunks, scratch);
   bn_stats_final<<<(segs * C * 32 + 255) / 256, 256, 0, st>>>(scratch, chunks, C, seg_rows, segs, mean, invstd, 1e-5f);
   bn_apply_kernel<<<grid_for(rows * C, 256), 256, 0, st>>>(x, res, y, gamma, beta, mean, invstd, rows, C, seg_rows, relu);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bn_forward_colsum(const float* part, const uint16_t* x, const uint16_t* res, uint16_t* y,
+                                    const float* gamma, const float* beta, float* mean, float* invstd, int segs,
+                                    int seg_rows, int C, int relu, double* scratch, cudaStream_t st) {
+  if (seg_rows % 32 || C % 8) return cudaErrorInvalidValue;
+  const int gps = seg_rows / 32;
+  const int64_t rows = static_cast<int64_t>(segs) * seg_rows;
+  const int chunks = std::min(bn_chunks(segs, seg_rows, C), gps);
+  bn_colsum_partial<<<dim3((C + 31) / 32, chunks, segs), 256, 0, st>>>(part, static_cast<int64_t>(segs) * gps, gps, C,
+                                                                        chunks, scratch);
+  bn_stats_final<<<(segs * C * 32 + 255) / 256, 256, 0, st>>>(scratch, chunks, C, seg_rows, segs, mean, invstd, 1e-5f);
+  const int C8 = C / 8, tx = std::min(C8, 32);
+  bn_apply_rows<<<bn_rows_grid(static_cast<int>(rows), C8), tx * (256 / tx), 0, st>>>(
+      reinterpret_cast<const uint4*>(x), reinterpret_cast<const uint4*>(res), reinterpret_cast<uint4*>(y), gamma, beta,
+      mean, invstd, static_cast<int>(rows), C8, seg_rows, relu);
   return cudaGetLastError();
 }
 

@@ -57,6 +57,11 @@ struct GemmArgs {
   // update and layer k-1's input gradient CONCURRENTLY on two streams; capping both persistent
   // grids partitions the SMs between them so they co-run instead of queueing for SMs.
   int max_ctas;
+  // column sums of the stored output (plain epilogue, no split-K): colsum[g·N + n] = Σ over rows
+  // [32g, 32g+32) of out[·, n] (g < ceil(M/32)); with colsum_sq the Σx² plane follows at
+  // colsum + ceil(M/32)·N.  Fed to the bias gradient of the next layer down and to batch-norm
+  // statistics without another pass over the tensor.  Null = off.
+  float* colsum; int colsum_sq;
 };
 
 // floats of split-K workspace gemm_run needs for this weight-gradient GEMM (0: no split)

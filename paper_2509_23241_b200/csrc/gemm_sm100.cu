@@ -130,6 +130,22 @@ __device__ __forceinline__ void tile_split(int t, int num_m, int num_n, int num_
 }
 
 
+// a[i] holds row `lane`, column i of a 32 x 32 block; afterwards a[0] of lane j = Σ_rows of
+// column j.  Five butterfly rounds, each halving the columns a lane keeps (lane bit b picks the
+// upper or lower half), fixed order: deterministic.
+__device__ __forceinline__ void warp_transpose_sum(float (&a)[32], int lane) {
+#pragma unroll
+  for (int w = 16; w >= 1; w >>= 1) {
+    const bool upper = (lane & w) != 0;
+#pragma unroll
+    for (int i = 0; i < w; ++i) {
+      const float send = upper ? a[i] : a[i + w];          // the half this lane gives away
+      const float keep = upper ? a[i + w] : a[i];
+      a[i] = keep + __shfl_xor_sync(0xffffffffu, send, w);
+    }
+  }
+}
+
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
@@ -606,10 +622,12 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
         // plain epilogue: thread = row, 16-byte vector loads/stores along the row
         const int grow = row0 + lane;
         const int gcol = nb * BN + c * 32;
-        if (grow >= args.M || gcol >= args.N) continue;
+        if (gcol >= args.N) continue;                    // warp-uniform
+        const bool live = grow < args.M;
         float v[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+        if (live) {
         const int nchunk = min(4, (args.N - gcol) >> 3);   // 8-column chunks inside N
         if (args.alpha != 1.0f) {
 #pragma unroll
@@ -688,6 +706,27 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
               o.w = pack_bf16(v[ch * 8 + 6], v[ch * 8 + 7]);
               reinterpret_cast<uint4*>(op)[ch] = o;
             }
+          }
+        }
+        }   // live
+        if (args.colsum && args.splits <= 1 && row0 < args.M) {   // warp-uniform: the group holds rows
+          // column sums of the values as STORED (bf16-rounded unless fp32 out) over this warp's 32
+          // rows: a fixed butterfly transposes the reduction so lane j ends with column gcol + j;
+          // written as one partial row per 32-row group (Σx, and Σx² in a second plane if asked)
+          float a[32], q2[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const float x = !live ? 0.0f : (args.out_f32 ? v[i] : __bfloat162float(__float2bfloat16_rn(v[i])));
+            a[i] = x;
+            q2[i] = x * x;
+          }
+          warp_transpose_sum(a, lane);
+          if (args.colsum_sq) warp_transpose_sum(q2, lane);
+          const int64_t grp = row0 >> 5;
+          const int64_t groups = (args.M + 31) >> 5;
+          if (gcol + lane < args.N) {
+            args.colsum[grp * args.N + gcol + lane] = a[0];
+            if (args.colsum_sq) args.colsum[(groups + grp) * args.N + gcol + lane] = q2[0];
           }
         }
       }

@@ -35,6 +35,11 @@ cudaError_t launch_bias_grad(const uint16_t* G, int rows, int cols, int ldg, flo
 cudaError_t launch_bias_grad_sgd(const uint16_t* G, int rows, int cols, int ldg, float* db, float* scratch, float* b,
                                  float* vb, float lr, float mu, float wd, cudaStream_t st);
 
+// db[c] = Σ_g part[g·cols + c] (the 32-row column sums a GEMM epilogue wrote, GemmArgs.colsum;
+// fixed order, fp64 accumulation), then the bias SGD/momentum step if b != nullptr.
+cudaError_t launch_bias_from_colsum(const float* part, int groups, int cols, float* db, float* b, float* vb, float lr,
+                                   float mu, float wd, cudaStream_t st);
+
 // Softmax cross-entropy forward+backward for `rows` rows of fp32 logits [rows, ldl] with
 // `classes` valid columns: loss_rows[r] = logsumexp(z) - z_y ;
 // G[r, c] = bf16((softmax(z)_c - [c == y]) / batch) for c < classes, 0 for classes <= c < ldg.
@@ -74,6 +79,12 @@ int64_t bn_scratch_doubles(int segs, int seg_rows, int C);
 cudaError_t launch_bn_forward(const uint16_t* x, const uint16_t* res, uint16_t* y, const float* gamma,
                               const float* beta, float* mean, float* invstd, int segs, int seg_rows, int C, int relu,
                               double* scratch, cudaStream_t st);
+// batch-norm forward whose statistics come from the producing convolution's epilogue column sums
+// (GemmArgs.colsum + colsum_sq over the same rows: Σx plane, then Σx² plane; seg_rows % 32 == 0):
+// same mean / invstd / y as launch_bn_forward up to the fp32 rounding of the 32-row partials
+cudaError_t launch_bn_forward_colsum(const float* part, const uint16_t* x, const uint16_t* res, uint16_t* y,
+                                    const float* gamma, const float* beta, float* mean, float* invstd, int segs,
+                                    int seg_rows, int C, int relu, double* scratch, cudaStream_t st);
 cudaError_t launch_bn_backward(const uint16_t* dy, const uint16_t* y, const uint16_t* x, const float* mean,
                                const float* invstd, const float* gs, const float* gl, float ga, float gb, int segs,
                                int seg_rows, int C, int relu, uint16_t* dx, uint16_t* dres, float* dgamma,

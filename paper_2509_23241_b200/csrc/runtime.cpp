@@ -109,6 +109,13 @@ struct Layer {
   std::vector<float*> verf;           // BN: R fp32 γ versions [C]
   std::vector<float*> mean, invstd;   // BN: per stash slot, [m, C] per-micro-batch statistics
   std::vector<uint8_t*> argmax;       // MAXPOOL3 (C % 8 == 0): per stash slot, first-max tap per output
+  // this backward's bias gradient source: 32-row column sums of G written by the input-gradient
+  // GEMM of the layer above (GemmArgs.colsum), or null (full pass over G)
+  const float* bias_part = nullptr;
+  int bias_groups = 0;
+  // graph networks: this conv's epilogue also writes the column sums (Σx, Σx²) that the batch norm
+  // right after it needs, so the BN skips its statistics pass over the conv output
+  bool stats_to_next = false;
   bool has_w() const {
     return kind == TPS_LAYER_LINEAR || kind == TPS_LAYER_CONV3X3 || kind == TPS_LAYER_CONV || kind == TPS_LAYER_BN;
   }
@@ -159,6 +166,7 @@ struct tps_pipeline {
   uint16_t* gin[2] = {nullptr, nullptr};
   uint16_t* gout[2] = {nullptr, nullptr};
   uint16_t* gwork[3] = {nullptr, nullptr, nullptr};
+  float* bpart[3] = {nullptr, nullptr, nullptr};   // column partial sums of gwork[i] (bias gradients)
   float* logits = nullptr;
   uint16_t* gce = nullptr;                  // dlogits, one [B, ld] slot per in-flight mini-batch
   float* loss_rows = nullptr;
@@ -175,6 +183,7 @@ struct tps_pipeline {
   uint16_t* patches = nullptr;
   float* dpatches = nullptr;
   double* bn_scr = nullptr;
+  float* bn_colsum = nullptr;               // conv epilogue -> next BN: Σx, Σx² per 32-row group
   float* splitk_ws = nullptr;               // split-K partials of weight-gradient GEMMs
   int64_t splitk_floats = 0;
   std::vector<void*> allocs;
@@ -665,6 +674,10 @@ tps_status graph_forward(tps_pipeline* p, int64_t j, int a0, int cnt, int64_t v)
         tps::GemmArgs ga{};
         ga.alpha = 1.f; ga.xa = 1.f; ga.out = out; ga.ldo = L.Co;
         ga.M = nr * L.hw_out; ga.N = L.Co; ga.K = L.Kp;
+        if (L.stats_to_next) {
+          ga.colsum = p->bn_colsum;
+          ga.colsum_sq = 1;
+        }
         const uint16_t* Wv = L.ver[v % p->R];
         if (L.conv_mode == 1 || L.conv_mode == 3) {
           tps::GemmOperands op{X, 0, Wv, L.Kp, nullptr};
@@ -685,11 +698,19 @@ tps_status graph_forward(tps_pipeline* p, int64_t j, int a0, int cnt, int64_t v)
       case TPS_LAYER_BN: {
         const uint16_t* res = L.res >= -1 ? gtensor(p, slot0, slot, L.res) + static_cast<size_t>(r0) * gelems(p, L.res)
                                           : nullptr;
-        CUDA_OK(tps::launch_bn_forward(X, res, static_cast<uint16_t*>(out), L.verf[v % p->R], L.b,
-                                       L.mean[slot] + static_cast<size_t>(a0) * L.Ci,
-                                       L.invstd[slot] + static_cast<size_t>(a0) * L.Ci, cnt, p->bsz * L.hw_in, L.Ci,
-                                       L.relu ? 1 : 0, p->bn_scr, p->cs));
-        p->launches += 3;
+        if (k > 0 && L.src == k - 1 && p->layers[k - 1].stats_to_next) {
+          CUDA_OK(tps::launch_bn_forward_colsum(p->bn_colsum, X, res, static_cast<uint16_t*>(out), L.verf[v % p->R], L.b,
+                                                L.mean[slot] + static_cast<size_t>(a0) * L.Ci,
+                                                L.invstd[slot] + static_cast<size_t>(a0) * L.Ci, cnt,
+                                                p->bsz * L.hw_in, L.Ci, L.relu ? 1 : 0, p->bn_scr, p->cs));
+          p->launches += 3;
+        } else {
+          CUDA_OK(tps::launch_bn_forward(X, res, static_cast<uint16_t*>(out), L.verf[v % p->R], L.b,
+                                         L.mean[slot] + static_cast<size_t>(a0) * L.Ci,
+                                         L.invstd[slot] + static_cast<size_t>(a0) * L.Ci, cnt, p->bsz * L.hw_in, L.Ci,
+                                         L.relu ? 1 : 0, p->bn_scr, p->cs));
+          p->launches += 3;
+        }
         break;
       }
       case TPS_LAYER_MAXPOOL3:
@@ -1042,6 +1063,7 @@ tps_status do_backward(tps_pipeline* p, int64_t j, int staleness) {
   int wbuf = 0;
   const int64_t vn = vl + 1;   // version the update of this mini-batch produces
   const bool blend_on_load = p->variant == TPS_I && delta > 0 && (p->blend == TPS_BLEND_CONVEX || p->eq1_on_load);
+  for (Layer& L : p->layers) { L.bias_part = nullptr; L.bias_groups = 0; }
   if (p->graph) TPS_TRY(graph_backward(p, j, v_used, vl, vn, alpha, beta, blend_on_load, G));
   for (int k = (p->graph ? -1 : nl - 1); k >= 0; --k) {
     Layer& Lk = p->layers[k];
@@ -1064,15 +1086,21 @@ tps_status do_backward(tps_pipeline* p, int64_t j, int staleness) {
       CUDA_OK(cudaEventRecord(p->ev_bias_in, p->cs));
       CUDA_OK(cudaStreamWaitEvent(p->s_upd, p->ev_bias_in, 0));
       // own scratch: a compute-stream bias step of a narrower layer below may run concurrently
-      CUDA_OK(tps::launch_bias_grad_sgd(G, B * Lk.hw_out, Lk.Np, Lk.Np, Lk.db, p->scratch_side, Lk.b, Lk.mb, p->lr,
-                                        p->mu, p->wd, p->s_upd));
+      if (Lk.bias_part)
+        CUDA_OK(tps::launch_bias_from_colsum(Lk.bias_part, Lk.bias_groups, Lk.Np, Lk.db, Lk.b, Lk.mb, p->lr, p->mu,
+                                             p->wd, p->s_upd));
+      else
+        CUDA_OK(tps::launch_bias_grad_sgd(G, B * Lk.hw_out, Lk.Np, Lk.Np, Lk.db, p->scratch_side, Lk.b, Lk.mb, p->lr,
+                                          p->mu, p->wd, p->s_upd));
       CUDA_OK(cudaEventRecord(p->split_w ? p->ev_bias_l[k] : p->ev_bias_done, p->s_upd));
       p->launches += 1;
     }
     // input gradient first: it must read this layer's weights before a fused update rewrites them
     uint16_t* dst = nullptr;
+    int pidx = -1;      // which column-partial buffer goes with dst (bias gradient of layer k-1)
     if (Lk.gidx > 0) {  // the network's first layer has no input gradient
       if (k > 0 && p->split_w) {
+        pidx = k % 3;
         // three rotating buffers: this dgrad overwrites the gradient that layer k+2's weight
         // gradient (stream s_w) and bias step (optimizer stream) read
         dst = p->gwork[k % 3];
@@ -1081,6 +1109,7 @@ tps_status do_backward(tps_pipeline* p, int64_t j, int staleness) {
           CUDA_OK(cudaStreamWaitEvent(p->cs, p->ev_bias_l[k + 2], 0));
         }
       } else if (k > 0) {
+        pidx = wbuf;
         dst = p->gwork[wbuf];
         wbuf ^= 1;
       } else if (p->ipc_direct) {
@@ -1111,6 +1140,12 @@ tps_status do_backward(tps_pipeline* p, int64_t j, int staleness) {
         if (conv) {
           op.cv = tps::ConvGeom{B, Lk.H, Lk.Wd, Lk.Co};
           op.Cw = Lk.Ci;
+        }
+        // the layer below takes its bias gradient from this epilogue's column sums of G
+        if (pidx >= 0 && p->bpart[pidx] && p->layers[k - 1].has_b() && p->layers[k - 1].Np == ga.N) {
+          ga.colsum = p->bpart[pidx];
+          p->layers[k - 1].bias_part = p->bpart[pidx];
+          p->layers[k - 1].bias_groups = (ga.M + 31) / 32;
         }
         if (blend_on_load) {
           op.B2 = Wl;
@@ -1160,8 +1195,12 @@ tps_status do_backward(tps_pipeline* p, int64_t j, int staleness) {
       if (p->split_w) CUDA_OK(cudaEventRecord(p->ev_w_done[k], p->s_w));
       if (!bias_side) {   // bias gradient and the bias's SGD/momentum step in one launch
         // (data parallel: the gradient only; the step runs on the replica average below)
-        CUDA_OK(tps::launch_bias_grad_sgd(G, rows, Lk.Np, Lk.Np, Lk.db, p->scratch, p->dp > 1 ? nullptr : Lk.b, Lk.mb,
-                                          p->lr, p->mu, p->wd, p->cs));
+        if (Lk.bias_part)
+          CUDA_OK(tps::launch_bias_from_colsum(Lk.bias_part, Lk.bias_groups, Lk.Np, Lk.db, p->dp > 1 ? nullptr : Lk.b,
+                                               Lk.mb, p->lr, p->mu, p->wd, p->cs));
+        else
+          CUDA_OK(tps::launch_bias_grad_sgd(G, rows, Lk.Np, Lk.Np, Lk.db, p->scratch, p->dp > 1 ? nullptr : Lk.b, Lk.mb,
+                                            p->lr, p->mu, p->wd, p->cs));
         p->launches += 1;
       }
       // U(j) always directly follows B(j) in the static order (reading Z7), so the update of
@@ -1512,6 +1551,26 @@ tps_status init_graph(tps_pipeline* p, const tps_config* c, int lb, int le) {
     p->layers.push_back(L);
   }
   const int nl = p->nlayers();
+  {
+    // conv -> BN pairs where the conv's epilogue provides the BN statistics (the BN reads the
+    // conv output directly and right after it; 32-row groups must not straddle micro-batches).
+    // Off by default (TPS_COLSUM=1 enables): ResNet-50 7.25k vs 7.47k samples/s with it -- its
+    // convolutions with small K are epilogue-bound, so the extra reduction is not free
+    const char* e = std::getenv("TPS_COLSUM");
+    const bool on = e && e[0] == '1';
+    int64_t cf = 0;
+    for (int k = 0; k + 1 < nl && on; ++k) {
+      Layer& L = p->layers[k];
+      const Layer& N = p->layers[k + 1];
+      if (L.kind == TPS_LAYER_CONV && N.kind == TPS_LAYER_BN && N.src == k && (p->bsz * L.hw_out) % 32 == 0 &&
+          L.Co % 8 == 0) {
+        L.stats_to_next = true;
+        const int64_t rows = static_cast<int64_t>(p->g) * p->bsz * L.hw_out;
+        cf = std::max(cf, 2 * ((rows + 31) / 32) * L.Co);
+      }
+    }
+    if (cf > 0) TPS_TRY(alloc_t(p, &p->bn_colsum, static_cast<size_t>(cf), &p->mem_acts));
+  }
   p->in0_elems = sh[lb].elems();
   p->act.assign(std::max(p->A0, p->Kmax), std::vector<uint16_t*>(nl + 1, nullptr));
   for (int slot = 0; slot < static_cast<int>(p->act.size()); ++slot) {
@@ -1720,6 +1779,21 @@ tps_status tps_pipeline_init(const tps_config* c, tps_pipeline** out) {
   }
   if (p->split_w && (st = alloc_t(p, &p->gwork[2], static_cast<size_t>(p->B) * max_elems, &p->mem_acts)) != TPS_OK)
     return cleanup(st);
+  if (nl > 1 && std::getenv("TPS_COLSUM") && std::getenv("TPS_COLSUM")[0] == '1') {
+    // column partial sums of the input gradients (bias gradients without another pass over G):
+    // ceil(rows / 32) x cols floats for the largest input gradient of the stage.  Off by default:
+    // the epilogue reduction costs more than the pass it saves (C5 589k vs 600k samples/s)
+    int64_t pf = 0;
+    for (int k = 1; k < nl; ++k) {
+      const Layer& Lk = p->layers[k];
+      if (Lk.kind == TPS_LAYER_MAXPOOL2) continue;
+      const int64_t rows = static_cast<int64_t>(p->B) * Lk.hw_in;
+      const int64_t cols = Lk.kind == TPS_LAYER_CONV3X3 ? Lk.Ci : Lk.Kp;
+      pf = std::max(pf, (rows + 31) / 32 * cols);
+    }
+    for (int i = 0; i < (p->split_w ? 3 : 2) && pf > 0; ++i)
+      if ((st = alloc_t(p, &p->bpart[i], static_cast<size_t>(pf), &p->mem_acts)) != TPS_OK) return cleanup(st);
+  }
   if (p->split_w) {
     // SM partition of the concurrent pair (dgrad of layer k-1 | fused wgrad + update of layer k):
     // TPS_SPLIT_FRAC = the dgrad's fraction (default 0 = no partition, both grids full: measured

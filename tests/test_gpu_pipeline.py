@@ -161,3 +161,23 @@ def test_memory_v_vs_i(gpu_lib):
     # I keeps K_0 - 1 = 3 extra bf16 versions of stage 0's two 512x512 layers
     assert mem[tps.TPS_I]["stash"] - mem[tps.TPS_V]["stash"] == 3 * 2 * 512 * 512 * 2
     assert mem[tps.TPS_V]["stash"] == 0
+
+
+@pytest.mark.parametrize("name", ["S4-I-CONVEX", "S3-ragged", "S1-widening"])
+def test_parity_with_epilogue_column_sums(gpu_lib, name, monkeypatch):
+    """TPS_COLSUM=1: bias gradients from the input-gradient GEMM's epilogue column sums (no
+    second pass over G); same oracle bars."""
+    monkeypatch.setenv("TPS_COLSUM", "1")
+    dims, bounds, m, b, M, var, blend, lam, lr, mu, kind = CASES[name]
+    ref = run_oracle(dims, bounds, m, b, M, var, blend, lam, lr, mu, kind=kind)
+    ex = run_oracle(dims, bounds, m, b, M, var, blend, lam, lr, mu, kind=kind, exact=True)
+    stages, losses = run_gpu(dims, bounds, m, b, M, var, blend, lam, lr, mu, kind=kind)
+    assert expand_gpu_trace(stages) == oracle_trace(ref)
+    np.testing.assert_allclose(losses, ref.losses, rtol=1e-3, atol=0)
+    for st in stages:
+        for k, l in enumerate(st.layers):
+            w, bb, _, _ = st.get_weights(k)
+            assert layer_rel_err(w, bb, ref.weights[l], ref.biases[l]) <= 5e-3, (name, l)
+            if np.abs(ref.biases[l]).max() > 0:
+                gap = weight_rel_err(ex.biases[l], ref.biases[l])
+                assert weight_rel_err(bb, ref.biases[l]) <= max(5e-3, 2 * gap), (name, l)

@@ -135,6 +135,15 @@ def test_tiny_resnet_forward_groups(gpu_lib, fwd_group, extra_slot):
             fwd_group=fwd_group, extra_recv_slot=extra_slot)
 
 
+@pytest.mark.parametrize("colsum", ["0", "1"])
+def test_resnet_bn_statistics_from_conv_epilogue(gpu_lib, colsum, monkeypatch):
+    """TPS_COLSUM=1: batch-norm statistics from the producing convolution's epilogue column sums
+    (Σx, Σx² per 32-row group) instead of a pass over the conv output; the same bars."""
+    monkeypatch.setenv("TPS_COLSUM", colsum)
+    layers, starts = tiny(widths=(64, 128), H=32, stem_c=64, blocks=(2, 1))
+    compare(layers, [0, starts[2], len(layers)], 2, 8, 10, ost.I_VARIANT, ost.CONVEX)
+
+
 @pytest.mark.parametrize("vn", list(VARIANTS))
 def test_resnet_implicit_conv_paths(gpu_lib, vn):
     """widths 64/128: 3x3 stride-1 convs take the 4-D TMA implicit-GEMM path, 1x1 convs the
