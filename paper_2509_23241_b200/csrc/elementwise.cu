@@ -941,8 +941,8 @@ __global__ void __launch_bounds__(256) bn_partial_vec(const uint4* __restrict__ 
       load8f(mean + seg * C + cg * 8, m);
       load8f(invstd + seg * C + cg * 8, is);
     }
-#pragma unroll 4
-    for (int r = lo + ly; r < hi; r += ty) {
+#pragma unroll 8
+    for (int r = lo + ly; r < hi; r += ty) {   // 8 rows of loads in flight per thread
       const int64_t o = (r0 + r) * C8 + cg;
       float v[8];
       unpack8(a[o], v);
