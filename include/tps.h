@@ -362,6 +362,22 @@ tps_status tps_memory_observed(tps_pipeline* p, int64_t* device_bytes);
 tps_status tps_set_profiling(tps_pipeline* p, int32_t enable);
 tps_status tps_kernel_stats(tps_pipeline* p, int32_t which, int64_t* launches, double* ms,
                             double* work);
+/* Per-event device timeline (Chrome trace export, tools/chrome_trace.py): when enabled, every
+ * schedule event this handle executes (walker or step-wise) is bracketed by two CUDA events on
+ * its compute stream; tps_get_timeline returns, per event, its trace record and the device times
+ * of the brackets in ms since `origin_event` (a caller-owned cudaEvent_t recorded BEFORE the
+ * events, on any stream of this device, so several handles share one time axis; 0: the handle
+ * records its own origin on its compute stream now).  F spans the forward's launches, B the
+ * backward's (with the fused update, if on), U is a zero-width commit marker.  Enabling or
+ * disabling synchronises and clears the records; graph capture is refused while enabled.
+ * tps_get_timeline synchronises on the last bracket.  With TPS_NVTX=1 in the environment at
+ * tps_pipeline_init, every event is also an NVTX range "s<stage> <F|B|U> mb<j>" (host side). */
+typedef struct {
+  tps_event ev;
+  double t0_ms, t1_ms;
+} tps_timeline_rec;
+tps_status tps_set_timeline(tps_pipeline* p, int32_t enable, uint64_t origin_event);
+tps_status tps_get_timeline(tps_pipeline* p, tps_timeline_rec* out, int64_t cap, int64_t* n);
 /* Number of kernels this handle has launched since init (product kernels only). */
 tps_status tps_launch_count(tps_pipeline* p, int64_t* n);
 

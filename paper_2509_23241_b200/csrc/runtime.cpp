@@ -15,6 +15,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cmath>
@@ -258,6 +259,12 @@ struct tps_pipeline {
   int64_t stat_n[5] = {0, 0, 0, 0, 0};
   int64_t launches = 0;
   bool poisoned = false;
+  // ---- per-event device timeline (tps_set_timeline; Chrome trace) and NVTX ranges (TPS_NVTX=1)
+  bool timeline = false, own_origin = false, nvtx = false;
+  cudaEvent_t tl_origin = nullptr;
+  struct TlPending { tps_event e; cudaEvent_t a, b; };
+  std::vector<TlPending> tl_pending;
+  std::vector<tps_timeline_rec> tl_done;
 
   int nlayers() const { return static_cast<int>(layers.size()); }
 };
@@ -1317,6 +1324,67 @@ tps_status begin_run(tps_pipeline* p, int64_t first, int64_t n) {
   return TPS_OK;
 }
 
+// Timeline / NVTX bracket of one schedule event on the compute stream (off: one branch).
+tps_status tl_take(tps_pipeline* p, cudaEvent_t* e) {
+  if (p->ev_pool.empty()) {
+    for (int i = 0; i < 64; ++i) {
+      cudaEvent_t ev;
+      CUDA_OK(cudaEventCreate(&ev));
+      p->ev_pool.push_back(ev);
+    }
+  }
+  *e = p->ev_pool.back();
+  p->ev_pool.pop_back();
+  return TPS_OK;
+}
+
+template <class F>
+tps_status bracket(tps_pipeline* p, int kind, int64_t mb, F&& body) {
+  if (!p->timeline && !p->nvtx) return body();
+  if (p->nvtx) {
+    char name[64];
+    std::snprintf(name, sizeof(name), "s%d %c mb%lld", p->s, "FBU"[kind], static_cast<long long>(mb));
+    nvtxRangePushA(name);
+  }
+  cudaEvent_t a = nullptr, b = nullptr;
+  if (p->timeline) {
+    TPS_TRY(tl_take(p, &a));
+    CUDA_OK(cudaEventRecord(a, p->cs));
+  }
+  const size_t n0 = p->trace.size();
+  const tps_status st = body();
+  if (p->nvtx) nvtxRangePop();
+  if (p->timeline) {
+    if (st != TPS_OK || p->trace.size() != n0 + 1) {
+      p->ev_pool.push_back(a);
+      return st;
+    }
+    TPS_TRY(tl_take(p, &b));
+    CUDA_OK(cudaEventRecord(b, p->cs));
+    p->tl_pending.push_back({p->trace.back(), a, b});
+  }
+  return st;
+}
+
+tps_status drain_timeline(tps_pipeline* p) {
+  if (p->tl_pending.empty()) return TPS_OK;
+  CUDA_OK(cudaEventSynchronize(p->tl_pending.back().b));
+  for (auto& t : p->tl_pending) {
+    tps_timeline_rec r{};
+    r.ev = t.e;
+    float a = 0.f, b = 0.f;
+    CUDA_OK(cudaEventElapsedTime(&a, p->tl_origin, t.a));
+    CUDA_OK(cudaEventElapsedTime(&b, p->tl_origin, t.b));
+    r.t0_ms = a;
+    r.t1_ms = b;
+    p->tl_done.push_back(r);
+    p->ev_pool.push_back(t.a);
+    p->ev_pool.push_back(t.b);
+  }
+  p->tl_pending.clear();
+  return TPS_OK;
+}
+
 tps_status fire(tps_pipeline* p, const tps_event& e, const void* x_pool, const int32_t* y_pool, int pool) {
   if (e.kind == TPS_EV_F) {
     const int64_t slot = e.mb % pool;
@@ -1326,10 +1394,10 @@ tps_status fire(tps_pipeline* p, const tps_event& e, const void* x_pool, const i
     const int64_t row = (slot * p->dp + p->dp_rank) * p->B + static_cast<int64_t>(e.micro) * p->bsz;
     if (p->first) x = static_cast<const uint16_t*>(x_pool) + row * p->dims[0];
     if (p->last) y = y_pool + row;
-    return do_forward(p, e.mb, e.micro, e.micro_count, x, y);
+    return bracket(p, TPS_EV_F, e.mb, [&] { return do_forward(p, e.mb, e.micro, e.micro_count, x, y); });
   }
-  if (e.kind == TPS_EV_B) return do_backward(p, e.mb, -1);
-  return do_update(p, e.mb);
+  if (e.kind == TPS_EV_B) return bracket(p, TPS_EV_B, e.mb, [&] { return do_backward(p, e.mb, -1); });
+  return bracket(p, TPS_EV_U, e.mb, [&] { return do_update(p, e.mb); });
 }
 
 }  // namespace
@@ -1858,6 +1926,7 @@ tps_status tps_pipeline_init(const tps_config* c, tps_pipeline** out) {
   int prio_lo = 0, prio_hi = 0;   // least (0) and greatest (< 0) stream priority
   cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
   if (const char* e = std::getenv("TPS_PRIO"); e && e[0] == '0') prio_hi = prio_lo;
+  if (const char* e = std::getenv("TPS_NVTX"); e && e[0] == '1') p->nvtx = true;
   p->ev_caller = new_event();
   if (c->compute_stream) {
     p->cs = reinterpret_cast<cudaStream_t>(c->compute_stream);
@@ -1953,6 +2022,8 @@ tps_status tps_pipeline_destroy(tps_pipeline* p) {
   for (auto e : p->ev_upd_done) kill_ev(e);
   for (auto e : p->ev_pool) kill_ev(e);
   for (auto& t : p->timed) { kill_ev(t.a); kill_ev(t.b); }
+  for (auto& t : p->tl_pending) { kill_ev(t.a); kill_ev(t.b); }
+  if (p->own_origin) kill_ev(p->tl_origin);
   for (cudaEvent_t e : {p->ev_caller, p->ev_recv, p->ev_gout_ready, p->ev_gin_ready, p->ev_gin_free[0], p->ev_gin_free[1],
                         p->ev_bwd_sent[0], p->ev_bwd_sent[1]})
     kill_ev(e);
@@ -2167,17 +2238,17 @@ tps_status tps_begin_run(tps_pipeline* p, int64_t first_mb, int64_t n_mb) {
 tps_status tps_stage_forward(tps_pipeline* p, int64_t mb, int32_t micro, int32_t count, const void* x,
                              const int32_t* labels) {
   TPS_TRY(check_usable(p));
-  return do_forward(p, mb, micro, count, x, labels);
+  return bracket(p, TPS_EV_F, mb, [&] { return do_forward(p, mb, micro, count, x, labels); });
 }
 
 tps_status tps_stage_backward(tps_pipeline* p, int64_t mb, int32_t staleness) {
   TPS_TRY(check_usable(p));
-  return do_backward(p, mb, staleness);
+  return bracket(p, TPS_EV_B, mb, [&] { return do_backward(p, mb, staleness); });
 }
 
 tps_status tps_stage_update(tps_pipeline* p, int64_t mb) {
   TPS_TRY(check_usable(p));
-  return do_update(p, mb);
+  return bracket(p, TPS_EV_U, mb, [&] { return do_update(p, mb); });
 }
 
 tps_status tps_run_schedule(tps_pipeline* p, int64_t first_mb, int64_t n_mb, const void* x_pool, const int32_t* y_pool,
@@ -2266,7 +2337,8 @@ tps_status tps_graph_capture(tps_pipeline* const* st, int32_t n, int64_t first_m
     TPS_TRY(check_usable(p));
     if (p->transport == TPS_TRANSPORT_IPC || p->transport == TPS_TRANSPORT_NCCL || p->dp > 1)
       return fail(TPS_E_UNSUPPORTED, "graph capture: LOCAL / single-stage handles only");
-    if (p->profiling) return fail(TPS_E_STATE, "graph capture with per-launch profiling enabled");
+    if (p->profiling || p->timeline)
+      return fail(TPS_E_STATE, "graph capture with per-launch profiling or the timeline enabled");
     if (p->in_run) return fail(TPS_E_ORDER, "handle %d is inside a run", i);
     period = lcm64(period, lcm64(lcm64(p->A0, p->Kmax), p->R));
   }
@@ -2665,6 +2737,36 @@ tps_status tps_set_profiling(tps_pipeline* p, int32_t enable) {
   TPS_TRY(drain_timing(p));
   p->profiling = enable != 0;
   for (int k = 0; k < 5; ++k) { p->stat_ms[k] = 0; p->stat_work[k] = 0; p->stat_n[k] = 0; }
+  return TPS_OK;
+}
+
+tps_status tps_set_timeline(tps_pipeline* p, int32_t enable, uint64_t origin_event) {
+  TPS_TRY(check_usable(p));
+  TPS_TRY(sync_streams(p));
+  for (auto& t : p->tl_pending) { p->ev_pool.push_back(t.a); p->ev_pool.push_back(t.b); }
+  p->tl_pending.clear();
+  p->tl_done.clear();
+  if (p->own_origin && p->tl_origin) cudaEventDestroy(p->tl_origin);
+  p->tl_origin = nullptr;
+  p->own_origin = false;
+  p->timeline = enable != 0;
+  if (!p->timeline) return TPS_OK;
+  if (origin_event) {
+    p->tl_origin = reinterpret_cast<cudaEvent_t>(origin_event);
+  } else {
+    CUDA_OK(cudaEventCreate(&p->tl_origin));
+    p->own_origin = true;
+    CUDA_OK(cudaEventRecord(p->tl_origin, p->cs));
+  }
+  return TPS_OK;
+}
+
+tps_status tps_get_timeline(tps_pipeline* p, tps_timeline_rec* out, int64_t cap, int64_t* n) {
+  TPS_TRY(check_usable(p));
+  if (!n || cap < 0 || (cap > 0 && !out)) return fail(TPS_E_INVALID_ARG, "bad timeline buffer");
+  TPS_TRY(drain_timeline(p));
+  *n = static_cast<int64_t>(p->tl_done.size());
+  if (out) std::memcpy(out, p->tl_done.data(), sizeof(tps_timeline_rec) * static_cast<size_t>(std::min(cap, *n)));
   return TPS_OK;
 }
 

@@ -35,7 +35,7 @@ EXPORTS = [
     "tps_conv_gemm", "tps_partition", "tps_im2col", "tps_col2im", "tps_bn_forward", "tps_bn_backward",
     "tps_pool_op", "tps_conv2d_gemm", "tps_debug_progress", "tps_memory_observed", "tps_join", "tps_ipc_export", "tps_ipc_connect",
     "tps_dp_export", "tps_dp_connect", "tps_gemm_wgrad_sgd", "tps_graph_capture", "tps_graph_replay",
-    "tps_graph_destroy", "tps_read_losses_async",
+    "tps_graph_destroy", "tps_read_losses_async", "tps_set_timeline", "tps_get_timeline",
 ]
 TPS_LAYER_LINEAR, TPS_LAYER_CONV3X3, TPS_LAYER_MAXPOOL2 = 0, 1, 2
 TPS_LAYER_CONV, TPS_LAYER_BN, TPS_LAYER_MAXPOOL3, TPS_LAYER_AVGPOOL = 3, 4, 5, 6
@@ -51,6 +51,10 @@ class Event(C.Structure):
     _fields_ = [("stage", C.c_int32), ("kind", C.c_int32), ("micro", C.c_int32), ("micro_count", C.c_int32),
                 ("mb", C.c_int64), ("v_used", C.c_int64), ("v_latest", C.c_int64), ("delta", C.c_int32),
                 ("alpha", C.c_float), ("beta", C.c_float)]
+
+
+class TimelineRec(C.Structure):
+    _fields_ = [("ev", Event), ("t0_ms", C.c_double), ("t1_ms", C.c_double)]
 
 
 class Layer(C.Structure):
@@ -138,6 +142,8 @@ def lib() -> C.CDLL:
             "tps_clear_trace": (I32, [P]),
             "tps_memory_stats": (I32, [P] + [C.POINTER(I64)] * 6),
             "tps_set_profiling": (I32, [P, I32]),
+            "tps_set_timeline": (I32, [P, I32, U64]),
+            "tps_get_timeline": (I32, [P, C.POINTER(TimelineRec), I64, C.POINTER(I64)]),
             "tps_kernel_stats": (I32, [P, I32, C.POINTER(I64), C.POINTER(D), C.POINTER(D)]),
             "tps_launch_count": (I32, [P, C.POINTER(I64)]),
             "tps_fill_synthetic": (I32, [I32, U64, U64, I64, I64, I32, P, U64]),
@@ -508,6 +514,17 @@ class Pipeline:
 
     def set_profiling(self, on: bool):
         check(lib().tps_set_profiling(self.h, 1 if on else 0))
+
+    def set_timeline(self, on: bool, origin_event: int = 0):
+        """Per-event device brackets; origin_event = a recorded torch.cuda.Event's .cuda_event (0: own)."""
+        check(lib().tps_set_timeline(self.h, 1 if on else 0, origin_event))
+
+    def timeline(self) -> list[TimelineRec]:
+        n = C.c_int64()
+        check(lib().tps_get_timeline(self.h, None, 0, C.byref(n)))
+        buf = (TimelineRec * max(1, n.value))()
+        check(lib().tps_get_timeline(self.h, buf, n.value, C.byref(n)))
+        return list(buf)[: n.value]
 
     def kernel_stats(self, which: int):
         n, ms, work = C.c_int64(), C.c_double(), C.c_double()
