@@ -418,6 +418,21 @@ tps_status tps_gemm_wgrad_sgd(int32_t M, int32_t N, int32_t K, const void* A, in
                               int32_t ldb, float* w, float* v, void* ver, int32_t ldw, float lr, float mu,
                               float wd, uint64_t stream);
 
+/* The dual backward launch the pipeline runs with fuse_update = 1 (rows a8 + a10): ONE
+ * persistent kernel computing tps_gemm_wgrad_sgd(M, N, K, A, lda, B, ldb, w, v, ver, ldw, lr,
+ * mu, wd) (layer k's weight gradient + update) AND the input gradient of layer k-1,
+ *   outd [Md, Nd] (bf16, ld=ldod) = bf16_rne(alpha · (Ad · Bd)) zeroed where mask <= 0,
+ * Ad [Md, Kd] K-major (ld=ldad), Bd stored [Kd, Nd] (ld=ldbd), mask bf16 [Md, Nd] (ld=ldm, may
+ * be NULL) — i.e. tps_gemm mode 1.  Each cluster pair interleaves tiles of both, so the input
+ * gradient's MMAs run while the update epilogue streams w / v.  Both outputs are bit-identical
+ * to the two separate calls.  The two problems must not overlap in memory.  TPS_E_UNSUPPORTED
+ * when either has fewer than 256 rows or N <= 128, or the balanced tile split does not exist. */
+tps_status tps_gemm_bwd_dual(int32_t M, int32_t N, int32_t K, const void* A, int32_t lda, const void* B,
+                             int32_t ldb, float* w, float* v, void* ver, int32_t ldw, float lr, float mu,
+                             float wd, int32_t Md, int32_t Nd, int32_t Kd, const void* Ad, int32_t ldad,
+                             const void* Bd, int32_t ldbd, void* outd, int32_t ldod, float alpha,
+                             const void* mask, int32_t ldm, uint64_t stream);
+
 /* ---- stage partitioner ("distribute the DNNs ... in such a way
  * that a balance is maintained between the memory consumptions in each node") ----------
  * Splits L layers into S consecutive non-empty stages minimising the largest per-stage

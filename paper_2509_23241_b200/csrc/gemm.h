@@ -64,6 +64,24 @@ struct GemmArgs {
   float* colsum; int colsum_sq;
 };
 
+// The input-gradient half of a dual backward launch (gemm_bwd_dual): dX[M, N] = α·(G·W)
+// ⊙ 1[mask > 0], G [M, K] K-major (op.A, lda), W stored [K, N] (op.B, ldb), bf16 out.
+struct DualArgs {
+  int M, N, K;
+  float alpha;
+  void* out; int ldo;
+  const uint16_t* mask; int ldm;
+};
+
+// One persistent launch computing layer k's weight gradient with the fused SGD/momentum update
+// (opw / aw as gemm_run's GEMM_WGRAD with epi = EPI_SGD) AND layer k-1's input gradient (opd /
+// dg as GEMM_DGRAD without blend): every CTA pair interleaves tiles of both, so the tensor
+// pipe runs the input gradient's MMAs while the update epilogue streams w / v through HBM.
+// Results are bit-identical to the two separate launches.  cudaErrorNotSupported when the
+// shapes do not suit it (the caller then launches the two separately).
+cudaError_t gemm_bwd_dual(const GemmOperands& opw, const GemmArgs& aw, const GemmOperands& opd, const DualArgs& dg,
+                          cudaStream_t st);
+
 // floats of split-K workspace gemm_run needs for this weight-gradient GEMM (0: no split)
 int64_t gemm_splitk_floats(int mode, int M, int N, int K, int ldo);
 

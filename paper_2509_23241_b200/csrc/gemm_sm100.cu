@@ -80,6 +80,9 @@ constexpr int SGD_NB = TPS_SGD_NB;
 // fused update: columns per w / v chunk (32: 128B-swizzled 32x32 fp32 boxes; 16: 64B-swizzled
 // 32x16 boxes, half the bytes per buffer, so twice the buffers fit the same shared memory and
 // more chunks are in flight per warp)
+#ifndef TPS_SGD_PF0
+#define TPS_SGD_PF0 0      // fused update: L2 prefetch of the first N tiles' w / v at kernel start
+#endif
 #ifndef TPS_SGD_CW
 #define TPS_SGD_CW 32
 #endif
@@ -468,6 +471,10 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
       if (TPS_SGD_PF)
         for (int i = SGD_NB; i < SGD_NB + TPS_SGD_PF; ++i) prefetch(i);
       for (int i = 0; i < SGD_NB; ++i) issue(i);
+      // HBM idles while the first tile's MMAs run: pull the first tiles' w / v into L2 so
+      // their epilogues run at L2 latency
+      if (TPS_SGD_PF0)
+        for (int i = SGD_NB; i < NCHW * TPS_SGD_PF0; ++i) prefetch(i);
     }
     int i = 0, it = 0;
     for (int t = cid; t < num_tiles; t += ncl, ++it) {
@@ -776,6 +783,343 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
       ptx::tmem_relinquish();
       ptx::tmem_dealloc(tmem_base, C::TMEM_COLS);
     }
+  }
+}
+
+
+// ---------------------------------------------------------------- dual backward launch
+// Layer k's weight gradient + fused update (tiles "W": K = batch rows, HBM-heavy epilogue) and
+// layer k-1's input gradient (tiles "D": K = layer width, light epilogue) in ONE persistent
+// launch.  The split backward used to run them as two kernels that queued for the same SMs, so
+// each SM's tensor pipe idled while its update epilogue streamed w / v.  Here every CTA pair
+// walks a list mixing both kinds: the MMAs of a D tile run while the epilogue warps stream the
+// previous W tile's update.  Each tile is computed exactly as by the separate kernels (same
+// operand staging, instruction shapes and K order), so the results are bit-identical.
+//
+// Work split (closed form, no device memory, graph-safe): D tiles are dealt round-robin over
+// the cluster pairs; W tiles are given out in consecutive runs so that every pair's MMA work
+// (in K blocks) is within one W tile of the average.  Inside a pair's list the D tiles are
+// spread evenly among the W tiles (a W tile first, a D tile last: its epilogue is the short one).
+__host__ __device__ inline int64_t dual_dpre(int c, int n_d, int ncl) {
+  return static_cast<int64_t>(n_d / ncl) * c + (c < n_d % ncl ? c : n_d % ncl);
+}
+__host__ __device__ inline int dual_wpre(int c, int n_d, int n_w, int kd, int kw, int ncl) {
+  const int64_t U = static_cast<int64_t>(n_d) * kd + static_cast<int64_t>(n_w) * kw;
+  const int64_t r = static_cast<int64_t>(c) * U / ncl - static_cast<int64_t>(kd) * dual_dpre(c, n_d, ncl);
+  const int64_t w = r <= 0 ? 0 : (r + kw / 2) / kw;
+  return static_cast<int>(w < n_w ? w : n_w);
+}
+
+template <int BN, int CG>
+__global__ void __launch_bounds__(Cfg<BN, 0, 1, CG>::THREADS, 1)
+    bwd_dual_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    const __grid_constant__ CUtensorMap tmDA, const __grid_constant__ CUtensorMap tmDB,
+                    const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmV,
+                    const GemmArgs args, const DualArgs dg) {
+  using C = Cfg<BN, 0, 1, CG>;
+  static_assert(CG == 2 && TPS_SGD_STG, "dual launch: CTA pairs, STG write-back");
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* stages = smem;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tmem_full = empty + 2 * C::STAGES;
+  uint64_t* tmem_empty = tmem_full + C::ACC;
+  uint64_t* sgd_bar = tmem_empty + C::ACC;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sgd_bar + SGD_WARPS * SGD_NB);
+  uint8_t* epi_smem = smem + C::STAGES * C::STAGE_BYTES + 1024;
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = ptx::cluster_rank();
+  const int cid = blockIdx.x / CG, ncl = gridDim.x / CG;
+  const int wm = (args.M + BM * CG - 1) / (BM * CG), wn = (args.N + BN - 1) / BN, kw = (args.K + BK - 1) / BK;
+  const int dm = (dg.M + BM * CG - 1) / (BM * CG), dn = (dg.N + BN - 1) / BN, kd = (dg.K + BK - 1) / BK;
+  const int n_w = wm * wn, n_d = dm * dn;
+  const int d_c = cid < n_d ? (n_d - cid - 1) / ncl + 1 : 0;
+  const int w0 = dual_wpre(cid, n_d, n_w, kd, kw, ncl);
+  const int w_c = dual_wpre(cid + 1, n_d, n_w, kd, kw, ncl) - w0;
+  const int len = d_c + w_c;
+  // position k of this pair's list -> (kind, tile index within its GEMM)
+  auto at = [&](int k, bool& is_d, int& t) {
+    const int before = static_cast<int>(static_cast<int64_t>(k) * d_c / len);     // D tiles before k
+    is_d = static_cast<int>(static_cast<int64_t>(k + 1) * d_c / len) > before;
+    t = is_d ? cid + before * ncl : w0 + (k - before);
+  };
+
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&tmA);
+    ptx::prefetch_tmap(&tmB);
+    ptx::prefetch_tmap(&tmDA);
+    ptx::prefetch_tmap(&tmDB);
+    for (int s = 0; s < C::STAGES; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < C::ACC; ++a) {
+      ptx::mbar_init(&tmem_full[a], 1);
+      ptx::mbar_init(&tmem_empty[a], C::NEPI * CG);
+    }
+    for (int i = 0; i < SGD_WARPS * SGD_NB; ++i) ptx::mbar_init(&sgd_bar[i], 1);
+    ptx::fence_barrier_init();
+  }
+  ptx::cluster_sync();   // both CTAs resident before the pair's TMEM allocation (see gemm_kernel)
+  if (warp == 1) ptx::tmem_alloc_cg2(tmem_slot, C::TMEM_COLS);
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  ptx::grid_dep_wait();
+
+  if (warp == 0) {
+    // ===================== TMA producer =====================
+    if (lane == 0) {
+      const uint64_t pol_keep = TPS_SGD_L2HINT ? ptx::policy_evict_last() : 0ull;
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int k = 0; k < len; ++k) {
+        bool is_d;
+        int t, mb, nb;
+        at(k, is_d, t);
+        tile_coords(t, is_d ? dm : wm, is_d ? dn : wn, mb, nb);
+        const int m0 = mb * BM * CG + static_cast<int>(rank) * BM;
+        const int n0 = nb * BN + static_cast<int>(rank) * (BN / CG);
+        const int nk = is_d ? kd : kw;
+        const CUtensorMap* mA = is_d ? &tmDA : &tmA;
+        const CUtensorMap* mB = is_d ? &tmDB : &tmB;
+        for (int kb = 0; kb < nk; ++kb) {
+          MBAR_WAIT(1, &empty[stage], phase ^ 1);
+          uint8_t* sA = stages + stage * C::STAGE_BYTES;
+          uint8_t* sB = sA + A_BYTES;
+          if (rank == 0) ptx::mbar_expect_tx(&full[stage], C::TX);
+          const uint32_t fb = ptx::mapa(ptx::smem_u32(&full[stage]), 0);
+          auto ld2 = [&](void* dst, const CUtensorMap* m, int x, int y) {
+            if (TPS_SGD_L2HINT) ptx::tma_load_2d_cg2_hint(dst, m, fb, x, y, pol_keep);
+            else ptx::tma_load_2d_cg2(dst, m, fb, x, y);
+          };
+          if (is_d) {
+            ld2(sA, mA, kb * BK, m0);                                   // G [M, K], K-major
+          } else {
+#pragma unroll
+            for (int i = 0; i < BM / 64; ++i) ld2(sA + i * 8192, mA, m0 + 64 * i, kb * BK);   // stored [K, M]
+          }
+#pragma unroll
+          for (int i = 0; i < BN / CG / 64; ++i) ld2(sB + i * 8192, mB, n0 + 64 * i, kb * BK);  // stored [K, N]
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer (leader CTA) =====================
+    if (lane == 0 && rank == 0) {
+      constexpr uint32_t idesc_w = ptx::make_idesc_bf16(BM * CG, BN, 1, 1);
+      constexpr uint32_t idesc_d = ptx::make_idesc_bf16(BM * CG, BN, 0, 1);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int k = 0; k < len; ++k) {
+        const int acc = k % C::ACC;
+        MBAR_WAIT(2, &tmem_empty[acc], ((k / C::ACC) & 1) ^ 1);
+        ptx::tc_fence_after();
+        bool is_d;
+        int t;
+        at(k, is_d, t);
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        const int nk = is_d ? kd : kw;
+        for (int kb = 0; kb < nk; ++kb) {
+          MBAR_WAIT(3, &full[stage], phase);
+          ptx::tc_fence_after();
+          const uint32_t a_addr = ptx::smem_u32(stages + stage * C::STAGE_BYTES);
+          const uint32_t b_addr = a_addr + A_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            const uint64_t ad = is_d ? ptx::make_sdesc_sw128(a_addr + kk * 32, 16, 1024)
+                                     : ptx::make_sdesc_sw128(a_addr + kk * 2048, 8192, 1024);
+            const uint64_t bd = ptx::make_sdesc_sw128(b_addr + kk * 2048, 8192, 1024);
+            ptx::umma_f16_cg2(d_tmem, ad, bd, is_d ? idesc_d : idesc_w, (kb != 0) || (kk != 0));
+          }
+          ptx::umma_commit_cg2_mc(&empty[stage], 0x3);
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+        ptx::umma_commit_cg2_mc(&tmem_full[acc], 0x3);
+      }
+    }
+  } else if (warp < 2 + SGD_WARPS) {
+    // ===================== epilogue: fused update (W tiles) / masked bf16 store (D tiles) ==========
+    const int e = warp - 2;
+    const int q = warp & 3;
+    uint8_t* ebase = epi_smem + e * (SGD_NB * SGD_BUF);
+    uint64_t* ebar = sgd_bar + e * SGD_NB;
+    constexpr int CW = SGD_CW, ROWB = CW * 4, NCH = BN / CW;
+    constexpr int NW = SGD_WARPS / 4;
+    constexpr int NCHW = NCH / NW;
+    constexpr int NCHD = BN / 32 / NW;                 // 32-column D chunks per warp per tile
+    const int half = e / 4;
+    const bool mom = args.mu != 0.0f;
+    const uint64_t pol_stream = TPS_SGD_L2HINT ? ptx::policy_evict_first() : 0ull;
+    auto swz = [](int row, int ch) { return CW == 32 ? (ch ^ (row & 7)) : (ch ^ ((row >> 1) & 3)); };
+    auto issue = [&](int i) {            // lane 0: TMA loads of this warp's W chunk i (W tiles only)
+      const int ti = i / NCHW, c = half + NW * (i - ti * NCHW);
+      if (ti >= w_c) return;
+      int mb, nb;
+      tile_coords(w0 + ti, wm, wn, mb, nb);
+      const int row0 = mb * BM * CG + static_cast<int>(rank) * BM + q * 32;
+      const int col0 = nb * BN + c * CW;
+      const int buf = i % SGD_NB;
+      uint8_t* w_s = ebase + buf * SGD_BUF;
+      ptx::mbar_expect_tx(&ebar[buf], mom ? 2u * SGD_WBYTES : 1u * SGD_WBYTES);
+      if (TPS_SGD_L2HINT) {
+        ptx::tma_load_2d_hint(w_s, &tmW, &ebar[buf], col0, row0, pol_stream);
+        if (mom) ptx::tma_load_2d_hint(w_s + SGD_WBYTES, &tmV, &ebar[buf], col0, row0, pol_stream);
+      } else {
+        ptx::tma_load_2d(w_s, &tmW, &ebar[buf], col0, row0);
+        if (mom) ptx::tma_load_2d(w_s + SGD_WBYTES, &tmV, &ebar[buf], col0, row0);
+      }
+    };
+    if (lane == 0)
+      for (int i = 0; i < SGD_NB; ++i) issue(i);
+    int i = 0;
+    for (int k = 0; k < len; ++k) {
+      bool is_d;
+      int t, mb, nb;
+      at(k, is_d, t);
+      tile_coords(t, is_d ? dm : wm, is_d ? dn : wn, mb, nb);
+      const int acc = k % C::ACC;
+      MBAR_WAIT(5, &tmem_full[acc], (k / C::ACC) & 1);
+      ptx::tc_fence_after();
+      const int row0 = mb * BM * CG + static_cast<int>(rank) * BM + q * 32;
+      if (is_d) {
+        // ---- input gradient: α, ReLU mask, bf16 store (thread = row, as gemm_kernel's epilogue)
+#pragma unroll 1
+        for (int ci = 0; ci < NCHD; ++ci) {
+          const int c = half + NW * ci;
+          uint32_t r[32];
+          ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c * 32, r);
+          ptx::tmem_ld_wait();
+          if (ci == NCHD - 1) {
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive_remote(ptx::mapa(ptx::smem_u32(&tmem_empty[acc]), 0));
+          }
+          const int grow = row0 + lane;
+          const int gcol = nb * BN + c * 32;
+          if (gcol < dg.N && grow < dg.M) {     // (rows past M: lane-divergent, reconverges below)
+          const int nchunk = min(4, (dg.N - gcol) >> 3);
+          float v[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+          if (dg.alpha != 1.0f) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = __fmul_rn(v[j], dg.alpha);
+          }
+          if (dg.mask) {
+            const uint4* mp = reinterpret_cast<const uint4*>(dg.mask + static_cast<size_t>(grow) * dg.ldm + gcol);
+#pragma unroll
+            for (int ch = 0; ch < 4; ++ch) {
+              if (ch < nchunk) {
+                const uint4 mv = __ldg(mp + ch);
+                const uint32_t w[4] = {mv.x, mv.y, mv.z, mv.w};
+#pragma unroll
+                for (int e2 = 0; e2 < 8; ++e2) {
+                  const uint32_t h = (w[e2 >> 1] >> ((e2 & 1) * 16)) & 0xFFFFu;
+                  const bool pos = ((h & 0x8000u) == 0u) && ((h & 0x7FFFu) != 0u);
+                  if (!pos) v[ch * 8 + e2] = 0.0f;
+                }
+              }
+            }
+          }
+          __nv_bfloat16* op = reinterpret_cast<__nv_bfloat16*>(dg.out) + static_cast<size_t>(grow) * dg.ldo + gcol;
+#pragma unroll
+          for (int ch = 0; ch < 4; ++ch) {
+            if (ch < nchunk) {
+              uint4 o;
+              o.x = pack_bf16(v[ch * 8 + 0], v[ch * 8 + 1]);
+              o.y = pack_bf16(v[ch * 8 + 2], v[ch * 8 + 3]);
+              o.z = pack_bf16(v[ch * 8 + 4], v[ch * 8 + 5]);
+              o.w = pack_bf16(v[ch * 8 + 6], v[ch * 8 + 7]);
+              reinterpret_cast<uint4*>(op)[ch] = o;
+            }
+          }
+          }   // live
+          __syncwarp();
+        }
+        continue;
+      }
+      // ---- weight gradient: the fused SGD/momentum update (as gemm_kernel's SGD epilogue)
+#pragma unroll 1
+      for (int ci = 0; ci < NCHW; ++ci, ++i) {
+        const int c = half + NW * ci;
+        uint32_t r[CW];
+        if constexpr (CW == 32)
+          ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c * CW,
+                                  *reinterpret_cast<uint32_t(*)[32]>(r));
+        else
+          ptx::tmem_ld_32x32b_x16(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c * CW,
+                                  *reinterpret_cast<uint32_t(*)[16]>(r));
+        ptx::tmem_ld_wait();
+        if (ci == NCHW - 1) {
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive_remote(ptx::mapa(ptx::smem_u32(&tmem_empty[acc]), 0));
+        }
+        const int buf = i % SGD_NB;
+        MBAR_WAIT(6, &ebar[buf], (i / SGD_NB) & 1);
+        uint8_t* w_s = ebase + buf * SGD_BUF;
+        float4* wrow = reinterpret_cast<float4*>(w_s + lane * ROWB);
+        float4* vrow = reinterpret_cast<float4*>(w_s + SGD_WBYTES + lane * ROWB);
+#pragma unroll
+        for (int j = 0; j < CW / 4; ++j) {
+          const int pos = swz(lane, j);
+          float4 wv = wrow[pos];
+          float4 vv = mom ? vrow[pos] : make_float4(0.f, 0.f, 0.f, 0.f);
+          float* wp = &wv.x;
+          float* vp = &vv.x;
+#pragma unroll
+          for (int k2 = 0; k2 < 4; ++k2) {
+            const float g = __uint_as_float(r[4 * j + k2]);
+            const float gp = __fadd_rn(g, __fmul_rn(args.wd, wp[k2]));
+            float upd = gp;
+            if (mom) {
+              vp[k2] = __fadd_rn(__fmul_rn(args.mu, vp[k2]), gp);
+              upd = vp[k2];
+            }
+            wp[k2] = __fsub_rn(wp[k2], __fmul_rn(args.lr, upd));
+          }
+          wrow[pos] = wv;
+          if (mom) vrow[pos] = vv;
+        }
+        __syncwarp();
+        const int col0 = nb * BN + c * CW;
+        const size_t ld = static_cast<size_t>(args.ldo);
+        constexpr int LPR = CW / 4;
+#pragma unroll
+        for (int k2 = 0; k2 < 32 / (32 / LPR); ++k2) {
+          const int rr = (32 / LPR) * k2 + lane / LPR, ch = lane % LPR;
+          const int pos = swz(rr, ch);
+          const int grow = row0 + rr, gcol = col0 + ch * 4;
+          const float4 wv = *reinterpret_cast<const float4*>(w_s + rr * ROWB + pos * 16);
+          float4 vv;
+          if (mom) vv = *reinterpret_cast<const float4*>(w_s + SGD_WBYTES + rr * ROWB + pos * 16);
+          if (grow < args.M && gcol < args.N) {
+            __stcs(reinterpret_cast<float4*>(args.w + grow * ld + gcol), wv);
+            if (mom) __stcs(reinterpret_cast<float4*>(args.v + grow * ld + gcol), vv);
+            *reinterpret_cast<uint2*>(args.ver + grow * ld + gcol) =
+                make_uint2(pack_bf16(wv.x, wv.y), pack_bf16(wv.z, wv.w));
+          }
+        }
+        ptx::fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) issue(i + SGD_NB);
+        __syncwarp();
+      }
+    }
+  }
+
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_relinquish_cg2();
+    ptx::tmem_dealloc_cg2(tmem_base, C::TMEM_COLS);
   }
 }
 
@@ -1188,6 +1532,58 @@ cudaError_t gemm_run(int mode, const GemmOperands& op, const GemmArgs& args_in, 
   const int blocks = static_cast<int>(std::min<int64_t>((n4 + 255) / 256, static_cast<int64_t>(num_sms()) * 8));
   splitk_reduce<<<blocks, 256, 0, st>>>(reinterpret_cast<const float4*>(args.ws), reinterpret_cast<float4*>(args.out),
                                         n4, tl.splits);
+  return cudaGetLastError();
+}
+
+cudaError_t gemm_bwd_dual(const GemmOperands& opw, const GemmArgs& aw_in, const GemmOperands& opd, const DualArgs& dg,
+                          cudaStream_t st) {
+  constexpr int BN = 256, CG = 2;
+  using C = Cfg<BN, 0, 1, CG>;
+  GemmArgs aw = aw_in;
+  if (aw.epi != EPI_SGD || aw.M < BM * CG || dg.M < BM * CG || aw.N <= BN / 2 || dg.N <= BN / 2 || aw.K <= 0 ||
+      dg.K <= 0 || (dg.N & 7) || (aw.N & 7))
+    return cudaErrorNotSupported;
+  const int n_w = ((aw.M + BM * CG - 1) / (BM * CG)) * ((aw.N + BN - 1) / BN);
+  const int n_d = ((dg.M + BM * CG - 1) / (BM * CG)) * ((dg.N + BN - 1) / BN);
+  const int kw = (aw.K + BK - 1) / BK, kd = (dg.K + BK - 1) / BK;
+  const int ncl = std::min(num_sms() / CG, n_w + n_d);
+  // the closed-form split must hand every W tile to exactly one pair (monotone prefix)
+  for (int c = 0; c < ncl; ++c)
+    if (dual_wpre(c + 1, n_d, n_w, kd, kw, ncl) < dual_wpre(c, n_d, n_w, kd, kw, ncl)) return cudaErrorNotSupported;
+  if (dual_wpre(ncl, n_d, n_w, kd, kw, ncl) != n_w) return cudaErrorNotSupported;
+  aw.splits = 1;
+  aw.kper = kw;
+  CUtensorMap ta, tb, tda, tdb, tw, tv;
+  bool ok = make_tmap(&ta, opw.A, aw.K, aw.M, opw.lda, 64) && make_tmap(&tb, opw.B, aw.K, aw.N, opw.ldb, 64) &&
+            make_tmap(&tda, opd.A, dg.M, dg.K, opd.lda, BM) && make_tmap(&tdb, opd.B, dg.K, dg.N, opd.ldb, 64);
+  const CUtensorMapSwizzle wsw = SGD_CW == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
+  ok = ok && make_tmap_box(&tw, aw.w, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, aw.M, aw.N, aw.ldo, SGD_CW, 32, wsw);
+  if (aw.mu != 0.0f)
+    ok = ok && make_tmap_box(&tv, aw.v, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, aw.M, aw.N, aw.ldo, SGD_CW, 32, wsw);
+  else
+    tv = tw;
+  if (!ok) return cudaErrorInvalidValue;
+  auto kern = bwd_dual_kernel<BN, CG>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(ncl * CG);
+  cfg.blockDim = dim3(C::THREADS);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tb, tda, tdb, tw, tv, aw, dg);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 

@@ -217,6 +217,7 @@ struct tps_pipeline {
   // own stream s_w, concurrent with the next layer's input gradient; three rotating gradient
   // buffers (each dgrad waits for the weight gradient / bias step two layers up)
   bool split_w = false;
+  bool dual = false;    // split backward: layer k's wgrad + update and layer k-1's dgrad in one launch
   cudaStream_t s_w = nullptr;
   int nsm = 148, part_dgrad = 0;   // SMs of a concurrent (dgrad, wgrad+update) pair given to the dgrad
   std::vector<cudaEvent_t> ev_dg, ev_w_done, ev_bias_l;   // per layer
@@ -255,8 +256,8 @@ struct tps_pipeline {
   bool profiling = false;
   std::vector<TimedLaunch> timed;
   std::vector<cudaEvent_t> ev_pool;
-  double stat_ms[5] = {0, 0, 0, 0, 0}, stat_work[5] = {0, 0, 0, 0, 0};
-  int64_t stat_n[5] = {0, 0, 0, 0, 0};
+  double stat_ms[6] = {0, 0, 0, 0, 0, 0}, stat_work[6] = {0, 0, 0, 0, 0, 0};
+  int64_t stat_n[6] = {0, 0, 0, 0, 0, 0};
   int64_t launches = 0;
   bool poisoned = false;
   // ---- per-event device timeline (tps_set_timeline; Chrome trace) and NVTX ranges (TPS_NVTX=1)
@@ -376,6 +377,39 @@ tps_status run_gemm(tps_pipeline* p, int mode, const tps::GemmOperands& op, cons
   return TPS_OK;
 }
 
+// the dual backward launch (gemm_bwd_dual); *done = false when the shapes do not suit it
+tps_status run_dual(tps_pipeline* p, const tps::GemmOperands& opw, const tps::GemmArgs& aw,
+                    const tps::GemmOperands& opd, const tps::DualArgs& dg, bool* done) {
+  TimedLaunch tl{};
+  if (p->profiling) {
+    if (p->ev_pool.size() < 2) {
+      for (int i = 0; i < 64; ++i) {
+        cudaEvent_t e;
+        CUDA_OK(cudaEventCreate(&e));
+        p->ev_pool.push_back(e);
+      }
+    }
+    tl.kind = 5;
+    tl.work = gemm_flops(aw.M, aw.N, aw.K) + gemm_flops(dg.M, dg.N, dg.K);
+    tl.a = p->ev_pool.back(); p->ev_pool.pop_back();
+    tl.b = p->ev_pool.back(); p->ev_pool.pop_back();
+    CUDA_OK(cudaEventRecord(tl.a, p->cs));
+  }
+  const cudaError_t e = tps::gemm_bwd_dual(opw, aw, opd, dg, p->cs);
+  *done = e == cudaSuccess;
+  if (e == cudaErrorNotSupported) {
+    if (p->profiling) { p->ev_pool.push_back(tl.a); p->ev_pool.push_back(tl.b); }
+    return TPS_OK;
+  }
+  CUDA_OK(e);
+  p->launches += 1;
+  if (p->profiling) {
+    CUDA_OK(cudaEventRecord(tl.b, p->cs));
+    p->timed.push_back(tl);
+  }
+  return TPS_OK;
+}
+
 tps_status time_begin(tps_pipeline* p, TimedLaunch* tl, int kind, double work, cudaStream_t st = nullptr) {
   if (!p->profiling) return TPS_OK;
   if (p->ev_pool.size() < 2) {
@@ -406,7 +440,7 @@ tps_status drain_timing(tps_pipeline* p) {
     CUDA_OK(cudaEventElapsedTime(&ms, t.a, t.b));
     const int k = t.kind;
     p->stat_ms[k] += ms; p->stat_work[k] += t.work; p->stat_n[k] += 1;
-    if (k <= 2) { p->stat_ms[3] += ms; p->stat_work[3] += t.work; p->stat_n[3] += 1; }
+    if (k <= 2 || k == 5) { p->stat_ms[3] += ms; p->stat_work[3] += t.work; p->stat_n[3] += 1; }
     p->ev_pool.push_back(t.a);
     p->ev_pool.push_back(t.b);
   }
@@ -1072,6 +1106,40 @@ tps_status do_backward(tps_pipeline* p, int64_t j, int staleness) {
   const bool blend_on_load = p->variant == TPS_I && delta > 0 && (p->blend == TPS_BLEND_CONVEX || p->eq1_on_load);
   for (Layer& L : p->layers) { L.bias_part = nullptr; L.bias_groups = 0; }
   if (p->graph) TPS_TRY(graph_backward(p, j, v_used, vl, vn, alpha, beta, blend_on_load, G));
+  // dual launches (p->dual): layer k's fused wgrad + update is held back and issued together with
+  // layer k-1's input gradient (independent: different layers' weights, distinct gradient buffers
+  // of the three-way rotation), on the compute stream
+  struct PendingW {
+    int k = -1;
+    tps::GemmOperands op{};
+    tps::GemmArgs ga{};
+    bool bias_side = false;
+  } pend;
+  // a plain Linear input gradient of layer kk that can share a launch
+  auto dgrad_pairable = [&](int kk) {
+    if (kk < 0 || !p->dual || blend_on_load || p->part_dgrad > 0 || p->bpart[0]) return false;
+    const Layer& L = p->layers[kk];
+    return L.gidx > 0 && L.kind == TPS_LAYER_LINEAR;
+  };
+  // events that follow layer kk's fused wgrad + update on the split backward (stream st)
+  auto finish_w = [&](int kk, bool bside, cudaStream_t st) -> tps_status {
+    CUDA_OK(cudaEventRecord(p->ev_w_done[kk], st));
+    if (bside) {
+      CUDA_OK(cudaStreamWaitEvent(p->s_upd, p->ev_w_done[kk], 0));
+      CUDA_OK(cudaEventRecord(p->ev_upd_done[kk], p->s_upd));
+    } else {
+      CUDA_OK(cudaEventRecord(p->ev_bias_l[kk], p->cs));   // bias ran on the compute stream
+      CUDA_OK(cudaEventRecord(p->ev_upd_done[kk], st));
+    }
+    return TPS_OK;
+  };
+  auto flush_pending = [&]() -> tps_status {   // issue a held-back wgrad + update on its own
+    if (pend.k < 0) return TPS_OK;
+    TPS_TRY(run_gemm(p, tps::GEMM_WGRAD, pend.op, pend.ga, 2, p->cs));
+    TPS_TRY(finish_w(pend.k, pend.bias_side, p->cs));
+    pend.k = -1;
+    return TPS_OK;
+  };
   for (int k = (p->graph ? -1 : nl - 1); k >= 0; --k) {
     Layer& Lk = p->layers[k];
     // the previous update of this layer must be done: it reads dW / db (rewritten below) and,
@@ -1128,6 +1196,7 @@ tps_status do_backward(tps_pipeline* p, int64_t j, int staleness) {
         CUDA_OK(cudaStreamWaitEvent(p->cs, p->ev_bwd_sent[j & 1], 0));  // gout of mb j-2 has left
         dst = p->gout[j & 1];
       }
+      if (!dgrad_pairable(k)) TPS_TRY(flush_pending());
       if (Lk.kind == TPS_LAYER_MAXPOOL2) {
         // gradient to the first window maximum; the ReLU mask was applied by the layer above
         CUDA_OK(tps::launch_maxpool2_bwd(X, G, dst, B, Lk.H, Lk.Wd, Lk.Ci, p->cs));
@@ -1160,7 +1229,19 @@ tps_status do_backward(tps_pipeline* p, int64_t j, int staleness) {
           TPS_TRY(run_gemm(p, conv ? tps::GEMM_CONV_DGRAD_BLEND : tps::GEMM_DGRAD_BLEND, op, ga, 1));
         } else {
           ga.alpha = (p->variant == TPS_I) ? alpha : 1.f;   // EQ1: α·(G·W_stash) = G·(α·W_stash)
-          TPS_TRY(run_gemm(p, conv ? tps::GEMM_CONV_DGRAD : tps::GEMM_DGRAD, op, ga, 1));
+          bool done = false;
+          if (pend.k == k + 1 && dgrad_pairable(k) && !ga.colsum) {
+            tps::DualArgs dg{ga.M, ga.N, ga.K, ga.alpha, ga.out, ga.ldo, ga.mask, ga.ldm};
+            TPS_TRY(run_dual(p, pend.op, pend.ga, op, dg, &done));
+            if (done) {
+              TPS_TRY(finish_w(pend.k, pend.bias_side, p->cs));
+              pend.k = -1;
+            }
+          }
+          if (!done) {
+            TPS_TRY(flush_pending());
+            TPS_TRY(run_gemm(p, conv ? tps::GEMM_CONV_DGRAD : tps::GEMM_DGRAD, op, ga, 1));
+          }
         }
       }
     }
@@ -1186,12 +1267,20 @@ tps_status do_backward(tps_pipeline* p, int64_t j, int staleness) {
       if (p->split_w && p->part_dgrad > 0 && k > 0 && p->layers[k - 1].gidx > 0 &&
           p->layers[k - 1].kind != TPS_LAYER_MAXPOOL2)
         ga.max_ctas = p->nsm - p->part_dgrad;
-      if (p->split_w) {   // after this layer's dgrad (it reads the weights the fused update rewrites)
+      TPS_TRY(flush_pending());   // (a held-back update of layer k+1 whose dgrad partner did not come)
+      const bool defer = p->dual && p->dp == 1 && Lk.kind == TPS_LAYER_LINEAR && ga.max_ctas == 0 &&
+                         dgrad_pairable(k - 1);
+      if (p->split_w && !defer) {   // after this layer's dgrad (it reads the weights the fused update rewrites)
         CUDA_OK(cudaEventRecord(p->ev_dg[k], p->cs));
         CUDA_OK(cudaStreamWaitEvent(p->s_w, p->ev_dg[k], 0));
         ws = p->s_w;
       }
-      if (Lk.kind == TPS_LAYER_CONV3X3 && !Lk.im2col) {
+      if (defer) {
+        pend.k = k;
+        pend.op = tps::GemmOperands{G, Lk.Np, X, Lk.Kp, nullptr};
+        pend.ga = ga;
+        pend.bias_side = bias_side;
+      } else if (Lk.kind == TPS_LAYER_CONV3X3 && !Lk.im2col) {
         tps::GemmOperands op{G, Lk.Np, X, 0, nullptr};
         op.cv = tps::ConvGeom{B, Lk.H, Lk.Wd, Lk.Ci};
         TPS_TRY(run_gemm(p, tps::GEMM_CONV_WGRAD, op, ga, 2, ws));
@@ -1199,7 +1288,7 @@ tps_status do_backward(tps_pipeline* p, int64_t j, int staleness) {
         tps::GemmOperands op{G, Lk.Np, X, Lk.Kp, nullptr};
         TPS_TRY(run_gemm(p, tps::GEMM_WGRAD, op, ga, 2, ws));
       }
-      if (p->split_w) CUDA_OK(cudaEventRecord(p->ev_w_done[k], p->s_w));
+      if (p->split_w && !defer) CUDA_OK(cudaEventRecord(p->ev_w_done[k], p->s_w));
       if (!bias_side) {   // bias gradient and the bias's SGD/momentum step in one launch
         // (data parallel: the gradient only; the step runs on the replica average below)
         if (Lk.bias_part)
@@ -1228,7 +1317,9 @@ tps_status do_backward(tps_pipeline* p, int64_t j, int staleness) {
         TPS_TRY(time_end(p, &tl, us));
         p->launches += 1;
       }
-      if (p->split_w) {
+      if (defer) {
+        // events follow the shared launch (finish_w) or flush_pending
+      } else if (p->split_w) {
         // parameters final once the fused wgrad+update (s_w) and the bias step are done
         if (bias_side) {
           CUDA_OK(cudaStreamWaitEvent(p->s_upd, p->ev_w_done[k], 0));
@@ -1250,6 +1341,7 @@ tps_status do_backward(tps_pipeline* p, int64_t j, int staleness) {
     }
     if (dst) G = dst;
   }
+  TPS_TRY(flush_pending());
   if (p->split_w) {
     // the weight gradients read this mini-batch's stashed activations and the gradients: join
     for (int k = 0; k < nl; ++k) {
@@ -1844,6 +1936,12 @@ tps_status tps_pipeline_init(const tps_config* c, tps_pipeline** out) {
     // default on (C5: +9.5 % A/B); TPS_SPLIT_W=0 keeps every backward kernel on the compute stream
     const char* e = std::getenv("TPS_SPLIT_W");
     p->split_w = !(e && e[0] == '0') && p->fuse_update && !p->graph && nl > 1;
+  }
+  {
+    // default on: the split backward's wgrad + update of layer k and dgrad of layer k-1 share one
+    // persistent launch (gemm_bwd_dual); TPS_DUAL=0 launches them separately on two streams
+    const char* e = std::getenv("TPS_DUAL");
+    p->dual = p->split_w && !(e && e[0] == '0');
   }
   if (p->split_w && (st = alloc_t(p, &p->gwork[2], static_cast<size_t>(p->B) * max_elems, &p->mem_acts)) != TPS_OK)
     return cleanup(st);
@@ -2736,7 +2834,7 @@ tps_status tps_set_profiling(tps_pipeline* p, int32_t enable) {
   TPS_TRY(sync_streams(p));
   TPS_TRY(drain_timing(p));
   p->profiling = enable != 0;
-  for (int k = 0; k < 5; ++k) { p->stat_ms[k] = 0; p->stat_work[k] = 0; p->stat_n[k] = 0; }
+  for (int k = 0; k < 6; ++k) { p->stat_ms[k] = 0; p->stat_work[k] = 0; p->stat_n[k] = 0; }
   return TPS_OK;
 }
 
@@ -2772,7 +2870,7 @@ tps_status tps_get_timeline(tps_pipeline* p, tps_timeline_rec* out, int64_t cap,
 
 tps_status tps_kernel_stats(tps_pipeline* p, int32_t which, int64_t* launches, double* ms, double* work) {
   TPS_TRY(check_usable(p));
-  if (which < 0 || which > 4) return fail(TPS_E_INVALID_ARG, "bad kernel class");
+  if (which < 0 || which > 5) return fail(TPS_E_INVALID_ARG, "bad kernel class");
   TPS_TRY(sync_streams(p));
   TPS_TRY(drain_timing(p));
   if (launches) *launches = p->stat_n[which];
@@ -3026,6 +3124,28 @@ tps_status tps_gemm_wgrad_sgd(int32_t M, int32_t N, int32_t K, const void* A, in
   ga.epi = tps::EPI_SGD; ga.w = w; ga.v = v; ga.ver = static_cast<uint16_t*>(ver);
   ga.lr = lr; ga.mu = mu; ga.wd = wd;
   CUDA_OK(tps::gemm_run(tps::GEMM_WGRAD, op, ga, reinterpret_cast<cudaStream_t>(stream)));
+  return TPS_OK;
+}
+
+tps_status tps_gemm_bwd_dual(int32_t M, int32_t N, int32_t K, const void* A, int32_t lda, const void* B, int32_t ldb,
+                             float* w, float* v, void* ver, int32_t ldw, float lr, float mu, float wd, int32_t Md,
+                             int32_t Nd, int32_t Kd, const void* Ad, int32_t ldad, const void* Bd, int32_t ldbd,
+                             void* outd, int32_t ldod, float alpha, const void* mask, int32_t ldm, uint64_t stream) {
+  if (M < 1 || N < 1 || K < 1 || !A || !B || !w || !ver || (mu != 0.f && !v)) return fail(TPS_E_INVALID_ARG, "bad operands");
+  if (Md < 1 || Nd < 1 || Kd < 1 || !Ad || !Bd || !outd) return fail(TPS_E_INVALID_ARG, "bad input-gradient operands");
+  if (N % 8 || lda % 8 || ldb % 8 || ldw % 8 || Nd % 8 || ldad % 8 || ldbd % 8 || ldod % 8 || (mask && ldm % 8))
+    return fail(TPS_E_INVALID_ARG, "N and leading dims must be multiples of 8");
+  TPS_TRY(op_prologue());
+  tps::GemmOperands opw{A, lda, B, ldb, nullptr};
+  tps::GemmArgs ga{};
+  ga.M = M; ga.N = N; ga.K = K; ga.ldo = ldw; ga.out_f32 = 1; ga.alpha = 1.f; ga.xa = 1.f;
+  ga.epi = tps::EPI_SGD; ga.w = w; ga.v = v; ga.ver = static_cast<uint16_t*>(ver);
+  ga.lr = lr; ga.mu = mu; ga.wd = wd;
+  tps::GemmOperands opd{Ad, ldad, Bd, ldbd, nullptr};
+  tps::DualArgs dg{Md, Nd, Kd, alpha, outd, ldod, static_cast<const uint16_t*>(mask), ldm};
+  const cudaError_t e = tps::gemm_bwd_dual(opw, ga, opd, dg, reinterpret_cast<cudaStream_t>(stream));
+  if (e == cudaErrorNotSupported) return fail(TPS_E_UNSUPPORTED, "shapes unsuited to the dual launch");
+  CUDA_OK(e);
   return TPS_OK;
 }
 

@@ -36,6 +36,7 @@ EXPORTS = [
     "tps_pool_op", "tps_conv2d_gemm", "tps_debug_progress", "tps_memory_observed", "tps_join", "tps_ipc_export", "tps_ipc_connect",
     "tps_dp_export", "tps_dp_connect", "tps_gemm_wgrad_sgd", "tps_graph_capture", "tps_graph_replay",
     "tps_graph_destroy", "tps_read_losses_async", "tps_set_timeline", "tps_get_timeline",
+    "tps_gemm_bwd_dual",
 ]
 TPS_LAYER_LINEAR, TPS_LAYER_CONV3X3, TPS_LAYER_MAXPOOL2 = 0, 1, 2
 TPS_LAYER_CONV, TPS_LAYER_BN, TPS_LAYER_MAXPOOL3, TPS_LAYER_AVGPOOL = 3, 4, 5, 6
@@ -162,6 +163,8 @@ def lib() -> C.CDLL:
             "tps_ipc_export": (I32, [P, P, I64, C.POINTER(I64)]),
             "tps_ipc_connect": (I32, [P, P, P]),
             "tps_gemm_wgrad_sgd": (I32, [I32, I32, I32, P, I32, P, I32, P, P, P, I32, F, F, F, U64]),
+            "tps_gemm_bwd_dual": (I32, [I32, I32, I32, P, I32, P, I32, P, P, P, I32, F, F, F,
+                                        I32, I32, I32, P, I32, P, I32, P, I32, F, P, I32, U64]),
             "tps_graph_capture": (I32, [C.POINTER(P), I32, I64, I64, P, P, I32, U64, C.POINTER(P)]),
             "tps_graph_replay": (I32, [P]),
             "tps_graph_destroy": (I32, [P]),
@@ -225,6 +228,14 @@ def gemm(mode, M, N, K, A, lda, B, ldb, out, ldo, out_f32=0, bias=None, relu=0, 
 def gemm_wgrad_sgd(M, N, K, A, lda, B, ldb, w, v, ver, ldw, lr, mu, wd=0.0, stream: int = 0) -> None:
     check(lib().tps_gemm_wgrad_sgd(M, N, K, ptr(A), lda, ptr(B), ldb, ptr(w), ptr(v), ptr(ver), ldw, lr, mu, wd,
                                    stream))
+
+
+def gemm_bwd_dual(M, N, K, A, lda, B, ldb, w, v, ver, ldw, lr, mu, wd, Md, Nd, Kd, Ad, ldad, Bd, ldbd, outd, ldod,
+                  alpha=1.0, mask=None, ldm=0, stream: int = 0) -> None:
+    """One launch: gemm_wgrad_sgd(M, N, K, ...) and the masked input gradient outd = α·Ad·Bd (mode 1)."""
+    check(lib().tps_gemm_bwd_dual(M, N, K, ptr(A), lda, ptr(B), ldb, ptr(w), ptr(v), ptr(ver), ldw, lr, mu, wd,
+                                  Md, Nd, Kd, ptr(Ad), ldad, ptr(Bd), ldbd, ptr(outd), ldod, alpha, ptr(mask), ldm,
+                                  stream))
 
 
 def conv_gemm(mode, N, H, W, Ci, Co, A, Wt, out, out_f32=0, bias=None, relu=0, alpha=1.0, beta=0.0, mask=None,

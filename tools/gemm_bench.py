@@ -49,6 +49,16 @@ def main():
     vm = torch.zeros(N, N, device="cuda")
     qm = torch.empty(N, N, device="cuda", dtype=torch.bfloat16)
     fl = 2.0 * M * N * K
+    # dual: the fused wgrad + update above together with a dgrad of the same size (one launch)
+    Gd = torch.randn(M, N, device="cuda").to(torch.bfloat16)
+    Wd = (torch.randn(N, N, device="cuda") * N ** -0.5).to(torch.bfloat16)
+    od = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    maskd = torch.randn(M, N, device="cuda").to(torch.bfloat16)
+
+    def sep():
+        tps.gemm_wgrad_sgd(N, N, M, G4, N, X4, N, wm, vm, qm, N, 1e-9, 0.9)
+        tps.gemm(1, M, N, N, Gd, N, Wd, N, od, N, 0, None, 0, 0.9, 0.0, maskd, N)
+
     runs = {
         0: ("fwd  (K-major A,B; bias+ReLU)", lambda: tps.gemm(0, M, N, K, X, K, W, K, ob, N, 0, bias, 1)),
         1: ("dgrad(MN-major B; α, mask)", lambda: tps.gemm(1, M, N, K, X, K, Wt, N, ob, N, 0, None, 0, 0.9, 0.0, mask, N)),
@@ -56,15 +66,21 @@ def main():
         3: ("dgrad blend-on-load", lambda: tps.gemm(3, M, N, K, X, K, Wt, N, ob, N, 0, None, 0, 0.7, 0.3, mask, N, B2=W2)),
         4: ("wgrad + fused SGD/momentum update", lambda: tps.gemm_wgrad_sgd(N, N, M, G4, N, X4, N, wm, vm, qm, N,
                                                                            1e-9, 0.9)),
+        5: ("dual: wgrad+update & dgrad, one launch", lambda: tps.gemm_bwd_dual(
+            N, N, M, G4, N, X4, N, wm, vm, qm, N, 1e-9, 0.9, 0.0, M, N, N, Gd, N, Wd, N, od, N, 0.9, maskd, N)),
+        6: ("the same two as separate launches", sep),
     }
     for m in [int(x) for x in a.modes.split(",")]:
         name, fn = runs[m]
         ms = timeit(fn, a.iters)
         extra = ""
+        f = fl
         if m == 4:   # HBM roofline of the fused kernel: operands + 18 B per parameter (w, v r/w + bf16 version)
             by = 2.0 * (M * N + M * N) + 18.0 * N * N
             extra = f"  {by / ms / 1e6:7.1f} GB/s algorithmic ({by / 1e6:.1f} MB)"
-        print(f"mode {m} {name:34s} {M}x{N}x{K}: {ms*1e3:8.1f} us  {fl/ms/1e9:7.1f} TFLOP/s{extra}", flush=True)
+        if m in (5, 6):
+            f = 2.0 * M * N * N * 2
+        print(f"mode {m} {name:34s} {M}x{N}x{K}: {ms*1e3:8.1f} us  {f/ms/1e9:7.1f} TFLOP/s{extra}", flush=True)
     ms = timeit(lambda: torch.matmul(X, W.T), a.iters)
     print(f"cuBLAS torch.matmul bf16 {M}x{N}x{K}: {ms*1e3:8.1f} us  {fl/ms/1e9:7.1f} TFLOP/s")
 
