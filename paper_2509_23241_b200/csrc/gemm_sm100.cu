@@ -92,24 +92,29 @@ constexpr int SGD_WBYTES = 32 * SGD_CW * 4;                 // one 32-row chunk 
 constexpr int SGD_BUF = 2 * SGD_WBYTES + (TPS_SGD_STG ? 0 : 32 * 32 * 2);
 constexpr int XF_WARPS = 8;                                // BLEND operand transform warps
 
-template <int BN, int BLEND, int SGD = 0, int CG = 1>
+// MH = 2 (BLEND on CTA pairs): each CTA stages TWO 128-row A blocks per K step and the pair
+// computes a 512 x BN tile as two 256 x BN accumulators that share one blended B tile, so the
+// blend's shared-memory passes (stash + latest read, blend written) are spread over twice the MMA
+// work.  Single accumulator buffer (2·BN·MH = all 512 TMEM columns).
+template <int BN, int BLEND, int SGD = 0, int CG = 1, int MH = 1>
 struct Cfg {
+  static_assert(MH == 1 || (MH == 2 && !SGD && CG == 2 && BN == 256), "MH = 2: plain epilogue, CTA pairs, BN 256");
   static constexpr int NEPI = SGD ? SGD_WARPS : EPI_WARPS;            // epilogue warps
   // fused-update buffers (SGD = 1: TMA-fed shared-memory chunks; SGD = 2: register-staged, none)
   static constexpr int EPI = SGD ? SGD_WARPS * SGD_NB * SGD_BUF : 0;  // fused-update buffers
   static constexpr int B_BYTES = (BN / CG) * BK * 2;   // this CTA's share of the B tile
-  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES * (BLEND ? 2 : 1);
+  static constexpr int STAGE_BYTES = A_BYTES * MH + B_BYTES * (BLEND ? 2 : 1);
   static constexpr int STAGES_RAW = (SMEM_BUDGET - 2048 - EPI) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr int THREADS = 32 * (2 + NEPI + (BLEND ? XF_WARPS : 0));
   // accumulator stages in TMEM: the fused-update variant keeps up to 4 so the MMAs can run
   // several tiles ahead of its HBM-bound epilogue
-  static constexpr int ACC = (SGD && 512 / BN >= 4) ? 4 : 2;
-  static constexpr int TMEM_COLS = ACC * BN;
+  static constexpr int ACC = MH == 2 ? 1 : ((SGD && 512 / BN >= 4) ? 4 : 2);
+  static constexpr int TMEM_COLS = ACC * BN * MH;
   static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + 1024 + EPI;   // ring | barriers | epilogue
   // bytes the leader's full barrier waits for per stage: both CTAs' A (and, without BLEND, B)
   // land on it; with BLEND each CTA counts its own stash + latest B tiles on its own barrier
-  static constexpr uint32_t TX = A_BYTES * CG + (BLEND ? 2 * B_BYTES : B_BYTES * CG);
+  static constexpr uint32_t TX = A_BYTES * MH * CG + (BLEND ? 2 * B_BYTES : B_BYTES * CG);
 };
 
 __device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int& mb, int& nb) {
@@ -176,16 +181,17 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 #define MBAR_WAIT(tag, bar, par) ptx::mbar_wait((bar), (par))
 #endif
 
-template <int BN, int A_MN, int B_MN, int BLEND, int SGD, int CG, int CONV>
-__global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
+template <int BN, int A_MN, int B_MN, int BLEND, int SGD, int CG, int CONV, int MH = 1>
+__global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG, MH>::THREADS, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmB2, const __grid_constant__ CUtensorMap tmW,
                 const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmQ, const GemmArgs args) {
   // CG = 2: a cluster of two CTAs on one TPC computes a 256 x BN tile with one
   // tcgen05.mma.cta_group::2 stream issued by the leader; each CTA stages its own 128 rows
   // of A and half of the B tile, so per-SM operand traffic drops by a third.
-  using C = Cfg<BN, BLEND, SGD, CG>;
+  using C = Cfg<BN, BLEND, SGD, CG, MH>;
   static_assert(CG == 1 || BN / CG >= 64, "pair mode: >= 64 B columns per CTA");
+  constexpr int MROWS = BM * CG * MH;                 // output rows per tile
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1 KiB alignment by pointer arithmetic on the __shared__ array itself, so every derived
   // pointer keeps the shared address space (LDS/STS rather than generic LD/ST)
@@ -204,7 +210,7 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
   const int lane = threadIdx.x & 31;
   const uint32_t rank = CG == 2 ? ptx::cluster_rank() : 0;
   const int cid = blockIdx.x / CG, ncl = gridDim.x / CG;
-  const int num_m = (args.M + BM * CG - 1) / (BM * CG);
+  const int num_m = (args.M + MROWS - 1) / MROWS;
   const int num_n = (args.N + BN - 1) / BN;
   const int num_k = (args.K + BK - 1) / BK;
   // split-K (args.splits > 1, plain fp32 epilogue only): tile t covers K blocks
@@ -256,12 +262,11 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
       for (int t = cid; t < num_tiles; t += ncl) {
         int mb, nb, kb0, kb1;
         tile_split(t, num_m, num_n, num_k, args.kper, mb, nb, kb0, kb1);
-        const int m0 = mb * BM * CG + static_cast<int>(rank) * BM;          // this CTA's 128 rows
         const int n0 = nb * BN + static_cast<int>(rank) * (BN / CG);       // this CTA's B share
         for (int kb = kb0; kb < (TPS_DBG_NOMAIN ? kb0 : kb1); ++kb) {
           MBAR_WAIT(1, &empty[stage], phase ^ 1);
-          uint8_t* sA = stages + stage * C::STAGE_BYTES;
-          uint8_t* sB = sA + A_BYTES;
+          uint8_t* const sA0 = stages + stage * C::STAGE_BYTES;
+          uint8_t* sB = sA0 + MH * A_BYTES;
           if (rank == 0) ptx::mbar_expect_tx(&full[stage], C::TX);
           else if (BLEND) ptx::mbar_expect_tx(&full[stage], 2 * C::B_BYTES);   // own B tiles, own barrier
           // every load of this stage completes on the leader CTA's full barrier
@@ -296,7 +301,11 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
               ptx::tma_load_im2col_4d(dst, m, &full[stage], c, w, h, n, static_cast<uint16_t>(ow),
                                       static_cast<uint16_t>(oh));
           };
-          // ---- A tile: 128 rows x 64 K
+          // ---- A tile(s): 128 rows x 64 K (MH of them: this CTA's rows of each 256-row half)
+#pragma unroll
+          for (int h = 0; h < MH; ++h) {
+          uint8_t* const sA = sA0 + h * A_BYTES;
+          const int m0 = mb * MROWS + h * BM * CG + static_cast<int>(rank) * BM;   // this CTA's 128 rows
           if ((CONV == CONV_FWD || CONV == CONV_DGRAD) && args.cv.im2col) {
             // im2col-mode TMA: K block kb = (filter tap, 64-channel block); the 128 output pixels
             // of this M block are 128 consecutive receptive-field origins of the traversal,
@@ -323,6 +332,7 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
 #pragma unroll
             for (int i = 0; i < BM / 64; ++i) ld2(sA + i * 8192, &tmA, m0 + 64 * i, kb * BK);
           }
+          }   // h
           // ---- B tile: BN/CG rows (K-major) or BN/CG columns (MN-major) x 64 K
           // BLEND: stash -> sB (the MMA operand slot), latest -> sB + B_BYTES; the transform
           // warps overwrite sB with the blend in place
@@ -387,7 +397,7 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
         const uint32_t acc_phase = (it / C::ACC) & 1;
         MBAR_WAIT(2, &tmem_empty[acc], acc_phase ^ 1);
         ptx::tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * BN;
+        const uint32_t d_tmem = tmem_base + acc * BN * MH;
         int mb_, nb_, kb0, kb1;
         tile_split(t, num_m, num_n, num_k, args.kper, mb_, nb_, kb0, kb1);
         for (int kb = kb0; kb < (TPS_DBG_NOMAIN ? kb0 : kb1); ++kb) {
@@ -395,17 +405,21 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
           if (BLEND) MBAR_WAIT(4, &xform[stage], phase);
           ptx::tc_fence_after();
           const uint32_t a_addr = ptx::smem_u32(stages + stage * C::STAGE_BYTES);
-          const uint32_t b_addr = a_addr + A_BYTES;
+          const uint32_t b_addr = a_addr + MH * A_BYTES;
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk) {
             // K-major SW128: +32 B per 16-element K step, SBO = 8 rows x 128 B
             // MN-major SW128: +16 K-rows x 128 B per step, LBO = 64-element MN chunk (8 KiB), SBO = 1 KiB
-            const uint64_t ad = A_MN ? ptx::make_sdesc_sw128(a_addr + kk * 2048, 8192, 1024)
-                                     : ptx::make_sdesc_sw128(a_addr + kk * 32, 16, 1024);
             const uint64_t bd = B_MN ? ptx::make_sdesc_sw128(b_addr + kk * 2048, 8192, 1024)
                                      : ptx::make_sdesc_sw128(b_addr + kk * 32, 16, 1024);
-            if (CG == 2) ptx::umma_f16_cg2(d_tmem, ad, bd, idesc, (kb != kb0) || (kk != 0));
-            else ptx::umma_f16(d_tmem, ad, bd, idesc, (kb != kb0) || (kk != 0));
+#pragma unroll
+            for (int h = 0; h < MH; ++h) {   // MH = 2: both row halves reuse this B tile
+              const uint32_t ah = a_addr + h * A_BYTES;
+              const uint64_t ad = A_MN ? ptx::make_sdesc_sw128(ah + kk * 2048, 8192, 1024)
+                                       : ptx::make_sdesc_sw128(ah + kk * 32, 16, 1024);
+              if (CG == 2) ptx::umma_f16_cg2(d_tmem + h * BN, ad, bd, idesc, (kb != kb0) || (kk != 0));
+              else ptx::umma_f16(d_tmem + h * BN, ad, bd, idesc, (kb != kb0) || (kk != 0));
+            }
           }
           if (CG == 2) ptx::umma_commit_cg2_mc(&empty[stage], 0x3);
           else ptx::umma_commit(&empty[stage]);
@@ -611,14 +625,16 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
       const uint32_t acc_phase = (it / C::ACC) & 1;
       MBAR_WAIT(7, &tmem_full[acc], acc_phase);
       ptx::tc_fence_after();
-      const int row0 = mb * BM * CG + static_cast<int>(rank) * BM + q * 32;
+#pragma unroll 1
+      for (int h = 0; h < MH; ++h) {
+      const int row0 = mb * MROWS + h * BM * CG + static_cast<int>(rank) * BM + q * 32;
 #pragma unroll 1
       for (int ci = 0; ci < CPW; ++ci) {
         const int c = half * CPW + ci;
         uint32_t r[32];
-        ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c * 32, r);
+        ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + (acc * MH + h) * BN + c * 32, r);
         ptx::tmem_ld_wait();
-        if (ci == CPW - 1) {                // last TMEM read of this warp for this tile
+        if (ci == CPW - 1 && h == MH - 1) {   // last TMEM read of this warp for this tile
           ptx::tc_fence_before();
           __syncwarp();
           if (lane == 0) {
@@ -737,6 +753,7 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
           }
         }
       }
+      }   // h
     }
   } else if (BLEND) {
     // ===================== operand transform: W_res = α·W_stash + β·W_latest =====================
@@ -750,7 +767,7 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG>::THREADS, 1)
     for (int t = cid; t < num_tiles; t += ncl) {
       for (int kb = 0; kb < num_k; ++kb) {
         MBAR_WAIT(8, &full[stage], phase);
-        uint8_t* sB = stages + stage * C::STAGE_BYTES + A_BYTES;
+        uint8_t* sB = stages + stage * C::STAGE_BYTES + MH * A_BYTES;
         uint4* s = reinterpret_cast<uint4*>(sB);
         const uint4* l = reinterpret_cast<const uint4*>(sB + C::B_BYTES);
 #pragma unroll
@@ -1263,18 +1280,18 @@ struct EpiMaps {
   CUtensorMap w, v, q;   // fused update: fp32 master, fp32 momentum, bf16 version (32x32 boxes)
 };
 
-template <int BN, int A_MN, int B_MN, int BLEND, int SGD = 0, int CG = 1, int CONV = CONV_NONE>
+template <int BN, int A_MN, int B_MN, int BLEND, int SGD = 0, int CG = 1, int CONV = CONV_NONE, int MH = 1>
 cudaError_t launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& b2, const EpiMaps& em,
                    const GemmArgs& args, cudaStream_t st) {
-  using C = Cfg<BN, BLEND, SGD, CG>;
-  auto kern = gemm_kernel<BN, A_MN, B_MN, BLEND, SGD, CG, CONV>;
+  using C = Cfg<BN, BLEND, SGD, CG, MH>;
+  auto kern = gemm_kernel<BN, A_MN, B_MN, BLEND, SGD, CG, CONV, MH>;
   static bool attr_set = false;   // per instantiation
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  const int tiles = ((args.M + BM * CG - 1) / (BM * CG)) * ((args.N + BN - 1) / BN) * std::max(1, args.splits);
+  const int tiles = ((args.M + BM * CG * MH - 1) / (BM * CG * MH)) * ((args.N + BN - 1) / BN) * std::max(1, args.splits);
   const int sms = args.max_ctas > 0 ? std::min(args.max_ctas, num_sms()) : num_sms();
   const int clusters = std::max(1, std::min(tiles, sms / CG));
   cudaLaunchConfig_t cfg{};
@@ -1404,6 +1421,22 @@ cudaError_t dispatch(const Tiling& tl, const CUtensorMap& ta, const CUtensorMap&
 
 }  // namespace
 
+// Blended input gradient on CTA pairs: 512-row tiles (MH = 2, two accumulators sharing one
+// blended B tile) when the K loop is long enough that the single accumulator buffer's exposed
+// epilogue is small and two waves of 256-row tiles become (at most) one of 512-row tiles.  TPS_BLEND_MH=1 keeps 256-row tiles.
+bool blend_mh2(const GemmArgs& a) {
+  static int mh = -1;
+  if (mh < 0) {
+    const char* e = std::getenv("TPS_BLEND_MH");
+    mh = e ? std::atoi(e) : 2;
+  }
+  if (mh != 2 || (a.K + BK - 1) / BK < 16) return false;
+  const int pairs = num_sms() / 2, nn = (a.N + 255) / 256;
+  const int w256 = ((a.M + 255) / 256 * nn + pairs - 1) / pairs;       // waves of 256-row tiles
+  const int w512 = ((a.M + 511) / 512 * nn + pairs - 1) / pairs;       // waves of 512-row tiles
+  return 2 * w512 <= w256;
+}
+
 const char* gemm_mode_name(int mode) {
   switch (mode) {
     case GEMM_FWD: return "fwd";
@@ -1512,13 +1545,15 @@ cudaError_t gemm_run(int mode, const GemmOperands& op, const GemmArgs& args_in, 
       e = sgd ? dispatch<1, 1, 1>(tl, ta, tb, tb2, em, args, st) : dispatch<1, 1, 0>(tl, ta, tb, tb2, em, args, st);
       break;
     case GEMM_DGRAD_BLEND:
-      e = tl.cg == 2 ? launch<256, 0, 1, 1, 0, 2>(ta, tb, tb2, em, args, st)
+      e = tl.cg == 2 ? (blend_mh2(args) ? launch<256, 0, 1, 1, 0, 2, CONV_NONE, 2>(ta, tb, tb2, em, args, st)
+                                        : launch<256, 0, 1, 1, 0, 2>(ta, tb, tb2, em, args, st))
                      : launch<128, 0, 1, 1, 0, 1>(ta, tb, tb2, em, args, st);
       break;
     case GEMM_CONV_FWD: e = dispatch<0, 0, 0, CONV_FWD>(tl, ta, tb, tb2, em, args, st); break;
     case GEMM_CONV_DGRAD: e = dispatch<0, 1, 0, CONV_DGRAD>(tl, ta, tb, tb2, em, args, st); break;
     case GEMM_CONV_DGRAD_BLEND:
-      e = tl.cg == 2 ? launch<256, 0, 1, 1, 0, 2, CONV_DGRAD>(ta, tb, tb2, em, args, st)
+      e = tl.cg == 2 ? (blend_mh2(args) ? launch<256, 0, 1, 1, 0, 2, CONV_DGRAD, 2>(ta, tb, tb2, em, args, st)
+                                        : launch<256, 0, 1, 1, 0, 2, CONV_DGRAD>(ta, tb, tb2, em, args, st))
                      : launch<128, 0, 1, 1, 0, 1, CONV_DGRAD>(ta, tb, tb2, em, args, st);
       break;
     case GEMM_CONV_WGRAD:

@@ -1938,10 +1938,12 @@ tps_status tps_pipeline_init(const tps_config* c, tps_pipeline** out) {
     p->split_w = !(e && e[0] == '0') && p->fuse_update && !p->graph && nl > 1;
   }
   {
-    // default on: the split backward's wgrad + update of layer k and dgrad of layer k-1 share one
-    // persistent launch (gemm_bwd_dual); TPS_DUAL=0 launches them separately on two streams
+    // opt-in (TPS_DUAL=1): the split backward's wgrad + update of layer k and dgrad of layer k-1
+    // share one persistent launch (gemm_bwd_dual).  Off by default: the step runs at the 1 kW power
+    // cap, so overlapping the two inside one launch only lowers the clock (dual 159 us at 1395 MHz
+    // vs 166 us for the two launches at 1515 MHz; the C5 step unchanged)
     const char* e = std::getenv("TPS_DUAL");
-    p->dual = p->split_w && !(e && e[0] == '0');
+    p->dual = p->split_w && e && e[0] == '1';
   }
   if (p->split_w && (st = alloc_t(p, &p->gwork[2], static_cast<size_t>(p->B) * max_elems, &p->mem_acts)) != TPS_OK)
     return cleanup(st);

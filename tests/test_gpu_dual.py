@@ -7,7 +7,7 @@ Checks: (1) raw kernel == the two separate kernels BIT FOR BIT where both use th
 shapes, momentum on / off, mask and α); (2) unsuitable shapes report TPS_E_UNSUPPORTED;
 (3) whole pipelines (multi-layer S = 1, multi-stage LOCAL with EQ1 α, V, the bias step on the
 optimizer stream) produce bit-identical losses, parameters and momentum with the dual launch
-on (default) and off (TPS_DUAL=0: the two launches on two streams)."""
+on (TPS_DUAL=1) and off (the default: the two launches on two streams)."""
 import os
 
 import numpy as np

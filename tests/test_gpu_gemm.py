@@ -85,7 +85,9 @@ def test_wgrad_both_mn_major(gpu_lib, M, N, K):
     torch.testing.assert_close(out.double(), ref, rtol=1e-5, atol=2e-6 * K ** 0.5 * ref.abs().max().item())
 
 
-@pytest.mark.parametrize("M,N,K", [(64, 256, 64), (300, 264, 136), (2048, 4096, 1024)])
+# (2048, 4096, 1024) and (1800, 4000, 1040) run on 512-row CTA-pair tiles (two accumulators sharing
+# one blended B tile, ragged M / N / K tails in the second case); the others on 256- or 128-row tiles
+@pytest.mark.parametrize("M,N,K", [(64, 256, 64), (300, 264, 136), (2048, 4096, 1024), (1800, 4000, 1040)])
 @pytest.mark.parametrize("a,b", [(0.25, 0.75), (0.9512294, 0.0487706), (-6.0, 0.0)])
 def test_dgrad_blended_operand(gpu_lib, M, N, K, a, b):
     # G · bf16(α·W_stash + β·W_latest), operand formed in shared memory (K8 definition, reading Z14)

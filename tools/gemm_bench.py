@@ -2,7 +2,9 @@
 CUDA-event timed, with cuBLAS (torch.matmul) beside it for context."""
 import argparse
 import os
+import statistics
 import sys
+import time
 
 import torch
 
@@ -10,7 +12,56 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2509_23241_b200 import tps  # noqa: E402
 
 
-def timeit(fn, iters=20, warm=5):
+class Nvml:
+    """pynvml sampling (SM clock MHz, board power W) in a thread while a mode runs, so a
+    number can be read against the clock it ran at (this pool's B200s are power-capped)."""
+
+    def __init__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(torch.cuda.current_device())
+        except Exception:
+            self.nv = None
+        self.rows = []
+
+    def __enter__(self):
+        import threading
+        self.rows, self.stop = [], False
+
+        def run():
+            while not self.stop and self.nv:
+                try:
+                    self.rows.append((self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM),
+                                      self.nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0))
+                except Exception:
+                    break
+                time.sleep(0.005)
+        self.t = threading.Thread(target=run, daemon=True)
+        self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop = True
+        self.t.join()
+
+    def summary(self):
+        if not self.rows:
+            return ""
+        rows = self.rows[len(self.rows) // 4:]          # skip the ramp
+        mhz = statistics.median(r[0] for r in rows)
+        w = statistics.median(r[1] for r in rows)
+        return f"  [{mhz:.0f} MHz, {w:.0f} W]"
+
+
+def timeit(fn, iters=20, warm=5, seconds=0.0):
+    if seconds > 0:            # steady state under the power cap: run ~seconds before timing
+        t0 = time.time()
+        while time.time() - t0 < seconds:
+            for _ in range(20):
+                fn()
+            torch.cuda.synchronize()
     for _ in range(warm):
         fn()
     torch.cuda.synchronize()
@@ -30,6 +81,8 @@ def main():
     ap.add_argument("--K", type=int, default=4096)
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--modes", default="0,1,2,3,4")
+    ap.add_argument("--seconds", type=float, default=0.0,
+                    help="run each mode this long first and sample SM clock / power while timing")
     a = ap.parse_args()
     M, N, K = a.M, a.N, a.K
     X = torch.randn(M, K, device="cuda").to(torch.bfloat16)          # fwd A / dgrad A (G)
@@ -72,7 +125,9 @@ def main():
     }
     for m in [int(x) for x in a.modes.split(",")]:
         name, fn = runs[m]
-        ms = timeit(fn, a.iters)
+        nv = Nvml()
+        with nv:
+            ms = timeit(fn, a.iters if not a.seconds else max(a.iters, 200), seconds=a.seconds)
         extra = ""
         f = fl
         if m == 4:   # HBM roofline of the fused kernel: operands + 18 B per parameter (w, v r/w + bf16 version)
@@ -80,9 +135,12 @@ def main():
             extra = f"  {by / ms / 1e6:7.1f} GB/s algorithmic ({by / 1e6:.1f} MB)"
         if m in (5, 6):
             f = 2.0 * M * N * N * 2
-        print(f"mode {m} {name:34s} {M}x{N}x{K}: {ms*1e3:8.1f} us  {f/ms/1e9:7.1f} TFLOP/s{extra}", flush=True)
-    ms = timeit(lambda: torch.matmul(X, W.T), a.iters)
-    print(f"cuBLAS torch.matmul bf16 {M}x{N}x{K}: {ms*1e3:8.1f} us  {fl/ms/1e9:7.1f} TFLOP/s")
+        print(f"mode {m} {name:34s} {M}x{N}x{K}: {ms*1e3:8.1f} us  {f/ms/1e9:7.1f} TFLOP/s{extra}{nv.summary()}",
+              flush=True)
+    nv = Nvml()
+    with nv:
+        ms = timeit(lambda: torch.matmul(X, W.T), a.iters if not a.seconds else max(a.iters, 200), seconds=a.seconds)
+    print(f"cuBLAS torch.matmul bf16 {M}x{N}x{K}: {ms*1e3:8.1f} us  {fl/ms/1e9:7.1f} TFLOP/s{nv.summary()}")
 
 
 if __name__ == "__main__":
