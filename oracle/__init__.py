@@ -9,6 +9,7 @@ links or executes anything here, and this package never imports the product.
 Modules (each function cites the passage it follows; P:n = PAPER.md line n,
 S:n = SPEC.md line n, Z# = DESIGN.md reading):
   bf16       -- round-to-nearest-even bfloat16 storage emulation (Z13)
+  tf32       -- round-to-nearest (ties away) tf32 storage emulation (tf32 mode, Z28)
   staleness  -- f(δ) = e^{-λδ} (Eq. 2), Eq. 1 factor, blend coeffs (Z1)
   schedule   -- static nF1B per-stage event order (Z6, Z7)
                 and a dependency-driven executor

@@ -13,7 +13,7 @@ Paper passages:
     fp32 master (reading Z9).
 
 Precision (reading Z13): inputs/weights/activations/activation-gradients are
-bf16 values (held here as fp64 numbers); products and sums are fp64; weight
+bf16 values (tf32 values in tf32 mode, reading Z28; held here as fp64 numbers); products and sums are fp64; weight
 gradients are rounded to fp32; the update is numpy float32, one rounding per
 operation.  `Precision(exact=True)` disables every rounding (finite-difference
 and autograd pins).
@@ -24,16 +24,19 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from . import bf16
+from . import bf16, tf32
 
 
 @dataclass(frozen=True)
 class Precision:
     exact: bool = False
+    dtype: str = "bf16"        # storage of activations / weight copies / gradients: "bf16" | "tf32"
 
     def store(self, x: np.ndarray) -> np.ndarray:
-        """Value as stored in a bf16 tensor (Z13)."""
-        return np.asarray(x, dtype=np.float64) if self.exact else bf16.rne(x)
+        """Value as stored in a bf16 tensor (Z13), or in a tf32 tensor in tf32 mode (Z28)."""
+        if self.exact:
+            return np.asarray(x, dtype=np.float64)
+        return tf32.rna(x) if self.dtype == "tf32" else bf16.rne(x)
 
     def f32(self, x: np.ndarray) -> np.ndarray:
         """Value as stored in an fp32 tensor."""
@@ -87,16 +90,18 @@ def resolve_backward_weight(W_stash: np.ndarray, W_latest: np.ndarray,
 
 
 def materialize_blend(W_stash_bf16: np.ndarray, W_latest_bf16: np.ndarray,
-                      alpha: float, beta: float) -> np.ndarray:
+                      alpha: float, beta: float, dtype: str = "bf16") -> np.ndarray:
     """K8 debug materialiser definition (reading Z14):
-    bf16_rne(fp32(fp32(α·s) + fp32(β·l))), every op a single fp32 rounding."""
+    bf16_rne(fp32(fp32(α·s) + fp32(β·l))), every op a single fp32 rounding
+    (tf32 mode: tf32_rna of the same fp32 sum, reading Z28)."""
     a = np.float32(alpha)
     b = np.float32(beta)
     s = np.asarray(W_stash_bf16, dtype=np.float32)
     l = np.asarray(W_latest_bf16, dtype=np.float32)
     with np.errstate(over="ignore", invalid="ignore"):
         t = (a * s).astype(np.float32) + (b * l).astype(np.float32)
-    return bf16.rne(t.astype(np.float32))
+    t = t.astype(np.float32)
+    return tf32.rna(t) if dtype == "tf32" else bf16.rne(t)
 
 
 def sgd_update(w: np.ndarray, v: np.ndarray, g: np.ndarray, lr: float, mu: float,

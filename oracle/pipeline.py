@@ -48,6 +48,8 @@ class Config:
     layers: list | None = None
     # mini-batches in flight for a ONE-stage pipeline (0 => S - s; schedule.inflight)
     max_inflight: int = 0
+    # storage precision of activations / weight copies / gradients (Z13 bf16; Z28 tf32)
+    dtype: str = "bf16"
 
     @property
     def S(self) -> int:
@@ -96,7 +98,8 @@ def run(cfg: Config, xs: list[np.ndarray], ys: list[np.ndarray],
         w0: list[np.ndarray], b0: list[np.ndarray]) -> Result:
     """Train M mini-batches; xs[j] is [B, d0] (bf16-exact), ys[j] is [B] int."""
     S, L, B, m, bsz = cfg.S, cfg.L, cfg.B, cfg.m, cfg.b
-    prec = mlp.Precision(cfg.exact)
+    prec = mlp.Precision(cfg.exact, cfg.dtype)
+    assert cfg.dtype in ("bf16", "tf32")
     assert cfg.stage_bounds[0] == 0 and cfg.stage_bounds[-1] == L
     stage_of = {}
     for s in range(S):
