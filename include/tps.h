@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define TPS_ABI_VERSION 3
+#define TPS_ABI_VERSION 4
 
 typedef enum {
   TPS_OK = 0,
@@ -61,6 +61,11 @@ typedef enum { TPS_V = 0, TPS_I = 1 } tps_variant;
 /* Z1: EQ1 = the paper's closed form α = 2 - e^{λδ}, β = 0 (Eq. 1, Eq. 12);
  *     CONVEX = the prose reading α = e^{-λδ}, β = 1 - α.               */
 typedef enum { TPS_BLEND_EQ1 = 0, TPS_BLEND_CONVEX = 1 } tps_blend;
+
+/* Storage precision of activations, weight versions and activation-gradients (reading Z13 /
+ * Z28; north_star "bf16/tf32 inputs with fp32 accumulation"): bf16 (RNE) or tf32 values in
+ * 4-byte fp32 containers (RNA).  See tps_config.dtype.                                    */
+typedef enum { TPS_BF16 = 0, TPS_TF32 = 1 } tps_dtype;
 
 /* How a stage exchanges activations / activation-gradients with its neighbours
  * (one-to-one transfers).  NONE: S = 1.  LOCAL: all stages are handles
@@ -205,7 +210,15 @@ typedef struct {
    * Replica r of mini-batch j reads rows [r·B, (r+1)·B) of pool entry j % pool.               */
   int32_t dp_size;              /* R >= 1 (<= 8)                                        */
   int32_t dp_rank;              /* 0 <= dp_rank < R                                     */
-  int32_t reserved[2];
+  /* Storage precision (tps_dtype; reading Z28, north_star "bf16/tf32 inputs"): TPS_BF16 (0)
+   * stores activations, weight versions / stash and activation-gradients as bf16 (RNE);
+   * TPS_TF32 (1) stores them as tf32 values in fp32 containers (RNA, cvt.rna.tf32.f32) and
+   * runs the stage GEMMs as kind::tf32: every activation / version buffer, input pool and
+   * exchanged message then holds 4-byte elements.  fp32 master weights, momentum, weight
+   * gradients and losses are the same in both.  TF32: chain MLP networks only (no
+   * layer_specs, dp_size 1), else TPS_E_UNSUPPORTED; another value: TPS_E_CONFIG.            */
+  int32_t dtype;
+  int32_t reserved;
 } tps_config;
 
 typedef struct tps_pipeline tps_pipeline;  /* opaque; one per stage */
@@ -316,12 +329,13 @@ tps_status tps_stash_info(tps_pipeline* p, int32_t* live_versions, int64_t* stas
                           int64_t* peak_stash_bytes);
 /* Debug materialiser (K8): out_bf16 (device, [out, ld_in]) =
  * bf16_rne(fp32(α·W_stash) + fp32(β·W_latest)) for stage-local layer index
- * `layer`, with W_stash = latest - staleness.  Never used by the training path. */
+ * `layer`, with W_stash = latest - staleness.  Never used by the training path.
+ * (dtype TPS_TF32: out is fp32 [out, ld_in] = tf32_rna of the same fp32 sum.)    */
 tps_status tps_intermediate_weight(tps_pipeline* p, int32_t layer, int32_t staleness,
                                    void* out_bf16);
 
 /* Debug read of a live bf16 weight version (device out, [pad16(out), pad16(in)]):
- * version latest - staleness of stage-local layer `layer`.                    */
+ * version latest - staleness of stage-local layer `layer`.  (TPS_TF32: fp32 elements.) */
 tps_status tps_get_version(tps_pipeline* p, int32_t layer, int32_t staleness, void* out_bf16);
 
 /* ---- static schedule (host only) ------------------------------------------- */
@@ -403,7 +417,11 @@ tps_status tps_debug_progress(tps_pipeline* p, int64_t* pos, int64_t* n_events, 
  * mode 2 (wgrad):    A stored [K,M] ld=lda (MN-major), B stored [K,N] (MN-major); fp32 out.
  * mode 3 (dgrad, blended operand, CONVEX/I): B = alpha·B + beta·B2 formed in shared memory
  *        before the MMA (B2 same layout/ld as B); mask as mode 1; no extra alpha scale.
- * out_f32: 1 => fp32 output, else bf16.  Requires N % 8 == 0 and 16-byte aligned rows. */
+ * out_f32: 1 => fp32 output, else bf16.  Requires N % 8 == 0 and 16-byte aligned rows.
+ * mode | TPS_GEMM_TF32: tf32 storage (reading Z28): A, B, B2, mask and a non-fp32 out are fp32
+ *        arrays holding tf32 values (ld in elements), the MMAs run kind::tf32 and a non-fp32
+ *        out is rounded RNA to tf32.                                                       */
+#define TPS_GEMM_TF32 16
 tps_status tps_gemm(int32_t mode, int32_t M, int32_t N, int32_t K,
                     const void* A, int32_t lda, const void* B, int32_t ldb, const void* B2,
                     void* out, int32_t ldo, int32_t out_f32, const float* bias, int32_t relu,

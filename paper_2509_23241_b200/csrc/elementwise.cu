@@ -42,9 +42,15 @@ __device__ __forceinline__ uint16_t f2bf(float x) {
   return *reinterpret_cast<uint16_t*>(&h);
 }
 __device__ __forceinline__ float bf2f(uint32_t h) { return __uint_as_float(h << 16); }
+// tf32 storage (reading Z28): nearest tf32 value, ties away from zero, in an fp32 container
+__device__ __forceinline__ float rna_tf32(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
 
 // ------------------------------------------------------------------ SGD update
-template <bool MOMENTUM, bool WRITE_VER>
+template <bool MOMENTUM, bool WRITE_VER, bool TF = false>
 __global__ void __launch_bounds__(256) sgd_update_kernel(float* __restrict__ w, float* __restrict__ v,
                                                          const float* __restrict__ g, uint16_t* __restrict__ ver,
                                                          int64_t n4, float lr, float mu, float wd) {
@@ -73,7 +79,10 @@ __global__ void __launch_bounds__(256) sgd_update_kernel(float* __restrict__ w, 
     }
     reinterpret_cast<float4*>(w)[i] = make_float4(ww[0], ww[1], ww[2], ww[3]);
     if (MOMENTUM) reinterpret_cast<float4*>(v)[i] = make_float4(vv[0], vv[1], vv[2], vv[3]);
-    if (WRITE_VER) {
+    if (WRITE_VER && TF) {   // tf32 version (fp32 container)
+      reinterpret_cast<float4*>(ver)[i] =
+          make_float4(rna_tf32(ww[0]), rna_tf32(ww[1]), rna_tf32(ww[2]), rna_tf32(ww[3]));
+    } else if (WRITE_VER) {
       uint2 o;
       o.x = static_cast<uint32_t>(f2bf(ww[0])) | (static_cast<uint32_t>(f2bf(ww[1])) << 16);
       o.y = static_cast<uint32_t>(f2bf(ww[2])) | (static_cast<uint32_t>(f2bf(ww[3])) << 16);
@@ -137,6 +146,7 @@ constexpr int BG_COLS = 256;   // columns per block (32 threads x 8 columns)
 constexpr int BG_ROWS = 8;     // row lanes per block
 constexpr int BG_CNT = 64;     // arrival counters at the head of the scratch (cols <= 64·BG_COLS)
 
+template <bool TF>
 __global__ void __launch_bounds__(256) bias_grad_partial(const uint16_t* __restrict__ G, int rows, int cols, int ldg,
                                                          int rows_per_split, float* __restrict__ part) {
   __shared__ float red[BG_ROWS][BG_COLS + 4];
@@ -146,10 +156,19 @@ __global__ void __launch_bounds__(256) bias_grad_partial(const uint16_t* __restr
   float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   if (c0 < cols) {
     for (int r = r_begin + threadIdx.y; r < r_end; r += BG_ROWS) {
-      const uint4 u = __ldg(reinterpret_cast<const uint4*>(G + static_cast<size_t>(r) * ldg + c0));
-      const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+      if (TF) {   // fp32 (tf32) gradient: two 16-byte loads per 8 columns
+        const float4* q =
+            reinterpret_cast<const float4*>(reinterpret_cast<const float*>(G) + static_cast<size_t>(r) * ldg + c0);
+        const float4 u0 = __ldg(q), u1 = __ldg(q + 1);
+        const float f[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
 #pragma unroll
-      for (int e = 0; e < 8; ++e) acc[e] += bf2f((w[e >> 1] >> ((e & 1) * 16)) & 0xFFFFu);
+        for (int e = 0; e < 8; ++e) acc[e] += f[e];
+      } else {
+        const uint4 u = __ldg(reinterpret_cast<const uint4*>(G + static_cast<size_t>(r) * ldg + c0));
+        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[e] += bf2f((w[e >> 1] >> ((e & 1) * 16)) & 0xFFFFu);
+      }
     }
   }
 #pragma unroll
@@ -168,6 +187,7 @@ __global__ void __launch_bounds__(256) bias_grad_partial(const uint16_t* __restr
 // bias_grad_partial, then the LAST block of each column block (arrival counter, self-resetting)
 // sums the splits in fixed order (deterministic, same bits as bias_grad_final) and, if b != null,
 // applies the SGD/momentum step of sgd_update_kernel to the fp32 bias and its momentum.
+template <bool TF>
 __global__ void __launch_bounds__(256) bias_grad_fused(const uint16_t* __restrict__ G, int rows, int cols, int ldg,
                                                        int rows_per_split, float* __restrict__ part,
                                                        unsigned int* __restrict__ cnt, float* __restrict__ db,
@@ -182,10 +202,19 @@ __global__ void __launch_bounds__(256) bias_grad_fused(const uint16_t* __restric
   if (c0 < cols) {
 #pragma unroll 8
     for (int r = r_begin + threadIdx.y; r < r_end; r += BG_ROWS) {   // unrolled: loads in flight, same add order
-      const uint4 u = __ldg(reinterpret_cast<const uint4*>(G + static_cast<size_t>(r) * ldg + c0));
-      const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+      if (TF) {   // fp32 (tf32) gradient: two 16-byte loads per 8 columns
+        const float4* q =
+            reinterpret_cast<const float4*>(reinterpret_cast<const float*>(G) + static_cast<size_t>(r) * ldg + c0);
+        const float4 u0 = __ldg(q), u1 = __ldg(q + 1);
+        const float f[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
 #pragma unroll
-      for (int e = 0; e < 8; ++e) acc[e] += bf2f((w[e >> 1] >> ((e & 1) * 16)) & 0xFFFFu);
+        for (int e = 0; e < 8; ++e) acc[e] += f[e];
+      } else {
+        const uint4 u = __ldg(reinterpret_cast<const uint4*>(G + static_cast<size_t>(r) * ldg + c0));
+        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[e] += bf2f((w[e >> 1] >> ((e & 1) * 16)) & 0xFFFFu);
+      }
     }
   }
 #pragma unroll
@@ -276,6 +305,7 @@ int bias_grad_splits(int rows, int cols) {
 }
 
 // ------------------------------------------------------------------ softmax cross-entropy
+template <bool TF>
 __global__ void __launch_bounds__(256) softmax_xent_kernel(const float* __restrict__ logits, int ldl,
                                                            const int32_t* __restrict__ labels, int rows, int classes,
                                                            int batch, float* __restrict__ loss_rows,
@@ -294,7 +324,6 @@ __global__ void __launch_bounds__(256) softmax_xent_kernel(const float* __restri
   for (int o = 16; o; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
   const int y = labels[warp];
   if (lane == 0) loss_rows[warp] = static_cast<float>(mx + log(se) - static_cast<double>(z[y]));
-  uint16_t* g = G + static_cast<size_t>(warp) * ldg;
   for (int c = lane; c < ldg; c += 32) {
     float out = 0.f;
     if (c < classes) {
@@ -302,7 +331,8 @@ __global__ void __launch_bounds__(256) softmax_xent_kernel(const float* __restri
       if (c == y) p -= 1.0;
       out = static_cast<float>(p / batch);
     }
-    g[c] = f2bf(out);
+    if (TF) reinterpret_cast<float*>(G)[static_cast<size_t>(warp) * ldg + c] = rna_tf32(out);
+    else G[static_cast<size_t>(warp) * ldg + c] = f2bf(out);
   }
 }
 
@@ -329,6 +359,19 @@ __global__ void f32_to_bf16_kernel(const float* __restrict__ in, uint16_t* __res
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)
     out[i] = f2bf(in[i]);
+}
+
+__global__ void f32_to_tf32_kernel(const float* __restrict__ in, float* __restrict__ out, int64_t n) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[i] = rna_tf32(in[i]);
+}
+
+__global__ void blend_materialize_tf32_kernel(const float* __restrict__ s, const float* __restrict__ l,
+                                              float* __restrict__ out, int64_t n, float a, float b) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[i] = rna_tf32(__fadd_rn(__fmul_rn(a, s[i]), __fmul_rn(b, l[i])));
 }
 
 __global__ void blend_materialize_kernel(const uint16_t* __restrict__ s, const uint16_t* __restrict__ l,
@@ -1254,13 +1297,16 @@ uint64_t host_mix64(uint64_t x) {
 }  // namespace
 
 cudaError_t launch_sgd_update(float* w, float* v, const float* g, uint16_t* ver, int64_t n, float lr, float mu,
-                              float wd, cudaStream_t st, int blocks_per_sm) {
+                              float wd, cudaStream_t st, int blocks_per_sm, int tf) {
   if (n <= 0) return cudaSuccess;
   if (n % 4) return cudaErrorInvalidValue;
   const int64_t n4 = n / 4;
   const int grid = grid_for(n4, 256, blocks_per_sm);
   const bool mom = mu != 0.0f;
-  if (mom && ver) sgd_update_kernel<true, true><<<grid, 256, 0, st>>>(w, v, g, ver, n4, lr, mu, wd);
+  if (tf && ver) {
+    if (mom) sgd_update_kernel<true, true, true><<<grid, 256, 0, st>>>(w, v, g, ver, n4, lr, mu, wd);
+    else sgd_update_kernel<false, true, true><<<grid, 256, 0, st>>>(w, v, g, ver, n4, lr, mu, wd);
+  } else if (mom && ver) sgd_update_kernel<true, true><<<grid, 256, 0, st>>>(w, v, g, ver, n4, lr, mu, wd);
   else if (mom) sgd_update_kernel<true, false><<<grid, 256, 0, st>>>(w, v, g, ver, n4, lr, mu, wd);
   else if (ver) sgd_update_kernel<false, true><<<grid, 256, 0, st>>>(w, v, g, ver, n4, lr, mu, wd);
   else sgd_update_kernel<false, false><<<grid, 256, 0, st>>>(w, v, g, ver, n4, lr, mu, wd);
@@ -1295,7 +1341,7 @@ int64_t bias_grad_scratch_floats(int rows, int cols) {
 }
 
 cudaError_t launch_bias_grad_sgd(const uint16_t* G, int rows, int cols, int ldg, float* db, float* scratch, float* b,
-                                 float* vb, float lr, float mu, float wd, cudaStream_t st) {
+                                 float* vb, float lr, float mu, float wd, cudaStream_t st, int tf) {
   if (cols <= 0) return cudaSuccess;
   if (cols % 8 || ldg % 8) return cudaErrorInvalidValue;
   const int splits = bias_grad_splits(rows, cols);
@@ -1303,28 +1349,38 @@ cudaError_t launch_bias_grad_sgd(const uint16_t* G, int rows, int cols, int ldg,
   dim3 grid((cols + BG_COLS - 1) / BG_COLS, splits);
   if (static_cast<int>(grid.x) > BG_CNT) return cudaErrorInvalidValue;
   unsigned int* cnt = reinterpret_cast<unsigned int*>(scratch);
-  bias_grad_fused<<<grid, dim3(32, BG_ROWS), 0, st>>>(G, rows, cols, ldg, rps, scratch + BG_CNT, cnt, db, b, vb, lr,
-                                                      mu, wd);
+  if (tf)
+    bias_grad_fused<true><<<grid, dim3(32, BG_ROWS), 0, st>>>(G, rows, cols, ldg, rps, scratch + BG_CNT, cnt, db, b, vb,
+                                                              lr, mu, wd);
+  else
+    bias_grad_fused<false><<<grid, dim3(32, BG_ROWS), 0, st>>>(G, rows, cols, ldg, rps, scratch + BG_CNT, cnt, db, b,
+                                                               vb, lr, mu, wd);
   return cudaGetLastError();
 }
 
 cudaError_t launch_bias_grad(const uint16_t* G, int rows, int cols, int ldg, float* db, float* scratch,
-                             cudaStream_t st) {
+                             cudaStream_t st, int tf) {
   if (cols <= 0) return cudaSuccess;
   if (cols % 8 || ldg % 8) return cudaErrorInvalidValue;
   const int splits = bias_grad_splits(rows, cols);
   const int rps = (rows + splits - 1) / splits;
   dim3 grid((cols + BG_COLS - 1) / BG_COLS, splits);
-  bias_grad_partial<<<grid, dim3(32, BG_ROWS), 0, st>>>(G, rows, cols, ldg, rps, scratch + BG_CNT);
+  if (tf) bias_grad_partial<true><<<grid, dim3(32, BG_ROWS), 0, st>>>(G, rows, cols, ldg, rps, scratch + BG_CNT);
+  else bias_grad_partial<false><<<grid, dim3(32, BG_ROWS), 0, st>>>(G, rows, cols, ldg, rps, scratch + BG_CNT);
   bias_grad_final<<<(cols + 255) / 256, 256, 0, st>>>(scratch + BG_CNT, splits, cols, db);
   return cudaGetLastError();
 }
 
 cudaError_t launch_softmax_xent(const float* logits, int ldl, const int32_t* labels, int rows, int classes, int batch,
-                                float* loss_rows, uint16_t* G, int ldg, cudaStream_t st) {
+                                float* loss_rows, uint16_t* G, int ldg, cudaStream_t st, int tf) {
   if (rows <= 0) return cudaSuccess;
   const int warps_per_block = 8;
-  softmax_xent_kernel<<<(rows + warps_per_block - 1) / warps_per_block, 32 * warps_per_block, 0, st>>>(
+  if (tf) {
+    softmax_xent_kernel<true><<<(rows + warps_per_block - 1) / warps_per_block, 32 * warps_per_block, 0, st>>>(
+        logits, ldl, labels, rows, classes, batch, loss_rows, G, ldg);
+    return cudaGetLastError();
+  }
+  softmax_xent_kernel<false><<<(rows + warps_per_block - 1) / warps_per_block, 32 * warps_per_block, 0, st>>>(
       logits, ldl, labels, rows, classes, batch, loss_rows, G, ldg);
   return cudaGetLastError();
 }
@@ -1337,6 +1393,19 @@ cudaError_t launch_loss_mean(const float* loss_rows, int rows, float* losses, in
 cudaError_t launch_f32_to_bf16(const float* in, uint16_t* out, int64_t n, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   f32_to_bf16_kernel<<<grid_for(n, 256), 256, 0, st>>>(in, out, n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_f32_to_tf32(const float* in, float* out, int64_t n, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  f32_to_tf32_kernel<<<grid_for(n, 256), 256, 0, st>>>(in, out, n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_blend_materialize_tf32(const float* s, const float* l, float* out, int64_t n, float a, float b,
+                                         cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  blend_materialize_tf32_kernel<<<grid_for(n, 256), 256, 0, st>>>(s, l, out, n, a, b);
   return cudaGetLastError();
 }
 

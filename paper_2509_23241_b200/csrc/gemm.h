@@ -62,6 +62,10 @@ struct GemmArgs {
   // colsum + ceil(M/32)·N.  Fed to the bias gradient of the next layer down and to batch-norm
   // statistics without another pass over the tensor.  Null = off.
   float* colsum; int colsum_sq;
+  // tf32 storage (reading Z28): A, B (and B2, mask, a non-fp32 out, the fused update's version)
+  // are fp32 arrays holding tf32 values, MMAs run kind::tf32, stores round RNA to tf32.
+  // Linear modes only (GEMM_FWD / DGRAD / WGRAD / DGRAD_BLEND), no addend, no split-K.
+  int tf32;
 };
 
 // The input-gradient half of a dual backward launch (gemm_bwd_dual): dX[M, N] = α·(G·W)

@@ -181,7 +181,7 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 #define MBAR_WAIT(tag, bar, par) ptx::mbar_wait((bar), (par))
 #endif
 
-template <int BN, int A_MN, int B_MN, int BLEND, int SGD, int CG, int CONV, int MH = 1>
+template <int BN, int A_MN, int B_MN, int BLEND, int SGD, int CG, int CONV, int MH = 1, int TF = 0>
 __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG, MH>::THREADS, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmB2, const __grid_constant__ CUtensorMap tmW,
@@ -192,6 +192,15 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG, MH>::THREADS, 1)
   using C = Cfg<BN, BLEND, SGD, CG, MH>;
   static_assert(CG == 1 || BN / CG >= 64, "pair mode: >= 64 B columns per CTA");
   constexpr int MROWS = BM * CG * MH;                 // output rows per tile
+  // TF = 1 (tf32 storage, reading Z28): fp32 containers holding tf32 values, kind::tf32 MMAs.
+  // A stage still holds one 128-byte swizzle row per operand row, so it covers 32 K elements
+  // instead of 64 and every byte count of the ring is unchanged.
+  static_assert(!TF || (CONV == CONV_NONE && TPS_SGD_STG), "tf32: Linear GEMMs, STG update write-back");
+  constexpr int ESZ = TF ? 4 : 2;                     // operand element bytes
+  constexpr int BKE = 128 / ESZ;                      // K elements per stage
+  constexpr int MNC = 128 / ESZ;                      // MN elements per MN-major swizzle row
+  constexpr int CHB = MNC * BKE * ESZ;                // bytes of one MN-major box (MNC x BKE)
+  constexpr int KSTEP_MN = (TF ? 8 : 16) * 128;       // MN-major descriptor advance per MMA (K rows x 128 B)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1 KiB alignment by pointer arithmetic on the __shared__ array itself, so every derived
   // pointer keeps the shared address space (LDS/STS rather than generic LD/ST)
@@ -212,7 +221,7 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG, MH>::THREADS, 1)
   const int cid = blockIdx.x / CG, ncl = gridDim.x / CG;
   const int num_m = (args.M + MROWS - 1) / MROWS;
   const int num_n = (args.N + BN - 1) / BN;
-  const int num_k = (args.K + BK - 1) / BK;
+  const int num_k = (args.K + BKE - 1) / BKE;
   // split-K (args.splits > 1, plain fp32 epilogue only): tile t covers K blocks
   // [ks·kper, min(num_k, (ks+1)·kper)) of output tile t mod (num_m·num_n), ks = t / (num_m·num_n)
   const int num_tiles = num_m * num_n * args.splits;
@@ -327,10 +336,10 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG, MH>::THREADS, 1)
             const int n_img = m0 / P, rem = m0 - n_img * P, h0 = rem / args.cv.W, w0 = rem - h0 * args.cv.W;
             ld4(sA, &tmA, c0, w0 + khw % 3 - 1, h0 + khw / 3 - 1, n_img);
           } else if (!A_MN) {
-            ld2(sA, &tmA, kb * BK, m0);
+            ld2(sA, &tmA, kb * BKE, m0);
           } else {
 #pragma unroll
-            for (int i = 0; i < BM / 64; ++i) ld2(sA + i * 8192, &tmA, m0 + 64 * i, kb * BK);
+            for (int i = 0; i < BM / MNC; ++i) ld2(sA + i * CHB, &tmA, m0 + MNC * i, kb * BKE);
           }
           }   // h
           // ---- B tile: BN/CG rows (K-major) or BN/CG columns (MN-major) x 64 K
@@ -372,13 +381,13 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG, MH>::THREADS, 1)
               ld4(dB + i * 8192, &tmB, ci0, w0 + khw % 3 - 1, h0 + khw / 3 - 1, n_img);
             }
           } else if (!B_MN) {
-            ldb2(dB, &tmB, kb * BK, n0);
-            if (BLEND) ldb2(dB + C::B_BYTES, &tmB2, kb * BK, n0);
+            ldb2(dB, &tmB, kb * BKE, n0);
+            if (BLEND) ldb2(dB + C::B_BYTES, &tmB2, kb * BKE, n0);
           } else {
 #pragma unroll
-            for (int i = 0; i < BN / CG / 64; ++i) {
-              ldb2(dB + i * 8192, &tmB, n0 + 64 * i, kb * BK);
-              if (BLEND) ldb2(dB + C::B_BYTES + i * 8192, &tmB2, n0 + 64 * i, kb * BK);
+            for (int i = 0; i < BN / CG / MNC; ++i) {
+              ldb2(dB + i * CHB, &tmB, n0 + MNC * i, kb * BKE);
+              if (BLEND) ldb2(dB + C::B_BYTES + i * CHB, &tmB2, n0 + MNC * i, kb * BKE);
             }
           }
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
@@ -388,7 +397,8 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG, MH>::THREADS, 1)
   } else if (warp == 1) {
     // ===================== MMA issuer =====================
     if (lane == 0 && rank == 0) {
-      constexpr uint32_t idesc = ptx::make_idesc_bf16(BM * CG, BN, A_MN, B_MN);
+      constexpr uint32_t idesc = TF ? ptx::make_idesc_tf32(BM * CG, BN, A_MN, B_MN)
+                                    : ptx::make_idesc_bf16(BM * CG, BN, A_MN, B_MN);
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
@@ -407,18 +417,27 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG, MH>::THREADS, 1)
           const uint32_t a_addr = ptx::smem_u32(stages + stage * C::STAGE_BYTES);
           const uint32_t b_addr = a_addr + MH * A_BYTES;
 #pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk) {
-            // K-major SW128: +32 B per 16-element K step, SBO = 8 rows x 128 B
-            // MN-major SW128: +16 K-rows x 128 B per step, LBO = 64-element MN chunk (8 KiB), SBO = 1 KiB
-            const uint64_t bd = B_MN ? ptx::make_sdesc_sw128(b_addr + kk * 2048, 8192, 1024)
-                                     : ptx::make_sdesc_sw128(b_addr + kk * 32, 16, 1024);
+          for (int kk = 0; kk < 4; ++kk) {   // 4 MMAs per stage: K = 16 (bf16) or 8 (tf32) each
+            // K-major SW128: +32 B per MMA K step, SBO = 8 rows x 128 B
+            // MN-major SW128: +16 (bf16) / 8 (tf32) K-rows x 128 B per step, LBO = one MN chunk box
+            // (64 bf16 / 32 tf32 columns: CHB bytes), SBO = 1 KiB
+            // (tf32 MN-major: SWIZZLE_128B_BASE32B, SBO = 4 rows x 128 B)
+            auto mn_desc = [&](uint32_t addr) {
+              return TF ? ptx::make_sdesc_sw128_base32b(addr, CHB, 512) : ptx::make_sdesc_sw128(addr, CHB, 1024);
+            };
+            const uint64_t bd = B_MN ? mn_desc(b_addr + kk * KSTEP_MN) : ptx::make_sdesc_sw128(b_addr + kk * 32, 16, 1024);
 #pragma unroll
             for (int h = 0; h < MH; ++h) {   // MH = 2: both row halves reuse this B tile
               const uint32_t ah = a_addr + h * A_BYTES;
-              const uint64_t ad = A_MN ? ptx::make_sdesc_sw128(ah + kk * 2048, 8192, 1024)
-                                       : ptx::make_sdesc_sw128(ah + kk * 32, 16, 1024);
-              if (CG == 2) ptx::umma_f16_cg2(d_tmem + h * BN, ad, bd, idesc, (kb != kb0) || (kk != 0));
-              else ptx::umma_f16(d_tmem + h * BN, ad, bd, idesc, (kb != kb0) || (kk != 0));
+              const uint64_t ad = A_MN ? mn_desc(ah + kk * KSTEP_MN) : ptx::make_sdesc_sw128(ah + kk * 32, 16, 1024);
+              const uint32_t acc_on = (kb != kb0) || (kk != 0);
+              if (TF) {
+                if (CG == 2) ptx::umma_tf32_cg2(d_tmem + h * BN, ad, bd, idesc, acc_on);
+                else ptx::umma_tf32(d_tmem + h * BN, ad, bd, idesc, acc_on);
+              } else {
+                if (CG == 2) ptx::umma_f16_cg2(d_tmem + h * BN, ad, bd, idesc, acc_on);
+                else ptx::umma_f16(d_tmem + h * BN, ad, bd, idesc, acc_on);
+              }
             }
           }
           if (CG == 2) ptx::umma_commit_cg2_mc(&empty[stage], 0x3);
@@ -570,8 +589,12 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG, MH>::THREADS, 1)
             if (grow < args.M && gcol < args.N) {
               __stcs(reinterpret_cast<float4*>(args.w + grow * ld + gcol), wv);
               if (mom) __stcs(reinterpret_cast<float4*>(args.v + grow * ld + gcol), vv);
-              *reinterpret_cast<uint2*>(args.ver + grow * ld + gcol) =
-                  make_uint2(pack_bf16(wv.x, wv.y), pack_bf16(wv.z, wv.w));   // new bf16 version
+              if (TF)   // new tf32 version
+                *reinterpret_cast<float4*>(reinterpret_cast<float*>(args.ver) + grow * ld + gcol) =
+                    make_float4(ptx::rna_tf32(wv.x), ptx::rna_tf32(wv.y), ptx::rna_tf32(wv.z), ptx::rna_tf32(wv.w));
+              else      // new bf16 version
+                *reinterpret_cast<uint2*>(args.ver + grow * ld + gcol) =
+                    make_uint2(pack_bf16(wv.x, wv.y), pack_bf16(wv.z, wv.w));
             }
           }
           ptx::fence_proxy_async_smem();   // generic reads of the buffer before the async refill
@@ -678,7 +701,20 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG, MH>::THREADS, 1)
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.0f);
         }
-        if (args.mask) {
+        if (args.mask && TF) {   // fp32 (tf32) mask source: positive = sign clear, nonzero
+          const uint4* mp = reinterpret_cast<const uint4*>(reinterpret_cast<const uint32_t*>(args.mask) +
+                                                           static_cast<size_t>(grow) * args.ldm + gcol);
+#pragma unroll
+          for (int ch = 0; ch < 8; ++ch) {
+            if ((ch >> 1) < nchunk) {
+              const uint4 mv = __ldg(mp + ch);
+              const uint32_t w[4] = {mv.x, mv.y, mv.z, mv.w};
+#pragma unroll
+              for (int e2 = 0; e2 < 4; ++e2)
+                if (!(((w[e2] & 0x80000000u) == 0u) && ((w[e2] & 0x7FFFFFFFu) != 0u))) v[ch * 4 + e2] = 0.0f;
+            }
+          }
+        } else if (args.mask) {
           const uint4* mp = reinterpret_cast<const uint4*>(args.mask + static_cast<size_t>(grow) * args.ldm + gcol);
 #pragma unroll
           for (int ch = 0; ch < 4; ++ch) {
@@ -694,7 +730,7 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG, MH>::THREADS, 1)
             }
           }
         }
-        if (args.addend) {
+        if (args.addend && !TF) {
           const uint4* ap = reinterpret_cast<const uint4*>(args.addend + static_cast<size_t>(grow) * args.ldo + gcol);
 #pragma unroll
           for (int ch = 0; ch < 4; ++ch) {
@@ -707,7 +743,20 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG, MH>::THREADS, 1)
             }
           }
         }
-        if (args.out_f32) {
+        if (TF && !args.out_f32) {   // tf32 store (reading Z28)
+          float* op = reinterpret_cast<float*>(outp) + static_cast<size_t>(grow) * args.ldo + gcol;
+#pragma unroll
+          for (int ch = 0; ch < 4; ++ch) {
+            if (ch < nchunk) {
+              reinterpret_cast<float4*>(op + ch * 8)[0] =
+                  make_float4(ptx::rna_tf32(v[ch * 8]), ptx::rna_tf32(v[ch * 8 + 1]), ptx::rna_tf32(v[ch * 8 + 2]),
+                              ptx::rna_tf32(v[ch * 8 + 3]));
+              reinterpret_cast<float4*>(op + ch * 8)[1] =
+                  make_float4(ptx::rna_tf32(v[ch * 8 + 4]), ptx::rna_tf32(v[ch * 8 + 5]), ptx::rna_tf32(v[ch * 8 + 6]),
+                              ptx::rna_tf32(v[ch * 8 + 7]));
+            }
+          }
+        } else if (args.out_f32) {
           float* op = reinterpret_cast<float*>(outp) + static_cast<size_t>(grow) * args.ldo + gcol;
 #pragma unroll
           for (int ch = 0; ch < 4; ++ch) {
@@ -739,7 +788,8 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG, MH>::THREADS, 1)
           float a[32], q2[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
-            const float x = !live ? 0.0f : (args.out_f32 ? v[i] : __bfloat162float(__float2bfloat16_rn(v[i])));
+            const float x = !live ? 0.0f
+                                  : (args.out_f32 ? v[i] : (TF ? ptx::rna_tf32(v[i]) : __bfloat162float(__float2bfloat16_rn(v[i]))));
             a[i] = x;
             q2[i] = x * x;
           }
@@ -772,10 +822,17 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG, MH>::THREADS, 1)
         const uint4* l = reinterpret_cast<const uint4*>(sB + C::B_BYTES);
 #pragma unroll
         for (int i = tt; i < (TPS_DBG_XF ? 0 : C::B_BYTES / 16); i += XF_WARPS * 32) {
-          const uint4 a = s[i];
-          const uint4 b = l[i];
-          s[i] = make_uint4(ptx::blend_bf16x2(a.x, b.x, xa2, xb2), ptx::blend_bf16x2(a.y, b.y, xa2, xb2),
-                            ptx::blend_bf16x2(a.z, b.z, xa2, xb2), ptx::blend_bf16x2(a.w, b.w, xa2, xb2));
+          if (TF) {   // 4 tf32 values per 16-byte chunk
+            const ulonglong2 a = reinterpret_cast<const ulonglong2*>(s)[i];
+            const ulonglong2 b = reinterpret_cast<const ulonglong2*>(l)[i];
+            reinterpret_cast<ulonglong2*>(s)[i] =
+                make_ulonglong2(ptx::blend_tf32x2(a.x, b.x, xa2, xb2), ptx::blend_tf32x2(a.y, b.y, xa2, xb2));
+          } else {
+            const uint4 a = s[i];
+            const uint4 b = l[i];
+            s[i] = make_uint4(ptx::blend_bf16x2(a.x, b.x, xa2, xb2), ptx::blend_bf16x2(a.y, b.y, xa2, xb2),
+                              ptx::blend_bf16x2(a.z, b.z, xa2, xb2), ptx::blend_bf16x2(a.w, b.w, xa2, xb2));
+          }
         }
         ptx::fence_proxy_async_smem();
         __syncwarp();                   // one arrival per warp once all its lanes have fenced
@@ -1171,6 +1228,25 @@ bool make_tmap(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, u
   return r == CUDA_SUCCESS;
 }
 
+// 2-D operand tensor [rows, cols] (cols contiguous, ld elements) of bf16 (box {64, box_rows}) or,
+// tf = 1, of fp32-held tf32 values (box {32, box_rows}): one 128-byte swizzled row per box row
+// (mn = 1: the tile is an MN-major operand; tf32 MN-major operands use the 32-byte-atom 128-byte
+// swizzle, the only MN-major smem layout kind::tf32 reads)
+bool make_tmap_t(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint64_t ld, uint32_t box_rows,
+                 int tf, int mn) {
+  if (!tf) return make_tmap(m, base, rows, cols, ld, box_rows);
+  EncodeTiledFn enc = get_encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {ld * 4};
+  cuuint32_t box[2] = {32, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, mn ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 // 2-D tensor of any element type with an explicit box and swizzle (fused-update epilogue boxes)
 bool make_tmap_box(CUtensorMap* m, const void* base, CUtensorMapDataType dt, uint32_t esize, uint64_t rows,
                    uint64_t cols, uint64_t ld, uint32_t box_cols, uint32_t box_rows, CUtensorMapSwizzle sw) {
@@ -1280,11 +1356,11 @@ struct EpiMaps {
   CUtensorMap w, v, q;   // fused update: fp32 master, fp32 momentum, bf16 version (32x32 boxes)
 };
 
-template <int BN, int A_MN, int B_MN, int BLEND, int SGD = 0, int CG = 1, int CONV = CONV_NONE, int MH = 1>
+template <int BN, int A_MN, int B_MN, int BLEND, int SGD = 0, int CG = 1, int CONV = CONV_NONE, int MH = 1, int TF = 0>
 cudaError_t launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& b2, const EpiMaps& em,
                    const GemmArgs& args, cudaStream_t st) {
   using C = Cfg<BN, BLEND, SGD, CG, MH>;
-  auto kern = gemm_kernel<BN, A_MN, B_MN, BLEND, SGD, CG, CONV, MH>;
+  auto kern = gemm_kernel<BN, A_MN, B_MN, BLEND, SGD, CG, CONV, MH, TF>;
   static bool attr_set = false;   // per instantiation
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
@@ -1407,16 +1483,16 @@ Tiling pick_tiling(int M, int N, int K, int mode, bool sgd, int max_ctas = 0) {
   return {1, 64};
 }
 
-template <int A_MN, int B_MN, int SGD, int CONV = CONV_NONE>
+template <int A_MN, int B_MN, int SGD, int CONV = CONV_NONE, int TF = 0>
 cudaError_t dispatch(const Tiling& tl, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tb2,
                      const EpiMaps& em, const GemmArgs& args, cudaStream_t st) {
   if (tl.cg == 2) {
-    if (tl.bn == 256) return launch<256, A_MN, B_MN, 0, SGD, 2, CONV>(ta, tb, tb2, em, args, st);
-    return launch<128, A_MN, B_MN, 0, SGD, 2, CONV>(ta, tb, tb2, em, args, st);
+    if (tl.bn == 256) return launch<256, A_MN, B_MN, 0, SGD, 2, CONV, 1, TF>(ta, tb, tb2, em, args, st);
+    return launch<128, A_MN, B_MN, 0, SGD, 2, CONV, 1, TF>(ta, tb, tb2, em, args, st);
   }
-  if (tl.bn == 256) return launch<256, A_MN, B_MN, 0, SGD, 1, CONV>(ta, tb, tb2, em, args, st);
-  if (tl.bn == 128) return launch<128, A_MN, B_MN, 0, SGD, 1, CONV>(ta, tb, tb2, em, args, st);
-  return launch<64, A_MN, B_MN, 0, SGD, 1, CONV>(ta, tb, tb2, em, args, st);
+  if (tl.bn == 256) return launch<256, A_MN, B_MN, 0, SGD, 1, CONV, 1, TF>(ta, tb, tb2, em, args, st);
+  if (tl.bn == 128) return launch<128, A_MN, B_MN, 0, SGD, 1, CONV, 1, TF>(ta, tb, tb2, em, args, st);
+  return launch<64, A_MN, B_MN, 0, SGD, 1, CONV, 1, TF>(ta, tb, tb2, em, args, st);
 }
 
 }  // namespace
@@ -1455,13 +1531,16 @@ cudaError_t gemm_run(int mode, const GemmOperands& op, const GemmArgs& args_in, 
   GemmArgs args = args_in;
   if (args.M <= 0 || args.N <= 0 || args.K <= 0) return cudaSuccess;
   const bool sgd = ((mode == GEMM_WGRAD || mode == GEMM_CONV_WGRAD) && args.epi == EPI_SGD);
+  if (args.tf32 && (mode >= GEMM_CONV_FWD || args.addend)) return cudaErrorInvalidValue;
   Tiling tl = pick_tiling(args.M, args.N, args.K, mode, sgd, args.max_ctas);
+  if (args.tf32) tl.splits = 1;                      // tf32: one pass over K
   if (tl.splits > 1 &&
       (!args.ws || args.ws_floats < static_cast<int64_t>(tl.splits) * args.M * args.ldo || !args.out_f32 ||
        args.ldo != args.N))
     tl.splits = 1;                                   // no workspace supplied: one pass over K
   args.splits = tl.splits;
-  args.kper = tl.splits > 1 ? tl.kper : (args.K + BK - 1) / BK;
+  const int bke = args.tf32 ? 32 : BK;             // K elements per pipeline stage
+  args.kper = tl.splits > 1 ? tl.kper : (args.K + bke - 1) / bke;
   CUtensorMap ta, tb, tb2;
   bool ok = true;
   if (mode >= GEMM_CONV_FWD) {
@@ -1518,11 +1597,13 @@ cudaError_t gemm_run(int mode, const GemmOperands& op, const GemmArgs& args_in, 
     const bool b_mn = (mode != GEMM_FWD);
     // A: K-major [M,K] -> box {64 K, 128 rows}; MN-major stored [K,M] -> box {64 M, 64 K}
     // B: K-major [N,K] -> box {64 K, BN/CG rows} (each CTA of a pair loads its share)
-    if (!a_mn) ok &= make_tmap(&ta, op.A, args.M, args.K, op.lda, BM);
-    else ok &= make_tmap(&ta, op.A, args.K, args.M, op.lda, 64);
-    if (!b_mn) ok &= make_tmap(&tb, op.B, args.N, args.K, op.ldb, tl.bn / tl.cg);
-    else ok &= make_tmap(&tb, op.B, args.K, args.N, op.ldb, 64);
-    if (mode == GEMM_DGRAD_BLEND) ok &= make_tmap(&tb2, op.B2, args.K, args.N, op.ldb, 64);
+    // (tf32: box {32, ·}; MN-major boxes 32 x 32)
+    const int tf = args.tf32;
+    if (!a_mn) ok &= make_tmap_t(&ta, op.A, args.M, args.K, op.lda, BM, tf, 0);
+    else ok &= make_tmap_t(&ta, op.A, args.K, args.M, op.lda, bke, tf, 1);
+    if (!b_mn) ok &= make_tmap_t(&tb, op.B, args.N, args.K, op.ldb, tl.bn / tl.cg, tf, 0);
+    else ok &= make_tmap_t(&tb, op.B, args.K, args.N, op.ldb, bke, tf, 1);
+    if (mode == GEMM_DGRAD_BLEND) ok &= make_tmap_t(&tb2, op.B2, args.K, args.N, op.ldb, bke, tf, 1);
     else tb2 = tb;
   }
   EpiMaps em;
@@ -1538,6 +1619,21 @@ cudaError_t gemm_run(int mode, const GemmOperands& op, const GemmArgs& args_in, 
   if (!ok) return cudaErrorInvalidValue;
   if (bn_out) *bn_out = tl.bn * 10 + tl.cg;
   cudaError_t e = cudaErrorInvalidValue;
+  if (args.tf32) {
+    switch (mode) {
+      case GEMM_FWD: return dispatch<0, 0, 0, CONV_NONE, 1>(tl, ta, tb, tb2, em, args, st);
+      case GEMM_DGRAD: return dispatch<0, 1, 0, CONV_NONE, 1>(tl, ta, tb, tb2, em, args, st);
+      case GEMM_WGRAD:
+        return sgd ? dispatch<1, 1, 1, CONV_NONE, 1>(tl, ta, tb, tb2, em, args, st)
+                   : dispatch<1, 1, 0, CONV_NONE, 1>(tl, ta, tb, tb2, em, args, st);
+      case GEMM_DGRAD_BLEND:
+        if (tl.cg == 2)
+          return blend_mh2(args) ? launch<256, 0, 1, 1, 0, 2, CONV_NONE, 2, 1>(ta, tb, tb2, em, args, st)
+                                 : launch<256, 0, 1, 1, 0, 2, CONV_NONE, 1, 1>(ta, tb, tb2, em, args, st);
+        return launch<128, 0, 1, 1, 0, 1, CONV_NONE, 1, 1>(ta, tb, tb2, em, args, st);
+      default: return cudaErrorInvalidValue;
+    }
+  }
   switch (mode) {
     case GEMM_FWD: e = dispatch<0, 0, 0>(tl, ta, tb, tb2, em, args, st); break;
     case GEMM_DGRAD: e = dispatch<0, 1, 0>(tl, ta, tb, tb2, em, args, st); break;
@@ -1575,7 +1671,7 @@ cudaError_t gemm_bwd_dual(const GemmOperands& opw, const GemmArgs& aw_in, const 
   constexpr int BN = 256, CG = 2;
   using C = Cfg<BN, 0, 1, CG>;
   GemmArgs aw = aw_in;
-  if (aw.epi != EPI_SGD || aw.M < BM * CG || dg.M < BM * CG || aw.N <= BN / 2 || dg.N <= BN / 2 || aw.K <= 0 ||
+  if (aw.tf32 || aw.epi != EPI_SGD || aw.M < BM * CG || dg.M < BM * CG || aw.N <= BN / 2 || dg.N <= BN / 2 || aw.K <= 0 ||
       dg.K <= 0 || (dg.N & 7) || (aw.N & 7))
     return cudaErrorNotSupported;
   const int n_w = ((aw.M + BM * CG - 1) / (BM * CG)) * ((aw.N + BN - 1) / BN);

@@ -10,8 +10,9 @@ namespace tps {
 //   g' = g + wd·w ; v = μ·v + g' ; w = w - lr·v   (fp32, one rounding per op, PyTorch order)
 //   ver = bf16_rne(w)  (skipped if ver == nullptr).  μ == 0 => v untouched (14 B/param).
 // blocks_per_sm bounds the grid (a small grid lets the update run underneath a persistent GEMM).
+// tf = 1: ver is an fp32 array that receives tf32_rna(w) (tf32 storage, reading Z28).
 cudaError_t launch_sgd_update(float* w, float* v, const float* g, uint16_t* ver, int64_t n, float lr, float mu,
-                              float wd, cudaStream_t st, int blocks_per_sm = 8);
+                              float wd, cudaStream_t st, int blocks_per_sm = 8, int tf = 0);
 
 // Data parallelism (NEXT-2): the gradients of the R replicas of a stage (own + peers' mapped
 // buffers), averaged in replica order g = (Σ_r g_r)·(1/R) and applied as launch_sgd_update does.
@@ -26,14 +27,15 @@ cudaError_t launch_sgd_update_dp(float* w, float* v, const GradList& g, uint16_t
 // db[c] = Σ_{r<rows} G[r, c] for c < cols (G bf16 [rows, ldg]); deterministic two-phase
 // reduction using `scratch` (>= bias_grad_scratch_floats(rows, cols) floats).
 int64_t bias_grad_scratch_floats(int rows, int cols);
+// (tf = 1: G is an fp32 array of tf32 values, reading Z28; same for launch_bias_grad_sgd)
 cudaError_t launch_bias_grad(const uint16_t* G, int rows, int cols, int ldg, float* db, float* scratch,
-                             cudaStream_t st);
+                             cudaStream_t st, int tf = 0);
 // The same column sums in ONE launch (the last block of each column block finishes the
 // fixed-order reduction; its arrival counters live at the end of `scratch` and reset
 // themselves), followed, if b != nullptr, by the SGD/momentum step of launch_sgd_update on the
 // fp32 bias b and its momentum vb (same operations, same bits).  Bit-identical db.
 cudaError_t launch_bias_grad_sgd(const uint16_t* G, int rows, int cols, int ldg, float* db, float* scratch, float* b,
-                                 float* vb, float lr, float mu, float wd, cudaStream_t st);
+                                 float* vb, float lr, float mu, float wd, cudaStream_t st, int tf = 0);
 
 // db[c] = Σ_g part[g·cols + c] (the 32-row column sums a GEMM epilogue wrote, GemmArgs.colsum;
 // fixed order, fp64 accumulation), then the bias SGD/momentum step if b != nullptr.
@@ -43,8 +45,9 @@ cudaError_t launch_bias_from_colsum(const float* part, int groups, int cols, flo
 // Softmax cross-entropy forward+backward for `rows` rows of fp32 logits [rows, ldl] with
 // `classes` valid columns: loss_rows[r] = logsumexp(z) - z_y ;
 // G[r, c] = bf16((softmax(z)_c - [c == y]) / batch) for c < classes, 0 for classes <= c < ldg.
+// (tf = 1: G is an fp32 array receiving tf32_rna of the same value)
 cudaError_t launch_softmax_xent(const float* logits, int ldl, const int32_t* labels, int rows, int classes,
-                                int batch, float* loss_rows, uint16_t* G, int ldg, cudaStream_t st);
+                                int batch, float* loss_rows, uint16_t* G, int ldg, cudaStream_t st, int tf = 0);
 
 // losses[*ctr] = (Σ_{r<rows} loss_rows[r]) / rows, then ++*ctr  (fixed-order fp64 reduction, one
 // block; the device-side slot counter lets a replayed CUDA graph append)
@@ -52,6 +55,12 @@ cudaError_t launch_loss_mean(const float* loss_rows, int rows, float* losses, in
 
 // fp32 -> bf16 RNE, n elements
 cudaError_t launch_f32_to_bf16(const float* in, uint16_t* out, int64_t n, cudaStream_t st);
+
+// fp32 -> tf32 (RNA, fp32 container), n elements
+cudaError_t launch_f32_to_tf32(const float* in, float* out, int64_t n, cudaStream_t st);
+// K8 debug materialiser in tf32 storage: out = tf32_rna(fp32(α·s) + fp32(β·l))
+cudaError_t launch_blend_materialize_tf32(const float* s, const float* l, float* out, int64_t n, float a, float b,
+                                         cudaStream_t st);
 
 // K8 debug materialiser: out = bf16(fp32(α·s) + fp32(β·l))
 cudaError_t launch_blend_materialize(const uint16_t* s, const uint16_t* l, uint16_t* out, int64_t n, float a,

@@ -131,6 +131,25 @@ __device__ __forceinline__ uint32_t blend_bf16x2(uint32_t a, uint32_t b, uint64_
       : "r"(a), "r"(b), "l"(xa2), "l"(xb2));
   return out;
 }
+// tf32 storage (reading Z28): round an fp32 value to the nearest tf32 value, ties away from zero;
+// the result is an fp32 bit pattern whose 13 low mantissa bits are zero
+__device__ __forceinline__ float rna_tf32(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+// tf32(fma(xb, b, fp32(xa·a))) on two fp32 pairs (the tf32 twin of blend_bf16x2)
+__device__ __forceinline__ uint64_t blend_tf32x2(uint64_t a, uint64_t b, uint64_t xa2, uint64_t xb2) {
+  uint64_t t;
+  asm("{\n\t.reg .b64 pa;\n\tmul.rn.f32x2 pa, %1, %3;\n\tfma.rn.f32x2 %0, %2, %4, pa;\n\t}"
+      : "=l"(t)
+      : "l"(a), "l"(b), "l"(xa2), "l"(xb2));
+  float lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(t));
+  uint64_t out;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(out) : "f"(rna_tf32(lo)), "f"(rna_tf32(hi)));
+  return out;
+}
 // generic-proxy smem writes -> visible to the async proxy (tensor core / TMA)
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -240,6 +259,28 @@ __device__ __forceinline__ void tmem_dealloc_cg2(uint32_t taddr, uint32_t ncols)
   asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
 }
 // 2-SM MMA (issued by the leader CTA): D[256 x N] over the pair, A/B halves in each CTA's smem
+__device__ __forceinline__ void umma_tf32_cg2(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                              uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
 __device__ __forceinline__ void umma_f16_cg2(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                              uint32_t accumulate) {
   asm volatile(
@@ -326,12 +367,31 @@ __device__ __forceinline__ uint64_t make_sdesc_sw128(uint32_t saddr, uint32_t lb
   return d;
 }
 
+// MN-major tf32 operands (32-bit elements): the only UMMA smem layout is SWIZZLE_128B_BASE32B
+// (descriptor layout type 1): 128-byte rows, 32-byte chunks XOR-ed with (row mod 4) — what a TMA
+// load with CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B writes.  LBO = stride between 128-byte MN chunks,
+// SBO = stride between 4-row K groups.
+__device__ __forceinline__ uint64_t make_sdesc_sw128_base32b(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+  d |= static_cast<uint64_t>((lbo_bytes >> 4) & 0x3FFF) << 16;
+  d |= static_cast<uint64_t>((sbo_bytes >> 4) & 0x3FFF) << 32;
+  d |= static_cast<uint64_t>(1) << 46;
+  d |= static_cast<uint64_t>(1) << 61;
+  return d;
+}
+
 // Instruction descriptor for kind::f16: bf16 A/B, fp32 D, M x N, A/B major (0 = K, 1 = MN).
 __host__ __device__ constexpr uint32_t make_idesc_bf16(uint32_t M, uint32_t N, uint32_t a_mn, uint32_t b_mn) {
   return (1u << 4)            // D format f32
          | (1u << 7)          // A format bf16
          | (1u << 10)         // B format bf16
          | (a_mn << 15) | (b_mn << 16) | ((N >> 3) << 17) | ((M >> 4) << 24);
+}
+
+// kind::tf32 instruction descriptor: D f32, A / B format tf32 (2), K = 8 per instruction
+__host__ __device__ constexpr uint32_t make_idesc_tf32(uint32_t M, uint32_t N, uint32_t a_mn, uint32_t b_mn) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | (a_mn << 15) | (b_mn << 16) | ((N >> 3) << 17) | ((M >> 4) << 24);
 }
 
 }  // namespace ptx

@@ -149,6 +149,10 @@ struct tps_pipeline {
   uint64_t seed = 0;
   bool first = true, last = true, eq1_on_load = false, fuse_update = false;
   bool graph = false;                        // ResNet-style layer graph (CONV/BN/MAXPOOL3/AVGPOOL)
+  // storage precision (reading Z28): bf16 (ew = 1 uint16 unit per element, 2 bytes) or tf32 values
+  // in fp32 containers (ew = 2, 4 bytes).  Buffers stay typed uint16_t*; offsets scale by ew.
+  bool tf = false;
+  int ew = 1, esz = 2;
   int staleness_mode = 0;                    // 1: explicit δ may be any live version (microbenchmark)
   void* (*alloc_fn)(size_t, void*) = nullptr;   // caller's device allocator (tps_config.dev_alloc)
   void (*free_fn)(void*, void*) = nullptr;
@@ -368,6 +372,7 @@ tps_status run_gemm(tps_pipeline* p, int mode, const tps::GemmOperands& op, cons
   tps::GemmArgs a2 = args;
   a2.ws = p->splitk_ws;
   a2.ws_floats = p->splitk_floats;
+  a2.tf32 = p->tf ? 1 : 0;
   CUDA_OK(tps::gemm_run(mode, op, a2, gs));
   p->launches += 1;
   if (p->profiling) {
@@ -507,7 +512,7 @@ tps_status send_fwd(tps_pipeline* p, int64_t j, int grp, const void* src, size_t
   CUDA_OK(cudaEventRecord(p->ev_fwd_ready[e], p->cs));
   if (p->transport == TPS_TRANSPORT_NCCL) {
     CUDA_OK(cudaStreamWaitEvent(p->s_fout, p->ev_fwd_ready[e], 0));
-    NCCL_OK(ncclSend(src, bytes / 2, ncclBfloat16, 1, p->c_fout, p->s_fout));
+    NCCL_OK(ncclSend(src, bytes / p->esz, p->tf ? ncclFloat32 : ncclBfloat16, 1, p->c_fout, p->s_fout));
     CUDA_OK(cudaEventRecord(p->ev_fwd_sent[e], p->s_fout));
   } else if (p->transport == TPS_TRANSPORT_IPC) {
     const uint64_t seq = static_cast<uint64_t>(j) * p->ng + grp + 1;
@@ -516,7 +521,7 @@ tps_status send_fwd(tps_pipeline* p, int64_t j, int grp, const void* src, size_t
       CUDA_OK(cudaStreamWaitEvent(p->s_fout, p->ev_fwd_ready[e], 0));
       TPS_TRY(flag_wait(p->s_fout, &p->flags[2], static_cast<uint64_t>(std::max<int64_t>(0, j - nA0 + 1))));
       uint16_t* dst = p->next_in[j % nA0] + static_cast<size_t>(grp) * p->g * p->bsz *
-                                                 p->layers[p->nlayers() - 1].out_elems();
+                                                 p->layers[p->nlayers() - 1].out_elems() * p->ew;
       CUDA_OK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, p->s_fout));
       TPS_TRY(flag_write(p->s_fout, &p->next_flags[0], seq));
       CUDA_OK(cudaEventRecord(p->ev_fwd_sent[e], p->s_fout));
@@ -535,7 +540,7 @@ tps_status recv_fwd(tps_pipeline* p, int64_t j, int grp, void* dst, size_t bytes
   const int slot = static_cast<int>(j % p->A0);
   CUDA_OK(cudaStreamWaitEvent(p->s_fin, p->ev_act_free[slot], 0));
   if (p->transport == TPS_TRANSPORT_NCCL) {
-    NCCL_OK(ncclRecv(dst, bytes / 2, ncclBfloat16, 0, p->c_fin, p->s_fin));
+    NCCL_OK(ncclRecv(dst, bytes / p->esz, p->tf ? ncclFloat32 : ncclBfloat16, 0, p->c_fin, p->s_fin));
   } else if (p->transport == TPS_TRANSPORT_IPC) {
     // the previous stage stores straight into this slot; wait for its announcement
     TPS_TRY(flag_wait(p->s_fin, &p->flags[0], static_cast<uint64_t>(j) * p->ng + grp + 1));
@@ -559,7 +564,7 @@ tps_status send_bwd(tps_pipeline* p, int64_t j, const void* src, size_t bytes) {
   CUDA_OK(cudaEventRecord(p->ev_gout_ready, p->cs));
   if (p->transport == TPS_TRANSPORT_NCCL) {
     CUDA_OK(cudaStreamWaitEvent(p->s_bout, p->ev_gout_ready, 0));
-    NCCL_OK(ncclSend(src, bytes / 2, ncclBfloat16, 0, p->c_bout, p->s_bout));
+    NCCL_OK(ncclSend(src, bytes / p->esz, p->tf ? ncclFloat32 : ncclBfloat16, 0, p->c_bout, p->s_bout));
     CUDA_OK(cudaEventRecord(p->ev_bwd_sent[e], p->s_bout));
   } else if (p->transport == TPS_TRANSPORT_IPC) {
     if (!p->ipc_direct) {
@@ -586,7 +591,7 @@ tps_status recv_bwd(tps_pipeline* p, int64_t j, void* dst, size_t bytes) {
   const int e = static_cast<int>(j & 1);
   CUDA_OK(cudaStreamWaitEvent(p->s_bin, p->ev_gin_free[e], 0));
   if (p->transport == TPS_TRANSPORT_NCCL) {
-    NCCL_OK(ncclRecv(dst, bytes / 2, ncclBfloat16, 1, p->c_bin, p->s_bin));
+    NCCL_OK(ncclRecv(dst, bytes / p->esz, p->tf ? ncclFloat32 : ncclBfloat16, 1, p->c_bin, p->s_bin));
   } else if (p->transport == TPS_TRANSPORT_IPC) {
     TPS_TRY(flag_wait(p->s_bin, &p->flags[1], static_cast<uint64_t>(j) + 1));
   } else {
@@ -974,7 +979,7 @@ tps_status do_forward(tps_pipeline* p, int64_t j, int a0, int cnt, const void* x
   const int slot0 = static_cast<int>(j % p->A0);
   const int slot = static_cast<int>(j % p->Kmax);
   Layer& L0 = p->layers[0];
-  uint16_t* X = p->act[slot0][0] + static_cast<size_t>(r0) * (p->graph ? p->in0_elems : L0.in_elems());
+  uint16_t* X = p->act[slot0][0] + static_cast<size_t>(r0) * (p->graph ? p->in0_elems : L0.in_elems()) * p->ew;
   if (p->first && p->graph) {
     CUDA_OK(cudaStreamWaitEvent(p->s_fin, p->ev_act_free[slot0], 0));
     CUDA_OK(cudaMemcpyAsync(X, x, static_cast<size_t>(nr) * p->in0_elems * 2, cudaMemcpyDefault, p->s_fin));
@@ -988,10 +993,10 @@ tps_status do_forward(tps_pipeline* p, int64_t j, int a0, int cnt, const void* x
       uint16_t* xs = p->x_stage[slot0] + static_cast<size_t>(r0) * p->in0_elems;
       CUDA_OK(cudaMemcpyAsync(xs, x, static_cast<size_t>(nr) * p->in0_elems * 2, cudaMemcpyDefault, p->s_fin));
     } else if (L0.kind == TPS_LAYER_LINEAR && L0.in != L0.Kp) {
-      const size_t w = static_cast<size_t>(L0.in) * 2;   // pad the rows to the 16-aligned ld
-      CUDA_OK(cudaMemcpy2DAsync(X, static_cast<size_t>(L0.Kp) * 2, x, w, w, nr, cudaMemcpyDefault, p->s_fin));
+      const size_t w = static_cast<size_t>(L0.in) * p->esz;   // pad the rows to the 16-aligned ld
+      CUDA_OK(cudaMemcpy2DAsync(X, static_cast<size_t>(L0.Kp) * p->esz, x, w, w, nr, cudaMemcpyDefault, p->s_fin));
     } else if (L0.kind == TPS_LAYER_LINEAR) {
-      CUDA_OK(cudaMemcpyAsync(X, x, static_cast<size_t>(nr) * L0.Kp * 2, cudaMemcpyDefault, p->s_fin));
+      CUDA_OK(cudaMemcpyAsync(X, x, static_cast<size_t>(nr) * L0.Kp * p->esz, cudaMemcpyDefault, p->s_fin));
     } else {
       CUDA_OK(cudaMemcpyAsync(X, x, static_cast<size_t>(nr) * L0.in_elems() * 2, cudaMemcpyDefault, p->s_fin));
     }
@@ -1003,7 +1008,7 @@ tps_status do_forward(tps_pipeline* p, int64_t j, int a0, int cnt, const void* x
       p->launches += 1;
     }
   } else {
-    TPS_TRY(recv_fwd(p, j, grp, X, static_cast<size_t>(nr) * (p->graph ? p->in0_elems : L0.in_elems()) * 2));
+    TPS_TRY(recv_fwd(p, j, grp, X, static_cast<size_t>(nr) * (p->graph ? p->in0_elems : L0.in_elems()) * p->esz));
   }
   if (!p->last) {  // the send buffer of mb j-2 must have left
     CUDA_OK(cudaStreamWaitEvent(p->cs, p->ev_fwd_sent[static_cast<int>(j & 1) * p->ng + grp], 0));
@@ -1017,15 +1022,15 @@ tps_status do_forward(tps_pipeline* p, int64_t j, int a0, int cnt, const void* x
     void* out;
     const bool logits = (k == nl - 1) && p->last;
     if (k < nl - 1) {
-      out = p->act[slot][k + 1] + static_cast<size_t>(r0) * Lk.out_elems();
+      out = p->act[slot][k + 1] + static_cast<size_t>(r0) * Lk.out_elems() * p->ew;
     } else if (!p->last && p->ipc_direct) {
       // fused compute + send: the epilogue stores into the next stage's input slot (NVLink peer
       // memory across GPUs) once that stage has freed it (its backward of mb j - A0_next)
       const int nA0 = static_cast<int>(p->next_in.size());
       TPS_TRY(flag_wait(p->cs, &p->flags[2], static_cast<uint64_t>(std::max<int64_t>(0, j - nA0 + 1))));
-      out = p->next_in[j % nA0] + static_cast<size_t>(r0) * Lk.out_elems();
+      out = p->next_in[j % nA0] + static_cast<size_t>(r0) * Lk.out_elems() * p->ew;
     } else if (!p->last) {
-      out = p->send_fwd[j & 1] + static_cast<size_t>(r0) * Lk.out_elems();
+      out = p->send_fwd[j & 1] + static_cast<size_t>(r0) * Lk.out_elems() * p->ew;
     } else {
       out = p->logits + static_cast<size_t>(r0) * Lk.Np;
     }
@@ -1041,7 +1046,8 @@ tps_status do_forward(tps_pipeline* p, int64_t j, int a0, int cnt, const void* x
     }
     CUDA_OK(tps::launch_softmax_xent(p->logits + static_cast<size_t>(r0) * Ll.Np, Ll.Np, lab, nr, p->classes, p->B,
                                      p->loss_rows + r0,
-                                     p->gce + (static_cast<size_t>(slot) * p->B + r0) * Ll.Np, Ll.Np, p->cs));
+                                     p->gce + (static_cast<size_t>(slot) * p->B + r0) * Ll.Np * p->ew, Ll.Np, p->cs,
+                                     p->tf ? 1 : 0));
     p->launches += 1;
     if (a0 + cnt == p->m) {
       if (p->loss_count >= p->loss_cap) return fail(TPS_E_STATE, "loss buffer full (%lld mini-batches)", (long long)p->loss_cap);
@@ -1052,8 +1058,8 @@ tps_status do_forward(tps_pipeline* p, int64_t j, int a0, int cnt, const void* x
   } else {
     Layer& Ll = p->layers[nl - 1];
     uint16_t* sb = p->graph ? p->act[slot][nl] : p->send_fwd[j & 1];   // graph: send from the stash
-    TPS_TRY(send_fwd(p, j, grp, sb + static_cast<size_t>(r0) * Ll.out_elems(),
-                     static_cast<size_t>(nr) * Ll.out_elems() * 2));
+    TPS_TRY(send_fwd(p, j, grp, sb + static_cast<size_t>(r0) * Ll.out_elems() * p->ew,
+                     static_cast<size_t>(nr) * Ll.out_elems() * p->esz));
   }
   tps_event e{};
   e.stage = p->s; e.kind = TPS_EV_F; e.micro = a0; e.micro_count = cnt; e.mb = j;
@@ -1093,9 +1099,9 @@ tps_status do_backward(tps_pipeline* p, int64_t j, int staleness) {
     return fail(TPS_E_ORDER, "stage %d: gradient of mb %lld not sent yet", p->s, (long long)j);
   const uint16_t* G;
   if (p->last) {
-    G = p->gce + static_cast<size_t>(j % p->Kmax) * p->B * Ll.Np;   // slot of mb j (K_s may exceed 1, S = 1)
+    G = p->gce + static_cast<size_t>(j % p->Kmax) * p->B * Ll.Np * p->ew;   // slot of mb j (K_s may exceed 1, S = 1)
   } else {
-    TPS_TRY(recv_bwd(p, j, p->gin[j & 1], static_cast<size_t>(p->B) * Ll.out_elems() * 2));
+    TPS_TRY(recv_bwd(p, j, p->gin[j & 1], static_cast<size_t>(p->B) * Ll.out_elems() * p->esz));
     G = p->gin[j & 1];
   }
   const int slot0 = static_cast<int>(j % p->A0);
@@ -1166,7 +1172,7 @@ tps_status do_backward(tps_pipeline* p, int64_t j, int staleness) {
                                              p->wd, p->s_upd));
       else
         CUDA_OK(tps::launch_bias_grad_sgd(G, B * Lk.hw_out, Lk.Np, Lk.Np, Lk.db, p->scratch_side, Lk.b, Lk.mb, p->lr,
-                                          p->mu, p->wd, p->s_upd));
+                                          p->mu, p->wd, p->s_upd, p->tf ? 1 : 0));
       CUDA_OK(cudaEventRecord(p->split_w ? p->ev_bias_l[k] : p->ev_bias_done, p->s_upd));
       p->launches += 1;
     }
@@ -1296,7 +1302,7 @@ tps_status do_backward(tps_pipeline* p, int64_t j, int staleness) {
                                                Lk.mb, p->lr, p->mu, p->wd, p->cs));
         else
           CUDA_OK(tps::launch_bias_grad_sgd(G, rows, Lk.Np, Lk.Np, Lk.db, p->scratch, p->dp > 1 ? nullptr : Lk.b, Lk.mb,
-                                            p->lr, p->mu, p->wd, p->cs));
+                                            p->lr, p->mu, p->wd, p->cs, p->tf ? 1 : 0));
         p->launches += 1;
       }
       // U(j) always directly follows B(j) in the static order (reading Z7), so the update of
@@ -1313,7 +1319,7 @@ tps_status do_backward(tps_pipeline* p, int64_t j, int staleness) {
         TimedLaunch tl{};
         TPS_TRY(time_begin(p, &tl, 4, (p->mu != 0.f ? 22.0 : 14.0) * n, us));
         CUDA_OK(tps::launch_sgd_update(Lk.W, Lk.mW, Lk.dW, Lk.ver[vn % p->R], n, p->lr, p->mu, p->wd, us,
-                                       p->upd_blocks_per_sm));
+                                       p->upd_blocks_per_sm, p->tf ? 1 : 0));
         TPS_TRY(time_end(p, &tl, us));
         p->launches += 1;
       }
@@ -1359,7 +1365,7 @@ tps_status do_backward(tps_pipeline* p, int64_t j, int staleness) {
     if (!p->last) TPS_TRY(flag_write(p->cs, &p->next_flags[3], static_cast<uint64_t>(j) + 1));
   }
   if (!p->first) {
-    TPS_TRY(send_bwd(p, j, p->gout[j & 1], static_cast<size_t>(p->B) * p->in0_elems * 2));
+    TPS_TRY(send_bwd(p, j, p->gout[j & 1], static_cast<size_t>(p->B) * p->in0_elems * p->esz));
   }
   tps_event e{};
   e.stage = p->s; e.kind = TPS_EV_B; e.micro = -1; e.mb = j;
@@ -1484,7 +1490,7 @@ tps_status fire(tps_pipeline* p, const tps_event& e, const void* x_pool, const i
     const int32_t* y = nullptr;
     // replica r of mini-batch j reads rows [r·B, (r+1)·B) of pool entry j % pool
     const int64_t row = (slot * p->dp + p->dp_rank) * p->B + static_cast<int64_t>(e.micro) * p->bsz;
-    if (p->first) x = static_cast<const uint16_t*>(x_pool) + row * p->dims[0];
+    if (p->first) x = static_cast<const uint16_t*>(x_pool) + row * p->dims[0] * p->ew;
     if (p->last) y = y_pool + row;
     return bracket(p, TPS_EV_F, e.mb, [&] { return do_forward(p, e.mb, e.micro, e.micro_count, x, y); });
   }
@@ -1805,6 +1811,9 @@ tps_status tps_pipeline_init(const tps_config* c, tps_pipeline** out) {
   if (c->transport < TPS_TRANSPORT_NONE || c->transport > TPS_TRANSPORT_IPC) return fail(TPS_E_CONFIG, "bad transport");
   if (c->num_stages > 1 && c->transport == TPS_TRANSPORT_NONE) return fail(TPS_E_CONFIG, "S > 1 needs a transport");
   if (c->transport == TPS_TRANSPORT_NCCL && c->num_stages > 1 && !c->nccl_ids) return fail(TPS_E_CONFIG, "NCCL transport needs ids");
+  if (c->dtype != TPS_BF16 && c->dtype != TPS_TF32) return fail(TPS_E_CONFIG, "bad dtype %d", c->dtype);
+  if (c->dtype == TPS_TF32 && (c->num_layer_specs > 0 || c->dp_size > 1))
+    return fail(TPS_E_UNSUPPORTED, "tf32 storage is implemented for chain MLP networks (dims, no layer specs, dp_size 1)");
   TPS_TRY(check_arch(c->device));
   CUDA_OK(cudaSetDevice(c->device));
 
@@ -1835,6 +1844,9 @@ tps_status tps_pipeline_init(const tps_config* c, tps_pipeline** out) {
   p->eq1_on_load = env && env[0] == '1';
   p->fuse_update = c->fuse_update != 0;
   p->graph = graph;
+  p->tf = c->dtype == TPS_TF32;
+  p->ew = p->tf ? 2 : 1;
+  p->esz = 2 * p->ew;
   p->dp = std::max(1, c->dp_size);
   p->dp_rank = p->dp > 1 ? c->dp_rank : 0;
   if (p->dp > 1) {
@@ -1901,8 +1913,9 @@ tps_status tps_pipeline_init(const tps_config* c, tps_pipeline** out) {
       if ((st = alloc_t(p, &L.db, L.Np, &p->mem_optim)) != TPS_OK) return cleanup(st);
       L.ver.resize(p->R);
       for (int r = 0; r < p->R; ++r)
-        if ((st = alloc_t(p, &L.ver[r], n, r == 0 ? &p->mem_weights : &p->mem_stash)) != TPS_OK) return cleanup(st);
-      p->ver_bytes += static_cast<int64_t>(n) * 2;
+        if ((st = alloc_t(p, &L.ver[r], n * p->ew, r == 0 ? &p->mem_weights : &p->mem_stash)) != TPS_OK)
+          return cleanup(st);
+      p->ver_bytes += static_cast<int64_t>(n) * p->esz;
     }
     p->layers.push_back(L);
   }
@@ -1914,7 +1927,8 @@ tps_status tps_pipeline_init(const tps_config* c, tps_pipeline** out) {
   for (int slot = 0; slot < static_cast<int>(p->act.size()); ++slot)
     for (int k = 0; k < nl; ++k) {
       const bool need = (k == 0) ? slot < p->A0 : slot < p->Kmax;
-      if (need && (st = alloc_t(p, &p->act[slot][k], static_cast<size_t>(p->B) * p->layers[k].in_elems(), &p->mem_acts)) != TPS_OK)
+      if (need && (st = alloc_t(p, &p->act[slot][k], static_cast<size_t>(p->B) * p->layers[k].in_elems() * p->ew,
+                                &p->mem_acts)) != TPS_OK)
         return cleanup(st);
     }
   if (L0.im2col) {
@@ -1926,11 +1940,15 @@ tps_status tps_pipeline_init(const tps_config* c, tps_pipeline** out) {
   const int64_t outL = p->layers[nl - 1].out_elems(), in0 = p->in0_elems;
   for (int i = 0; i < 2; ++i) {
     if (!p->last) {
-      if ((st = alloc_t(p, &p->send_fwd[i], static_cast<size_t>(p->B) * outL, &p->mem_comm)) != TPS_OK) return cleanup(st);
-      if ((st = alloc_t(p, &p->gin[i], static_cast<size_t>(p->B) * outL, &p->mem_comm)) != TPS_OK) return cleanup(st);
+      if ((st = alloc_t(p, &p->send_fwd[i], static_cast<size_t>(p->B) * outL * p->ew, &p->mem_comm)) != TPS_OK)
+        return cleanup(st);
+      if ((st = alloc_t(p, &p->gin[i], static_cast<size_t>(p->B) * outL * p->ew, &p->mem_comm)) != TPS_OK)
+        return cleanup(st);
     }
-    if (!p->first && (st = alloc_t(p, &p->gout[i], static_cast<size_t>(p->B) * in0, &p->mem_comm)) != TPS_OK) return cleanup(st);
-    if (nl > 1 && (st = alloc_t(p, &p->gwork[i], static_cast<size_t>(p->B) * max_elems, &p->mem_acts)) != TPS_OK) return cleanup(st);
+    if (!p->first && (st = alloc_t(p, &p->gout[i], static_cast<size_t>(p->B) * in0 * p->ew, &p->mem_comm)) != TPS_OK)
+      return cleanup(st);
+    if (nl > 1 && (st = alloc_t(p, &p->gwork[i], static_cast<size_t>(p->B) * max_elems * p->ew, &p->mem_acts)) != TPS_OK)
+      return cleanup(st);
   }
   {
     // default on (C5: +9.5 % A/B); TPS_SPLIT_W=0 keeps every backward kernel on the compute stream
@@ -1943,11 +1961,11 @@ tps_status tps_pipeline_init(const tps_config* c, tps_pipeline** out) {
     // cap, so overlapping the two inside one launch only lowers the clock (dual 159 us at 1395 MHz
     // vs 166 us for the two launches at 1515 MHz; the C5 step unchanged)
     const char* e = std::getenv("TPS_DUAL");
-    p->dual = p->split_w && e && e[0] == '1';
+    p->dual = p->split_w && e && e[0] == '1' && !p->tf;
   }
-  if (p->split_w && (st = alloc_t(p, &p->gwork[2], static_cast<size_t>(p->B) * max_elems, &p->mem_acts)) != TPS_OK)
+  if (p->split_w && (st = alloc_t(p, &p->gwork[2], static_cast<size_t>(p->B) * max_elems * p->ew, &p->mem_acts)) != TPS_OK)
     return cleanup(st);
-  if (nl > 1 && std::getenv("TPS_COLSUM") && std::getenv("TPS_COLSUM")[0] == '1') {
+  if (nl > 1 && !p->tf && std::getenv("TPS_COLSUM") && std::getenv("TPS_COLSUM")[0] == '1') {
     // column partial sums of the input gradients (bias gradients without another pass over G):
     // ceil(rows / 32) x cols floats for the largest input gradient of the stage.  Off by default:
     // the epilogue reduction costs more than the pass it saves (C5 589k vs 600k samples/s)
@@ -1974,7 +1992,7 @@ tps_status tps_pipeline_init(const tps_config* c, tps_pipeline** out) {
   if (p->last) {
     if (p->layers[nl - 1].kind != TPS_LAYER_LINEAR) return cleanup(fail(TPS_E_CONFIG, "the last layer must be the Linear head"));
     if ((st = alloc_t(p, &p->logits, static_cast<size_t>(p->B) * outL, &p->mem_acts)) != TPS_OK) return cleanup(st);
-    if ((st = alloc_t(p, &p->gce, static_cast<size_t>(p->Kmax) * p->B * outL, &p->mem_acts)) != TPS_OK)
+    if ((st = alloc_t(p, &p->gce, static_cast<size_t>(p->Kmax) * p->B * outL * p->ew, &p->mem_acts)) != TPS_OK)
       return cleanup(st);
     if ((st = alloc_t(p, &p->loss_rows, p->B, &p->mem_acts)) != TPS_OK) return cleanup(st);
     if ((st = alloc_t(p, &p->labels_dev, p->B, &p->mem_acts)) != TPS_OK) return cleanup(st);
@@ -2174,8 +2192,8 @@ tps_status tps_ipc_export(tps_pipeline* p, void* out, int64_t cap, int64_t* n) {
   if (p->A0 > 16) return fail(TPS_E_UNSUPPORTED, "more than 16 input slots");
   IpcBlob b{};
   b.magic = IPC_MAGIC; b.stage = p->s; b.num_stages = p->S; b.A0 = p->A0;
-  b.in_bytes = static_cast<int64_t>(p->B) * p->in0_elems * 2;
-  b.gin_bytes = p->last ? 0 : static_cast<int64_t>(p->B) * p->layers[p->nlayers() - 1].out_elems() * 2;
+  b.in_bytes = static_cast<int64_t>(p->B) * p->in0_elems * p->esz;
+  b.gin_bytes = p->last ? 0 : static_cast<int64_t>(p->B) * p->layers[p->nlayers() - 1].out_elems() * p->esz;
   CUDA_OK(cudaIpcGetMemHandle(&b.flags, p->flags));
   if (!p->first)
     for (int i = 0; i < p->A0; ++i) CUDA_OK(cudaIpcGetMemHandle(&b.in[i], p->act[i][0]));
@@ -2196,7 +2214,7 @@ tps_status tps_ipc_connect(tps_pipeline* p, const void* prev_blob, const void* n
   if (prev_blob) {
     IpcBlob b;
     std::memcpy(&b, prev_blob, sizeof(b));
-    const int64_t want = static_cast<int64_t>(p->B) * p->in0_elems * 2;
+    const int64_t want = static_cast<int64_t>(p->B) * p->in0_elems * p->esz;
     if (b.magic != IPC_MAGIC || b.stage != p->s - 1 || b.num_stages != p->S || b.gin_bytes != want)
       return fail(TPS_E_CONFIG, "bad descriptor for stage %d (stage %d, %lld gradient bytes, want %lld)", p->s - 1,
                   b.stage, (long long)b.gin_bytes, (long long)want);
@@ -2211,7 +2229,7 @@ tps_status tps_ipc_connect(tps_pipeline* p, const void* prev_blob, const void* n
   if (next_blob) {
     IpcBlob b;
     std::memcpy(&b, next_blob, sizeof(b));
-    const int64_t want = static_cast<int64_t>(p->B) * p->layers[p->nlayers() - 1].out_elems() * 2;
+    const int64_t want = static_cast<int64_t>(p->B) * p->layers[p->nlayers() - 1].out_elems() * p->esz;
     if (b.magic != IPC_MAGIC || b.stage != p->s + 1 || b.num_stages != p->S || b.in_bytes != want || b.A0 < 1 ||
         b.A0 > 16)
       return fail(TPS_E_CONFIG, "bad descriptor for stage %d (stage %d, %lld input bytes, want %lld)", p->s + 1,
@@ -2671,8 +2689,14 @@ tps_status tps_intermediate_weight(tps_pipeline* p, int32_t layer, int32_t stale
   if (L.kind == TPS_LAYER_BN) return fail(TPS_E_INVALID_ARG, "layer %d: BN γ versions are fp32 (use tps_get_weights)", layer);
   CUDA_OK(cudaStreamWaitEvent(p->cs, p->ev_upd_done[layer], 0));
   const int64_t vs = p->latest - staleness;
-  CUDA_OK(tps::launch_blend_materialize(L.ver[vs % p->R], L.ver[p->latest % p->R], static_cast<uint16_t*>(out_bf16),
-                                        static_cast<int64_t>(L.Np) * L.Kp, a, b, p->cs));
+  if (p->tf)   // tf32 storage: fp32 out, tf32_rna(fp32(α·s) + fp32(β·l))
+    CUDA_OK(tps::launch_blend_materialize_tf32(reinterpret_cast<const float*>(L.ver[vs % p->R]),
+                                               reinterpret_cast<const float*>(L.ver[p->latest % p->R]),
+                                               static_cast<float*>(out_bf16), static_cast<int64_t>(L.Np) * L.Kp, a, b,
+                                               p->cs));
+  else
+    CUDA_OK(tps::launch_blend_materialize(L.ver[vs % p->R], L.ver[p->latest % p->R], static_cast<uint16_t*>(out_bf16),
+                                          static_cast<int64_t>(L.Np) * L.Kp, a, b, p->cs));
   p->launches += 1;
   return TPS_OK;
 }
@@ -2685,7 +2709,7 @@ tps_status tps_get_version(tps_pipeline* p, int32_t layer, int32_t staleness, vo
   Layer& L = p->layers[layer];
   if (L.kind == TPS_LAYER_BN) return fail(TPS_E_INVALID_ARG, "layer %d: BN γ versions are fp32 (use tps_get_weights)", layer);
   CUDA_OK(cudaStreamWaitEvent(p->cs, p->ev_upd_done[layer], 0));
-  CUDA_OK(cudaMemcpyAsync(out_bf16, L.ver[(p->latest - staleness) % p->R], static_cast<size_t>(L.Np) * L.Kp * 2,
+  CUDA_OK(cudaMemcpyAsync(out_bf16, L.ver[(p->latest - staleness) % p->R], static_cast<size_t>(L.Np) * L.Kp * p->esz,
                           cudaMemcpyDeviceToDevice, p->cs));
   TPS_TRY(sync_streams(p));
   return TPS_OK;
@@ -2737,6 +2761,8 @@ tps_status tps_set_weights(tps_pipeline* p, int32_t layer, const float* w, const
   if (L.mb) CUDA_OK(cudaMemsetAsync(L.mb, 0, static_cast<size_t>(L.Np) * 4, p->cs));
   if (L.kind == TPS_LAYER_BN)
     CUDA_OK(cudaMemcpyAsync(L.verf[p->latest % p->R], L.W, n * 4, cudaMemcpyDeviceToDevice, p->cs));
+  else if (p->tf)
+    CUDA_OK(tps::launch_f32_to_tf32(L.W, reinterpret_cast<float*>(L.ver[p->latest % p->R]), static_cast<int64_t>(n), p->cs));
   else
     CUDA_OK(tps::launch_f32_to_bf16(L.W, L.ver[p->latest % p->R], static_cast<int64_t>(n), p->cs));
   p->launches += 1;
@@ -2766,7 +2792,11 @@ tps_status tps_init_weights_synthetic(tps_pipeline* p) {
     if (L.b) CUDA_OK(cudaMemsetAsync(L.b, 0, static_cast<size_t>(L.Np) * 4, p->cs));
     if (L.mW) CUDA_OK(cudaMemsetAsync(L.mW, 0, static_cast<size_t>(L.Np) * L.Kp * 4, p->cs));
     if (L.mb) CUDA_OK(cudaMemsetAsync(L.mb, 0, static_cast<size_t>(L.Np) * 4, p->cs));
-    CUDA_OK(tps::launch_f32_to_bf16(L.W, L.ver[p->latest % p->R], static_cast<int64_t>(L.Np) * L.Kp, p->cs));
+    if (p->tf)
+      CUDA_OK(tps::launch_f32_to_tf32(L.W, reinterpret_cast<float*>(L.ver[p->latest % p->R]),
+                                      static_cast<int64_t>(L.Np) * L.Kp, p->cs));
+    else
+      CUDA_OK(tps::launch_f32_to_bf16(L.W, L.ver[p->latest % p->R], static_cast<int64_t>(L.Np) * L.Kp, p->cs));
     p->launches += 2;
   }
   TPS_TRY(sync_streams(p));
@@ -3154,6 +3184,8 @@ tps_status tps_gemm_bwd_dual(int32_t M, int32_t N, int32_t K, const void* A, int
 tps_status tps_gemm(int32_t mode, int32_t M, int32_t N, int32_t K, const void* A, int32_t lda, const void* B,
                     int32_t ldb, const void* B2, void* out, int32_t ldo, int32_t out_f32, const float* bias,
                     int32_t relu, float alpha, float beta, const void* mask, int32_t ldm, uint64_t stream) {
+  const int tf = (mode & TPS_GEMM_TF32) != 0;
+  mode &= ~TPS_GEMM_TF32;
   if (mode < 0 || mode > 3) return fail(TPS_E_INVALID_ARG, "bad mode");
   if (M < 0 || N < 0 || K < 0 || !A || !B || !out) return fail(TPS_E_INVALID_ARG, "bad operands");
   if (N % 8 || ldo % 8 || lda % 8 || ldb % 8 || (mask && ldm % 8)) return fail(TPS_E_INVALID_ARG, "N and leading dims must be multiples of 8");
@@ -3166,6 +3198,7 @@ tps_status tps_gemm(int32_t mode, int32_t M, int32_t N, int32_t K, const void* A
   ga.M = M; ga.N = N; ga.K = K; ga.out = out; ga.ldo = ldo; ga.out_f32 = out_f32; ga.bias = bias; ga.relu = relu;
   ga.alpha = mode == 3 ? 1.f : alpha; ga.xa = alpha; ga.xb = beta;
   ga.mask = static_cast<const uint16_t*>(mask); ga.ldm = ldm;
+  ga.tf32 = tf;
   return gemm_with_ws(mode, op, ga, reinterpret_cast<cudaStream_t>(stream));
 }
 

@@ -16,6 +16,8 @@ LIB_PATH = os.environ.get("TPS_LIB") or os.path.join(HERE, "lib", "libtps.so")
 
 TPS_V, TPS_I = 0, 1
 TPS_BLEND_EQ1, TPS_BLEND_CONVEX = 0, 1
+TPS_BF16, TPS_TF32 = 0, 1            # tps_dtype (storage precision, reading Z28)
+TPS_GEMM_TF32 = 16                   # tps_gemm mode flag: tf32 operands in fp32 containers
 TPS_TRANSPORT_NONE, TPS_TRANSPORT_LOCAL, TPS_TRANSPORT_NCCL, TPS_TRANSPORT_IPC = 0, 1, 2, 3
 TPS_IPC_BLOB_BYTES = 2048
 TPS_EV_F, TPS_EV_B, TPS_EV_U = 0, 1, 2
@@ -75,7 +77,7 @@ class Config(C.Structure):
                 ("num_layer_specs", C.c_int32), ("layer_specs", C.POINTER(Layer)),
                 ("max_inflight", C.c_int32), ("staleness_mode", C.c_int32),
                 ("dev_alloc", C.c_void_p), ("dev_free", C.c_void_p), ("alloc_ctx", C.c_void_p),
-                ("dp_size", C.c_int32), ("dp_rank", C.c_int32), ("reserved", C.c_int32 * 2)]
+                ("dp_size", C.c_int32), ("dp_rank", C.c_int32), ("dtype", C.c_int32), ("reserved", C.c_int32)]
 
 
 # tps_config.dev_alloc / dev_free signatures
@@ -356,6 +358,7 @@ class StageSpec:
     torch_alloc: bool = False        # allocate through PyTorch's caching allocator
     dp_size: int = 1                 # data-parallel replicas of the pipeline (NEXT-2)
     dp_rank: int = 0
+    dtype: int = TPS_BF16            # TPS_TF32: activations / versions / gradients as tf32 (fp32 containers)
     _keep: list = field(default_factory=list)
 
 
@@ -388,7 +391,7 @@ class Pipeline:
                      layer_specs=specs, max_inflight=spec.max_inflight, staleness_mode=spec.staleness_mode,
                      dev_alloc=C.cast(self._alloc.alloc, C.c_void_p) if self._alloc else None,
                      dev_free=C.cast(self._alloc.free, C.c_void_p) if self._alloc else None,
-                     dp_size=spec.dp_size, dp_rank=spec.dp_rank)
+                     dp_size=spec.dp_size, dp_rank=spec.dp_rank, dtype=spec.dtype)
         h = C.c_void_p()
         check(lib().tps_pipeline_init(C.byref(cfg), C.byref(h)))
         self.h = h

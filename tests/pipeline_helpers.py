@@ -81,13 +81,13 @@ def run_oracle_graph(layers, bounds, m, b, M, variant, blend, lam, lr, mu, wd=0.
 
 
 def run_oracle(dims, bounds, m, b, M, variant, blend, lam, lr, mu, wd=0.0, seed=0, kind=synthgen.X_SIGNED,
-               layers=None, max_inflight=0, exact=False):
+               layers=None, max_inflight=0, exact=False, dtype="bf16"):
     if layers:
         xs, ys, w0, b0 = net_workload(layers, m, b, M, seed, kind)
     else:
         xs, ys, w0, b0 = workload(dims, m, b, M, seed, kind)
     cfg = opipe.Config(dims, bounds, m, b, M, variant=variant, blend=blend, lam=lam, lr=lr, momentum=mu, wd=wd,
-                       layers=layers, max_inflight=max_inflight, exact=exact)
+                       layers=layers, max_inflight=max_inflight, exact=exact, dtype=dtype)
     return opipe.run(cfg, xs, ys, w0, b0)
 
 
@@ -113,7 +113,9 @@ def run_gpu(dims, bounds, m, b, M, variant, blend, lam, lr, mu, wd=0.0, seed=0, 
         xs, ys, w0, b0 = net_workload(layers, m, b, M, seed, kind)
     else:
         xs, ys, w0, b0 = workload(dims, m, b, M, seed, kind)
-    x_pool = torch.from_numpy(np.stack(xs)).to(torch.bfloat16).cuda().contiguous()
+    # bf16 input pools, or fp32 containers in tf32 storage mode (the inputs are exact in both)
+    xdt = torch.float32 if spec_kw.get("dtype", 0) == tps.TPS_TF32 else torch.bfloat16
+    x_pool = torch.from_numpy(np.stack(xs)).to(xdt).cuda().contiguous()
     y_pool = torch.from_numpy(np.stack(ys)).cuda().contiguous()
     V = tps.TPS_V if variant == ost.V_VARIANT else tps.TPS_I
     BL = tps.TPS_BLEND_EQ1 if blend == ost.EQ1 else tps.TPS_BLEND_CONVEX

@@ -30,7 +30,7 @@ def test_library_exports_every_declared_symbol():
     exported = set(re.findall(r"\bT (tps_[a-z_0-9]+)", out))
     missing = [s for s in declared_symbols() if s not in exported]
     assert not missing, missing
-    assert tps.lib().tps_abi_version() == 3
+    assert tps.lib().tps_abi_version() == 4
 
 
 @pytest.mark.parametrize("S", [1, 2, 4, 8])
@@ -79,6 +79,20 @@ def test_config_validation_errors_without_gpu():
         with pytest.raises(tps.TpsError) as e:
             tps.Pipeline(spec)
         assert e.value.status == 2, spec
+
+
+def test_dtype_validation_without_gpu():
+    """tps_config.dtype (reading Z28): an unknown value is TPS_E_CONFIG; tf32 storage on an
+    image network or with data parallelism is TPS_E_UNSUPPORTED; both before the device check."""
+    with pytest.raises(tps.TpsError) as e:
+        tps.Pipeline(tps.StageSpec([8, 8, 4], [0, 2], 0, 2, 4, dtype=7))
+    assert e.value.status == 2
+    layers = [{"kind": "conv3", "cin": 3, "cout": 64, "h": 8, "w": 8}, {"kind": "linear", "in": 4096, "out": 10}]
+    for spec in (tps.StageSpec([192, 10], [0, 2], 0, 2, 4, layers=layers, dtype=tps.TPS_TF32),
+                 tps.StageSpec([8, 8, 4], [0, 2], 0, 2, 4, dp_size=2, dp_rank=0, dtype=tps.TPS_TF32)):
+        with pytest.raises(tps.TpsError) as e:
+            tps.Pipeline(spec)
+        assert e.value.status == 10, tps.last_error() if hasattr(tps, "last_error") else spec
 
 
 def test_no_cpu_fallback():
