@@ -211,15 +211,16 @@ def method_leg(torch, tps, windows=3, epoch=32, pool=4):
     torch.cuda.synchronize()
     fl_c2 = sum(2.0 * dims[l] * dims[l + 1] * (3 if l > 0 else 2) for l in range(len(dims) - 1))
 
-    def timed(stages, n_windows):
+    def timed(stages, n_windows, xp=None):
+        xp = x if xp is None else xp
         mb = 0
-        tps.run_schedule_local(stages, mb, epoch, x, y, pool)          # warm-up epoch
+        tps.run_schedule_local(stages, mb, epoch, xp, y, pool)         # warm-up epoch
         mb += epoch
         torch.cuda.synchronize()
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(n_windows + 1)]
         ev[0].record()
         for i in range(n_windows):
-            tps.run_schedule_local(stages, mb, epoch, x, y, pool)
+            tps.run_schedule_local(stages, mb, epoch, xp, y, pool)
             mb += epoch
             for st in stages:
                 st.join(cur.cuda_stream)                                  # stream-ordered end of the window
@@ -258,6 +259,28 @@ def method_leg(torch, tps, windows=3, epoch=32, pool=4):
         }
         for st in stages:
             st.close()
+    # the same C2 pipeline in tf32 storage (tps_config.dtype = TPS_TF32, reading Z28): I-EQ1,
+    # fp32-container inputs (the synthetic inputs are exact in both precisions)
+    xf = x.float()
+    torch.cuda.synchronize()
+    torch.cuda.reset_peak_memory_stats()
+    base = torch.cuda.memory_allocated()
+    stages = [tps.Pipeline(tps.StageSpec(dims=dims, stage_bounds=bounds, stage_id=s, micro_batches=m, micro_batch_size=b,
+                                         variant=tps.TPS_I, blend=tps.TPS_BLEND_EQ1, lam=LAM, lr=LR, momentum=MU,
+                                         transport=tps.TPS_TRANSPORT_LOCAL, seed=1, torch_alloc=True,
+                                         dtype=tps.TPS_TF32))
+              for s in range(4)]
+    for st in stages:
+        st.init_weights_synthetic()
+    tps.local_link(stages)
+    t = timed(stages, windows, xf)
+    out["tf32"] = {"variant": "I-EQ1", "samples_per_s": t, "tflops_median": fl_c2 * t["median"] / 1e12,
+                   "memory_measured_bytes_all_stages": int(torch.cuda.max_memory_allocated() - base),
+                   "per_stage_stash_peak_bytes": [st.stash_info()[2] for st in stages],
+                   "note": "kind::tf32 stage GEMMs, activations / versions / gradients as tf32 in fp32 containers"}
+    for st in stages:
+        st.close()
+    del xf
     # staleness sweep on one stage
     dims1 = [WIDTH, WIDTH, WIDTH, CLASSES]
     fl1 = sum(2.0 * dims1[l] * dims1[l + 1] * (3 if l > 0 else 2) for l in range(3))

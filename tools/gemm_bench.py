@@ -108,6 +108,8 @@ def main():
     od = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
     maskd = torch.randn(M, N, device="cuda").to(torch.bfloat16)
 
+    Xf, Wf, Wtf, maskf, Gkf, Xkf = (t.float() for t in (X, W, Wt, mask, Gk, Xk))
+
     def sep():
         tps.gemm_wgrad_sgd(N, N, M, G4, N, X4, N, wm, vm, qm, N, 1e-9, 0.9)
         tps.gemm(1, M, N, N, Gd, N, Wd, N, od, N, 0, None, 0, 0.9, 0.0, maskd, N)
@@ -122,6 +124,11 @@ def main():
         5: ("dual: wgrad+update & dgrad, one launch", lambda: tps.gemm_bwd_dual(
             N, N, M, G4, N, X4, N, wm, vm, qm, N, 1e-9, 0.9, 0.0, M, N, N, Gd, N, Wd, N, od, N, 0.9, maskd, N)),
         6: ("the same two as separate launches", sep),
+        # tf32 storage (reading Z28): kind::tf32 on fp32 containers (half the bf16 tensor rate)
+        7: ("tf32 fwd", lambda: tps.gemm(tps.GEMM_FWD | tps.TPS_GEMM_TF32, M, N, K, Xf, K, Wf, K, of, N, 0, bias, 1)),
+        8: ("tf32 dgrad", lambda: tps.gemm(tps.GEMM_DGRAD | tps.TPS_GEMM_TF32, M, N, K, Xf, K, Wtf, N, of, N, 0, None,
+                                           0, 0.9, 0.0, maskf, N)),
+        9: ("tf32 wgrad", lambda: tps.gemm(tps.GEMM_WGRAD | tps.TPS_GEMM_TF32, M, N, K, Gkf, M, Xkf, N, of, N, 1)),
     }
     for m in [int(x) for x in a.modes.split(",")]:
         name, fn = runs[m]
