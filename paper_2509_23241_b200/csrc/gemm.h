@@ -66,6 +66,10 @@ struct GemmArgs {
   // are fp32 arrays holding tf32 values, MMAs run kind::tf32, stores round RNA to tf32.
   // Linear modes only (GEMM_FWD / DGRAD / WGRAD / DGRAD_BLEND), no addend, no split-K.
   int tf32;
+  // fused update (EPI_SGD) on 256-column CTA-pair tiles: split a last partial wave of tiles into
+  // half tiles so no pair runs one whole HBM-bound update epilogue more than the others (set by
+  // gemm_run: on unless TPS_SGD_SPLIT_TAIL=0)
+  int split_tail;
 };
 
 // The input-gradient half of a dual backward launch (gemm_bwd_dual): dX[M, N] = α·(G·W)

@@ -225,6 +225,21 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG, MH>::THREADS, 1)
   // split-K (args.splits > 1, plain fp32 epilogue only): tile t covers K blocks
   // [ks·kper, min(num_k, (ks+1)·kper)) of output tile t mod (num_m·num_n), ks = t / (num_m·num_n)
   const int num_tiles = num_m * num_n * args.splits;
+  // split tail (fused update, args.split_tail): the HBM-bound update epilogue makes a tile's time
+  // ~ its epilogue, so a last partial wave of R <= pairs/2 full tiles would leave R pairs doing
+  // one tile more than the rest.  Those R tiles are split into 2R half tiles (N = BN/2) dealt to
+  // 2R different pairs: work item i < n_full is tile i, item n_full + h is half (h & 1) of tile
+  // n_full + h/2.  Every pair's half item (if any) is its last.
+  constexpr bool ST_OK = SGD && CG == 2 && BN == 256 && MH == 1 && B_MN && !CONV;
+  const int st_waves = num_tiles / ncl, st_rem = num_tiles - st_waves * ncl;
+  const bool split_tail = ST_OK && args.split_tail && args.splits <= 1 && st_waves >= 1 && st_rem > 0 &&
+                          2 * st_rem <= ncl;
+  const int n_full = split_tail ? st_waves * ncl : num_tiles;
+  const int n_items = split_tail ? n_full + 2 * st_rem : num_tiles;
+  auto item = [&](int i, int& t, int& noff, int& nw) {
+    if (i < n_full) { t = i; noff = 0; nw = BN; }
+    else { const int h = i - n_full; t = n_full + h / 2; noff = (h & 1) * (BN / 2); nw = BN / 2; }
+  };
 
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&tmA);
@@ -268,15 +283,17 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG, MH>::THREADS, 1)
       const uint64_t pol_keep = (SGD && TPS_SGD_L2HINT) ? ptx::policy_evict_last() : 0ull;
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = cid; t < num_tiles; t += ncl) {
+      for (int wi = cid; wi < n_items; wi += ncl) {
+        int t, noff, nw;
+        item(wi, t, noff, nw);
         int mb, nb, kb0, kb1;
         tile_split(t, num_m, num_n, num_k, args.kper, mb, nb, kb0, kb1);
-        const int n0 = nb * BN + static_cast<int>(rank) * (BN / CG);       // this CTA's B share
+        const int n0 = nb * BN + noff + static_cast<int>(rank) * (nw / CG);   // this CTA's B share
         for (int kb = kb0; kb < (TPS_DBG_NOMAIN ? kb0 : kb1); ++kb) {
           MBAR_WAIT(1, &empty[stage], phase ^ 1);
           uint8_t* const sA0 = stages + stage * C::STAGE_BYTES;
           uint8_t* sB = sA0 + MH * A_BYTES;
-          if (rank == 0) ptx::mbar_expect_tx(&full[stage], C::TX);
+          if (rank == 0) ptx::mbar_expect_tx(&full[stage], C::TX - (BN - nw) * BK * 2);   // (half item: half of B)
           else if (BLEND) ptx::mbar_expect_tx(&full[stage], 2 * C::B_BYTES);   // own B tiles, own barrier
           // every load of this stage completes on the leader CTA's full barrier
           const uint32_t fb = CG == 2 ? ptx::mapa(ptx::smem_u32(&full[stage]), 0) : 0u;
@@ -386,6 +403,7 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG, MH>::THREADS, 1)
           } else {
 #pragma unroll
             for (int i = 0; i < BN / CG / MNC; ++i) {
+              if (i >= nw / CG / MNC) break;      // half item: this CTA's half of the narrower B
               ldb2(dB + i * CHB, &tmB, n0 + MNC * i, kb * BKE);
               if (BLEND) ldb2(dB + C::B_BYTES + i * CHB, &tmB2, n0 + MNC * i, kb * BKE);
             }
@@ -397,12 +415,17 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG, MH>::THREADS, 1)
   } else if (warp == 1) {
     // ===================== MMA issuer =====================
     if (lane == 0 && rank == 0) {
-      constexpr uint32_t idesc = TF ? ptx::make_idesc_tf32(BM * CG, BN, A_MN, B_MN)
-                                    : ptx::make_idesc_bf16(BM * CG, BN, A_MN, B_MN);
+      constexpr uint32_t idesc_full = TF ? ptx::make_idesc_tf32(BM * CG, BN, A_MN, B_MN)
+                                         : ptx::make_idesc_bf16(BM * CG, BN, A_MN, B_MN);
+      constexpr uint32_t idesc_half = TF ? ptx::make_idesc_tf32(BM * CG, BN / 2, A_MN, B_MN)
+                                         : ptx::make_idesc_bf16(BM * CG, BN / 2, A_MN, B_MN);
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int t = cid; t < num_tiles; t += ncl, ++it) {
+      for (int wi = cid; wi < n_items; wi += ncl, ++it) {
+        int t, noff_, nw;
+        item(wi, t, noff_, nw);
+        const uint32_t idesc = nw == BN ? idesc_full : idesc_half;
         const int acc = it % C::ACC;
         const uint32_t acc_phase = (it / C::ACC) & 1;
         MBAR_WAIT(2, &tmem_empty[acc], acc_phase ^ 1);
@@ -469,14 +492,24 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG, MH>::THREADS, 1)
     // 16-byte chunk `ch` of row `row` in the swizzled box (128B swizzle for 128-byte rows, 64B
     // swizzle for 64-byte rows)
     auto swz = [](int row, int ch) { return CW == 32 ? (ch ^ (row & 7)) : (ch ^ ((row >> 1) & 3)); };
-    auto issue = [&](int i) {            // lane 0: TMA loads of this warp's chunk i into buffer i % SGD_NB
-      const int ti = i / NCHW, c = half + NW * (i - ti * NCHW);
-      const int t = cid + ti * ncl;
-      if (t >= num_tiles) return;
+    // this warp's chunk i (running count: item ti = i / NCHW, chunk i % NCHW of it) -> global
+    // (row0, col0); false past the last item or past a half item's chunks
+    auto chunk_at = [&](int i, int& row0, int& col0) {
+      const int ti = i / NCHW, cl = i - ti * NCHW;
+      const int wi = cid + ti * ncl;
+      if (wi >= n_items) return false;
+      int t, noff, nw;
+      item(wi, t, noff, nw);
+      if (cl >= nw / CW / NW) return false;
       int mb, nb;
       tile_coords(t, num_m, num_n, mb, nb);
-      const int row0 = mb * BM * CG + static_cast<int>(rank) * BM + q * 32;
-      const int col0 = nb * BN + c * CW;
+      row0 = mb * BM * CG + static_cast<int>(rank) * BM + q * 32;
+      col0 = nb * BN + noff + (half + NW * cl) * CW;
+      return true;
+    };
+    auto issue = [&](int i) {            // lane 0: TMA loads of this warp's chunk i into buffer i % SGD_NB
+      int row0, col0;
+      if (!chunk_at(i, row0, col0)) return;
       const int buf = i % SGD_NB;
       uint8_t* w_s = ebase + buf * SGD_BUF;
       ptx::mbar_expect_tx(&ebar[buf], mom ? 2u * SGD_WBYTES : 1u * SGD_WBYTES);
@@ -491,14 +524,10 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG, MH>::THREADS, 1)
     // L2 prefetch of chunk i (TPS_SGD_PF chunks ahead of its shared-memory load), so that load
     // hits L2 instead of waiting a full DRAM round trip; no shared memory or registers held
     auto prefetch = [&](int i) {
-      const int ti = i / NCHW, c = half + NW * (i - ti * NCHW);
-      const int t = cid + ti * ncl;
-      if (t >= num_tiles) return;
-      int mb, nb;
-      tile_coords(t, num_m, num_n, mb, nb);
-      const int row0 = mb * BM * CG + static_cast<int>(rank) * BM + q * 32;
-      ptx::tma_prefetch_2d(&tmW, nb * BN + c * CW, row0);
-      if (mom) ptx::tma_prefetch_2d(&tmV, nb * BN + c * CW, row0);
+      int row0, col0;
+      if (!chunk_at(i, row0, col0)) return;
+      ptx::tma_prefetch_2d(&tmW, col0, row0);
+      if (mom) ptx::tma_prefetch_2d(&tmV, col0, row0);
     };
     if (lane == 0 && !TPS_DBG_SGD) {
       if (TPS_SGD_PF)
@@ -510,7 +539,9 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG, MH>::THREADS, 1)
         for (int i = SGD_NB; i < NCHW * TPS_SGD_PF0; ++i) prefetch(i);
     }
     int i = 0, it = 0;
-    for (int t = cid; t < num_tiles; t += ncl, ++it) {
+    for (int wi = cid; wi < n_items; wi += ncl, ++it) {
+      int t, noff, nw;
+      item(wi, t, noff, nw);
       int mb, nb;
       tile_coords(t, num_m, num_n, mb, nb);
       const int acc = it % C::ACC;
@@ -518,8 +549,9 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG, MH>::THREADS, 1)
       MBAR_WAIT(5, &tmem_full[acc], acc_phase);
       ptx::tc_fence_after();
       const int row0 = mb * BM * CG + static_cast<int>(rank) * BM + q * 32;
+      const int nchw = nw / CW / NW;                  // this item's chunks per warp
 #pragma unroll 1
-      for (int ci = 0; ci < NCHW; ++ci, ++i) {
+      for (int ci = 0; ci < nchw; ++ci, ++i) {
         const int c = half + NW * ci;
         uint32_t r[CW];
         if constexpr (CW == 32)
@@ -529,7 +561,7 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG, MH>::THREADS, 1)
           ptx::tmem_ld_32x32b_x16(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c * CW,
                                   *reinterpret_cast<uint32_t(*)[16]>(r));
         ptx::tmem_ld_wait();
-        if (ci == NCHW - 1) {              // last TMEM read of this warp for this tile
+        if (ci == nchw - 1) {              // last TMEM read of this warp for this tile
           ptx::tc_fence_before();
           __syncwarp();
           if (lane == 0) {
@@ -575,7 +607,7 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG, MH>::THREADS, 1)
           // 16-byte column chunks so each store instruction writes whole 128-byte row segments;
           // the buffer can be refilled as soon as its contents sit in registers
           __syncwarp();
-          const int col0 = nb * BN + c * CW;
+          const int col0 = nb * BN + noff + c * CW;
           const size_t ld = static_cast<size_t>(args.ldo);
           constexpr int LPR = CW / 4;                     // lanes per row segment (16 B each)
 #pragma unroll
@@ -609,7 +641,7 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG, MH>::THREADS, 1)
         ptx::fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-          const int col0 = nb * BN + c * CW;
+          const int col0 = nb * BN + noff + c * CW;
           if (TPS_SGD_L2HINT) {
             ptx::tma_store_2d_hint(&tmW, w_s, col0, row0, pol_stream);
             if (mom) ptx::tma_store_2d_hint(&tmV, w_s + SGD_WBYTES, col0, row0, pol_stream);
@@ -1532,6 +1564,14 @@ cudaError_t gemm_run(int mode, const GemmOperands& op, const GemmArgs& args_in, 
   if (args.M <= 0 || args.N <= 0 || args.K <= 0) return cudaSuccess;
   const bool sgd = ((mode == GEMM_WGRAD || mode == GEMM_CONV_WGRAD) && args.epi == EPI_SGD);
   if (args.tf32 && (mode >= GEMM_CONV_FWD || args.addend)) return cudaErrorInvalidValue;
+  {
+    static int st_env = -1;
+    if (st_env < 0) {
+      const char* e = std::getenv("TPS_SGD_SPLIT_TAIL");
+      st_env = (e && e[0] == '0') ? 0 : 1;
+    }
+    args.split_tail = sgd && st_env;
+  }
   Tiling tl = pick_tiling(args.M, args.N, args.K, mode, sgd, args.max_ctas);
   if (args.tf32) tl.splits = 1;                      // tf32: one pass over K
   if (tl.splits > 1 &&

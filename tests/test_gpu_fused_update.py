@@ -16,6 +16,7 @@ SHAPES = [
     ([1024, 512, 256, 16], 2, 32),  # small: single-CTA tiles
     ([784, 256, 10], 4, 8),         # config-1 shapes
     ([2048, 2048, 16], 8, 64),      # pair, BN = 256, several tiles per CTA
+    ([4096, 2560, 16], 4, 64),      # 160 tiles on 74 pairs: the last 12 split into 24 half tiles (split tail)
 ]
 
 
@@ -35,7 +36,8 @@ def test_fused_equals_separate_bitwise(gpu_lib, dims, m, b, mu):
     np.testing.assert_array_equal(res[0][1], res[1][1])
 
 
-@pytest.mark.parametrize("MNK", [(4096, 4096, 2048), (512, 4096, 128), (1024, 520, 96), (4096, 256, 2048)])
+@pytest.mark.parametrize("MNK", [(4096, 4096, 2048), (512, 4096, 128), (1024, 520, 96), (4096, 256, 2048),
+                                 (2560, 4096, 1024)])
 @pytest.mark.parametrize("mu", [0.0, 0.9])
 def test_raw_fused_kernel_matches_oracle_update(gpu_lib, MNK, mu):
     """tps_gemm_wgrad_sgd (the fused wgrad + SGD/momentum kernel alone) == oracle.mlp.sgd_update
