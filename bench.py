@@ -501,8 +501,9 @@ def main():
     ncu_path = os.path.join(ROOT, "profiles", "r02_ncu_full_summary.json")
     if os.path.exists(ncu_path):
         try:
-            names = {"<256, 1, 1, 0, 1, 2, 0>": "wgrad+update", "<256, 0, 0, 0, 0, 2, 0>": "fwd",
-                     "<256, 0, 1, 0, 0, 2, 0>": "dgrad", "<256, 0, 1, 1, 0, 2, 0>": "dgrad_blend"}
+            # gemm_kernel<BN, A_MN, B_MN, BLEND, SGD, CG, CONV, MH, TF>
+            names = {"<256, 1, 1, 0, 1, 2, 0, 1, 0>": "wgrad+update", "<256, 0, 0, 0, 0, 2, 0, 1, 0>": "fwd",
+                     "<256, 0, 1, 0, 0, 2, 0, 1, 0>": "dgrad", "<256, 0, 1, 1, 0, 2, 0, 2, 0>": "dgrad_blend"}
             ncu_kinds = {"source": "profiles/r02_ncu_full_summary.json (ncu --set full --clock-control none)"}
             for r in json.load(open(ncu_path)):
                 for key, kind in names.items():
@@ -596,15 +597,16 @@ def main():
             # the dominant kernel: wgrad + fused SGD/momentum update (HBM-bound: its roofline time
             # max(FLOPs / tensor peak, algorithmic bytes / HBM peak) is the HBM term); achieved =
             # algorithmic bytes per launch / average launch duration (CUDA events on its stream)
-            "roofline": {"bound": "hbm", "kernel": "wgrad + fused SGD/momentum update, gemm_kernel<256,1,1,0,1,2,0> "
-                         "(CTA pairs, 256x256 tiles, TMA-fed update epilogue)",
+            "roofline": {"bound": "hbm", "kernel": "wgrad + fused SGD/momentum update, gemm_kernel<256,1,1,0,1,2,0,1,0> "
+                         "(CTA pairs, 256x256 tiles with a split tail, TMA-fed update epilogue)",
                          "achieved": dom["gbs"], "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
                          "frac": dom["gbs"] / peaks.get("hbm_gbs") if dom["gbs"] else None, "traffic": traffic,
                          "algorithmic_bytes_per_launch": dom["bytes"], "flops_per_launch": dom["flops"],
                          "avg_launch_us": dom["us"], "roofline_time_us": dom["roof_us"],
                          "frac_of_roofline_time": dom["roof_us"] / dom["us"] if dom["us"] else None,
-                         "isolated": "tools/gemm_bench.py --modes 4 (same kernel alone): 87.2 us = 0.59 of the HBM "
-                                     "roofline time (profiles/r02_gemm_microbench.txt)",
+                         "isolated": "tools/gemm_bench.py --modes 4 (same kernel alone): 84.1 us at 1965 MHz = 0.57 "
+                                     "of its HBM roofline time, 96.0 us sustained under the power cap "
+                                     "(profiles/r02_gemm_microbench.txt, r02_fused_kernel_variants.txt)",
                          "launch_note": "in the pipeline each launch runs concurrently with the next layer's input "
                                         "gradient on the compute stream (split backward), so its event duration "
                                         "includes SM sharing",

@@ -12,7 +12,8 @@
 #   bench    bench.py default line (C5, S=1) + the reference arm
 #   configs  tools/bench_configs.py (per-config one-GPU numbers incl. C2/C4 V vs I)
 #   launches ncu launch list of one bench epoch window + its summary
-#   gemm     tools/gemm_bench.py microbenchmarks at the bench shape
+#   gemm     tools/gemm_bench.py microbenchmarks at the bench shape (clock / power sampled)
+#   ncu      ncu --set full of one launch each of the fwd / dgrad / blend / fused-update GEMMs
 #   sanitize compute-sanitizer racecheck/synccheck/memcheck on small pipeline runs
 # Every step runs under its own timeout so one hang cannot eat the box.
 set -u
@@ -40,7 +41,13 @@ for s in $STEPS; do
         --log-file ${O}_launches.csv python bench.py --steps 1 --warmup 1 --epoch-mb 16 --no-cpu-baseline --no-e2e --no-v > /dev/null 2>&1
       python tools/launches_summary.py ${O}_launches.csv ${O}_launches_summary.json "bench.py C5 S=1, one epoch window" > /dev/null 2>&1 ;;
     gemm)
-      timeout 600 python tools/gemm_bench.py > ${O}_gemm.txt 2>&1 ;;
+      timeout 600 python tools/gemm_bench.py --modes 0,1,2,3,4,7,8,9 --seconds 1.0 > ${O}_gemm.txt 2>&1 ;;
+    ncu)
+      # one launch each of fwd / dgrad / blended dgrad / fused wgrad + update at the C5 shapes
+      for m in 0 1 3 4; do
+        timeout 400 ncu --set full --clock-control none --import-source on -k regex:gemm_kernel -s 3 -c 1 \
+          -o ${O}_mode$m python tools/gemm_bench.py --modes $m --iters 1 > ${O}_ncu_mode$m.log 2>&1
+      done ;;
     sanitize)
       for tool in racecheck synccheck memcheck; do
         TPS_SANITIZE=1 timeout 1200 compute-sanitizer --tool $tool --error-exitcode 9 \
