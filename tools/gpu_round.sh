@@ -35,7 +35,7 @@ for s in $STEPS; do
       timeout 900 python bench.py 2>${O}_bench.err | tail -1 > ${O}_bench.json
       timeout 900 python bench.py --impl reference --steps 2 --warmup 3 2>/dev/null | tail -1 > ${O}_ref.json ;;
     configs)
-      timeout 1500 python tools/bench_configs.py --out ${O}_configs.json > ${O}_configs.log 2>&1 ;;
+      timeout 1500 python tools/bench_configs.py --graph --out ${O}_configs.json > ${O}_configs.log 2>&1 ;;
     launches)
       timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -s 2500 -c 600 --csv \
         --log-file ${O}_launches.csv python bench.py --steps 1 --warmup 1 --epoch-mb 16 --no-cpu-baseline --no-e2e --no-v > /dev/null 2>&1
