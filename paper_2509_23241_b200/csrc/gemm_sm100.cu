@@ -86,6 +86,9 @@ constexpr int SGD_NB = TPS_SGD_NB;
 #ifndef TPS_SGD_CW
 #define TPS_SGD_CW 32
 #endif
+#ifndef TPS_SGD_LDGSTS
+#define TPS_SGD_LDGSTS 1   // fused update: w / v chunks loaded by per-lane cp.async (LSU path); 0 = TMA boxes
+#endif
 constexpr int SGD_CW = TPS_SGD_CW;
 static_assert(SGD_CW == 32 || (SGD_CW == 16 && TPS_SGD_STG), "16-column chunks need the STG write-back");
 constexpr int SGD_WBYTES = 32 * SGD_CW * 4;                 // one 32-row chunk of w (or v)
@@ -255,7 +258,7 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG, MH>::THREADS, 1)
       ptx::mbar_init(&tmem_empty[a], C::NEPI * CG);
     }
     if (SGD)
-      for (int i = 0; i < SGD_WARPS * SGD_NB; ++i) ptx::mbar_init(&sgd_bar[i], 1);
+      for (int i = 0; i < SGD_WARPS * SGD_NB; ++i) ptx::mbar_init(&sgd_bar[i], TPS_SGD_LDGSTS ? 32 : 1);
     ptx::fence_barrier_init();
   }
   // CTA pairs: the cta_group::2 TMEM allocation handshakes through the PEER's shared memory
@@ -507,6 +510,28 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG, MH>::THREADS, 1)
       col0 = nb * BN + noff + (half + NW * cl) * CW;
       return true;
     };
+    // TPS_SGD_LDGSTS: every lane copies 8 x 16 B of w (and of v) with cp.async into the same
+    // 128B-swizzled layout the TMA box has (row r at r·128 B, 16-byte chunk j at (j ^ (r & 7))),
+    // 4 whole rows per instruction, then arrives (noinc) on the chunk's barrier (count 32)
+    auto issue_lsu = [&](int i) {
+      int row0, col0;
+      if (!chunk_at(i, row0, col0)) {
+        ptx::cp_async_mbar_arrive_noinc(&ebar[i % SGD_NB]);   // keep the barrier's phase count
+        return;
+      }
+      uint8_t* w_s = ebase + (i % SGD_NB) * SGD_BUF;
+      const size_t ld = static_cast<size_t>(args.ldo);
+      const int j = lane & 7;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int rr = (lane >> 3) + 4 * k;
+        const size_t g = static_cast<size_t>(row0 + rr) * ld + col0 + j * 4;
+        const int off = rr * 128 + ((j ^ (rr & 7)) * 16);
+        ptx::cp_async_16(w_s + off, args.w + g);
+        if (mom) ptx::cp_async_16(w_s + SGD_WBYTES + off, args.v + g);
+      }
+      ptx::cp_async_mbar_arrive_noinc(&ebar[i % SGD_NB]);
+    };
     auto issue = [&](int i) {            // lane 0: TMA loads of this warp's chunk i into buffer i % SGD_NB
       int row0, col0;
       if (!chunk_at(i, row0, col0)) return;
@@ -529,10 +554,13 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG, MH>::THREADS, 1)
       ptx::tma_prefetch_2d(&tmW, col0, row0);
       if (mom) ptx::tma_prefetch_2d(&tmV, col0, row0);
     };
+    if (TPS_SGD_LDGSTS && !TPS_DBG_SGD)
+      for (int i = 0; i < SGD_NB; ++i) issue_lsu(i);
     if (lane == 0 && !TPS_DBG_SGD) {
       if (TPS_SGD_PF)
         for (int i = SGD_NB; i < SGD_NB + TPS_SGD_PF; ++i) prefetch(i);
-      for (int i = 0; i < SGD_NB; ++i) issue(i);
+      if (!TPS_SGD_LDGSTS)
+        for (int i = 0; i < SGD_NB; ++i) issue(i);
       // HBM idles while the first tile's MMAs run: pull the first tiles' w / v into L2 so
       // their epilogues run at L2 latency
       if (TPS_SGD_PF0)
@@ -631,8 +659,9 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG, MH>::THREADS, 1)
           }
           ptx::fence_proxy_async_smem();   // generic reads of the buffer before the async refill
           __syncwarp();
+          if (TPS_SGD_LDGSTS) issue_lsu(i + SGD_NB);
           if (lane == 0) {
-            issue(i + SGD_NB);
+            if (!TPS_SGD_LDGSTS) issue(i + SGD_NB);
             if (TPS_SGD_PF) prefetch(i + SGD_NB + TPS_SGD_PF);
           }
           __syncwarp();
@@ -1446,6 +1475,10 @@ Tiling pick_tiling(int M, int N, int K, int mode, bool sgd, int max_ctas = 0) {
     }
     if (force_cg_b != 1 && M >= 256 && N > 128 && ((M + 255) / 256) * ((N + 255) / 256) >= num_sms() / 2 * 3 / 4)
       return {2, 256};
+    // fewer rows (C2: M = 512): 256 x 128 pair tiles still fill the pairs and, per SM, stage and
+    // blend half the B bytes of a 128 x 128 single-CTA tile for the same MMA work
+    if (force_cg_b != 1 && M >= 256 && N > 64 && ((M + 255) / 256) * ((N + 127) / 128) >= num_sms() / 2 * 3 / 4)
+      return {2, 128};
     return {1, 128};
   }
   const int sms0 = max_ctas > 0 ? std::min(max_ctas, num_sms()) : num_sms();
@@ -1668,8 +1701,9 @@ cudaError_t gemm_run(int mode, const GemmOperands& op, const GemmArgs& args_in, 
                    : dispatch<1, 1, 0, CONV_NONE, 1>(tl, ta, tb, tb2, em, args, st);
       case GEMM_DGRAD_BLEND:
         if (tl.cg == 2)
-          return blend_mh2(args) ? launch<256, 0, 1, 1, 0, 2, CONV_NONE, 2, 1>(ta, tb, tb2, em, args, st)
-                                 : launch<256, 0, 1, 1, 0, 2, CONV_NONE, 1, 1>(ta, tb, tb2, em, args, st);
+          return tl.bn == 128 ? launch<128, 0, 1, 1, 0, 2, CONV_NONE, 1, 1>(ta, tb, tb2, em, args, st)
+                 : blend_mh2(args) ? launch<256, 0, 1, 1, 0, 2, CONV_NONE, 2, 1>(ta, tb, tb2, em, args, st)
+                                   : launch<256, 0, 1, 1, 0, 2, CONV_NONE, 1, 1>(ta, tb, tb2, em, args, st);
         return launch<128, 0, 1, 1, 0, 1, CONV_NONE, 1, 1>(ta, tb, tb2, em, args, st);
       default: return cudaErrorInvalidValue;
     }
@@ -1681,15 +1715,17 @@ cudaError_t gemm_run(int mode, const GemmOperands& op, const GemmArgs& args_in, 
       e = sgd ? dispatch<1, 1, 1>(tl, ta, tb, tb2, em, args, st) : dispatch<1, 1, 0>(tl, ta, tb, tb2, em, args, st);
       break;
     case GEMM_DGRAD_BLEND:
-      e = tl.cg == 2 ? (blend_mh2(args) ? launch<256, 0, 1, 1, 0, 2, CONV_NONE, 2>(ta, tb, tb2, em, args, st)
-                                        : launch<256, 0, 1, 1, 0, 2>(ta, tb, tb2, em, args, st))
+      e = tl.cg == 2 ? (tl.bn == 128 ? launch<128, 0, 1, 1, 0, 2>(ta, tb, tb2, em, args, st)
+                        : blend_mh2(args) ? launch<256, 0, 1, 1, 0, 2, CONV_NONE, 2>(ta, tb, tb2, em, args, st)
+                                          : launch<256, 0, 1, 1, 0, 2>(ta, tb, tb2, em, args, st))
                      : launch<128, 0, 1, 1, 0, 1>(ta, tb, tb2, em, args, st);
       break;
     case GEMM_CONV_FWD: e = dispatch<0, 0, 0, CONV_FWD>(tl, ta, tb, tb2, em, args, st); break;
     case GEMM_CONV_DGRAD: e = dispatch<0, 1, 0, CONV_DGRAD>(tl, ta, tb, tb2, em, args, st); break;
     case GEMM_CONV_DGRAD_BLEND:
-      e = tl.cg == 2 ? (blend_mh2(args) ? launch<256, 0, 1, 1, 0, 2, CONV_DGRAD, 2>(ta, tb, tb2, em, args, st)
-                                        : launch<256, 0, 1, 1, 0, 2, CONV_DGRAD>(ta, tb, tb2, em, args, st))
+      e = tl.cg == 2 ? (tl.bn == 128 ? launch<128, 0, 1, 1, 0, 2, CONV_DGRAD>(ta, tb, tb2, em, args, st)
+                        : blend_mh2(args) ? launch<256, 0, 1, 1, 0, 2, CONV_DGRAD, 2>(ta, tb, tb2, em, args, st)
+                                          : launch<256, 0, 1, 1, 0, 2, CONV_DGRAD>(ta, tb, tb2, em, args, st))
                      : launch<128, 0, 1, 1, 0, 1, CONV_DGRAD>(ta, tb, tb2, em, args, st);
       break;
     case GEMM_CONV_WGRAD:

@@ -150,6 +150,14 @@ __device__ __forceinline__ uint64_t blend_tf32x2(uint64_t a, uint64_t b, uint64_
   asm("mov.b64 %0, {%1, %2};" : "=l"(out) : "f"(rna_tf32(lo)), "f"(rna_tf32(hi)));
   return out;
 }
+// Ampere-style 16-byte global -> shared copy (LDGSTS, L2 only), and the per-thread arrival on an
+// mbarrier once all of this thread's prior cp.async copies have landed (no pending-count increment)
+__device__ __forceinline__ void cp_async_16(void* smem_dst, const void* gmem_src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 // generic-proxy smem writes -> visible to the async proxy (tensor core / TMA)
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");

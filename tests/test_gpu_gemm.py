@@ -86,8 +86,10 @@ def test_wgrad_both_mn_major(gpu_lib, M, N, K):
 
 
 # (2048, 4096, 1024) and (1800, 4000, 1040) run on 512-row CTA-pair tiles (two accumulators sharing
-# one blended B tile, ragged M / N / K tails in the second case); the others on 256- or 128-row tiles
-@pytest.mark.parametrize("M,N,K", [(64, 256, 64), (300, 264, 136), (2048, 4096, 1024), (1800, 4000, 1040)])
+# one blended B tile, ragged M / N / K tails in the second case); (512, 4096, 1024) and (520, 3000, 200)
+# on 256 x 128 CTA-pair tiles; the others on 128-row single-CTA tiles
+@pytest.mark.parametrize("M,N,K", [(64, 256, 64), (300, 264, 136), (2048, 4096, 1024), (1800, 4000, 1040),
+                                   (512, 4096, 1024), (520, 3000, 200)])
 @pytest.mark.parametrize("a,b", [(0.25, 0.75), (0.9512294, 0.0487706), (-6.0, 0.0)])
 def test_dgrad_blended_operand(gpu_lib, M, N, K, a, b):
     # G · bf16(α·W_stash + β·W_latest), operand formed in shared memory (K8 definition, reading Z14)

@@ -90,7 +90,8 @@ def test_tf32_wgrad(gpu_lib, M, N, K):
 
 
 # 128-row (CG = 1), 256-row pair and 512-row pair (MH = 2) tiles
-@pytest.mark.parametrize("M,N,K", [(64, 256, 64), (300, 264, 136), (2048, 4096, 1024), (1800, 4000, 1040)])
+@pytest.mark.parametrize("M,N,K", [(64, 256, 64), (300, 264, 136), (2048, 4096, 1024), (1800, 4000, 1040),
+                                   (512, 4096, 1024)])
 @pytest.mark.parametrize("a,b", [(0.25, 0.75), (-6.0, 0.0)])
 def test_tf32_dgrad_blended_operand(gpu_lib, M, N, K, a, b):
     g = torch.Generator(device="cuda").manual_seed(11 + M)
