@@ -57,7 +57,8 @@ def main():
     spec = tps.StageSpec(dims=dims, stage_bounds=bounds, stage_id=stage, micro_batches=m, micro_batch_size=b,
                          variant=case["variant"], blend=case["blend"], lam=case["lam"], lr=case["lr"],
                          momentum=case["mu"], transport=tps.TPS_TRANSPORT_IPC, device=a.device,
-                         fuse_update=case.get("fuse", 1), layers=layers, dp_size=a.dp, dp_rank=rep_id)
+                         fuse_update=case.get("fuse", 1), layers=layers, dp_size=a.dp, dp_rank=rep_id,
+                         dtype=case.get("dtype", 0))
     p = tps.Pipeline(spec)
     for k, l in enumerate(p.layers):
         if w0[l] is not None:
@@ -72,7 +73,8 @@ def main():
         dist.all_gather_object(dblobs, p.dp_export())
         p.dp_connect([dblobs[r * S + stage] for r in range(a.dp)])
     dist.barrier()
-    x_pool = torch.from_numpy(np.stack(xs)).to(torch.bfloat16).cuda() if stage == 0 else None
+    xdt = torch.float32 if case.get("dtype", 0) == tps.TPS_TF32 else torch.bfloat16   # tf32: fp32 containers
+    x_pool = torch.from_numpy(np.stack(xs)).to(xdt).cuda() if stage == 0 else None
     y_pool = torch.from_numpy(np.stack(ys)).cuda() if stage == S - 1 else None
     torch.cuda.synchronize()
     p.run_schedule(0, M, x_pool, y_pool, M)

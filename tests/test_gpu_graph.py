@@ -16,12 +16,12 @@ from paper_2509_23241_b200 import tps
 pytestmark = pytest.mark.gpu
 
 
-def make(dims, bounds, m, b, variant, blend, fuse=1):
+def make(dims, bounds, m, b, variant, blend, fuse=1, dtype=tps.TPS_BF16):
     S = len(bounds) - 1
     st = [tps.Pipeline(tps.StageSpec(dims=dims, stage_bounds=bounds, stage_id=s, micro_batches=m, micro_batch_size=b,
                                      variant=variant, blend=blend, lam=0.3, lr=0.05, momentum=0.9, seed=3,
                                      transport=tps.TPS_TRANSPORT_LOCAL if S > 1 else tps.TPS_TRANSPORT_NONE,
-                                     fuse_update=fuse))
+                                     fuse_update=fuse, dtype=dtype))
           for s in range(S)]
     for h in st:
         h.init_weights_synthetic()
@@ -30,9 +30,10 @@ def make(dims, bounds, m, b, variant, blend, fuse=1):
     return st
 
 
-def pools(dims, m, b, pool):
+def pools(dims, m, b, pool, dtype=tps.TPS_BF16):
     B = m * b
-    x = torch.from_numpy(np.stack([synthgen.inputs(3, j, B, dims[0]) for j in range(pool)])).to(torch.bfloat16).cuda()
+    xdt = torch.float32 if dtype == tps.TPS_TF32 else torch.bfloat16
+    x = torch.from_numpy(np.stack([synthgen.inputs(3, j, B, dims[0]) for j in range(pool)])).to(xdt).cuda()
     y = torch.from_numpy(np.stack([synthgen.labels(3, j, B, dims[-1]) for j in range(pool)])).cuda()
     return x, y
 
@@ -46,22 +47,23 @@ def state(st):
     return out, trace
 
 
-@pytest.mark.parametrize("dims,bounds,m,b,pool,n,variant,blend,fuse", [
-    ([256, 256, 192, 128, 10], [0, 2, 4], 2, 32, 6, 12, tps.TPS_I, tps.TPS_BLEND_CONVEX, 1),   # period 6
-    ([256, 256, 192, 128, 10], [0, 1, 2, 4], 2, 32, 8, 24, tps.TPS_I, tps.TPS_BLEND_EQ1, 0),   # period 24
-    ([512, 512, 512, 10], [0, 3], 4, 64, 4, 8, tps.TPS_I, tps.TPS_BLEND_EQ1, 1),              # one stage
-    ([256, 256, 10], [0, 1, 2], 2, 16, 6, 6, tps.TPS_V, tps.TPS_BLEND_EQ1, 1),
+@pytest.mark.parametrize("dims,bounds,m,b,pool,n,variant,blend,fuse,dtype", [
+    ([256, 256, 192, 128, 10], [0, 2, 4], 2, 32, 6, 12, tps.TPS_I, tps.TPS_BLEND_CONVEX, 1, tps.TPS_BF16),   # period 6
+    ([256, 256, 192, 128, 10], [0, 1, 2, 4], 2, 32, 8, 24, tps.TPS_I, tps.TPS_BLEND_EQ1, 0, tps.TPS_BF16),   # period 24
+    ([512, 512, 512, 10], [0, 3], 4, 64, 4, 8, tps.TPS_I, tps.TPS_BLEND_EQ1, 1, tps.TPS_BF16),              # one stage
+    ([256, 256, 10], [0, 1, 2], 2, 16, 6, 6, tps.TPS_V, tps.TPS_BLEND_EQ1, 1, tps.TPS_BF16),
+    ([256, 256, 192, 128, 10], [0, 2, 4], 2, 32, 6, 12, tps.TPS_I, tps.TPS_BLEND_CONVEX, 1, tps.TPS_TF32),   # tf32 (Z28)
 ])
-def test_graph_replay_equals_walk_bitwise(gpu_lib, dims, bounds, m, b, pool, n, variant, blend, fuse):
-    x, y = pools(dims, m, b, pool)
+def test_graph_replay_equals_walk_bitwise(gpu_lib, dims, bounds, m, b, pool, n, variant, blend, fuse, dtype):
+    x, y = pools(dims, m, b, pool, dtype)
     stream = torch.cuda.Stream()
     runs = 3
-    walked = make(dims, bounds, m, b, variant, blend, fuse)
+    walked = make(dims, bounds, m, b, variant, blend, fuse, dtype)
     for r in range(runs):
         tps.run_schedule_local(walked, r * n, n, x, y, pool)
     for h in walked:
         h.synchronize()
-    graphed = make(dims, bounds, m, b, variant, blend, fuse)
+    graphed = make(dims, bounds, m, b, variant, blend, fuse, dtype)
     g = tps.Graph(graphed, 0, n, x, y, pool, stream.cuda_stream)
     for _ in range(runs - 1):
         g.replay()

@@ -87,7 +87,7 @@ def local_reference(case):
     blend = ost.EQ1 if case["blend"] == 0 else ost.CONVEX
     stages, losses = run_gpu(case["dims"], case["bounds"], case["m"], case["b"], case["M"], var, blend, case["lam"],
                              case["lr"], case["mu"], kind=case["kind"], layers=case.get("layers"),
-                             fuse_update=case.get("fuse", 1))
+                             fuse_update=case.get("fuse", 1), dtype=case.get("dtype", 0))
     w = [[st.get_weights(k) if st.shapes[k] is not None else None for k in range(len(st.layers))] for st in stages]
     for st in stages:
         st.close()
@@ -124,6 +124,24 @@ def test_ipc_mlp_three_processes(gpu_lib, direct, variant, blend):
             w, bb, _, _ = st["weights"][k]
             assert weight_rel_err(w, ref.weights[l]) <= 5e-3
             assert layer_rel_err(w, bb, ref.weights[l], ref.biases[l]) <= 5e-3
+
+
+@pytest.mark.timeout(900, method="thread")
+def test_ipc_tf32_three_processes(gpu_lib):
+    """tf32 storage (reading Z28) over the IPC transport: 4-byte elements in every exchanged
+    buffer and offset (fused compute + send); bitwise equal to the LOCAL run, and the tf32 oracle's
+    trace / tolerances."""
+    case = dict(MLP, variant=1, blend=1, dtype=1)
+    res = run_ipc(case)
+    assert_same_as_local(res, case)
+    ref = run_oracle(case["dims"], case["bounds"], case["m"], case["b"], case["M"], ost.I_VARIANT, ost.CONVEX,
+                     case["lam"], case["lr"], case["mu"], kind=case["kind"], dtype="tf32")
+    assert trace_rows(res) == oracle_trace(ref)
+    np.testing.assert_allclose(res[-1]["losses"], ref.losses, rtol=1e-3, atol=0)
+    for st in res:
+        for k, l in enumerate(st["layers"]):
+            w, bb, _, _ = st["weights"][k]
+            assert weight_rel_err(w, ref.weights[l]) <= 5e-3
 
 
 @pytest.mark.timeout(900, method="thread")
