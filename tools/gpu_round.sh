@@ -44,9 +44,13 @@ for s in $STEPS; do
       timeout 600 python tools/gemm_bench.py --modes 0,1,2,3,4,7,8,9 --seconds 1.0 > ${O}_gemm.txt 2>&1 ;;
     ncu)
       # one launch each of fwd / dgrad / blended dgrad / fused wgrad + update at the C5 shapes
+      # (summarised on the box with stall reasons; only the dominant kernel's report is kept, so
+      # gpurun_out stays under the 64 MiB copy-back limit)
       for m in 0 1 3 4; do
         timeout 400 ncu --set full --clock-control none --import-source on -k regex:gemm_kernel -s 3 -c 1 \
           -o ${O}_mode$m python tools/gemm_bench.py --modes $m --iters 1 > ${O}_ncu_mode$m.log 2>&1
+        python tools/ncu_summary.py ${O}_mode$m.ncu-rep --stalls --json ${O}_ncu_mode$m.json > /dev/null 2>&1
+        [ $m = 4 ] || rm -f ${O}_mode$m.ncu-rep
       done ;;
     sanitize)
       for tool in racecheck synccheck memcheck; do
