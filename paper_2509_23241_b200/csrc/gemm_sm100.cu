@@ -522,13 +522,17 @@ __global__ void __launch_bounds__(Cfg<BN, BLEND, SGD, CG, MH>::THREADS, 1)
       uint8_t* w_s = ebase + (i % SGD_NB) * SGD_BUF;
       const size_t ld = static_cast<size_t>(args.ldo);
       const int j = lane & 7;
+      // rows past M (a tile's padding rows) and columns past N are not read (zero-filled, never
+      // written back): the TMA boxes clip them the same way
+      const bool col_ok = col0 + j * 4 + 4 <= args.N;
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         const int rr = (lane >> 3) + 4 * k;
-        const size_t g = static_cast<size_t>(row0 + rr) * ld + col0 + j * 4;
+        const bool ok = col_ok && row0 + rr < args.M;
+        const size_t g = ok ? static_cast<size_t>(row0 + rr) * ld + col0 + j * 4 : 0;
         const int off = rr * 128 + ((j ^ (rr & 7)) * 16);
-        ptx::cp_async_16(w_s + off, args.w + g);
-        if (mom) ptx::cp_async_16(w_s + SGD_WBYTES + off, args.v + g);
+        ptx::cp_async_16(w_s + off, args.w + g, ok ? 16u : 0u);
+        if (mom) ptx::cp_async_16(w_s + SGD_WBYTES + off, args.v + g, ok ? 16u : 0u);
       }
       ptx::cp_async_mbar_arrive_noinc(&ebar[i % SGD_NB]);
     };

@@ -152,8 +152,11 @@ __device__ __forceinline__ uint64_t blend_tf32x2(uint64_t a, uint64_t b, uint64_
 }
 // Ampere-style 16-byte global -> shared copy (LDGSTS, L2 only), and the per-thread arrival on an
 // mbarrier once all of this thread's prior cp.async copies have landed (no pending-count increment)
-__device__ __forceinline__ void cp_async_16(void* smem_dst, const void* gmem_src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gmem_src) : "memory");
+// (src_bytes < 16: the rest of the 16 bytes is zero-filled; 0 reads nothing, for out-of-range sources)
+__device__ __forceinline__ void cp_async_16(void* smem_dst, const void* gmem_src, uint32_t src_bytes = 16) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(smem_dst)), "l"(gmem_src),
+               "r"(src_bytes)
+               : "memory");
 }
 __device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint64_t* bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");

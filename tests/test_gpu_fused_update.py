@@ -66,3 +66,38 @@ def test_raw_fused_kernel_matches_oracle_update(gpu_lib, MNK, mu):
     if mu:
         assert np.abs(v.cpu().numpy() - vr).max() <= 1e-3 * np.abs(vr - v0.numpy()).max() + 1e-6 * np.abs(vr).max()
     np.testing.assert_array_equal(q.float().cpu().numpy(), obf.rne(wg.astype(np.float64)))
+
+
+@pytest.mark.parametrize("MNK", [(16, 4096, 2048), (16, 784, 512), (200, 520, 256)])
+def test_fused_update_reads_nothing_past_w(gpu_lib, MNK):
+    """Tiles are 128 (or 256) rows and 32-column chunks wide: rows past M and columns past N of
+    w / v must not be read (the head layer has M = 16).  w / v / version sit at the very END of a
+    dedicated allocation (a tensor of >= 2 MiB gets its own cudaMalloc segment), so a read past
+    them touches unmapped memory and faults; the update must still match the oracle's."""
+    import torch
+    from oracle import bf16 as obf
+    from oracle import mlp as omlp
+    from paper_2509_23241_b200 import tps
+    M, N, K = MNK
+    g = torch.Generator().manual_seed(7 + M)
+    A = torch.randn(K, M, generator=g).to(torch.bfloat16)
+    B = torch.randn(K, N, generator=g).to(torch.bfloat16)
+    w0 = torch.randn(M, N, generator=g)
+    v0 = torch.randn(M, N, generator=g) * 0.1
+
+    def at_end(n, dtype):
+        seg = (4 << 20) // torch.tensor([], dtype=dtype).element_size()
+        buf = torch.zeros(max(seg, n), dtype=dtype, device="cuda")
+        return buf[buf.numel() - n:].view(M, N)
+
+    w, v, q = at_end(M * N, torch.float32), at_end(M * N, torch.float32), at_end(M * N, torch.bfloat16)
+    w.copy_(w0.cuda())
+    v.copy_(v0.cuda())
+    lr, mu, wd = 0.01, 0.9, 1e-4
+    tps.gemm_wgrad_sgd(M, N, K, A.cuda(), M, B.cuda(), N, w, v, q, N, lr, mu, wd)
+    torch.cuda.synchronize()
+    gref = (A.double().T @ B.double()).numpy().astype(np.float32)
+    wr, vr = omlp.sgd_update(w0.numpy(), v0.numpy(), gref, lr, mu, wd, False)
+    wg = w.cpu().numpy()
+    assert np.abs(wg - wr).max() <= 1e-3 * np.abs(wr - w0.numpy()).max() + 1e-6 * np.abs(wr).max()
+    np.testing.assert_array_equal(q.float().cpu().numpy(), obf.rne(wg.astype(np.float64)))
