@@ -32,7 +32,9 @@ def family(name):
 
 def main(path, out, src):
     rows = list(csv.reader(open(path)))
-    hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
+    hi = next((i for i, r in enumerate(rows) if "Kernel Name" in r), None)
+    if hi is None:   # ncu captured nothing (the profiled program failed): say so instead of a traceback
+        raise SystemExit(f"{path}: no kernel rows (did the profiled command fail? see its log)")
     hdr = rows[hi]
     ki, ui, vi = hdr.index("Kernel Name"), hdr.index("Metric Unit"), hdr.index("Metric Value")
     agg = collections.defaultdict(lambda: [0, 0.0])
