@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 
 #include "kernels.h"
 
@@ -296,9 +297,14 @@ __global__ void bias_grad_final(const float* __restrict__ part, int splits, int 
 }
 
 int bias_grad_splits(int rows, int cols) {
+  // blocks per SM of the column-sum pass (TPS_BG_WAVES, default 2) and at least
+  // TPS_BG_MIN_ROWS rows per split (default 64); read once, so the scratch sized at init fits
+  static const int waves = std::getenv("TPS_BG_WAVES") ? std::max(1, std::atoi(std::getenv("TPS_BG_WAVES"))) : 2;
+  static const int min_rows =
+      std::getenv("TPS_BG_MIN_ROWS") ? std::max(8, std::atoi(std::getenv("TPS_BG_MIN_ROWS"))) : 64;
   const int col_blocks = (cols + BG_COLS - 1) / BG_COLS;
-  int splits = (2 * sm_count() + col_blocks - 1) / col_blocks;
-  const int max_splits = (rows + 63) / 64;
+  int splits = (waves * sm_count() + col_blocks - 1) / col_blocks;
+  const int max_splits = (rows + min_rows - 1) / min_rows;
   if (splits > max_splits) splits = max_splits;
   if (splits < 1) splits = 1;
   return splits;
@@ -601,10 +607,11 @@ __global__ void bn_stats_final(const double* __restrict__ part, int chunks, int 
   if (i >= segs * C) return;
   const int seg = i / C, c = i - seg * C;
   double s1 = 0.0, s2 = 0.0;
+#pragma unroll 8
   for (int k = lane; k < chunks; k += 32) {
     const size_t o = (static_cast<size_t>(seg) * chunks + k) * C + c;
-    s1 += part[2 * o];
-    s2 += part[2 * o + 1];
+    s1 += __ldcg(part + 2 * o);
+    s2 += __ldcg(part + 2 * o + 1);
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
@@ -862,9 +869,36 @@ __device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
   return o;
 }
 
+// bit e = [bf16 element e of v > 0] (0 < bits <= 0x7F80: positive, +inf included, NaN excluded)
+__device__ __forceinline__ uint8_t relu_bits8(const uint4& v) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+  uint32_t m = 0;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const uint32_t h = (w[e >> 1] >> ((e & 1) * 16)) & 0xFFFFu;
+    m |= static_cast<uint32_t>(h - 1u < 0x7F80u) << e;
+  }
+  return static_cast<uint8_t>(m);
+}
+
 __device__ __forceinline__ void load8f(const float* p, float (&f)[8]) {
   const float4 a = *reinterpret_cast<const float4*>(p), b = *reinterpret_cast<const float4*>(p + 4);
   f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w; f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+}
+
+// gradient of the global average pool over 8 channels per thread (C % 8 == 0): 16-byte stores
+__global__ void avgpool_bwd_vec(const uint4* __restrict__ dY, uint4* __restrict__ dX, int N, int HW, int C8) {
+  const int64_t total = static_cast<int64_t>(N) * HW * C8;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int cv = static_cast<int>(i % C8);
+    const int64_t n = i / (static_cast<int64_t>(HW) * C8);
+    float d[8];
+    unpack8(__ldg(dY + n * C8 + cv), d);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) d[e] = d[e] / HW;
+    dX[i] = pack8(d);
+  }
 }
 
 // Row-mapped BN apply kernels: a thread owns one 8-channel group and walks rows, so the
@@ -875,7 +909,7 @@ __global__ void __launch_bounds__(256) bn_apply_rows(const uint4* __restrict__ x
                                                      uint4* __restrict__ y, const float* __restrict__ gamma,
                                                      const float* __restrict__ beta, const float* __restrict__ mean,
                                                      const float* __restrict__ invstd, int rows, int C8, int seg_rows,
-                                                     int relu) {
+                                                     int relu, uint8_t* __restrict__ mask) {
   const int tx = min(C8, 32), ty = blockDim.x / tx;
   const int cg = blockIdx.x * tx + static_cast<int>(threadIdx.x) % tx;
   if (cg >= C8 || static_cast<int>(threadIdx.x) >= tx * ty) return;
@@ -908,7 +942,9 @@ __global__ void __launch_bounds__(256) bn_apply_rows(const uint4* __restrict__ x
 #pragma unroll
       for (int e = 0; e < 8; ++e) v[e] = fmaxf(v[e], 0.f);
     }
-    y[o] = pack8(v);
+    const uint4 py = pack8(v);
+    y[o] = py;
+    if (mask) mask[o] = relu_bits8(py);
   }
 }
 
@@ -916,7 +952,7 @@ __global__ void __launch_bounds__(256) bn_bwd_apply_rows(const uint4* __restrict
                                                          const uint4* __restrict__ xv, const float4* __restrict__ coef,
                                                          const float* __restrict__ invstd, int rows, int C8,
                                                          int seg_rows, int relu, uint4* __restrict__ dx,
-                                                         uint4* __restrict__ dres) {
+                                                         uint4* __restrict__ dres, const uint8_t* __restrict__ mask) {
   const int tx = min(C8, 32), ty = blockDim.x / tx;
   const int cg = blockIdx.x * tx + static_cast<int>(threadIdx.x) % tx;
   if (cg >= C8 || static_cast<int>(threadIdx.x) >= tx * ty) return;
@@ -941,7 +977,12 @@ __global__ void __launch_bounds__(256) bn_bwd_apply_rows(const uint4* __restrict
     float d[8], xx[8], out[8];
     unpack8(dy[o], d);
     unpack8(xv[o], xx);
-    if (relu) {
+    if (relu && mask) {
+      const uint32_t mb = mask[o];
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        if (!((mb >> e) & 1u)) d[e] = 0.f;
+    } else if (relu) {
       float yy[8];
       unpack8(yv[o], yy);
 #pragma unroll
@@ -965,7 +1006,8 @@ template <int MODE>
 __global__ void __launch_bounds__(256) bn_partial_vec(const uint4* __restrict__ a, const uint4* __restrict__ yv,
                                                       const uint4* __restrict__ xv, const float* __restrict__ mean,
                                                       const float* __restrict__ invstd, int seg_rows, int C8,
-                                                      int chunks, int relu, double* __restrict__ part) {
+                                                      int chunks, int relu, double* __restrict__ part,
+                                                      const uint8_t* __restrict__ mask = nullptr) {
   extern __shared__ double red[];            // [ty][tx][16]
   const int tx = min(C8, 32), ty = blockDim.x / tx;
   const int lx = threadIdx.x % tx, ly = threadIdx.x / tx;
@@ -998,7 +1040,13 @@ __global__ void __launch_bounds__(256) bn_partial_vec(const uint4* __restrict__ 
       } else {
         float yy[8], xx[8];
         unpack8(xv[o], xx);
-        if (relu) unpack8(yv[o], yy);
+        if (relu && mask) {
+          const uint32_t mb = mask[o];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) yy[e] = ((mb >> e) & 1u) ? 1.f : 0.f;
+        } else if (relu) {
+          unpack8(yv[o], yy);
+        }
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           const double d = (relu && !(yy[e] > 0.f)) ? 0.0 : static_cast<double>(v[e]);
@@ -1034,23 +1082,27 @@ __global__ void __launch_bounds__(256) bn_partial_vec(const uint4* __restrict__ 
 }
 
 // backward coefficients per (segment, channel), packed float4 {γ_r·invstd, Σdy'/m, Σdy'x̂/m, mean}
-// with γ_r = a·γ_stash + b·γ_latest; and dγ, dβ summed over segments
-// one warp per channel: lanes stride the chunks, shuffle tree (fixed order), lane 0 writes
-__global__ void bn_bwd_coef(const double* __restrict__ part, int chunks, int C, int segs, int seg_rows,
-                            const float* __restrict__ mean, const float* __restrict__ invstd,
-                            const float* __restrict__ gs, const float* __restrict__ gl, float ga, float gb,
-                            float4* __restrict__ coef, float* __restrict__ dgamma, float* __restrict__ dbeta) {
-  const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (c >= C) return;
+// with γ_r = a·γ_stash + b·γ_latest; and dγ, dβ summed over segments in segment order.
+// One block per channel, one warp per segment (warps stride the segments): lanes stride the
+// chunks, fixed shuffle tree, lane 0 parks the segment's sums in shared memory; thread 0 then
+// adds them in segment order.  (One warp per channel walking the segments serially left the
+// grid at C/8 blocks and ran ~29 µs per launch, latency-bound, on ResNet-50's 64-channel layers.)
+constexpr int kBnCoefWarps = 8;
+__global__ void __launch_bounds__(32 * kBnCoefWarps) bn_bwd_coef(
+    const double* __restrict__ part, int chunks, int C, int segs, int seg_rows, const float* __restrict__ mean,
+    const float* __restrict__ invstd, const float* __restrict__ gs, const float* __restrict__ gl, float ga, float gb,
+    float4* __restrict__ coef, float* __restrict__ dgamma, float* __restrict__ dbeta) {
+  extern __shared__ double seg_sums[];   // [segs][2]
+  const int c = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const float g = __fadd_rn(__fmul_rn(ga, gs[c]), __fmul_rn(gb, gl[c]));
-  double tg = 0.0, tb = 0.0;
-  for (int seg = 0; seg < segs; ++seg) {
+  for (int seg = warp; seg < segs; seg += blockDim.x >> 5) {
     double s1 = 0.0, s2 = 0.0;
+#pragma unroll 8
     for (int k = lane; k < chunks; k += 32) {
       const size_t o = (static_cast<size_t>(seg) * chunks + k) * C + c;
-      s1 += part[2 * o];
-      s2 += part[2 * o + 1];
+      s1 += __ldcg(part + 2 * o);
+      s2 += __ldcg(part + 2 * o + 1);
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
@@ -1058,13 +1110,19 @@ __global__ void bn_bwd_coef(const double* __restrict__ part, int chunks, int C, 
       s2 += __shfl_xor_sync(0xffffffffu, s2, off);
     }
     if (lane) continue;
-    tb += s1;
-    tg += s2;
+    seg_sums[2 * seg] = s1;
+    seg_sums[2 * seg + 1] = s2;
     const int sc = seg * C + c;
     coef[sc] = make_float4(g * invstd[sc], static_cast<float>(s1 / seg_rows), static_cast<float>(s2 / seg_rows),
                            mean[sc]);
   }
-  if (lane) return;
+  __syncthreads();
+  if (threadIdx.x) return;
+  double tg = 0.0, tb = 0.0;
+  for (int seg = 0; seg < segs; ++seg) {
+    tb += seg_sums[2 * seg];
+    tg += seg_sums[2 * seg + 1];
+  }
   dgamma[c] = static_cast<float>(tg);
   dbeta[c] = static_cast<float>(tb);
 }
@@ -1178,6 +1236,52 @@ __global__ void col2im_vec4(const float* __restrict__ dP, uint2* __restrict__ dX
     }
     if (add) {
       const uint2 a = add[i];
+      acc.x += bf2f(a.x & 0xFFFFu); acc.y += bf2f(a.x >> 16); acc.z += bf2f(a.y & 0xFFFFu); acc.w += bf2f(a.y >> 16);
+    }
+    dX[i] = make_uint2(static_cast<uint32_t>(f2bf(acc.x)) | (static_cast<uint32_t>(f2bf(acc.y)) << 16),
+                       static_cast<uint32_t>(f2bf(acc.z)) | (static_cast<uint32_t>(f2bf(acc.w)) << 16));
+  }
+}
+
+// col2im_vec4 with the kernel size and stride fixed at compile time (the strided ResNet-50
+// convolutions: 3x3/2 and 1x1/2): every tap's load is issued before the first add (predicated,
+// up to ceil(K/S)^2 live), where the generic loop's data-dependent branches serialised them; the
+// adds keep the generic kernel's order (kh, kw ascending), so the result is bitwise the same
+template <int K, int S>
+__global__ void __launch_bounds__(256) col2im_vec4_ks(const float* __restrict__ dP, uint2* __restrict__ dX,
+                                                      const uint2* __restrict__ add, int N, int H, int W, int C,
+                                                      int p, int Ho, int Wo, int ldp) {
+  const int C4 = C / 4;
+  const int64_t total = static_cast<int64_t>(N) * H * W * C4;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int c = static_cast<int>(i % C4) * 4;
+    int64_t t = i / C4;
+    const int w = static_cast<int>(t % W);
+    t /= W;
+    const int h = static_cast<int>(t % H);
+    const int64_t n = t / H;
+    float4 v[K * K];
+    bool ok[K * K];
+#pragma unroll
+    for (int kh = 0; kh < K; ++kh) {
+#pragma unroll
+      for (int kw = 0; kw < K; ++kw) {
+        const int hy = h + p - kh, wy = w + p - kw;
+        const int ho = hy / S, wo = wy / S;
+        const bool o = hy >= 0 && hy % S == 0 && ho < Ho && wy >= 0 && wy % S == 0 && wo < Wo;
+        ok[kh * K + kw] = o;
+        v[kh * K + kw] = o ? __ldcs(reinterpret_cast<const float4*>(
+                                 dP + ((n * Ho + ho) * Wo + wo) * static_cast<int64_t>(ldp) + (kh * K + kw) * C + c))
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+    const uint2 a = add ? __ldcs(add + i) : make_uint2(0u, 0u);
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int q = 0; q < K * K; ++q)
+      if (ok[q]) { acc.x += v[q].x; acc.y += v[q].y; acc.z += v[q].z; acc.w += v[q].w; }
+    if (add) {
       acc.x += bf2f(a.x & 0xFFFFu); acc.y += bf2f(a.x >> 16); acc.z += bf2f(a.y & 0xFFFFu); acc.w += bf2f(a.y >> 16);
     }
     dX[i] = make_uint2(static_cast<uint32_t>(f2bf(acc.x)) | (static_cast<uint32_t>(f2bf(acc.y)) << 16),
@@ -1468,7 +1572,12 @@ cudaError_t launch_col2im(const float* dP, uint16_t* dX, const uint16_t* add, in
   const int Ho = (H + 2 * p - k) / s + 1, Wo = (W + 2 * p - k) / s + 1;
   const int64_t total = static_cast<int64_t>(N) * H * W * C;
   if (total <= 0) return cudaSuccess;
-  if (C % 4 == 0 && ldp % 4 == 0) {
+  static const bool generic = std::getenv("TPS_COL2IM_GENERIC") != nullptr;   // A/B of the specialised kernel
+  if (C % 4 == 0 && ldp % 4 == 0 && s == 2 && (k == 3 || k == 1) && !generic) {
+    auto* kern = k == 3 ? col2im_vec4_ks<3, 2> : col2im_vec4_ks<1, 2>;
+    kern<<<grid_for(total / 4, 256), 256, 0, st>>>(dP, reinterpret_cast<uint2*>(dX), reinterpret_cast<const uint2*>(add),
+                                                   N, H, W, C, p, Ho, Wo, ldp);
+  } else if (C % 4 == 0 && ldp % 4 == 0) {
     col2im_vec4<<<grid_for(total / 4, 256), 256, 0, st>>>(dP, reinterpret_cast<uint2*>(dX),
                                                           reinterpret_cast<const uint2*>(add), N, H, W, C, k, s, p, Ho,
                                                           Wo, ldp);
@@ -1504,9 +1613,10 @@ int64_t bn_scratch_doubles(int segs, int seg_rows, int C) {
 
 cudaError_t launch_bn_forward(const uint16_t* x, const uint16_t* res, uint16_t* y, const float* gamma,
                               const float* beta, float* mean, float* invstd, int segs, int seg_rows, int C, int relu,
-                              double* scratch, cudaStream_t st) {
+                              double* scratch, cudaStream_t st, uint8_t* relu_mask) {
   const int chunks = bn_chunks(segs, seg_rows, C);
   const int64_t rows = static_cast<int64_t>(segs) * seg_rows;
+  if (!relu || C % 8) relu_mask = nullptr;
   if (C % 8 == 0) {
     const int C8 = C / 8, tx = std::min(C8, 32);
     dim3 grid((C8 + tx - 1) / tx, chunks, segs);
@@ -1518,7 +1628,7 @@ cudaError_t launch_bn_forward(const uint16_t* x, const uint16_t* res, uint16_t* 
       const int C8r = C8, tx = std::min(C8r, 32);
       bn_apply_rows<<<bn_rows_grid(static_cast<int>(rows), C8r), tx * (256 / tx), 0, st>>>(
           reinterpret_cast<const uint4*>(x), reinterpret_cast<const uint4*>(res), reinterpret_cast<uint4*>(y), gamma,
-          beta, mean, invstd, static_cast<int>(rows), C8r, seg_rows, relu);
+          beta, mean, invstd, static_cast<int>(rows), C8r, seg_rows, relu, relu_mask);
     }
     return cudaGetLastError();
   }
@@ -1531,8 +1641,10 @@ cudaError_t launch_bn_forward(const uint16_t* x, const uint16_t* res, uint16_t* 
 
 cudaError_t launch_bn_forward_colsum(const float* part, const uint16_t* x, const uint16_t* res, uint16_t* y,
                                     const float* gamma, const float* beta, float* mean, float* invstd, int segs,
-                                    int seg_rows, int C, int relu, double* scratch, cudaStream_t st) {
+                                    int seg_rows, int C, int relu, double* scratch, cudaStream_t st,
+                                    uint8_t* relu_mask) {
   if (seg_rows % 32 || C % 8) return cudaErrorInvalidValue;
+  if (!relu) relu_mask = nullptr;
   const int gps = seg_rows / 32;
   const int64_t rows = static_cast<int64_t>(segs) * seg_rows;
   const int chunks = std::min(bn_chunks(segs, seg_rows, C), gps);
@@ -1542,15 +1654,16 @@ cudaError_t launch_bn_forward_colsum(const float* part, const uint16_t* x, const
   const int C8 = C / 8, tx = std::min(C8, 32);
   bn_apply_rows<<<bn_rows_grid(static_cast<int>(rows), C8), tx * (256 / tx), 0, st>>>(
       reinterpret_cast<const uint4*>(x), reinterpret_cast<const uint4*>(res), reinterpret_cast<uint4*>(y), gamma, beta,
-      mean, invstd, static_cast<int>(rows), C8, seg_rows, relu);
+      mean, invstd, static_cast<int>(rows), C8, seg_rows, relu, relu_mask);
   return cudaGetLastError();
 }
 
 cudaError_t launch_bn_backward(const uint16_t* dy, const uint16_t* y, const uint16_t* x, const float* mean,
                                const float* invstd, const float* gs, const float* gl, float ga, float gb, int segs,
                                int seg_rows, int C, int relu, uint16_t* dx, uint16_t* dres, float* dgamma,
-                               float* dbeta, double* scratch, cudaStream_t st) {
+                               float* dbeta, double* scratch, cudaStream_t st, const uint8_t* relu_mask) {
   const int chunks = bn_chunks(segs, seg_rows, C);
+  if (!relu || C % 8) relu_mask = nullptr;
   double* sums = scratch + static_cast<int64_t>(segs) * chunks * C * 2;
   if (C % 8 == 0) {
     const int C8 = C / 8, tx = std::min(C8, 32);
@@ -1558,16 +1671,17 @@ cudaError_t launch_bn_backward(const uint16_t* dy, const uint16_t* y, const uint
     dim3 grid((C8 + tx - 1) / tx, chunks, segs);
     bn_partial_vec<1><<<grid, tx * (256 / tx), 256 * 16 * sizeof(double), st>>>(
         reinterpret_cast<const uint4*>(dy), reinterpret_cast<const uint4*>(y), reinterpret_cast<const uint4*>(x), mean,
-        invstd, seg_rows, C8, chunks, relu, scratch);
+        invstd, seg_rows, C8, chunks, relu, scratch, relu_mask);
     float4* coef = reinterpret_cast<float4*>(sums);   // segs·C float4 = the sums region
-    bn_bwd_coef<<<(C * 32 + 255) / 256, 256, 0, st>>>(scratch, chunks, C, segs, seg_rows, mean, invstd, gs, gl, ga,
+    bn_bwd_coef<<<C, 32 * std::min(segs, kBnCoefWarps), 2 * segs * sizeof(double), st>>>(
+        scratch, chunks, C, segs, seg_rows, mean, invstd, gs, gl, ga,
                                                       gb, coef, dgamma, dbeta);
     {
       const int C8r = C8, tx = std::min(C8r, 32);
       bn_bwd_apply_rows<<<bn_rows_grid(static_cast<int>(rows), C8r), tx * (256 / tx), 0, st>>>(
           reinterpret_cast<const uint4*>(dy), reinterpret_cast<const uint4*>(y), reinterpret_cast<const uint4*>(x),
           coef, invstd, static_cast<int>(rows), C8r, seg_rows, relu, reinterpret_cast<uint4*>(dx),
-          reinterpret_cast<uint4*>(dres));
+          reinterpret_cast<uint4*>(dres), relu_mask);
     }
     return cudaGetLastError();
   }
@@ -1626,6 +1740,11 @@ cudaError_t launch_avgpool_fwd(const uint16_t* X, uint16_t* Y, int N, int HW, in
 }
 
 cudaError_t launch_avgpool_bwd(const uint16_t* dY, uint16_t* dX, int N, int HW, int C, cudaStream_t st) {
+  if (C % 8 == 0) {
+    avgpool_bwd_vec<<<grid_for(static_cast<int64_t>(N) * HW * (C / 8), 256), 256, 0, st>>>(
+        reinterpret_cast<const uint4*>(dY), reinterpret_cast<uint4*>(dX), N, HW, C / 8);
+    return cudaGetLastError();
+  }
   avgpool_bwd_kernel<<<grid_for(static_cast<int64_t>(N) * HW * C, 256), 256, 0, st>>>(dY, dX, N, HW, C);
   return cudaGetLastError();
 }

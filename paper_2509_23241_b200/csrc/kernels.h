@@ -87,17 +87,20 @@ cudaError_t launch_col2im(const float* dP, uint16_t* dX, const uint16_t* add, in
 int64_t bn_scratch_doubles(int segs, int seg_rows, int C);
 cudaError_t launch_bn_forward(const uint16_t* x, const uint16_t* res, uint16_t* y, const float* gamma,
                               const float* beta, float* mean, float* invstd, int segs, int seg_rows, int C, int relu,
-                              double* scratch, cudaStream_t st);
+                              double* scratch, cudaStream_t st, uint8_t* relu_mask = nullptr);
+// relu_mask (optional, relu && C % 8 == 0): one byte per (row, 8-channel group), bit e = [y_e > 0],
+// written by the forward and read by the backward in place of y (0.125 instead of 2 B per element)
 // batch-norm forward whose statistics come from the producing convolution's epilogue column sums
 // (GemmArgs.colsum + colsum_sq over the same rows: Σx plane, then Σx² plane; seg_rows % 32 == 0):
 // same mean / invstd / y as launch_bn_forward up to the fp32 rounding of the 32-row partials
 cudaError_t launch_bn_forward_colsum(const float* part, const uint16_t* x, const uint16_t* res, uint16_t* y,
                                     const float* gamma, const float* beta, float* mean, float* invstd, int segs,
-                                    int seg_rows, int C, int relu, double* scratch, cudaStream_t st);
+                                    int seg_rows, int C, int relu, double* scratch, cudaStream_t st,
+                                    uint8_t* relu_mask = nullptr);
 cudaError_t launch_bn_backward(const uint16_t* dy, const uint16_t* y, const uint16_t* x, const float* mean,
                                const float* invstd, const float* gs, const float* gl, float ga, float gb, int segs,
                                int seg_rows, int C, int relu, uint16_t* dx, uint16_t* dres, float* dgamma,
-                               float* dbeta, double* scratch, cudaStream_t st);
+                               float* dbeta, double* scratch, cudaStream_t st, const uint8_t* relu_mask = nullptr);
 cudaError_t launch_maxpool3_fwd(const uint16_t* X, uint16_t* Y, int N, int H, int W, int C, cudaStream_t st);
 cudaError_t launch_maxpool3_bwd(const uint16_t* X, const uint16_t* dY, uint16_t* dX, int N, int H, int W, int C,
                                 cudaStream_t st);

@@ -65,6 +65,12 @@ tps_status fail(tps_status st, const char* fmt, ...) {
 
 inline int pad16(int d) { return (d + 15) / 16 * 16; }
 
+// TPS_RELU_MASK=0: BN backward reads y for the ReLU mask (A/B of the bit-mask path)
+bool no_relu_mask() {
+  const char* e = std::getenv("TPS_RELU_MASK");
+  return e && e[0] == '0';
+}
+
 bool is_host_ptr(const void* p) {
   if (!p) return false;
   cudaPointerAttributes a;
@@ -110,6 +116,9 @@ struct Layer {
   std::vector<float*> verf;           // BN: R fp32 γ versions [C]
   std::vector<float*> mean, invstd;   // BN: per stash slot, [m, C] per-micro-batch statistics
   std::vector<uint8_t*> argmax;       // MAXPOOL3 (C % 8 == 0): per stash slot, first-max tap per output
+  // BN with ReLU (C % 8 == 0): per stash slot, [rows, C/8] bytes, bit e = [y > 0]; the backward
+  // reads it instead of y (0.125 instead of 2 B per element, in both backward passes)
+  std::vector<uint8_t*> relu_mask;
   // this backward's bias gradient source: 32-row column sums of G written by the input-gradient
   // GEMM of the layer above (GemmArgs.colsum), or null (full pass over G)
   const float* bias_part = nullptr;
@@ -699,6 +708,12 @@ tps_status layer_forward(tps_pipeline* p, Layer& Lk, int nr, const uint16_t* Xin
 
 // ------------------------------------------------------------------ graph networks (ResNet)
 // local tensor t: -1 = stage input (input slot), k = output of local layer k (stash slot)
+// relu-mask bytes of rows [r0, ...) of stash slot `slot` (null: the backward reads y)
+uint8_t* relu_mask_at(Layer& L, int slot, int r0) {
+  if (L.relu_mask.empty()) return nullptr;
+  return L.relu_mask[slot] + static_cast<size_t>(r0) * L.hw_in * (L.Ci / 8);
+}
+
 uint16_t* gtensor(tps_pipeline* p, int slot0, int slot, int t) {
   return t < 0 ? p->act[slot0][0] : p->act[slot][t + 1];
 }
@@ -748,13 +763,14 @@ tps_status graph_forward(tps_pipeline* p, int64_t j, int a0, int cnt, int64_t v)
           CUDA_OK(tps::launch_bn_forward_colsum(p->bn_colsum, X, res, static_cast<uint16_t*>(out), L.verf[v % p->R], L.b,
                                                 L.mean[slot] + static_cast<size_t>(a0) * L.Ci,
                                                 L.invstd[slot] + static_cast<size_t>(a0) * L.Ci, cnt,
-                                                p->bsz * L.hw_in, L.Ci, L.relu ? 1 : 0, p->bn_scr, p->cs));
+                                                p->bsz * L.hw_in, L.Ci, L.relu ? 1 : 0, p->bn_scr, p->cs,
+                                                relu_mask_at(L, slot, r0)));
           p->launches += 3;
         } else {
           CUDA_OK(tps::launch_bn_forward(X, res, static_cast<uint16_t*>(out), L.verf[v % p->R], L.b,
                                          L.mean[slot] + static_cast<size_t>(a0) * L.Ci,
                                          L.invstd[slot] + static_cast<size_t>(a0) * L.Ci, cnt, p->bsz * L.hw_in, L.Ci,
-                                         L.relu ? 1 : 0, p->bn_scr, p->cs));
+                                         L.relu ? 1 : 0, p->bn_scr, p->cs, relu_mask_at(L, slot, r0)));
           p->launches += 3;
         }
         break;
@@ -936,7 +952,7 @@ tps_status graph_backward(tps_pipeline* p, int64_t j, int64_t v_used, int64_t vl
         const float ga = p->variant == TPS_I ? alpha : 1.f, gb = p->variant == TPS_I ? beta : 0.f;
         CUDA_OK(tps::launch_bn_backward(g, y, X, L.mean[slot], L.invstd[slot], L.verf[v_used % p->R],
                                         L.verf[vl % p->R], ga, gb, p->m, p->bsz * L.hw_in, L.Ci, L.relu ? 1 : 0, dx,
-                                        dres, L.dW, L.db, p->bn_scr, p->cs));
+                                        dres, L.dW, L.db, p->bn_scr, p->cs, relu_mask_at(L, slot, 0)));
         p->launches += 3;
         if (L.res >= -1) TPS_TRY(settle(L.res, rt, p->gtmp[0]));
         TPS_TRY(settle(L.src, xt, p->gtmp[1]));
@@ -1707,6 +1723,11 @@ tps_status init_graph(tps_pipeline* p, const tps_config* c, int lb, int le) {
         for (int r = 0; r < p->Kmax; ++r) {
           TPS_TRY(alloc_t(p, &L.mean[r], static_cast<size_t>(p->m) * L.Ci, &p->mem_acts));
           TPS_TRY(alloc_t(p, &L.invstd[r], static_cast<size_t>(p->m) * L.Ci, &p->mem_acts));
+        }
+        if (L.relu && L.Ci % 8 == 0 && !no_relu_mask()) {
+          L.relu_mask.resize(p->Kmax);
+          for (int r = 0; r < p->Kmax; ++r)
+            TPS_TRY(alloc_t(p, &L.relu_mask[r], static_cast<size_t>(p->B) * L.hw_in * (L.Ci / 8), &p->mem_acts));
         }
       } else {
         L.ver.resize(p->R);

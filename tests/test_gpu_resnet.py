@@ -205,3 +205,33 @@ def test_resnet50_reduced_resolution_negative_control(gpu_lib, monkeypatch):
     monkeypatch.setenv("TPS_FAULT", "skip_update")
     bad, allv = measure(layers, [0, len(layers)], 2, 32, 1, ost.I_VARIANT, ost.CONVEX, **R50_KW)
     assert len(bad) >= 0.9 * len(allv), (len(bad), len(allv))
+
+
+@pytest.mark.parametrize("vn", ["V", "I-CONVEX"])
+def test_resnet_relu_mask_bitwise_equals_y_path(gpu_lib, vn, monkeypatch):
+    """The BN backward's ReLU mask from the forward's bit mask (1 bit per element, bit = [y > 0]
+    of the stored bf16 y) is the mask the y path computes, so TPS_RELU_MASK=0 (read y) and the
+    default (read the bits) give bitwise-identical losses and weights; both paths also meet the
+    oracle bars (test_resnet_implicit_conv_paths runs the default)."""
+    layers, starts = tiny(widths=(64, 128), H=32, stem_c=64, blocks=(2, 1))
+    bounds = [0, starts[2], len(layers)]
+    dims = [layers[0]["h"] * layers[0]["w"] * layers[0]["cin"], layers[-1]["out"]]
+    out = {}
+    for flag in ("0", "1"):
+        monkeypatch.setenv("TPS_RELU_MASK", flag)
+        stages, losses = run_gpu(dims, bounds, 2, 8, 6, *VARIANTS[vn], 0.05, 0.01, 0.9, kind=synthgen.X_UNIT,
+                                 layers=layers)
+        ws = []
+        for st in stages:
+            for k, l in enumerate(st.layers):
+                if layers[l]["kind"] in ("conv", "bn", "linear"):
+                    w, bb, _, _ = st.get_weights(k)
+                    ws.append(np.asarray(w).copy())
+                    if bb is not None:
+                        ws.append(np.asarray(bb).copy())
+            st.close()
+        out[flag] = (np.asarray(losses).copy(), ws)
+    assert np.array_equal(out["0"][0], out["1"][0])
+    assert len(out["0"][1]) == len(out["1"][1]) and len(out["0"][1]) > 0
+    for a, b in zip(out["0"][1], out["1"][1]):
+        assert np.array_equal(a, b)

@@ -31,7 +31,7 @@ def close_bf16(got, ref, atol=0.0):
     assert (err <= bound).all(), f"max excess {float((err - bound).max()):.3e}"
 
 
-@pytest.mark.parametrize("k,s,p,C", [(7, 2, 3, 3), (3, 2, 1, 16), (1, 2, 0, 16), (3, 1, 1, 8)])
+@pytest.mark.parametrize("k,s,p,C", [(7, 2, 3, 3), (3, 2, 1, 16), (1, 2, 0, 16), (3, 1, 1, 8), (3, 2, 1, 64), (1, 2, 0, 68)])
 def test_im2col_col2im(gpu_lib, k, s, p, C):
     from paper_2509_23241_b200 import tps
     rng = np.random.default_rng(k * 10 + s)

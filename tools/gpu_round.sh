@@ -15,6 +15,8 @@
 #   gemm     tools/gemm_bench.py microbenchmarks at the bench shape (clock / power sampled)
 #   ncu      ncu --set full of one launch each of the fwd / dgrad / blend / fused-update GEMMs
 #   sanitize compute-sanitizer racecheck/synccheck/memcheck on small pipeline runs
+#   resnet   ResNet GPU tests, C4 one-GPU numbers with the BN ReLU bit mask + specialised col2im
+#            on and off (A/B), and the ResNet-50 per-kernel launch list with DRAM bytes
 # Every step runs under its own timeout so one hang cannot eat the box.
 set -u
 TAG=${1:?tag}; shift
@@ -58,6 +60,17 @@ for s in $STEPS; do
           python -m pytest tests/test_gpu_sanitize.py -q -m gpu -p no:cacheprovider > ${O}_san_${tool}.log 2>&1
         echo "exit $?" >> ${O}_san_${tool}.log
       done ;;
+    resnet)
+      timeout 1500 python -m pytest tests/test_gpu_resnet_ops.py tests/test_gpu_resnet.py tests/test_gpu_resnet50_ops.py \
+        -q -m gpu --timeout=900 -p no:cacheprovider > ${O}_resnet_tests.log 2>&1
+      for rep in 1 2; do
+        timeout 600 python tools/bench_configs.py --graph --only C4 --out ${O}_c4_new$rep.json > ${O}_c4_new$rep.log 2>&1
+        TPS_RELU_MASK=0 TPS_COL2IM_GENERIC=1 timeout 600 python tools/bench_configs.py --graph --only C4 \
+          --out ${O}_c4_old$rep.json > ${O}_c4_old$rep.log 2>&1
+      done
+      timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+        --csv --log-file ${O}_r50_launches.csv python tools/profile_resnet.py --mb 1 > ${O}_r50_prof.log 2>&1
+      python tools/ncu_launch_bw.py ${O}_r50_launches.csv --json ${O}_r50_launches_bw.json > ${O}_r50_bw.txt 2>&1 ;;
     *) echo "unknown step $s" ;;
   esac
 done
