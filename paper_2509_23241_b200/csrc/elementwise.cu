@@ -905,6 +905,7 @@ __global__ void avgpool_bwd_vec(const uint4* __restrict__ dY, uint4* __restrict_
 // per-channel parameters (γ, β, and the current segment's statistics / backward coefficients)
 // stay in registers; a warp covers 512 contiguous bytes of a row (or of 32/tx adjacent rows).
 // block = tx channel groups x ty rows (tx = min(C8, 32)), grid = (ceil(C8/tx), row blocks).
+template <bool MASK>   // MASK: also write the ReLU bit mask (compile-time)
 __global__ void __launch_bounds__(256) bn_apply_rows(const uint4* __restrict__ x, const uint4* __restrict__ res,
                                                      uint4* __restrict__ y, const float* __restrict__ gamma,
                                                      const float* __restrict__ beta, const float* __restrict__ mean,
@@ -944,10 +945,11 @@ __global__ void __launch_bounds__(256) bn_apply_rows(const uint4* __restrict__ x
     }
     const uint4 py = pack8(v);
     y[o] = py;
-    if (mask) mask[o] = relu_bits8(py);
+    if (MASK) mask[o] = relu_bits8(py);
   }
 }
 
+template <bool MASK>   // MASK: ReLU mask from the forward's bit mask (compile-time, see bn_partial_vec)
 __global__ void __launch_bounds__(256) bn_bwd_apply_rows(const uint4* __restrict__ dy, const uint4* __restrict__ yv,
                                                          const uint4* __restrict__ xv, const float4* __restrict__ coef,
                                                          const float* __restrict__ invstd, int rows, int C8,
@@ -977,7 +979,7 @@ __global__ void __launch_bounds__(256) bn_bwd_apply_rows(const uint4* __restrict
     float d[8], xx[8], out[8];
     unpack8(dy[o], d);
     unpack8(xv[o], xx);
-    if (relu && mask) {
+    if (MASK) {
       const uint32_t mb = mask[o];
 #pragma unroll
       for (int e = 0; e < 8; ++e)
@@ -1000,14 +1002,16 @@ __global__ void __launch_bounds__(256) bn_bwd_apply_rows(const uint4* __restrict
 }
 
 // per (segment, chunk) partial sums over 8 channels per thread, fp64:
-//   MODE 0 (statistics): Σx, Σx²;  MODE 1 (backward): Σdy', Σdy'·x̂ (dy' = dy ⊙ [y > 0] if relu)
+//   MODE 0 (statistics): Σx, Σx²;  MODE 1 (backward): Σdy', Σdy'·x̂ (dy' = dy ⊙ [y > 0] if relu);
+//   MODE 2: MODE 1 with the ReLU mask from the forward's bit mask (compile-time, so the unrolled
+//   loop keeps its loads in flight: a run-time choice between the two mask sources serialised them)
 // block: tx = min(C8, 32) channel groups x ty = 256 / tx rows; grid (ceil(C8/tx), chunks, segs)
 template <int MODE>
 __global__ void __launch_bounds__(256) bn_partial_vec(const uint4* __restrict__ a, const uint4* __restrict__ yv,
                                                       const uint4* __restrict__ xv, const float* __restrict__ mean,
                                                       const float* __restrict__ invstd, int seg_rows, int C8,
                                                       int chunks, int relu, double* __restrict__ part,
-                                                      const uint8_t* __restrict__ mask = nullptr) {
+                                                      const uint8_t* __restrict__ mask) {
   extern __shared__ double red[];            // [ty][tx][16]
   const int tx = min(C8, 32), ty = blockDim.x / tx;
   const int lx = threadIdx.x % tx, ly = threadIdx.x / tx;
@@ -1022,7 +1026,7 @@ __global__ void __launch_bounds__(256) bn_partial_vec(const uint4* __restrict__ 
   for (int e = 0; e < 8; ++e) s1[e] = s2[e] = 0.0;
   if (cg < C8) {
     float m[8], is[8];
-    if (MODE == 1) {
+    if (MODE != 0) {
       load8f(mean + seg * C + cg * 8, m);
       load8f(invstd + seg * C + cg * 8, is);
     }
@@ -1040,7 +1044,7 @@ __global__ void __launch_bounds__(256) bn_partial_vec(const uint4* __restrict__ 
       } else {
         float yy[8], xx[8];
         unpack8(xv[o], xx);
-        if (relu && mask) {
+        if (MODE == 2) {
           const uint32_t mb = mask[o];
 #pragma unroll
           for (int e = 0; e < 8; ++e) yy[e] = ((mb >> e) & 1u) ? 1.f : 0.f;
@@ -1049,7 +1053,7 @@ __global__ void __launch_bounds__(256) bn_partial_vec(const uint4* __restrict__ 
         }
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          const double d = (relu && !(yy[e] > 0.f)) ? 0.0 : static_cast<double>(v[e]);
+          const double d = ((MODE == 2 || relu) && !(yy[e] > 0.f)) ? 0.0 : static_cast<double>(v[e]);
           s1[e] += d;
           s2[e] += d * ((static_cast<double>(xx[e]) - m[e]) * is[e]);
         }
@@ -1367,6 +1371,54 @@ __global__ void __launch_bounds__(256) im2col_rowtile(const uint16_t* __restrict
   }
 }
 
+// im2col_rowtile with the k input rows staged by 16-byte loads (W·C % 8 == 0: every input row
+// starts 16-byte aligned).  Tile row layout: [lead zeros | W·C data at D0 | trail zeros], D0 =
+// p·C rounded up to 8 elements, so padded pixel wp, channel c sits at D0 − p·C + wp·C + c; rows
+// outside the image are all zeros.  The scalar fill of im2col_rowtile issued its 2-byte loads
+// one after another (integer divisions between them) and dominated that kernel.
+__global__ void __launch_bounds__(256) im2col_rowtile_v(const uint16_t* __restrict__ X, uint4* __restrict__ P, int H,
+                                                        int W, int C, int k, int s, int p, int Ho, int Wo, int ldp,
+                                                        int D0, int rowlen) {
+  extern __shared__ __align__(16) uint16_t smv[];
+  uint16_t* tile = smv;                                    // [k][rowlen], rowlen % 8 == 0
+  int* off = reinterpret_cast<int*>(smv + k * rowlen);     // [ldp]
+  const int n = blockIdx.x / Ho, ho = blockIdx.x - n * Ho;
+  const int h0 = ho * s - p;
+  const int WC8 = W * C / 8, row8 = rowlen / 8, D08 = D0 / 8;
+  uint4* tile4 = reinterpret_cast<uint4*>(tile);
+  const uint4* X4 = reinterpret_cast<const uint4*>(X);
+  for (int i = threadIdx.x; i < k * row8; i += blockDim.x) {
+    const int kh = i / row8, q = i - kh * row8;
+    const int h = h0 + kh, d = q - D08;
+    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+    if (h >= 0 && h < H && d >= 0 && d < WC8) v = __ldg(X4 + (static_cast<int64_t>(n) * H + h) * WC8 + d);
+    tile4[i] = v;
+  }
+  const int kkC = k * k * C, shift = D0 - p * C;
+  for (int col = threadIdx.x; col < ldp; col += blockDim.x) {
+    int o = -1;
+    if (col < kkC) {
+      const int kh = col / (k * C), rem = col - kh * k * C;    // rem = kw·C + c
+      o = kh * rowlen + shift + rem;
+    }
+    off[col] = o;
+  }
+  __syncthreads();
+  const int v8 = ldp / 8;
+  uint4* prow = P + (static_cast<int64_t>(n) * Ho + ho) * Wo * v8;
+  for (int i = threadIdx.x; i < Wo * v8; i += blockDim.x) {
+    const int wo = i / v8, cv = i - wo * v8;
+    const int base = wo * s * C;
+    uint32_t v[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int o = off[cv * 8 + e];
+      v[e] = o >= 0 ? tile[o + base] : 0u;
+    }
+    __stcs(prow + i, make_uint4(v[0] | (v[1] << 16), v[2] | (v[3] << 16), v[4] | (v[5] << 16), v[6] | (v[7] << 16)));
+  }
+}
+
 // explicit patches, one output pixel row per block iteration (32-bit index math per element)
 __global__ void im2col_rows(const uint16_t* __restrict__ X, uint16_t* __restrict__ P, int N, int H, int W, int C,
                             int k, int s, int p, int Ho, int Wo, int ldp, int64_t rows) {
@@ -1549,6 +1601,17 @@ cudaError_t launch_im2col(const uint16_t* X, uint16_t* P, int N, int H, int W, i
   const int Ho = (H + 2 * p - k) / s + 1, Wo = (W + 2 * p - k) / s + 1;
   const int64_t rows = static_cast<int64_t>(N) * Ho * Wo;
   if (rows <= 0) return cudaSuccess;
+  if (ldp % 8 == 0 && (W * C) % 8 == 0) {
+    // right padding: the last window reaches padded pixel (Wo−1)·s + k − 1 < W + 2p
+    const int D0 = (p * C + 7) / 8 * 8;
+    const int rowlen = (D0 + W * C + p * C + 7) / 8 * 8;
+    const size_t smem_v = static_cast<size_t>(k) * rowlen * 2 + static_cast<size_t>(ldp) * 4;
+    if (smem_v <= 48 * 1024) {
+      im2col_rowtile_v<<<static_cast<unsigned>(static_cast<int64_t>(N) * Ho), 256, smem_v, st>>>(
+          X, reinterpret_cast<uint4*>(P), H, W, C, k, s, p, Ho, Wo, ldp, D0, rowlen);
+      return cudaGetLastError();
+    }
+  }
   const size_t smem = static_cast<size_t>((k * (W + 2 * p) * C + 1) & ~1) * 2 + static_cast<size_t>(ldp) * 4;
   if (ldp % 8 == 0 && smem <= 48 * 1024) {
     im2col_rowtile<<<static_cast<unsigned>(static_cast<int64_t>(N) * Ho), 256, smem, st>>>(
@@ -1622,11 +1685,12 @@ cudaError_t launch_bn_forward(const uint16_t* x, const uint16_t* res, uint16_t* 
     dim3 grid((C8 + tx - 1) / tx, chunks, segs);
     bn_partial_vec<0><<<grid, tx * (256 / tx), 256 * 16 * sizeof(double), st>>>(reinterpret_cast<const uint4*>(x), nullptr,
                                                                      nullptr, nullptr, nullptr, seg_rows, C8, chunks,
-                                                                     0, scratch);
+                                                                     0, scratch, nullptr);
     bn_stats_final<<<(segs * C * 32 + 255) / 256, 256, 0, st>>>(scratch, chunks, C, seg_rows, segs, mean, invstd, 1e-5f);
     {
       const int C8r = C8, tx = std::min(C8r, 32);
-      bn_apply_rows<<<bn_rows_grid(static_cast<int>(rows), C8r), tx * (256 / tx), 0, st>>>(
+      auto* apply = relu_mask ? bn_apply_rows<true> : bn_apply_rows<false>;
+      apply<<<bn_rows_grid(static_cast<int>(rows), C8r), tx * (256 / tx), 0, st>>>(
           reinterpret_cast<const uint4*>(x), reinterpret_cast<const uint4*>(res), reinterpret_cast<uint4*>(y), gamma,
           beta, mean, invstd, static_cast<int>(rows), C8r, seg_rows, relu, relu_mask);
     }
@@ -1652,7 +1716,8 @@ cudaError_t launch_bn_forward_colsum(const float* part, const uint16_t* x, const
                                                                         chunks, scratch);
   bn_stats_final<<<(segs * C * 32 + 255) / 256, 256, 0, st>>>(scratch, chunks, C, seg_rows, segs, mean, invstd, 1e-5f);
   const int C8 = C / 8, tx = std::min(C8, 32);
-  bn_apply_rows<<<bn_rows_grid(static_cast<int>(rows), C8), tx * (256 / tx), 0, st>>>(
+  auto* apply = relu_mask ? bn_apply_rows<true> : bn_apply_rows<false>;
+  apply<<<bn_rows_grid(static_cast<int>(rows), C8), tx * (256 / tx), 0, st>>>(
       reinterpret_cast<const uint4*>(x), reinterpret_cast<const uint4*>(res), reinterpret_cast<uint4*>(y), gamma, beta,
       mean, invstd, static_cast<int>(rows), C8, seg_rows, relu, relu_mask);
   return cudaGetLastError();
@@ -1669,7 +1734,8 @@ cudaError_t launch_bn_backward(const uint16_t* dy, const uint16_t* y, const uint
     const int C8 = C / 8, tx = std::min(C8, 32);
     const int64_t rows = static_cast<int64_t>(segs) * seg_rows;
     dim3 grid((C8 + tx - 1) / tx, chunks, segs);
-    bn_partial_vec<1><<<grid, tx * (256 / tx), 256 * 16 * sizeof(double), st>>>(
+    auto* partial = relu_mask ? bn_partial_vec<2> : bn_partial_vec<1>;
+    partial<<<grid, tx * (256 / tx), 256 * 16 * sizeof(double), st>>>(
         reinterpret_cast<const uint4*>(dy), reinterpret_cast<const uint4*>(y), reinterpret_cast<const uint4*>(x), mean,
         invstd, seg_rows, C8, chunks, relu, scratch, relu_mask);
     float4* coef = reinterpret_cast<float4*>(sums);   // segs·C float4 = the sums region
@@ -1678,7 +1744,8 @@ cudaError_t launch_bn_backward(const uint16_t* dy, const uint16_t* y, const uint
                                                       gb, coef, dgamma, dbeta);
     {
       const int C8r = C8, tx = std::min(C8r, 32);
-      bn_bwd_apply_rows<<<bn_rows_grid(static_cast<int>(rows), C8r), tx * (256 / tx), 0, st>>>(
+      auto* apply = relu_mask ? bn_bwd_apply_rows<true> : bn_bwd_apply_rows<false>;
+      apply<<<bn_rows_grid(static_cast<int>(rows), C8r), tx * (256 / tx), 0, st>>>(
           reinterpret_cast<const uint4*>(dy), reinterpret_cast<const uint4*>(y), reinterpret_cast<const uint4*>(x),
           coef, invstd, static_cast<int>(rows), C8r, seg_rows, relu, reinterpret_cast<uint4*>(dx),
           reinterpret_cast<uint4*>(dres), relu_mask);

@@ -58,6 +58,24 @@ def test_im2col_col2im(gpu_lib, k, s, p, C):
     close_bf16(host(dX2), ref + A, 1e-6)
 
 
+@pytest.mark.parametrize("N,H,W,C", [(2, 20, 16, 3), (3, 13, 24, 3), (1, 9, 8, 8)])
+def test_im2col_stem_vector_fill(gpu_lib, N, H, W, C):
+    """The 7x7/2/3 stem patches with W·C % 8 == 0 (16-byte-staged input rows, as at 224 x 224 x 3):
+    bit-exact against the oracle's im2col, zero pad columns."""
+    from paper_2509_23241_b200 import tps
+    k, s, p = 7, 2, 3
+    rng = np.random.default_rng(N * 100 + W)
+    X, Xd = bf(rng.standard_normal((N, H, W, C)))
+    cols, Ho, Wo = resnet.im2col(X, k, s, p)
+    ldp = -(-k * k * C // 16) * 16
+    P = torch.full((N * Ho * Wo, ldp), 7.0, dtype=torch.bfloat16, device="cuda")
+    tps.im2col(Xd, P, N, H, W, C, k, s, p, ldp)
+    torch.cuda.synchronize()
+    got = host(P)
+    assert np.array_equal(got[:, :k * k * C], cols)
+    assert not got[:, k * k * C:].any()
+
+
 def test_maxpool3_and_avgpool(gpu_lib):
     from paper_2509_23241_b200 import tps
     rng = np.random.default_rng(3)

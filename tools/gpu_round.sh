@@ -17,6 +17,7 @@
 #   sanitize compute-sanitizer racecheck/synccheck/memcheck on small pipeline runs
 #   resnet   ResNet GPU tests, C4 one-GPU numbers with the BN ReLU bit mask + specialised col2im
 #            on and off (A/B), and the ResNet-50 per-kernel launch list with DRAM bytes
+#   vgg      VGG-16 (C3, S = 1) per-kernel launch list with DRAM bytes (mid-run window)
 # Every step runs under its own timeout so one hang cannot eat the box.
 set -u
 TAG=${1:?tag}; shift
@@ -71,6 +72,11 @@ for s in $STEPS; do
       timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
         --csv --log-file ${O}_r50_launches.csv python tools/profile_resnet.py --mb 1 > ${O}_r50_prof.log 2>&1
       python tools/ncu_launch_bw.py ${O}_r50_launches.csv --json ${O}_r50_launches_bw.json > ${O}_r50_bw.txt 2>&1 ;;
+    vgg)
+      timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+        -s 1500 -c 450 --csv --log-file ${O}_vgg_launches.csv python tools/bench_configs.py --only "C3 VGG-16 CIFAR S=1" \
+        > ${O}_vgg_prof.log 2>&1
+      python tools/ncu_launch_bw.py ${O}_vgg_launches.csv --json ${O}_vgg_launches_bw.json > ${O}_vgg_bw.txt 2>&1 ;;
     *) echo "unknown step $s" ;;
   esac
 done
