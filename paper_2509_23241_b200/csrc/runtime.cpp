@@ -126,6 +126,12 @@ struct Layer {
   // graph networks: this conv's epilogue also writes the column sums (Σx, Σx²) that the batch norm
   // right after it needs, so the BN skips its statistics pass over the conv output
   bool stats_to_next = false;
+  // fuse_update run: this layer's SGD step rides in its weight-gradient epilogue.  False for the
+  // layers whose weight-gradient output tiles cannot fill the GPU (small M x N, long K: the
+  // convolutions of VGG's early blocks, the patch layer): those take the split-K weight gradient
+  // and the separate update kernel on the same stream (one fused CTA per 64-column tile ran
+  // ~0.7 ms at 32 x 32 x 64 channels, B = 128)
+  bool fuse = false;
   bool has_w() const {
     return kind == TPS_LAYER_LINEAR || kind == TPS_LAYER_CONV3X3 || kind == TPS_LAYER_CONV || kind == TPS_LAYER_BN;
   }
@@ -1274,7 +1280,7 @@ tps_status do_backward(tps_pipeline* p, int64_t j, int staleness) {
       tps::GemmArgs ga{};
       ga.M = Lk.Np; ga.N = Lk.Kp; ga.K = rows; ga.out = Lk.dW; ga.ldo = Lk.Kp; ga.out_f32 = 1;
       ga.alpha = 1.f; ga.xa = 1.f;
-      if (p->fuse_update) {
+      if (p->fuse_update && Lk.fuse) {
         ga.epi = tps::EPI_SGD;
         ga.w = Lk.W; ga.v = Lk.mW; ga.ver = Lk.ver[vn % p->R];
         ga.lr = p->lr; ga.mu = p->mu; ga.wd = p->wd;
@@ -1291,7 +1297,7 @@ tps_status do_backward(tps_pipeline* p, int64_t j, int staleness) {
         ga.max_ctas = p->nsm - p->part_dgrad;
       TPS_TRY(flush_pending());   // (a held-back update of layer k+1 whose dgrad partner did not come)
       const bool defer = p->dual && p->dp == 1 && Lk.kind == TPS_LAYER_LINEAR && ga.max_ctas == 0 &&
-                         dgrad_pairable(k - 1);
+                         Lk.fuse && dgrad_pairable(k - 1);
       if (p->split_w && !defer) {   // after this layer's dgrad (it reads the weights the fused update rewrites)
         CUDA_OK(cudaEventRecord(p->ev_dg[k], p->cs));
         CUDA_OK(cudaStreamWaitEvent(p->s_w, p->ev_dg[k], 0));
@@ -1309,6 +1315,12 @@ tps_status do_backward(tps_pipeline* p, int64_t j, int staleness) {
       } else {
         tps::GemmOperands op{G, Lk.Np, X, Lk.Kp, nullptr};
         TPS_TRY(run_gemm(p, tps::GEMM_WGRAD, op, ga, 2, ws));
+      }
+      if (p->fuse_update && !Lk.fuse) {   // split-K weight gradient above, its update right behind it
+        const int64_t n = static_cast<int64_t>(Lk.Np) * Lk.Kp;
+        CUDA_OK(tps::launch_sgd_update(Lk.W, Lk.mW, Lk.dW, Lk.ver[vn % p->R], n, p->lr, p->mu, p->wd, ws,
+                                       p->upd_blocks_per_sm, p->tf ? 1 : 0));
+        p->launches += 1;
       }
       if (p->split_w && !defer) CUDA_OK(cudaEventRecord(p->ev_w_done[k], p->s_w));
       if (!bias_side) {   // bias gradient and the bias's SGD/momentum step in one launch
@@ -2041,15 +2053,27 @@ tps_status tps_pipeline_init(const tps_config* c, tps_pipeline** out) {
   }
   {
     // split-K workspace for the weight-gradient GEMMs whose output tiles cannot fill the GPU
+    // (TPS_FUSE_ALL=1: fuse the update into every weight gradient, as before)
+    const char* fa = std::getenv("TPS_FUSE_ALL");
+    const bool fuse_all = fa && fa[0] == '1';
     int64_t wsf = 0;
-    for (const Layer& L : p->layers) {
+    bool any_unfused = false;
+    for (Layer& L : p->layers) {
       if (!L.has_w() || L.kind == TPS_LAYER_BN) continue;
       const bool implicit = (L.kind == TPS_LAYER_CONV3X3 && !L.im2col) ||
                             (L.kind == TPS_LAYER_CONV && (L.conv_mode == 1 || L.conv_mode == 3));
       const int K = p->B * (L.kind == TPS_LAYER_LINEAR ? 1 : L.hw_out);
-      wsf = std::max(wsf, tps::gemm_splitk_floats(implicit ? tps::GEMM_CONV_WGRAD : tps::GEMM_WGRAD, L.Np, L.Kp, K, L.Kp));
+      const int64_t f =
+          tps::gemm_splitk_floats(implicit ? tps::GEMM_CONV_WGRAD : tps::GEMM_WGRAD, L.Np, L.Kp, K, L.Kp);
+      wsf = std::max(wsf, f);
+      L.fuse = p->fuse_update && !p->graph && (f == 0 || p->tf || fuse_all);
+      if (p->fuse_update && !p->graph && !L.fuse) {
+        any_unfused = true;
+        const tps_status dw_st = alloc_t(p, &L.dW, static_cast<size_t>(L.Np) * L.Kp, &p->mem_optim);
+        if (dw_st != TPS_OK) return cleanup(dw_st);
+      }
     }
-    if (!p->fuse_update || p->graph) {
+    if (!p->fuse_update || p->graph || any_unfused) {
       const tps_status ws_st = alloc_t(p, &p->splitk_ws, wsf, &p->mem_optim);
       if (ws_st != TPS_OK) return cleanup(ws_st);
       p->splitk_floats = wsf;

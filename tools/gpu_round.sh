@@ -18,6 +18,8 @@
 #   resnet   ResNet GPU tests, C4 one-GPU numbers with the BN ReLU bit mask + specialised col2im
 #            on and off (A/B), and the ResNet-50 per-kernel launch list with DRAM bytes
 #   vgg      VGG-16 (C3, S = 1) per-kernel launch list with DRAM bytes (mid-run window)
+#   vggab    conv / VGG parity tests, C3 one-GPU numbers with the tile-starved weight gradients
+#            unfused (default) and fused (TPS_FUSE_ALL=1)
 # Every step runs under its own timeout so one hang cannot eat the box.
 set -u
 TAG=${1:?tag}; shift
@@ -77,6 +79,15 @@ for s in $STEPS; do
         -s 1500 -c 450 --csv --log-file ${O}_vgg_launches.csv python tools/bench_configs.py --only "C3 VGG-16 CIFAR S=1" \
         > ${O}_vgg_prof.log 2>&1
       python tools/ncu_launch_bw.py ${O}_vgg_launches.csv --json ${O}_vgg_launches_bw.json > ${O}_vgg_bw.txt 2>&1 ;;
+    vggab)
+      timeout 1200 python -m pytest tests/test_gpu_conv.py tests/test_gpu_resnet_ops.py \
+        "tests/test_gpu_fullsize.py::test_c3_vgg16_four_stage" -q -m gpu --timeout=900 -p no:cacheprovider \
+        > ${O}_vgg_tests.log 2>&1
+      for rep in 1 2; do
+        timeout 600 python tools/bench_configs.py --graph --only C3 --out ${O}_c3_new$rep.json > ${O}_c3_new$rep.log 2>&1
+        TPS_FUSE_ALL=1 timeout 600 python tools/bench_configs.py --graph --only C3 --out ${O}_c3_old$rep.json \
+          > ${O}_c3_old$rep.log 2>&1
+      done ;;
     *) echo "unknown step $s" ;;
   esac
 done
