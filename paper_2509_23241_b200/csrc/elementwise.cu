@@ -143,20 +143,29 @@ __global__ void __launch_bounds__(256) sgd_update_dp_kernel(float* __restrict__ 
 }
 
 // ------------------------------------------------------------------ bias gradient
-constexpr int BG_COLS = 256;   // columns per block (32 threads x 8 columns)
-constexpr int BG_ROWS = 8;     // row lanes per block
+constexpr int BG_COLS = 256;   // columns per block at most (32 threads x 8 columns)
+constexpr int BG_ROWS = 8;     // row lanes per block at the full width
+// column threads per block (8 columns each): 32, or the largest power of two <= cols/8 for narrow
+// gradients, the other threads becoming row lanes (block = tx x 256/tx).  A 64-column conv bias
+// on 32 x 32 images with full-width blocks left 3/4 of the threads idle.
+inline int bg_tx(int cols) {
+  int tx = 32;
+  while (tx > 1 && tx * 8 > cols) tx >>= 1;
+  return tx;
+}
 constexpr int BG_CNT = 64;     // arrival counters at the head of the scratch (cols <= 64·BG_COLS)
 
 template <bool TF>
 __global__ void __launch_bounds__(256) bias_grad_partial(const uint16_t* __restrict__ G, int rows, int cols, int ldg,
                                                          int rows_per_split, float* __restrict__ part) {
-  __shared__ float red[BG_ROWS][BG_COLS + 4];
-  const int c0 = blockIdx.x * BG_COLS + threadIdx.x * 8;
+  __shared__ float red[BG_ROWS * (BG_COLS + 4) + 1024];   // [ty][cbw + 4], ty = 256 / tx
+  const int cbw = blockDim.x * 8, ty = blockDim.y, rs = cbw + 4;
+  const int c0 = blockIdx.x * cbw + threadIdx.x * 8;
   const int r_begin = blockIdx.y * rows_per_split;
   const int r_end = min(rows, r_begin + rows_per_split);
   float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   if (c0 < cols) {
-    for (int r = r_begin + threadIdx.y; r < r_end; r += BG_ROWS) {
+    for (int r = r_begin + threadIdx.y; r < r_end; r += ty) {
       if (TF) {   // fp32 (tf32) gradient: two 16-byte loads per 8 columns
         const float4* q =
             reinterpret_cast<const float4*>(reinterpret_cast<const float*>(G) + static_cast<size_t>(r) * ldg + c0);
@@ -173,14 +182,14 @@ __global__ void __launch_bounds__(256) bias_grad_partial(const uint16_t* __restr
     }
   }
 #pragma unroll
-  for (int e = 0; e < 8; ++e) red[threadIdx.y][threadIdx.x * 8 + e] = acc[e];
+  for (int e = 0; e < 8; ++e) red[threadIdx.y * rs + threadIdx.x * 8 + e] = acc[e];
   __syncthreads();
   // fixed-order sum over the row lanes
-  const int t = threadIdx.y * 32 + threadIdx.x;   // 0..255 -> one column each
-  const int c = blockIdx.x * BG_COLS + t;
+  const int t = threadIdx.y * blockDim.x + threadIdx.x;   // 0..cbw-1 -> one column each
+  const int c = blockIdx.x * cbw + t;
+  if (t >= cbw) return;
   float s = 0.f;
-#pragma unroll
-  for (int y = 0; y < BG_ROWS; ++y) s += red[y][t];
+  for (int y = 0; y < ty; ++y) s += red[y * rs + t];
   if (c < cols) part[static_cast<size_t>(blockIdx.y) * cols + c] = s;
 }
 
@@ -194,15 +203,16 @@ __global__ void __launch_bounds__(256) bias_grad_fused(const uint16_t* __restric
                                                        unsigned int* __restrict__ cnt, float* __restrict__ db,
                                                        float* __restrict__ b, float* __restrict__ vb, float lr,
                                                        float mu, float wd) {
-  __shared__ float red[BG_ROWS][BG_COLS + 4];
+  __shared__ float red[BG_ROWS * (BG_COLS + 4) + 1024];   // [ty][cbw + 4], ty = 256 / tx
   __shared__ bool last;
-  const int c0 = blockIdx.x * BG_COLS + threadIdx.x * 8;
+  const int cbw = blockDim.x * 8, ty = blockDim.y, rs = cbw + 4;
+  const int c0 = blockIdx.x * cbw + threadIdx.x * 8;
   const int r_begin = blockIdx.y * rows_per_split;
   const int r_end = min(rows, r_begin + rows_per_split);
   float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   if (c0 < cols) {
 #pragma unroll 8
-    for (int r = r_begin + threadIdx.y; r < r_end; r += BG_ROWS) {   // unrolled: loads in flight, same add order
+    for (int r = r_begin + threadIdx.y; r < r_end; r += ty) {   // unrolled: loads in flight, same add order
       if (TF) {   // fp32 (tf32) gradient: two 16-byte loads per 8 columns
         const float4* q =
             reinterpret_cast<const float4*>(reinterpret_cast<const float*>(G) + static_cast<size_t>(r) * ldg + c0);
@@ -219,14 +229,15 @@ __global__ void __launch_bounds__(256) bias_grad_fused(const uint16_t* __restric
     }
   }
 #pragma unroll
-  for (int e = 0; e < 8; ++e) red[threadIdx.y][threadIdx.x * 8 + e] = acc[e];
+  for (int e = 0; e < 8; ++e) red[threadIdx.y * rs + threadIdx.x * 8 + e] = acc[e];
   __syncthreads();
-  const int t = threadIdx.y * 32 + threadIdx.x;   // 0..255 -> one column each
-  const int c = blockIdx.x * BG_COLS + t;
-  float s = 0.f;
-#pragma unroll
-  for (int y = 0; y < BG_ROWS; ++y) s += red[y][t];
-  if (c < cols) part[static_cast<size_t>(blockIdx.y) * cols + c] = s;
+  const int t = threadIdx.y * blockDim.x + threadIdx.x;   // 0..cbw-1 -> one column each
+  const int c = blockIdx.x * cbw + t;
+  if (t < cbw) {
+    float s = 0.f;
+    for (int y = 0; y < ty; ++y) s += red[y * rs + t];
+    if (c < cols) part[static_cast<size_t>(blockIdx.y) * cols + c] = s;
+  }
   __threadfence();
   __syncthreads();
   if (t == 0) last = atomicAdd(&cnt[blockIdx.x], 1u) == gridDim.y - 1;
@@ -234,7 +245,7 @@ __global__ void __launch_bounds__(256) bias_grad_fused(const uint16_t* __restric
   if (!last) return;
   __threadfence();
   if (t == 0) cnt[blockIdx.x] = 0u;               // ready for the next launch (stream-ordered)
-  if (c >= cols) return;
+  if (t >= cbw || c >= cols) return;
   float d = 0.f;
 #pragma unroll 8
   for (int k = 0; k < static_cast<int>(gridDim.y); ++k) d += __ldcg(part + static_cast<size_t>(k) * cols + c);
@@ -302,7 +313,8 @@ int bias_grad_splits(int rows, int cols) {
   static const int waves = std::getenv("TPS_BG_WAVES") ? std::max(1, std::atoi(std::getenv("TPS_BG_WAVES"))) : 2;
   static const int min_rows =
       std::getenv("TPS_BG_MIN_ROWS") ? std::max(8, std::atoi(std::getenv("TPS_BG_MIN_ROWS"))) : 64;
-  const int col_blocks = (cols + BG_COLS - 1) / BG_COLS;
+  const int cbw = bg_tx(cols) * 8;
+  const int col_blocks = (cols + cbw - 1) / cbw;
   int splits = (waves * sm_count() + col_blocks - 1) / col_blocks;
   const int max_splits = (rows + min_rows - 1) / min_rows;
   if (splits > max_splits) splits = max_splits;
@@ -1067,15 +1079,29 @@ __global__ void __launch_bounds__(256) bn_partial_vec(const uint4* __restrict__ 
     mine[8 + e] = s2[e];
   }
   __syncthreads();
-  if (ly == 0 && cg < C8) {
-    for (int yy = 1; yy < ty; ++yy) {
-      const double* o = red + (static_cast<size_t>(yy) * tx + lx) * 16;
+  // fixed pairwise tree over the ty row lanes: every level folds the upper half onto the lower,
+  // so narrow layers (tx = 8, ty = 32) no longer have 8 threads walk 31 rows serially
+  for (int n = ty; n > 1;) {
+    const int half = (n + 1) >> 1;
+    if (ly < n - half) {
+      const double* o = red + (static_cast<size_t>(ly + half) * tx + lx) * 16;
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
         s1[e] += o[e];
         s2[e] += o[8 + e];
       }
+      if (half > 1) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          mine[e] = s1[e];
+          mine[8 + e] = s2[e];
+        }
+      }
     }
+    n = half;
+    __syncthreads();
+  }
+  if (ly == 0 && cg < C8) {
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
       const size_t o = (static_cast<size_t>(seg) * chunks + blockIdx.y) * C + cg * 8 + e;
@@ -1502,15 +1528,14 @@ cudaError_t launch_bias_grad_sgd(const uint16_t* G, int rows, int cols, int ldg,
   if (cols % 8 || ldg % 8) return cudaErrorInvalidValue;
   const int splits = bias_grad_splits(rows, cols);
   const int rps = (rows + splits - 1) / splits;
-  dim3 grid((cols + BG_COLS - 1) / BG_COLS, splits);
+  const int tx = bg_tx(cols);
+  dim3 grid((cols + tx * 8 - 1) / (tx * 8), splits), block(tx, 256 / tx);
   if (static_cast<int>(grid.x) > BG_CNT) return cudaErrorInvalidValue;
   unsigned int* cnt = reinterpret_cast<unsigned int*>(scratch);
   if (tf)
-    bias_grad_fused<true><<<grid, dim3(32, BG_ROWS), 0, st>>>(G, rows, cols, ldg, rps, scratch + BG_CNT, cnt, db, b, vb,
-                                                              lr, mu, wd);
+    bias_grad_fused<true><<<grid, block, 0, st>>>(G, rows, cols, ldg, rps, scratch + BG_CNT, cnt, db, b, vb, lr, mu, wd);
   else
-    bias_grad_fused<false><<<grid, dim3(32, BG_ROWS), 0, st>>>(G, rows, cols, ldg, rps, scratch + BG_CNT, cnt, db, b,
-                                                               vb, lr, mu, wd);
+    bias_grad_fused<false><<<grid, block, 0, st>>>(G, rows, cols, ldg, rps, scratch + BG_CNT, cnt, db, b, vb, lr, mu, wd);
   return cudaGetLastError();
 }
 
@@ -1520,9 +1545,10 @@ cudaError_t launch_bias_grad(const uint16_t* G, int rows, int cols, int ldg, flo
   if (cols % 8 || ldg % 8) return cudaErrorInvalidValue;
   const int splits = bias_grad_splits(rows, cols);
   const int rps = (rows + splits - 1) / splits;
-  dim3 grid((cols + BG_COLS - 1) / BG_COLS, splits);
-  if (tf) bias_grad_partial<true><<<grid, dim3(32, BG_ROWS), 0, st>>>(G, rows, cols, ldg, rps, scratch + BG_CNT);
-  else bias_grad_partial<false><<<grid, dim3(32, BG_ROWS), 0, st>>>(G, rows, cols, ldg, rps, scratch + BG_CNT);
+  const int tx = bg_tx(cols);
+  dim3 grid((cols + tx * 8 - 1) / (tx * 8), splits), block(tx, 256 / tx);
+  if (tf) bias_grad_partial<true><<<grid, block, 0, st>>>(G, rows, cols, ldg, rps, scratch + BG_CNT);
+  else bias_grad_partial<false><<<grid, block, 0, st>>>(G, rows, cols, ldg, rps, scratch + BG_CNT);
   bias_grad_final<<<(cols + 255) / 256, 256, 0, st>>>(scratch + BG_CNT, splits, cols, db);
   return cudaGetLastError();
 }
