@@ -1079,29 +1079,15 @@ __global__ void __launch_bounds__(256) bn_partial_vec(const uint4* __restrict__ 
     mine[8 + e] = s2[e];
   }
   __syncthreads();
-  // fixed pairwise tree over the ty row lanes: every level folds the upper half onto the lower,
-  // so narrow layers (tx = 8, ty = 32) no longer have 8 threads walk 31 rows serially
-  for (int n = ty; n > 1;) {
-    const int half = (n + 1) >> 1;
-    if (ly < n - half) {
-      const double* o = red + (static_cast<size_t>(ly + half) * tx + lx) * 16;
+  if (ly == 0 && cg < C8) {
+    for (int yy = 1; yy < ty; ++yy) {
+      const double* o = red + (static_cast<size_t>(yy) * tx + lx) * 16;
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
         s1[e] += o[e];
         s2[e] += o[8 + e];
       }
-      if (half > 1) {
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          mine[e] = s1[e];
-          mine[8 + e] = s2[e];
-        }
-      }
     }
-    n = half;
-    __syncthreads();
-  }
-  if (ly == 0 && cg < C8) {
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
       const size_t o = (static_cast<size_t>(seg) * chunks + blockIdx.y) * C + cg * 8 + e;
@@ -1404,7 +1390,7 @@ __global__ void __launch_bounds__(256) im2col_rowtile(const uint16_t* __restrict
 // one after another (integer divisions between them) and dominated that kernel.
 __global__ void __launch_bounds__(256) im2col_rowtile_v(const uint16_t* __restrict__ X, uint4* __restrict__ P, int H,
                                                         int W, int C, int k, int s, int p, int Ho, int Wo, int ldp,
-                                                        int D0, int rowlen) {
+                                                        int D0, int rowlen, int staged) {
   extern __shared__ __align__(16) uint16_t smv[];
   uint16_t* tile = smv;                                    // [k][rowlen], rowlen % 8 == 0
   int* off = reinterpret_cast<int*>(smv + k * rowlen);     // [ldp]
@@ -1432,6 +1418,22 @@ __global__ void __launch_bounds__(256) im2col_rowtile_v(const uint16_t* __restri
   __syncthreads();
   const int v8 = ldp / 8;
   uint4* prow = P + (static_cast<int64_t>(n) * Ho + ho) * Wo * v8;
+  if (staged) {
+    // the block's patch rows assembled element by element in shared memory (consecutive threads
+    // read consecutive tile elements and write consecutive outputs: no bank conflicts), then
+    // streamed out as 16-byte stores.  Gathering 8 elements per thread at a 16-byte stride
+    // between neighbouring threads was a 4-way bank conflict and bounded the kernel.
+    uint16_t* outs = reinterpret_cast<uint16_t*>(off + ldp);   // [Wo][ldp]
+    for (int i = threadIdx.x; i < Wo * ldp; i += blockDim.x) {
+      const int wo = i / ldp, col = i - wo * ldp;
+      const int o = off[col];
+      outs[i] = o >= 0 ? tile[o + wo * s * C] : static_cast<uint16_t>(0);
+    }
+    __syncthreads();
+    const uint4* outs4 = reinterpret_cast<const uint4*>(outs);
+    for (int i = threadIdx.x; i < Wo * v8; i += blockDim.x) __stcs(prow + i, outs4[i]);
+    return;
+  }
   for (int i = threadIdx.x; i < Wo * v8; i += blockDim.x) {
     const int wo = i / v8, cv = i - wo * v8;
     const int base = wo * s * C;
@@ -1632,9 +1634,11 @@ cudaError_t launch_im2col(const uint16_t* X, uint16_t* P, int N, int H, int W, i
     const int D0 = (p * C + 7) / 8 * 8;
     const int rowlen = (D0 + W * C + p * C + 7) / 8 * 8;
     const size_t smem_v = static_cast<size_t>(k) * rowlen * 2 + static_cast<size_t>(ldp) * 4;
+    const size_t smem_s = smem_v + static_cast<size_t>(Wo) * ldp * 2;   // + the staged patch rows
     if (smem_v <= 48 * 1024) {
-      im2col_rowtile_v<<<static_cast<unsigned>(static_cast<int64_t>(N) * Ho), 256, smem_v, st>>>(
-          X, reinterpret_cast<uint4*>(P), H, W, C, k, s, p, Ho, Wo, ldp, D0, rowlen);
+      const int staged = smem_s <= 48 * 1024 ? 1 : 0;
+      im2col_rowtile_v<<<static_cast<unsigned>(static_cast<int64_t>(N) * Ho), 256, staged ? smem_s : smem_v, st>>>(
+          X, reinterpret_cast<uint4*>(P), H, W, C, k, s, p, Ho, Wo, ldp, D0, rowlen, staged);
       return cudaGetLastError();
     }
   }
