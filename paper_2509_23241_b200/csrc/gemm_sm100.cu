@@ -1397,6 +1397,61 @@ __global__ void splitk_reduce(const float4* __restrict__ ws, float4* __restrict_
   }
 }
 
+// split-K forward / input gradient: out = epilogue(Σ_ks ws[ks]) — the partials summed in split
+// order (deterministic), then the plain epilogue's steps in its order: α scale, + bias, ReLU,
+// ReLU mask (bf16 source, positive = sign clear and nonzero), + bf16 addend, bf16 RNE store.
+// One thread per 8 columns of a row (N % 8 == 0).
+__global__ void splitk_finish(const float* __restrict__ ws, int splits, int M, int N, GemmArgs a) {
+  const int n8 = N / 8;
+  const int64_t total = static_cast<int64_t>(M) * n8;
+  const int64_t slice = static_cast<int64_t>(M) * N;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int row = static_cast<int>(i / n8), col = static_cast<int>(i - static_cast<int64_t>(row) * n8) * 8;
+    const float4* p = reinterpret_cast<const float4*>(ws + static_cast<int64_t>(row) * N + col);
+    float4 a0 = __ldcs(p), a1 = __ldcs(p + 1);
+    for (int k = 1; k < splits; ++k) {
+      const float4 b0 = __ldcs(p + k * slice / 4), b1 = __ldcs(p + k * slice / 4 + 1);
+      a0.x += b0.x; a0.y += b0.y; a0.z += b0.z; a0.w += b0.w;
+      a1.x += b1.x; a1.y += b1.y; a1.z += b1.z; a1.w += b1.w;
+    }
+    float v[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+    if (a.alpha != 1.0f) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) v[e] = __fmul_rn(v[e], a.alpha);
+    }
+    if (a.bias) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) v[e] = __fadd_rn(v[e], __ldg(a.bias + col + e));
+    }
+    if (a.relu) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) v[e] = fmaxf(v[e], 0.0f);
+    }
+    if (a.mask) {
+      const uint4 mv = __ldg(reinterpret_cast<const uint4*>(a.mask + static_cast<size_t>(row) * a.ldm + col));
+      const uint32_t w[4] = {mv.x, mv.y, mv.z, mv.w};
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const uint32_t h = (w[e >> 1] >> ((e & 1) * 16)) & 0xFFFFu;
+        if (!(((h & 0x8000u) == 0u) && ((h & 0x7FFFu) != 0u))) v[e] = 0.0f;
+      }
+    }
+    if (a.addend) {
+      const uint4 av = *reinterpret_cast<const uint4*>(a.addend + static_cast<size_t>(row) * a.ldo + col);
+      const uint32_t w[4] = {av.x, av.y, av.z, av.w};
+#pragma unroll
+      for (int e = 0; e < 8; ++e) v[e] = __fadd_rn(v[e], __uint_as_float(((w[e >> 1] >> ((e & 1) * 16)) & 0xFFFFu) << 16));
+    }
+    uint4 o;
+    o.x = pack_bf16(v[0], v[1]);
+    o.y = pack_bf16(v[2], v[3]);
+    o.z = pack_bf16(v[4], v[5]);
+    o.w = pack_bf16(v[6], v[7]);
+    *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(a.out) + static_cast<size_t>(row) * a.ldo + col) = o;
+  }
+}
+
 }  // namespace
 
 bool conv_implicit_ok(int H, int W) {
@@ -1468,7 +1523,34 @@ struct Tiling {
 // Pick the CTA-pair mode and tile width.  Pairs (256 x BN tiles, cta_group::2) cut operand
 // traffic per SM by a third; they are used when M fills at least two 128-row blocks and the
 // pair grid still covers the chip.  Env TPS_GEMM_CG=1 forces single-CTA tiles.
+Tiling pick_tiling_base(int M, int N, int K, int mode, bool sgd, int max_ctas);
+
+// Forward / input-gradient GEMMs whose single-CTA tiles cannot fill a third of the GPU while
+// their K is long (VGG-16 on 32x32 inputs: the 2x2 convolutions and the 4096-wide heads at
+// 64-sample micro-batches; 32 CTAs for ~29 us) split K like the weight gradients; the caller
+// (gemm_run) reduces the partials and applies the epilogue in splitk_finish.  TPS_NO_SPLITK_FD=1
+// disables it.
 Tiling pick_tiling(int M, int N, int K, int mode, bool sgd, int max_ctas = 0) {
+  Tiling tl = pick_tiling_base(M, N, K, mode, sgd, max_ctas);
+  static int no_fd = -1;
+  if (no_fd < 0) {
+    const char* e = std::getenv("TPS_NO_SPLITK_FD");
+    no_fd = (e && e[0] == '1') ? 1 : 0;
+  }
+  const bool fd = mode == GEMM_FWD || mode == GEMM_DGRAD || mode == GEMM_CONV_FWD || mode == GEMM_CONV_DGRAD;
+  if (!fd || no_fd || tl.cg != 1 || tl.splits > 1 || (N & 7)) return tl;
+  const int sms = max_ctas > 0 ? std::min(max_ctas, num_sms()) : num_sms();
+  const int tiles = ((M + BM - 1) / BM) * ((N + tl.bn - 1) / tl.bn);
+  const int num_k = (K + BK - 1) / BK;
+  if (tiles * 3 > sms || num_k < 32) return tl;
+  int splits = std::min({sms / tiles, num_k / 16, 8});
+  if (splits < 2) return tl;
+  const int kper = (num_k + splits - 1) / splits;
+  splits = (num_k + kper - 1) / kper;
+  return {1, tl.bn, splits, kper};
+}
+
+Tiling pick_tiling_base(int M, int N, int K, int mode, bool sgd, int max_ctas) {
   if (mode == GEMM_DGRAD_BLEND || mode == GEMM_CONV_DGRAD_BLEND) {
     // three operand tiles per stage: CTA pairs (256 x 256 tiles) halve the L2 -> SM operand
     // bytes per FLOP, which is what bounds the blended dgrad
@@ -1611,10 +1693,24 @@ cudaError_t gemm_run(int mode, const GemmOperands& op, const GemmArgs& args_in, 
   }
   Tiling tl = pick_tiling(args.M, args.N, args.K, mode, sgd, args.max_ctas);
   if (args.tf32) tl.splits = 1;                      // tf32: one pass over K
-  if (tl.splits > 1 &&
-      (!args.ws || args.ws_floats < static_cast<int64_t>(tl.splits) * args.M * args.ldo || !args.out_f32 ||
-       args.ldo != args.N))
+  const bool fd = mode == GEMM_FWD || mode == GEMM_DGRAD || mode == GEMM_CONV_FWD || mode == GEMM_CONV_DGRAD;
+  GemmArgs fin{};                                    // split forward / input gradient: the epilogue
+  bool fd_split = false;
+  if (tl.splits > 1 && fd) {
+    if (!args.ws || args.ws_floats < static_cast<int64_t>(tl.splits) * args.M * args.N || args.colsum ||
+        args.out_f32 || (args.ldo & 7) || (args.mask && (args.ldm & 7))) {
+      tl.splits = 1;
+    } else {
+      fd_split = true;
+      fin = args;
+      args.out_f32 = 1; args.ldo = args.N; args.bias = nullptr; args.relu = 0; args.mask = nullptr;
+      args.addend = nullptr; args.alpha = 1.0f;
+    }
+  } else if (tl.splits > 1 &&
+             (!args.ws || args.ws_floats < static_cast<int64_t>(tl.splits) * args.M * args.ldo || !args.out_f32 ||
+              args.ldo != args.N)) {
     tl.splits = 1;                                   // no workspace supplied: one pass over K
+  }
   args.splits = tl.splits;
   const int bke = args.tf32 ? 32 : BK;             // K elements per pipeline stage
   args.kper = tl.splits > 1 ? tl.kper : (args.K + bke - 1) / bke;
@@ -1738,6 +1834,12 @@ cudaError_t gemm_run(int mode, const GemmOperands& op, const GemmArgs& args_in, 
       break;
   }
   if (e != cudaSuccess || tl.splits <= 1) return e;
+  if (fd_split) {
+    const int64_t n8 = static_cast<int64_t>(args.M) * args.N / 8;
+    const int blocks = static_cast<int>(std::min<int64_t>((n8 + 255) / 256, static_cast<int64_t>(num_sms()) * 8));
+    splitk_finish<<<blocks, 256, 0, st>>>(args.ws, tl.splits, args.M, args.N, fin);
+    return cudaGetLastError();
+  }
   // ordered reduction of the split-K partials: out = Σ_ks ws[ks] (deterministic)
   const int64_t n4 = static_cast<int64_t>(args.M) * args.ldo / 4;
   const int blocks = static_cast<int>(std::min<int64_t>((n4 + 255) / 256, static_cast<int64_t>(num_sms()) * 8));
@@ -1801,7 +1903,7 @@ cudaError_t gemm_bwd_dual(const GemmOperands& opw, const GemmArgs& aw_in, const 
 int64_t gemm_splitk_floats(int mode, int M, int N, int K, int ldo) {
   if (M <= 0 || N <= 0 || K <= 0) return 0;
   const Tiling tl = pick_tiling(M, N, K, mode, false);
-  return tl.splits > 1 ? static_cast<int64_t>(tl.splits) * M * ldo : 0;
+  return tl.splits > 1 ? static_cast<int64_t>(tl.splits) * M * std::max(ldo, N) : 0;
 }
 
 }  // namespace tps

@@ -205,6 +205,10 @@ struct tps_pipeline {
   double* bn_scr = nullptr;
   float* bn_colsum = nullptr;               // conv epilogue -> next BN: Σx, Σx² per 32-row group
   float* splitk_ws = nullptr;               // split-K partials of weight-gradient GEMMs
+  // split-K partials of tile-starved forward / input-gradient GEMMs (compute stream; its own
+  // buffer because the weight gradients run concurrently on the weight-gradient stream)
+  float* splitk_ws_fd = nullptr;
+  int64_t splitk_fd_floats = 0;
   int64_t splitk_floats = 0;
   std::vector<void*> allocs;
 
@@ -385,8 +389,10 @@ tps_status run_gemm(tps_pipeline* p, int mode, const tps::GemmOperands& op, cons
     CUDA_OK(cudaEventRecord(tl.a, gs));
   }
   tps::GemmArgs a2 = args;
-  a2.ws = p->splitk_ws;
-  a2.ws_floats = p->splitk_floats;
+  const bool fd = mode == tps::GEMM_FWD || mode == tps::GEMM_DGRAD || mode == tps::GEMM_CONV_FWD ||
+                  mode == tps::GEMM_CONV_DGRAD;
+  a2.ws = fd ? p->splitk_ws_fd : p->splitk_ws;
+  a2.ws_floats = fd ? p->splitk_fd_floats : p->splitk_floats;
   a2.tf32 = p->tf ? 1 : 0;
   CUDA_OK(tps::gemm_run(mode, op, a2, gs));
   p->launches += 1;
@@ -2071,6 +2077,28 @@ tps_status tps_pipeline_init(const tps_config* c, tps_pipeline** out) {
         any_unfused = true;
         const tps_status dw_st = alloc_t(p, &L.dW, static_cast<size_t>(L.Np) * L.Kp, &p->mem_optim);
         if (dw_st != TPS_OK) return cleanup(dw_st);
+      }
+    }
+    // forward / input-gradient split-K workspace (chain nets): the largest need over the
+    // forward group sizes and the collective input gradient of every weight layer
+    if (!p->graph && !p->tf) {
+      int64_t fdf = 0;
+      for (const Layer& L : p->layers) {
+        if (!L.has_w() || L.kind == TPS_LAYER_BN) continue;
+        const bool conv = L.kind == TPS_LAYER_CONV3X3 && !L.im2col;
+        const int hw = L.kind == TPS_LAYER_LINEAR ? 1 : L.hw_out;
+        const int fm = conv ? tps::GEMM_CONV_FWD : tps::GEMM_FWD;
+        for (int g = 1; g <= p->m; ++g)
+          fdf = std::max(fdf, tps::gemm_splitk_floats(fm, g * p->bsz * hw, L.Np, L.Kp, L.Np));
+        if (L.kind == TPS_LAYER_LINEAR)
+          fdf = std::max(fdf, tps::gemm_splitk_floats(tps::GEMM_DGRAD, p->B, L.Kp, L.Np, L.Kp));
+        else if (conv)
+          fdf = std::max(fdf, tps::gemm_splitk_floats(tps::GEMM_CONV_DGRAD, p->B * hw, L.Kp / 9, 9 * L.Np, L.Kp / 9));
+      }
+      if (fdf > 0) {
+        const tps_status fd_st = alloc_t(p, &p->splitk_ws_fd, fdf, &p->mem_optim);
+        if (fd_st != TPS_OK) return cleanup(fd_st);
+        p->splitk_fd_floats = fdf;
       }
     }
     if (!p->fuse_update || p->graph || any_unfused) {
