@@ -18,6 +18,8 @@
 #   resnet   ResNet GPU tests, C4 one-GPU numbers with the BN ReLU bit mask + specialised col2im
 #            on and off (A/B), and the ResNet-50 per-kernel launch list with DRAM bytes
 #   vgg      VGG-16 (C3, S = 1) per-kernel launch list with DRAM bytes (mid-run window)
+#   fdab     parity suites with the forward / input-gradient split-K on (TPS_SPLITK_FD=1) and
+#            C1-C3 one-GPU numbers with it on and off
 #   vggab    conv / VGG parity tests, C3 one-GPU numbers with the tile-starved weight gradients
 #            unfused (default) and fused (TPS_FUSE_ALL=1)
 # Every step runs under its own timeout so one hang cannot eat the box.
@@ -87,6 +89,16 @@ for s in $STEPS; do
         timeout 600 python tools/bench_configs.py --graph --only C3 --out ${O}_c3_new$rep.json > ${O}_c3_new$rep.log 2>&1
         TPS_FUSE_ALL=1 timeout 600 python tools/bench_configs.py --graph --only C3 --out ${O}_c3_old$rep.json \
           > ${O}_c3_old$rep.log 2>&1
+      done ;;
+    fdab)
+      TPS_SPLITK_FD=1 timeout 1500 python -m pytest tests/test_gpu_conv.py tests/test_gpu_pipeline.py \
+        tests/test_gpu_fused_update.py tests/test_gpu_stepwise.py tests/test_gpu_ipc.py tests/test_gpu_graph.py \
+        "tests/test_gpu_fullsize.py::test_c3_vgg16_four_stage" -q -m gpu --timeout=900 -p no:cacheprovider \
+        > ${O}_fd_tests.log 2>&1
+      for c in C2 C3; do
+        TPS_SPLITK_FD=1 timeout 900 python tools/bench_configs.py --graph --only $c --out ${O}_fd_on_$c.json \
+          > ${O}_fd_on_$c.log 2>&1
+        timeout 900 python tools/bench_configs.py --graph --only $c --out ${O}_fd_off_$c.json > ${O}_fd_off_$c.log 2>&1
       done ;;
     *) echo "unknown step $s" ;;
   esac
