@@ -1420,9 +1420,8 @@ __global__ void __launch_bounds__(256) im2col_rowtile_v(const uint16_t* __restri
   uint4* prow = P + (static_cast<int64_t>(n) * Ho + ho) * Wo * v8;
   if (staged) {
     // the block's patch rows assembled element by element in shared memory (consecutive threads
-    // read consecutive tile elements and write consecutive outputs: no bank conflicts), then
-    // streamed out as 16-byte stores.  Gathering 8 elements per thread at a 16-byte stride
-    // between neighbouring threads was a 4-way bank conflict and bounded the kernel.
+    // read consecutive tile elements and write consecutive outputs), then streamed out as
+    // 16-byte stores (opt-in: measured slower than the direct 8-element gather below)
     uint16_t* outs = reinterpret_cast<uint16_t*>(off + ldp);   // [Wo][ldp]
     for (int i = threadIdx.x; i < Wo * ldp; i += blockDim.x) {
       const int wo = i / ldp, col = i - wo * ldp;
@@ -1636,7 +1635,10 @@ cudaError_t launch_im2col(const uint16_t* X, uint16_t* P, int N, int H, int W, i
     const size_t smem_v = static_cast<size_t>(k) * rowlen * 2 + static_cast<size_t>(ldp) * 4;
     const size_t smem_s = smem_v + static_cast<size_t>(Wo) * ldp * 2;   // + the staged patch rows
     if (smem_v <= 48 * 1024) {
-      const int staged = smem_s <= 48 * 1024 ? 1 : 0;
+      // staging the patch rows through shared memory measured slower at the ResNet-50 stem
+      // (639 vs 549 us per launch): opt-in TPS_IM2COL_STAGED=1
+      static const bool want_staged = std::getenv("TPS_IM2COL_STAGED") && std::getenv("TPS_IM2COL_STAGED")[0] == '1';
+      const int staged = want_staged && smem_s <= 48 * 1024 ? 1 : 0;
       im2col_rowtile_v<<<static_cast<unsigned>(static_cast<int64_t>(N) * Ho), 256, staged ? smem_s : smem_v, st>>>(
           X, reinterpret_cast<uint4*>(P), H, W, C, k, s, p, Ho, Wo, ldp, D0, rowlen, staged);
       return cudaGetLastError();
