@@ -465,9 +465,11 @@ def main():
             per_kind[nm] = {"launches": n_k, "ms": round(ms_k, 3), "tflops": round(fl_k / (ms_k * 1e-3) / 1e12, 1)}
     n_u, ms_u, by_u = pI.kernel_stats(4)
     peaks_early, _ = load_peaks()
-    # dominant kernel: the fused wgrad + update (17 launches per mini-batch: 16 x 4096^2 + the head);
-    # algorithmic bytes per launch = G and X read once + 18 B/param (w, v read + write, bf16 version),
-    # averaged over the 17 launches like the measured duration
+    # dominant kernel: the fused wgrad + update (17 weight-gradient launches per mini-batch: 16 x
+    # 4096^2 fused, and the 16-row head, whose tiles cannot fill the GPU, as a split-K weight
+    # gradient with its update in a separate kernel -- its update bytes are < 0.5 % of the sum);
+    # algorithmic bytes per launch = G and X read once + 18 B/param (w, v read + write, bf16
+    # version), averaged over the 17 launches like the measured duration
     n_w, ms_w, fl_w = pI.kernel_stats(2)
     Bm = MICRO_B * MICRO_M
     dmod = [WIDTH] * (HIDDEN + 1) + [CLASSES]
